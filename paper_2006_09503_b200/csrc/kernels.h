@@ -1,0 +1,52 @@
+// Host-side launch interface of the sm_100a stage kernels.  Internal to
+// libp2bw.so: the engine (engine.cpp) and the C-ABI test hooks (capi.cpp)
+// call these; nothing outside the library sees them.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace p2bw {
+
+using bf16 = __nv_bfloat16;
+
+// Storage order of a GEMM operand relative to its (row, k) indexing.
+//   K  : element (r, k) at ptr[r * ld + k]   (k contiguous)
+//   MN : element (r, k) at ptr[k * ld + r]   (r contiguous)
+enum class Major : int { K = 0, MN = 1 };
+
+struct GemmOperand {
+    const bf16* ptr = nullptr;
+    int64_t ld = 0;
+    Major major = Major::K;
+};
+
+enum class EpiKind : int {
+    StoreBF16 = 0,  // D_bf16 = [gelu](alpha*acc + bias) [+ residual]; preact stored before gelu
+    StoreF32 = 1,   // D_f32 = beta*D_f32 + alpha*acc
+    DGeluBF16 = 2,  // D_bf16 = alpha*acc * gelu'(u)
+};
+
+struct GemmEpilogue {
+    EpiKind kind = EpiKind::StoreBF16;
+    void* d = nullptr;
+    int64_t ldd = 0;
+    const bf16* bias = nullptr;      // [N]
+    const bf16* residual = nullptr;  // [M x ldr]
+    int64_t ldr = 0;
+    bf16* preact = nullptr;          // [M x ldd] pre-GELU copy (StoreBF16 with gelu)
+    bool gelu = false;
+    const bf16* aux = nullptr;       // u for DGeluBF16, [M x ldd]
+    float alpha = 1.0f;
+    float beta = 0.0f;
+};
+
+// D[M x N] = A[M x K] . B[N x K]^T on tcgen05 (TMA -> SMEM -> UMMA -> TMEM -> epilogue).
+// Requirements: N % 32 == 0, leading dims multiple of 8 elements, 16-byte aligned pointers.
+void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
+               const GemmEpilogue& epi, cudaStream_t stream);
+
+int num_sms();
+
+}  // namespace p2bw

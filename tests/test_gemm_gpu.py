@@ -1,0 +1,97 @@
+"""Parity of the tcgen05 GEMM (p2bw_kernel_gemm_bf16) against a torch fp32
+reference of the same contraction, for every operand-major combination the
+stage executor uses (forward K/K, dgrad K/MN, wgrad MN/MN) and every epilogue.
+Reference ops replaced: matmul / matmul_tn / matmul_nt, semantics.cpp:9-44."""
+import ctypes as C
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2006_09503_b200._lib import GemmEpilogue, call  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _operand(rows, k, major, gen):
+    """Logical [rows x k] matrix stored K-major (rows x k) or MN-major (k x rows)."""
+    logical = torch.randn(rows, k, generator=gen, device="cuda").to(torch.bfloat16)
+    if major == 0:
+        store = logical.contiguous()
+        return logical, store, store.stride(0)
+    store = logical.t().contiguous()
+    return logical, store, store.stride(0)
+
+
+def _gemm(a, lda, am, b, ldb, bm, m, n, k, epi):
+    call("p2bw_kernel_gemm_bf16", C.c_void_p(a.data_ptr()), lda, am, C.c_void_p(b.data_ptr()), ldb,
+         bm, m, n, k, C.byref(epi), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+
+def gelu_tanh(x):
+    return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+@pytest.mark.parametrize("am,bm", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("m,n,k", [(256, 256, 128), (384, 768, 320), (200, 96, 64), (1024, 2304, 768)])
+def test_gemm_f32_store_matches_torch(am, bm, m, n, k):
+    gen = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k + am * 2 + bm)
+    A, a, lda = _operand(m, k, am, gen)
+    B, b, ldb = _operand(n, k, bm, gen)
+    d = torch.full((m, n), 7.0, device="cuda", dtype=torch.float32)
+    epi = GemmEpilogue(kind=1, d=d.data_ptr(), ldd=n, alpha=1.0, beta=0.0)
+    _gemm(a, lda, am, b, ldb, bm, m, n, k, epi)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    err = (d - ref).abs().max().item()
+    assert err <= 1e-3 * (1 + ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("am,bm", [(0, 0), (1, 1)])
+def test_gemm_f32_accumulate(am, bm):
+    m, n, k = 512, 512, 256
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    A, a, lda = _operand(m, k, am, gen)
+    B, b, ldb = _operand(n, k, bm, gen)
+    d0 = torch.randn(m, n, device="cuda", generator=gen)
+    d = d0.clone()
+    epi = GemmEpilogue(kind=1, d=d.data_ptr(), ldd=n, alpha=0.5, beta=1.0)
+    _gemm(a, lda, am, b, ldb, bm, m, n, k, epi)
+    torch.cuda.synchronize()
+    ref = d0 + 0.5 * (A.float() @ B.float().t())
+    assert (d - ref).abs().max().item() < 2e-3 * ref.abs().max().item()
+
+
+def test_gemm_bf16_bias_gelu_residual():
+    m, n, k = 640, 1024, 384
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    A, a, lda = _operand(m, k, 0, gen)
+    B, b, ldb = _operand(n, k, 0, gen)
+    bias = torch.randn(n, device="cuda", generator=gen).to(torch.bfloat16)
+    res = torch.randn(m, n, device="cuda", generator=gen).to(torch.bfloat16)
+    out = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    pre = torch.empty_like(out)
+    epi = GemmEpilogue(kind=0, d=out.data_ptr(), ldd=n, bias=bias.data_ptr(), residual=res.data_ptr(),
+                       ldr=n, preact=pre.data_ptr(), gelu=1, alpha=1.0)
+    _gemm(a, lda, 0, b, ldb, 0, m, n, k, epi)
+    torch.cuda.synchronize()
+    u = A.float() @ B.float().t() + bias.float()
+    assert (pre.float() - u).abs().max().item() < 0.05 * u.abs().max().item()
+    ref = gelu_tanh(pre.float()) + res.float()
+    assert (out.float() - ref).abs().max().item() < 0.02 * ref.abs().max().item()
+
+
+def test_gemm_dgelu_epilogue():
+    m, n, k = 256, 512, 256
+    gen = torch.Generator(device="cuda").manual_seed(13)
+    A, a, lda = _operand(m, k, 0, gen)
+    B, b, ldb = _operand(n, k, 1, gen)
+    u = torch.randn(m, n, device="cuda", generator=gen).to(torch.bfloat16)
+    out = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    epi = GemmEpilogue(kind=2, d=out.data_ptr(), ldd=n, aux=u.data_ptr(), alpha=1.0)
+    _gemm(a, lda, 0, b, ldb, 1, m, n, k, epi)
+    torch.cuda.synchronize()
+    uf = u.float().requires_grad_(True)
+    g = torch.autograd.grad(gelu_tanh(uf).sum(), uf)[0]
+    ref = (A.float() @ B.float().t()) * g
+    assert (out.float() - ref).abs().max().item() < 0.02 * ref.abs().max().item()
