@@ -62,12 +62,112 @@ enum {
 
 #define P2BW_LATEST_VERSION (-1) /* == pipesim::kLatestVersion (schedule.hpp:36) */
 
+/* Stage model families the executor can run. */
+enum {
+    P2BW_MODEL_LINEAR_F64 = 0,  /* the reference ToyModel (semantics.hpp:31-43), fp64, bit-exact */
+    P2BW_MODEL_TRANSFORMER = 1  /* pre-LN transformer blocks, bf16 tcgen05 kernels, fp32 master */
+};
+
 /* == pipesim::ScheduledOp (schedule.hpp:40-46). */
 typedef struct {
     int kind;
     int microbatch;
     int weight_version;
 } p2bw_op;
+
+/* ---- schedule: schedule.hpp:53-65 ------------------------------------------ */
+
+typedef struct p2bw_schedule p2bw_schedule; /* == std::vector<StageProgram> */
+
+/* weight_version_2bw (schedule.hpp:53-55 / schedule.cpp:58-62). */
+int p2bw_weight_version_2bw(int k, int m, int* out);
+/* required_versions (schedule.hpp:57-58). */
+int p2bw_required_versions(int policy, int d, int m, int* out);
+/* generate_schedule (schedule.hpp:60-61 / schedule.cpp:148-175). */
+int p2bw_schedule_generate(int policy, int d, int m, int num_batches, p2bw_schedule** out);
+/* parse_programs (schedule.hpp:64 / schedule.cpp:197-242). */
+int p2bw_schedule_parse(const char* text, p2bw_schedule** out);
+int p2bw_schedule_num_stages(const p2bw_schedule* sched, int* out);
+/* Borrowed view of one StageProgram's ops, valid until p2bw_schedule_destroy. */
+int p2bw_schedule_ops(const p2bw_schedule* sched, int stage, const p2bw_op** ops, size_t* n);
+/* serialize_programs (schedule.hpp:63 / schedule.cpp:177-195); free with p2bw_free. */
+int p2bw_schedule_serialize(const p2bw_schedule* sched, char** text);
+void p2bw_schedule_destroy(p2bw_schedule* sched);
+/* Policy names: to_string / parse_policy (schedule.hpp:18-19). */
+int p2bw_policy_name(int policy, const char** name);
+int p2bw_policy_parse(const char* name, int* policy);
+
+void p2bw_free(void* p);
+
+/* ---- planner and partition: planner.hpp:40-41, profile.hpp:76 ------------- */
+
+/* plan(load_model_profile(model_json), load_cluster_spec(cluster_json), B, policy)
+ * rendered by plan_to_json (planner.cpp:160-186) or plan_to_text (:139-158).
+ * JSON inputs use the reference's profile / cluster documents (profile.cpp:162-241). */
+int p2bw_plan(const char* model_json, const char* cluster_json, long long max_batch, int policy,
+              int as_text, char** out);
+/* partition_equal (profile.cpp:104-131) rendered as a JSON array of stages
+ * {fwd_time, bwd_time, weight_bytes, act_total_bytes, act_input_bytes,
+ *  act_output_bytes} in SI units (seconds, bytes), keys = microbatch sizes. */
+int p2bw_partition_equal(const char* model_json, int d, char** out_json);
+
+/* ---- the stage executor: pipelined_execute (semantics.hpp:73-74) ---------- */
+
+typedef struct p2bw_engine p2bw_engine;
+
+typedef struct {
+    int model_kind;      /* P2BW_MODEL_* */
+    int policy;          /* P2BW_POLICY_* */
+    int depth;           /* pipeline stages d (layers split by partition_equal) */
+    int width;           /* data-parallel replicas w (1 in this process) */
+    int microbatches;    /* m: microbatches per batch (TrainerConfig, semantics.hpp:45-52) */
+    int microbatch_size; /* b: columns (linear) or sequences (transformer) */
+    int layers;          /* blocks */
+    int dim;             /* linear chain width (ToyModel::dim) */
+    int hidden, heads, seq_len, vocab;
+    int causal;          /* 1: GPT decoder mask, 0: BERT encoder */
+    int head_rows;       /* LM-head rows per sequence (0: every position) */
+    double learning_rate;
+    double momentum;
+    unsigned long long seed;
+    const int* devices;  /* one CUDA device per stage, or NULL: all on the current device */
+} p2bw_desc;
+
+typedef struct {
+    int version_consistent; /* PipelinedResult::version_consistent */
+    int max_versions_held;  /* PipelinedResult::max_versions_held */
+    long long ops_executed;
+    double last_run_ms;     /* device time of the last run, max over stages (CUDA events) */
+} p2bw_counters;
+
+int p2bw_engine_create(const p2bw_desc* desc, p2bw_engine** out);
+void p2bw_engine_destroy(p2bw_engine* eng);
+/* Bytes of one stage's weights in the public layout (linear: fp64 column-major
+ * matrices of the stage's layers; transformer: fp32 flat parameter vector). */
+int p2bw_engine_stage_weight_bytes(p2bw_engine* eng, int stage, size_t* bytes);
+/* Initial weights (version 0) of one stage (host buffer, borrowed). */
+int p2bw_engine_load_stage_weights(p2bw_engine* eng, int stage, const void* host, size_t bytes);
+/* Deterministic initial weights from desc->seed (transformer). */
+int p2bw_engine_init_weights(p2bw_engine* eng);
+/* Microbatches [first_mb, first_mb+count), 1-based like ScheduledOp::microbatch.
+ * Linear: inputs/targets fp64 [count][dim*b] column-major (ToyModel::dataset).
+ * Transformer: int32 token ids / targets [count][b*seq_len]. */
+int p2bw_engine_set_data(p2bw_engine* eng, const void* inputs, const void* targets, int first_mb,
+                         int count);
+/* Interpret one program per stage (n_ops[s] ops at programs[s]).  Asynchronous. */
+int p2bw_engine_run(p2bw_engine* eng, const p2bw_op* const* programs, const size_t* n_ops,
+                    int snapshot_updates);
+/* generate_schedule(desc->policy, d, m, num_batches) followed by p2bw_engine_run. */
+int p2bw_engine_run_schedule(p2bw_engine* eng, int num_batches, int snapshot_updates);
+int p2bw_engine_sync(p2bw_engine* eng);
+int p2bw_engine_counters(p2bw_engine* eng, p2bw_counters* out);
+/* Weights created by a stage's update_index-th update of the last run (snapshots on). */
+int p2bw_engine_read_snapshot(p2bw_engine* eng, int stage, int update_index, void* host,
+                              size_t bytes);
+/* A live weight version of a stage (at most 2 under 2BW). */
+int p2bw_engine_read_version(p2bw_engine* eng, int stage, int version, void* host, size_t bytes);
+/* Training losses of microbatches [first_mb, first_mb+count) (last stage). */
+int p2bw_engine_losses(p2bw_engine* eng, int first_mb, int count, double* out);
 
 /* ---- stage kernels (parity-test hooks; device pointers, CUDA stream) ------- */
 

@@ -23,8 +23,12 @@ LIB = PKG / "libp2bw.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-          f"-I{CSRC}", f"-I{INCLUDE}"]
+# nlohmann/json (header-only, the JSON library the reference's profile I/O uses)
+JSON_INC = os.environ.get(
+    "P2BW_JSON_INCLUDE",
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty")
+COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+          f"-I{CSRC}", f"-I{INCLUDE}", f"-I{JSON_INC}"]
 
 
 def _sources() -> list[Path]:

@@ -1,0 +1,186 @@
+// C-ABI over the stage executor (include/p2bw.h, "the stage executor").
+#include <algorithm>
+#include <cstring>
+#include <memory>
+
+#include "capi_internal.h"
+#include "engine.h"
+#include "p2bw.h"
+#include "pipesim/schedule.hpp"
+
+struct p2bw_engine {
+    std::unique_ptr<p2bw::Engine> impl;
+};
+
+using p2bw::guarded;
+
+namespace {
+
+p2bw::Engine& eng_of(p2bw_engine* e) {
+    if (e == nullptr || !e->impl) throw std::invalid_argument("engine is NULL");
+    return *e->impl;
+}
+
+void check_stage(p2bw::Engine& e, int stage) {
+    if (stage < 0 || stage >= e.depth()) throw std::invalid_argument("stage out of range");
+}
+
+}  // namespace
+
+extern "C" {
+
+int p2bw_engine_create(const p2bw_desc* d, p2bw_engine** out) {
+    return guarded([&] {
+        if (d == nullptr || out == nullptr) throw std::invalid_argument("NULL argument");
+        if (d->width != 1 && d->width != 0)
+            throw p2bw::Error("width > 1 runs one replica per process (see DESIGN.md); "
+                              "this engine instance drives a single pipeline");
+        p2bw::EngineConfig c;
+        c.model_kind = d->model_kind;
+        c.policy = d->policy;
+        c.depth = d->depth;
+        c.microbatches = d->microbatches;
+        c.microbatch_size = d->microbatch_size;
+        c.layers = d->layers;
+        c.dim = d->dim;
+        c.hidden = d->hidden;
+        c.heads = d->heads;
+        c.seq_len = d->seq_len;
+        c.vocab = d->vocab;
+        c.causal = d->causal;
+        c.head_rows = d->head_rows;
+        c.lr = d->learning_rate;
+        c.momentum = d->momentum;
+        c.seed = d->seed;
+        if (d->devices != nullptr) c.devices.assign(d->devices, d->devices + d->depth);
+        if (c.lr < 0) throw p2bw::Error("learning rate must be >= 0");
+        if (c.momentum < 0 || c.momentum >= 1) throw p2bw::Error("momentum must be in [0, 1)");
+        auto e = std::make_unique<p2bw_engine>();
+        e->impl = std::make_unique<p2bw::Engine>(c);
+        *out = e.release();
+    });
+}
+
+void p2bw_engine_destroy(p2bw_engine* eng) { delete eng; }
+
+int p2bw_engine_stage_weight_bytes(p2bw_engine* eng, int stage, size_t* bytes) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (bytes == nullptr) throw std::invalid_argument("bytes is NULL");
+        *bytes = e.model(stage).weight_bytes_public();
+    });
+}
+
+int p2bw_engine_load_stage_weights(p2bw_engine* eng, int stage, const void* host, size_t bytes) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (host == nullptr) throw std::invalid_argument("host buffer is NULL");
+        e.model(stage).load_weights(0, host, bytes);
+    });
+}
+
+int p2bw_engine_init_weights(p2bw_engine* eng) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        for (int s = 0; s < e.depth(); ++s) e.model(s).init_weights(e.config().seed);
+    });
+}
+
+int p2bw_engine_set_data(p2bw_engine* eng, const void* inputs, const void* targets, int first_mb,
+                         int count) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        if (first_mb < 1) throw std::invalid_argument("microbatch ids are 1-based");
+        // Inputs feed stage 0, targets the last stage (they may be the same stage).
+        e.model(0).set_data(inputs, e.depth() == 1 ? targets : nullptr, first_mb, count);
+        if (e.depth() > 1) e.model(e.depth() - 1).set_data(nullptr, targets, first_mb, count);
+    });
+}
+
+int p2bw_engine_run(p2bw_engine* eng, const p2bw_op* const* programs, const size_t* n_ops,
+                    int snapshot_updates) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        if (programs == nullptr || n_ops == nullptr) throw std::invalid_argument("NULL programs");
+        std::vector<p2bw::Program> progs(static_cast<size_t>(e.depth()));
+        for (int s = 0; s < e.depth(); ++s) {
+            for (size_t i = 0; i < n_ops[s]; ++i) {
+                const p2bw_op& op = programs[s][i];
+                progs[s].push_back({op.kind, op.microbatch, op.weight_version});
+            }
+        }
+        e.set_snapshot_every_update(snapshot_updates != 0);
+        e.run(progs);
+    });
+}
+
+int p2bw_engine_run_schedule(p2bw_engine* eng, int num_batches, int snapshot_updates) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        const auto& c = e.config();
+        const auto programs = pipesim::generate_schedule(
+            static_cast<pipesim::PipelinePolicy>(c.policy), c.depth, c.microbatches, num_batches);
+        std::vector<p2bw::Program> progs;
+        for (const auto& p : programs) {
+            p2bw::Program prog;
+            for (const auto& op : p.ops)
+                prog.push_back({static_cast<int>(op.kind), op.microbatch, op.weight_version});
+            progs.push_back(std::move(prog));
+        }
+        e.set_snapshot_every_update(snapshot_updates != 0);
+        e.run(progs);
+    });
+}
+
+int p2bw_engine_sync(p2bw_engine* eng) {
+    return guarded([&] { eng_of(eng).sync(); });
+}
+
+int p2bw_engine_counters(p2bw_engine* eng, p2bw_counters* out) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        if (out == nullptr) throw std::invalid_argument("out is NULL");
+        out->version_consistent = e.stats().version_consistent ? 1 : 0;
+        out->max_versions_held = e.stats().max_versions_held;
+        out->ops_executed = e.stats().ops_executed;
+        out->last_run_ms = e.elapsed_ms_last_run();
+    });
+}
+
+int p2bw_engine_read_snapshot(p2bw_engine* eng, int stage, int update_index, void* host,
+                              size_t bytes) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        e.sync();
+        const auto& snaps = e.snapshots(stage);
+        if (update_index < 1 || update_index > static_cast<int>(snaps.size()))
+            throw p2bw::Error("no snapshot for update " + std::to_string(update_index));
+        const auto& buf = snaps[static_cast<size_t>(update_index - 1)];
+        if (bytes != buf.size()) throw std::invalid_argument("snapshot size mismatch");
+        std::memcpy(host, buf.data(), bytes);
+    });
+}
+
+int p2bw_engine_read_version(p2bw_engine* eng, int stage, int version, void* host, size_t bytes) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        e.sync();
+        e.read_version(stage, version, host, bytes);
+    });
+}
+
+int p2bw_engine_losses(p2bw_engine* eng, int first_mb, int count, double* out) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        if (out == nullptr || count < 0) throw std::invalid_argument("bad loss buffer");
+        e.sync();
+        const auto l = e.losses(first_mb, count);
+        std::copy(l.begin(), l.end(), out);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,404 @@
+// Stage executor: interprets the per-stage op programs on CUDA streams.
+//
+// Mirrors reference pipelined_execute (core/src/semantics.cpp:238-375):
+//   - the same round-robin "run each stage until blocked" issue order (:270-361),
+//     except that "blocked" means "the producing op has not been *issued* yet":
+//     ordering on the GPU is carried by CUDA events, so the host never waits;
+//   - the same version bookkeeping (versions map, prune rules :213-234, the
+//     "needs discarded weight version" check :282-287, max_versions_held);
+//   - the same deadlock detection and error text (:360).
+// Buffers: every stage owns a receive ring for its input activations (which is
+// also the stash of its first-layer input) and one for its output gradient.
+// The producing stage's last kernel writes straight into those slots, so a
+// stage hand-off is a peer store over NVLink when stages sit on different GPUs.
+#include "engine.h"
+
+#include <algorithm>
+#include <cstring>
+
+namespace p2bw {
+
+namespace {
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        check_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+int weight_slots_for(int policy, int depth) {
+    switch (policy) {
+        case P2BW_POLICY_2BW: return 2;          // exactly two versions (paper §3.1)
+        case P2BW_POLICY_1F1B: return depth + 1; // weight stashing worst case + the new one
+        default: return 1;                       // flush policies update in place
+    }
+}
+
+}  // namespace
+
+Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
+    if (cfg_.depth < 1) throw Error("depth must be >= 1");
+    if (cfg_.layers < 1) throw Error("layer count must be >= 1");
+    if (cfg_.layers % cfg_.depth != 0)
+        throw Error("block count " + std::to_string(cfg_.layers) + " not divisible by depth " +
+                    std::to_string(cfg_.depth));
+    if (cfg_.microbatches < 1) throw Error("m must be >= 1");
+    if (cfg_.policy == P2BW_POLICY_2BW && cfg_.microbatches < cfg_.depth)
+        throw Error("2bw requires m >= d (m=" + std::to_string(cfg_.microbatches) +
+                    ", d=" + std::to_string(cfg_.depth) + ")");
+    if (cfg_.devices.empty()) {
+        int dev = 0;
+        check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+        cfg_.devices.assign(static_cast<size_t>(cfg_.depth), dev);
+    }
+    if (static_cast<int>(cfg_.devices.size()) != cfg_.depth)
+        throw Error("device list must have one entry per stage");
+
+    // Peer access between devices of adjacent stages (NVLink / NVSwitch).
+    for (int s = 0; s + 1 < cfg_.depth; ++s) {
+        const int a = cfg_.devices[s], b = cfg_.devices[s + 1];
+        if (a == b) continue;
+        for (auto [x, y] : {std::pair{a, b}, std::pair{b, a}}) {
+            DeviceGuard g(x);
+            int can = 0;
+            check_cuda(cudaDeviceCanAccessPeer(&can, x, y), "cudaDeviceCanAccessPeer");
+            if (!can) throw Error("no peer access between GPU " + std::to_string(x) + " and " +
+                                  std::to_string(y));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(y, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                check_cuda(e, "cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+        }
+    }
+
+    // Ring sizes come from the policy's programs: the peak in-flight count of a
+    // stage bounds its stash; one extra input slot lets the upstream stage run
+    // its next forward without waiting for this stage's oldest backward.
+    const int per = cfg_.layers / cfg_.depth;
+    stages_.resize(static_cast<size_t>(cfg_.depth));
+    try {
+        for (int s = 0; s < cfg_.depth; ++s) {
+            Stage& st = stages_[s];
+            st.index = s;
+            st.device = cfg_.devices[s];
+            st.lo = s * per;
+            st.hi = st.lo + per;
+            const int warm = std::min(cfg_.depth - s, cfg_.microbatches);
+            int inflight;
+            switch (cfg_.policy) {
+                case P2BW_POLICY_GPIPE: inflight = cfg_.microbatches; break;
+                case P2BW_POLICY_NONE: inflight = 1; break;
+                default: inflight = std::max(warm, 1); break;
+            }
+            st.stash_slots = inflight + (s > 0 ? 1 : 0);
+            st.grad_slots = st.stash_slots;
+            st.weight_slots = weight_slots_for(cfg_.policy, cfg_.depth);
+            DeviceGuard g(st.device);
+            check_cuda(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking),
+                       "cudaStreamCreate");
+            check_cuda(cudaEventCreate(&st.t0), "cudaEventCreate");
+            check_cuda(cudaEventCreate(&st.t1), "cudaEventCreate");
+            if (cfg_.model_kind == P2BW_MODEL_LINEAR_F64) {
+                st.model = make_linear_f64_stage(cfg_, s, st.lo, st.hi, st.stash_slots,
+                                                 st.weight_slots);
+            } else if (cfg_.model_kind == P2BW_MODEL_TRANSFORMER) {
+                st.model = make_transformer_stage(cfg_, s, st.lo, st.hi, st.stash_slots,
+                                                  st.weight_slots);
+            } else {
+                throw Error("unknown model kind " + std::to_string(cfg_.model_kind));
+            }
+            const size_t nb = st.model->boundary_bytes();
+            if (s > 0) {
+                st.act_ring.assign(static_cast<size_t>(st.stash_slots), nullptr);
+                for (auto& p : st.act_ring) check_cuda(cudaMalloc(&p, nb), "cudaMalloc(act ring)");
+            }
+            if (s + 1 < cfg_.depth) {
+                st.grad_ring.assign(static_cast<size_t>(st.grad_slots), nullptr);
+                for (auto& p : st.grad_ring)
+                    check_cuda(cudaMalloc(&p, nb), "cudaMalloc(grad ring)");
+            }
+            st.version_slot[0] = 0;
+        }
+    } catch (...) {
+        free_buffers();
+        throw;
+    }
+}
+
+Engine::~Engine() { free_buffers(); }
+
+void Engine::free_buffers() {
+    for (Stage& st : stages_) {
+        DeviceGuard g(st.device);
+        if (st.stream) cudaStreamSynchronize(st.stream);
+        for (void* p : st.act_ring) cudaFree(p);
+        for (void* p : st.grad_ring) cudaFree(p);
+        st.act_ring.clear();
+        st.grad_ring.clear();
+        st.model.reset();
+        if (st.t0) cudaEventDestroy(st.t0);
+        if (st.t1) cudaEventDestroy(st.t1);
+        if (st.stream) cudaStreamDestroy(st.stream);
+        st.stream = nullptr;
+        st.t0 = st.t1 = nullptr;
+    }
+}
+
+namespace {
+
+// Per-run event tables: one event per (stage, microbatch, pass), created lazily
+// when the op is issued.  Destroying an event with pending waits is legal.
+struct EventTable {
+    std::vector<std::map<int, cudaEvent_t>> fwd, bwd;
+    explicit EventTable(size_t d) : fwd(d), bwd(d) {}
+    ~EventTable() {
+        for (auto& m : fwd)
+            for (auto& kv : m) cudaEventDestroy(kv.second);
+        for (auto& m : bwd)
+            for (auto& kv : m) cudaEventDestroy(kv.second);
+    }
+};
+
+thread_local EventTable* g_events = nullptr;
+
+cudaEvent_t record(std::map<int, cudaEvent_t>& tab, int k, cudaStream_t s) {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    check_cuda(cudaEventRecord(e, s), "cudaEventRecord");
+    tab[k] = e;
+    return e;
+}
+
+void wait_on(const std::map<int, cudaEvent_t>& tab, int k, cudaStream_t s) {
+    const auto it = tab.find(k);
+    if (it == tab.end()) throw Error("internal: missing event for microbatch " + std::to_string(k));
+    check_cuda(cudaStreamWaitEvent(s, it->second, 0), "cudaStreamWaitEvent");
+}
+
+}  // namespace
+
+int Engine::resolve_version(const Stage& st, const OpRec& op) const {
+    return op.weight_version == P2BW_LATEST_VERSION ? st.updates_done : op.weight_version;
+}
+
+bool Engine::ready(const Stage& st, const OpRec& op) const {
+    const int s = st.index, d = cfg_.depth, k = op.microbatch;
+    auto issued = [](const std::map<int, bool>& m, int key) { return key < 1 || m.count(key); };
+    if (op.kind == P2BW_OP_FORWARD) {
+        if (s > 0 && !issued(stages_[s - 1].fwd_issued, k)) return false;  // semantics.cpp:279
+        if (!issued(st.bwd_issued, k - st.stash_slots)) return false;      // own stash slot
+        if (s + 1 < d && !issued(stages_[s + 1].bwd_issued, k - stages_[s + 1].stash_slots))
+            return false;  // next stage's receive slot
+        return true;
+    }
+    if (op.kind == P2BW_OP_BACKWARD) {
+        if (s + 1 < d && !issued(stages_[s + 1].bwd_issued, k)) return false;  // :301
+        if (s > 0 && !issued(stages_[s - 1].bwd_issued, k - stages_[s - 1].grad_slots))
+            return false;  // previous stage's gradient slot
+        return true;
+    }
+    return true;
+}
+
+void Engine::issue_forward(Stage& st, const OpRec& op) {
+    const int s = st.index, d = cfg_.depth, k = op.microbatch;
+    const int v = resolve_version(st, op);
+    const auto vit = st.version_slot.find(v);
+    if (vit == st.version_slot.end())
+        throw Error("stage " + std::to_string(s) + " forward of microbatch " + std::to_string(k) +
+                    " needs discarded weight version " + std::to_string(v));
+    if (k < 1) throw Error("forward of microbatch " + std::to_string(k));
+    const int sslot = (k - 1) % st.stash_slots;
+    if (s > 0) wait_on(g_events->fwd[s - 1], k, st.stream);
+    void* x_out = nullptr;
+    if (s + 1 < d) {
+        const Stage& nx = stages_[s + 1];
+        if (k > nx.stash_slots) wait_on(g_events->bwd[s + 1], k - nx.stash_slots, st.stream);
+        x_out = nx.act_ring[(k - 1) % nx.stash_slots];
+    }
+    const void* x_in = s > 0 ? st.act_ring[sslot] : nullptr;
+    st.model->forward(k, vit->second, sslot, x_in, x_out, st.stream);
+    record(g_events->fwd[s], k, st.stream);
+    st.stash_version[k] = v;
+    st.fwd_issued[k] = true;
+}
+
+void Engine::issue_backward(Stage& st, const OpRec& op) {
+    const int s = st.index, d = cfg_.depth, k = op.microbatch;
+    const auto sit = st.stash_version.find(k);
+    if (sit == st.stash_version.end())
+        throw Error("backward before forward for microbatch " + std::to_string(k));  // :304
+    const int v = sit->second;
+    if (op.weight_version != P2BW_LATEST_VERSION && op.weight_version != v)
+        stats_.version_consistent = false;
+    const int wslot = st.version_slot.at(v);
+    const int sslot = (k - 1) % st.stash_slots;
+    const void* g_in = nullptr;
+    if (s + 1 < d) {
+        wait_on(g_events->bwd[s + 1], k, st.stream);
+        g_in = st.grad_ring[(k - 1) % st.grad_slots];
+    }
+    void* g_out = nullptr;
+    if (s > 0) {
+        const Stage& pv = stages_[s - 1];
+        if (k > pv.grad_slots) wait_on(g_events->bwd[s - 1], k - pv.grad_slots, st.stream);
+        g_out = pv.grad_ring[(k - 1) % pv.grad_slots];
+    }
+    st.model->backward(k, wslot, sslot, g_in, g_out, st.grad_count == 0, st.stream);
+    record(g_events->bwd[s], k, st.stream);
+    st.grad_count += 1;
+    st.stash_version.erase(sit);
+    st.bwd_issued[k] = true;
+}
+
+// semantics.cpp:213-234, applied to a version set.
+void Engine::prune_versions(Stage& st) {
+    const int latest = st.updates_done;
+    auto& vs = st.version_slot;
+    if (cfg_.policy == P2BW_POLICY_2BW) {
+        vs.erase(latest - 2);
+        return;
+    }
+    if (cfg_.policy == P2BW_POLICY_1F1B) {
+        for (auto it = vs.begin(); it != vs.end();) {
+            bool referenced = it->first == latest;
+            for (const auto& kv : st.stash_version) referenced = referenced || kv.second == it->first;
+            it = referenced ? std::next(it) : vs.erase(it);
+        }
+        return;
+    }
+    for (auto it = vs.begin(); it != vs.end();) it = it->first == latest ? std::next(it) : vs.erase(it);
+}
+
+// WeightUpdate (semantics.cpp:335-350): new version u+1 from the latest u.
+void Engine::issue_update(Stage& st) {
+    if (st.grad_count == 0) throw Error("weight update with no gradients");
+    const int src_version = st.updates_done;
+    const int src_slot = st.version_slot.at(src_version);
+    // Which versions survive once u+1 exists?  Its buffer may be any slot not
+    // holding one of them (the source slot itself when the source is dropped).
+    Stage probe_state;  // only the bookkeeping fields are used
+    probe_state.updates_done = src_version + 1;
+    probe_state.version_slot = st.version_slot;
+    probe_state.version_slot[src_version + 1] = -1;
+    probe_state.stash_version = st.stash_version;
+    prune_versions(probe_state);
+    std::vector<bool> used(static_cast<size_t>(st.weight_slots), false);
+    for (const auto& kv : probe_state.version_slot)
+        if (kv.first != src_version + 1) used[static_cast<size_t>(kv.second)] = true;
+    int dst_slot = -1;
+    if (!used[static_cast<size_t>(src_slot)] && !probe_state.version_slot.count(src_version))
+        dst_slot = src_slot;
+    for (int i = 0; i < st.weight_slots && dst_slot < 0; ++i)
+        if (!used[static_cast<size_t>(i)]) dst_slot = i;
+    if (dst_slot < 0)
+        throw Error("stage " + std::to_string(st.index) + ": no free weight buffer for version " +
+                    std::to_string(src_version + 1));
+    st.model->update(src_slot, dst_slot, st.grad_count, st.stream);
+    st.updates_done += 1;
+    st.version_slot[st.updates_done] = dst_slot;
+    prune_versions(st);
+    st.grad_count = 0;
+    stats_.max_versions_held =
+        std::max(stats_.max_versions_held, static_cast<int>(st.version_slot.size()));
+    if (snapshots_on_) {
+        std::vector<uint8_t> buf(st.model->weight_bytes_public());
+        st.model->read_weights(dst_slot, buf.data(), buf.size(), st.stream);
+        st.snaps.push_back(std::move(buf));
+    }
+}
+
+void Engine::run(const std::vector<Program>& programs) {
+    if (static_cast<int>(programs.size()) != cfg_.depth)
+        throw Error("expected one program per stage");
+    EventTable events(stages_.size());
+    g_events = &events;
+    struct Reset {
+        ~Reset() { g_events = nullptr; }
+    } reset;
+    size_t total = 0;
+    for (Stage& st : stages_) {
+        st.ptr = 0;
+        st.fwd_issued.clear();
+        st.bwd_issued.clear();
+        st.snaps.clear();
+        DeviceGuard g(st.device);
+        check_cuda(cudaEventRecord(st.t0, st.stream), "cudaEventRecord");
+    }
+    for (const Program& p : programs) total += p.size();
+    size_t done = 0;
+    while (done < total) {
+        bool progress = false;
+        for (Stage& st : stages_) {
+            const Program& prog = programs[static_cast<size_t>(st.index)];
+            DeviceGuard g(st.device);
+            while (st.ptr < prog.size()) {
+                const OpRec& op = prog[st.ptr];
+                if (!ready(st, op)) break;
+                switch (op.kind) {
+                    case P2BW_OP_FORWARD: issue_forward(st, op); break;
+                    case P2BW_OP_BACKWARD: issue_backward(st, op); break;
+                    case P2BW_OP_UPDATE: issue_update(st); break;
+                    case P2BW_OP_ALLREDUCE:  // w == 1: nothing to reduce (semantics.cpp:351-354)
+                    case P2BW_OP_FLUSH:      // ordering is already implied by stream order
+                        break;
+                    default:
+                        throw Error("op kind " + std::to_string(op.kind) +
+                                    " is not executable by the stage executor");
+                }
+                st.ptr += 1;
+                done += 1;
+                stats_.ops_executed += 1;
+                progress = true;
+            }
+        }
+        if (!progress) throw Error("dependency deadlock in toy-model replay");
+    }
+    for (Stage& st : stages_) {
+        DeviceGuard g(st.device);
+        check_cuda(cudaEventRecord(st.t1, st.stream), "cudaEventRecord");
+    }
+}
+
+void Engine::sync() {
+    for (Stage& st : stages_) {
+        DeviceGuard g(st.device);
+        check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
+    }
+}
+
+double Engine::elapsed_ms_last_run() {
+    sync();
+    double worst = 0.0;
+    for (Stage& st : stages_) {
+        float ms = 0.0f;
+        check_cuda(cudaEventElapsedTime(&ms, st.t0, st.t1), "cudaEventElapsedTime");
+        worst = std::max(worst, static_cast<double>(ms));
+    }
+    return worst;
+}
+
+std::vector<double> Engine::losses(int first_mb, int count) {
+    Stage& st = stages_.back();
+    std::vector<double> out(static_cast<size_t>(count));
+    DeviceGuard g(st.device);
+    st.model->read_losses(out.data(), first_mb, count, st.stream);
+    check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
+    return out;
+}
+
+void Engine::read_version(int s, int version, void* host, size_t bytes) {
+    Stage& st = stages_.at(static_cast<size_t>(s));
+    const auto it = st.version_slot.find(version);
+    if (it == st.version_slot.end())
+        throw Error("stage " + std::to_string(s) + " no longer holds weight version " +
+                    std::to_string(version));
+    DeviceGuard g(st.device);
+    st.model->read_weights(it->second, host, bytes, st.stream);
+    check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
+}
+
+}  // namespace p2bw

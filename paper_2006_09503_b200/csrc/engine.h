@@ -1,0 +1,157 @@
+// The B200 stage executor: the third interpreter of pipesim's op stream
+// (reference interpreters: semantics.cpp:270-361 numerically, simulator.cpp:195-290
+// for timing).  One CUDA stream per pipeline stage; cross-stage hand-offs are
+// producer kernels writing straight into the consumer stage's receive ring
+// (same device or an NVLink peer), ordered by CUDA events.  The host issues
+// every op asynchronously in the reference's round-robin order; nothing blocks
+// on the GPU inside run().
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "p2bw.h"
+#include "util.h"
+
+namespace p2bw {
+
+struct OpRec {
+    int kind = 0;
+    int microbatch = 0;
+    int weight_version = 0;
+};
+using Program = std::vector<OpRec>;
+
+struct EngineConfig {
+    int model_kind = P2BW_MODEL_LINEAR_F64;
+    int policy = P2BW_POLICY_2BW;
+    int depth = 1;
+    int microbatches = 1;     // m
+    int microbatch_size = 1;  // b (columns / sequences)
+    // linear chain
+    int dim = 0;
+    // shared
+    int layers = 0;
+    // transformer
+    int hidden = 0, heads = 0, seq_len = 0, vocab = 0, causal = 0, head_rows = 0;
+    double lr = 0.0, momentum = 0.0;
+    uint64_t seed = 0;
+    std::vector<int> devices;  // per stage
+};
+
+// One pipeline stage's model slice: parameters, version buffers, stash and the
+// kernels of the Forward / Backward / WeightUpdate ops.
+class StageModel {
+public:
+    virtual ~StageModel() = default;
+    virtual size_t num_params() const = 0;
+    // Elements of the boundary tensor handed to the next stage (and of its gradient).
+    virtual size_t boundary_bytes() const = 0;
+    // Forward of microbatch k on weight slot `wslot`, stash slot `sslot`.
+    //   x_in : this stage's input (receive-ring slot), nullptr on stage 0 (data)
+    //   x_out: next stage's receive-ring slot, nullptr on the last stage
+    virtual void forward(int k, int wslot, int sslot, const void* x_in, void* x_out,
+                         cudaStream_t s) = 0;
+    //   g_in : gradient of this stage's output, nullptr on the last stage (loss)
+    //   g_out: previous stage's gradient ring slot, nullptr on stage 0
+    //   first: first backward since the last update (gradient buffer is overwritten)
+    virtual void backward(int k, int wslot, int sslot, const void* g_in, void* g_out,
+                          bool first, cudaStream_t s) = 0;
+    // Fused optimizer: new version into dst_slot from src_slot (may alias).
+    virtual void update(int src_slot, int dst_slot, int grad_count, cudaStream_t s) = 0;
+    // Host <-> device weights of one version slot, in the model's public layout.
+    virtual void load_weights(int wslot, const void* host, size_t bytes) = 0;
+    virtual void read_weights(int wslot, void* host, size_t bytes, cudaStream_t s) = 0;
+    virtual size_t weight_bytes_public() const = 0;
+    // Per-microbatch training loss (last stage only), indexed like the data ring.
+    virtual void read_losses(double* host, int first_mb, int count, cudaStream_t s) {
+        (void)host, (void)first_mb, (void)count, (void)s;
+        throw Error("this stage computes no loss");
+    }
+    // Deterministic synthetic initial weights (version 0) from a seed.
+    virtual void init_weights(uint64_t seed) {
+        (void)seed;
+        throw Error("this model takes its initial weights from the caller");
+    }
+    virtual void set_data(const void* inputs, const void* targets, int first_mb, int count) = 0;
+    virtual int data_capacity() const = 0;
+};
+
+std::unique_ptr<StageModel> make_linear_f64_stage(const EngineConfig& cfg, int stage, int lo,
+                                                   int hi, int stash_slots, int weight_slots);
+std::unique_ptr<StageModel> make_transformer_stage(const EngineConfig& cfg, int stage, int lo,
+                                                    int hi, int stash_slots, int weight_slots);
+
+struct RunStats {
+    bool version_consistent = true;
+    int max_versions_held = 1;
+    long long ops_executed = 0;
+};
+
+class Engine {
+public:
+    explicit Engine(const EngineConfig& cfg);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    const EngineConfig& config() const { return cfg_; }
+    int depth() const { return cfg_.depth; }
+    StageModel& model(int s) { return *stages_.at(s).model; }
+
+    // Interpret one program per stage (asynchronous; call sync() to wait).
+    void run(const std::vector<Program>& programs);
+    void sync();
+    // Weights of stage s for the version created by its u-th update (0 = initial).
+    void read_version(int s, int version, void* host, size_t bytes);
+    void set_snapshot_every_update(bool on) { snapshots_on_ = on; }
+    const std::vector<std::vector<uint8_t>>& snapshots(int s) const { return stages_.at(s).snaps; }
+    const RunStats& stats() const { return stats_; }
+    double elapsed_ms_last_run();
+    // Losses of microbatches [first_mb, first_mb + count) (last stage), after sync.
+    std::vector<double> losses(int first_mb, int count);
+
+private:
+    struct Stage {
+        int index = 0;
+        int device = 0;
+        int lo = 0, hi = 0;
+        cudaStream_t stream = nullptr;
+        std::unique_ptr<StageModel> model;
+        int stash_slots = 1;
+        int grad_slots = 1;
+        int weight_slots = 1;
+        // receive rings owned by this stage (written by the neighbours)
+        std::vector<void*> act_ring;   // [stash_slots] boundary tensors (stage input)
+        std::vector<void*> grad_ring;  // [grad_slots] gradient of this stage's output
+        // host-side interpreter state (mirrors semantics.cpp:198-211)
+        size_t ptr = 0;
+        int updates_done = 0;
+        std::map<int, int> version_slot;  // live version -> weight slot
+        std::map<int, int> stash_version; // in-flight microbatch -> version
+        int grad_count = 0;
+        std::map<int, bool> fwd_issued, bwd_issued;
+        std::vector<std::vector<uint8_t>> snaps;  // snapshot per update (optional)
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+    };
+
+    void issue_forward(Stage& st, const OpRec& op);
+    void issue_backward(Stage& st, const OpRec& op);
+    void issue_update(Stage& st);
+    bool ready(const Stage& st, const OpRec& op) const;
+    int resolve_version(const Stage& st, const OpRec& op) const;
+    void prune_versions(Stage& st);
+    void free_buffers();
+
+    EngineConfig cfg_;
+    std::vector<Stage> stages_;
+    RunStats stats_;
+    bool snapshots_on_ = false;
+};
+
+}  // namespace p2bw

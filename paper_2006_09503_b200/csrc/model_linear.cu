@@ -1,0 +1,243 @@
+// Linear-chain stage (the reference ToyModel, semantics.hpp:31-43) in fp64 on
+// the GPU.  This is the engine's reference-pinned numeric mode: each output
+// element is produced by one thread that accumulates in the reference's loop
+// order with explicitly rounded (__dmul_rn / __dadd_rn, no FMA contraction)
+// operations, so trajectories are bit-identical to pipesim::pipelined_execute.
+//   matmul     semantics.cpp:9-19   Y(i,j)  = sum_k W(i,k) X(k,j)     (k ascending)
+//   matmul_tn  semantics.cpp:21-32  G'(i,j) = sum_k W(k,i) G(k,j)
+//   matmul_nt  semantics.cpp:34-44  T(i,j)  = sum_c G(i,c) X(j,c); grad += T (axpy :329)
+//   loss grad  semantics.cpp:314-319  g = (out - y) / b
+//   update     semantics.cpp:153-165, 335-350
+// Layout: column-major dim x cols, exactly the reference Mat (semantics.hpp:12-21).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "engine.h"
+
+namespace p2bw {
+namespace {
+
+constexpr int kThreads = 256;
+
+int blocks_for(long n) { return static_cast<int>(std::min<long>((n + kThreads - 1) / kThreads, 65535L * 8)); }
+
+// Y = W X  (W: n x n, X: n x c)
+__global__ void k_matmul_nn(const double* __restrict__ w, const double* __restrict__ x,
+                            double* __restrict__ y, int n, int c) {
+    const long total = static_cast<long>(n) * c;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+        double acc = 0.0;
+        for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, __dmul_rn(w[static_cast<long>(k) * n + i], x[static_cast<long>(j) * n + k]));
+        y[idx] = acc;
+    }
+}
+
+// Y = W^T G  (W: n x n, G: n x c)
+__global__ void k_matmul_tn(const double* __restrict__ w, const double* __restrict__ g,
+                            double* __restrict__ y, int n, int c) {
+    const long total = static_cast<long>(n) * c;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+        double acc = 0.0;
+        for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, __dmul_rn(w[static_cast<long>(i) * n + k], g[static_cast<long>(j) * n + k]));
+        y[idx] = acc;
+    }
+}
+
+// grad (=|+=) G X^T  (G, X: n x c; grad: n x n).  The product is formed first and
+// then added, like axpy(1.0, matmul_nt(g, in), grad_sum).
+__global__ void k_wgrad_nt(const double* __restrict__ g, const double* __restrict__ x,
+                           double* __restrict__ grad, int n, int c, int overwrite) {
+    const long total = static_cast<long>(n) * n;
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+        double acc = 0.0;
+        for (int k = 0; k < c; ++k) acc = __dadd_rn(acc, __dmul_rn(g[static_cast<long>(k) * n + i], x[static_cast<long>(k) * n + j]));
+        grad[idx] = overwrite ? __dadd_rn(0.0, acc) : __dadd_rn(grad[idx], acc);
+    }
+}
+
+// g = (out - y) / b   (semantics.cpp:314-319)
+__global__ void k_loss_grad(const double* __restrict__ out, const double* __restrict__ y,
+                            double* __restrict__ g, long total, double b) {
+    for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long>(gridDim.x) * blockDim.x)
+        g[idx] = __ddiv_rn(__dsub_rn(out[idx], y[idx]), b);
+}
+
+// loss = sum (out - y)^2 / (2b), one block, fixed summation order (deterministic).
+__global__ void k_loss(const double* __restrict__ out, const double* __restrict__ y, long total,
+                       double b, double* __restrict__ loss) {
+    __shared__ double part[kThreads];
+    double acc = 0.0;
+    for (long i = threadIdx.x; i < total; i += kThreads) {
+        const double diff = out[i] - y[i];
+        acc += diff * diff / (2.0 * b);
+    }
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
+        if (static_cast<int>(threadIdx.x) < w) part[threadIdx.x] += part[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *loss = part[0];
+}
+
+// v = beta v + (1-beta) (gsum / count);  W_dst = W_src + (-lr) v
+__global__ void k_update(const double* __restrict__ wsrc, double* __restrict__ wdst,
+                         double* __restrict__ vel, const double* __restrict__ gsum, long total,
+                         double count, double lr, double beta) {
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long>(gridDim.x) * blockDim.x) {
+        const double g = __ddiv_rn(gsum[i], count);
+        const double v = __dadd_rn(__dmul_rn(beta, vel[i]), __dmul_rn(__dsub_rn(1.0, beta), g));
+        vel[i] = v;
+        wdst[i] = __dadd_rn(wsrc[i], __dmul_rn(-lr, v));
+    }
+}
+
+class LinearF64Stage final : public StageModel {
+public:
+    LinearF64Stage(const EngineConfig& cfg, int stage, int lo, int hi, int sslots, int wslots)
+        : n_(cfg.dim), cols_(cfg.microbatch_size), layers_(hi - lo), stage0_(stage == 0),
+          stageL_(stage == cfg.depth - 1), sslots_(sslots), wslots_(wslots), lr_(cfg.lr),
+          beta_(cfg.momentum) {
+        if (n_ < 1 || cols_ < 1) throw Error("toy model dimensions must be >= 1");
+        mat_ = static_cast<size_t>(n_) * n_;
+        act_ = static_cast<size_t>(n_) * cols_;
+        alloc(&w_, static_cast<size_t>(wslots_) * layers_ * mat_);
+        alloc(&vel_, layers_ * mat_);
+        alloc(&gsum_, layers_ * mat_);
+        alloc(&stash_, static_cast<size_t>(sslots_) * layers_ * act_);
+        alloc(&gtmp_, 2 * act_);
+        if (stageL_) alloc(&out_, static_cast<size_t>(sslots_) * act_);
+        check_cuda(cudaMemset(vel_, 0, layers_ * mat_ * sizeof(double)), "cudaMemset");
+        xin_.assign(static_cast<size_t>(sslots_), nullptr);
+    }
+    ~LinearF64Stage() override {
+        for (double* p : {w_, vel_, gsum_, stash_, gtmp_, out_, x_, y_, loss_}) cudaFree(p);
+    }
+
+    size_t num_params() const override { return layers_ * mat_; }
+    size_t boundary_bytes() const override { return act_ * sizeof(double); }
+    size_t weight_bytes_public() const override { return layers_ * mat_ * sizeof(double); }
+    int data_capacity() const override { return capacity_; }
+
+    void set_data(const void* inputs, const void* targets, int first_mb, int count) override {
+        if (count < 1) throw Error("set_data: empty microbatch range");
+        if (first_mb + count - 1 > capacity_) {
+            for (double* p : {x_, y_, loss_}) cudaFree(p);
+                capacity_ = first_mb + count - 1;
+            alloc(&x_, static_cast<size_t>(capacity_) * act_);
+            alloc(&y_, static_cast<size_t>(capacity_) * act_);
+            alloc(&loss_, static_cast<size_t>(capacity_));
+            check_cuda(cudaMemset(loss_, 0, sizeof(double) * capacity_), "cudaMemset");
+        }
+        const size_t off = static_cast<size_t>(first_mb - 1) * act_;
+        const size_t bytes = static_cast<size_t>(count) * act_ * sizeof(double);
+        if (inputs) check_cuda(cudaMemcpy(x_ + off, inputs, bytes, cudaMemcpyHostToDevice), "H2D x");
+        if (targets) check_cuda(cudaMemcpy(y_ + off, targets, bytes, cudaMemcpyHostToDevice), "H2D y");
+    }
+
+    void load_weights(int wslot, const void* host, size_t bytes) override {
+        if (bytes != weight_bytes_public()) throw Error("load_weights: size mismatch");
+        check_cuda(cudaMemcpy(wslot_ptr(wslot, 0), host, bytes, cudaMemcpyHostToDevice), "H2D W");
+    }
+    void read_weights(int wslot, void* host, size_t bytes, cudaStream_t s) override {
+        if (bytes != weight_bytes_public()) throw Error("read_weights: size mismatch");
+        check_cuda(cudaMemcpyAsync(host, wslot_ptr(wslot, 0), bytes, cudaMemcpyDeviceToHost, s), "D2H W");
+        check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    }
+    void read_losses(double* host, int first_mb, int count, cudaStream_t s) override {
+        if (!stageL_) throw Error("this stage computes no loss");
+        if (first_mb < 1 || first_mb + count - 1 > capacity_) throw Error("loss index out of range");
+        check_cuda(cudaMemcpyAsync(host, loss_ + first_mb - 1, sizeof(double) * count,
+                                   cudaMemcpyDeviceToHost, s), "D2H loss");
+    }
+
+    void forward(int k, int wslot, int sslot, const void* x_in, void* x_out, cudaStream_t s) override {
+        const double* cur = stage0_ ? data_x(k) : static_cast<const double*>(x_in);
+        xin_[static_cast<size_t>(sslot)] = cur;
+        for (int l = 0; l < layers_; ++l) {
+            double* y;
+            if (l + 1 < layers_) y = stash_ptr(sslot, l + 1);
+            else y = stageL_ ? out_ + static_cast<size_t>(sslot) * act_ : static_cast<double*>(x_out);
+            k_matmul_nn<<<blocks_for(static_cast<long>(act_)), kThreads, 0, s>>>(wslot_ptr(wslot, l), cur, y, n_, cols_);
+            cur = y;
+        }
+        check_cuda(cudaGetLastError(), "linear forward");
+    }
+
+    void backward(int k, int wslot, int sslot, const void* g_in, void* g_out, bool first,
+                  cudaStream_t s) override {
+        const double* g = static_cast<const double*>(g_in);
+        int flip = 0;
+        if (stageL_) {
+            double* lg = gtmp_ + static_cast<size_t>(flip) * act_;
+            flip ^= 1;
+            const double* out = out_ + static_cast<size_t>(sslot) * act_;
+            k_loss<<<1, kThreads, 0, s>>>(out, data_y(k), static_cast<long>(act_),
+                                          static_cast<double>(cols_), loss_ + (k - 1));
+            k_loss_grad<<<blocks_for(static_cast<long>(act_)), kThreads, 0, s>>>(
+                out, data_y(k), lg, static_cast<long>(act_), static_cast<double>(cols_));
+            g = lg;
+        }
+        for (int l = layers_ - 1; l >= 0; --l) {
+            const double* in = l == 0 ? xin_[static_cast<size_t>(sslot)] : stash_ptr(sslot, l);
+            k_wgrad_nt<<<blocks_for(static_cast<long>(mat_)), kThreads, 0, s>>>(
+                g, in, gsum_ + static_cast<size_t>(l) * mat_, n_, cols_, first ? 1 : 0);
+            if (l > 0 || !stage0_) {
+                double* dst = l == 0 ? static_cast<double*>(g_out) : gtmp_ + static_cast<size_t>(flip) * act_;
+                flip ^= 1;
+                k_matmul_tn<<<blocks_for(static_cast<long>(act_)), kThreads, 0, s>>>(wslot_ptr(wslot, l), g, dst, n_, cols_);
+                g = dst;
+            }
+        }
+        check_cuda(cudaGetLastError(), "linear backward");
+    }
+
+    void update(int src_slot, int dst_slot, int count, cudaStream_t s) override {
+        const long total = static_cast<long>(layers_ * mat_);
+        k_update<<<blocks_for(total), kThreads, 0, s>>>(wslot_ptr(src_slot, 0), wslot_ptr(dst_slot, 0), vel_,
+                                                        gsum_, total, static_cast<double>(count), lr_, beta_);
+        check_cuda(cudaGetLastError(), "linear update");
+    }
+
+private:
+    static void alloc(double** p, size_t n) {
+        check_cuda(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(double)), "cudaMalloc");
+    }
+    double* wslot_ptr(int slot, int l) const { return w_ + (static_cast<size_t>(slot) * layers_ + l) * mat_; }
+    double* stash_ptr(int slot, int l) const { return stash_ + (static_cast<size_t>(slot) * layers_ + l) * act_; }
+    const double* data_x(int k) const { check_k(k); return x_ + static_cast<size_t>(k - 1) * act_; }
+    const double* data_y(int k) const { check_k(k); return y_ + static_cast<size_t>(k - 1) * act_; }
+    void check_k(int k) const {
+        if (k < 1 || k > capacity_) throw Error("toy dataset has too few microbatches for the requested run");
+    }
+
+    int n_, cols_, layers_;
+    bool stage0_, stageL_;
+    int sslots_, wslots_;
+    double lr_, beta_;
+    size_t mat_ = 0, act_ = 0;
+    int capacity_ = 0;
+    double *w_ = nullptr, *vel_ = nullptr, *gsum_ = nullptr, *stash_ = nullptr, *gtmp_ = nullptr,
+           *out_ = nullptr, *x_ = nullptr, *y_ = nullptr, *loss_ = nullptr;
+    std::vector<const double*> xin_;
+};
+
+}  // namespace
+
+std::unique_ptr<StageModel> make_linear_f64_stage(const EngineConfig& cfg, int stage, int lo,
+                                                   int hi, int stash_slots, int weight_slots) {
+    return std::make_unique<LinearF64Stage>(cfg, stage, lo, hi, stash_slots, weight_slots);
+}
+
+}  // namespace p2bw
