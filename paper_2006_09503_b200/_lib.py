@@ -41,11 +41,52 @@ class Op(C.Structure):
     _fields_ = [("kind", C.c_int), ("microbatch", C.c_int), ("weight_version", C.c_int)]
 
 
+def _signatures():
+    """(name, restype, argtypes) for every function include/p2bw.h declares."""
+    i, ll, vp, sz, cp = C.c_int, C.c_longlong, C.c_void_p, C.c_size_t, C.c_char_p
+    pi, pvp, psz = C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)
+    return [
+        ("p2bw_last_error", cp, []),
+        ("p2bw_version", cp, []),
+        ("p2bw_free", None, [vp]),
+        ("p2bw_weight_version_2bw", i, [i, i, pi]),
+        ("p2bw_required_versions", i, [i, i, i, pi]),
+        ("p2bw_schedule_generate", i, [i, i, i, i, pvp]),
+        ("p2bw_schedule_parse", i, [cp, pvp]),
+        ("p2bw_schedule_num_stages", i, [vp, pi]),
+        ("p2bw_schedule_ops", i, [vp, i, C.POINTER(C.POINTER(Op)), psz]),
+        ("p2bw_schedule_serialize", i, [vp, pvp]),
+        ("p2bw_schedule_destroy", None, [vp]),
+        ("p2bw_policy_name", i, [i, C.POINTER(cp)]),
+        ("p2bw_policy_parse", i, [cp, pi]),
+        ("p2bw_plan", i, [cp, cp, ll, i, i, pvp]),
+        ("p2bw_partition_equal", i, [cp, i, pvp]),
+        ("p2bw_engine_create", i, [vp, pvp]),
+        ("p2bw_engine_destroy", None, [vp]),
+        ("p2bw_engine_stage_weight_bytes", i, [vp, i, psz]),
+        ("p2bw_engine_load_stage_weights", i, [vp, i, vp, sz]),
+        ("p2bw_engine_init_weights", i, [vp]),
+        ("p2bw_engine_set_data", i, [vp, vp, vp, i, i]),
+        ("p2bw_engine_run", i, [vp, vp, vp, i]),
+        ("p2bw_engine_run_schedule", i, [vp, i, i]),
+        ("p2bw_engine_sync", i, [vp]),
+        ("p2bw_engine_counters", i, [vp, vp]),
+        ("p2bw_engine_read_snapshot", i, [vp, i, i, vp, sz]),
+        ("p2bw_engine_read_version", i, [vp, i, i, vp, sz]),
+        ("p2bw_engine_losses", i, [vp, i, i, vp]),
+        ("p2bw_kernel_gemm_bf16", i, [vp, ll, i, vp, ll, i, i, i, i, C.POINTER(GemmEpilogue), vp]),
+    ]
+
+
+def declared_symbols() -> list[str]:
+    return [name for name, _, _ in _signatures()]
+
+
 def _declare(lib: C.CDLL) -> None:
-    i, ll, vp, f, d = C.c_int, C.c_longlong, C.c_void_p, C.c_float, C.c_double
-    lib.p2bw_last_error.restype = C.c_char_p
-    lib.p2bw_version.restype = C.c_char_p
-    lib.p2bw_kernel_gemm_bf16.argtypes = [vp, ll, i, vp, ll, i, i, i, i, C.POINTER(GemmEpilogue), vp]
+    for name, res, args in _signatures():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
 
 
 def lib() -> C.CDLL:

@@ -1,0 +1,104 @@
+"""Generates the golden fixtures in tests/golden/ from the REFERENCE itself
+(oracle/_ref/ref_tool, built from /root/reference by oracle/Makefile).
+
+Run in the build container (where /root/reference exists):
+    make -C oracle ref && python tests/golden/make_golden.py
+The outputs are committed; GPU-box tests read them without /root/reference.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+from oracle import pipesim_oracle as O  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+TOOL = ROOT / "oracle" / "_ref" / "ref_tool"
+
+
+def tool(*args) -> str:
+    r = subprocess.run([str(TOOL), *map(str, args)], capture_output=True, text=True)
+    return r.stdout
+
+
+def schedule_text(policy, d, m, T):
+    return tool("schedule", policy, d, m, T)
+
+
+SMALL_SCHEDULES = [(p, d, m, T) for p in range(5) for (d, m, T) in
+                   [(1, 1, 3), (2, 4, 1), (2, 4, 3), (4, 4, 3), (4, 8, 2), (8, 8, 2), (3, 5, 2)]]
+SWEEP_SCHEDULES = [(p, d, m, 2) for p in (1, 3, 4) for d in (2, 4, 8) for m in (4, 8, 16, 32) if m >= d or p != 4]
+
+CLUSTERS = {
+    "fixture_8x8": dict(total_workers=8, gpus_per_server=8, bandwidth_high_gbps=1000,
+                        bandwidth_low_gbps=100, memory_capacity_gb=32),
+    "fixture_16x8": dict(total_workers=16, gpus_per_server=8, bandwidth_high_gbps=1000,
+                         bandwidth_low_gbps=100, memory_capacity_gb=32),
+    "fixture_4x4_8gb": dict(total_workers=4, gpus_per_server=4, bandwidth_high_gbps=1000,
+                            bandwidth_low_gbps=100, memory_capacity_gb=8),
+    # one 8x B200 NVSwitch node: 900 GB/s per direction NVLink, 180 GB HBM3e
+    "b200_8": dict(total_workers=8, gpus_per_server=8, bandwidth_high_gbps=900,
+                   bandwidth_low_gbps=50, memory_capacity_gb=180),
+}
+MODELS = {
+    "uniform8": O.uniform_profile_json("uniform8", 8, 1e-3, 2e-3, 1e8, 1e6, 2.5e5, [1, 2, 4]),
+    "uniform24": O.uniform_profile_json("uniform24", 24, 1e-3, 2e-3, 1e8, 1e6, 2.5e5, [1, 2, 4, 8]),
+    "fat4": O.uniform_profile_json("fat", 4, 1e-3, 2e-3, 1e8, 3e9, 1e9, [1]),
+    "gpt_like48": O.uniform_profile_json("gpt48", 48, 2.1e-4, 4.2e-4, 8.85e7, 4.0e8, 2.0e6,
+                                         [1, 2, 4, 8, 16]),
+}
+PLANS = [("uniform8", "fixture_8x8", 128), ("uniform8", "fixture_16x8", 128),
+         ("uniform24", "fixture_8x8", 512), ("fat4", "fixture_4x4_8gb", 64),
+         ("gpt_like48", "b200_8", 2048), ("uniform24", "b200_8", 256)]
+
+TOY_GRID = [dict(dim=4, layers=d, b=2, seed=12345, lr=0.05, beta=beta, m=m, T=10, policy=p, depth=d)
+            for d in (1, 2, 4) for m in (d, 2 * d) for beta in (0.0, 0.9) for p in (1, 3, 4)]
+TOY_EXTRA = [dict(dim=16, layers=4, b=8, seed=424242, lr=0.05, beta=0.9, m=4, T=6, policy=4, depth=2),
+             dict(dim=32, layers=8, b=16, seed=7, lr=0.02, beta=0.9, m=8, T=4, policy=4, depth=8),
+             dict(dim=8, layers=4, b=4, seed=99, lr=0.05, beta=0.9, m=4, T=5, policy=2, depth=4)]
+
+
+def main():
+    sched = {f"{p}/{d}/{m}/{T}": schedule_text(p, d, m, T) for p, d, m, T in SMALL_SCHEDULES}
+    sweep = {f"{p}/{d}/{m}/{T}": hashlib.sha256(schedule_text(p, d, m, T).encode()).hexdigest()
+             for p, d, m, T in SWEEP_SCHEDULES}
+    versions = {f"{k}/{m}": int(tool("version", k, m)) for k in range(1, 40) for m in (1, 2, 4, 8)}
+    json.dump({"schedules": sched, "sweep_sha256": sweep, "versions": versions},
+              open(OUT / "schedules.json", "w"), indent=1, sort_keys=True)
+
+    plans = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for mname, cname, B in PLANS:
+            mp, cp = Path(tmp) / "m.json", Path(tmp) / "c.json"
+            mp.write_text(MODELS[mname])
+            cp.write_text(json.dumps(CLUSTERS[cname]))
+            out = tool("plan", mp, cp, B, 4)
+            plans[f"{mname}/{cname}/{B}"] = (json.loads(out) if not out.startswith("ERROR")
+                                             else {"error": out.strip()})
+        json.dump({"models": MODELS, "clusters": CLUSTERS, "plans": plans},
+                  open(OUT / "plans.json", "w"), indent=1, sort_keys=True)
+
+        arrays, meta = {}, []
+        for idx, c in enumerate(TOY_GRID + TOY_EXTRA):
+            path = Path(tmp) / "traj.bin"
+            info = json.loads(tool("toy", c["dim"], c["layers"], c["b"], c["seed"], repr(c["lr"]),
+                                   repr(c["beta"]), c["m"], c["T"], c["policy"], c["depth"], path))
+            traj = np.fromfile(path, dtype=np.float64).reshape(c["T"] + 1, c["layers"], c["dim"] ** 2)
+            arrays[f"traj_{idx}"] = traj
+            meta.append(dict(c, **info))
+    np.savez_compressed(OUT / "toy_trajectories.npz", **arrays)
+    json.dump(meta, open(OUT / "toy_trajectories.json", "w"), indent=1)
+    print("wrote", sorted(os.listdir(OUT)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,111 @@
+"""libp2bw.so host path (schedule, planner, partition) through the C-ABI,
+checked bit-exactly against the reference's golden vectors and the oracle.
+No GPU needed: these entry points are host C++ (the reference's own behaviour,
+schedule.cpp / planner.cpp / profile.cpp)."""
+import ctypes as C
+import hashlib
+import json
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from oracle import pipesim_oracle as O
+from paper_2006_09503_b200 import _lib
+from paper_2006_09503_b200 import pipesim as P
+from tests import _golden as G
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_exports_every_declared_symbol():
+    header = (ROOT / "include" / "p2bw.h").read_text()
+    declared = set(re.findall(r"^\s*(?:const\s+char\s*\*|int|void)\s+(p2bw_\w+)\s*\(", header, re.M))
+    assert declared, "no declarations parsed"
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines()}
+    assert declared <= exported, sorted(declared - exported)
+    assert set(_lib.declared_symbols()) == declared  # the ctypes table covers the header exactly
+    lib = _lib.lib()
+    for name in declared:
+        getattr(lib, name)
+
+
+def test_version_formula_and_errors():
+    for key, v in G.schedules()["versions"].items():
+        k, m = map(int, key.split("/"))
+        assert P.weight_version_2bw(k, m) == v
+    with pytest.raises(P.PipesimError, match="microbatch index must be >= 1"):
+        P.weight_version_2bw(0, 4)
+    with pytest.raises(P.PipesimError, match="m >= d"):
+        P.generate_schedule(P.PipelinePolicy.TwoBW, 4, 2, 1)
+    assert P.required_versions(P.PipelinePolicy.TwoBW, 8, 8) == 2
+    assert P.required_versions(P.PipelinePolicy.PipeDream1F1B, 4, 1) == 4
+
+
+def test_schedules_bit_identical_to_reference():
+    g = G.schedules()
+    for key, text in g["schedules"].items():
+        p, d, m, T = map(int, key.split("/"))
+        if text.startswith("ERROR"):
+            with pytest.raises(P.PipesimError):
+                P.schedule_text(p, d, m, T)
+            continue
+        assert P.schedule_text(p, d, m, T) == text, key
+    for key, digest in g["sweep_sha256"].items():
+        p, d, m, T = map(int, key.split("/"))
+        assert hashlib.sha256(P.schedule_text(p, d, m, T).encode()).hexdigest() == digest, key
+
+
+def test_program_round_trip_and_parse_errors():
+    text = P.schedule_text(P.PipelinePolicy.TwoBW, 4, 8, 2)
+    progs = P.parse_programs(text)
+    assert P.serialize_programs(progs) == text
+    assert progs == P.generate_schedule(P.PipelinePolicy.TwoBW, 4, 8, 2)
+    with pytest.raises(P.PipesimError, match="teleport"):
+        P.parse_programs("stage=0 op=teleport")
+    with pytest.raises(P.PipesimError, match="missing stage"):
+        P.parse_programs("op=forward mb=1 ver=0")
+    for pol in P.PipelinePolicy:
+        assert P.parse_policy(P.to_string(pol)) == pol
+    with pytest.raises(P.PipesimError, match="bogus"):
+        P.parse_policy("bogus")
+
+
+def test_plans_bit_identical_to_reference():
+    g = G.plans()
+    for key, ref in g["plans"].items():
+        mname, cname, B = key.split("/")
+        got = P.plan(g["models"][mname], json.dumps(g["clusters"][cname]), int(B))
+        assert got == ref, key  # every field, parsed values
+
+
+def test_plan_errors_keep_reference_wording():
+    fat = O.uniform_profile_json("fat", 4, 1e-3, 2e-3, 1e8, 3e9, 1e9, [1])
+    tiny = json.dumps(dict(total_workers=4, gpus_per_server=4, bandwidth_high_gbps=1000,
+                           bandwidth_low_gbps=100, memory_capacity_gb=1e-3))
+    with pytest.raises(P.PipesimError, match="no feasible"):
+        P.plan(fat, tiny, 64)
+    with pytest.raises(P.PipesimError, match="max safe batch size"):
+        P.plan(fat, tiny, 0)
+    assert "best configuration: w=" in P.plan_text(
+        fat, json.dumps(dict(total_workers=4, gpus_per_server=4, bandwidth_high_gbps=1000,
+                             bandwidth_low_gbps=100, memory_capacity_gb=8)), 64)
+
+
+def test_partition_equal_matches_oracle_exactly():
+    mj = G.plans()["models"]["gpt_like48"]
+    blocks = O.load_model_profile(mj)
+    for d in (1, 2, 3, 4, 6, 8, 12, 16, 24, 48):
+        got = P.partition_equal(mj, d)
+        ref = O.partition_equal(blocks, d)
+        assert len(got) == d
+        for g, r in zip(got, ref):
+            assert {int(k): v for k, v in g["fwd_time"].items()} == r.fwd
+            assert {int(k): v for k, v in g["bwd_time"].items()} == r.bwd
+            assert g["weight_bytes"] == r.weight_bytes
+            assert {int(k): v for k, v in g["act_output_bytes"].items()} == r.act_output
+    with pytest.raises(P.PipesimError, match="does not divide"):
+        P.partition_equal(mj, 5)
