@@ -2,7 +2,7 @@
  * p2bw.h — C-ABI of libp2bw.so, the B200-native PipeDream-2BW engine.
  *
  * This is the drop-in boundary for the reference's pipelined training path
- * (pipesim, /root/reference/proj/core/include/pipesim/*.hpp).  The reference
+ * (pipesim, /root/reference/proj/core/include/pipesim/ headers).  The reference
  * has no FFI of its own; every entry point below names the C++ interface it
  * replaces (file:line, relative to /root/reference/proj).  Plain pointers and
  * sizes only: no torch / C++ types cross this boundary.
@@ -166,6 +166,8 @@ int p2bw_engine_read_snapshot(p2bw_engine* eng, int stage, int update_index, voi
                               size_t bytes);
 /* A live weight version of a stage (at most 2 under 2BW). */
 int p2bw_engine_read_version(p2bw_engine* eng, int stage, int version, void* host, size_t bytes);
+/* fp32 master weights of a stage (transformer: the latest version, unrounded). */
+int p2bw_engine_read_master(p2bw_engine* eng, int stage, void* host, size_t bytes);
 /* Training losses of microbatches [first_mb, first_mb+count) (last stage). */
 int p2bw_engine_losses(p2bw_engine* eng, int first_mb, int count, double* out);
 
@@ -195,6 +197,23 @@ typedef struct {
 int p2bw_kernel_gemm_bf16(const void* a, long long lda, int a_major, const void* b,
                           long long ldb, int b_major, int m, int n, int k,
                           const p2bw_gemm_epilogue* epi, void* stream);
+
+/* Attention over qkv [b*seq x 3h] (heads of 64): o [b*seq x h], lse [b*heads*seq] fp32. */
+int p2bw_kernel_attention_fwd(const void* qkv, void* o, void* lse, int batch, int seq, int heads,
+                              int causal, void* stream);
+/* dqkv [b*seq x 3h] from dO; delta scratch [b*heads*seq] fp32. */
+int p2bw_kernel_attention_bwd(const void* qkv, const void* o, const void* dout, const void* lse,
+                              void* dqkv, void* delta, int batch, int seq, int heads, int causal,
+                              void* stream);
+/* LayerNorm forward / backward (bf16 rows, fp32 stats and parameter gradients). */
+int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void* y, void* mean,
+                              void* rstd, int rows, int h, void* stream);
+int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
+                              const void* g, const void* dres, void* dx, void* dg, void* db,
+                              int overwrite, int rows, int h, void* stream);
+/* Fused softmax cross-entropy: logits [rows x vp] -> dlogits in place, row_loss [rows]. */
+int p2bw_kernel_softmax_xent(void* logits, const void* targets, int rows, int vocab, int vp,
+                             float grad_scale, void* row_loss, void* stream);
 
 #ifdef __cplusplus
 }

@@ -173,6 +173,16 @@ int p2bw_engine_read_version(p2bw_engine* eng, int stage, int version, void* hos
     });
 }
 
+int p2bw_engine_read_master(p2bw_engine* eng, int stage, void* host, size_t bytes) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (host == nullptr) throw std::invalid_argument("host buffer is NULL");
+        e.sync();
+        e.model(stage).read_master(host, bytes);
+    });
+}
+
 int p2bw_engine_losses(p2bw_engine* eng, int first_mb, int count, double* out) {
     return guarded([&] {
         auto& e = eng_of(eng);

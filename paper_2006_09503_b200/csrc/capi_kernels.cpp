@@ -2,6 +2,7 @@
 // (p2bw_kernel_*).  Device pointers in, status code out; see include/p2bw.h.
 #include "capi_internal.h"
 #include "kernels.h"
+#include "tkernels.h"
 #include "util.h"
 #include "p2bw.h"
 
@@ -27,5 +28,58 @@ extern "C" int p2bw_kernel_gemm_bf16(const void* a, long long lda, int a_major, 
         e.alpha = epi->alpha;
         e.beta = epi->beta;
         gemm_bf16(A, B, m, n, k, e, static_cast<cudaStream_t>(stream));
+    });
+}
+
+namespace {
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+const bf16* cb(const void* p) { return static_cast<const bf16*>(p); }
+bf16* mb(void* p) { return static_cast<bf16*>(p); }
+}  // namespace
+
+extern "C" int p2bw_kernel_attention_fwd(const void* qkv, void* o, void* lse, int batch, int seq, int heads,
+                                         int causal, void* stream) {
+    return guarded([&] {
+        attention_fwd(cb(qkv), mb(o), static_cast<float*>(lse), batch, seq, heads, causal != 0, as_stream(stream));
+    });
+}
+
+extern "C" int p2bw_kernel_attention_bwd(const void* qkv, const void* o, const void* dout, const void* lse,
+                                         void* dqkv, void* delta, int batch, int seq, int heads, int causal,
+                                         void* stream) {
+    return guarded([&] {
+        attention_bwd(cb(qkv), cb(o), cb(dout), static_cast<const float*>(lse), mb(dqkv),
+                      static_cast<float*>(delta), batch, seq, heads, causal != 0, as_stream(stream));
+    });
+}
+
+extern "C" int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void* y, void* mean,
+                                         void* rstd, int rows, int h, void* stream) {
+    return guarded([&] {
+        layernorm_fwd(cb(x), cb(g), cb(b), mb(y), static_cast<float*>(mean), static_cast<float*>(rstd), rows, h,
+                      as_stream(stream));
+    });
+}
+
+extern "C" int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
+                                         const void* g, const void* dres, void* dx, void* dg, void* db,
+                                         int overwrite, int rows, int h, void* stream) {
+    return guarded([&] {
+        float* scratch = nullptr;
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                   layernorm_bwd_scratch_floats(rows, h) * sizeof(float), as_stream(stream)),
+                   "cudaMallocAsync");
+        layernorm_bwd(cb(dy), cb(x), static_cast<const float*>(mean), static_cast<const float*>(rstd), cb(g),
+                      cb(dres), mb(dx), static_cast<float*>(dg), static_cast<float*>(db), overwrite != 0, rows, h,
+                      scratch, as_stream(stream));
+        check_cuda(cudaFreeAsync(scratch, as_stream(stream)), "cudaFreeAsync");
+    });
+}
+
+extern "C" int p2bw_kernel_softmax_xent(void* logits, const void* targets, int rows, int vocab, int vp,
+                                        float grad_scale, void* row_loss, void* stream) {
+    return guarded([&] {
+        softmax_xent(mb(logits), static_cast<const int*>(targets), rows, vocab, vp, grad_scale,
+                     static_cast<float*>(row_loss), as_stream(stream));
     });
 }

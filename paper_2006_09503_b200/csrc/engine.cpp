@@ -110,6 +110,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             } else {
                 throw Error("unknown model kind " + std::to_string(cfg_.model_kind));
             }
+            st.model->bind_stream(st.stream);
             const size_t nb = st.model->boundary_bytes();
             if (s > 0) {
                 st.act_ring.assign(static_cast<size_t>(st.stash_slots), nullptr);

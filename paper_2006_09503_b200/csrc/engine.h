@@ -73,6 +73,12 @@ public:
         (void)host, (void)first_mb, (void)count, (void)s;
         throw Error("this stage computes no loss");
     }
+    virtual void bind_stream(cudaStream_t s) { (void)s; }
+    // fp32 master weights (models that keep one), public layout.
+    virtual void read_master(void* host, size_t bytes) {
+        (void)host, (void)bytes;
+        throw Error("this model keeps no separate master weights");
+    }
     // Deterministic synthetic initial weights (version 0) from a seed.
     virtual void init_weights(uint64_t seed) {
         (void)seed;

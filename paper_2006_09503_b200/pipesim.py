@@ -290,6 +290,12 @@ class Engine:
               C.c_size_t(n))
         return out
 
+    def read_master(self, s: int) -> np.ndarray:
+        n = self.stage_weight_bytes(s)
+        out = np.empty(n // 4, dtype=np.float32)
+        _call("p2bw_engine_read_master", self.h, s, out.ctypes.data_as(C.c_void_p), C.c_size_t(n))
+        return out
+
     def losses(self, first_mb: int, count: int) -> np.ndarray:
         out = np.empty(count, dtype=np.float64)
         _call("p2bw_engine_losses", self.h, first_mb, count, out.ctypes.data_as(C.c_void_p))

@@ -1,0 +1,76 @@
+"""The transformer 2BW pipeline on the B200 engine against the CPU oracle
+(oracle/transformer_oracle.py, torch float64): the engine's per-microbatch
+losses and weight updates after N batches must match the reference's delay-1
+loop (semantics.cpp:167-184) within bf16 tolerance, and must NOT match vanilla
+SGD (so a version-bookkeeping bug cannot hide inside the tolerance).
+Depth 1 and depth 2 (two stages on one device, one stream each) are covered."""
+import numpy as np
+import pytest
+
+from oracle import transformer_oracle as TO
+from paper_2006_09503_b200 import pipesim as P
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-2      # per-microbatch loss, bf16 activations vs float64
+DELTA_RTOL = 6e-2     # ||dW_gpu - dW_ref|| / ||dW_ref|| over each stage's parameters
+
+
+def make_engine(spec, depth, m, lr, beta, seed, policy=P.PipelinePolicy.TwoBW):
+    return P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=policy, depth=depth, microbatches=m,
+                    microbatch_size=spec.batch, layers=spec.layers, hidden=spec.hidden, heads=spec.heads,
+                    seq_len=spec.seq, vocab=spec.vocab, causal=int(spec.causal), head_rows=spec.head_rows,
+                    learning_rate=lr, momentum=beta, seed=seed)
+
+
+def run_case(spec, depth, m, T, lr, beta, seed):
+    ids, tg = TO.synthetic_batch(spec, m * T, seed + 1)
+    eng = make_engine(spec, depth, m, lr, beta, seed)
+    eng.init_weights()
+    params = TO.init_params(spec, seed)
+    for s in range(depth):
+        got = eng.read_master(s)
+        ref = TO.flatten_stage(params, spec, depth, s)
+        assert np.array_equal(got, ref), "device initialiser differs from the oracle's"
+    eng.set_data(ids, tg, 1, m * T)
+    eng.run_schedule(T)
+    eng.sync()
+    losses = eng.losses(1, m * T)
+    finals = [eng.read_master(s) for s in range(depth)]
+    c = eng.counters()
+    eng.close()
+    return params, ids, tg, losses, finals, c
+
+
+@pytest.mark.parametrize("depth,causal,head_rows", [(1, True, 0), (2, True, 0), (2, False, 16)])
+def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows):
+    spec = TO.Spec(layers=2, hidden=128, heads=2, seq=64, vocab=500, batch=2, causal=causal, head_rows=head_rows)
+    m, T, lr, beta, seed = 2, 4, 0.5, 0.9, 1234
+    params, ids, tg, losses, finals, c = run_case(spec, depth, m, T, lr, beta, seed)
+    assert c.max_versions_held == 2
+    traj, ref_losses = TO.train(params, spec, ids, tg, lr, beta, m, T, delayed=True)
+    van, van_losses = TO.train(params, spec, ids, tg, lr, beta, m, T, delayed=False)
+    assert np.all(np.abs(losses - ref_losses) <= LOSS_RTOL * np.abs(ref_losses)), (losses, ref_losses)
+    for s in range(depth):
+        w0 = TO.flatten_stage(params, spec, depth, s).astype(np.float64)
+        ref = TO.flatten_stage({k: v.numpy() for k, v in traj[-1].items()}, spec, depth, s).astype(np.float64)
+        vr = TO.flatten_stage({k: v.numpy() for k, v in van[-1].items()}, spec, depth, s).astype(np.float64)
+        d_gpu, d_ref, d_van = finals[s] - w0, ref - w0, vr - w0
+        err = np.linalg.norm(d_gpu - d_ref) / np.linalg.norm(d_ref)
+        gap = np.linalg.norm(d_van - d_ref) / np.linalg.norm(d_ref)
+        assert err < DELTA_RTOL, (s, err)
+        assert gap > 2 * err, (s, gap, err)  # 2BW is distinguishable from vanilla at this tolerance
+
+
+def test_depths_agree_with_each_other():
+    spec = TO.Spec(layers=4, hidden=128, heads=2, seq=64, vocab=300, batch=2, causal=True)
+    m, T = 4, 3
+    _, _, _, l1, f1, _ = run_case(spec, 1, m, T, 0.3, 0.9, 77)
+    _, _, _, l4, f4, _ = run_case(spec, 4, m, T, 0.3, 0.9, 77)
+    assert np.allclose(l1, l4, rtol=2e-3)
+    params = TO.init_params(spec, 77)
+    full1 = TO.unflatten_stage(f1[0], spec, 1, 0)
+    for s in range(4):
+        st = TO.unflatten_stage(f4[s], spec, 4, s)
+        for name, v in st.items():
+            assert np.allclose(v, full1[name], rtol=2e-2, atol=2e-4), (s, name)

@@ -1,0 +1,108 @@
+"""Transformer-stage kernels against torch fp32 references of the same op on
+the GPU (the reference has no layer math): attention fwd/bwd
+(head dim 64, causal and bidirectional), LayerNorm fwd/bwd, fused softmax-CE.
+Tolerances are bf16-storage level and stated per test."""
+import ctypes as C
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2006_09503_b200._lib import call  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ref_attention(qkv, b, s, nh, causal):
+    h = nh * 64
+    q, k, v = qkv.float().view(b, s, 3, nh, 64).permute(2, 0, 3, 1, 4)
+    sc = q @ k.transpose(-1, -2) * 0.125
+    if causal:
+        sc = sc.masked_fill(torch.triu(torch.ones(s, s, dtype=torch.bool, device=qkv.device), 1), float("-inf"))
+    p = torch.softmax(sc, -1)
+    o = (p @ v).transpose(1, 2).reshape(b * s, h)
+    lse = torch.logsumexp(sc, -1).reshape(-1)
+    return o, lse
+
+
+@pytest.mark.parametrize("b,s,nh,causal", [(2, 128, 2, True), (2, 128, 2, False), (1, 512, 4, True),
+                                           (3, 512, 2, False), (2, 96, 3, True)])
+def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
+    h = nh * 64
+    g = torch.Generator(device="cuda").manual_seed(b * 1000 + s + nh)
+    qkv = (torch.randn(b * s, 3 * h, device="cuda", generator=g) * 0.8).to(torch.bfloat16)
+    o = torch.empty(b * s, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b * nh * s, device="cuda", dtype=torch.float32)
+    call("p2bw_kernel_attention_fwd", ptr(qkv), ptr(o), ptr(lse), b, s, nh, int(causal), stream())
+    ref_in = qkv.float().requires_grad_(True)
+    ro, rl = ref_attention(ref_in, b, s, nh, causal)
+    torch.cuda.synchronize()
+    assert (o.float() - ro).abs().max().item() < 2e-2          # bf16 output rounding
+    assert (lse - rl.detach()).abs().max().item() < 1e-2
+    dout = torch.randn(b * s, h, device="cuda", generator=g).to(torch.bfloat16)
+    dqkv = torch.empty_like(qkv)
+    delta = torch.empty(b * nh * s, device="cuda", dtype=torch.float32)
+    call("p2bw_kernel_attention_bwd", ptr(qkv), ptr(o), ptr(dout), ptr(lse), ptr(dqkv), ptr(delta), b, s, nh,
+         int(causal), stream())
+    ro.backward(dout.float())
+    torch.cuda.synchronize()
+    ref = ref_in.grad
+    err = (dqkv.float() - ref).abs().max().item()
+    assert err < 3e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("rows,h", [(300, 256), (1024, 768), (64, 1024), (33, 1920)])
+def test_layernorm_fwd_bwd_vs_torch(rows, h):
+    g = torch.Generator(device="cuda").manual_seed(rows + h)
+    x = (torch.randn(rows, h, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).to(torch.bfloat16)
+    bb = (0.1 * torch.randn(h, device="cuda", generator=g)).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    call("p2bw_kernel_layernorm_fwd", ptr(x), ptr(w), ptr(bb), ptr(y), ptr(mean), ptr(rstd), rows, h, stream())
+    xr = x.float().requires_grad_(True)
+    wr = w.float().requires_grad_(True)
+    br = bb.float().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (h,), wr, br, 1e-5)
+    torch.cuda.synchronize()
+    assert (y.float() - yr).abs().max().item() < 3e-2
+    dy = torch.randn(rows, h, device="cuda", generator=g).to(torch.bfloat16)
+    dres = torch.randn(rows, h, device="cuda", generator=g).to(torch.bfloat16)
+    dx = torch.empty_like(x)
+    dg = torch.full((h,), 5.0, device="cuda")
+    db = torch.full((h,), 5.0, device="cuda")
+    call("p2bw_kernel_layernorm_bwd", ptr(dy), ptr(x), ptr(mean), ptr(rstd), ptr(w), ptr(dres), ptr(dx), ptr(dg),
+         ptr(db), 0, rows, h, stream())  # accumulate onto 5.0
+    yr.backward(dy.float())
+    torch.cuda.synchronize()
+    ref_dx = xr.grad + dres.float()
+    assert (dx.float() - ref_dx).abs().max().item() < 3e-2 * max(1.0, ref_dx.abs().max().item())
+    assert (dg - 5.0 - wr.grad).abs().max().item() < 1e-2 * max(1.0, wr.grad.abs().max().item())
+    assert (db - 5.0 - br.grad).abs().max().item() < 1e-2 * max(1.0, br.grad.abs().max().item())
+
+
+@pytest.mark.parametrize("rows,vocab", [(64, 1000), (16, 51200), (130, 30522)])
+def test_softmax_xent_vs_torch(rows, vocab):
+    vp = (vocab + 127) // 128 * 128
+    g = torch.Generator(device="cuda").manual_seed(rows + vocab)
+    logits = (torch.randn(rows, vp, device="cuda", generator=g) * 3).to(torch.bfloat16)
+    tgt = torch.randint(0, vocab, (rows,), device="cuda", generator=g, dtype=torch.int32)
+    lr = logits.float()[:, :vocab].requires_grad_(True)
+    loss = torch.nn.functional.cross_entropy(lr, tgt.long(), reduction="none")
+    row_loss = torch.empty(rows, device="cuda")
+    call("p2bw_kernel_softmax_xent", ptr(logits), ptr(tgt), rows, vocab, vp, C.c_float(1.0 / rows), ptr(row_loss),
+         stream())
+    loss.mean().backward()
+    torch.cuda.synchronize()
+    assert (row_loss - loss.detach()).abs().max().item() < 1e-3 * max(1.0, loss.abs().max().item())
+    assert (logits.float()[:, :vocab] - lr.grad).abs().max().item() < 2e-3 / rows + 1e-5
+    assert logits.float()[:, vocab:].abs().max().item() == 0.0
