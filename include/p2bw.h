@@ -159,6 +159,16 @@ int p2bw_engine_run(p2bw_engine* eng, const p2bw_op* const* programs, const size
                     int snapshot_updates);
 /* generate_schedule(desc->policy, d, m, num_batches) followed by p2bw_engine_run. */
 int p2bw_engine_run_schedule(p2bw_engine* eng, int num_batches, int snapshot_updates);
+/* Streaming form of run_schedule: begin() installs generate_schedule(policy, d, m,
+ * num_batches); issue(t) issues every stage's ops up to and including its weight
+ * update of batch t (so batch t+1's data must already be set: 2BW forwards of the
+ * next batch are admitted before the update); finish() issues the remainder. */
+int p2bw_engine_begin(p2bw_engine* eng, int num_batches);
+int p2bw_engine_issue(p2bw_engine* eng, int upto_batch);
+int p2bw_engine_finish(p2bw_engine* eng);
+/* Device time between stage `stage`'s u0-th and u1-th WeightUpdate of the current
+ * run (CUDA events on the stage's stream; waits for u1). */
+int p2bw_engine_update_elapsed_ms(p2bw_engine* eng, int stage, int u0, int u1, double* ms);
 int p2bw_engine_sync(p2bw_engine* eng);
 int p2bw_engine_counters(p2bw_engine* eng, p2bw_counters* out);
 /* Weights created by a stage's update_index-th update of the last run (snapshots on). */

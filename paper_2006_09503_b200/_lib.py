@@ -69,6 +69,10 @@ def _signatures():
         ("p2bw_engine_set_data", i, [vp, vp, vp, i, i]),
         ("p2bw_engine_run", i, [vp, vp, vp, i]),
         ("p2bw_engine_run_schedule", i, [vp, i, i]),
+        ("p2bw_engine_begin", i, [vp, i]),
+        ("p2bw_engine_issue", i, [vp, i]),
+        ("p2bw_engine_finish", i, [vp]),
+        ("p2bw_engine_update_elapsed_ms", i, [vp, i, i, i, C.POINTER(C.c_double)]),
         ("p2bw_engine_sync", i, [vp]),
         ("p2bw_engine_counters", i, [vp, vp]),
         ("p2bw_engine_read_snapshot", i, [vp, i, i, vp, sz]),

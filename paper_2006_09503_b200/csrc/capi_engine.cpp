@@ -134,6 +134,41 @@ int p2bw_engine_run_schedule(p2bw_engine* eng, int num_batches, int snapshot_upd
     });
 }
 
+int p2bw_engine_begin(p2bw_engine* eng, int num_batches) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        const auto& c = e.config();
+        const auto programs = pipesim::generate_schedule(
+            static_cast<pipesim::PipelinePolicy>(c.policy), c.depth, c.microbatches, num_batches);
+        std::vector<p2bw::Program> progs;
+        for (const auto& p : programs) {
+            p2bw::Program prog;
+            for (const auto& op : p.ops)
+                prog.push_back({static_cast<int>(op.kind), op.microbatch, op.weight_version});
+            progs.push_back(std::move(prog));
+        }
+        e.set_snapshot_every_update(false);
+        e.begin(progs);
+    });
+}
+
+int p2bw_engine_issue(p2bw_engine* eng, int upto_batch) {
+    return guarded([&] { eng_of(eng).issue(upto_batch); });
+}
+
+int p2bw_engine_finish(p2bw_engine* eng) {
+    return guarded([&] { eng_of(eng).finish(); });
+}
+
+int p2bw_engine_update_elapsed_ms(p2bw_engine* eng, int stage, int u0, int u1, double* ms) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (ms == nullptr) throw std::invalid_argument("ms is NULL");
+        *ms = e.update_elapsed_ms(stage, u0, u1);
+    });
+}
+
 int p2bw_engine_sync(p2bw_engine* eng) {
     return guarded([&] { eng_of(eng).sync(); });
 }

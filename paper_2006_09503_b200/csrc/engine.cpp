@@ -148,22 +148,26 @@ void Engine::free_buffers() {
     }
 }
 
-namespace {
-
 // Per-run event tables: one event per (stage, microbatch, pass), created lazily
-// when the op is issued.  Destroying an event with pending waits is legal.
+// when the op is issued, plus a timing event after every WeightUpdate.
+// Destroying an event with pending waits is legal.
 struct EventTable {
     std::vector<std::map<int, cudaEvent_t>> fwd, bwd;
-    explicit EventTable(size_t d) : fwd(d), bwd(d) {}
+    std::vector<std::vector<cudaEvent_t>> upd;
+    explicit EventTable(size_t d) : fwd(d), bwd(d), upd(d) {}
     ~EventTable() {
         for (auto& m : fwd)
             for (auto& kv : m) cudaEventDestroy(kv.second);
         for (auto& m : bwd)
             for (auto& kv : m) cudaEventDestroy(kv.second);
+        for (auto& v : upd)
+            for (cudaEvent_t e : v) cudaEventDestroy(e);
     }
 };
 
-thread_local EventTable* g_events = nullptr;
+void Engine::EventTableDeleter::operator()(EventTable* t) const { delete t; }
+
+namespace {
 
 cudaEvent_t record(std::map<int, cudaEvent_t>& tab, int k, cudaStream_t s) {
     cudaEvent_t e;
@@ -182,7 +186,8 @@ void wait_on(const std::map<int, cudaEvent_t>& tab, int k, cudaStream_t s) {
 }  // namespace
 
 int Engine::resolve_version(const Stage& st, const OpRec& op) const {
-    return op.weight_version == P2BW_LATEST_VERSION ? st.updates_done : op.weight_version;
+    // Program versions count from the engine's version at begin() (0 on a fresh engine).
+    return op.weight_version == P2BW_LATEST_VERSION ? st.updates_done : st.version_base + op.weight_version;
 }
 
 bool Engine::ready(const Stage& st, const OpRec& op) const {
@@ -213,16 +218,16 @@ void Engine::issue_forward(Stage& st, const OpRec& op) {
                     " needs discarded weight version " + std::to_string(v));
     if (k < 1) throw Error("forward of microbatch " + std::to_string(k));
     const int sslot = (k - 1) % st.stash_slots;
-    if (s > 0) wait_on(g_events->fwd[s - 1], k, st.stream);
+    if (s > 0) wait_on(ev_->fwd[s - 1], k, st.stream);
     void* x_out = nullptr;
     if (s + 1 < d) {
         const Stage& nx = stages_[s + 1];
-        if (k > nx.stash_slots) wait_on(g_events->bwd[s + 1], k - nx.stash_slots, st.stream);
+        if (k > nx.stash_slots) wait_on(ev_->bwd[s + 1], k - nx.stash_slots, st.stream);
         x_out = nx.act_ring[(k - 1) % nx.stash_slots];
     }
     const void* x_in = s > 0 ? st.act_ring[sslot] : nullptr;
     st.model->forward(k, vit->second, sslot, x_in, x_out, st.stream);
-    record(g_events->fwd[s], k, st.stream);
+    record(ev_->fwd[s], k, st.stream);
     st.stash_version[k] = v;
     st.fwd_issued[k] = true;
 }
@@ -233,23 +238,23 @@ void Engine::issue_backward(Stage& st, const OpRec& op) {
     if (sit == st.stash_version.end())
         throw Error("backward before forward for microbatch " + std::to_string(k));  // :304
     const int v = sit->second;
-    if (op.weight_version != P2BW_LATEST_VERSION && op.weight_version != v)
+    if (op.weight_version != P2BW_LATEST_VERSION && st.version_base + op.weight_version != v)
         stats_.version_consistent = false;
     const int wslot = st.version_slot.at(v);
     const int sslot = (k - 1) % st.stash_slots;
     const void* g_in = nullptr;
     if (s + 1 < d) {
-        wait_on(g_events->bwd[s + 1], k, st.stream);
+        wait_on(ev_->bwd[s + 1], k, st.stream);
         g_in = st.grad_ring[(k - 1) % st.grad_slots];
     }
     void* g_out = nullptr;
     if (s > 0) {
         const Stage& pv = stages_[s - 1];
-        if (k > pv.grad_slots) wait_on(g_events->bwd[s - 1], k - pv.grad_slots, st.stream);
+        if (k > pv.grad_slots) wait_on(ev_->bwd[s - 1], k - pv.grad_slots, st.stream);
         g_out = pv.grad_ring[(k - 1) % pv.grad_slots];
     }
     st.model->backward(k, wslot, sslot, g_in, g_out, st.grad_count == 0, st.stream);
-    record(g_events->bwd[s], k, st.stream);
+    record(ev_->bwd[s], k, st.stream);
     st.grad_count += 1;
     st.stash_version.erase(sit);
     st.bwd_issued[k] = true;
@@ -303,6 +308,13 @@ void Engine::issue_update(Stage& st) {
     st.version_slot[st.updates_done] = dst_slot;
     prune_versions(st);
     st.grad_count = 0;
+    st.updates_issued += 1;
+    {
+        cudaEvent_t e;
+        check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+        check_cuda(cudaEventRecord(e, st.stream), "cudaEventRecord");
+        ev_->upd[static_cast<size_t>(st.index)].push_back(e);
+    }
     stats_.max_versions_held =
         std::max(stats_.max_versions_held, static_cast<int>(st.version_slot.size()));
     if (snapshots_on_) {
@@ -312,31 +324,39 @@ void Engine::issue_update(Stage& st) {
     }
 }
 
-void Engine::run(const std::vector<Program>& programs) {
+void Engine::begin(const std::vector<Program>& programs) {
     if (static_cast<int>(programs.size()) != cfg_.depth)
         throw Error("expected one program per stage");
-    EventTable events(stages_.size());
-    g_events = &events;
-    struct Reset {
-        ~Reset() { g_events = nullptr; }
-    } reset;
-    size_t total = 0;
+    sync();
+    ev_.reset(new EventTable(stages_.size()));
+    progs_ = programs;
+    total_ops_ = 0;
+    done_ops_ = 0;
+    for (const Program& p : progs_) total_ops_ += p.size();
     for (Stage& st : stages_) {
         st.ptr = 0;
         st.fwd_issued.clear();
         st.bwd_issued.clear();
         st.snaps.clear();
+        st.updates_issued = 0;
+        st.version_base = st.updates_done;
         DeviceGuard g(st.device);
         check_cuda(cudaEventRecord(st.t0, st.stream), "cudaEventRecord");
     }
-    for (const Program& p : programs) total += p.size();
-    size_t done = 0;
-    while (done < total) {
-        bool progress = false;
+}
+
+// Round-robin issue (semantics.cpp:270-361) until every stage has issued the
+// updates of batches 1..upto_batch of this run (or its whole program).
+void Engine::issue(int upto_batch) {
+    if (!ev_) throw Error("issue() before begin()");
+    const int per_batch = cfg_.policy == P2BW_POLICY_1F1B ? cfg_.microbatches : 1;
+    const long long target = static_cast<long long>(upto_batch) * per_batch;
+    while (true) {
+        bool progress = false, pending = false;
         for (Stage& st : stages_) {
-            const Program& prog = programs[static_cast<size_t>(st.index)];
+            const Program& prog = progs_[static_cast<size_t>(st.index)];
             DeviceGuard g(st.device);
-            while (st.ptr < prog.size()) {
+            while (st.ptr < prog.size() && st.updates_issued < target) {
                 const OpRec& op = prog[st.ptr];
                 if (!ready(st, op)) break;
                 switch (op.kind) {
@@ -351,17 +371,42 @@ void Engine::run(const std::vector<Program>& programs) {
                                     " is not executable by the stage executor");
                 }
                 st.ptr += 1;
-                done += 1;
+                done_ops_ += 1;
                 stats_.ops_executed += 1;
                 progress = true;
             }
+            if (st.ptr < prog.size() && st.updates_issued < target) pending = true;
         }
+        if (!pending) break;
         if (!progress) throw Error("dependency deadlock in toy-model replay");
     }
+}
+
+void Engine::finish() {
+    if (done_ops_ != total_ops_) issue(1 << 30);
     for (Stage& st : stages_) {
         DeviceGuard g(st.device);
         check_cuda(cudaEventRecord(st.t1, st.stream), "cudaEventRecord");
     }
+}
+
+void Engine::run(const std::vector<Program>& programs) {
+    begin(programs);
+    issue(1 << 30);
+    finish();
+}
+
+double Engine::update_elapsed_ms(int s, int u0, int u1) {
+    Stage& st = stages_.at(static_cast<size_t>(s));
+    const auto& ev = ev_->upd.at(static_cast<size_t>(s));
+    if (u0 < 1 || u1 > static_cast<int>(ev.size()) || u0 > u1)
+        throw Error("no update events for that range");
+    DeviceGuard g(st.device);
+    check_cuda(cudaEventSynchronize(ev[static_cast<size_t>(u1 - 1)]), "cudaEventSynchronize");
+    float ms = 0.0f;
+    check_cuda(cudaEventElapsedTime(&ms, ev[static_cast<size_t>(u0 - 1)], ev[static_cast<size_t>(u1 - 1)]),
+               "cudaEventElapsedTime");
+    return ms;
 }
 
 void Engine::sync() {

@@ -20,6 +20,8 @@
 
 namespace p2bw {
 
+struct EventTable;  // engine.cpp
+
 struct OpRec {
     int kind = 0;
     int microbatch = 0;
@@ -112,6 +114,14 @@ public:
 
     // Interpret one program per stage (asynchronous; call sync() to wait).
     void run(const std::vector<Program>& programs);
+    // Incremental form of run(): begin() installs the programs, issue(t) issues
+    // ops until every stage has issued the weight updates of batches 1..t,
+    // finish() issues the rest.  Lets a caller stream data in batch by batch.
+    void begin(const std::vector<Program>& programs);
+    void issue(int upto_batch);
+    void finish();
+    // Device time between a stage's u0-th and u1-th update of the current run.
+    double update_elapsed_ms(int stage, int u0, int u1);
     void sync();
     // Weights of stage s for the version created by its u-th update (0 = initial).
     void read_version(int s, int version, void* host, size_t bytes);
@@ -138,6 +148,8 @@ private:
         // host-side interpreter state (mirrors semantics.cpp:198-211)
         size_t ptr = 0;
         int updates_done = 0;
+        int updates_issued = 0;  // in the current run
+        int version_base = 0;    // updates_done at begin()
         std::map<int, int> version_slot;  // live version -> weight slot
         std::map<int, int> stash_version; // in-flight microbatch -> version
         int grad_count = 0;
@@ -154,8 +166,15 @@ private:
     void prune_versions(Stage& st);
     void free_buffers();
 
+    struct EventTableDeleter {
+        void operator()(struct EventTable* t) const;
+    };
+
     EngineConfig cfg_;
     std::vector<Stage> stages_;
+    std::vector<Program> progs_;
+    size_t total_ops_ = 0, done_ops_ = 0;
+    std::unique_ptr<struct EventTable, EventTableDeleter> ev_;
     RunStats stats_;
     bool snapshots_on_ = false;
 };

@@ -268,6 +268,20 @@ class Engine:
         ns = (C.c_size_t * len(arrs))(*[len(p.ops) for p in programs])
         _call("p2bw_engine_run", self.h, ptrs, ns, int(snapshots))
 
+    def begin(self, num_batches: int):
+        _call("p2bw_engine_begin", self.h, num_batches)
+
+    def issue(self, upto_batch: int):
+        _call("p2bw_engine_issue", self.h, upto_batch)
+
+    def finish(self):
+        _call("p2bw_engine_finish", self.h)
+
+    def update_elapsed_ms(self, stage: int, u0: int, u1: int) -> float:
+        out = C.c_double()
+        _call("p2bw_engine_update_elapsed_ms", self.h, stage, u0, u1, C.byref(out))
+        return out.value
+
     def sync(self):
         _call("p2bw_engine_sync", self.h)
 

@@ -105,4 +105,5 @@ def test_softmax_xent_vs_torch(rows, vocab):
     torch.cuda.synchronize()
     assert (row_loss - loss.detach()).abs().max().item() < 1e-3 * max(1.0, loss.abs().max().item())
     assert (logits.float()[:, :vocab] - lr.grad).abs().max().item() < 2e-3 / rows + 1e-5
-    assert logits.float()[:, vocab:].abs().max().item() == 0.0
+    if vp > vocab:
+        assert logits.float()[:, vocab:].abs().max().item() == 0.0
