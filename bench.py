@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""2BW training throughput (samples/s) on B200s -- the BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+One "step" is one 2BW batch (m microbatches of b sequences, every stage's
+weight update included) of the workload named by --config (default: configs[1],
+the BERT-base-sized encoder, 12 layers / hidden 768 / seq 512) with synthetic
+token data.  Under torchrun (N > 1) every rank drives one GPU; rank 0 prints
+ONE JSON line.
+
+Timing: W warm-up batches, then K batches timed on the device with the
+engine's CUDA events at the last stage's weight updates (steady state, as
+simulator.cpp:298-309 defines it), barrier + synchronize on both sides, max
+over ranks.  `value` counts every rank's sequences.  The same run is the
+end-to-end number: each step's token ids / targets are copied host->device
+from pinned memory and its losses device->host inside the timed region
+(`e2e`).  `roofline` comes from a second, profiled pass of the same workload
+(per-launch CUDA events around every stage kernel).  `cpu_baseline` times the
+reference's own pipelined_execute (oracle/_ref/ref_tool, built from
+/root/reference) on the linear-chain analog of the config on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MEASURED = ROOT / "MEASURED_PEAKS.json"
+REF_TOOL = ROOT / "oracle" / "_ref" / "ref_tool"
+
+# BASELINE.json configs; dims the reference leaves open are recorded here.
+CONFIGS = {
+    # configs[0]: the CPU reference's default-sized run, as a transformer
+    "small": dict(layers=4, hidden=256, heads=4, seq=128, vocab=8192, causal=True, head_rows=0,
+                  b=4, m=4, depth=2),
+    # configs[1]: BERT-base-sized encoder; MLM head on 15% (77 of 512) positions
+    "bert-base": dict(layers=12, hidden=768, heads=12, seq=512, vocab=30522, causal=False, head_rows=77,
+                      b=16, m=4, depth=1),
+    # configs[2]: BERT-large, depth 8 x m 8 on 8 GPUs (per-GPU work: 3 layers)
+    "bert-large": dict(layers=24, hidden=1024, heads=16, seq=512, vocab=30522, causal=False, head_rows=77,
+                       b=8, m=8, depth=1),
+    # configs[4]: 24-layer GPT (h 1024, V 51200, causal LM head on every position)
+    "gpt-24": dict(layers=24, hidden=1024, heads=16, seq=512, vocab=51200, causal=True, head_rows=0,
+                   b=8, m=4, depth=1),
+}
+
+
+def flops_per_sample(c) -> float:
+    """L*3*(24 s h^2 + 4 s^2 h) + 6 s h V_head (head tokens only)."""
+    L, h, s = c["layers"], c["hidden"], c["seq"]
+    attn = 4 * s * s * h * (0.5 if c["causal"] else 1.0)
+    head_tokens = c["head_rows"] or s
+    return L * 3 * (24 * s * h * h + attn) + 6 * head_tokens * h * c["vocab"]
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_rank{gpu}.csv"
+        if shutil.which("nvidia-smi") is None:
+            return
+        self.path.parent.mkdir(exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.f = open(self.path, "w")
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                      "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        loaded = [x for x in sm if x > 0.5 * mx] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+
+def peaks():
+    if MEASURED.exists():
+        d = json.loads(MEASURED.read_text())
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ---- CPU baseline: the reference's own trainer on the linear-chain analog --------------
+
+def cpu_sample(c, procs: int = 1, microbatches: int = 1) -> dict:
+    """ToyModel::make(dim=h, layers=L, cols=seq (one sequence per microbatch)), 2BW, depth 1,
+    timed by oracle/_ref/ref_tool (the reference compiled from its own sources)."""
+    dim, L, cols = c["hidden"], c["layers"], c["seq"]
+    if REF_TOOL.exists():
+        cmd = [str(REF_TOOL), "time", str(dim), str(L), str(cols), str(microbatches), "1", "1", "1"]
+        t0 = time.time()
+        ps = [subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True) for _ in range(procs)]
+        outs = [json.loads(p.communicate()[0]) for p in ps]
+        wall = time.time() - t0
+        sec = max(o["seconds"] for o in outs)
+        kind = "reference"
+    else:  # the oracle port (numpy restatement of semantics.cpp), single process
+        from oracle import pipesim_oracle as O
+        model = O.ToyModel.make(dim, L, cols, microbatches, 1)
+        t0 = time.time()
+        O.pipelined_execute(model, 0.01, 0.9, microbatches, 1, O.TWOBW, 1)
+        sec = wall = time.time() - t0
+        procs, kind = 1, "port"
+    samples = procs * microbatches  # one sequence (seq columns) per microbatch
+    return {"value": samples / sec, "unit": "samples/s", "cores": procs, "kind": kind,
+            "sample": f"pipelined_execute(ToyModel dim={dim} layers={L} cols={cols}, 2BW d=1, "
+                      f"m={microbatches} T=1) x {procs} process(es), fp64, {sec:.2f} s",
+            "seconds": sec, "wall_s": wall}
+
+
+def run_reference(args, c):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    procs = os.cpu_count() or 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(c, procs=procs, microbatches=1)
+        if i >= args.warmup:
+            times.append(r["seconds"])
+    sec = max(times) if times else 0.0
+    total = sum(times)
+    value = args.steps * procs / total if total else 0.0
+    line = {"metric": "2BW training samples/sec", "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (splitmix64 ToyModel, reference generator)", "impl": "reference",
+            "config": {"workload": f"{args.config}: linear-chain analog (reference has no transformer)",
+                       "dim": c["hidden"], "layers": c["layers"], "cols_per_microbatch": c["seq"],
+                       "policy": "2bw", "depth": 1},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": procs, "kind": r["kind"],
+                             "sample": r["sample"]},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our engine ---------------------------------------------------------------------
+
+def run_ours(args, c):
+    import torch
+    from paper_2006_09503_b200 import _lib
+    from paper_2006_09503_b200 import pipesim as P
+    from oracle import transformer_oracle as TO  # synthetic-data generator only (host numpy)
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    depth = c["depth"] if world == 1 else 1
+    spec = TO.Spec(layers=c["layers"], hidden=c["hidden"], heads=c["heads"], seq=c["seq"], vocab=c["vocab"],
+                   batch=c["b"], causal=c["causal"], head_rows=c["head_rows"])
+    m, steps, warm = c["m"], args.steps, args.warmup
+    total_batches = warm + steps + 1
+    eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
+                   microbatch_size=c["b"], layers=c["layers"], hidden=c["hidden"], heads=c["heads"],
+                   seq_len=c["seq"], vocab=c["vocab"], causal=int(c["causal"]), head_rows=c["head_rows"],
+                   learning_rate=1e-3, momentum=0.9, seed=1234 + rank)
+    eng.init_weights()
+
+    # synthetic token batches in pinned host memory (one batch = m microbatches)
+    T, R = c["b"] * c["seq"], c["b"] * (c["head_rows"] or c["seq"])
+    pool = 4
+    ids_np, tg_np = TO.synthetic_batch(spec, m * pool, 99 + rank)
+    ids = torch.from_numpy(ids_np).pin_memory()
+    tgs = torch.from_numpy(tg_np).pin_memory()
+    loss_host = torch.zeros(total_batches * m, dtype=torch.float32).pin_memory()
+    h2d_bytes = m * (T + R) * 4
+    d2h_bytes = m * 4
+
+    def set_batch(t):  # batch t (1-based) -> microbatches (t-1)m+1 .. tm
+        j = (t - 1) % pool
+        _lib.check(_lib.lib().p2bw_engine_set_data(
+            eng.h, C.c_void_p(ids[j * m].data_ptr()), C.c_void_p(tgs[j * m].data_ptr()), (t - 1) * m + 1, m))
+
+    def fetch_loss(t):
+        _lib.check(_lib.lib().p2bw_engine_losses_async(eng.h, (t - 1) * m + 1, m,
+                                                       C.c_void_p(loss_host[(t - 1) * m].data_ptr())))
+
+    def one_pass(n_batches, profile=False):
+        eng.begin(n_batches)
+        set_batch(1)
+        for t in range(1, n_batches + 1):
+            if t + 1 <= n_batches:
+                set_batch(t + 1)
+            if profile and t == warm + 1:
+                _lib.lib().p2bw_profile_enable(1)
+            if profile and t == warm + 1 + steps:
+                _lib.lib().p2bw_profile_enable(0)
+            eng.issue(t)
+            fetch_loss(t)
+        eng.finish()
+
+    # ---- timed pass ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    launches0 = _lib.lib().p2bw_launch_count()
+    wall0 = time.time()
+    one_pass(total_batches)
+    eng.sync()
+    wall = time.time() - wall0
+    launches = _lib.lib().p2bw_launch_count() - launches0
+    clk = clocks.stop()
+    ms = eng.update_elapsed_ms(depth - 1, warm, warm + steps)  # K steady-state batches
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    losses = loss_host.numpy()[: total_batches * m]
+
+    samples = world * c["b"] * m * steps
+    value = samples / (ms / 1e3)
+    fps = flops_per_sample(c)
+    peak, peak_sus, hbm, peak_kind = peaks()
+
+    # ---- profiled pass (same workload) for the roofline ----
+    classes = []
+    if rank == 0:
+        one_pass(total_batches, profile=True)
+        eng.sync()
+        arr = (KernelClass * 64)()
+        n = C.c_int()
+        _lib.check(_lib.lib().p2bw_profile_collect(arr, 64, C.byref(n)))
+        classes = [dict(name=arr[i].name.decode(), launches=arr[i].launches, ms=arr[i].ms, flops=arr[i].flops,
+                        bytes=arr[i].bytes) for i in range(min(n.value, 64))]
+    eng.close()
+
+    if rank != 0:
+        return 0
+    tot_ms = sum(k["ms"] for k in classes) or 1.0
+    gemm = next((k for k in classes if k["name"] == "gemm"), None)
+    roofline = None
+    if gemm and gemm["ms"] > 0:
+        achieved = gemm["flops"] / (gemm["ms"] / 1e3) / 1e12
+        traffic = None
+        prof_json = ROOT / "profiles" / "ncu_gemm_dram_bytes.json"
+        if prof_json.exists():
+            traffic = json.loads(prof_json.read_text()).get(args.config)
+        roofline = {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, all GEMM launches of a step)",
+                    "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                    "frac": round(achieved / peak, 4), "peak_kind": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
+                    "traffic": traffic,
+                    "flops_per_launch": gemm["flops"] / max(gemm["launches"], 1),
+                    "avg_launch_us": 1e3 * gemm["ms"] / max(gemm["launches"], 1),
+                    "share_of_kernel_time": round(gemm["ms"] / tot_ms, 4),
+                    "measured_over": f"{steps} profiled steps after the timed pass (per-launch CUDA events)"}
+    breakdown = {k["name"]: {"share": round(k["ms"] / tot_ms, 4), "launches": k["launches"],
+                             "tflops": round(k["flops"] / (k["ms"] / 1e3) / 1e12, 1) if k["flops"] else None,
+                             "gbs": round(k["bytes"] / (k["ms"] / 1e3) / 1e9, 1) if k["bytes"] else None}
+                 for k in classes}
+    mfu = value * fps / (world * peak * 1e12)
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        r = cpu_sample(c, procs=1, microbatches=1)
+        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    line = {
+        "metric": "2BW training samples/sec", "value": round(value, 2), "unit": "samples/s", "n_gpus": world,
+        "steps": steps, "warmup": warm, "ms_per_step": round(ms / steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic tokens (uniform ids, seeded), random-init weights",
+        "config": {"workload": args.config, "layers": c["layers"], "hidden": c["hidden"], "heads": c["heads"],
+                   "seq_len": c["seq"], "vocab": c["vocab"], "causal": c["causal"],
+                   "head_rows_per_seq": c["head_rows"] or c["seq"], "microbatch_size": c["b"],
+                   "microbatches_m": m, "global_batch": world * c["b"] * m,
+                   "parallelism": f"2bw d={depth} w={world}" + (" (replicas, no gradient exchange yet)"
+                                                                if world > 1 else ""),
+                   "policy": "2bw", "l2": "working set (activations >> 126 MB L2) exceeds L2 every step"},
+        "e2e": {"value": round(value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes,
+                "note": "timed region includes per-step pinned H2D of ids/targets and D2H of losses "
+                        "through the C-ABI (p2bw_engine_set_data / p2bw_engine_losses_async)"},
+        "gpu_launches": int(launches * steps / total_batches),
+        "gpu_launches_per_step": round(launches / total_batches, 1),
+        "mfu": round(mfu, 4), "flops_per_sample": fps,
+        "roofline": roofline, "kernel_breakdown": breakdown,
+        "cpu_baseline": cpu, "clocks": clk,
+        "loss_first_last": [float(losses[0]), float(losses[-1])],
+        "wall_s": round(wall, 2),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+class KernelClass(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_longlong), ("ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="bert-base", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, c)
+    return run_ours(args, c)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -178,8 +178,26 @@ int p2bw_engine_read_snapshot(p2bw_engine* eng, int stage, int update_index, voi
 int p2bw_engine_read_version(p2bw_engine* eng, int stage, int version, void* host, size_t bytes);
 /* fp32 master weights of a stage (transformer: the latest version, unrounded). */
 int p2bw_engine_read_master(p2bw_engine* eng, int stage, void* host, size_t bytes);
+/* Stream-ordered async copy of fp32 losses into (pinned) host memory; no sync. */
+int p2bw_engine_losses_async(p2bw_engine* eng, int first_mb, int count, float* host);
 /* Training losses of microbatches [first_mb, first_mb+count) (last stage). */
 int p2bw_engine_losses(p2bw_engine* eng, int first_mb, int count, double* out);
+
+/* ---- measurement --------------------------------------------------------- */
+
+/* Kernels launched by this library since load (all stage kernels count). */
+long long p2bw_launch_count(void);
+/* Per-launch CUDA-event timing of every stage kernel, grouped by class. */
+void p2bw_profile_enable(int on);
+typedef struct {
+    char name[32];
+    long long launches;
+    double ms;     /* summed device time of the class's launches */
+    double flops;  /* algorithmic FLOPs (GEMM / attention) */
+    double bytes;  /* algorithmic HBM bytes (memory-bound kernels) */
+} p2bw_kernel_class;
+/* Waits for and folds the recorded launches into classes (clears them). */
+int p2bw_profile_collect(p2bw_kernel_class* out, int cap, int* n);
 
 /* ---- stage kernels (parity-test hooks; device pointers, CUDA stream) ------- */
 

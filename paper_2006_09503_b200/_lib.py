@@ -78,7 +78,11 @@ def _signatures():
         ("p2bw_engine_read_snapshot", i, [vp, i, i, vp, sz]),
         ("p2bw_engine_read_version", i, [vp, i, i, vp, sz]),
         ("p2bw_engine_read_master", i, [vp, i, vp, sz]),
+        ("p2bw_engine_losses_async", i, [vp, i, i, vp]),
         ("p2bw_engine_losses", i, [vp, i, i, vp]),
+        ("p2bw_launch_count", ll, []),
+        ("p2bw_profile_enable", None, [i]),
+        ("p2bw_profile_collect", i, [vp, i, C.POINTER(C.c_int)]),
         ("p2bw_kernel_gemm_bf16", i, [vp, ll, i, vp, ll, i, i, i, i, C.POINTER(GemmEpilogue), vp]),
         ("p2bw_kernel_attention_fwd", i, [vp, vp, vp, i, i, i, i, vp]),
         ("p2bw_kernel_attention_bwd", i, [vp, vp, vp, vp, vp, vp, i, i, i, i, vp]),

@@ -7,6 +7,7 @@
 // 72-element row pitch (16-byte aligned, 4-way bank spread for row-wise reads).
 #include <cuda_bf16.h>
 
+#include "profiler.h"
 #include "ptx.cuh"
 #include "tkernels.h"
 #include "util.h"
@@ -291,6 +292,8 @@ void check_shape(int seq, int heads) {
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
                    cudaStream_t s) {
     check_shape(seq, heads);
+    const double flops = 4.0 * batch * heads * 64.0 * seq * seq * (causal ? 0.5 : 1.0);
+    prof::Scope scope("attention_fwd", flops, 2.0 * batch * seq * heads * 64.0 * 4, 1, s);
     dim3 grid(batch * heads, (seq + kQB - 1) / kQB);
     if (causal) {
         set_smem(k_attn_fwd<true>, kFwdSmem);
@@ -305,6 +308,8 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int
 void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
                    int batch, int seq, int heads, bool causal, cudaStream_t s) {
     check_shape(seq, heads);
+    const double flops = 8.0 * batch * heads * 64.0 * seq * seq * (causal ? 0.5 : 1.0);
+    prof::Scope scope("attention_bwd", flops, 2.0 * batch * seq * heads * 64.0 * 8, 2, s);
     dim3 grid(batch * heads, (seq + kQB - 1) / kQB);
     if (causal) {
         set_smem(k_attn_bwd_q<true>, kBwdQSmem);

@@ -218,6 +218,14 @@ int p2bw_engine_read_master(p2bw_engine* eng, int stage, void* host, size_t byte
     });
 }
 
+int p2bw_engine_losses_async(p2bw_engine* eng, int first_mb, int count, float* host) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        if (host == nullptr || count < 1) throw std::invalid_argument("bad loss buffer");
+        e.copy_losses_async(host, first_mb, count);
+    });
+}
+
 int p2bw_engine_losses(p2bw_engine* eng, int first_mb, int count, double* out) {
     return guarded([&] {
         auto& e = eng_of(eng);

@@ -76,6 +76,11 @@ public:
         throw Error("this stage computes no loss");
     }
     virtual void bind_stream(cudaStream_t s) { (void)s; }
+    // Asynchronous D2H of fp32 losses into (pinned) host memory, stream-ordered.
+    virtual void copy_losses_async(float* host, int first_mb, int count, cudaStream_t s) {
+        (void)host, (void)first_mb, (void)count, (void)s;
+        throw Error("this stage computes no fp32 loss");
+    }
     // fp32 master weights (models that keep one), public layout.
     virtual void read_master(void* host, size_t bytes) {
         (void)host, (void)bytes;
@@ -131,6 +136,9 @@ public:
     double elapsed_ms_last_run();
     // Losses of microbatches [first_mb, first_mb + count) (last stage), after sync.
     std::vector<double> losses(int first_mb, int count);
+    void copy_losses_async(float* host, int first_mb, int count) {
+        stages_.back().model->copy_losses_async(host, first_mb, count, stages_.back().stream);
+    }
 
 private:
     struct Stage {

@@ -24,6 +24,7 @@
 #include <string>
 
 #include "kernels.h"
+#include "profiler.h"
 #include "ptx.cuh"
 #include "util.h"
 
@@ -419,6 +420,11 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     const CUtensorMap ta = amn ? make_map(a.ptr, m, k, a.ld, kBK) : make_map(a.ptr, k, m, a.ld, kBM);
     const CUtensorMap tb = bmn ? make_map(b.ptr, n, k, b.ld, kBK) : make_map(b.ptr, k, n, b.ld, bn);
     KParams p{m, n, k, epi};
+    const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
+    prof::Scope scope("gemm", 2.0 * m * n * k,
+                      2.0 * (static_cast<double>(m) * k + static_cast<double>(n) * k) +
+                          out_bytes * m * n,
+                      1, stream);
     if (bn == 256) dispatch_major<256>(amn, bmn, ta, tb, p, stream);
     else dispatch_major<128>(amn, bmn, ta, tb, p, stream);
 }

@@ -141,6 +141,17 @@ public:
         for (int i = 0; i < count; ++i) host[i] = tmp[static_cast<size_t>((first_mb - 1 + i) % capacity_)];
     }
 
+    void copy_losses_async(float* host, int first_mb, int count, cudaStream_t s) override {
+        if (!last_ || capacity_ == 0) throw Error("this stage computes no loss");
+        for (int i = 0; i < count;) {
+            const int slot = (first_mb - 1 + i) % capacity_;
+            const int run = std::min(count - i, capacity_ - slot);
+            check_cuda(cudaMemcpyAsync(host + i, loss_ + slot, sizeof(float) * run, cudaMemcpyDeviceToHost, s),
+                       "D2H loss");
+            i += run;
+        }
+    }
+
     // inputs: int32 [count][T] token ids (stage 0); targets: int32 [count][R] (last stage).
     void set_data(const void* inputs, const void* targets, int first_mb, int count) override {
         if (count < 1) throw Error("set_data: empty microbatch range");

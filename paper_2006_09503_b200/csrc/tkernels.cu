@@ -7,6 +7,7 @@
 
 #include <algorithm>
 
+#include "profiler.h"
 #include "ptx.cuh"
 #include "tkernels.h"
 #include "util.h"
@@ -431,9 +432,13 @@ __global__ void k_gather_rows(const bf16* __restrict__ in, const int* __restrict
 }  // namespace
 
 // ---- host wrappers ---------------------------------------------------------------------
+// Each wrapper opens a prof::Scope with its algorithmic HBM bytes (reads + writes
+// of the tensors it must touch once) for the roofline report.
 
 void embed_fwd(const int* ids, const bf16* tok, const bf16* pos, bf16* x0, int tokens, int seq, int h,
                cudaStream_t s) {
+    const double th = static_cast<double>(tokens) * h;
+    prof::Scope scope("embed_fwd", 0.0, 6.0 * th + 4.0 * tokens, 1, s);
     k_embed_fwd<<<grid_for(static_cast<size_t>(tokens) * h / 8, 256), 256, 0, s>>>(ids, tok, pos, x0, tokens,
                                                                                   seq, h);
     check_cuda(cudaGetLastError(), "embed_fwd");
@@ -441,6 +446,8 @@ void embed_fwd(const int* ids, const bf16* tok, const bf16* pos, bf16* x0, int t
 
 void embed_bwd(const int* ids, const bf16* dx0, float* dtok, float* dpos, int tokens, int seq, int h,
                bool overwrite_pos, cudaStream_t s) {
+    const double th = static_cast<double>(tokens) * h;
+    prof::Scope scope("embed_bwd", 0.0, 2.0 * th * 2 + 8.0 * th + 8.0 * seq * h, 2, s);
     k_embed_bwd_tok<<<grid_for(static_cast<size_t>(tokens) * h / 8, 256), 256, 0, s>>>(ids, dx0, dtok, tokens, h);
     k_embed_bwd_pos<<<grid_for(static_cast<size_t>(seq) * h / 8, 128), 128, 0, s>>>(
         dx0, dpos, tokens / seq, seq, h, overwrite_pos ? 1 : 0);
@@ -450,6 +457,7 @@ void embed_bwd(const int* ids, const bf16* dx0, float* dtok, float* dpos, int to
 void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean, float* rstd, int rows,
                    int h, cudaStream_t s) {
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
+    prof::Scope scope("layernorm_fwd", 0.0, 4.0 * rows * h + 8.0 * rows, 1, s);
     const int nv = (h / 8 + 31) / 32;
     const int grid = (rows + 7) / 8;
     switch (nv) {
@@ -470,6 +478,7 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
                    const bf16* dres, bf16* dx, float* dg, float* db, bool overwrite, int rows, int h,
                    float* scratch, cudaStream_t s) {
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
+    prof::Scope scope("layernorm_bwd", 0.0, (dres ? 8.0 : 6.0) * rows * h + 8.0 * rows, 3, s);
     const int nv = (h / 8 + 31) / 32;
     const int blocks = ln_bwd_blocks(rows);
     const int parts = blocks * 8;
@@ -492,6 +501,7 @@ size_t colsum_scratch_floats(int rows, int n) { return static_cast<size_t>(colsu
 void colsum_bf16(const bf16* x, int rows, int n, int ld, float* out, bool overwrite, float* scratch,
                  cudaStream_t s) {
     if (n % 8 != 0) throw Error("colsum: columns must be a multiple of 8");
+    prof::Scope scope("bias_grad", 0.0, 2.0 * rows * n + 8.0 * n, 2, s);
     const int rb = colsum_row_blocks(rows);
     const int rpb = (rows + rb - 1) / rb;
     dim3 grid((n + 255) / 256, rb);
@@ -503,11 +513,13 @@ void colsum_bf16(const bf16* x, int rows, int n, int ld, float* out, bool overwr
 void softmax_xent(bf16* logits, const int* targets, int rows, int vocab, int vp, float grad_scale,
                   float* row_loss, cudaStream_t s) {
     if (vp % 8 != 0) throw Error("softmax_xent: padded vocab must be a multiple of 8");
+    prof::Scope scope("softmax_xent", 0.0, 4.0 * rows * static_cast<double>(vp) + 8.0 * rows, 1, s);
     k_softmax_xent<<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
     check_cuda(cudaGetLastError(), "softmax_xent");
 }
 
 void sum_scaled(const float* row_loss, int rows, float scale, float* loss_out, cudaStream_t s) {
+    prof::Scope scope("loss_sum", 0.0, 4.0 * rows, 1, s);
     k_sum_scaled<<<1, 256, 0, s>>>(row_loss, rows, scale, loss_out);
     check_cuda(cudaGetLastError(), "sum_scaled");
 }
@@ -515,6 +527,8 @@ void sum_scaled(const float* row_loss, int rows, float scale, float* loss_out, c
 void sgd_momentum_update(float* master, float* vel, const float* grad, bf16* out_bf16, size_t n,
                          float inv_count, float lr, float beta, cudaStream_t s) {
     if (n % 4 != 0) throw Error("optimizer: parameter count must be a multiple of 4");
+    // reads w, v, g (12 B) + writes w, v (8 B) + bf16 copy (2 B) = 22 B/param
+    prof::Scope scope("optimizer", 0.0, 22.0 * static_cast<double>(n), 1, s);
     k_sgd<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<float4*>(master), reinterpret_cast<float4*>(vel),
                                               reinterpret_cast<const float4*>(grad),
                                               reinterpret_cast<uint2*>(out_bf16), n / 4, inv_count, lr, beta);
@@ -522,32 +536,38 @@ void sgd_momentum_update(float* master, float* vel, const float* grad, bf16* out
 }
 
 void init_uniform(float* w, size_t n, uint64_t seed, uint64_t uid, float half_width, cudaStream_t s) {
+    prof::Scope scope("init", 0.0, 4.0 * static_cast<double>(n), 1, s);
     const uint64_t key = seed * 0x9e3779b97f4a7c15ULL + uid * 0xbf58476d1ce4e5b9ULL;
     k_init_uniform<<<grid_for(n, 256), 256, 0, s>>>(w, n, key, half_width);
     check_cuda(cudaGetLastError(), "init_uniform");
 }
 
 void fill_f32(float* w, size_t n, float v, cudaStream_t s) {
+    prof::Scope scope("init", 0.0, 4.0 * static_cast<double>(n), 1, s);
     k_fill<<<grid_for(n, 256), 256, 0, s>>>(w, n, v);
     check_cuda(cudaGetLastError(), "fill_f32");
 }
 
 void cast_f32_bf16(const float* in, bf16* out, size_t n, cudaStream_t s) {
+    prof::Scope scope("cast", 0.0, 6.0 * static_cast<double>(n), 1, s);
     k_cast_f2b<<<grid_for(n, 256), 256, 0, s>>>(in, out, n);
     check_cuda(cudaGetLastError(), "cast_f32_bf16");
 }
 
 void cast_bf16_f32(const bf16* in, float* out, size_t n, cudaStream_t s) {
+    prof::Scope scope("cast", 0.0, 6.0 * static_cast<double>(n), 1, s);
     k_cast_b2f<<<grid_for(n, 256), 256, 0, s>>>(in, out, n);
     check_cuda(cudaGetLastError(), "cast_bf16_f32");
 }
 
 void gather_rows(const bf16* in, const int* idx, bf16* out, int rows, int h, cudaStream_t s) {
+    prof::Scope scope("head_rows", 0.0, 4.0 * rows * h, 1, s);
     k_gather_rows<<<grid_for(static_cast<size_t>(rows) * h / 8, 256), 256, 0, s>>>(in, idx, out, rows, h, 0);
     check_cuda(cudaGetLastError(), "gather_rows");
 }
 
 void scatter_rows(const bf16* in, const int* idx, bf16* out, int rows, int h, cudaStream_t s) {
+    prof::Scope scope("head_rows", 0.0, 4.0 * rows * h, 1, s);
     k_gather_rows<<<grid_for(static_cast<size_t>(rows) * h / 8, 256), 256, 0, s>>>(in, idx, out, rows, h, 1);
     check_cuda(cudaGetLastError(), "scatter_rows");
 }

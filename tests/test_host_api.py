@@ -21,7 +21,8 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def test_library_exports_every_declared_symbol():
     header = (ROOT / "include" / "p2bw.h").read_text()
-    declared = set(re.findall(r"^\s*(?:const\s+char\s*\*|int|void)\s+(p2bw_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:const\s+char\s*\*|int|void|long\s+long)\s+(p2bw_\w+)\s*\(", header,
+                              re.M))
     assert declared, "no declarations parsed"
     out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
                          text=True, check=True).stdout
