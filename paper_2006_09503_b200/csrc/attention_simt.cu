@@ -294,6 +294,10 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int
     check_shape(seq, heads);
     const double flops = 4.0 * batch * heads * 64.0 * seq * seq * (causal ? 0.5 : 1.0);
     prof::Scope scope("attention_fwd", flops, 2.0 * batch * seq * heads * 64.0 * 4, 1, s);
+    if (attention_tc_supported(seq)) {  // tensor-core path: seq in {128, 256, 384, 512}
+        attention_fwd_tc(qkv, o, lse, batch, seq, heads, causal, s);
+        return;
+    }
     dim3 grid(batch * heads, (seq + kQB - 1) / kQB);
     if (causal) {
         set_smem(k_attn_fwd<true>, kFwdSmem);
@@ -305,10 +309,19 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int
     check_cuda(cudaGetLastError(), "attention_fwd");
 }
 
+size_t attention_bwd_scratch_floats(int batch, int seq, int heads) {
+    return attention_tc_supported(seq) ? attention_bwd_tc_scratch_floats(batch, seq, heads) : 0;
+}
+
 void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
-                   int batch, int seq, int heads, bool causal, cudaStream_t s) {
+                   float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s) {
     check_shape(seq, heads);
     const double flops = 8.0 * batch * heads * 64.0 * seq * seq * (causal ? 0.5 : 1.0);
+    if (attention_tc_supported(seq)) {  // tensor-core path
+        prof::Scope scope("attention_bwd", flops, 2.0 * batch * seq * heads * 64.0 * 8, 3, s);
+        attention_bwd_tc(qkv, o, dout, lse, dqkv, delta, scratch, batch, seq, heads, causal, s);
+        return;
+    }
     prof::Scope scope("attention_bwd", flops, 2.0 * batch * seq * heads * 64.0 * 8, 2, s);
     dim3 grid(batch * heads, (seq + kQB - 1) / kQB);
     if (causal) {

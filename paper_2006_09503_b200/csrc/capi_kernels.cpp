@@ -48,8 +48,13 @@ extern "C" int p2bw_kernel_attention_bwd(const void* qkv, const void* o, const v
                                          void* dqkv, void* delta, int batch, int seq, int heads, int causal,
                                          void* stream) {
     return guarded([&] {
+        float* scratch = nullptr;
+        const size_t n = attention_bwd_scratch_floats(batch, seq, heads);
+        if (n) check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch), n * sizeof(float), as_stream(stream)),
+                          "cudaMallocAsync");
         attention_bwd(cb(qkv), cb(o), cb(dout), static_cast<const float*>(lse), mb(dqkv),
-                      static_cast<float*>(delta), batch, seq, heads, causal != 0, as_stream(stream));
+                      static_cast<float*>(delta), scratch, batch, seq, heads, causal != 0, as_stream(stream));
+        if (n) check_cuda(cudaFreeAsync(scratch, as_stream(stream)), "cudaFreeAsync");
     });
 }
 

@@ -34,6 +34,7 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kThreads = 256;
+constexpr int kEpiBuf = 32 * 128;  // one staging buffer: 32 rows x 128 B (TMA box, SW128)
 
 template <int BN>
 struct GemmCfg {
@@ -42,7 +43,8 @@ struct GemmCfg {
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = 2 * BN;  // 256 or 512: a power of two
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kEpiBytes = 4 * 2 * kEpiBuf;  // 4 epilogue warps x 2 buffers
+    static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ float gelu_fwd(float x) {
@@ -65,103 +67,41 @@ struct KParams {
     GemmEpilogue epi;
 };
 
-// One 32-column chunk of the epilogue for one output row (this thread's TMEM lane).
-template <EpiKind kKind>
-__device__ __forceinline__ void epilogue_chunk(const KParams& p, int64_t row, int col,
-                                               const uint32_t (&v)[32]) {
-    const GemmEpilogue& e = p.epi;
-    if constexpr (kKind == EpiKind::StoreF32) {
-        float* d = static_cast<float*>(e.d) + row * e.ldd + col;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-            float4 acc = make_float4(__uint_as_float(v[j]) * e.alpha, __uint_as_float(v[j + 1]) * e.alpha,
-                                     __uint_as_float(v[j + 2]) * e.alpha,
-                                     __uint_as_float(v[j + 3]) * e.alpha);
-            if (e.beta != 0.0f) {
-                const float4 old = *reinterpret_cast<const float4*>(d + j);
-                acc.x += e.beta * old.x;
-                acc.y += e.beta * old.y;
-                acc.z += e.beta * old.z;
-                acc.w += e.beta * old.w;
-            }
-            *reinterpret_cast<float4*>(d + j) = acc;
-        }
-    } else if constexpr (kKind == EpiKind::DGeluBF16) {
-        bf16* d = static_cast<bf16*>(e.d) + row * e.ldd + col;
-        const bf16* u = e.aux + row * e.ldd + col;
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-            const uint4 uu = *reinterpret_cast<const uint4*>(u + j);
-            const uint32_t uw[4] = {uu.x, uu.y, uu.z, uu.w};
-            uint32_t out[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float2 uf = ptx::unpack_bf16x2(uw[q]);
-                const float a0 = __uint_as_float(v[j + 2 * q]) * e.alpha * gelu_bwd(uf.x);
-                const float a1 = __uint_as_float(v[j + 2 * q + 1]) * e.alpha * gelu_bwd(uf.y);
-                out[q] = ptx::pack_bf16x2(a0, a1);
-            }
-            *reinterpret_cast<uint4*>(d + j) = make_uint4(out[0], out[1], out[2], out[3]);
-        }
-    } else {
-        bf16* d = static_cast<bf16*>(e.d) + row * e.ldd + col;
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-            float x[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) x[q] = __uint_as_float(v[j + q]) * e.alpha;
-            if (e.bias != nullptr) {
-                const uint4 bb = *reinterpret_cast<const uint4*>(e.bias + col + j);
-                const uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 bf = ptx::unpack_bf16x2(bw[q]);
-                    x[2 * q] += bf.x;
-                    x[2 * q + 1] += bf.y;
-                }
-            }
-            if (e.gelu) {
-                if (e.preact != nullptr) {
-                    uint32_t pre[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) pre[q] = ptx::pack_bf16x2(x[2 * q], x[2 * q + 1]);
-                    *reinterpret_cast<uint4*>(e.preact + row * e.ldd + col + j) =
-                        make_uint4(pre[0], pre[1], pre[2], pre[3]);
-                    // GELU is applied to the bf16-rounded pre-activation so that the
-                    // backward (which only sees the stored bf16 u) differentiates the
-                    // exact function the forward evaluated.
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float2 r = ptx::unpack_bf16x2(pre[q]);
-                        x[2 * q] = r.x;
-                        x[2 * q + 1] = r.y;
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) x[q] = gelu_fwd(x[q]);
-            }
-            if (e.residual != nullptr) {
-                const uint4 rr = *reinterpret_cast<const uint4*>(e.residual + row * e.ldr + col + j);
-                const uint32_t rw[4] = {rr.x, rr.y, rr.z, rr.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 rf = ptx::unpack_bf16x2(rw[q]);
-                    x[2 * q] += rf.x;
-                    x[2 * q + 1] += rf.y;
-                }
-            }
-            uint32_t out[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) out[q] = ptx::pack_bf16x2(x[2 * q], x[2 * q + 1]);
-            *reinterpret_cast<uint4*>(d + j) = make_uint4(out[0], out[1], out[2], out[3]);
-        }
-    }
+// Output / side-input tensor maps of the epilogue (32-row boxes, 128 B rows, SW128).
+struct EpiMaps {
+    CUtensorMap d;    // D: bf16 box 64x32, or fp32 box 32x32
+    CUtensorMap pre;  // GELU pre-activation copy (bf16)
+    CUtensorMap aux;  // residual (StoreBF16) or u (DGeluBF16), bf16
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(ptx::smem_u32(src))
+                 : "memory");
 }
+
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(ptx::smem_u32(src))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+// Byte offset of 16-byte chunk j of row r in a 128 B-row SW128 staging buffer.
+__device__ __forceinline__ int swz(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
 
 template <int BN, bool kAMN, bool kBMN, EpiKind kKind>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                   const __grid_constant__ CUtensorMap tmap_b, const KParams p) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                   const __grid_constant__ EpiMaps em, const KParams p) {
     using Cfg = GemmCfg<BN>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -169,11 +109,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* s_a = smem;
     uint8_t* s_b = smem + S * Cfg::kABytes;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+    uint8_t* s_epi = smem + S * Cfg::kStageBytes;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_epi + Cfg::kEpiBytes);
     uint64_t* empty_bar = full_bar + S;
     uint64_t* tfull_bar = empty_bar + S;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* aux_bar = tempty_bar + 2;    // [4] per epilogue warp
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -185,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmap_a);
         ptx::tma_prefetch_desc(&tmap_b);
+        ptx::tma_prefetch_desc(&em.d);
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
             ptx::mbar_init(&empty_bar[s], 1);
@@ -193,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&tfull_bar[i], 1);
             ptx::mbar_init(&tempty_bar[i], 4);
         }
+        for (int i = 0; i < 4; ++i) ptx::mbar_init(&aux_bar[i], 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -217,16 +161,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (kAMN) {
 #pragma unroll
                         for (int j = 0; j < kBM / 64; ++j)
-                            ptx::tma_load_2d(da + j * 64 * kBK * 2, &tmap_a, &full_bar[stage],
-                                             m0 + j * 64, k0);
+                            ptx::tma_load_2d(da + j * 64 * kBK * 2, &tmap_a, &full_bar[stage], m0 + j * 64, k0);
                     } else {
                         ptx::tma_load_2d(da, &tmap_a, &full_bar[stage], k0, m0);
                     }
                     if constexpr (kBMN) {
 #pragma unroll
                         for (int j = 0; j < BN / 64; ++j)
-                            ptx::tma_load_2d(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage],
-                                             n0 + j * 64, k0);
+                            ptx::tma_load_2d(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage], n0 + j * 64, k0);
                     } else {
                         ptx::tma_load_2d(db, &tmap_b, &full_bar[stage], k0, n0);
                     }
@@ -281,24 +223,145 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        // Epilogue: warp q owns tile rows [32q, 32q+32) (its TMEM lane quarter).  Each
+        // chunk of 128 B per row (64 bf16 / 32 fp32 columns) goes TMEM -> registers ->
+        // fused math -> swizzled SMEM -> one TMA bulk-tensor store (or reduce-add).
+        const int q = warp & 3;
+        const GemmEpilogue& e = p.epi;
+        uint8_t* ebuf = s_epi + q * 2 * kEpiBuf;
+        constexpr bool kF32 = kKind == EpiKind::StoreF32;
+        constexpr int W = kF32 ? 32 : 64;  // columns per chunk
+        const bool need_aux = kKind == EpiKind::DGeluBF16 || (kKind == EpiKind::StoreBF16 && e.residual != nullptr);
+        const bool two_out = kKind == EpiKind::StoreBF16 && e.gelu && e.preact != nullptr;
+        const bool reduce = kF32 && e.beta != 0.0f;
+        uint32_t aux_phase = 0;
+        int slot = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m0 = (tile % tiles_m) * kBM;
             const int n0 = (tile / tiles_m) * BN;
+            const int r0 = m0 + q * 32;
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
-            const int64_t row = m0 + q * 32 + lane;
+            const uint32_t tbase =
+                tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t v[32];
-                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                       static_cast<uint32_t>(acc * BN + c * 32);
-                ptx::tmem_ld_32x32b_x32(taddr, v);
-                ptx::tmem_ld_wait();
-                const int col = n0 + c * 32;
-                if (row < p.m && col < p.n) epilogue_chunk<kKind>(p, row, col, v);
+            for (int c = 0; c < BN / W; ++c) {
+                const int col0 = n0 + c * W;
+                if (col0 >= p.n || r0 >= p.m) continue;  // warp-uniform: whole chunk out of range
+                uint8_t* buf = ebuf + slot * kEpiBuf;
+                // the buffer's previous bulk store must have finished reading it
+                if (lane == 0) {
+                    if (two_out) bulk_wait_read<0>();
+                    else bulk_wait_read<1>();
+                }
+                __syncwarp();
+                if (need_aux) {
+                    if (lane == 0) {
+                        ptx::mbar_arrive_expect_tx(&aux_bar[q], kEpiBuf);
+                        ptx::tma_load_2d(buf, &em.aux, &aux_bar[q], col0, r0);
+                    }
+                }
+                float x[W];
+                {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(tbase + c * W, v);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(v[j]) * e.alpha;
+                    if constexpr (W == 64) {
+                        ptx::tmem_ld_32x32b_x32(tbase + c * W + 32, v);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) x[32 + j] = __uint_as_float(v[j]) * e.alpha;
+                    }
+                }
+                if constexpr (kF32) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<float4*>(buf + swz(lane, j)) =
+                            make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+                } else {
+                    if (need_aux) ptx::mbar_wait(&aux_bar[q], aux_phase), aux_phase ^= 1;
+                    if (kKind == EpiKind::StoreBF16 && e.bias != nullptr) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const uint4 bb = *reinterpret_cast<const uint4*>(e.bias + col0 + 8 * j);
+                            const uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const float2 bf = ptx::unpack_bf16x2(bw[t]);
+                                x[8 * j + 2 * t] += bf.x;
+                                x[8 * j + 2 * t + 1] += bf.y;
+                            }
+                        }
+                    }
+                    if constexpr (kKind == EpiKind::DGeluBF16) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const uint4 uu = *reinterpret_cast<const uint4*>(buf + swz(lane, j));
+                            const uint32_t uw[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const float2 uf = ptx::unpack_bf16x2(uw[t]);
+                                x[8 * j + 2 * t] *= gelu_bwd(uf.x);
+                                x[8 * j + 2 * t + 1] *= gelu_bwd(uf.y);
+                            }
+                        }
+                    } else {
+                        if (two_out) {
+                            // pre-activation copy into the other buffer; GELU of the
+                            // bf16-rounded value so the backward sees the same function
+                            uint8_t* pbuf = ebuf + (slot ^ 1) * kEpiBuf;
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                uint32_t w4[4];
+#pragma unroll
+                                for (int t = 0; t < 4; ++t) {
+                                    w4[t] = ptx::pack_bf16x2(x[8 * j + 2 * t], x[8 * j + 2 * t + 1]);
+                                    const float2 r = ptx::unpack_bf16x2(w4[t]);
+                                    x[8 * j + 2 * t] = r.x;
+                                    x[8 * j + 2 * t + 1] = r.y;
+                                }
+                                *reinterpret_cast<uint4*>(pbuf + swz(lane, j)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                            }
+                        }
+                        if (e.gelu) {
+#pragma unroll
+                            for (int j = 0; j < W; ++j) x[j] = gelu_fwd(x[j]);
+                        }
+                        if (need_aux) {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const uint4 rr = *reinterpret_cast<const uint4*>(buf + swz(lane, j));
+                                const uint32_t rw[4] = {rr.x, rr.y, rr.z, rr.w};
+#pragma unroll
+                                for (int t = 0; t < 4; ++t) {
+                                    const float2 rf = ptx::unpack_bf16x2(rw[t]);
+                                    x[8 * j + 2 * t] += rf.x;
+                                    x[8 * j + 2 * t + 1] += rf.y;
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<uint4*>(buf + swz(lane, j)) =
+                            make_uint4(ptx::pack_bf16x2(x[8 * j], x[8 * j + 1]),
+                                       ptx::pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
+                                       ptx::pack_bf16x2(x[8 * j + 4], x[8 * j + 5]),
+                                       ptx::pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
+                }
+                ptx::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    if (reduce) tma_reduce_add_2d(&em.d, buf, col0, r0);
+                    else tma_store_2d(&em.d, buf, col0, r0);
+                    if (two_out) tma_store_2d(&em.pre, ebuf + (slot ^ 1) * kEpiBuf, col0, r0);
+                    bulk_commit();
+                }
+                if (!two_out) slot ^= 1;
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -308,6 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -339,25 +404,28 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 2-D bf16 tensor map with a 64-element (128 B) inner box and 128 B swizzle.
-CUtensorMap make_map(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld_elems,
-                     uint32_t box_outer) {
+// 2-D tensor map with 128 B swizzle; box = {box_inner, box_outer} elements.
+CUtensorMap make_map_t(const void* ptr, CUtensorMapDataType dt, int esize, uint64_t inner, uint64_t outer,
+                       int64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
     CUtensorMap map;
     const cuuint64_t dims[2] = {inner, outer};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
-    const cuuint32_t box[2] = {64, box_outer};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * esize};
+    const cuuint32_t box[2] = {box_inner, box_outer};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                   const_cast<bf16*>(ptr), dims, strides, box, estr,
+    const CUresult r = encode_fn()(&map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return map;
 }
 
+// bf16 map with a 64-element (128 B) inner box.
+CUtensorMap make_map(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld_elems, uint32_t box_outer) {
+    return make_map_t(ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, inner, outer, ld_elems, 64, box_outer);
+}
+
 template <int BN, bool kAMN, bool kBMN, EpiKind kKind>
-void launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& p, cudaStream_t s) {
+void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p, cudaStream_t s) {
     using Cfg = GemmCfg<BN>;
     auto kern = gemm_tc_kernel<BN, kAMN, kBMN, kKind>;
     static std::atomic<uint32_t> configured{0};  // one attribute call per device
@@ -365,33 +433,33 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& p, cuda
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const uint32_t bit = 1u << (dev & 31);
     if ((configured.load() & bit) == 0) {
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        Cfg::kSmemBytes),
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes),
                    "cudaFuncSetAttribute(gemm smem)");
         configured.fetch_or(bit);
     }
     const int tiles = ((p.m + kBM - 1) / kBM) * ((p.n + BN - 1) / BN);
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kThreads, Cfg::kSmemBytes, s>>>(ta, tb, p);
+    kern<<<grid, kThreads, Cfg::kSmemBytes, s>>>(ta, tb, em, p);
     check_cuda(cudaGetLastError(), "gemm_tc_kernel launch");
 }
 
 template <int BN, bool kAMN, bool kBMN>
-void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& p, cudaStream_t s) {
+void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p,
+                  cudaStream_t s) {
     switch (p.epi.kind) {
-        case EpiKind::StoreBF16: launch<BN, kAMN, kBMN, EpiKind::StoreBF16>(ta, tb, p, s); break;
-        case EpiKind::StoreF32: launch<BN, kAMN, kBMN, EpiKind::StoreF32>(ta, tb, p, s); break;
-        case EpiKind::DGeluBF16: launch<BN, kAMN, kBMN, EpiKind::DGeluBF16>(ta, tb, p, s); break;
+        case EpiKind::StoreBF16: launch<BN, kAMN, kBMN, EpiKind::StoreBF16>(ta, tb, em, p, s); break;
+        case EpiKind::StoreF32: launch<BN, kAMN, kBMN, EpiKind::StoreF32>(ta, tb, em, p, s); break;
+        case EpiKind::DGeluBF16: launch<BN, kAMN, kBMN, EpiKind::DGeluBF16>(ta, tb, em, p, s); break;
     }
 }
 
 template <int BN>
-void dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
+void dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em,
                     const KParams& p, cudaStream_t s) {
-    if (!amn && !bmn) dispatch_epi<BN, false, false>(ta, tb, p, s);
-    else if (!amn && bmn) dispatch_epi<BN, false, true>(ta, tb, p, s);
-    else if (amn && !bmn) dispatch_epi<BN, true, false>(ta, tb, p, s);
-    else dispatch_epi<BN, true, true>(ta, tb, p, s);
+    if (!amn && !bmn) dispatch_epi<BN, false, false>(ta, tb, em, p, s);
+    else if (!amn && bmn) dispatch_epi<BN, false, true>(ta, tb, em, p, s);
+    else if (amn && !bmn) dispatch_epi<BN, true, false>(ta, tb, em, p, s);
+    else dispatch_epi<BN, true, true>(ta, tb, em, p, s);
 }
 
 // Pick the N tile that wastes the fewest MMA slots over whole waves of SMs.
@@ -409,24 +477,47 @@ int choose_bn(int m, int n) {
 
 }  // namespace
 
+CUtensorMap make_tmap_bf16_2d(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld_elems,
+                              uint32_t box_inner, uint32_t box_outer) {
+    if (box_inner != 64) throw Error("tensor maps here use a 64-element (128 B) swizzled inner box");
+    return make_map(ptr, inner, outer, ld_elems, box_outer);
+}
+
 void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
                const GemmEpilogue& epi, cudaStream_t stream) {
     if (m <= 0 || n <= 0 || k <= 0) throw Error("gemm: empty problem");
     if (n % 32 != 0) throw Error("gemm: N must be a multiple of 32");
     if ((a.ld % 8) != 0 || (b.ld % 8) != 0) throw Error("gemm: leading dims must be multiples of 8");
+    if (epi.kind == EpiKind::StoreF32 && epi.beta != 0.0f && epi.beta != 1.0f)
+        throw Error("gemm: fp32 epilogue supports beta 0 (store) or 1 (TMA reduce-add) only");
+    if ((epi.ldd % 8) != 0 || (epi.residual && epi.ldr % 8 != 0))
+        throw Error("gemm: output leading dims must be multiples of 8");
     const int bn = choose_bn(m, n);
     const bool amn = a.major == Major::MN, bmn = b.major == Major::MN;
     // A: rows = m (tile kBM), B: rows = n (tile bn).  K-major maps put k innermost.
     const CUtensorMap ta = amn ? make_map(a.ptr, m, k, a.ld, kBK) : make_map(a.ptr, k, m, a.ld, kBM);
     const CUtensorMap tb = bmn ? make_map(b.ptr, n, k, b.ld, kBK) : make_map(b.ptr, k, n, b.ld, bn);
+    EpiMaps em{};
+    if (epi.kind == EpiKind::StoreF32) {
+        em.d = make_map_t(epi.d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n, m, epi.ldd, 32, 32);
+    } else {
+        em.d = make_map(static_cast<const bf16*>(epi.d), n, m, epi.ldd, 32);
+        if (epi.kind == EpiKind::StoreBF16 && epi.gelu && epi.preact)
+            em.pre = make_map(epi.preact, n, m, epi.ldd, 32);
+        if (epi.kind == EpiKind::StoreBF16 && epi.residual)
+            em.aux = make_map(epi.residual, n, m, epi.ldr, 32);
+        if (epi.kind == EpiKind::DGeluBF16) {
+            if (!epi.aux) throw Error("gemm: DGelu epilogue needs the pre-activation");
+            em.aux = make_map(epi.aux, n, m, epi.ldd, 32);
+        }
+    }
     KParams p{m, n, k, epi};
     const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
     prof::Scope scope("gemm", 2.0 * m * n * k,
-                      2.0 * (static_cast<double>(m) * k + static_cast<double>(n) * k) +
-                          out_bytes * m * n,
-                      1, stream);
-    if (bn == 256) dispatch_major<256>(amn, bmn, ta, tb, p, stream);
-    else dispatch_major<128>(amn, bmn, ta, tb, p, stream);
+                      2.0 * (static_cast<double>(m) * k + static_cast<double>(n) * k) + out_bytes * m * n, 1,
+                      stream);
+    if (bn == 256) dispatch_major<256>(amn, bmn, ta, tb, em, p, stream);
+    else dispatch_major<128>(amn, bmn, ta, tb, em, p, stream);
 }
 
 int num_sms() {

@@ -252,7 +252,8 @@ public:
             gemm_wgrad(gB_, h_, st.o[l], h_, h_, h_, T_, grad_ + o.wo, beta, s);
             colsum_bf16(gB_, T_, h_, h_, grad_ + o.bo, first, red_scratch_, s);
             // attention
-            attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, b_, seq_, heads_, cfg_.causal != 0, s);
+            attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
+                          cfg_.causal != 0, s);
             // QKV: dxn1 = dqkv Wqkv
             gemm_store_mn_b(g3_, 3 * h_, W + o.wqkv, h_, T_, h_, 3 * h_, gX_, s);
             gemm_wgrad(g3_, 3 * h_, st.xn1[l], h_, 3 * h_, h_, T_, grad_ + o.wqkv, beta, s);
@@ -366,6 +367,7 @@ private:
         g3_ = dalloc<bf16>(T * 3 * h);
         g4_ = dalloc<bf16>(T * 4 * h);
         delta_ = dalloc<float>(stat);
+        attn_scratch_ = dalloc<float>(attention_bwd_scratch_floats(b_, seq_, heads_));
         if (last_) {
             row_loss_ = dalloc<float>(static_cast<size_t>(R_));
             if (R_ < T_) gH_ = dalloc<bf16>(static_cast<size_t>(R_) * h);
@@ -453,6 +455,7 @@ private:
     std::vector<Slot> slots_;
     bf16 *gA_ = nullptr, *gB_ = nullptr, *gX_ = nullptr, *g3_ = nullptr, *g4_ = nullptr, *gH_ = nullptr;
     float* delta_ = nullptr;
+    float* attn_scratch_ = nullptr;
     float* red_scratch_ = nullptr;
     float* row_loss_ = nullptr;
     int* head_idx_ = nullptr;

@@ -213,6 +213,7 @@ __global__ void k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x
                          const bf16* __restrict__ g, const bf16* __restrict__ dres, bf16* __restrict__ dx,
                          float* __restrict__ part_g, float* __restrict__ part_b, int rows, int h) {
     const int lane = threadIdx.x & 31;
+    // rows are dealt block-contiguously so each CTA's partial covers a row range
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int hv = h / 8;
@@ -264,20 +265,31 @@ __global__ void k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x
             }
         }
     }
+    // Block-level reduction of the 8 warps' dg / db partials in fixed order, one
+    // partial row per CTA (deterministic).
+    extern __shared__ float red[];  // [8][h]
+    const int w = threadIdx.x >> 5;
+    for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int vi = lane + 32 * i;
-        if (vi < hv) {
+        for (int i = 0; i < NV; ++i) {
+            const int vi = lane + 32 * i;
+            if (vi < hv)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                part_g[static_cast<size_t>(gwarp) * h + vi * 8 + q] = ag[i][q];
-                part_b[static_cast<size_t>(gwarp) * h + vi * 8 + q] = ab[i][q];
-            }
+                for (int q = 0; q < 8; ++q) red[w * h + vi * 8 + q] = pass == 0 ? ag[i][q] : ab[i][q];
         }
+        __syncthreads();
+        float* dst = (pass == 0 ? part_g : part_b) + static_cast<size_t>(blockIdx.x) * h;
+        for (int c = threadIdx.x; c < h; c += blockDim.x) {
+            float s = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += red[k * h + c];
+            dst[c] = s;
+        }
+        __syncthreads();
     }
 }
 
-int ln_bwd_blocks(int rows) { return std::max(1, std::min(148, (rows + 63) / 64)); }
+int ln_bwd_blocks(int rows) { return std::max(1, std::min(4 * 148, (rows + 15) / 16)); }
 
 // ---- softmax cross-entropy ------------------------------------------------------------
 
@@ -471,7 +483,7 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 }
 
 size_t layernorm_bwd_scratch_floats(int rows, int h) {
-    return static_cast<size_t>(ln_bwd_blocks(rows)) * 8 * h * 2;
+    return static_cast<size_t>(ln_bwd_blocks(rows)) * h * 2;
 }
 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
@@ -481,15 +493,20 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
     prof::Scope scope("layernorm_bwd", 0.0, (dres ? 8.0 : 6.0) * rows * h + 8.0 * rows, 3, s);
     const int nv = (h / 8 + 31) / 32;
     const int blocks = ln_bwd_blocks(rows);
-    const int parts = blocks * 8;
+    const int parts = blocks;
     float* pg = scratch;
     float* pb = scratch + static_cast<size_t>(parts) * h;
+    const size_t sm = 8 * static_cast<size_t>(h) * sizeof(float);
     switch (nv) {
-        case 1: k_ln_bwd<1><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        case 2: k_ln_bwd<2><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        case 3: k_ln_bwd<3><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        case 4: k_ln_bwd<4><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        default: k_ln_bwd<8><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
+        case 1: k_ln_bwd<1><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
+        case 2: k_ln_bwd<2><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
+        case 3: k_ln_bwd<3><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
+        case 4: k_ln_bwd<4><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
+        default:
+            check_cuda(cudaFuncSetAttribute(k_ln_bwd<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(sm)), "cudaFuncSetAttribute(ln_bwd)");
+            k_ln_bwd<8><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h);
+            break;
     }
     reduce_parts(pg, parts, h, dg, overwrite, s);
     reduce_parts(pb, parts, h, db, overwrite, s);

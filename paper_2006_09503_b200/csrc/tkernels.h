@@ -44,9 +44,17 @@ void sum_scaled(const float* row_loss, int rows, float scale, float* loss_out, c
 // Attention over qkv [T x 3h] (q | k | v, heads of 64), output o [T x h], lse [b*nh*seq].
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
                    cudaStream_t s);
-// dqkv [T x 3h] from do [T x h]; scratch: delta [b*nh*seq] floats.
+// tcgen05 forward (attention_tc.cu) for seq % 128 == 0, seq <= 512; attention_fwd dispatches.
+bool attention_tc_supported(int seq);
+void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
+                      cudaStream_t s);
+size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads);
+void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv,
+                      float* delta, float* dq_part, int batch, int seq, int heads, bool causal, cudaStream_t s);
+// dqkv [T x 3h] from do [T x h]; delta: [b*nh*seq] floats; scratch: attention_bwd_scratch_floats.
+size_t attention_bwd_scratch_floats(int batch, int seq, int heads);
 void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv,
-                   float* delta, int batch, int seq, int heads, bool causal, cudaStream_t s);
+                   float* delta, float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s);
 
 // Momentum SGD with dampening (semantics.cpp:153-165) on the flat fp32 master:
 //   g = grad / count; v = beta v + (1-beta) g; w -= lr v; out_bf16 = bf16(w)
