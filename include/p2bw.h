@@ -169,6 +169,14 @@ int p2bw_engine_finish(p2bw_engine* eng);
 /* Device time between stage `stage`'s u0-th and u1-th WeightUpdate of the current
  * run (CUDA events on the stage's stream; waits for u1). */
 int p2bw_engine_update_elapsed_ms(p2bw_engine* eng, int stage, int u0, int u1, double* ms);
+/* Data-parallel width w > 1 (planner's "width", profile.hpp:50-62): one process
+ * per pipeline replica.  Rank 0 makes one 128-byte NCCL unique id per stage and
+ * shares them; every replica calls join_replicas with the same ids.  The
+ * AllReduce op (schedule.cpp:80-84) then sums each stage's coalesced gradient
+ * across its w replicas (NCCL, on the stage's stream) and WeightUpdate divides
+ * by count * w -- the replicas' average, as costmodel.cpp:23-27 prices it. */
+int p2bw_nccl_unique_id(void* out, size_t bytes);
+int p2bw_engine_join_replicas(p2bw_engine* eng, const void* ids, int nranks, int rank);
 int p2bw_engine_sync(p2bw_engine* eng);
 int p2bw_engine_counters(p2bw_engine* eng, p2bw_counters* out);
 /* Weights created by a stage's update_index-th update of the last run (snapshots on). */

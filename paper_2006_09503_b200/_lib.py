@@ -73,6 +73,8 @@ def _signatures():
         ("p2bw_engine_issue", i, [vp, i]),
         ("p2bw_engine_finish", i, [vp]),
         ("p2bw_engine_update_elapsed_ms", i, [vp, i, i, i, C.POINTER(C.c_double)]),
+        ("p2bw_nccl_unique_id", i, [vp, sz]),
+        ("p2bw_engine_join_replicas", i, [vp, vp, i, i]),
         ("p2bw_engine_sync", i, [vp]),
         ("p2bw_engine_counters", i, [vp, vp]),
         ("p2bw_engine_read_snapshot", i, [vp, i, i, vp, sz]),

@@ -5,6 +5,7 @@
 
 #include "capi_internal.h"
 #include "engine.h"
+#include "nccl_dl.h"
 #include "p2bw.h"
 #include "pipesim/schedule.hpp"
 
@@ -166,6 +167,22 @@ int p2bw_engine_update_elapsed_ms(p2bw_engine* eng, int stage, int u0, int u1, d
         check_stage(e, stage);
         if (ms == nullptr) throw std::invalid_argument("ms is NULL");
         *ms = e.update_elapsed_ms(stage, u0, u1);
+    });
+}
+
+int p2bw_nccl_unique_id(void* out, size_t bytes) {
+    return guarded([&] {
+        if (out == nullptr || bytes != sizeof(ncclUniqueId))
+            throw std::invalid_argument("unique id buffer must be " + std::to_string(sizeof(ncclUniqueId)) + " bytes");
+        const ncclUniqueId id = p2bw::nccl_unique_id();
+        std::memcpy(out, &id, sizeof(id));
+    });
+}
+
+int p2bw_engine_join_replicas(p2bw_engine* eng, const void* ids, int nranks, int rank) {
+    return guarded([&] {
+        if (ids == nullptr) throw std::invalid_argument("ids is NULL");
+        eng_of(eng).join_replicas(ids, nranks, rank);
     });
 }
 

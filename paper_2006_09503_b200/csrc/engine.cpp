@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include "nccl_dl.h"
+
 namespace p2bw {
 
 namespace {
@@ -131,6 +133,19 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
 
 Engine::~Engine() { free_buffers(); }
 
+void Engine::join_replicas(const void* ids, int nranks, int rank) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error("bad data-parallel rank / size");
+    for (Stage& st : stages_) {
+        if (st.comm) throw Error("stage already joined a replica group");
+        if (nranks == 1) continue;
+        ncclUniqueId id;
+        std::memcpy(&id, static_cast<const uint8_t*>(ids) + sizeof(ncclUniqueId) * st.index, sizeof(id));
+        DeviceGuard g(st.device);
+        st.comm = nccl_comm_init(id, nranks, rank);
+        st.replicas = nranks;
+    }
+}
+
 void Engine::free_buffers() {
     for (Stage& st : stages_) {
         DeviceGuard g(st.device);
@@ -140,6 +155,8 @@ void Engine::free_buffers() {
         st.act_ring.clear();
         st.grad_ring.clear();
         st.model.reset();
+        if (st.comm) nccl_comm_destroy(static_cast<ncclComm_t>(st.comm));
+        st.comm = nullptr;
         if (st.t0) cudaEventDestroy(st.t0);
         if (st.t1) cudaEventDestroy(st.t1);
         if (st.stream) cudaStreamDestroy(st.stream);
@@ -303,7 +320,9 @@ void Engine::issue_update(Stage& st) {
     if (dst_slot < 0)
         throw Error("stage " + std::to_string(st.index) + ": no free weight buffer for version " +
                     std::to_string(src_version + 1));
-    st.model->update(src_slot, dst_slot, st.grad_count, st.stream);
+    // gradients are summed over grad_count microbatches (and over the replicas by
+    // the AllReduce): divide by both (semantics.cpp:338-340; PAPER §3 "w replicas")
+    st.model->update(src_slot, dst_slot, st.grad_count * st.replicas, st.stream);
     st.updates_done += 1;
     st.version_slot[st.updates_done] = dst_slot;
     prune_versions(st);
@@ -363,8 +382,17 @@ void Engine::issue(int upto_batch) {
                     case P2BW_OP_FORWARD: issue_forward(st, op); break;
                     case P2BW_OP_BACKWARD: issue_backward(st, op); break;
                     case P2BW_OP_UPDATE: issue_update(st); break;
-                    case P2BW_OP_ALLREDUCE:  // w == 1: nothing to reduce (semantics.cpp:351-354)
-                    case P2BW_OP_FLUSH:      // ordering is already implied by stream order
+                    case P2BW_OP_ALLREDUCE:  // sum the coalesced gradient over the w replicas
+                        if (st.comm) {       // (w == 1: no-op, semantics.cpp:351-354)
+                            void* buf = nullptr;
+                            size_t n = 0;
+                            int dt = 0;
+                            st.model->grad_buffer(&buf, &n, &dt);
+                            nccl_allreduce_sum(buf, n, dt == 1 ? ncclFloat64 : ncclFloat32,
+                                               static_cast<ncclComm_t>(st.comm), st.stream);
+                        }
+                        break;
+                    case P2BW_OP_FLUSH:  // ordering is already implied by stream order
                         break;
                     default:
                         throw Error("op kind " + std::to_string(op.kind) +

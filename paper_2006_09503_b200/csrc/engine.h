@@ -76,6 +76,9 @@ public:
         throw Error("this stage computes no loss");
     }
     virtual void bind_stream(cudaStream_t s) { (void)s; }
+    // The coalesced gradient buffer (all-reduced across data-parallel replicas).
+    // dtype: 0 = fp32, 1 = fp64.
+    virtual void grad_buffer(void** ptr, size_t* count, int* dtype) = 0;
     // Asynchronous D2H of fp32 losses into (pinned) host memory, stream-ordered.
     virtual void copy_losses_async(float* host, int first_mb, int count, cudaStream_t s) {
         (void)host, (void)first_mb, (void)count, (void)s;
@@ -127,6 +130,11 @@ public:
     void finish();
     // Device time between a stage's u0-th and u1-th update of the current run.
     double update_elapsed_ms(int stage, int u0, int u1);
+    // Data parallelism: stage s of this pipeline joins the communicator of its
+    // `nranks` replicas (one NCCL unique id per stage, 128 bytes each).  The
+    // AllReduce op then sums the coalesced gradient across replicas and the
+    // update divides by count * nranks (the replicas' average).
+    void join_replicas(const void* ids, int nranks, int rank);
     void sync();
     // Weights of stage s for the version created by its u-th update (0 = initial).
     void read_version(int s, int version, void* host, size_t bytes);
@@ -157,6 +165,8 @@ private:
         size_t ptr = 0;
         int updates_done = 0;
         int updates_issued = 0;  // in the current run
+        void* comm = nullptr;    // ncclComm_t over this stage's data-parallel replicas
+        int replicas = 1;
         int version_base = 0;    // updates_done at begin()
         std::map<int, int> version_slot;  // live version -> weight slot
         std::map<int, int> stash_version; // in-flight microbatch -> version

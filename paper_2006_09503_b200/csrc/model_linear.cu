@@ -126,6 +126,11 @@ public:
     }
 
     size_t num_params() const override { return layers_ * mat_; }
+    void grad_buffer(void** ptr, size_t* count, int* dtype) override {
+        *ptr = gsum_;
+        *count = layers_ * mat_;
+        *dtype = 1;
+    }
     size_t boundary_bytes() const override { return act_ * sizeof(double); }
     size_t weight_bytes_public() const override { return layers_ * mat_ * sizeof(double); }
     int data_capacity() const override { return capacity_; }

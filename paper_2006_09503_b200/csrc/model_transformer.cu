@@ -82,6 +82,11 @@ public:
     size_t weight_bytes_public() const override { return nparam_ * sizeof(float); }
     int data_capacity() const override { return capacity_; }
     void bind_stream(cudaStream_t s) override { stream_ = s; }
+    void grad_buffer(void** ptr, size_t* count, int* dtype) override {
+        *ptr = grad_;
+        *count = nparam_;
+        *dtype = 0;
+    }
 
     void init_weights(uint64_t seed) override {
         const float hw = static_cast<float>(0.02 * std::sqrt(3.0));  // U(-a, a), std of N(0, 0.02)

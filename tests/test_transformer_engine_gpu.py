@@ -42,9 +42,11 @@ def run_case(spec, depth, m, T, lr, beta, seed):
     return params, ids, tg, losses, finals, c
 
 
-@pytest.mark.parametrize("depth,causal,head_rows", [(1, True, 0), (2, True, 0), (2, False, 16)])
-def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows):
-    spec = TO.Spec(layers=2, hidden=128, heads=2, seq=64, vocab=500, batch=2, causal=causal, head_rows=head_rows)
+@pytest.mark.parametrize("depth,causal,head_rows,seq", [(1, True, 0, 64), (2, True, 0, 64), (2, False, 16, 64),
+                                                        (2, True, 0, 128), (1, False, 20, 256)])
+def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows, seq):
+    # seq 64 runs the CUDA-core attention, seq % 128 == 0 the tcgen05 attention
+    spec = TO.Spec(layers=2, hidden=128, heads=2, seq=seq, vocab=500, batch=2, causal=causal, head_rows=head_rows)
     m, T, lr, beta, seed = 2, 4, 0.5, 0.9, 1234
     params, ids, tg, losses, finals, c = run_case(spec, depth, m, T, lr, beta, seed)
     assert c.max_versions_held == 2
