@@ -64,6 +64,7 @@ __device__ __forceinline__ float gelu_bwd(float x) {
 
 struct KParams {
     int m, n, k;
+    int splits;  // split-K factor (fp32 reduce-add epilogue only)
     GemmEpilogue epi;
 };
 
@@ -123,6 +124,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tiles_n = p.n / BN + (p.n % BN != 0);
     const int num_tiles = tiles_m * tiles_n;
     const int kblocks = (p.k + kBK - 1) / kBK;
+    // work item w: output tile (w % num_tiles), K slice (w / num_tiles) of kb_per k-blocks
+    const int num_work = num_tiles * p.splits;
+    const int kb_per = (kblocks + p.splits - 1) / p.splits;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmap_a);
@@ -149,10 +153,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+                const int tile = w % num_tiles;
                 const int m0 = (tile % tiles_m) * kBM;
                 const int n0 = (tile / tiles_m) * BN;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                const int kb0 = (w / num_tiles) * kb_per;
+                const int kb1 = min(kblocks, kb0 + kb_per);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
                     uint8_t* da = s_a + stage * Cfg::kABytes;
@@ -194,11 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+                const int kb0 = (w / num_tiles) * kb_per;
+                const int kb1 = min(kblocks, kb0 + kb_per);
                 ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full_bar[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a_addr = ptx::smem_u32(s_a + stage * Cfg::kABytes);
@@ -207,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint64_t ad = ptx::sdesc_sw128(a_addr + kk * a_kstep, a_lbo, a_sbo);
                         const uint64_t bd = ptx::sdesc_sw128(b_addr + kk * b_kstep, b_lbo, b_sbo);
-                        ptx::umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        ptx::umma_bf16(d_tmem, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
                     }
                     ptx::umma_commit(&empty_bar[stage]);
                     if (++stage == S) {
@@ -233,12 +242,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int W = kF32 ? 32 : 64;  // columns per chunk
         const bool need_aux = kKind == EpiKind::DGeluBF16 || (kKind == EpiKind::StoreBF16 && e.residual != nullptr);
         const bool two_out = kKind == EpiKind::StoreBF16 && e.gelu && e.preact != nullptr;
-        const bool reduce = kF32 && e.beta != 0.0f;
+        const bool reduce = kF32 && (e.beta != 0.0f || p.splits > 1);  // split-K: host pre-zeroed D
         uint32_t aux_phase = 0;
         int slot = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+            const int tile = w % num_tiles;
             const int m0 = (tile % tiles_m) * kBM;
             const int n0 = (tile / tiles_m) * BN;
             const int r0 = m0 + q * 32;
@@ -437,8 +447,8 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, con
                    "cudaFuncSetAttribute(gemm smem)");
         configured.fetch_or(bit);
     }
-    const int tiles = ((p.m + kBM - 1) / kBM) * ((p.n + BN - 1) / BN);
-    const int grid = tiles < num_sms() ? tiles : num_sms();
+    const int work = ((p.m + kBM - 1) / kBM) * ((p.n + BN - 1) / BN) * p.splits;
+    const int grid = work < num_sms() ? work : num_sms();
     kern<<<grid, kThreads, Cfg::kSmemBytes, s>>>(ta, tb, em, p);
     check_cuda(cudaGetLastError(), "gemm_tc_kernel launch");
 }
@@ -511,7 +521,29 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
             em.aux = make_map(epi.aux, n, m, epi.ldd, 32);
         }
     }
-    KParams p{m, n, k, epi};
+    // Split-K for fp32 (wgrad) GEMMs whose output has too few tiles to fill the
+    // SMs: every K slice reduce-adds into D (pre-zeroed when beta == 0).
+    int splits = 1;
+    if (epi.kind == EpiKind::StoreF32) {
+        const int tiles = ((m + kBM - 1) / kBM) * ((n + bn - 1) / bn);
+        const int kblocks = (k + kBK - 1) / kBK;
+        if (tiles < 2 * num_sms() && kblocks >= 16) {
+            splits = std::min(kblocks / 8, (2 * num_sms() + tiles - 1) / tiles);
+            splits = std::max(splits, 1);
+            const int kb_per = (kblocks + splits - 1) / splits;
+            splits = (kblocks + kb_per - 1) / kb_per;  // no empty slices
+        }
+        if (splits > 1 && epi.beta == 0.0f) {
+            if (epi.ldd == n) {
+                check_cuda(cudaMemsetAsync(epi.d, 0, static_cast<size_t>(m) * n * sizeof(float), stream), "memset");
+            } else {
+                check_cuda(cudaMemset2DAsync(epi.d, static_cast<size_t>(epi.ldd) * sizeof(float), 0,
+                                             static_cast<size_t>(n) * sizeof(float), static_cast<size_t>(m), stream),
+                           "memset2D");
+            }
+        }
+    }
+    KParams p{m, n, k, splits, epi};
     const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
     prof::Scope scope("gemm", 2.0 * m * n * k,
                       2.0 * (static_cast<double>(m) * k + static_cast<double>(n) * k) + out_bytes * m * n, 1,

@@ -128,35 +128,62 @@ void reduce_parts(const float* part, int parts, int n, float* out, bool overwrit
     k_reduce_parts<<<(n + 31) / 32, 256, 0, s>>>(part, parts, n, out, overwrite ? 1 : 0);
 }
 
-// Column sums of a bf16 matrix: block = 32 column-vectors (256 columns) x 8 row lanes.
-__global__ void k_colsum_part(const bf16* __restrict__ x, int rows, int n, int ld, int rows_per_block,
-                              float* __restrict__ part) {
+// Column statistics of a bf16 matrix, per row-block partials (block = 32 column
+// vectors of 8 = 256 columns x 8 row lanes):
+//   kLn = false: part0[c] = sum_r x[r, c]                       (bias gradient)
+//   kLn = true : part0[c] = sum_r dy[r, c] * (x[r, c] - mean_r) * rstd_r   (LN gamma)
+//                part1[c] = sum_r dy[r, c]                                (LN beta)
+template <bool kLn>
+__global__ void __launch_bounds__(256) k_colstats(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                  const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                  int rows, int n, int ld, int rows_per_block,
+                                                  float* __restrict__ part0, float* __restrict__ part1) {
     __shared__ float red[8][256 + 8];
     const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
     const int col = blockIdx.x * 256 + cv * 8;
     const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (col < n) {
+#pragma unroll 4
         for (int r = r0 + rl; r < r1; r += 8) {
-            float v[8];
-            load8(x + static_cast<size_t>(r) * ld + col, v);
+            float g[8];
+            load8(dy + static_cast<size_t>(r) * ld + col, g);
+            if constexpr (kLn) {
+                float xv[8];
+                load8(x + static_cast<size_t>(r) * ld + col, xv);
+                const float mu = mean[r], rs = rstd[r];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] += v[q];
+                for (int q = 0; q < 8; ++q) {
+                    a0[q] = fmaf(g[q], (xv[q] - mu) * rs, a0[q]);
+                    a1[q] += g[q];
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) a0[q] += g[q];
+            }
         }
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) red[rl][cv * 8 + q] = acc[q];
-    __syncthreads();
     const int c = threadIdx.x;  // 256 columns of this block
-    if (blockIdx.x * 256 + c < n) {
-        float s = 0.0f;
+    for (int pass = 0; pass < (kLn ? 2 : 1); ++pass) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s += red[i][c];
-        part[static_cast<size_t>(blockIdx.y) * n + blockIdx.x * 256 + c] = s;
+        for (int q = 0; q < 8; ++q) red[rl][cv * 8 + q] = pass == 0 ? a0[q] : a1[q];
+        __syncthreads();
+        if (blockIdx.x * 256 + c < n) {
+            float s = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s += red[i][c];
+            (pass == 0 ? part0 : part1)[static_cast<size_t>(blockIdx.y) * n + blockIdx.x * 256 + c] = s;
+        }
+        __syncthreads();
     }
 }
 
-int colsum_row_blocks(int rows) { return std::max(1, std::min(148, (rows + 255) / 256)); }
+// Row blocks so that the grid has >= ~4 CTAs per SM; each block still sees >= 16 rows.
+int colsum_row_blocks(int rows, int n) {
+    const int col_blocks = (n + 255) / 256;
+    const int want = (4 * 148 + col_blocks - 1) / col_blocks;
+    return std::max(1, std::min(want, (rows + 15) / 16));
+}
 
 // ---- LayerNorm (one warp per row, up to NV 8-element vectors per lane) -------------------
 
@@ -205,91 +232,55 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
     }
 }
 
-// dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) (+ dres), dxh = dy * g.
-// Each warp walks rows; dg / db partials accumulate per warp and land in part.
+// dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) (+ dres), dxh = dy * g;
+// one warp per row, no cross-row state (gamma / beta gradients: k_colstats<true>).
 template <int NV>
-__global__ void k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                         const float* __restrict__ mean, const float* __restrict__ rstd,
-                         const bf16* __restrict__ g, const bf16* __restrict__ dres, bf16* __restrict__ dx,
-                         float* __restrict__ part_g, float* __restrict__ part_b, int rows, int h) {
+__global__ void __launch_bounds__(256) k_ln_bwd_dx(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                   const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                   const bf16* __restrict__ g, const bf16* __restrict__ dres,
+                                                   bf16* __restrict__ dx, int rows, int h) {
     const int lane = threadIdx.x & 31;
-    // rows are dealt block-contiguously so each CTA's partial covers a row range
-    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= rows) return;
     const int hv = h / 8;
-    float ag[NV][8], ab[NV][8], gg[NV][8];
+    const float mu = mean[r], rs = rstd[r];
+    float xh[NV][8], dxh[NV][8];
+    float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i)
+    for (int i = 0; i < NV; ++i) {
+        const int vi = lane + 32 * i;
+        if (vi < hv) {
+            float xv[8], dv[8], gv[8];
+            load8(x + static_cast<size_t>(r) * h + vi * 8, xv);
+            load8(dy + static_cast<size_t>(r) * h + vi * 8, dv);
+            load8(g + vi * 8, gv);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) ag[i][q] = ab[i][q] = 0.0f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i)
-        if (lane + 32 * i < hv) load8(g + (lane + 32 * i) * 8, gg[i]);
-    for (int r = gwarp; r < rows; r += nwarps) {
-        const float mu = mean[r], rs = rstd[r];
-        float xh[NV][8], dxh[NV][8];
-        float s1 = 0.0f, s2 = 0.0f;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv) {
-                float xv[8], dv[8];
-                load8(x + static_cast<size_t>(r) * h + vi * 8, xv);
-                load8(dy + static_cast<size_t>(r) * h + vi * 8, dv);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    xh[i][q] = (xv[q] - mu) * rs;
-                    dxh[i][q] = dv[q] * gg[i][q];
-                    s1 += dxh[i][q];
-                    s2 += dxh[i][q] * xh[i][q];
-                    ag[i][q] += dv[q] * xh[i][q];
-                    ab[i][q] += dv[q];
-                }
-            }
-        }
-        const float m1 = warp_sum(s1) / h, m2 = warp_sum(s2) / h;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv) {
-                float o[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) o[q] = rs * (dxh[i][q] - m1 - xh[i][q] * m2);
-                if (dres != nullptr) {
-                    float rv[8];
-                    load8(dres + static_cast<size_t>(r) * h + vi * 8, rv);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) o[q] += rv[q];
-                }
-                store8(dx + static_cast<size_t>(r) * h + vi * 8, o);
+            for (int q = 0; q < 8; ++q) {
+                xh[i][q] = (xv[q] - mu) * rs;
+                dxh[i][q] = dv[q] * gv[q];
+                s1 += dxh[i][q];
+                s2 += dxh[i][q] * xh[i][q];
             }
         }
     }
-    // Block-level reduction of the 8 warps' dg / db partials in fixed order, one
-    // partial row per CTA (deterministic).
-    extern __shared__ float red[];  // [8][h]
-    const int w = threadIdx.x >> 5;
-    for (int pass = 0; pass < 2; ++pass) {
+    const float m1 = warp_sum(s1) / h, m2 = warp_sum(s2) / h;
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv)
+    for (int i = 0; i < NV; ++i) {
+        const int vi = lane + 32 * i;
+        if (vi < hv) {
+            float o[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) red[w * h + vi * 8 + q] = pass == 0 ? ag[i][q] : ab[i][q];
+            for (int q = 0; q < 8; ++q) o[q] = rs * (dxh[i][q] - m1 - xh[i][q] * m2);
+            if (dres != nullptr) {
+                float rv[8];
+                load8(dres + static_cast<size_t>(r) * h + vi * 8, rv);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) o[q] += rv[q];
+            }
+            store8(dx + static_cast<size_t>(r) * h + vi * 8, o);
         }
-        __syncthreads();
-        float* dst = (pass == 0 ? part_g : part_b) + static_cast<size_t>(blockIdx.x) * h;
-        for (int c = threadIdx.x; c < h; c += blockDim.x) {
-            float s = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) s += red[k * h + c];
-            dst[c] = s;
-        }
-        __syncthreads();
     }
 }
-
-int ln_bwd_blocks(int rows) { return std::max(1, std::min(4 * 148, (rows + 15) / 16)); }
 
 // ---- softmax cross-entropy ------------------------------------------------------------
 
@@ -483,46 +474,43 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 }
 
 size_t layernorm_bwd_scratch_floats(int rows, int h) {
-    return static_cast<size_t>(ln_bwd_blocks(rows)) * h * 2;
+    return static_cast<size_t>(colsum_row_blocks(rows, h)) * h * 2;
 }
 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, float* dg, float* db, bool overwrite, int rows, int h,
                    float* scratch, cudaStream_t s) {
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
-    prof::Scope scope("layernorm_bwd", 0.0, (dres ? 8.0 : 6.0) * rows * h + 8.0 * rows, 3, s);
+    prof::Scope scope("layernorm_bwd", 0.0, (dres ? 10.0 : 8.0) * rows * h + 8.0 * rows, 5, s);
     const int nv = (h / 8 + 31) / 32;
-    const int blocks = ln_bwd_blocks(rows);
-    const int parts = blocks;
-    float* pg = scratch;
-    float* pb = scratch + static_cast<size_t>(parts) * h;
-    const size_t sm = 8 * static_cast<size_t>(h) * sizeof(float);
+    const int grid = (rows + 7) / 8;
     switch (nv) {
-        case 1: k_ln_bwd<1><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        case 2: k_ln_bwd<2><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        case 3: k_ln_bwd<3><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        case 4: k_ln_bwd<4><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h); break;
-        default:
-            check_cuda(cudaFuncSetAttribute(k_ln_bwd<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(sm)), "cudaFuncSetAttribute(ln_bwd)");
-            k_ln_bwd<8><<<blocks, 256, sm, s>>>(dy, x, mean, rstd, g, dres, dx, pg, pb, rows, h);
-            break;
+        case 1: k_ln_bwd_dx<1><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
+        case 2: k_ln_bwd_dx<2><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
+        case 3: k_ln_bwd_dx<3><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
+        case 4: k_ln_bwd_dx<4><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
+        default: k_ln_bwd_dx<8><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
     }
-    reduce_parts(pg, parts, h, dg, overwrite, s);
-    reduce_parts(pb, parts, h, db, overwrite, s);
+    const int rb = colsum_row_blocks(rows, h);
+    const int rpb = (rows + rb - 1) / rb;
+    float* pg = scratch;
+    float* pb = scratch + static_cast<size_t>(rb) * h;
+    k_colstats<true><<<dim3((h + 255) / 256, rb), 256, 0, s>>>(dy, x, mean, rstd, rows, h, h, rpb, pg, pb);
+    reduce_parts(pg, rb, h, dg, overwrite, s);
+    reduce_parts(pb, rb, h, db, overwrite, s);
     check_cuda(cudaGetLastError(), "layernorm_bwd");
 }
 
-size_t colsum_scratch_floats(int rows, int n) { return static_cast<size_t>(colsum_row_blocks(rows)) * n; }
+size_t colsum_scratch_floats(int rows, int n) { return static_cast<size_t>(colsum_row_blocks(rows, n)) * n; }
 
 void colsum_bf16(const bf16* x, int rows, int n, int ld, float* out, bool overwrite, float* scratch,
                  cudaStream_t s) {
     if (n % 8 != 0) throw Error("colsum: columns must be a multiple of 8");
     prof::Scope scope("bias_grad", 0.0, 2.0 * rows * n + 8.0 * n, 2, s);
-    const int rb = colsum_row_blocks(rows);
+    const int rb = colsum_row_blocks(rows, n);
     const int rpb = (rows + rb - 1) / rb;
-    dim3 grid((n + 255) / 256, rb);
-    k_colsum_part<<<grid, 256, 0, s>>>(x, rows, n, ld, rpb, scratch);
+    k_colstats<false><<<dim3((n + 255) / 256, rb), 256, 0, s>>>(x, nullptr, nullptr, nullptr, rows, n, ld, rpb,
+                                                                  scratch, nullptr);
     reduce_parts(scratch, rb, n, out, overwrite, s);
     check_cuda(cudaGetLastError(), "colsum");
 }
