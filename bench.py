@@ -190,8 +190,11 @@ def run_ours(args, c):
     eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
                    microbatch_size=c["b"], layers=c["layers"], hidden=c["hidden"], heads=c["heads"],
                    seq_len=c["seq"], vocab=c["vocab"], causal=int(c["causal"]), head_rows=c["head_rows"],
-                   learning_rate=1e-3, momentum=0.9, seed=1234 + rank)
+                   learning_rate=1e-3, momentum=0.9, seed=1234)  # replicas start identical
     eng.init_weights()
+    if world > 1:
+        from paper_2006_09503_b200.dist import join_replicas
+        join_replicas(eng, depth)  # one NCCL communicator per stage over the w replicas
 
     # synthetic token batches in pinned host memory (one batch = m microbatches)
     T, R = c["b"] * c["seq"], c["b"] * (c["head_rows"] or c["seq"])
@@ -240,9 +243,8 @@ def run_ours(args, c):
     clk = clocks.stop()
     ms = eng.update_elapsed_ms(depth - 1, warm, warm + steps)  # K steady-state batches
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        from paper_2006_09503_b200.dist import max_over_ranks
+        ms = max_over_ranks(ms)
         torch.distributed.barrier()
     losses = loss_host.numpy()[: total_batches * m]
 
@@ -302,8 +304,8 @@ def run_ours(args, c):
                    "seq_len": c["seq"], "vocab": c["vocab"], "causal": c["causal"],
                    "head_rows_per_seq": c["head_rows"] or c["seq"], "microbatch_size": c["b"],
                    "microbatches_m": m, "global_batch": world * c["b"] * m,
-                   "parallelism": f"2bw d={depth} w={world}" + (" (replicas, no gradient exchange yet)"
-                                                                if world > 1 else ""),
+                   "parallelism": f"2bw d={depth} w={world}" + (" (NCCL all-reduce of the coalesced gradient "
+                                                                "at each AllReduce op)" if world > 1 else ""),
                    "policy": "2bw", "l2": "working set (activations >> 126 MB L2) exceeds L2 every step"},
         "e2e": {"value": round(value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes,

@@ -247,6 +247,8 @@ int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void*
 int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                               const void* g, const void* dres, void* dx, void* dg, void* db,
                               int overwrite, int rows, int h, void* stream);
+/* Column sums of a bf16 matrix (bias gradients): out (=|+=) sum_r x[r, :]. */
+int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream);
 /* Fused softmax cross-entropy: logits [rows x vp] -> dlogits in place, row_loss [rows]. */
 int p2bw_kernel_softmax_xent(void* logits, const void* targets, int rows, int vocab, int vp,
                              float grad_scale, void* row_loss, void* stream);

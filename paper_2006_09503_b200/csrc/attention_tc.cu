@@ -4,13 +4,15 @@
 //   TMA     Q tile [128 x 64], K and V rows [kv x 64] of the head (one 2-D map over
 //           qkv [T x 3h], box 64 x 128, 128-byte swizzle) -> SMEM
 //   UMMA    S = Q K^T for every key at once: 128 x kv fp32 in TMEM (<= 512 columns)
-//   softmax one thread per query row: two passes over its TMEM row (max, then
-//           exp2 / sum), exact -- no online rescaling is needed because the whole
-//           row is resident; P is written as bf16 straight into SMEM in the UMMA
-//           K-major SW128 layout, 256 keys at a time
+//   softmax two threads per query row (8 warps; thread half `sel` takes the
+//           interleaved 32-key chunks 2j+sel): pass 1 row max, pass 2 exp2 and
+//           sum -- exact, no online rescaling, because the whole row is resident.
+//           Row max / sum are exchanged through SMEM (fixed order: deterministic).
+//           P is written as bf16 straight into SMEM in the UMMA K-major SW128 layout
 //   UMMA    O = P V (V read as an MN-major operand), TMEM columns 0..63, issued per
 //           256-key half so the second half's exp overlaps the first half's MMA
-//   epilogue O / l -> bf16 -> global; lse = m + ln l (fp32) for the backward
+//   epilogue O / l -> bf16 -> global (each row thread stores 32 of the 64 columns);
+//           lse = m + ln l (fp32) for the backward
 //
 // SMEM: Q 16 KB + K 64 KB + V 64 KB + P 64 KB (the second P half reuses K's
 // buffer once S is complete) = 208 KB; TMEM: 512 columns.
@@ -34,13 +36,15 @@ namespace {
 
 constexpr int kBQ = 128;
 constexpr int kD = 64;
+constexpr int kThreads = 384;                  // 4 role warps + 8 softmax warps
 constexpr int kRowBytes = 128;                 // one 64-element bf16 row
 constexpr int kTileBytes = kBQ * kRowBytes;    // 16 KB: 128 rows
 constexpr int kSmemQ = 0;
 constexpr int kSmemK = kSmemQ + kTileBytes;            // 4 tiles
 constexpr int kSmemV = kSmemK + 4 * kTileBytes;        // 4 tiles
 constexpr int kSmemP = kSmemV + 4 * kTileBytes;        // 4 blocks of 64 keys
-constexpr int kSmemBar = kSmemP + 4 * kTileBytes;
+constexpr int kSmemX = kSmemP + 4 * kTileBytes;        // row max / sum exchange [2][2][128] f32
+constexpr int kSmemBar = kSmemX + 4 * kBQ * 4;
 constexpr int kSmemTotal = kSmemBar + 128 + 1024;      // + barriers + alignment slack
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -59,8 +63,12 @@ __device__ __forceinline__ void store_p32(uint8_t* pbase, int r, int key0, const
     }
 }
 
+__device__ __forceinline__ void softmax_bar(int id) {
+    asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+}
+
 template <bool kCausal>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse,
                   int seq, int heads) {
     extern __shared__ uint8_t smem_raw[];
@@ -69,9 +77,11 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* bar_qk = bar + 0;
     uint64_t* bar_v = bar + 1;
     uint64_t* bar_s = bar + 2;
-    uint64_t* bar_p = bar + 3;  // [2]
+    uint64_t* bar_p = bar + 3;  // [2], 8 arrivals (one per softmax warp)
     uint64_t* bar_o = bar + 5;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+    float* xmax = reinterpret_cast<float*>(smem + kSmemX);  // [2][128]
+    float* xsum = xmax + 2 * kBQ;                            // [2][128]
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int bh = blockIdx.x, b = bh / heads, hd = bh % heads;
@@ -83,7 +93,7 @@ __global__ void __launch_bounds__(256, 1)
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tm);
-        for (int i = 0; i < 6; ++i) ptx::mbar_init(&bar[i], i == 3 || i == 4 ? 4 : 1);
+        for (int i = 0; i < 6; ++i) ptx::mbar_init(&bar[i], i == 3 || i == 4 ? 8 : 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -136,29 +146,35 @@ __global__ void __launch_bounds__(256, 1)
             ptx::umma_commit(bar_o);
         }
     } else if (warp >= 4) {
-        const int qw = warp & 3;
-        const int r = qw * 32 + lane;  // query row within the tile
+        const int qw = warp & 3;          // TMEM lane quarter
+        const int sel = (warp - 4) >> 2;  // which interleaved 32-key chunks
+        const int r = qw * 32 + lane;     // query row within the tile
         const int i = q0 + r;
         const int n_valid = kCausal ? i + 1 : kv;
         const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
         ptx::mbar_wait(bar_s, 0);
         ptx::tc_fence_after();
-        float m = -INFINITY;
-        for (int c = 0; c < kv; c += 32) {
+        float m0 = -INFINITY, m1 = -INFINITY;
+        for (int c = sel * 32; c < kv; c += 64) {
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x32(trow + c, v);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                if (c + j < n_valid) m = fmaxf(m, __uint_as_float(v[j]));
+            for (int j = 0; j < 32; j += 2) {
+                if (c + j < n_valid) m0 = fmaxf(m0, __uint_as_float(v[j]));
+                if (c + j + 1 < n_valid) m1 = fmaxf(m1, __uint_as_float(v[j + 1]));
+            }
         }
+        xmax[sel * kBQ + r] = fmaxf(m0, m1);
+        softmax_bar(1);
+        const float m = fmaxf(xmax[r], xmax[kBQ + r]);
         const float sc = 0.125f * kLog2e;
         const float mc = m * sc;
-        float l = 0.0f;
+        float l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         for (int hf = 0; hf < halves; ++hf) {
             uint8_t* pbuf = smem + (hf == 0 ? kSmemP : kSmemK);
             const int end = kv < (hf + 1) * 256 ? kv : (hf + 1) * 256;
-            for (int c = hf * 256; c < end; c += 32) {
+            for (int c = hf * 256 + sel * 32; c < end; c += 64) {
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(trow + c, v);
                 ptx::tmem_ld_wait();
@@ -166,7 +182,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     p[j] = c + j < n_valid ? exp2f(fmaf(__uint_as_float(v[j]), sc, -mc)) : 0.0f;
-                    l += p[j];
+                    l[j & 3] += p[j];
                 }
                 store_p32(pbuf, r, c - hf * 256, p);
             }
@@ -175,14 +191,15 @@ __global__ void __launch_bounds__(256, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&bar_p[hf]);
         }
+        xsum[sel * kBQ + r] = (l[0] + l[1]) + (l[2] + l[3]);
+        softmax_bar(2);
+        const float inv = 1.0f / (xsum[r] + xsum[kBQ + r]);
         ptx::mbar_wait(bar_o, 0);
         ptx::tc_fence_after();
-        const float inv = 1.0f / l;
-        bf16* orow = out + static_cast<size_t>(row0 + i) * h + hd * kD;
-#pragma unroll
-        for (int c = 0; c < kD; c += 32) {
+        bf16* orow = out + static_cast<size_t>(row0 + i) * h + hd * kD + sel * 32;
+        {
             uint32_t v[32];
-            ptx::tmem_ld_32x32b_x32(trow + c, v);
+            ptx::tmem_ld_32x32b_x32(trow + sel * 32, v);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -191,10 +208,10 @@ __global__ void __launch_bounds__(256, 1)
                     ptx::pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv),
                     ptx::pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv),
                     ptx::pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv));
-                *reinterpret_cast<uint4*>(orow + c + 8 * q) = w;
+                *reinterpret_cast<uint4*>(orow + 8 * q) = w;
             }
         }
-        lse[static_cast<size_t>(bh) * seq + i] = (mc + log2f(l)) / kLog2e;
+        if (sel == 0) lse[static_cast<size_t>(bh) * seq + i] = (mc + log2f(xsum[r] + xsum[kBQ + r])) / kLog2e;
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -228,10 +245,10 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
     dim3 grid(batch * heads, seq / kBQ);
     if (causal) {
         set_smem_once<true>();
-        k_attn_fwd_tc<true><<<grid, 256, kSmemTotal, s>>>(tm, o, lse, seq, heads);
+        k_attn_fwd_tc<true><<<grid, kThreads, kSmemTotal, s>>>(tm, o, lse, seq, heads);
     } else {
         set_smem_once<false>();
-        k_attn_fwd_tc<false><<<grid, 256, kSmemTotal, s>>>(tm, o, lse, seq, heads);
+        k_attn_fwd_tc<false><<<grid, kThreads, kSmemTotal, s>>>(tm, o, lse, seq, heads);
     }
     check_cuda(cudaGetLastError(), "attention_fwd_tc");
 }

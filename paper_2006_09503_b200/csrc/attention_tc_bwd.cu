@@ -67,8 +67,12 @@ __device__ __forceinline__ void store_row32(uint8_t* base, int r, int col0, cons
     }
 }
 
+__device__ __forceinline__ void elem_bar(int id) {
+    asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+}
+
 template <bool kCausal>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                   const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
                   float* __restrict__ dq_part, int seq, int heads) {
@@ -78,11 +82,12 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* b_kv = bar + 0;
     uint64_t* b_qfull = bar + 1;   // [2]
     uint64_t* b_qempty = bar + 3;  // [2]
-    uint64_t* b_sdp = bar + 5;
-    uint64_t* b_pds = bar + 6;     // count 4
-    uint64_t* b_mm2 = bar + 7;
-    uint64_t* b_dqfree = bar + 8;  // count 4
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+    uint64_t* b_sdp = bar + 5;     // S^T / dP^T of an iteration are in TMEM
+    uint64_t* b_pds = bar + 6;     // 8 arrivals: P^T / dS^T written to SMEM
+    uint64_t* b_mm2 = bar + 7;     // dV / dK / dQ MMAs of an iteration done
+    uint64_t* b_dqfree = bar + 8;  // 8 arrivals: dQ TMEM read out
+    uint64_t* b_sdfree = bar + 9;  // 8 arrivals: S^T / dP^T TMEM read into registers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int bh = blockIdx.x, b = bh / heads, hd = bh % heads;
@@ -96,7 +101,7 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tm_qkv);
         ptx::tma_prefetch_desc(&tm_do);
-        for (int q = 0; q < 9; ++q) ptx::mbar_init(&bar[q], (q == 6 || q == 8) ? 4 : 1);
+        for (int q = 0; q < 10; ++q) ptx::mbar_init(&bar[q], (q == 6 || q == 8 || q == 9) ? 8 : 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -129,8 +134,7 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t id_sq = ptx::idesc_bf16(128, 128, false, false);  // S^T, dP^T
             const uint32_t id_kv = ptx::idesc_bf16(128, 64, false, true);    // dV, dK: B MN-major
             const uint32_t id_q = ptx::idesc_bf16(128, 64, true, true);      // dQ: A and B MN-major
-            ptx::mbar_wait(b_kv, 0);
-            for (int it = 0; it < iters; ++it) {
+            auto issue_sdp = [&](int it) {
                 const int buf = it & 1;
                 const uint32_t aQ = ptx::smem_u32(smem + oQ + buf * kTile);
                 const uint32_t aDO = ptx::smem_u32(smem + oDO + buf * kTile);
@@ -144,6 +148,19 @@ __global__ void __launch_bounds__(256, 1)
                                    ptx::sdesc_sw128(aDO + kk * 32, 16, 1024), id_sq, kk > 0);
                 }
                 ptx::umma_commit(b_sdp);
+            };
+            ptx::mbar_wait(b_kv, 0);
+            issue_sdp(0);
+            for (int it = 0; it < iters; ++it) {
+                const int buf = it & 1;
+                if (it + 1 < iters) {
+                    // S^T / dP^T of the next query tile overlap this tile's P / dS math
+                    ptx::mbar_wait(b_sdfree, it & 1);
+                    ptx::tc_fence_after();
+                    issue_sdp(it + 1);
+                }
+                const uint32_t aQ = ptx::smem_u32(smem + oQ + buf * kTile);
+                const uint32_t aDO = ptx::smem_u32(smem + oDO + buf * kTile);
                 ptx::mbar_wait(b_pds, it & 1);
                 if (it > 0) ptx::mbar_wait(b_dqfree, (it - 1) & 1);
                 ptx::tc_fence_after();
@@ -165,25 +182,22 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp >= 4) {
         const int qw = warp & 3;
-        const int r = qw * 32 + lane;  // key row (S^T / dP^T / dV / dK) or query row (dQ)
+        const int sel = (warp - 4) >> 2;  // 32-column chunks sel and sel + 2 of every 128
+        const int r = qw * 32 + lane;     // key row (S^T / dP^T / dV / dK) or query row (dQ)
         const int key = j * kT + r;
         const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
         const float sc = 0.125f * kLog2e;
-        auto flush_dq = [&](int it) {  // dQ partial of query tile i0 + it, row r
+        auto flush_dq = [&](int it) {  // dQ partial of query tile i0 + it: row r, columns sel*32..+31
             const int i = i0 + it;
             float* dst = dq_part + (static_cast<size_t>(j) * (static_cast<size_t>(gridDim.x / heads) * seq) +
-                                    static_cast<size_t>(row0 + i * kT + r)) * h + hd * kD;
+                                    static_cast<size_t>(row0 + i * kT + r)) * h + hd * kD + sel * 32;
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(trow + tDQ + sel * 32, v);
+            ptx::tmem_ld_wait();
 #pragma unroll
-            for (int c = 0; c < kD; c += 32) {
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(trow + tDQ + c, v);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int q = 0; q < 32; q += 4)
-                    *reinterpret_cast<float4*>(dst + c + q) =
-                        make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]), __uint_as_float(v[q + 2]),
-                                    __uint_as_float(v[q + 3]));
-            }
+            for (int q = 0; q < 32; q += 4)
+                *reinterpret_cast<float4*>(dst + q) = make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]),
+                                                                  __uint_as_float(v[q + 2]), __uint_as_float(v[q + 3]));
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(b_dqfree);
@@ -191,21 +205,29 @@ __global__ void __launch_bounds__(256, 1)
         for (int it = 0; it < iters; ++it) {
             const int buf = it & 1, i = i0 + it;
             ptx::mbar_wait(b_sdp, it & 1);
-            ptx::mbar_wait(&b_qfull[buf], (it >> 1) & 1);
             ptx::tc_fence_after();
+            uint32_t s0[32], d0[32], s1[32], d1[32];
+            ptx::tmem_ld_32x32b_x32(trow + tS + sel * 32, s0);
+            ptx::tmem_ld_32x32b_x32(trow + tDP + sel * 32, d0);
+            ptx::tmem_ld_32x32b_x32(trow + tS + sel * 32 + 64, s1);
+            ptx::tmem_ld_32x32b_x32(trow + tDP + sel * 32 + 64, d1);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(b_sdfree);  // the MMA may overwrite S^T / dP^T now
+            ptx::mbar_wait(&b_qfull[buf], (it >> 1) & 1);
             if (it > 0) {
-                ptx::mbar_wait(b_mm2, (it - 1) & 1);  // Pt / dSt free, dQ of it-1 ready
+                ptx::mbar_wait(b_mm2, (it - 1) & 1);  // P^T / dS^T free, dQ of it-1 ready
                 ptx::tc_fence_after();
                 flush_dq(it - 1);
             }
             const float* sl = reinterpret_cast<const float*>(smem + oLse + buf * kT * 4);
             const float* sd = reinterpret_cast<const float*>(smem + oDel + buf * kT * 4);
-#pragma unroll 1
-            for (int c = 0; c < kT; c += 32) {
-                uint32_t s[32], dp[32];
-                ptx::tmem_ld_32x32b_x32(trow + tS + c, s);
-                ptx::tmem_ld_32x32b_x32(trow + tDP + c, dp);
-                ptx::tmem_ld_wait();
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int c = sel * 32 + half * 64;
+                uint32_t(&s)[32] = half == 0 ? s0 : s1;
+                uint32_t(&dp)[32] = half == 0 ? d0 : d1;
                 float p[32], ds[32];
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
@@ -225,14 +247,13 @@ __global__ void __launch_bounds__(256, 1)
         ptx::mbar_wait(b_mm2, (iters - 1) & 1);
         ptx::tc_fence_after();
         flush_dq(iters - 1);
-        // dK (x 1/8) and dV for key row r
-        bf16* dk = dqkv + static_cast<size_t>(row0 + key) * 3 * h + h + hd * kD;
+        // dK (x 1/8) and dV for key row r, columns sel*32..+31
+        bf16* dk = dqkv + static_cast<size_t>(row0 + key) * 3 * h + h + hd * kD + sel * 32;
         bf16* dv = dk + h;
-#pragma unroll
-        for (int c = 0; c < kD; c += 32) {
+        {
             uint32_t vk[32], vv[32];
-            ptx::tmem_ld_32x32b_x32(trow + tDK + c, vk);
-            ptx::tmem_ld_32x32b_x32(trow + tDV + c, vv);
+            ptx::tmem_ld_32x32b_x32(trow + tDK + sel * 32, vk);
+            ptx::tmem_ld_32x32b_x32(trow + tDV + sel * 32, vv);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int q = 0; q < 32; q += 8) {
@@ -243,8 +264,8 @@ __global__ void __launch_bounds__(256, 1)
                                              __uint_as_float(vk[q + 2 * e + 1]) * 0.125f);
                     wv[e] = ptx::pack_bf16x2(__uint_as_float(vv[q + 2 * e]), __uint_as_float(vv[q + 2 * e + 1]));
                 }
-                *reinterpret_cast<uint4*>(dk + c + q) = make_uint4(wk[0], wk[1], wk[2], wk[3]);
-                *reinterpret_cast<uint4*>(dv + c + q) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                *reinterpret_cast<uint4*>(dk + q) = make_uint4(wk[0], wk[1], wk[2], wk[3]);
+                *reinterpret_cast<uint4*>(dv + q) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
             }
         }
     }
@@ -334,10 +355,10 @@ void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const fl
     dim3 grid(batch * heads, seq / kT);
     if (causal) {
         set_smem_once<true>();
-        k_attn_bwd_tc<true><<<grid, 256, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
+        k_attn_bwd_tc<true><<<grid, 384, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
     } else {
         set_smem_once<false>();
-        k_attn_bwd_tc<false><<<grid, 256, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
+        k_attn_bwd_tc<false><<<grid, 384, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
     }
     const size_t vecs = static_cast<size_t>(tokens) * h / 4;
     k_attn_dq_sum<<<static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 32u)), 256, 0, s>>>(

@@ -88,3 +88,13 @@ extern "C" int p2bw_kernel_softmax_xent(void* logits, const void* targets, int r
                      static_cast<float*>(row_loss), as_stream(stream));
     });
 }
+
+extern "C" int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream) {
+    return guarded([&] {
+        float* scratch = nullptr;
+        check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch), colsum_scratch_floats(rows, n) * sizeof(float),
+                                   as_stream(stream)), "cudaMallocAsync");
+        colsum_bf16(cb(x), rows, n, ld, static_cast<float*>(out), overwrite != 0, scratch, as_stream(stream));
+        check_cuda(cudaFreeAsync(scratch, as_stream(stream)), "cudaFreeAsync");
+    });
+}

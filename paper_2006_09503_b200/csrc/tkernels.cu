@@ -111,9 +111,18 @@ __global__ void k_reduce_parts(const float* __restrict__ part, int parts, int n,
     __shared__ float red[8][33];
     const int col = blockIdx.x * 32 + (threadIdx.x & 31);
     const int lane8 = threadIdx.x >> 5;
-    float acc = 0.0f;
-    if (col < n)
-        for (int p = lane8; p < parts; p += 8) acc += part[static_cast<size_t>(p) * n + col];
+    // four independent accumulators (parts p, p+8, p+16, p+24 of each stride of 32)
+    // keep four loads in flight; combined in a fixed order, so still deterministic
+    float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (col < n) {
+        int p = lane8;
+        for (; p + 24 < parts; p += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] += part[static_cast<size_t>(p + 8 * u) * n + col];
+        }
+        for (int u = 0; p < parts; p += 8, ++u) a[u & 3] += part[static_cast<size_t>(p) * n + col];
+    }
+    const float acc = (a[0] + a[1]) + (a[2] + a[3]);
     red[lane8][threadIdx.x & 31] = acc;
     __syncthreads();
     if (lane8 == 0 && col < n) {
@@ -482,6 +491,14 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
                    float* scratch, cudaStream_t s) {
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
     prof::Scope scope("layernorm_bwd", 0.0, (dres ? 10.0 : 8.0) * rows * h + 8.0 * rows, 5, s);
+    // gamma / beta statistics first: dx may alias dy (in-place LN backward)
+    const int rb = colsum_row_blocks(rows, h);
+    const int rpb = (rows + rb - 1) / rb;
+    float* pg = scratch;
+    float* pb = scratch + static_cast<size_t>(rb) * h;
+    k_colstats<true><<<dim3((h + 255) / 256, rb), 256, 0, s>>>(dy, x, mean, rstd, rows, h, h, rpb, pg, pb);
+    reduce_parts(pg, rb, h, dg, overwrite, s);
+    reduce_parts(pb, rb, h, db, overwrite, s);
     const int nv = (h / 8 + 31) / 32;
     const int grid = (rows + 7) / 8;
     switch (nv) {
@@ -491,13 +508,6 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
         case 4: k_ln_bwd_dx<4><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
         default: k_ln_bwd_dx<8><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
     }
-    const int rb = colsum_row_blocks(rows, h);
-    const int rpb = (rows + rb - 1) / rb;
-    float* pg = scratch;
-    float* pb = scratch + static_cast<size_t>(rb) * h;
-    k_colstats<true><<<dim3((h + 255) / 256, rb), 256, 0, s>>>(dy, x, mean, rstd, rows, h, h, rpb, pg, pb);
-    reduce_parts(pg, rb, h, dg, overwrite, s);
-    reduce_parts(pb, rb, h, db, overwrite, s);
     check_cuda(cudaGetLastError(), "layernorm_bwd");
 }
 

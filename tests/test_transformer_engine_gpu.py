@@ -60,6 +60,12 @@ def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows, seq):
         d_gpu, d_ref, d_van = finals[s] - w0, ref - w0, vr - w0
         err = np.linalg.norm(d_gpu - d_ref) / np.linalg.norm(d_ref)
         gap = np.linalg.norm(d_van - d_ref) / np.linalg.norm(d_ref)
+        lay = TO.stage_layout(spec, s * (spec.layers // depth), (s + 1) * (spec.layers // depth), s == 0,
+                              s == depth - 1)[0]
+        worst = sorted(((np.linalg.norm((d_gpu - d_ref)[o:o + int(np.prod(sh))]) /
+                         max(np.linalg.norm(d_ref[o:o + int(np.prod(sh))]), 1e-30), name)
+                        for name, (o, sh) in lay.items()), reverse=True)[:3]
+        print(f"stage {s}: delta err {err:.4f} gap {gap:.4f} worst tensors {worst}")
         assert err < DELTA_RTOL, (s, err)
         assert gap > 2 * err, (s, gap, err)  # 2BW is distinguishable from vanilla at this tolerance
 

@@ -107,3 +107,48 @@ def test_softmax_xent_vs_torch(rows, vocab):
     assert (logits.float()[:, :vocab] - lr.grad).abs().max().item() < 2e-3 / rows + 1e-5
     if vp > vocab:
         assert logits.float()[:, vocab:].abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("rows,n,ld", [(128, 128, 128), (128, 384, 384), (8192, 768, 768), (8192, 3072, 3072),
+                                       (300, 2304, 2304), (77, 512, 640)])
+@pytest.mark.parametrize("overwrite", [0, 1])
+def test_colsum_bias_grad_vs_torch(rows, n, ld, overwrite):
+    g = torch.Generator(device="cuda").manual_seed(rows + n + overwrite)
+    x = torch.randn(rows, ld, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.full((n,), 3.0, device="cuda")
+    call("p2bw_kernel_colsum", ptr(x), rows, n, ld, ptr(out), overwrite, stream())
+    torch.cuda.synchronize()
+    ref = x.float()[:, :n].sum(0) + (0.0 if overwrite else 3.0)
+    assert (out - ref).abs().max().item() < 1e-3 * max(1.0, ref.abs().max().item())
+
+
+@pytest.mark.parametrize("rows,h", [(128, 128), (4096, 768)])
+def test_layernorm_bwd_small_hidden(rows, h):
+    test_layernorm_fwd_bwd_vs_torch(rows, h)
+
+
+def test_layernorm_bwd_in_place():
+    """The last stage runs LNf backward with dx aliasing dy (model_transformer.cu)."""
+    rows, h = 256, 768
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(rows, h, device="cuda", generator=g).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).to(torch.bfloat16)
+    bb = torch.zeros(h, device="cuda").to(torch.bfloat16)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    call("p2bw_kernel_layernorm_fwd", ptr(x), ptr(w), ptr(bb), ptr(y), ptr(mean), ptr(rstd), rows, h, stream())
+    dy = torch.randn(rows, h, device="cuda", generator=g).to(torch.bfloat16)
+    buf = dy.clone()
+    dg = torch.empty(h, device="cuda")
+    db = torch.empty(h, device="cuda")
+    call("p2bw_kernel_layernorm_bwd", ptr(buf), ptr(x), ptr(mean), ptr(rstd), ptr(w), None, ptr(buf), ptr(dg),
+         ptr(db), 1, rows, h, stream())
+    xr = x.float().requires_grad_(True)
+    wr = w.float().requires_grad_(True)
+    br = bb.float().requires_grad_(True)
+    torch.nn.functional.layer_norm(xr, (h,), wr, br, 1e-5).backward(dy.float())
+    torch.cuda.synchronize()
+    assert (buf.float() - xr.grad).abs().max().item() < 3e-2 * max(1.0, xr.grad.abs().max().item())
+    assert (dg - wr.grad).abs().max().item() < 1e-2 * max(1.0, wr.grad.abs().max().item())
+    assert (db - br.grad).abs().max().item() < 1e-2 * max(1.0, br.grad.abs().max().item())
