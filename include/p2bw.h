@@ -247,6 +247,9 @@ int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void*
 int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                               const void* g, const void* dres, void* dx, void* dg, void* db,
                               int overwrite, int rows, int h, void* stream);
+/* Debug: per-CTA phase clocks of the tcgen05 attention forward into a device buffer
+ * of 16 uint64 per CTA (NULL switches it off). */
+int p2bw_debug_attention_timing(void* dev_buf);
 /* Column sums of a bf16 matrix (bias gradients): out (=|+=) sum_r x[r, :]. */
 int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream);
 /* Fused softmax cross-entropy: logits [rows x vp] -> dlogits in place, row_loss [rows]. */

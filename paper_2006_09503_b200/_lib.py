@@ -92,6 +92,7 @@ def _signatures():
         ("p2bw_kernel_layernorm_bwd", i, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp]),
         ("p2bw_kernel_softmax_xent", i, [vp, vp, i, i, i, C.c_float, vp, vp]),
         ("p2bw_kernel_colsum", i, [vp, i, i, i, vp, i, vp]),
+        ("p2bw_debug_attention_timing", i, [vp]),
     ]
 
 

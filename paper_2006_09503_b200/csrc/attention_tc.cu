@@ -63,6 +63,19 @@ __device__ __forceinline__ void store_p32(uint8_t* pbase, int r, int key0, const
     }
 }
 
+// Phase timestamps of every CTA (debug; null in production): p2bw_debug_attention_timing.
+__device__ unsigned long long* g_attn_dbg = nullptr;
+
+__device__ __forceinline__ void dbg_mark(unsigned long long* d, int slot) {
+    if (d != nullptr) d[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + slot] = clock64();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void softmax_bar(int id) {
     asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
 }
@@ -152,8 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int i = q0 + r;
         const int n_valid = kCausal ? i + 1 : kv;
         const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+        unsigned long long* dbg = (warp == 4 && lane == 0) ? g_attn_dbg : nullptr;
+        dbg_mark(dbg, 0);
+        if (dbg) dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 8] = gtimer();
         ptx::mbar_wait(bar_s, 0);
         ptx::tc_fence_after();
+        dbg_mark(dbg, 1);
         float m0 = -INFINITY, m1 = -INFINITY;
         for (int c = sel * 32; c < kv; c += 64) {
             uint32_t v[32];
@@ -166,7 +183,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         xmax[sel * kBQ + r] = fmaxf(m0, m1);
+        dbg_mark(dbg, 2);
         softmax_bar(1);
+        dbg_mark(dbg, 3);
         const float m = fmaxf(xmax[r], xmax[kBQ + r]);
         const float sc = 0.125f * kLog2e;
         const float mc = m * sc;
@@ -192,10 +211,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) ptx::mbar_arrive(&bar_p[hf]);
         }
         xsum[sel * kBQ + r] = (l[0] + l[1]) + (l[2] + l[3]);
+        dbg_mark(dbg, 4);
         softmax_bar(2);
         const float inv = 1.0f / (xsum[r] + xsum[kBQ + r]);
+        dbg_mark(dbg, 5);
         ptx::mbar_wait(bar_o, 0);
         ptx::tc_fence_after();
+        dbg_mark(dbg, 6);
         bf16* orow = out + static_cast<size_t>(row0 + i) * h + hd * kD + sel * 32;
         {
             uint32_t v[32];
@@ -212,6 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (sel == 0) lse[static_cast<size_t>(bh) * seq + i] = (mc + log2f(xsum[r] + xsum[kBQ + r])) / kLog2e;
+        dbg_mark(dbg, 7);
+        if (dbg) dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 9] = gtimer();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -237,6 +261,10 @@ void set_smem_once() {
 }  // namespace
 
 bool attention_tc_supported(int seq) { return seq >= 128 && seq <= 512 && seq % 128 == 0; }
+
+void attention_debug_timing(unsigned long long* dev_buf) {
+    check_cuda(cudaMemcpyToSymbol(g_attn_dbg, &dev_buf, sizeof(dev_buf)), "cudaMemcpyToSymbol(g_attn_dbg)");
+}
 
 void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
                       cudaStream_t s) {

@@ -46,6 +46,8 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int
                    cudaStream_t s);
 // tcgen05 forward (attention_tc.cu) for seq % 128 == 0, seq <= 512; attention_fwd dispatches.
 bool attention_tc_supported(int seq);
+// Debug: per-CTA phase timestamps of the tcgen05 forward into dev_buf[cta * 16 + slot] (null: off).
+void attention_debug_timing(unsigned long long* dev_buf);
 void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
                       cudaStream_t s);
 size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads);
