@@ -36,15 +36,16 @@ namespace {
 
 constexpr int kBQ = 128;
 constexpr int kD = 64;
-constexpr int kThreads = 384;                  // 4 role warps + 8 softmax warps
+constexpr int kGroups = 4;                     // softmax threads per query row
+constexpr int kThreads = 128 + 128 * kGroups;  // 4 role warps + 4*kGroups softmax warps
 constexpr int kRowBytes = 128;                 // one 64-element bf16 row
 constexpr int kTileBytes = kBQ * kRowBytes;    // 16 KB: 128 rows
 constexpr int kSmemQ = 0;
 constexpr int kSmemK = kSmemQ + kTileBytes;            // 4 tiles
 constexpr int kSmemV = kSmemK + 4 * kTileBytes;        // 4 tiles
 constexpr int kSmemP = kSmemV + 4 * kTileBytes;        // 4 blocks of 64 keys
-constexpr int kSmemX = kSmemP + 4 * kTileBytes;        // row max / sum exchange [2][2][128] f32
-constexpr int kSmemBar = kSmemX + 4 * kBQ * 4;
+constexpr int kSmemX = kSmemP + 4 * kTileBytes;        // row max / sum exchange [2][kGroups][128] f32
+constexpr int kSmemBar = kSmemX + 2 * kGroups * kBQ * 4;
 constexpr int kSmemTotal = kSmemBar + 128 + 1024;      // + barriers + alignment slack
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -77,7 +78,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 __device__ __forceinline__ void softmax_bar(int id) {
-    asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(128 * kGroups) : "memory");
 }
 
 template <bool kCausal>
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bar_o = bar + 5;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
     float* xmax = reinterpret_cast<float*>(smem + kSmemX);  // [2][128]
-    float* xsum = xmax + 2 * kBQ;                            // [2][128]
+    float* xsum = xmax + kGroups * kBQ;                      // [kGroups][128]
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int bh = blockIdx.x, b = bh / heads, hd = bh % heads;
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tm);
-        for (int i = 0; i < 6; ++i) ptx::mbar_init(&bar[i], i == 3 || i == 4 ? 8 : 1);
+        for (int i = 0; i < 6; ++i) ptx::mbar_init(&bar[i], i == 3 || i == 4 ? 4 * kGroups : 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         const int qw = warp & 3;          // TMEM lane quarter
-        const int sel = (warp - 4) >> 2;  // which interleaved 32-key chunks
+        const int sel = (warp - 4) >> 2;  // which interleaved 32-key chunks (of kGroups)
         const int r = qw * 32 + lane;     // query row within the tile
         const int i = q0 + r;
         const int n_valid = kCausal ? i + 1 : kv;
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         dbg_mark(dbg, 1);
         float m0 = -INFINITY, m1 = -INFINITY;
-        for (int c = sel * 32; c < kv; c += 64) {
+        for (int c = sel * 32; c < kv; c += 32 * kGroups) {
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x32(trow + c, v);
             ptx::tmem_ld_wait();
@@ -186,21 +187,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         dbg_mark(dbg, 2);
         softmax_bar(1);
         dbg_mark(dbg, 3);
-        const float m = fmaxf(xmax[r], xmax[kBQ + r]);
+        float m = xmax[r];
+#pragma unroll
+        for (int g = 1; g < kGroups; ++g) m = fmaxf(m, xmax[g * kBQ + r]);
         const float sc = 0.125f * kLog2e;
         const float mc = m * sc;
         float l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         for (int hf = 0; hf < halves; ++hf) {
             uint8_t* pbuf = smem + (hf == 0 ? kSmemP : kSmemK);
             const int end = kv < (hf + 1) * 256 ? kv : (hf + 1) * 256;
-            for (int c = hf * 256 + sel * 32; c < end; c += 64) {
+            for (int c = hf * 256 + sel * 32; c < end; c += 32 * kGroups) {
                 uint32_t v[32];
                 ptx::tmem_ld_32x32b_x32(trow + c, v);
                 ptx::tmem_ld_wait();
                 float p[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    p[j] = c + j < n_valid ? exp2f(fmaf(__uint_as_float(v[j]), sc, -mc)) : 0.0f;
+                    p[j] = c + j < n_valid ? ptx::ex2(fmaf(__uint_as_float(v[j]), sc, -mc)) : 0.0f;
                     l[j & 3] += p[j];
                 }
                 store_p32(pbuf, r, c - hf * 256, p);
@@ -213,18 +216,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         xsum[sel * kBQ + r] = (l[0] + l[1]) + (l[2] + l[3]);
         dbg_mark(dbg, 4);
         softmax_bar(2);
-        const float inv = 1.0f / (xsum[r] + xsum[kBQ + r]);
+        float ltot = xsum[r];
+#pragma unroll
+        for (int g = 1; g < kGroups; ++g) ltot += xsum[g * kBQ + r];
+        const float inv = 1.0f / ltot;
         dbg_mark(dbg, 5);
         ptx::mbar_wait(bar_o, 0);
         ptx::tc_fence_after();
         dbg_mark(dbg, 6);
-        bf16* orow = out + static_cast<size_t>(row0 + i) * h + hd * kD + sel * 32;
+        bf16* orow = out + static_cast<size_t>(row0 + i) * h + hd * kD + sel * (kD / kGroups);
         {
-            uint32_t v[32];
-            ptx::tmem_ld_32x32b_x32(trow + sel * 32, v);
+            uint32_t v[16];
+            ptx::tmem_ld_32x32b_x16(trow + sel * (kD / kGroups), v);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < 2; ++q) {
                 const uint4 w = make_uint4(
                     ptx::pack_bf16x2(__uint_as_float(v[8 * q]) * inv, __uint_as_float(v[8 * q + 1]) * inv),
                     ptx::pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv),
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 *reinterpret_cast<uint4*>(orow + 8 * q) = w;
             }
         }
-        if (sel == 0) lse[static_cast<size_t>(bh) * seq + i] = (mc + log2f(xsum[r] + xsum[kBQ + r])) / kLog2e;
+        if (sel == 0) lse[static_cast<size_t>(bh) * seq + i] = (mc + log2f(ltot)) / kLog2e;
         dbg_mark(dbg, 7);
         if (dbg) dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 9] = gtimer();
     }

@@ -99,7 +99,10 @@ __device__ __forceinline__ void bulk_wait_read() {
 // Byte offset of 16-byte chunk j of row r in a 128 B-row SW128 staging buffer.
 __device__ __forceinline__ int swz(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
 
-template <int BN, bool kAMN, bool kBMN, EpiKind kKind>
+// kCl == 2: two CTAs of a cluster take vertically adjacent M tiles of the same N
+// tile; each loads half of the shared B tile and TMA-multicasts it to both, which
+// halves the L2 -> SM bytes of B (the GEMMs here are L2-bandwidth bound).
+template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ EpiMaps em, const KParams p) {
@@ -122,11 +125,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x % 32;
     const int tiles_m = (p.m + kBM - 1) / kBM;
     const int tiles_n = p.n / BN + (p.n % BN != 0);
-    const int num_tiles = tiles_m * tiles_n;
     const int kblocks = (p.k + kBK - 1) / kBK;
-    // work item w: output tile (w % num_tiles), K slice (w / num_tiles) of kb_per k-blocks
+    // work item w: tile group (w % num_tiles) -- kCl vertically adjacent M tiles of one
+    // N tile, this CTA taking M tile kCl*g + rank -- and K slice (w / num_tiles)
+    const int rank = kCl == 2 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+    const int tiles_mg = (tiles_m + kCl - 1) / kCl;
+    const int num_tiles = tiles_mg * tiles_n;
     const int num_work = num_tiles * p.splits;
     const int kb_per = (kblocks + p.splits - 1) / p.splits;
+    const int w0 = blockIdx.x / kCl, wstep = gridDim.x / kCl;
+    constexpr uint16_t kMask = kCl == 2 ? 0x3 : 0x1;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmap_a);
@@ -134,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&em.d);
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], kCl);  // both CTAs' MMAs free a stage
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull_bar[i], 1);
@@ -145,7 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (kCl == 2) ptx::cluster_sync();  // peer barriers initialised before any multicast
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -153,10 +162,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+            for (int w = w0; w < num_work; w += wstep) {
                 const int tile = w % num_tiles;
-                const int m0 = (tile % tiles_m) * kBM;
-                const int n0 = (tile / tiles_m) * BN;
+                const int m0 = ((tile % tiles_mg) * kCl + rank) * kBM;
+                const int n0 = (tile / tiles_mg) * BN;
                 const int kb0 = (w / num_tiles) * kb_per;
                 const int kb1 = min(kblocks, kb0 + kb_per);
                 for (int kb = kb0; kb < kb1; ++kb) {
@@ -172,7 +181,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         ptx::tma_load_2d(da, &tmap_a, &full_bar[stage], k0, m0);
                     }
-                    if constexpr (kBMN) {
+                    if constexpr (kCl == 2) {  // my half of B, multicast to both CTAs
+                        if constexpr (kBMN) {
+#pragma unroll
+                            for (int j = rank * BN / 128; j < (rank + 1) * BN / 128; ++j)
+                                ptx::tma_load_2d_mc(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage], n0 + j * 64,
+                                                    k0, kMask);
+                        } else {
+                            ptx::tma_load_2d_mc(db + rank * (BN / 2) * 128, &tmap_b, &full_bar[stage], k0,
+                                                n0 + rank * (BN / 2), kMask);
+                        }
+                    } else if constexpr (kBMN) {
 #pragma unroll
                         for (int j = 0; j < BN / 64; ++j)
                             ptx::tma_load_2d(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage], n0 + j * 64, k0);
@@ -201,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+            for (int w = w0; w < num_work; w += wstep) {
                 const int kb0 = (w / num_tiles) * kb_per;
                 const int kb1 = min(kblocks, kb0 + kb_per);
                 ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -218,7 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t bd = ptx::sdesc_sw128(b_addr + kk * b_kstep, b_lbo, b_sbo);
                         ptx::umma_bf16(d_tmem, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
                     }
-                    ptx::umma_commit(&empty_bar[stage]);
+                    if constexpr (kCl == 2) ptx::umma_commit_mc(&empty_bar[stage], kMask);
+                    else ptx::umma_commit(&empty_bar[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -247,10 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int slot = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+        for (int w = w0; w < num_work; w += wstep) {
             const int tile = w % num_tiles;
-            const int m0 = (tile % tiles_m) * kBM;
-            const int n0 = (tile / tiles_m) * BN;
+            const int m0 = ((tile % tiles_mg) * kCl + rank) * kBM;
+            const int n0 = (tile / tiles_mg) * BN;
             const int r0 = m0 + q * 32;
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
@@ -385,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (kCl == 2) ptx::cluster_sync();  // no CTA exits while its peer may still signal it
+    else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
@@ -434,10 +455,10 @@ CUtensorMap make_map(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld
     return make_map_t(ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, inner, outer, ld_elems, 64, box_outer);
 }
 
-template <int BN, bool kAMN, bool kBMN, EpiKind kKind>
+template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p, cudaStream_t s) {
     using Cfg = GemmCfg<BN>;
-    auto kern = gemm_tc_kernel<BN, kAMN, kBMN, kKind>;
+    auto kern = gemm_tc_kernel<BN, kAMN, kBMN, kKind, kCl>;
     static std::atomic<uint32_t> configured{0};  // one attribute call per device
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
@@ -447,42 +468,74 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, con
                    "cudaFuncSetAttribute(gemm smem)");
         configured.fetch_or(bit);
     }
-    const int work = ((p.m + kBM - 1) / kBM) * ((p.n + BN - 1) / BN) * p.splits;
-    const int grid = work < num_sms() ? work : num_sms();
-    kern<<<grid, kThreads, Cfg::kSmemBytes, s>>>(ta, tb, em, p);
-    check_cuda(cudaGetLastError(), "gemm_tc_kernel launch");
+    const int tiles_mg = ((p.m + kBM - 1) / kBM + kCl - 1) / kCl;
+    const int work = tiles_mg * ((p.n + BN - 1) / BN) * p.splits;
+    const int slots = num_sms() / kCl;
+    const int grid = kCl * (work < slots ? work : slots);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, em, p), "gemm_tc_kernel launch");
 }
 
-template <int BN, bool kAMN, bool kBMN>
+template <int BN, bool kAMN, bool kBMN, int kCl>
 void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p,
                   cudaStream_t s) {
     switch (p.epi.kind) {
-        case EpiKind::StoreBF16: launch<BN, kAMN, kBMN, EpiKind::StoreBF16>(ta, tb, em, p, s); break;
-        case EpiKind::StoreF32: launch<BN, kAMN, kBMN, EpiKind::StoreF32>(ta, tb, em, p, s); break;
-        case EpiKind::DGeluBF16: launch<BN, kAMN, kBMN, EpiKind::DGeluBF16>(ta, tb, em, p, s); break;
+        case EpiKind::StoreBF16: launch<BN, kAMN, kBMN, EpiKind::StoreBF16, kCl>(ta, tb, em, p, s); break;
+        case EpiKind::StoreF32: launch<BN, kAMN, kBMN, EpiKind::StoreF32, kCl>(ta, tb, em, p, s); break;
+        case EpiKind::DGeluBF16: launch<BN, kAMN, kBMN, EpiKind::DGeluBF16, kCl>(ta, tb, em, p, s); break;
     }
 }
 
-template <int BN>
+template <int BN, int kCl>
 void dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em,
                     const KParams& p, cudaStream_t s) {
-    if (!amn && !bmn) dispatch_epi<BN, false, false>(ta, tb, em, p, s);
-    else if (!amn && bmn) dispatch_epi<BN, false, true>(ta, tb, em, p, s);
-    else if (amn && !bmn) dispatch_epi<BN, true, false>(ta, tb, em, p, s);
-    else dispatch_epi<BN, true, true>(ta, tb, em, p, s);
+    if (!amn && !bmn) dispatch_epi<BN, false, false, kCl>(ta, tb, em, p, s);
+    else if (!amn && bmn) dispatch_epi<BN, false, true, kCl>(ta, tb, em, p, s);
+    else if (amn && !bmn) dispatch_epi<BN, true, false, kCl>(ta, tb, em, p, s);
+    else dispatch_epi<BN, true, true, kCl>(ta, tb, em, p, s);
 }
 
-// Pick the N tile that wastes the fewest MMA slots over whole waves of SMs.
-int choose_bn(int m, int n) {
-    if (n % 256 != 0) return 128;
+struct TileChoice {
+    int bn;
+    int cl;
+};
+
+// Tile shape and cluster size minimising a two-resource cost model: per k-block a
+// tile needs max(MMA cycles = 2 BN, L2->SM cycles = bytes / ~45 B/clk), where a
+// 2-CTA cluster halves the B bytes; whole waves of SM (pairs) are paid for.
+TileChoice choose_tile(int m, int n, int k) {
     const long tm = (m + kBM - 1) / kBM;
     const long sms = num_sms();
-    auto cost = [&](long bn) {
-        const long tiles = tm * ((n + bn - 1) / bn);
-        const long waves = (tiles + sms - 1) / sms;
-        return waves * bn;  // proportional to the busiest SM's MMA time
-    };
-    return cost(256) <= cost(128) ? 256 : 128;
+    const long kblocks = (k + kBK - 1) / kBK;
+    TileChoice best{128, 1};
+    double best_cost = 1e300;
+    for (const int bn : {128, 256}) {
+        if (bn == 256 && n % 256 != 0 && n < 256) continue;
+        for (const int cl : {1, 2}) {
+            const long tiles = ((tm + cl - 1) / cl) * ((n + bn - 1) / bn);
+            const long slots = sms / cl;
+            const long waves = (tiles + slots - 1) / slots;
+            const double mma = 2.0 * bn;
+            const double l2 = (16384.0 + 128.0 * bn / cl) / 45.0;
+            const double cost = static_cast<double>(waves) * kblocks * std::max(mma, l2);
+            if (cost < best_cost * 0.999 || (cost <= best_cost * 1.001 && cl > best.cl)) {
+                best_cost = cost;
+                best = {bn, cl};
+            }
+        }
+    }
+    return best;
 }
 
 }  // namespace
@@ -502,11 +555,13 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         throw Error("gemm: fp32 epilogue supports beta 0 (store) or 1 (TMA reduce-add) only");
     if ((epi.ldd % 8) != 0 || (epi.residual && epi.ldr % 8 != 0))
         throw Error("gemm: output leading dims must be multiples of 8");
-    const int bn = choose_bn(m, n);
+    const TileChoice tc = choose_tile(m, n, k);
+    const int bn = tc.bn, cl = tc.cl;
     const bool amn = a.major == Major::MN, bmn = b.major == Major::MN;
-    // A: rows = m (tile kBM), B: rows = n (tile bn).  K-major maps put k innermost.
+    // A: rows = m (tile kBM), B: rows = n (tile bn; each CTA of a pair loads bn / 2).
+    // K-major maps put k innermost.
     const CUtensorMap ta = amn ? make_map(a.ptr, m, k, a.ld, kBK) : make_map(a.ptr, k, m, a.ld, kBM);
-    const CUtensorMap tb = bmn ? make_map(b.ptr, n, k, b.ld, kBK) : make_map(b.ptr, k, n, b.ld, bn);
+    const CUtensorMap tb = bmn ? make_map(b.ptr, n, k, b.ld, kBK) : make_map(b.ptr, k, n, b.ld, bn / cl);
     EpiMaps em{};
     if (epi.kind == EpiKind::StoreF32) {
         em.d = make_map_t(epi.d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n, m, epi.ldd, 32, 32);
@@ -548,8 +603,10 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     prof::Scope scope("gemm", 2.0 * m * n * k,
                       2.0 * (static_cast<double>(m) * k + static_cast<double>(n) * k) + out_bytes * m * n, 1,
                       stream);
-    if (bn == 256) dispatch_major<256>(amn, bmn, ta, tb, em, p, stream);
-    else dispatch_major<128>(amn, bmn, ta, tb, em, p, stream);
+    if (bn == 256 && cl == 2) dispatch_major<256, 2>(amn, bmn, ta, tb, em, p, stream);
+    else if (bn == 256) dispatch_major<256, 1>(amn, bmn, ta, tb, em, p, stream);
+    else if (cl == 2) dispatch_major<128, 2>(amn, bmn, ta, tb, em, p, stream);
+    else dispatch_major<128, 1>(amn, bmn, ta, tb, em, p, stream);
 }
 
 int num_sms() {
