@@ -72,7 +72,7 @@ __device__ __forceinline__ void elem_bar(int id) {
 }
 
 template <bool kCausal>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(640, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                   const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
                   float* __restrict__ dq_part, int seq, int heads) {
@@ -83,10 +83,10 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* b_qfull = bar + 1;   // [2]
     uint64_t* b_qempty = bar + 3;  // [2]
     uint64_t* b_sdp = bar + 5;     // S^T / dP^T of an iteration are in TMEM
-    uint64_t* b_pds = bar + 6;     // 8 arrivals: P^T / dS^T written to SMEM
+    uint64_t* b_pds = bar + 6;     // 16 arrivals: P^T / dS^T written to SMEM
     uint64_t* b_mm2 = bar + 7;     // dV / dK / dQ MMAs of an iteration done
-    uint64_t* b_dqfree = bar + 8;  // 8 arrivals: dQ TMEM read out
-    uint64_t* b_sdfree = bar + 9;  // 8 arrivals: S^T / dP^T TMEM read into registers
+    uint64_t* b_dqfree = bar + 8;  // 16 arrivals: dQ TMEM read out
+    uint64_t* b_sdfree = bar + 9;  // 16 arrivals: S^T / dP^T TMEM read into registers
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tm_qkv);
         ptx::tma_prefetch_desc(&tm_do);
-        for (int q = 0; q < 10; ++q) ptx::mbar_init(&bar[q], (q == 6 || q == 8 || q == 9) ? 8 : 1);
+        for (int q = 0; q < 10; ++q) ptx::mbar_init(&bar[q], (q == 6 || q == 8 || q == 9) ? 16 : 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -181,21 +181,23 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp >= 4) {
+        // 16 elementwise warps: 4 threads per key row, thread `sel` owns query columns
+        // [32 sel, 32 sel + 32) of every 128-query tile and 16 of the 64 head dims.
         const int qw = warp & 3;
-        const int sel = (warp - 4) >> 2;  // 32-column chunks sel and sel + 2 of every 128
+        const int sel = (warp - 4) >> 2;
         const int r = qw * 32 + lane;     // key row (S^T / dP^T / dV / dK) or query row (dQ)
         const int key = j * kT + r;
         const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
         const float sc = 0.125f * kLog2e;
-        auto flush_dq = [&](int it) {  // dQ partial of query tile i0 + it: row r, columns sel*32..+31
+        auto flush_dq = [&](int it) {  // dQ partial of query tile i0 + it: row r, dims 16 sel..+15
             const int i = i0 + it;
             float* dst = dq_part + (static_cast<size_t>(j) * (static_cast<size_t>(gridDim.x / heads) * seq) +
-                                    static_cast<size_t>(row0 + i * kT + r)) * h + hd * kD + sel * 32;
-            uint32_t v[32];
-            ptx::tmem_ld_32x32b_x32(trow + tDQ + sel * 32, v);
+                                    static_cast<size_t>(row0 + i * kT + r)) * h + hd * kD + sel * 16;
+            uint32_t v[16];
+            ptx::tmem_ld_32x32b_x16(trow + tDQ + sel * 16, v);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int q = 0; q < 32; q += 4)
+            for (int q = 0; q < 16; q += 4)
                 *reinterpret_cast<float4*>(dst + q) = make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]),
                                                                   __uint_as_float(v[q + 2]), __uint_as_float(v[q + 3]));
             ptx::tc_fence_before();
@@ -206,11 +208,9 @@ __global__ void __launch_bounds__(384, 1)
             const int buf = it & 1, i = i0 + it;
             ptx::mbar_wait(b_sdp, it & 1);
             ptx::tc_fence_after();
-            uint32_t s0[32], d0[32], s1[32], d1[32];
-            ptx::tmem_ld_32x32b_x32(trow + tS + sel * 32, s0);
-            ptx::tmem_ld_32x32b_x32(trow + tDP + sel * 32, d0);
-            ptx::tmem_ld_32x32b_x32(trow + tS + sel * 32 + 64, s1);
-            ptx::tmem_ld_32x32b_x32(trow + tDP + sel * 32 + 64, d1);
+            uint32_t s[32], dp[32];
+            ptx::tmem_ld_32x32b_x32(trow + tS + sel * 32, s);
+            ptx::tmem_ld_32x32b_x32(trow + tDP + sel * 32, dp);
             ptx::tmem_ld_wait();
             ptx::tc_fence_before();
             __syncwarp();
@@ -223,22 +223,17 @@ __global__ void __launch_bounds__(384, 1)
             }
             const float* sl = reinterpret_cast<const float*>(smem + oLse + buf * kT * 4);
             const float* sd = reinterpret_cast<const float*>(smem + oDel + buf * kT * 4);
+            const int c = sel * 32;
+            float p[32], ds[32];
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int c = sel * 32 + half * 64;
-                uint32_t(&s)[32] = half == 0 ? s0 : s1;
-                uint32_t(&dp)[32] = half == 0 ? d0 : d1;
-                float p[32], ds[32];
-#pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const int qi = i * kT + c + q;  // absolute query index
-                    const bool vis = !kCausal || qi >= key;
-                    p[q] = vis ? exp2f(fmaf(__uint_as_float(s[q]), sc, -sl[c + q] * kLog2e)) : 0.0f;
-                    ds[q] = p[q] * (__uint_as_float(dp[q]) - sd[c + q]);
-                }
-                store_row32(smem + oPt, r, c, p);
-                store_row32(smem + oDSt, r, c, ds);
+            for (int q = 0; q < 32; ++q) {
+                const int qi = i * kT + c + q;  // absolute query index
+                const bool vis = !kCausal || qi >= key;
+                p[q] = vis ? ptx::ex2(fmaf(__uint_as_float(s[q]), sc, -sl[c + q] * kLog2e)) : 0.0f;
+                ds[q] = p[q] * (__uint_as_float(dp[q]) - sd[c + q]);
             }
+            store_row32(smem + oPt, r, c, p);
+            store_row32(smem + oDSt, r, c, ds);
             ptx::fence_proxy_async();
             ptx::tc_fence_before();
             __syncwarp();
@@ -247,16 +242,16 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_wait(b_mm2, (iters - 1) & 1);
         ptx::tc_fence_after();
         flush_dq(iters - 1);
-        // dK (x 1/8) and dV for key row r, columns sel*32..+31
-        bf16* dk = dqkv + static_cast<size_t>(row0 + key) * 3 * h + h + hd * kD + sel * 32;
+        // dK (x 1/8) and dV for key row r, dims 16 sel..+15
+        bf16* dk = dqkv + static_cast<size_t>(row0 + key) * 3 * h + h + hd * kD + sel * 16;
         bf16* dv = dk + h;
         {
-            uint32_t vk[32], vv[32];
-            ptx::tmem_ld_32x32b_x32(trow + tDK + sel * 32, vk);
-            ptx::tmem_ld_32x32b_x32(trow + tDV + sel * 32, vv);
+            uint32_t vk[16], vv[16];
+            ptx::tmem_ld_32x32b_x16(trow + tDK + sel * 16, vk);
+            ptx::tmem_ld_32x32b_x16(trow + tDV + sel * 16, vv);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int q = 0; q < 32; q += 8) {
+            for (int q = 0; q < 16; q += 8) {
                 uint32_t wk[4], wv[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -355,10 +350,10 @@ void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const fl
     dim3 grid(batch * heads, seq / kT);
     if (causal) {
         set_smem_once<true>();
-        k_attn_bwd_tc<true><<<grid, 384, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
+        k_attn_bwd_tc<true><<<grid, 640, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
     } else {
         set_smem_once<false>();
-        k_attn_bwd_tc<false><<<grid, 384, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
+        k_attn_bwd_tc<false><<<grid, 640, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
     }
     const size_t vecs = static_cast<size_t>(tokens) * h / 4;
     k_attn_dq_sum<<<static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 32u)), 256, 0, s>>>(

@@ -18,7 +18,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -515,6 +518,11 @@ struct TileChoice {
 // tile needs max(MMA cycles = 2 BN, L2->SM cycles = bytes / ~45 B/clk), where a
 // 2-CTA cluster halves the B bytes; whole waves of SM (pairs) are paid for.
 TileChoice choose_tile(int m, int n, int k) {
+    if (const char* env = std::getenv("P2BW_GEMM_TILE")) {  // tuning knob: "bn,cl"
+        int bn = 0, cl = 0;
+        if (std::sscanf(env, "%d,%d", &bn, &cl) == 2 && (bn == 128 || bn == 256) && (cl == 1 || cl == 2))
+            return {bn, cl};
+    }
     const long tm = (m + kBM - 1) / kBM;
     const long sms = num_sms();
     const long kblocks = (k + kBK - 1) / kBK;
