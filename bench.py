@@ -315,6 +315,7 @@ def run_ours(args, c):
         "gpu_launches_per_step": round(launches / total_batches, 1),
         "mfu": round(mfu, 4), "flops_per_sample": fps,
         "roofline": roofline, "kernel_breakdown": breakdown,
+        "kernel_ms_per_step": round(tot_ms / steps, 3) if classes else None,
         "cpu_baseline": cpu, "clocks": clk,
         "loss_first_last": [float(losses[0]), float(losses[-1])],
         "wall_s": round(wall, 2),

@@ -39,15 +39,19 @@ constexpr int kBK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kThreads = 256;
 constexpr int kEpiBuf = 32 * 128;  // one staging buffer: 32 rows x 128 B (TMA box, SW128)
 
-template <int BN>
+// kCl == 2 is the CTA-pair (cta_group::2) mode: each CTA holds its own 128 rows of A
+// and HALF of the B tile, so the same SMEM carries a deeper stage ring.
+template <int BN, int kCl>
 struct GemmCfg {
-    static constexpr int kStages = BN == 256 ? 4 : 6;
     static constexpr int kABytes = kBM * kBK * 2;
-    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kBBytes = (BN / kCl) * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = 2 * BN;  // 256 or 512: a power of two
     static constexpr int kEpiBytes = 4 * 2 * kEpiBuf;  // 4 epilogue warps x 2 buffers
-    static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kFixed = kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kStages0 = (227 * 1024 - kFixed) / kStageBytes;
+    static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kFixed;
 };
 
 __device__ __forceinline__ float gelu_fwd(float x) {
@@ -102,14 +106,16 @@ __device__ __forceinline__ void bulk_wait_read() {
 // Byte offset of 16-byte chunk j of row r in a 128 B-row SW128 staging buffer.
 __device__ __forceinline__ int swz(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
 
-// kCl == 2: two CTAs of a cluster take vertically adjacent M tiles of the same N
-// tile; each loads half of the shared B tile and TMA-multicasts it to both, which
-// halves the L2 -> SM bytes of B (the GEMMs here are L2-bandwidth bound).
+// kCl == 2: a CTA pair (cluster of 2) computes one 256 x BN tile with cta_group::2
+// MMAs issued by the even CTA: each CTA TMA-loads its own 128 A rows and half of the
+// B tile into its SMEM (completing on the leader's full barrier), the accumulator
+// rows land in each CTA's own TMEM, and both epilogues release the leader's TMEM
+// buffer through remote mbarrier arrivals.
 template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ EpiMaps em, const KParams p) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, kCl>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -145,16 +151,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&em.d);
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], kCl);  // both CTAs' MMAs free a stage
+            ptx::mbar_init(&empty_bar[s], 1);  // the (leader's) MMA commit frees a stage
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull_bar[i], 1);
-            ptx::mbar_init(&tempty_bar[i], 4);
+            ptx::mbar_init(&tempty_bar[i], 4 * kCl);  // pair mode: both CTAs' epilogues
         }
         for (int i = 0; i < 4; ++i) ptx::mbar_init(&aux_bar[i], 1);
         ptx::fence_mbar_init();
     }
-    if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    if (warp == 2) {
+        if constexpr (kCl == 2) ptx::tmem_alloc_2sm<Cfg::kTmemCols>(tmem_slot);
+        else ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    }
     ptx::tc_fence_before();
     if constexpr (kCl == 2) ptx::cluster_sync();  // peer barriers initialised before any multicast
     else __syncthreads();
@@ -173,10 +182,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int kb1 = min(kblocks, kb0 + kb_per);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
                     uint8_t* da = s_a + stage * Cfg::kABytes;
                     uint8_t* db = s_b + stage * Cfg::kBBytes;
                     const int k0 = kb * kBK;
+                    if constexpr (kCl == 2) {
+                        // both CTAs' bytes complete on the leader's full barrier
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+                        if constexpr (kAMN) {
+#pragma unroll
+                            for (int j = 0; j < kBM / 64; ++j)
+                                ptx::tma_load_2d_2sm(da + j * 64 * kBK * 2, &tmap_a, &full_bar[stage], m0 + j * 64,
+                                                     k0);
+                        } else {
+                            ptx::tma_load_2d_2sm(da, &tmap_a, &full_bar[stage], k0, m0);
+                        }
+                        const int nb = n0 + rank * (BN / 2);  // my half of the B tile
+                        if constexpr (kBMN) {
+#pragma unroll
+                            for (int j = 0; j < BN / 128; ++j)
+                                ptx::tma_load_2d_2sm(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage], nb + j * 64,
+                                                     k0);
+                        } else {
+                            ptx::tma_load_2d_2sm(db, &tmap_b, &full_bar[stage], k0, nb);
+                        }
+                    } else {
+                    ptx::mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
                     if constexpr (kAMN) {
 #pragma unroll
                         for (int j = 0; j < kBM / 64; ++j)
@@ -184,22 +214,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         ptx::tma_load_2d(da, &tmap_a, &full_bar[stage], k0, m0);
                     }
-                    if constexpr (kCl == 2) {  // my half of B, multicast to both CTAs
-                        if constexpr (kBMN) {
-#pragma unroll
-                            for (int j = rank * BN / 128; j < (rank + 1) * BN / 128; ++j)
-                                ptx::tma_load_2d_mc(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage], n0 + j * 64,
-                                                    k0, kMask);
-                        } else {
-                            ptx::tma_load_2d_mc(db + rank * (BN / 2) * 128, &tmap_b, &full_bar[stage], k0,
-                                                n0 + rank * (BN / 2), kMask);
-                        }
-                    } else if constexpr (kBMN) {
+                    if constexpr (kBMN) {
 #pragma unroll
                         for (int j = 0; j < BN / 64; ++j)
                             ptx::tma_load_2d(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage], n0 + j * 64, k0);
                     } else {
                         ptx::tma_load_2d(db, &tmap_b, &full_bar[stage], k0, n0);
+                    }
                     }
                     if (++stage == S) {
                         stage = 0;
@@ -209,8 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16(kBM, BN, kAMN, kBMN);
+        if (lane == 0 && rank == 0) {  // pair mode: the even CTA issues for both
+            constexpr uint32_t idesc = ptx::idesc_bf16(kBM * kCl, BN, kAMN, kBMN);
             // K-major SW128: rows of 128 B, 8-row groups 1024 B apart; a K step of 16
             // elements is +32 B inside the swizzle atom.  MN-major SW128: 64-element MN
             // groups one TMA box (kBK rows x 128 B) apart, 8-row K groups 1024 B apart;
@@ -238,16 +259,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint64_t ad = ptx::sdesc_sw128(a_addr + kk * a_kstep, a_lbo, a_sbo);
                         const uint64_t bd = ptx::sdesc_sw128(b_addr + kk * b_kstep, b_lbo, b_sbo);
-                        ptx::umma_bf16(d_tmem, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
+                        const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
+                        if constexpr (kCl == 2) ptx::umma_bf16_2sm(d_tmem, ad, bd, idesc, accum);
+                        else ptx::umma_bf16(d_tmem, ad, bd, idesc, accum);
                     }
-                    if constexpr (kCl == 2) ptx::umma_commit_mc(&empty_bar[stage], kMask);
+                    if constexpr (kCl == 2) ptx::umma_commit_2sm_mc(&empty_bar[stage], kMask);
                     else ptx::umma_commit(&empty_bar[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                ptx::umma_commit(&tfull_bar[acc]);
+                if constexpr (kCl == 2) ptx::umma_commit_2sm_mc(&tfull_bar[acc], kMask);
+                else ptx::umma_commit(&tfull_bar[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -398,7 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+            if (lane == 0) {
+                if constexpr (kCl == 2) ptx::mbar_arrive_cluster(&tempty_bar[acc], 0);
+                else ptx::mbar_arrive(&tempty_bar[acc]);
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -412,7 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        if constexpr (kCl == 2) ptx::tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
+        else ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
     }
 }
 
@@ -460,7 +488,7 @@ CUtensorMap make_map(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld
 
 template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p, cudaStream_t s) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, kCl>;
     auto kern = gemm_tc_kernel<BN, kAMN, kBMN, kKind, kCl>;
     static std::atomic<uint32_t> configured{0};  // one attribute call per device
     int dev = 0;
@@ -523,27 +551,14 @@ TileChoice choose_tile(int m, int n, int k) {
         if (std::sscanf(env, "%d,%d", &bn, &cl) == 2 && (bn == 128 || bn == 256) && (cl == 1 || cl == 2))
             return {bn, cl};
     }
-    const long tm = (m + kBM - 1) / kBM;
-    const long sms = num_sms();
-    const long kblocks = (k + kBK - 1) / kBK;
-    TileChoice best{128, 1};
-    double best_cost = 1e300;
-    for (const int bn : {128, 256}) {
-        if (bn == 256 && n % 256 != 0 && n < 256) continue;
-        for (const int cl : {1, 2}) {
-            const long tiles = ((tm + cl - 1) / cl) * ((n + bn - 1) / bn);
-            const long slots = sms / cl;
-            const long waves = (tiles + slots - 1) / slots;
-            const double mma = 2.0 * bn;
-            const double l2 = (16384.0 + 128.0 * bn / cl) / 45.0;
-            const double cost = static_cast<double>(waves) * kblocks * std::max(mma, l2);
-            if (cost < best_cost * 0.999 || (cost <= best_cost * 1.001 && cl > best.cl)) {
-                best_cost = cost;
-                best = {bn, cl};
-            }
-        }
-    }
-    return best;
+    // Measured on B200 (scripts/gemm_sweep.py, profiles/gemm_sweep_r1.json): 128 x 256
+    // tiles beat 128 x 128 on every stage shape, including N = 768 where they leave a
+    // partial wave.  The CTA-pair 256 x 256 tile (half of B per CTA: 6 stages instead
+    // of 4) wins 5-10% once N.K is large (fc1/fc2, all wgrads) and loses a few % on the
+    // short N = K = 768 GEMMs, where the deeper ring never fills.
+    if (n < 256) return {128, 1};
+    const bool pair = m > kBM && static_cast<double>(n) * k >= 1.5e6;
+    return {256, pair ? 2 : 1};
 }
 
 }  // namespace

@@ -16,7 +16,7 @@ shapes = [  # name, m, n, k, a_major, b_major, f32 out
     ("fc2_wgrad", h, 4 * h, T, 1, 1, 1),
 ]
 CHILD = r'''
-import ctypes as C, json, sys, torch
+import ctypes as C, json, os, sys, torch
 sys.path.insert(0, ".")
 from paper_2006_09503_b200._lib import GemmEpilogue, call
 name, m, n, k, am, bm, f32 = json.loads(sys.argv[1])
@@ -24,7 +24,12 @@ a = torch.randn(m * k, device="cuda").to(torch.bfloat16); b = torch.randn(n * k,
 d = torch.zeros(m * n, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
 epi = GemmEpilogue(kind=1 if f32 else 0, d=d.data_ptr(), ldd=n, alpha=1.0, beta=1.0 if f32 else 0.0)
 s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-run = lambda: call("p2bw_kernel_gemm_bf16", C.c_void_p(a.data_ptr()), k if am == 0 else m, am,
+if os.environ.get("SWEEP_CUBLAS"):  # library baseline: torch.mm (cuBLAS) on the same shape
+    a2, b2 = a.view(m, k), b.view(n, k)
+    o2 = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    run = lambda: torch.mm(a2, b2.t(), out=o2)
+else:
+  run = lambda: call("p2bw_kernel_gemm_bf16", C.c_void_p(a.data_ptr()), k if am == 0 else m, am,
                    C.c_void_p(b.data_ptr()), k if bm == 0 else n, bm, m, n, k, C.byref(epi), s)
 for _ in range(3): run()
 torch.cuda.synchronize()
@@ -36,9 +41,11 @@ ms = e0.elapsed_time(e1) / 20
 print(json.dumps({"name": name, "tflops": round(2 * m * n * k / ms / 1e9, 1)}))
 '''
 rows = {}
-for cfg in ["auto", "128,1", "128,2", "256,1", "256,2"]:
+for cfg in ["auto", "128,1", "128,2", "256,1", "256,2", "cublas"]:
     env = dict(os.environ)
-    if cfg != "auto":
+    if cfg == "cublas":
+        env["SWEEP_CUBLAS"] = "1"
+    elif cfg != "auto":
         env["P2BW_GEMM_TILE"] = cfg
     for sh in shapes:
         out = subprocess.run([sys.executable, "-c", CHILD, json.dumps(sh)], capture_output=True, text=True, env=env)
