@@ -7,15 +7,18 @@ One "step" is one 2BW batch (m microbatches of b sequences, every stage's
 weight update included) of the workload named by --config (default: configs[1],
 the BERT-base-sized encoder, 12 layers / hidden 768 / seq 512) with synthetic
 token data.  Under torchrun (N > 1) every rank drives one GPU; rank 0 prints
-ONE JSON line.
+ONE JSON line.  By default N GPUs run N data-parallel replicas of the whole
+pipeline (width N); --depth D > 1 under torchrun runs one pipeline stage per
+process (gpu = stage * width + replica, width = N / D) with CUDA-IPC stage
+hand-offs; on one GPU --depth D runs D stages on one device.
 
 Timing: W warm-up batches, then K batches timed on the device with the
-engine's CUDA events at the last stage's weight updates (steady state, as
+engine's CUDA events at each stage's weight updates (steady state, as
 simulator.cpp:298-309 defines it), barrier + synchronize on both sides, max
-over ranks.  `value` counts every rank's sequences.  The same run is the
-end-to-end number: each step's token ids / targets are copied host->device
-from pinned memory and its losses device->host inside the timed region
-(`e2e`).  `roofline` comes from a second, profiled pass of the same workload
+over ranks and stages.  `value` counts every replica's sequences with the
+token batches already resident in HBM.  `e2e` is a second timed pass through
+the C-ABI in which each step's token ids / targets are copied host->device
+from pinned memory and its losses device->host inside the timed region.  `roofline` comes from a second, profiled pass of the same workload
 (per-launch CUDA events around every stage kernel).  `cpu_baseline` times the
 reference's own pipelined_execute (oracle/_ref/ref_tool, built from
 /root/reference) on the linear-chain analog of the config on this host.
@@ -181,8 +184,15 @@ def run_ours(args, c):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2006_09503_b200 import dist as D
 
-    depth = c["depth"] if world == 1 else 1
+    depth = args.depth or (c["depth"] if world == 1 else 1)
+    pipelined = world > 1 and depth > 1  # one stage per process, CUDA-IPC hand-offs
+    if pipelined:
+        stage, _, width = D.grid(world, rank, depth)
+        local_stages = (stage, 1)
+    else:
+        width, local_stages = world, None
     spec = TO.Spec(layers=c["layers"], hidden=c["hidden"], heads=c["heads"], seq=c["seq"], vocab=c["vocab"],
                    batch=c["b"], causal=c["causal"], head_rows=c["head_rows"])
     m, steps, warm = c["m"], args.steps, args.warmup
@@ -190,16 +200,21 @@ def run_ours(args, c):
     eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
                    microbatch_size=c["b"], layers=c["layers"], hidden=c["hidden"], heads=c["heads"],
                    seq_len=c["seq"], vocab=c["vocab"], causal=int(c["causal"]), head_rows=c["head_rows"],
-                   learning_rate=1e-3, momentum=0.9, seed=1234)  # replicas start identical
+                   learning_rate=1e-3, momentum=0.9, seed=1234,  # replicas start identical
+                   local_stages=local_stages)
     eng.init_weights()
-    if world > 1:
-        from paper_2006_09503_b200.dist import join_replicas
-        join_replicas(eng, depth)  # one NCCL communicator per stage over the w replicas
+    my_stages = [s for s in range(depth) if eng.is_local(s)]
+    has_loss = eng.is_local(depth - 1)
+    if pipelined:
+        D.connect_pipeline(eng, depth)
+    if width > 1:
+        D.join_replicas(eng, depth, pipelined=pipelined)  # NCCL per stage over its w replicas
 
     # synthetic token batches in pinned host memory (one batch = m microbatches)
     T, R = c["b"] * c["seq"], c["b"] * (c["head_rows"] or c["seq"])
     pool = 4
-    ids_np, tg_np = TO.synthetic_batch(spec, m * pool, 99 + rank)
+    replica = D.grid(world, rank, depth)[1] if pipelined else rank
+    ids_np, tg_np = TO.synthetic_batch(spec, m * pool, 99 + replica)
     ids = torch.from_numpy(ids_np).pin_memory()
     tgs = torch.from_numpy(tg_np).pin_memory()
     loss_host = torch.zeros(total_batches * m, dtype=torch.float32).pin_memory()
@@ -212,63 +227,89 @@ def run_ours(args, c):
             eng.h, C.c_void_p(ids[j * m].data_ptr()), C.c_void_p(tgs[j * m].data_ptr()), (t - 1) * m + 1, m))
 
     def fetch_loss(t):
-        _lib.check(_lib.lib().p2bw_engine_losses_async(eng.h, (t - 1) * m + 1, m,
-                                                       C.c_void_p(loss_host[(t - 1) * m].data_ptr())))
+        if has_loss:
+            _lib.check(_lib.lib().p2bw_engine_losses_async(eng.h, (t - 1) * m + 1, m,
+                                                           C.c_void_p(loss_host[(t - 1) * m].data_ptr())))
 
-    def one_pass(n_batches, profile=False):
+    def one_pass(n_batches, io=True, profile=False):
+        """io=True: per-step H2D of the batch and D2H of its losses (the e2e pass);
+        io=False: the token ring already holds the batches (resident inputs)."""
         eng.begin(n_batches)
-        set_batch(1)
+        if io:
+            set_batch(1)
         for t in range(1, n_batches + 1):
-            if t + 1 <= n_batches:
+            if io and t + 1 <= n_batches:
                 set_batch(t + 1)
             if profile and t == warm + 1:
                 _lib.lib().p2bw_profile_enable(1)
             if profile and t == warm + 1 + steps:
                 _lib.lib().p2bw_profile_enable(0)
             eng.issue(t)
-            fetch_loss(t)
+            if io:
+                fetch_loss(t)
         eng.finish()
 
-    # ---- timed pass ----
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+    def steady_ms():
+        """K steady-state batches: update events of every local stage, max over ranks."""
+        ms = max(eng.update_elapsed_ms(s, warm, warm + steps) for s in my_stages)
+        if world > 1:
+            ms = D.max_over_ranks(ms)
+        return ms
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # token ring filled once (2 batches = the ring's capacity); the resident pass reuses it
+    set_batch(1)
+    set_batch(2)
+    eng.sync()
+
+    # ---- timed pass 1: inputs resident in HBM -> value ----
+    barrier()
     clocks = Clocks(local)
     launches0 = _lib.lib().p2bw_launch_count()
-    wall0 = time.time()
-    one_pass(total_batches)
+    one_pass(total_batches, io=False)
     eng.sync()
-    wall = time.time() - wall0
     launches = _lib.lib().p2bw_launch_count() - launches0
     clk = clocks.stop()
-    ms = eng.update_elapsed_ms(depth - 1, warm, warm + steps)  # K steady-state batches
-    if world > 1:
-        from paper_2006_09503_b200.dist import max_over_ranks
-        ms = max_over_ranks(ms)
-        torch.distributed.barrier()
+    ms = steady_ms()
+    barrier()
+
+    # ---- timed pass 2: end to end through the C-ABI with host buffers -> e2e ----
+    wall0 = time.time()
+    one_pass(total_batches, io=True)
+    eng.sync()
+    wall = time.time() - wall0
+    ms_e2e = steady_ms()
+    barrier()
     losses = loss_host.numpy()[: total_batches * m]
 
-    samples = world * c["b"] * m * steps
+    samples = width * c["b"] * m * steps
     value = samples / (ms / 1e3)
+    value_e2e = samples / (ms_e2e / 1e3)
     fps = flops_per_sample(c)
     peak, peak_sus, hbm, peak_kind = peaks()
 
-    # ---- profiled pass (same workload) for the roofline ----
+    # ---- profiled pass (same workload, every rank runs it, rank 0 records) ----
     classes = []
+    one_pass(total_batches, io=False, profile=(rank == 0))
+    eng.sync()
     if rank == 0:
-        one_pass(total_batches, profile=True)
-        eng.sync()
         arr = (KernelClass * 64)()
         n = C.c_int()
         _lib.check(_lib.lib().p2bw_profile_collect(arr, 64, C.byref(n)))
         classes = [dict(name=arr[i].name.decode(), launches=arr[i].launches, ms=arr[i].ms, flops=arr[i].flops,
                         bytes=arr[i].bytes) for i in range(min(n.value, 64))]
+    barrier()
     eng.close()
 
     if rank != 0:
         return 0
     tot_ms = sum(k["ms"] for k in classes) or 1.0
-    gemm = next((k for k in classes if k["name"] == "gemm"), None)
+    gk = [k for k in classes if k["name"].startswith("gemm")]
+    gemm = {"name": "gemm", **{f: sum(k[f] for k in gk) for f in ("launches", "ms", "flops", "bytes")}} if gk else None
     roofline = None
     if gemm and gemm["ms"] > 0:
         achieved = gemm["flops"] / (gemm["ms"] / 1e3) / 1e12
@@ -289,6 +330,11 @@ def run_ours(args, c):
                              "gbs": round(k["bytes"] / (k["ms"] / 1e3) / 1e9, 1) if k["bytes"] else None}
                  for k in classes}
     mfu = value * fps / (world * peak * 1e12)
+    par = f"2bw d={depth} w={width}"
+    if pipelined:
+        par += " (one stage per process, CUDA-IPC stage hand-offs over NVLink)"
+    if width > 1:
+        par += " (NCCL all-reduce of the coalesced gradient at each AllReduce op)"
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -303,22 +349,21 @@ def run_ours(args, c):
         "config": {"workload": args.config, "layers": c["layers"], "hidden": c["hidden"], "heads": c["heads"],
                    "seq_len": c["seq"], "vocab": c["vocab"], "causal": c["causal"],
                    "head_rows_per_seq": c["head_rows"] or c["seq"], "microbatch_size": c["b"],
-                   "microbatches_m": m, "global_batch": world * c["b"] * m,
-                   "parallelism": f"2bw d={depth} w={world}" + (" (NCCL all-reduce of the coalesced gradient "
-                                                                "at each AllReduce op)" if world > 1 else ""),
+                   "microbatches_m": m, "global_batch": width * c["b"] * m,
+                   "parallelism": par, "inputs": "value: token batches resident in HBM; e2e: per-step host copies",
                    "policy": "2bw", "l2": "working set (activations >> 126 MB L2) exceeds L2 every step"},
-        "e2e": {"value": round(value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
-                "d2h_bytes_per_step": d2h_bytes,
-                "note": "timed region includes per-step pinned H2D of ids/targets and D2H of losses "
-                        "through the C-ABI (p2bw_engine_set_data / p2bw_engine_losses_async)"},
+        "e2e": {"value": round(value_e2e, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes, "wall_s": round(wall, 3),
+                "note": "second timed pass: per-step pinned H2D of ids/targets and D2H of losses "
+                        "through the C-ABI (p2bw_engine_set_data / p2bw_engine_losses_async), "
+                        "device-timed between weight-update events like `value`"},
         "gpu_launches": int(launches * steps / total_batches),
         "gpu_launches_per_step": round(launches / total_batches, 1),
         "mfu": round(mfu, 4), "flops_per_sample": fps,
         "roofline": roofline, "kernel_breakdown": breakdown,
         "kernel_ms_per_step": round(tot_ms / steps, 3) if classes else None,
         "cpu_baseline": cpu, "clocks": clk,
-        "loss_first_last": [float(losses[0]), float(losses[-1])],
-        "wall_s": round(wall, 2),
+        "loss_first_last": [float(losses[0]), float(losses[-1])] if has_loss else None,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -337,6 +382,8 @@ def main():
     ap.add_argument("--config", default="bert-base", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--depth", type=int, default=0,
+                    help="pipeline depth (default: the config's on 1 GPU, 1 = data parallel on N GPUs)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

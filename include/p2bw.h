@@ -131,6 +131,12 @@ typedef struct {
     double momentum;
     unsigned long long seed;
     const int* devices;  /* one CUDA device per stage, or NULL: all on the current device */
+    /* Cross-process pipeline (one process per GPU): this process runs stages
+     * [first_local_stage, first_local_stage + local_stages); local_stages == 0 runs
+     * every stage here.  Neighbours in other processes are connected with
+     * p2bw_engine_export_stage / p2bw_engine_connect_stage before the first run. */
+    int first_local_stage;
+    int local_stages;
 } p2bw_desc;
 
 typedef struct {
@@ -177,6 +183,17 @@ int p2bw_engine_update_elapsed_ms(p2bw_engine* eng, int stage, int u0, int u1, d
  * by count * w -- the replicas' average, as costmodel.cpp:23-27 prices it. */
 int p2bw_nccl_unique_id(void* out, size_t bytes);
 int p2bw_engine_join_replicas(p2bw_engine* eng, const void* ids, int nranks, int rank);
+/* Cross-process pipelines: the reference interprets all stages in one loop
+ * (semantics.cpp:270-361); here each process interprets its own stages and the
+ * hand-offs of out_act (:299) / grad_to_prev (:333) to a stage in another process
+ * go through that stage's receive block, exported with CUDA IPC.  Each process
+ * exports its local stages' blobs, exchanges them (any transport), and connects
+ * every remote stage adjacent to one of its own.  Ordering between processes is
+ * GPU-side (sequence flags), so the host still never waits. */
+#define P2BW_STAGE_BLOB_BYTES 128
+int p2bw_engine_is_local(p2bw_engine* eng, int stage, int* out);
+int p2bw_engine_export_stage(p2bw_engine* eng, int stage, void* blob, size_t bytes);
+int p2bw_engine_connect_stage(p2bw_engine* eng, const void* blob, size_t bytes);
 int p2bw_engine_sync(p2bw_engine* eng);
 int p2bw_engine_counters(p2bw_engine* eng, p2bw_counters* out);
 /* Weights created by a stage's update_index-th update of the last run (snapshots on). */
@@ -244,8 +261,10 @@ int p2bw_kernel_attention_bwd(const void* qkv, const void* o, const void* dout, 
 /* LayerNorm forward / backward (bf16 rows, fp32 stats and parameter gradients). */
 int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void* y, void* mean,
                               void* rstd, int rows, int h, void* stream);
+/* dsum (optional, fp32 [h]): (=|+=) column sums of bf16(dx), the fused bias gradient
+ * of the layer whose output gradient dx is.  dx may alias dy. */
 int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
-                              const void* g, const void* dres, void* dx, void* dg, void* db,
+                              const void* g, const void* dres, void* dx, void* dg, void* db, void* dsum,
                               int overwrite, int rows, int h, void* stream);
 /* Debug: per-CTA phase clocks of the tcgen05 attention forward into a device buffer
  * of 16 uint64 per CTA (NULL switches it off). */

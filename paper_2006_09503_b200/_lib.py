@@ -75,6 +75,9 @@ def _signatures():
         ("p2bw_engine_update_elapsed_ms", i, [vp, i, i, i, C.POINTER(C.c_double)]),
         ("p2bw_nccl_unique_id", i, [vp, sz]),
         ("p2bw_engine_join_replicas", i, [vp, vp, i, i]),
+        ("p2bw_engine_is_local", i, [vp, i, C.POINTER(C.c_int)]),
+        ("p2bw_engine_export_stage", i, [vp, i, vp, sz]),
+        ("p2bw_engine_connect_stage", i, [vp, vp, sz]),
         ("p2bw_engine_sync", i, [vp]),
         ("p2bw_engine_counters", i, [vp, vp]),
         ("p2bw_engine_read_snapshot", i, [vp, i, i, vp, sz]),
@@ -89,7 +92,7 @@ def _signatures():
         ("p2bw_kernel_attention_fwd", i, [vp, vp, vp, i, i, i, i, vp]),
         ("p2bw_kernel_attention_bwd", i, [vp, vp, vp, vp, vp, vp, i, i, i, i, vp]),
         ("p2bw_kernel_layernorm_fwd", i, [vp, vp, vp, vp, vp, vp, i, i, vp]),
-        ("p2bw_kernel_layernorm_bwd", i, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp]),
+        ("p2bw_kernel_layernorm_bwd", i, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp]),
         ("p2bw_kernel_softmax_xent", i, [vp, vp, i, i, i, C.c_float, vp, vp]),
         ("p2bw_kernel_colsum", i, [vp, i, i, i, vp, i, vp]),
         ("p2bw_debug_attention_timing", i, [vp]),

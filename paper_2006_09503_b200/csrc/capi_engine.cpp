@@ -54,6 +54,8 @@ int p2bw_engine_create(const p2bw_desc* d, p2bw_engine** out) {
         c.momentum = d->momentum;
         c.seed = d->seed;
         if (d->devices != nullptr) c.devices.assign(d->devices, d->devices + d->depth);
+        c.first_local = d->first_local_stage;
+        c.local_count = d->local_stages;
         if (c.lr < 0) throw p2bw::Error("learning rate must be >= 0");
         if (c.momentum < 0 || c.momentum >= 1) throw p2bw::Error("momentum must be in [0, 1)");
         auto e = std::make_unique<p2bw_engine>();
@@ -85,7 +87,8 @@ int p2bw_engine_load_stage_weights(p2bw_engine* eng, int stage, const void* host
 int p2bw_engine_init_weights(p2bw_engine* eng) {
     return guarded([&] {
         auto& e = eng_of(eng);
-        for (int s = 0; s < e.depth(); ++s) e.model(s).init_weights(e.config().seed);
+        for (int s = 0; s < e.depth(); ++s)
+            if (e.is_local(s)) e.model(s).init_weights(e.config().seed);
     });
 }
 
@@ -94,9 +97,11 @@ int p2bw_engine_set_data(p2bw_engine* eng, const void* inputs, const void* targe
     return guarded([&] {
         auto& e = eng_of(eng);
         if (first_mb < 1) throw std::invalid_argument("microbatch ids are 1-based");
-        // Inputs feed stage 0, targets the last stage (they may be the same stage).
-        e.model(0).set_data(inputs, e.depth() == 1 ? targets : nullptr, first_mb, count);
-        if (e.depth() > 1) e.model(e.depth() - 1).set_data(nullptr, targets, first_mb, count);
+        // Inputs feed stage 0, targets the last stage (they may be the same stage);
+        // a process without either stage ignores the call.
+        if (e.is_local(0)) e.model(0).set_data(inputs, e.depth() == 1 ? targets : nullptr, first_mb, count);
+        if (e.depth() > 1 && e.is_local(e.depth() - 1))
+            e.model(e.depth() - 1).set_data(nullptr, targets, first_mb, count);
     });
 }
 
@@ -183,6 +188,39 @@ int p2bw_engine_join_replicas(p2bw_engine* eng, const void* ids, int nranks, int
     return guarded([&] {
         if (ids == nullptr) throw std::invalid_argument("ids is NULL");
         eng_of(eng).join_replicas(ids, nranks, rank);
+    });
+}
+
+int p2bw_engine_is_local(p2bw_engine* eng, int stage, int* out) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (out == nullptr) throw std::invalid_argument("out is NULL");
+        *out = e.is_local(stage) ? 1 : 0;
+    });
+}
+
+int p2bw_engine_export_stage(p2bw_engine* eng, int stage, void* blob, size_t bytes) {
+    static_assert(sizeof(p2bw::StageBlob) <= P2BW_STAGE_BLOB_BYTES, "stage blob does not fit");
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (blob == nullptr || bytes != P2BW_STAGE_BLOB_BYTES)
+            throw std::invalid_argument("stage blob buffer must be P2BW_STAGE_BLOB_BYTES bytes");
+        const p2bw::StageBlob b = e.export_stage(stage);
+        std::memset(blob, 0, bytes);
+        std::memcpy(blob, &b, sizeof(b));
+    });
+}
+
+int p2bw_engine_connect_stage(p2bw_engine* eng, const void* blob, size_t bytes) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        if (blob == nullptr || bytes != P2BW_STAGE_BLOB_BYTES)
+            throw std::invalid_argument("stage blob buffer must be P2BW_STAGE_BLOB_BYTES bytes");
+        p2bw::StageBlob b;
+        std::memcpy(&b, blob, sizeof(b));
+        e.connect_stage(b);
     });
 }
 

@@ -68,7 +68,7 @@ extern "C" int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const voi
 
 extern "C" int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                                          const void* g, const void* dres, void* dx, void* dg, void* db,
-                                         int overwrite, int rows, int h, void* stream) {
+                                         void* dsum, int overwrite, int rows, int h, void* stream) {
     return guarded([&] {
         float* scratch = nullptr;
         check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
@@ -76,7 +76,7 @@ extern "C" int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const vo
                    "cudaMallocAsync");
         layernorm_bwd(cb(dy), cb(x), static_cast<const float*>(mean), static_cast<const float*>(rstd), cb(g),
                       cb(dres), mb(dx), static_cast<float*>(dg), static_cast<float*>(db), overwrite != 0, rows, h,
-                      scratch, as_stream(stream));
+                      scratch, as_stream(stream), static_cast<float*>(dsum));
         check_cuda(cudaFreeAsync(scratch, as_stream(stream)), "cudaFreeAsync");
     });
 }

@@ -10,13 +10,19 @@
 // Buffers: every stage owns a receive ring for its input activations (which is
 // also the stash of its first-layer input) and one for its output gradient.
 // The producing stage's last kernel writes straight into those slots, so a
-// stage hand-off is a peer store over NVLink when stages sit on different GPUs.
+// stage hand-off is a peer store over NVLink when stages sit on different GPUs
+// of this process.  Stages in another process (one process per GPU) are reached
+// through CUDA IPC: the producer writes a local staging slot, a copy stream moves
+// it into the consumer's ring and bumps a sequence flag in the consumer's block;
+// slot reuse is gated by the consumer's backward progress, pushed back the same
+// way (transport.cu).
 #include "engine.h"
 
 #include <algorithm>
 #include <cstring>
 
 #include "nccl_dl.h"
+#include "transport.h"
 
 namespace p2bw {
 
@@ -58,9 +64,14 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     }
     if (static_cast<int>(cfg_.devices.size()) != cfg_.depth)
         throw Error("device list must have one entry per stage");
+    if (cfg_.local_count < 0 || cfg_.first_local < 0 || cfg_.first_local + cfg_.local_count > cfg_.depth)
+        throw Error("local stage range [" + std::to_string(cfg_.first_local) + ", " +
+                    std::to_string(cfg_.first_local + cfg_.local_count) + ") outside the pipeline");
+    const int lo_local = cfg_.local_count == 0 ? 0 : cfg_.first_local;
+    const int hi_local = cfg_.local_count == 0 ? cfg_.depth : cfg_.first_local + cfg_.local_count;
 
-    // Peer access between devices of adjacent stages (NVLink / NVSwitch).
-    for (int s = 0; s + 1 < cfg_.depth; ++s) {
+    // Peer access between devices of adjacent local stages (NVLink / NVSwitch).
+    for (int s = lo_local; s + 1 < hi_local; ++s) {
         const int a = cfg_.devices[s], b = cfg_.devices[s + 1];
         if (a == b) continue;
         for (auto [x, y] : {std::pair{a, b}, std::pair{b, a}}) {
@@ -98,6 +109,8 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             st.stash_slots = inflight + (s > 0 ? 1 : 0);
             st.grad_slots = st.stash_slots;
             st.weight_slots = weight_slots_for(cfg_.policy, cfg_.depth);
+            st.local = s >= lo_local && s < hi_local;
+            if (!st.local) continue;  // another process runs it; connect_stage maps its block
             DeviceGuard g(st.device);
             check_cuda(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking),
                        "cudaStreamCreate");
@@ -113,18 +126,37 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
                 throw Error("unknown model kind " + std::to_string(cfg_.model_kind));
             }
             st.model->bind_stream(st.stream);
+            // Receive block: [act ring][grad ring][flags], one allocation so that a
+            // single IPC handle exports it.
             const size_t nb = st.model->boundary_bytes();
-            if (s > 0) {
-                st.act_ring.assign(static_cast<size_t>(st.stash_slots), nullptr);
-                for (auto& p : st.act_ring) check_cuda(cudaMalloc(&p, nb), "cudaMalloc(act ring)");
-            }
-            if (s + 1 < cfg_.depth) {
-                st.grad_ring.assign(static_cast<size_t>(st.grad_slots), nullptr);
-                for (auto& p : st.grad_ring)
-                    check_cuda(cudaMalloc(&p, nb), "cudaMalloc(grad ring)");
-            }
+            auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+            const size_t act_b = s > 0 ? al(nb * st.stash_slots) : 0;
+            const size_t grad_b = s + 1 < cfg_.depth ? al(nb * st.grad_slots) : 0;
+            check_cuda(cudaMalloc(&st.block, act_b + grad_b + 256), "cudaMalloc(receive block)");
+            uint8_t* base = static_cast<uint8_t*>(st.block);
+            if (s > 0)
+                for (int i = 0; i < st.stash_slots; ++i) st.act_ring.push_back(base + i * nb);
+            if (s + 1 < cfg_.depth)
+                for (int i = 0; i < st.grad_slots; ++i) st.grad_ring.push_back(base + act_b + i * nb);
+            st.flags = reinterpret_cast<uint32_t*>(base + act_b + grad_b);
+            check_cuda(cudaMemset(st.flags, 0, 256), "cudaMemset(flags)");
             st.version_slot[0] = 0;
         }
+        // Staging slots and copy streams towards neighbours in other processes.
+        for (int s = lo_local; s < hi_local; ++s) {
+            Stage& st = stages_[s];
+            DeviceGuard g(st.device);
+            const size_t nb = st.model->boundary_bytes();
+            if (s + 1 < cfg_.depth && !stages_[s + 1].local) {
+                for (auto& p : st.send_act) check_cuda(cudaMalloc(&p, nb), "cudaMalloc(send slot)");
+                check_cuda(cudaStreamCreateWithFlags(&st.copy_fwd, cudaStreamNonBlocking), "cudaStreamCreate");
+            }
+            if (s > 0 && !stages_[s - 1].local) {
+                for (auto& p : st.send_grad) check_cuda(cudaMalloc(&p, nb), "cudaMalloc(send slot)");
+                check_cuda(cudaStreamCreateWithFlags(&st.copy_bwd, cudaStreamNonBlocking), "cudaStreamCreate");
+            }
+        }
+        check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     } catch (...) {
         free_buffers();
         throw;
@@ -136,6 +168,7 @@ Engine::~Engine() { free_buffers(); }
 void Engine::join_replicas(const void* ids, int nranks, int rank) {
     if (nranks < 1 || rank < 0 || rank >= nranks) throw Error("bad data-parallel rank / size");
     for (Stage& st : stages_) {
+        if (!st.local) continue;
         if (st.comm) throw Error("stage already joined a replica group");
         if (nranks == 1) continue;
         ncclUniqueId id;
@@ -146,12 +179,86 @@ void Engine::join_replicas(const void* ids, int nranks, int rank) {
     }
 }
 
+Engine::Stage& Engine::local_stage(int s) {
+    if (s < 0 || s >= cfg_.depth) throw Error("stage " + std::to_string(s) + " out of range");
+    Stage& st = stages_[static_cast<size_t>(s)];
+    if (!st.local) throw Error("stage " + std::to_string(s) + " runs in another process");
+    return st;
+}
+
+StageBlob Engine::export_stage(int s) {
+    Stage& st = local_stage(s);
+    StageBlob b{};
+    cudaIpcMemHandle_t h;
+    DeviceGuard g(st.device);
+    check_cuda(cudaIpcGetMemHandle(&h, st.block), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == sizeof(b.ipc), "IPC handle size");
+    std::memcpy(b.ipc, &h, sizeof(h));
+    b.stage = s;
+    b.stash_slots = st.stash_slots;
+    b.grad_slots = st.grad_slots;
+    b.slot_bytes = st.model->boundary_bytes();
+    const uint8_t* base = static_cast<const uint8_t*>(st.block);
+    b.act_off = st.act_ring.empty() ? 0 : static_cast<const uint8_t*>(st.act_ring[0]) - base;
+    b.grad_off = st.grad_ring.empty() ? 0 : static_cast<const uint8_t*>(st.grad_ring[0]) - base;
+    b.flag_off = reinterpret_cast<const uint8_t*>(st.flags) - base;
+    return b;
+}
+
+void Engine::connect_stage(const StageBlob& b) {
+    const int s = b.stage;
+    if (s < 0 || s >= cfg_.depth) throw Error("connect: stage " + std::to_string(s) + " out of range");
+    Stage& st = stages_[static_cast<size_t>(s)];
+    if (st.local) throw Error("connect: stage " + std::to_string(s) + " runs in this process");
+    if (st.connected) throw Error("connect: stage " + std::to_string(s) + " is already connected");
+    const bool left = s + 1 < cfg_.depth && stages_[s + 1].local, right = s > 0 && stages_[s - 1].local;
+    if (!left && !right) throw Error("connect: stage " + std::to_string(s) + " is not adjacent to a local stage");
+    if (b.stash_slots != st.stash_slots || b.grad_slots != st.grad_slots)
+        throw Error("connect: stage " + std::to_string(s) + " ring sizes differ between processes");
+    Stage& nb = stages_[static_cast<size_t>(left ? s + 1 : s - 1)];
+    if (b.slot_bytes != nb.model->boundary_bytes())
+        throw Error("connect: boundary tensor size differs between processes");
+    DeviceGuard g(nb.device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, b.ipc, sizeof(h));
+    check_cuda(cudaIpcOpenMemHandle(&st.block, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    st.block_mapped = true;
+    uint8_t* base = static_cast<uint8_t*>(st.block);
+    st.act_ring.clear();
+    st.grad_ring.clear();
+    if (s > 0)
+        for (int i = 0; i < st.stash_slots; ++i) st.act_ring.push_back(base + b.act_off + i * b.slot_bytes);
+    if (s + 1 < cfg_.depth)
+        for (int i = 0; i < st.grad_slots; ++i) st.grad_ring.push_back(base + b.grad_off + i * b.slot_bytes);
+    st.flags = reinterpret_cast<uint32_t*>(base + b.flag_off);
+    st.connected = true;
+}
+
+void Engine::signal_remote(uint32_t* flag, uint32_t value, cudaStream_t s) { stream_signal(flag, value, s); }
+
+void Engine::wait_flag(const uint32_t* flag, uint32_t value, cudaStream_t s) {
+    if (value != 0) stream_wait_geq(flag, value, s);
+}
+
 void Engine::free_buffers() {
     for (Stage& st : stages_) {
+        if (!st.local) {
+            if (st.block_mapped) cudaIpcCloseMemHandle(st.block);
+            st.block = nullptr;
+            st.block_mapped = false;
+            continue;
+        }
         DeviceGuard g(st.device);
         if (st.stream) cudaStreamSynchronize(st.stream);
-        for (void* p : st.act_ring) cudaFree(p);
-        for (void* p : st.grad_ring) cudaFree(p);
+        if (st.copy_fwd) cudaStreamSynchronize(st.copy_fwd);
+        if (st.copy_bwd) cudaStreamSynchronize(st.copy_bwd);
+        if (st.block) cudaFree(st.block);
+        st.block = nullptr;
+        for (void*& p : st.send_act) cudaFree(p), p = nullptr;
+        for (void*& p : st.send_grad) cudaFree(p), p = nullptr;
+        if (st.copy_fwd) cudaStreamDestroy(st.copy_fwd);
+        if (st.copy_bwd) cudaStreamDestroy(st.copy_bwd);
+        st.copy_fwd = st.copy_bwd = nullptr;
         st.act_ring.clear();
         st.grad_ring.clear();
         st.model.reset();
@@ -170,13 +277,13 @@ void Engine::free_buffers() {
 // Destroying an event with pending waits is legal.
 struct EventTable {
     std::vector<std::map<int, cudaEvent_t>> fwd, bwd;
+    std::vector<std::map<int, cudaEvent_t>> cpf, cpb;  // sends to remote neighbours done
     std::vector<std::vector<cudaEvent_t>> upd;
-    explicit EventTable(size_t d) : fwd(d), bwd(d), upd(d) {}
+    explicit EventTable(size_t d) : fwd(d), bwd(d), cpf(d), cpb(d), upd(d) {}
     ~EventTable() {
-        for (auto& m : fwd)
-            for (auto& kv : m) cudaEventDestroy(kv.second);
-        for (auto& m : bwd)
-            for (auto& kv : m) cudaEventDestroy(kv.second);
+        for (auto* t : {&fwd, &bwd, &cpf, &cpb})
+            for (auto& m : *t)
+                for (auto& kv : m) cudaEventDestroy(kv.second);
         for (auto& v : upd)
             for (cudaEvent_t e : v) cudaEventDestroy(e);
     }
@@ -210,16 +317,18 @@ int Engine::resolve_version(const Stage& st, const OpRec& op) const {
 bool Engine::ready(const Stage& st, const OpRec& op) const {
     const int s = st.index, d = cfg_.depth, k = op.microbatch;
     auto issued = [](const std::map<int, bool>& m, int key) { return key < 1 || m.count(key); };
+    // Neighbours in another process are ordered on the GPU by sequence flags.
+    const bool prev_l = s > 0 && stages_[s - 1].local, next_l = s + 1 < d && stages_[s + 1].local;
     if (op.kind == P2BW_OP_FORWARD) {
-        if (s > 0 && !issued(stages_[s - 1].fwd_issued, k)) return false;  // semantics.cpp:279
-        if (!issued(st.bwd_issued, k - st.stash_slots)) return false;      // own stash slot
-        if (s + 1 < d && !issued(stages_[s + 1].bwd_issued, k - stages_[s + 1].stash_slots))
+        if (prev_l && !issued(stages_[s - 1].fwd_issued, k)) return false;  // semantics.cpp:279
+        if (!issued(st.bwd_issued, k - st.stash_slots)) return false;       // own stash slot
+        if (next_l && !issued(stages_[s + 1].bwd_issued, k - stages_[s + 1].stash_slots))
             return false;  // next stage's receive slot
         return true;
     }
     if (op.kind == P2BW_OP_BACKWARD) {
-        if (s + 1 < d && !issued(stages_[s + 1].bwd_issued, k)) return false;  // :301
-        if (s > 0 && !issued(stages_[s - 1].bwd_issued, k - stages_[s - 1].grad_slots))
+        if (next_l && !issued(stages_[s + 1].bwd_issued, k)) return false;  // :301
+        if (prev_l && !issued(stages_[s - 1].bwd_issued, k - stages_[s - 1].grad_slots))
             return false;  // previous stage's gradient slot
         return true;
     }
@@ -235,9 +344,15 @@ void Engine::issue_forward(Stage& st, const OpRec& op) {
                     " needs discarded weight version " + std::to_string(v));
     if (k < 1) throw Error("forward of microbatch " + std::to_string(k));
     const int sslot = (k - 1) % st.stash_slots;
-    if (s > 0) wait_on(ev_->fwd[s - 1], k, st.stream);
+    const bool prev_remote = s > 0 && !stages_[s - 1].local;
+    const bool next_remote = s + 1 < d && !stages_[s + 1].local;
+    if (prev_remote) wait_flag(&st.flags[kActReady], seq(k), st.stream);
+    else if (s > 0) wait_on(ev_->fwd[s - 1], k, st.stream);
     void* x_out = nullptr;
-    if (s + 1 < d) {
+    if (next_remote) {  // staging slot, freed by the copy of microbatch k - 2
+        if (k > 2) wait_on(ev_->cpf[s], k - 2, st.stream);
+        x_out = st.send_act[(k - 1) % 2];
+    } else if (s + 1 < d) {
         const Stage& nx = stages_[s + 1];
         if (k > nx.stash_slots) wait_on(ev_->bwd[s + 1], k - nx.stash_slots, st.stream);
         x_out = nx.act_ring[(k - 1) % nx.stash_slots];
@@ -245,6 +360,17 @@ void Engine::issue_forward(Stage& st, const OpRec& op) {
     const void* x_in = s > 0 ? st.act_ring[sslot] : nullptr;
     st.model->forward(k, vit->second, sslot, x_in, x_out, st.stream);
     record(ev_->fwd[s], k, st.stream);
+    if (next_remote) {  // copy into the next process's ring once its slot is free
+        const Stage& nx = stages_[s + 1];
+        const cudaStream_t c = st.copy_fwd;
+        wait_on(ev_->fwd[s], k, c);
+        wait_flag(&st.flags[kNextBwd], k > nx.stash_slots ? seq(k - nx.stash_slots) : seq(0), c);
+        check_cuda(cudaMemcpyAsync(nx.act_ring[(k - 1) % nx.stash_slots], x_out, st.model->boundary_bytes(),
+                                   cudaMemcpyDeviceToDevice, c),
+                   "cudaMemcpyAsync(stage send)");
+        signal_remote(&nx.flags[kActReady], seq(k), c);
+        record(ev_->cpf[s], k, c);
+    }
     st.stash_version[k] = v;
     st.fwd_issued[k] = true;
 }
@@ -259,19 +385,40 @@ void Engine::issue_backward(Stage& st, const OpRec& op) {
         stats_.version_consistent = false;
     const int wslot = st.version_slot.at(v);
     const int sslot = (k - 1) % st.stash_slots;
+    const bool prev_remote = s > 0 && !stages_[s - 1].local;
+    const bool next_remote = s + 1 < d && !stages_[s + 1].local;
     const void* g_in = nullptr;
     if (s + 1 < d) {
-        wait_on(ev_->bwd[s + 1], k, st.stream);
+        if (next_remote) wait_flag(&st.flags[kGradReady], seq(k), st.stream);
+        else wait_on(ev_->bwd[s + 1], k, st.stream);
         g_in = st.grad_ring[(k - 1) % st.grad_slots];
     }
     void* g_out = nullptr;
-    if (s > 0) {
+    if (prev_remote) {
+        if (k > 2) wait_on(ev_->cpb[s], k - 2, st.stream);
+        g_out = st.send_grad[(k - 1) % 2];
+    } else if (s > 0) {
         const Stage& pv = stages_[s - 1];
         if (k > pv.grad_slots) wait_on(ev_->bwd[s - 1], k - pv.grad_slots, st.stream);
         g_out = pv.grad_ring[(k - 1) % pv.grad_slots];
     }
     st.model->backward(k, wslot, sslot, g_in, g_out, st.grad_count == 0, st.stream);
     record(ev_->bwd[s], k, st.stream);
+    // Backward k released this stage's act slot and grad slot of microbatch k:
+    // tell the remote producers (their flags live in their own blocks).
+    if (prev_remote) signal_remote(&stages_[s - 1].flags[kNextBwd], seq(k), st.stream);
+    if (next_remote) signal_remote(&stages_[s + 1].flags[kPrevBwd], seq(k), st.stream);
+    if (prev_remote) {
+        const Stage& pv = stages_[s - 1];
+        const cudaStream_t c = st.copy_bwd;
+        wait_on(ev_->bwd[s], k, c);
+        wait_flag(&st.flags[kPrevBwd], k > pv.grad_slots ? seq(k - pv.grad_slots) : seq(0), c);
+        check_cuda(cudaMemcpyAsync(pv.grad_ring[(k - 1) % pv.grad_slots], g_out, st.model->boundary_bytes(),
+                                   cudaMemcpyDeviceToDevice, c),
+                   "cudaMemcpyAsync(stage send)");
+        signal_remote(&pv.flags[kGradReady], seq(k), c);
+        record(ev_->cpb[s], k, c);
+    }
     st.grad_count += 1;
     st.stash_version.erase(sit);
     st.bwd_issued[k] = true;
@@ -346,13 +493,27 @@ void Engine::issue_update(Stage& st) {
 void Engine::begin(const std::vector<Program>& programs) {
     if (static_cast<int>(programs.size()) != cfg_.depth)
         throw Error("expected one program per stage");
+    for (int s = 0; s < cfg_.depth; ++s) {
+        const Stage& st = stages_[static_cast<size_t>(s)];
+        if (st.local) continue;
+        const bool adjacent = (s > 0 && stages_[s - 1].local) || (s + 1 < cfg_.depth && stages_[s + 1].local);
+        if (adjacent && !st.connected)
+            throw Error("stage " + std::to_string(s) + " runs in another process and is not connected");
+    }
     sync();
     ev_.reset(new EventTable(stages_.size()));
     progs_ = programs;
     total_ops_ = 0;
     done_ops_ = 0;
-    for (const Program& p : progs_) total_ops_ += p.size();
+    // Flag sequence numbers continue across runs (every process sees the same programs).
+    mb_base_ += run_max_mb_;
+    run_max_mb_ = 0;
+    for (const Program& p : progs_)
+        for (const OpRec& op : p) run_max_mb_ = std::max(run_max_mb_, op.microbatch);
+    for (int s = 0; s < cfg_.depth; ++s)
+        if (stages_[static_cast<size_t>(s)].local) total_ops_ += progs_[static_cast<size_t>(s)].size();
     for (Stage& st : stages_) {
+        if (!st.local) continue;
         st.ptr = 0;
         st.fwd_issued.clear();
         st.bwd_issued.clear();
@@ -373,6 +534,7 @@ void Engine::issue(int upto_batch) {
     while (true) {
         bool progress = false, pending = false;
         for (Stage& st : stages_) {
+            if (!st.local) continue;
             const Program& prog = progs_[static_cast<size_t>(st.index)];
             DeviceGuard g(st.device);
             while (st.ptr < prog.size() && st.updates_issued < target) {
@@ -413,6 +575,7 @@ void Engine::issue(int upto_batch) {
 void Engine::finish() {
     if (done_ops_ != total_ops_) issue(1 << 30);
     for (Stage& st : stages_) {
+        if (!st.local) continue;
         DeviceGuard g(st.device);
         check_cuda(cudaEventRecord(st.t1, st.stream), "cudaEventRecord");
     }
@@ -425,7 +588,7 @@ void Engine::run(const std::vector<Program>& programs) {
 }
 
 double Engine::update_elapsed_ms(int s, int u0, int u1) {
-    Stage& st = stages_.at(static_cast<size_t>(s));
+    Stage& st = local_stage(s);
     const auto& ev = ev_->upd.at(static_cast<size_t>(s));
     if (u0 < 1 || u1 > static_cast<int>(ev.size()) || u0 > u1)
         throw Error("no update events for that range");
@@ -439,8 +602,11 @@ double Engine::update_elapsed_ms(int s, int u0, int u1) {
 
 void Engine::sync() {
     for (Stage& st : stages_) {
+        if (!st.local) continue;
         DeviceGuard g(st.device);
         check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
+        if (st.copy_fwd) check_cuda(cudaStreamSynchronize(st.copy_fwd), "cudaStreamSynchronize");
+        if (st.copy_bwd) check_cuda(cudaStreamSynchronize(st.copy_bwd), "cudaStreamSynchronize");
     }
 }
 
@@ -448,6 +614,7 @@ double Engine::elapsed_ms_last_run() {
     sync();
     double worst = 0.0;
     for (Stage& st : stages_) {
+        if (!st.local) continue;
         float ms = 0.0f;
         check_cuda(cudaEventElapsedTime(&ms, st.t0, st.t1), "cudaEventElapsedTime");
         worst = std::max(worst, static_cast<double>(ms));
@@ -456,7 +623,7 @@ double Engine::elapsed_ms_last_run() {
 }
 
 std::vector<double> Engine::losses(int first_mb, int count) {
-    Stage& st = stages_.back();
+    Stage& st = local_stage(cfg_.depth - 1);
     std::vector<double> out(static_cast<size_t>(count));
     DeviceGuard g(st.device);
     st.model->read_losses(out.data(), first_mb, count, st.stream);
@@ -465,7 +632,7 @@ std::vector<double> Engine::losses(int first_mb, int count) {
 }
 
 void Engine::read_version(int s, int version, void* host, size_t bytes) {
-    Stage& st = stages_.at(static_cast<size_t>(s));
+    Stage& st = local_stage(s);
     const auto it = st.version_slot.find(version);
     if (it == st.version_slot.end())
         throw Error("stage " + std::to_string(s) + " no longer holds weight version " +

@@ -44,6 +44,20 @@ struct EngineConfig {
     double lr = 0.0, momentum = 0.0;
     uint64_t seed = 0;
     std::vector<int> devices;  // per stage
+    // Cross-process pipeline: this process runs stages [first_local, first_local +
+    // local_count); 0 = all stages.  Remote neighbours are reached through CUDA IPC
+    // (export_stage / connect_stage).
+    int first_local = 0, local_count = 0;
+};
+
+// Receive-side block of one stage, exported over CUDA IPC to its neighbours'
+// processes: the activation ring, the output-gradient ring and four u32 flags.
+struct StageBlob {
+    char ipc[64];       // cudaIpcMemHandle_t of the block
+    int stage;
+    int stash_slots, grad_slots;
+    uint64_t slot_bytes;
+    uint64_t act_off, grad_off, flag_off;  // byte offsets inside the block
 };
 
 // One pipeline stage's model slice: parameters, version buffers, stash and the
@@ -118,7 +132,7 @@ public:
 
     const EngineConfig& config() const { return cfg_; }
     int depth() const { return cfg_.depth; }
-    StageModel& model(int s) { return *stages_.at(s).model; }
+    StageModel& model(int s) { return *local_stage(s).model; }
 
     // Interpret one program per stage (asynchronous; call sync() to wait).
     void run(const std::vector<Program>& programs);
@@ -145,13 +159,23 @@ public:
     // Losses of microbatches [first_mb, first_mb + count) (last stage), after sync.
     std::vector<double> losses(int first_mb, int count);
     void copy_losses_async(float* host, int first_mb, int count) {
-        stages_.back().model->copy_losses_async(host, first_mb, count, stages_.back().stream);
+        Stage& st = local_stage(cfg_.depth - 1);
+        st.model->copy_losses_async(host, first_mb, count, st.stream);
     }
+    bool is_local(int s) const { return s >= 0 && s < cfg_.depth && stages_[static_cast<size_t>(s)].local; }
+    // CUDA IPC hand-off between processes (one process per stage group).
+    StageBlob export_stage(int s);
+    void connect_stage(const StageBlob& blob);
 
 private:
+    // Flags in a stage's receive block (seq numbers, monotonically increasing).
+    enum Flag { kActReady = 0, kGradReady = 1, kNextBwd = 2, kPrevBwd = 3, kNumFlags = 4 };
+
     struct Stage {
         int index = 0;
         int device = 0;
+        bool local = true;
+        bool connected = false;  // remote stage: its block is mapped into this process
         int lo = 0, hi = 0;
         cudaStream_t stream = nullptr;
         std::unique_ptr<StageModel> model;
@@ -161,6 +185,13 @@ private:
         // receive rings owned by this stage (written by the neighbours)
         std::vector<void*> act_ring;   // [stash_slots] boundary tensors (stage input)
         std::vector<void*> grad_ring;  // [grad_slots] gradient of this stage's output
+        void* block = nullptr;         // one allocation: rings + flags (IPC-exportable)
+        uint32_t* flags = nullptr;     // [kNumFlags] inside `block`
+        bool block_mapped = false;     // opened with cudaIpcOpenMemHandle (remote stage)
+        // sends to a remote neighbour: local staging slots + a copy stream each way
+        void* send_act[2] = {nullptr, nullptr};
+        void* send_grad[2] = {nullptr, nullptr};
+        cudaStream_t copy_fwd = nullptr, copy_bwd = nullptr;
         // host-side interpreter state (mirrors semantics.cpp:198-211)
         size_t ptr = 0;
         int updates_done = 0;
@@ -183,6 +214,10 @@ private:
     int resolve_version(const Stage& st, const OpRec& op) const;
     void prune_versions(Stage& st);
     void free_buffers();
+    Stage& local_stage(int s);
+    uint32_t seq(int k) const { return static_cast<uint32_t>(mb_base_ + k); }
+    void signal_remote(uint32_t* flag, uint32_t value, cudaStream_t s);
+    void wait_flag(const uint32_t* flag, uint32_t value, cudaStream_t s);
 
     struct EventTableDeleter {
         void operator()(struct EventTable* t) const;
@@ -195,6 +230,8 @@ private:
     std::unique_ptr<struct EventTable, EventTableDeleter> ev_;
     RunStats stats_;
     bool snapshots_on_ = false;
+    long long mb_base_ = 0;  // microbatches of earlier runs (flag sequence numbers)
+    int run_max_mb_ = 0;
 };
 
 }  // namespace p2bw

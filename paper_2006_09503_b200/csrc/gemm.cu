@@ -623,7 +623,9 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     }
     KParams p{m, n, k, splits, epi};
     const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
-    prof::Scope scope("gemm", 2.0 * m * n * k,
+    // profiler class by pass: forward (K-major x K-major), dgrad (B MN-major), wgrad (both MN-major)
+    const char* cls = amn ? "gemm_wgrad" : (bmn ? "gemm_dgrad" : "gemm_fwd");
+    prof::Scope scope(cls, 2.0 * m * n * k,
                       2.0 * (static_cast<double>(m) * k + static_cast<double>(n) * k) + out_bytes * m * n, 1,
                       stream);
     if (bn == 256 && cl == 2) dispatch_major<256, 2>(amn, bmn, ta, tb, em, p, stream);

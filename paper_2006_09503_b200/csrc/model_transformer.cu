@@ -230,8 +230,11 @@ public:
             gemm_wgrad(st.logits, vp_, st.xf, h_, vp_, h_, R_, grad_ + off_head_, beta, s);
             bf16* dsrc = dxf;
             bf16* dhead = R_ < T_ ? gB_ : gA_;
+            // the LNf gradient is the top layer's FC2 output gradient: its column sum is
+            // that layer's b2 gradient (rows outside the head are zero)
             layernorm_bwd(dsrc, R_ < T_ ? st.hg : st.xl, st.meanf, st.rstdf, W + off_lnfg_, nullptr, dhead,
-                          grad_ + off_lnfg_, grad_ + off_lnfb_, first, R_, h_, red_scratch_, s);
+                          grad_ + off_lnfg_, grad_ + off_lnfb_, first, R_, h_, red_scratch_, s,
+                          grad_ + lay_[layers_ - 1].b2);
             if (R_ < T_) {
                 check_cuda(cudaMemsetAsync(gA_, 0, static_cast<size_t>(T_) * h_ * sizeof(bf16), s), "memset");
                 scatter_rows(dhead, head_idx_, gA_, R_, h_, s);
@@ -244,18 +247,20 @@ public:
             // FC2 (+ GELU'): du = (g W2) * gelu'(u)
             gemm_dgelu(g, h_, W + o.w2, 4 * h_, T_, 4 * h_, h_, st.u[l], g4_, s);
             gemm_wgrad(g, h_, st.a[l], 4 * h_, h_, 4 * h_, T_, grad_ + o.w2, beta, s);
-            colsum_bf16(g, T_, h_, h_, grad_ + o.b2, first, red_scratch_, s);
+            // b2: fused into the LayerNorm backward that produced g (LNf or the layer
+            // above's LN1); only the gradient received from the next stage needs a pass
+            if (l == layers_ - 1 && !last_) colsum_bf16(g, T_, h_, h_, grad_ + o.b2, first, red_scratch_, s);
             // FC1: dxn2 = du W1
             gemm_store_mn_b(g4_, 4 * h_, W + o.w1, h_, T_, h_, 4 * h_, gX_, s);
             gemm_wgrad(g4_, 4 * h_, st.xn2[l], h_, 4 * h_, h_, T_, grad_ + o.w1, beta, s);
             colsum_bf16(g4_, T_, 4 * h_, 4 * h_, grad_ + o.b1, first, red_scratch_, s);
             // LN2 (+ residual): dx1 = LN2'(dxn2) + g
+            // (+ bo = colsum(dx1), fused)
             layernorm_bwd(gX_, st.x1[l], st.mean2[l], st.rstd2[l], W + o.ln2g, g, gB_, grad_ + o.ln2g,
-                          grad_ + o.ln2b, first, T_, h_, red_scratch_, s);
+                          grad_ + o.ln2b, first, T_, h_, red_scratch_, s, grad_ + o.bo);
             // proj: do = dx1 Wo
             gemm_store_mn_b(gB_, h_, W + o.wo, h_, T_, h_, h_, gX_, s);
             gemm_wgrad(gB_, h_, st.o[l], h_, h_, h_, T_, grad_ + o.wo, beta, s);
-            colsum_bf16(gB_, T_, h_, h_, grad_ + o.bo, first, red_scratch_, s);
             // attention
             attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
                           cfg_.causal != 0, s);
@@ -265,8 +270,9 @@ public:
             colsum_bf16(g3_, T_, 3 * h_, 3 * h_, grad_ + o.bqkv, first, red_scratch_, s);
             // LN1 (+ residual): dx = LN1'(dxn1) + dx1
             bf16* dst = (l > 0 || first_) ? gA_ : static_cast<bf16*>(g_out);
+            // (+ b2 of the layer below = colsum(dx), fused)
             layernorm_bwd(gX_, x, st.mean1[l], st.rstd1[l], W + o.ln1g, gB_, dst, grad_ + o.ln1g, grad_ + o.ln1b,
-                          first, T_, h_, red_scratch_, s);
+                          first, T_, h_, red_scratch_, s, l > 0 ? grad_ + lay_[l - 1].b2 : nullptr);
             g = dst;
         }
         if (first_) {

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "profiler.h"
 #include "ptx.cuh"
@@ -105,36 +106,47 @@ __global__ void k_embed_bwd_pos(const bf16* __restrict__ dx0, float* __restrict_
 
 // ---- deterministic reductions ------------------------------------------------------
 
-// out[c] (=|+=) sum_{p < parts} part[p * n + c], fixed order; 32 columns x 8 part lanes.
-__global__ void k_reduce_parts(const float* __restrict__ part, int parts, int n,
-                               float* __restrict__ out, int overwrite) {
+// Second phase of the deterministic column reductions, for up to 3 statistics at
+// once (blockIdx.y): out_y[c] (=|+=) sum_{p < parts} part[(y * parts + p) * n + c] in a
+// fixed order.  32 columns x 8 part lanes per CTA; eight independent accumulators
+// keep eight L2 loads in flight per thread (the phase is latency-, not byte-bound).
+struct ReduceOut {
+    float* out[3];
+};
+
+__global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ part, int parts, int n,
+                                                      ReduceOut outs, int overwrite) {
     __shared__ float red[8][33];
     const int col = blockIdx.x * 32 + (threadIdx.x & 31);
     const int lane8 = threadIdx.x >> 5;
-    // four independent accumulators (parts p, p+8, p+16, p+24 of each stride of 32)
-    // keep four loads in flight; combined in a fixed order, so still deterministic
-    float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const float* base = part + static_cast<size_t>(blockIdx.y) * parts * n;
+    float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
     if (col < n) {
         int p = lane8;
-        for (; p + 24 < parts; p += 32) {
+        for (; p + 56 < parts; p += 64) {
+            float v[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) a[u] += part[static_cast<size_t>(p + 8 * u) * n + col];
+            for (int u = 0; u < 8; ++u) v[u] = base[static_cast<size_t>(p + 8 * u) * n + col];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] += v[u];
         }
-        for (int u = 0; p < parts; p += 8, ++u) a[u & 3] += part[static_cast<size_t>(p) * n + col];
+        for (int u = 0; p < parts; p += 8, ++u) a[u & 7] += base[static_cast<size_t>(p) * n + col];
     }
-    const float acc = (a[0] + a[1]) + (a[2] + a[3]);
+    const float acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     red[lane8][threadIdx.x & 31] = acc;
     __syncthreads();
     if (lane8 == 0 && col < n) {
         float s = 0.0f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) s += red[i][threadIdx.x & 31];
+        float* out = outs.out[blockIdx.y];
         out[col] = overwrite ? s : out[col] + s;
     }
 }
 
 void reduce_parts(const float* part, int parts, int n, float* out, bool overwrite, cudaStream_t s) {
-    k_reduce_parts<<<(n + 31) / 32, 256, 0, s>>>(part, parts, n, out, overwrite ? 1 : 0);
+    ReduceOut o{{out, nullptr, nullptr}};
+    k_reduce_parts<<<dim3((n + 31) / 32, 1), 256, 0, s>>>(part, parts, n, o, overwrite ? 1 : 0);
 }
 
 // Column statistics of a bf16 matrix, per row-block partials (block = 32 column
@@ -241,55 +253,131 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
     }
 }
 
-// dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) (+ dres), dxh = dy * g;
-// one warp per row, no cross-row state (gamma / beta gradients: k_colstats<true>).
-template <int NV>
-__global__ void __launch_bounds__(256) k_ln_bwd_dx(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                                   const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                   const bf16* __restrict__ g, const bf16* __restrict__ dres,
-                                                   bf16* __restrict__ dx, int rows, int h) {
-    const int lane = threadIdx.x & 31;
-    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (r >= rows) return;
+// Fused LayerNorm backward.  Row part (warp per row):
+//   dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) (+ dres),  dxh = dy * g
+// Column part, accumulated in registers over the rows a warp visits and reduced
+// over the block's warps in SMEM -> one partial per block and statistic:
+//   stat 0: sum_r dy * xh  (d gamma)     stat 1: sum_r dy  (d beta)
+//   stat 2 (kSum): sum_r bf16(dx)  -- the bias gradient of the linear layer whose
+//                  output gradient dx is (saves a separate pass over dx).
+// dx may alias dy: each warp reads its whole row before writing it.  Row r goes
+// to warp r mod (grid warps): deterministic.  Row data stays packed bf16 in
+// registers between the two passes.
+// 16 warps per SM for h <= 768; wide rows (more accumulators per lane) get 8 warps
+// and the full 255-register budget.
+__host__ __device__ constexpr int ln_bwd_threads(int nv) { return nv >= 4 ? 256 : 512; }
+
+template <int NV, bool kSum>
+__global__ void __launch_bounds__(ln_bwd_threads(NV), 1)
+    k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
+             const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
+             bf16* dx, int rows, int h, float* __restrict__ part) {
+    extern __shared__ float red[];  // [kWarps][h]
+    constexpr int kThreads = ln_bwd_threads(NV), kWarps = kThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int hv = h / 8;
-    const float mu = mean[r], rs = rstd[r];
-    float xh[NV][8], dxh[NV][8];
-    float s1 = 0.0f, s2 = 0.0f;
+    float ag[NV][8], ab[NV][8], as[kSum ? NV : 1][8];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-        const int vi = lane + 32 * i;
-        if (vi < hv) {
-            float xv[8], dv[8], gv[8];
-            load8(x + static_cast<size_t>(r) * h + vi * 8, xv);
-            load8(dy + static_cast<size_t>(r) * h + vi * 8, dv);
-            load8(g + vi * 8, gv);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                xh[i][q] = (xv[q] - mu) * rs;
-                dxh[i][q] = dv[q] * gv[q];
-                s1 += dxh[i][q];
-                s2 += dxh[i][q] * xh[i][q];
+        for (int q = 0; q < 8; ++q) {
+            ag[i][q] = 0.0f;
+            ab[i][q] = 0.0f;
+            if constexpr (kSum) as[i][q] = 0.0f;
+        }
+    }
+    for (int r = blockIdx.x * kWarps + warp; r < rows; r += gridDim.x * kWarps) {
+        const float mu = mean[r], rs = rstd[r];
+        uint4 xp[NV], dp[NV];
+        float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int vi = lane + 32 * i;
+            if (vi < hv) {
+                xp[i] = *reinterpret_cast<const uint4*>(x + static_cast<size_t>(r) * h + vi * 8);
+                dp[i] = *reinterpret_cast<const uint4*>(dy + static_cast<size_t>(r) * h + vi * 8);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            if (lane + 32 * i < hv) {
+                const uint32_t xw[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
+                const uint32_t dw[4] = {dp[i].x, dp[i].y, dp[i].z, dp[i].w};
+                float gv[8];  // gamma: re-read per row from L1 (keeps registers for the sums)
+                load8(g + (lane + 32 * i) * 8, gv);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
+                    const float xh0 = (xf.x - mu) * rs, xh1 = (xf.y - mu) * rs;
+                    const float d0 = df.x * gv[2 * t], d1 = df.y * gv[2 * t + 1];
+                    s1 += d0 + d1;
+                    s2 += d0 * xh0 + d1 * xh1;
+                    ag[i][2 * t] = fmaf(df.x, xh0, ag[i][2 * t]);
+                    ag[i][2 * t + 1] = fmaf(df.y, xh1, ag[i][2 * t + 1]);
+                    ab[i][2 * t] += df.x;
+                    ab[i][2 * t + 1] += df.y;
+                }
+            }
+        }
+        const float m1 = warp_sum(s1) / h, m2 = warp_sum(s2) / h;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int vi = lane + 32 * i;
+            if (vi < hv) {
+                const uint32_t xw[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
+                const uint32_t dw[4] = {dp[i].x, dp[i].y, dp[i].z, dp[i].w};
+                float gv[8], o[8];
+                load8(g + vi * 8, gv);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
+                    o[2 * t] = rs * (df.x * gv[2 * t] - m1 - (xf.x - mu) * rs * m2);
+                    o[2 * t + 1] = rs * (df.y * gv[2 * t + 1] - m1 - (xf.y - mu) * rs * m2);
+                }
+                if (dres != nullptr) {
+                    float rv[8];
+                    load8(dres + static_cast<size_t>(r) * h + vi * 8, rv);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) o[q] += rv[q];
+                }
+                const uint4 packed = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
+                                                ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
+                *reinterpret_cast<uint4*>(dx + static_cast<size_t>(r) * h + vi * 8) = packed;
+                if constexpr (kSum) {  // the bias gradient sums what the next GEMM reads: bf16(dx)
+                    const uint32_t pw[4] = {packed.x, packed.y, packed.z, packed.w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float2 pf = ptx::unpack_bf16x2(pw[t]);
+                        as[i][2 * t] += pf.x;
+                        as[i][2 * t + 1] += pf.y;
+                    }
+                }
             }
         }
     }
-    const float m1 = warp_sum(s1) / h, m2 = warp_sum(s2) / h;
+    // block reduction over the warps, one statistic at a time, fixed order
+    for (int st = 0; st < (kSum ? 3 : 2); ++st) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int vi = lane + 32 * i;
-        if (vi < hv) {
-            float o[8];
+        for (int i = 0; i < NV; ++i) {
+            const int vi = lane + 32 * i;
+            if (vi < hv) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = rs * (dxh[i][q] - m1 - xh[i][q] * m2);
-            if (dres != nullptr) {
-                float rv[8];
-                load8(dres + static_cast<size_t>(r) * h + vi * 8, rv);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) o[q] += rv[q];
+                for (int q = 0; q < 8; ++q)
+                    red[warp * h + vi * 8 + q] = st == 0 ? ag[i][q] : (st == 1 ? ab[i][q] : as[kSum ? i : 0][q]);
             }
-            store8(dx + static_cast<size_t>(r) * h + vi * 8, o);
         }
+        __syncthreads();
+        for (int c = threadIdx.x; c < h; c += kThreads) {
+            float sum = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) sum += red[w * h + c];
+            part[(static_cast<size_t>(st) * gridDim.x + blockIdx.x) * h + c] = sum;
+        }
+        __syncthreads();
     }
 }
+
+int ln_bwd_blocks(int rows) { return std::max(1, std::min(148, (rows + 15) / 16)); }
 
 // ---- softmax cross-entropy ------------------------------------------------------------
 
@@ -482,32 +570,48 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
     check_cuda(cudaGetLastError(), "layernorm_fwd");
 }
 
-size_t layernorm_bwd_scratch_floats(int rows, int h) {
-    return static_cast<size_t>(colsum_row_blocks(rows, h)) * h * 2;
+size_t layernorm_bwd_scratch_floats(int rows, int h) { return static_cast<size_t>(ln_bwd_blocks(rows)) * h * 3; }
+
+template <int NV, bool kSum>
+void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
+                   const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
+    constexpr int kThreads = ln_bwd_threads(NV);
+    const size_t smem = static_cast<size_t>(kThreads / 32) * h * sizeof(float);
+    static std::atomic<uint32_t> configured{0};
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if ((configured.load() & (1u << (dev & 31))) == 0) {
+        check_cuda(cudaFuncSetAttribute(k_ln_bwd<NV, kSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        16 * 2048 * static_cast<int>(sizeof(float))),
+                   "cudaFuncSetAttribute(ln bwd smem)");
+        configured.fetch_or(1u << (dev & 31));
+    }
+    k_ln_bwd<NV, kSum><<<grid, kThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, part);
+}
+
+template <bool kSum>
+void dispatch_ln_bwd(int nv, int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd,
+                     const bf16* g, const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
+    switch (nv) {
+        case 1: launch_ln_bwd<1, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
+        case 2: launch_ln_bwd<2, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
+        case 3: launch_ln_bwd<3, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
+        case 4: launch_ln_bwd<4, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
+        default: launch_ln_bwd<8, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
+    }
 }
 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, float* dg, float* db, bool overwrite, int rows, int h,
-                   float* scratch, cudaStream_t s) {
+                   float* scratch, cudaStream_t s, float* dsum) {
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
-    prof::Scope scope("layernorm_bwd", 0.0, (dres ? 10.0 : 8.0) * rows * h + 8.0 * rows, 5, s);
-    // gamma / beta statistics first: dx may alias dy (in-place LN backward)
-    const int rb = colsum_row_blocks(rows, h);
-    const int rpb = (rows + rb - 1) / rb;
-    float* pg = scratch;
-    float* pb = scratch + static_cast<size_t>(rb) * h;
-    k_colstats<true><<<dim3((h + 255) / 256, rb), 256, 0, s>>>(dy, x, mean, rstd, rows, h, h, rpb, pg, pb);
-    reduce_parts(pg, rb, h, dg, overwrite, s);
-    reduce_parts(pb, rb, h, db, overwrite, s);
+    prof::Scope scope("layernorm_bwd", 0.0, (dres ? 8.0 : 6.0) * rows * h + 8.0 * rows, 2, s);
+    const int grid = ln_bwd_blocks(rows);
     const int nv = (h / 8 + 31) / 32;
-    const int grid = (rows + 7) / 8;
-    switch (nv) {
-        case 1: k_ln_bwd_dx<1><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
-        case 2: k_ln_bwd_dx<2><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
-        case 3: k_ln_bwd_dx<3><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
-        case 4: k_ln_bwd_dx<4><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
-        default: k_ln_bwd_dx<8><<<grid, 256, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h); break;
-    }
+    if (dsum) dispatch_ln_bwd<true>(nv, grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
+    else dispatch_ln_bwd<false>(nv, grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
+    ReduceOut o{{dg, db, dsum}};
+    k_reduce_parts<<<dim3((h + 31) / 32, dsum ? 3 : 2), 256, 0, s>>>(scratch, grid, h, o, overwrite ? 1 : 0);
     check_cuda(cudaGetLastError(), "layernorm_bwd");
 }
 

@@ -23,10 +23,12 @@ void embed_bwd(const int* ids, const bf16* dx0, float* dtok, float* dpos, int to
 // y = LN(x) * g + b ; mean / rstd per row saved for the backward.
 void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean, float* rstd,
                    int rows, int h, cudaStream_t s);
-// dx = LN'(dy) (+ dres); dg / db (=|+=) column sums, deterministic two-phase.
+// dx = LN'(dy) (+ dres); dg / db (=|+=) column sums, deterministic two-phase; with
+// dsum != nullptr also dsum (=|+=) sum_r bf16(dx[r, :]) (the bias gradient of the
+// layer that consumes dx as its output gradient).  dx may alias dy.
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, float* dg, float* db, bool overwrite, int rows, int h,
-                   float* scratch, cudaStream_t s);
+                   float* scratch, cudaStream_t s, float* dsum = nullptr);
 size_t layernorm_bwd_scratch_floats(int rows, int h);
 
 // out[n] (=|+=) sum_r x[r, n]  (bias gradients), deterministic two-phase.

@@ -1,7 +1,11 @@
-"""Multi-process plumbing for data-parallel replicas (torch.distributed is only
-plumbing here: rendezvous, the NCCL unique-id exchange and max-over-ranks
-timing).  The data-path collective itself is the engine's NCCL all-reduce at
-the AllReduce op (include/p2bw.h: p2bw_engine_join_replicas)."""
+"""Multi-process plumbing for pipelines and data-parallel replicas.
+
+torch.distributed is only plumbing here: rendezvous, the exchange of NCCL
+unique ids and of CUDA-IPC stage blobs, and max-over-ranks timing.  The data
+path is the engine's: stage hand-offs over CUDA IPC (p2bw_engine_connect_stage)
+and the NCCL all-reduce at the AllReduce op (p2bw_engine_join_replicas).
+
+Rank layout (profile.cpp:99-101): gpu = stage * width + replica."""
 from __future__ import annotations
 
 from typing import Callable
@@ -47,11 +51,47 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def join_replicas(engine, depth: int) -> None:
-    """Make this process's pipeline one of `world` data-parallel replicas."""
+def grid(world: int, rank: int, depth: int) -> tuple[int, int, int]:
+    """(stage, replica, width) of `rank` when `world` processes run a depth-`depth`
+    pipeline, one stage per process: gpu = stage * width + replica."""
+    if depth < 1 or world % depth:
+        raise ValueError(f"{world} processes cannot form pipelines of depth {depth}")
+    width = world // depth
+    return rank // width, rank % width, width
+
+
+def join_replicas(engine, depth: int, pipelined: bool = False) -> None:
+    """Join this process's stages to their data-parallel replica groups.
+
+    pipelined=False: every process runs a whole pipeline (width = world).
+    pipelined=True: one stage per process laid out by :func:`grid`."""
     import ctypes as C
 
     from . import _lib
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if pipelined:
+        _, replica, width = grid(world, rank, depth)
+    else:
+        replica, width = rank, world
     ids = share_unique_ids(depth, nccl_unique_id)
     arr = (C.c_ubyte * len(ids)).from_buffer_copy(ids)
-    _lib.check(_lib.lib().p2bw_engine_join_replicas(engine.h, arr, dist.get_world_size(), dist.get_rank()))
+    _lib.check(_lib.lib().p2bw_engine_join_replicas(engine.h, arr, width, replica))
+
+
+def connect_pipeline(engine, depth: int) -> None:
+    """Exchange CUDA-IPC stage blobs and connect each local stage's remote
+    neighbours (same replica, stage +- 1).  Collective over the default group."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    _, replica, width = grid(world, rank, depth)
+    mine = {s: engine.export_stage(s) for s in range(depth) if engine.is_local(s)}
+    gathered: list = [None] * world
+    dist.all_gather_object(gathered, (replica, mine))
+    for rep, blobs in gathered:
+        if rep != replica:
+            continue
+        for s, blob in blobs.items():
+            if engine.is_local(s):
+                continue
+            if (s > 0 and engine.is_local(s - 1)) or (s + 1 < depth and engine.is_local(s + 1)):
+                engine.connect_stage(blob)
+    dist.barrier()

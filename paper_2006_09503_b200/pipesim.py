@@ -204,7 +204,10 @@ class Desc(C.Structure):
                 ("dim", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("seq_len", C.c_int),
                 ("vocab", C.c_int), ("causal", C.c_int), ("head_rows", C.c_int),
                 ("learning_rate", C.c_double), ("momentum", C.c_double), ("seed", C.c_ulonglong),
-                ("devices", C.POINTER(C.c_int))]
+                ("devices", C.POINTER(C.c_int)), ("first_local_stage", C.c_int), ("local_stages", C.c_int)]
+
+
+STAGE_BLOB_BYTES = 128  # P2BW_STAGE_BLOB_BYTES
 
 
 class Counters(C.Structure):
@@ -217,17 +220,23 @@ MODEL_TRANSFORMER = 1
 
 
 class Engine:
-    """The B200 stage executor (one CUDA stream per stage, all stages of one pipeline)."""
+    """The B200 stage executor (one CUDA stream per stage).
+
+    ``local_stages=None`` runs every stage of the pipeline in this process;
+    ``local_stages=(first, count)`` runs only those, the others living in other
+    processes that are connected through :meth:`export_stage` / :meth:`connect_stage`
+    (see :func:`paper_2006_09503_b200.dist.connect_pipeline`)."""
 
     def __init__(self, *, model_kind: int, policy: PipelinePolicy, depth: int, microbatches: int,
                  microbatch_size: int, layers: int, dim: int = 0, hidden: int = 0, heads: int = 0,
                  seq_len: int = 0, vocab: int = 0, causal: int = 0, head_rows: int = 0,
                  learning_rate: float = 0.0, momentum: float = 0.0, seed: int = 0,
-                 devices: list[int] | None = None):
+                 devices: list[int] | None = None, local_stages: tuple[int, int] | None = None):
         self._devs = (C.c_int * depth)(*devices) if devices else None
+        first, count = local_stages if local_stages is not None else (0, 0)
         d = Desc(model_kind, int(policy), depth, 1, microbatches, microbatch_size, layers, dim, hidden,
                  heads, seq_len, vocab, causal, head_rows, learning_rate, momentum, seed,
-                 C.cast(self._devs, C.POINTER(C.c_int)) if self._devs else None)
+                 C.cast(self._devs, C.POINTER(C.c_int)) if self._devs else None, first, count)
         self.h = C.c_void_p()
         _call("p2bw_engine_create", C.byref(d), C.byref(self.h))
         self.depth = depth
@@ -284,6 +293,22 @@ class Engine:
 
     def sync(self):
         _call("p2bw_engine_sync", self.h)
+
+    def is_local(self, stage: int) -> bool:
+        out = C.c_int()
+        _call("p2bw_engine_is_local", self.h, stage, C.byref(out))
+        return bool(out.value)
+
+    def export_stage(self, stage: int) -> bytes:
+        buf = (C.c_char * STAGE_BLOB_BYTES)()
+        _call("p2bw_engine_export_stage", self.h, stage, buf, C.c_size_t(STAGE_BLOB_BYTES))
+        return bytes(buf)
+
+    def connect_stage(self, blob: bytes):
+        if len(blob) != STAGE_BLOB_BYTES:
+            raise ValueError("stage blob must be %d bytes" % STAGE_BLOB_BYTES)
+        buf = (C.c_char * STAGE_BLOB_BYTES).from_buffer_copy(blob)
+        _call("p2bw_engine_connect_stage", self.h, buf, C.c_size_t(STAGE_BLOB_BYTES))
 
     def counters(self) -> Counters:
         c = Counters()

@@ -68,3 +68,13 @@ def test_data_parallel_average_equals_wide_microbatch(w):
     g_one, _ = O._batch_gradient(model, W, 1, 4)
     for a, b in zip(g_dp, g_one):
         assert np.allclose(a, b, rtol=1e-12, atol=1e-14)
+
+
+def test_pipeline_rank_grid():
+    """gpu = stage * width + replica (profile.cpp:99-101)."""
+    from paper_2006_09503_b200.dist import grid
+    assert [grid(8, r, 4) for r in range(8)] == [(s, w, 2) for s in range(4) for w in range(2)]
+    assert [grid(4, r, 4)[0] for r in range(4)] == [0, 1, 2, 3]
+    assert grid(8, 5, 1) == (0, 5, 8)
+    with pytest.raises(ValueError):
+        grid(6, 0, 4)

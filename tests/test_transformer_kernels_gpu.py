@@ -60,7 +60,8 @@ def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
 
 
 @pytest.mark.parametrize("rows,h", [(300, 256), (1024, 768), (64, 1024), (33, 1920)])
-def test_layernorm_fwd_bwd_vs_torch(rows, h):
+@pytest.mark.parametrize("with_dsum", [False, True])
+def test_layernorm_fwd_bwd_vs_torch(rows, h, with_dsum=True):
     g = torch.Generator(device="cuda").manual_seed(rows + h)
     x = (torch.randn(rows, h, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
     w = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).to(torch.bfloat16)
@@ -80,14 +81,20 @@ def test_layernorm_fwd_bwd_vs_torch(rows, h):
     dx = torch.empty_like(x)
     dg = torch.full((h,), 5.0, device="cuda")
     db = torch.full((h,), 5.0, device="cuda")
+    ds = torch.full((h,), 5.0, device="cuda")
     call("p2bw_kernel_layernorm_bwd", ptr(dy), ptr(x), ptr(mean), ptr(rstd), ptr(w), ptr(dres), ptr(dx), ptr(dg),
-         ptr(db), 0, rows, h, stream())  # accumulate onto 5.0
+         ptr(db), ptr(ds) if with_dsum else None, 0, rows, h, stream())  # accumulate onto 5.0
     yr.backward(dy.float())
     torch.cuda.synchronize()
     ref_dx = xr.grad + dres.float()
     assert (dx.float() - ref_dx).abs().max().item() < 3e-2 * max(1.0, ref_dx.abs().max().item())
     assert (dg - 5.0 - wr.grad).abs().max().item() < 1e-2 * max(1.0, wr.grad.abs().max().item())
     assert (db - 5.0 - br.grad).abs().max().item() < 1e-2 * max(1.0, br.grad.abs().max().item())
+    if with_dsum:  # fused bias gradient: column sums of the bf16 dx the kernel stored
+        ref_ds = dx.float().sum(0)
+        assert (ds - 5.0 - ref_ds).abs().max().item() < 1e-3 * max(1.0, ref_ds.abs().max().item())
+    else:
+        assert torch.all(ds == 5.0)
 
 
 @pytest.mark.parametrize("rows,vocab", [(64, 1000), (16, 51200), (130, 30522)])
@@ -142,8 +149,9 @@ def test_layernorm_bwd_in_place():
     buf = dy.clone()
     dg = torch.empty(h, device="cuda")
     db = torch.empty(h, device="cuda")
+    ds = torch.empty(h, device="cuda")
     call("p2bw_kernel_layernorm_bwd", ptr(buf), ptr(x), ptr(mean), ptr(rstd), ptr(w), None, ptr(buf), ptr(dg),
-         ptr(db), 1, rows, h, stream())
+         ptr(db), ptr(ds), 1, rows, h, stream())
     xr = x.float().requires_grad_(True)
     wr = w.float().requires_grad_(True)
     br = bb.float().requires_grad_(True)
@@ -152,3 +160,4 @@ def test_layernorm_bwd_in_place():
     assert (buf.float() - xr.grad).abs().max().item() < 3e-2 * max(1.0, xr.grad.abs().max().item())
     assert (dg - wr.grad).abs().max().item() < 1e-2 * max(1.0, wr.grad.abs().max().item())
     assert (db - br.grad).abs().max().item() < 1e-2 * max(1.0, br.grad.abs().max().item())
+    assert (ds - buf.float().sum(0)).abs().max().item() < 1e-3 * max(1.0, buf.float().sum(0).abs().max().item())
