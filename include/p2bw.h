@@ -195,6 +195,15 @@ int p2bw_engine_is_local(p2bw_engine* eng, int stage, int* out);
 int p2bw_engine_export_stage(p2bw_engine* eng, int stage, void* blob, size_t bytes);
 int p2bw_engine_connect_stage(p2bw_engine* eng, const void* blob, size_t bytes);
 int p2bw_engine_sync(p2bw_engine* eng);
+/* Measured timeline.  With tracing on, every op the engine
+ * issues is bracketed by CUDA events on its stage stream (set before begin / run).
+ * trace_report renders the last run as the reference's SimReport document
+ * (report_to_json, simulator.cpp:356-390): timeline entries per worker in seconds,
+ * throughput / steady_batch_time / bubble_fraction computed as simulate() does
+ * (simulator.cpp:298-329) but from measured times, and per-op memory samples
+ * (live versions, stashes, bytes).  Free with p2bw_free. */
+int p2bw_engine_set_trace(p2bw_engine* eng, int on);
+int p2bw_engine_trace_report(p2bw_engine* eng, char** out_json);
 int p2bw_engine_counters(p2bw_engine* eng, p2bw_counters* out);
 /* Weights created by a stage's update_index-th update of the last run (snapshots on). */
 int p2bw_engine_read_snapshot(p2bw_engine* eng, int stage, int update_index, void* host,
@@ -207,6 +216,17 @@ int p2bw_engine_read_master(p2bw_engine* eng, int stage, void* host, size_t byte
 int p2bw_engine_losses_async(p2bw_engine* eng, int first_mb, int count, float* host);
 /* Training losses of microbatches [first_mb, first_mb+count) (last stage). */
 int p2bw_engine_losses(p2bw_engine* eng, int first_mb, int count, double* out);
+
+/* ---- B200 block profiler -> planner ------------------- */
+
+/* Times every block of the transformer described by *desc (one layer per block;
+ * the embedding folds into block 0, LNf + LM head + loss into the last block) on
+ * the current device at each microbatch size, running the stage executor's own
+ * Forward / Backward kernels, and returns the profile document the reference's
+ * load_model_profile reads (profile.cpp:162-193; fwd_ms / bwd_ms / weight_bytes /
+ * act_*_bytes keyed by microbatch size).  Feed it to p2bw_plan.  Free with p2bw_free. */
+int p2bw_profile_blocks(const p2bw_desc* desc, const int* microbatch_sizes, int n_sizes, int warmup,
+                        int iters, const char* name, char** out_json);
 
 /* ---- measurement --------------------------------------------------------- */
 
@@ -266,8 +286,8 @@ int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void*
 int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                               const void* g, const void* dres, void* dx, void* dg, void* db, void* dsum,
                               int overwrite, int rows, int h, void* stream);
-/* Debug: per-CTA phase clocks of the tcgen05 attention forward into a device buffer
- * of 16 uint64 per CTA (NULL switches it off). */
+/* Debug: per-CTA phase clocks of the tcgen05 attention forward (16 uint64 per CTA)
+ * and backward (64 uint64 per CTA) into a device buffer (NULL switches it off). */
 int p2bw_debug_attention_timing(void* dev_buf);
 /* Column sums of a bf16 matrix (bias gradients): out (=|+=) sum_r x[r, :]. */
 int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream);

@@ -79,12 +79,15 @@ def _signatures():
         ("p2bw_engine_export_stage", i, [vp, i, vp, sz]),
         ("p2bw_engine_connect_stage", i, [vp, vp, sz]),
         ("p2bw_engine_sync", i, [vp]),
+        ("p2bw_engine_set_trace", i, [vp, i]),
+        ("p2bw_engine_trace_report", i, [vp, pvp]),
         ("p2bw_engine_counters", i, [vp, vp]),
         ("p2bw_engine_read_snapshot", i, [vp, i, i, vp, sz]),
         ("p2bw_engine_read_version", i, [vp, i, i, vp, sz]),
         ("p2bw_engine_read_master", i, [vp, i, vp, sz]),
         ("p2bw_engine_losses_async", i, [vp, i, i, vp]),
         ("p2bw_engine_losses", i, [vp, i, i, vp]),
+        ("p2bw_profile_blocks", i, [vp, pi, i, i, i, cp, pvp]),
         ("p2bw_launch_count", ll, []),
         ("p2bw_profile_enable", None, [i]),
         ("p2bw_profile_collect", i, [vp, i, C.POINTER(C.c_int)]),

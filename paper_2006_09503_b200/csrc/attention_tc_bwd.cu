@@ -1,26 +1,35 @@
 // Softmax attention backward on tcgen05 tensor cores (head dim 64, seq % 128 == 0,
-// seq <= 512).  Key-outer: one CTA per (sequence, head, 128-key tile j) walks the
-// query tiles i that can see it (all of them, or i >= j when causal):
+// seq <= 512).  Persistent and key-outer: one CTA per SM walks work items
+// (128-key tile j, sequence, head) -- j-major, so causal items with the most query
+// tiles go first -- and for each item the query tiles i that can see it:
 //
 //   UMMA  S^T  = K_j Q_i^T          128 x 128 fp32, TMEM [0, 128)
 //   UMMA  dP^T = V_j dO_i^T         TMEM [128, 256)
-//   SIMT  P^T  = exp(S^T/8 - lse_i), dS^T = P^T (dP^T - delta_i)  (thread = key row)
-//         written as bf16 into SMEM in the UMMA K-major SW128 layout
-//   UMMA  dV_j += P^T dO_i          TMEM [256, 320)   (dO_i read MN-major)
+//   SIMT  P^T  = exp(S^T/8 - lse_i), dS^T = P^T (dP^T - delta_i)   (8 warps, thread =
+//         key row, warp half = 64 query columns); P^T goes back into TMEM as packed
+//         bf16 [448, 512), dS^T into SMEM in the UMMA K-major SW128 layout
+//   UMMA  dV_j += P^T dO_i          TMEM [256, 320)   (A = P^T from TMEM, dO_i MN-major)
 //   UMMA  dK_j += dS^T Q_i          TMEM [320, 384)   (Q_i read MN-major)
-//   UMMA  dQ_i|j = dS K_j           TMEM [384, 448)   (dS^T read MN-major, K_j MN-major)
+//   UMMA  dQ_i|j = dS K_j           TMEM [384, 448)   (dS^T and K_j read MN-major)
+//   flush dQ_i|j: TMEM -> SMEM (SW128) -> TMA reduce-add into an fp32 dQ accumulator
+//         (L2-resident, zeroed by the delta kernel; k_attn_dq_convert casts it)
 //
-// The same SMEM bytes serve as K-major and MN-major operands (a 128-byte swizzled
-// row of 64 elements is both "64 k-values of one row" and "64 mn-values of one
-// k"), so no transposes are materialised.  dQ partials are written per key tile
-// (fp32, no atomics) and summed in fixed order by a small kernel: deterministic.
-// Q_i / dO_i / lse_i / delta_i are double-buffered so TMA overlaps compute.
+// Warp roles (16 warps): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4-11
+// elementwise, 12-15 dQ flush + dK/dV epilogue of an item's last query tile.
+// K/V (per item) are double-buffered and Q/dO/lse/delta (per query tile) triple-
+// buffered, so TMA runs ahead across items; the S/dP MMAs of tile g+1 are issued before the dV/dK/dQ MMAs
+// of tile g, so the exp work of g+1 overlaps them.  The same SMEM bytes serve as
+// K-major and MN-major operands, so no transposes are materialised.
+//
+// The fp32 dQ reduce-add makes dQ's summation order over key tiles (<= 4 terms)
+// run-dependent; everything else is deterministic.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
 
+#include "kernels.h"
 #include "profiler.h"
 #include "ptx.cuh"
 #include "tkernels.h"
@@ -30,78 +39,89 @@ namespace p2bw {
 
 CUtensorMap make_tmap_bf16_2d(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld_elems,
                               uint32_t box_inner, uint32_t box_outer);  // gemm.cu
+CUtensorMap make_tmap_f32_2d(const float* ptr, uint64_t inner, uint64_t outer, int64_t ld_elems,
+                             uint32_t box_inner, uint32_t box_outer);  // gemm.cu
 
 namespace {
 
-constexpr int kT = 128;   // tile rows (keys or queries)
+constexpr int kT = 128;  // tile rows (keys or queries)
 constexpr int kD = 64;
-constexpr int kTile = kT * 128;  // 16 KB
-constexpr int oK = 0, oV = oK + kTile;
-constexpr int oQ = oV + kTile;          // [2] tiles
-constexpr int oDO = oQ + 2 * kTile;     // [2]
-constexpr int oPt = oDO + 2 * kTile;    // 2 blocks (q 0-63, 64-127)
-constexpr int oDSt = oPt + 2 * kTile;   // 2 blocks
-constexpr int oLse = oDSt + 2 * kTile;  // [2][128] f32
-constexpr int oDel = oLse + 2 * kT * 4; // [2][128] f32
-constexpr int oBar = oDel + 2 * kT * 4;
+constexpr int kTile = kT * 128;  // 16 KB: 128 rows of 64 bf16
+constexpr int kQS = 3;                  // query-tile ring depth (covers the TMA latency)
+constexpr int oK = 0;                   // [2] per item
+constexpr int oV = oK + 2 * kTile;      // [2]
+constexpr int oQ = oV + 2 * kTile;      // [kQS] per query tile
+constexpr int oDO = oQ + kQS * kTile;   // [kQS]
+constexpr int oDSt = oDO + kQS * kTile; // 2 blocks of 64 queries
+constexpr int oDQ = oDSt + 2 * kTile;   // 4 flush warps x 32 rows x 128 B
+constexpr int oLse = oDQ + 4 * 4096;    // [kQS][128] f32
+constexpr int oDel = oLse + kQS * kT * 4; // [kQS][128] f32
+constexpr int oBar = oDel + kQS * kT * 4;
 constexpr int kSmem = oBar + 256 + 1024;
+constexpr int kThreads = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     ptx::smem_u32(dst)),
+// barrier indices
+constexpr int bKvFull = 0, bKvEmpty = 2, bQFull = 4, bQEmpty = 4 + kQS, bSdpFull = 4 + 2 * kQS,
+              bSdpFree = bSdpFull + 1, bPdsFull = bSdpFull + 2, bMm2 = bSdpFull + 3, bDqFree = bSdpFull + 4,
+              bKvAccFree = bSdpFull + 5, kNumBars = bSdpFull + 6;
+// P^T lives in TMEM as bf16 (two per 32-bit column) and feeds dV = P^T dO as the
+// tcgen05 A operand straight from TMEM.
+constexpr uint32_t tS = 0, tDP = 128, tDV = 256, tDK = 320, tDQ = 384, tPT = 448;
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(ptx::smem_u32(bar))
                  : "memory");
 }
 
-// 32 consecutive q-values of key row r into a K-major SW128 pair of 64-column blocks.
-__device__ __forceinline__ void store_row32(uint8_t* base, int r, int col0, const float (&v)[32]) {
-    uint8_t* blk = base + (col0 / 64) * kTile + r * 128;
-    const int chunk0 = (col0 % 64) / 8;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint4 w = make_uint4(ptx::pack_bf16x2(v[8 * q], v[8 * q + 1]), ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                                   ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
-                                   ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
-        *reinterpret_cast<uint4*>(blk + (((chunk0 + q) ^ (r & 7)) << 4)) = w;
-    }
+// Phase timestamps (debug; null in production): p2bw_debug_attention_timing.  Per CTA
+// 64 u64 slots: [0..7] elem warp 4 "S/dP seen" for g = 0..7, [8..15] its "computed",
+// [16..23] its "mm2(g-1) seen", [24..31] its "pds arrived", [32..39] MMA "S/dP issued",
+// [40..47] MMA "mm2 issued", [48..55] flush "mm2 seen", [56..63] flush "dq free".
+__device__ unsigned long long* g_attn_bwd_dbg = nullptr;
+
+__device__ __forceinline__ void bmark(bool on, int slot, int g) {
+    if (on && g < 8) g_attn_bwd_dbg[blockIdx.x * 64 + slot * 8 + g] = clock64();
 }
 
-__device__ __forceinline__ void elem_bar(int id) {
-    asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory");
+struct Item {
+    int bh, j, i0, iters;
+};
+
+__device__ __forceinline__ Item item_of(int n, int bhn, int nq, bool causal) {
+    Item it;
+    it.j = n / bhn;
+    it.bh = n % bhn;
+    it.i0 = causal ? it.j : 0;
+    it.iters = nq - it.i0;
+    return it;
 }
 
 template <bool kCausal>
-__global__ void __launch_bounds__(640, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                  const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
-                  float* __restrict__ dq_part, int seq, int heads) {
-    extern __shared__ uint8_t smem_raw[];
+                  const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
+                  const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int heads, int bhn) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = ptx::smem_u32(smem);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + oBar);
-    uint64_t* b_kv = bar + 0;
-    uint64_t* b_qfull = bar + 1;   // [2]
-    uint64_t* b_qempty = bar + 3;  // [2]
-    uint64_t* b_sdp = bar + 5;     // S^T / dP^T of an iteration are in TMEM
-    uint64_t* b_pds = bar + 6;     // 16 arrivals: P^T / dS^T written to SMEM
-    uint64_t* b_mm2 = bar + 7;     // dV / dK / dQ MMAs of an iteration done
-    uint64_t* b_dqfree = bar + 8;  // 16 arrivals: dQ TMEM read out
-    uint64_t* b_sdfree = bar + 9;  // 16 arrivals: S^T / dP^T TMEM read into registers
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kNumBars);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int bh = blockIdx.x, b = bh / heads, hd = bh % heads;
-    const int j = blockIdx.y;                 // key tile
     const int nq = seq / kT;
-    const int i0 = kCausal ? j : 0;
-    const int iters = nq - i0;
+    const int items = bhn * nq;
     const int h = heads * kD;
-    const int row0 = b * seq;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tm_qkv);
         ptx::tma_prefetch_desc(&tm_do);
-        for (int q = 0; q < 10; ++q) ptx::mbar_init(&bar[q], (q == 6 || q == 8 || q == 9) ? 16 : 1);
+        ptx::tma_prefetch_desc(&tm_dq);
+        for (int q = 0; q < kNumBars; ++q) {
+            const uint32_t cnt = (q == bSdpFree || q == bPdsFull) ? 8 : (q == bDqFree || q == bKvAccFree) ? 4 : 1;
+            ptx::mbar_init(&bar[q], cnt);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -109,160 +129,245 @@ __global__ void __launch_bounds__(640, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t tS = 0, tDP = 128, tDV = 256, tDK = 320, tDQ = 384;
 
     if (warp == 0) {
+        // ---------------- TMA producer ----------------
         if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(b_kv, 2 * kTile);
-            ptx::tma_load_2d(smem + oK, &tm_qkv, b_kv, h + hd * kD, row0 + j * kT);
-            ptx::tma_load_2d(smem + oV, &tm_qkv, b_kv, 2 * h + hd * kD, row0 + j * kT);
-            for (int it = 0; it < iters; ++it) {
-                const int buf = it & 1, i = i0 + it;
-                if (it >= 2) ptx::mbar_wait(&b_qempty[buf], ((it - 2) >> 1) & 1);
-                ptx::mbar_arrive_expect_tx(&b_qfull[buf], 2 * kTile + 2 * kT * 4);
-                ptx::tma_load_2d(smem + oQ + buf * kTile, &tm_qkv, &b_qfull[buf], hd * kD, row0 + i * kT);
-                ptx::tma_load_2d(smem + oDO + buf * kTile, &tm_do, &b_qfull[buf], hd * kD, row0 + i * kT);
-                bulk_load(smem + oLse + buf * kT * 4, lse + static_cast<size_t>(bh) * seq + i * kT, kT * 4, &b_qfull[buf]);
-                bulk_load(smem + oDel + buf * kT * 4, delta + static_cast<size_t>(bh) * seq + i * kT, kT * 4,
-                          &b_qfull[buf]);
+            int ln = 0, g = 0;
+            for (int n = blockIdx.x; n < items; n += gridDim.x, ++ln) {
+                const Item it = item_of(n, bhn, nq, kCausal);
+                const int b = it.bh / heads, hd = it.bh % heads, row0 = b * seq;
+                const int kb = ln & 1;
+                ptx::mbar_wait(&bar[bKvEmpty + kb], ((ln >> 1) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&bar[bKvFull + kb], 2 * kTile);
+                ptx::tma_load_2d(smem + oK + kb * kTile, &tm_qkv, &bar[bKvFull + kb], h + hd * kD, row0 + it.j * kT);
+                ptx::tma_load_2d(smem + oV + kb * kTile, &tm_qkv, &bar[bKvFull + kb], 2 * h + hd * kD,
+                                 row0 + it.j * kT);
+                for (int t = 0; t < it.iters; ++t, ++g) {
+                    const int i = it.i0 + t, qb = g % kQS;
+                    ptx::mbar_wait(&bar[bQEmpty + qb], ((g / kQS) & 1) ^ 1);
+                    uint64_t* full = &bar[bQFull + qb];
+                    ptx::mbar_arrive_expect_tx(full, 2 * kTile + 2 * kT * 4);
+                    ptx::tma_load_2d(smem + oQ + qb * kTile, &tm_qkv, full, hd * kD, row0 + i * kT);
+                    ptx::tma_load_2d(smem + oDO + qb * kTile, &tm_do, full, hd * kD, row0 + i * kT);
+                    const size_t so = static_cast<size_t>(it.bh) * seq + i * kT;
+                    bulk_load(sbase + oLse + qb * kT * 4, lse + so, kT * 4, full);
+                    bulk_load(sbase + oDel + qb * kT * 4, delta + so, kT * 4, full);
+                }
             }
         }
     } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            const uint32_t aK = ptx::smem_u32(smem + oK), aV = ptx::smem_u32(smem + oV);
-            const uint32_t aPt = ptx::smem_u32(smem + oPt), aDSt = ptx::smem_u32(smem + oDSt);
-            const uint32_t id_sq = ptx::idesc_bf16(128, 128, false, false);  // S^T, dP^T
-            const uint32_t id_kv = ptx::idesc_bf16(128, 64, false, true);    // dV, dK: B MN-major
-            const uint32_t id_q = ptx::idesc_bf16(128, 64, true, true);      // dQ: A and B MN-major
-            auto issue_sdp = [&](int it) {
-                const int buf = it & 1;
-                const uint32_t aQ = ptx::smem_u32(smem + oQ + buf * kTile);
-                const uint32_t aDO = ptx::smem_u32(smem + oDO + buf * kTile);
-                ptx::mbar_wait(&b_qfull[buf], (it >> 1) & 1);
-                ptx::tc_fence_after();
-#pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk) {
-                    ptx::umma_bf16(tmem + tS, ptx::sdesc_sw128(aK + kk * 32, 16, 1024),
-                                   ptx::sdesc_sw128(aQ + kk * 32, 16, 1024), id_sq, kk > 0);
-                    ptx::umma_bf16(tmem + tDP, ptx::sdesc_sw128(aV + kk * 32, 16, 1024),
-                                   ptx::sdesc_sw128(aDO + kk * 32, 16, 1024), id_sq, kk > 0);
-                }
-                ptx::umma_commit(b_sdp);
+            const uint32_t aDSt = sbase + oDSt;
+            constexpr uint32_t id_sq = ptx::idesc_bf16(128, 128, false, false);  // S^T, dP^T
+            constexpr uint32_t id_kv = ptx::idesc_bf16(128, 64, false, true);    // dV, dK: B MN-major
+            constexpr uint32_t id_q = ptx::idesc_bf16(128, 64, true, true);      // dQ: A and B MN-major
+            struct Pend {
+                int g, ln, kb;
+                bool first, last;
             };
-            ptx::mbar_wait(b_kv, 0);
-            issue_sdp(0);
-            for (int it = 0; it < iters; ++it) {
-                const int buf = it & 1;
-                if (it + 1 < iters) {
-                    // S^T / dP^T of the next query tile overlap this tile's P / dS math
-                    ptx::mbar_wait(b_sdfree, it & 1);
-                    ptx::tc_fence_after();
-                    issue_sdp(it + 1);
-                }
-                const uint32_t aQ = ptx::smem_u32(smem + oQ + buf * kTile);
-                const uint32_t aDO = ptx::smem_u32(smem + oDO + buf * kTile);
-                ptx::mbar_wait(b_pds, it & 1);
-                if (it > 0) ptx::mbar_wait(b_dqfree, (it - 1) & 1);
+            auto issue_mm2 = [&](const Pend& p) {
+                const int qb = p.g % kQS;
+                const uint32_t aQ = sbase + oQ + qb * kTile, aDO = sbase + oDO + qb * kTile;
+                const uint32_t aK = sbase + oK + p.kb * kTile;
+                ptx::mbar_wait(&bar[bPdsFull], p.g & 1);
+                if (p.g > 0) ptx::mbar_wait(&bar[bDqFree], (p.g - 1) & 1);
+                if (p.first && p.ln > 0) ptx::mbar_wait(&bar[bKvAccFree], (p.ln - 1) & 1);
                 ptx::tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < kT / 16; ++kk) {
                     const uint32_t a_off = (kk / 4) * kTile + (kk % 4) * 32;  // K-major, 16 q per step
                     const uint32_t b_off = kk * 2048;                         // MN-major, 16 rows per step
-                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-                    ptx::umma_bf16(tmem + tDV, ptx::sdesc_sw128(aPt + a_off, 16, 1024),
-                                   ptx::sdesc_sw128(aDO + b_off, 8192, 1024), id_kv, acc);
+                    const uint32_t acc = (!p.first || kk > 0) ? 1u : 0u;
+                    ptx::umma_bf16_ts(tmem + tDV, tmem + tPT + kk * 8, ptx::sdesc_sw128(aDO + b_off, 8192, 1024),
+                                      id_kv, acc);
                     ptx::umma_bf16(tmem + tDK, ptx::sdesc_sw128(aDSt + a_off, 16, 1024),
                                    ptx::sdesc_sw128(aQ + b_off, 8192, 1024), id_kv, acc);
                     ptx::umma_bf16(tmem + tDQ, ptx::sdesc_sw128(aDSt + kk * 2048, kTile, 1024),
-                                   ptx::sdesc_sw128(aK + kk * 2048, 8192, 1024), id_q, kk > 0);
+                                   ptx::sdesc_sw128(aK + kk * 2048, 8192, 1024), id_q, kk > 0 ? 1u : 0u);
                 }
-                ptx::umma_commit(b_mm2);
-                ptx::umma_commit(&b_qempty[buf]);
+                ptx::umma_commit(&bar[bMm2]);
+                bmark(g_attn_bwd_dbg != nullptr, 5, p.g);
+                ptx::umma_commit(&bar[bQEmpty + qb]);
+                if (p.last) ptx::umma_commit(&bar[bKvEmpty + p.kb]);
+            };
+            Pend prev{};
+            bool have = false;
+            int ln = 0, g = 0;
+            for (int n = blockIdx.x; n < items; n += gridDim.x, ++ln) {
+                const Item it = item_of(n, bhn, nq, kCausal);
+                const int kb = ln & 1;
+                const uint32_t aK = sbase + oK + kb * kTile, aV = sbase + oV + kb * kTile;
+                ptx::mbar_wait(&bar[bKvFull + kb], (ln >> 1) & 1);
+                for (int t = 0; t < it.iters; ++t, ++g) {
+                    const int qb = g % kQS;
+                    const uint32_t aQ = sbase + oQ + qb * kTile, aDO = sbase + oDO + qb * kTile;
+                    ptx::mbar_wait(&bar[bQFull + qb], (g / kQS) & 1);
+                    if (g > 0) ptx::mbar_wait(&bar[bSdpFree], (g - 1) & 1);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < kD / 16; ++kk) {
+                        ptx::umma_bf16(tmem + tS, ptx::sdesc_sw128(aK + kk * 32, 16, 1024),
+                                       ptx::sdesc_sw128(aQ + kk * 32, 16, 1024), id_sq, kk > 0);
+                        ptx::umma_bf16(tmem + tDP, ptx::sdesc_sw128(aV + kk * 32, 16, 1024),
+                                       ptx::sdesc_sw128(aDO + kk * 32, 16, 1024), id_sq, kk > 0);
+                    }
+                    ptx::umma_commit(&bar[bSdpFull]);
+                    bmark(g_attn_bwd_dbg != nullptr, 4, g);
+                    if (have) issue_mm2(prev);
+                    prev = Pend{g, ln, kb, t == 0, t == it.iters - 1};
+                    have = true;
+                }
             }
+            if (have) issue_mm2(prev);
         }
-    } else if (warp >= 4) {
-        // 16 elementwise warps: 4 threads per key row, thread `sel` owns query columns
-        // [32 sel, 32 sel + 32) of every 128-query tile and 16 of the 64 head dims.
+    } else if (warp >= 4 && warp < 12) {
+        // ---------------- elementwise: P^T, dS^T ----------------
         const int qw = warp & 3;
-        const int sel = (warp - 4) >> 2;
-        const int r = qw * 32 + lane;     // key row (S^T / dP^T / dV / dK) or query row (dQ)
-        const int key = j * kT + r;
+        const int sel = (warp - 4) >> 2;  // query columns [64 sel, 64 sel + 64) = UMMA block sel
+        const int r = qw * 32 + lane;     // key row within the tile
         const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
         const float sc = 0.125f * kLog2e;
-        auto flush_dq = [&](int it) {  // dQ partial of query tile i0 + it: row r, dims 16 sel..+15
-            const int i = i0 + it;
-            float* dst = dq_part + (static_cast<size_t>(j) * (static_cast<size_t>(gridDim.x / heads) * seq) +
-                                    static_cast<size_t>(row0 + i * kT + r)) * h + hd * kD + sel * 16;
-            uint32_t v[16];
-            ptx::tmem_ld_32x32b_x16(trow + tDQ + sel * 16, v);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int q = 0; q < 16; q += 4)
-                *reinterpret_cast<float4*>(dst + q) = make_float4(__uint_as_float(v[q]), __uint_as_float(v[q + 1]),
-                                                                  __uint_as_float(v[q + 2]), __uint_as_float(v[q + 3]));
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(b_dqfree);
-        };
-        for (int it = 0; it < iters; ++it) {
-            const int buf = it & 1, i = i0 + it;
-            ptx::mbar_wait(b_sdp, it & 1);
-            ptx::tc_fence_after();
-            uint32_t s[32], dp[32];
-            ptx::tmem_ld_32x32b_x32(trow + tS + sel * 32, s);
-            ptx::tmem_ld_32x32b_x32(trow + tDP + sel * 32, dp);
-            ptx::tmem_ld_wait();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(b_sdfree);  // the MMA may overwrite S^T / dP^T now
-            ptx::mbar_wait(&b_qfull[buf], (it >> 1) & 1);
-            if (it > 0) {
-                ptx::mbar_wait(b_mm2, (it - 1) & 1);  // P^T / dS^T free, dQ of it-1 ready
+        const uint32_t drow = sbase + oDSt + sel * kTile + r * 128;
+        const bool dbg = g_attn_bwd_dbg != nullptr && warp == 4 && lane == 0;
+        int g = 0;
+        for (int n = blockIdx.x; n < items; n += gridDim.x) {
+            const Item it = item_of(n, bhn, nq, kCausal);
+            const int key = it.j * kT + r;
+            for (int t = 0; t < it.iters; ++t, ++g) {
+                const int i = it.i0 + t, qb = g % kQS;
+                ptx::mbar_wait(&bar[bSdpFull], g & 1);
+                bmark(dbg, 0, g);
+                ptx::mbar_wait(&bar[bQFull + qb], (g / kQS) & 1);  // lse / delta visible
                 ptx::tc_fence_after();
-                flush_dq(it - 1);
-            }
-            const float* sl = reinterpret_cast<const float*>(smem + oLse + buf * kT * 4);
-            const float* sd = reinterpret_cast<const float*>(smem + oDel + buf * kT * 4);
-            const int c = sel * 32;
-            float p[32], ds[32];
+                uint32_t pp[32], dd[32];  // bf16x2: 64 P^T and 64 dS^T values of row r
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                const int qi = i * kT + c + q;  // absolute query index
-                const bool vis = !kCausal || qi >= key;
-                p[q] = vis ? ptx::ex2(fmaf(__uint_as_float(s[q]), sc, -sl[c + q] * kLog2e)) : 0.0f;
-                ds[q] = p[q] * (__uint_as_float(dp[q]) - sd[c + q]);
-            }
-            store_row32(smem + oPt, r, c, p);
-            store_row32(smem + oDSt, r, c, ds);
-            ptx::fence_proxy_async();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(b_pds);
-        }
-        ptx::mbar_wait(b_mm2, (iters - 1) & 1);
-        ptx::tc_fence_after();
-        flush_dq(iters - 1);
-        // dK (x 1/8) and dV for key row r, dims 16 sel..+15
-        bf16* dk = dqkv + static_cast<size_t>(row0 + key) * 3 * h + h + hd * kD + sel * 16;
-        bf16* dv = dk + h;
-        {
-            uint32_t vk[16], vv[16];
-            ptx::tmem_ld_32x32b_x16(trow + tDK + sel * 16, vk);
-            ptx::tmem_ld_32x32b_x16(trow + tDV + sel * 16, vv);
-            ptx::tmem_ld_wait();
+                for (int c = 0; c < 4; ++c) {  // 16 query columns per TMEM load (register budget)
+                    const int col0 = sel * 64 + c * 16;
+                    uint32_t s[16], dp[16];
+                    ptx::tmem_ld_32x32b_x16(trow + tS + col0, s);
+                    ptx::tmem_ld_32x32b_x16(trow + tDP + col0, dp);
+                    ptx::tmem_ld_wait();
+                    const uint32_t la = sbase + oLse + qb * kT * 4 + col0 * 4;
+                    const uint32_t da = sbase + oDel + qb * kT * 4 + col0 * 4;
 #pragma unroll
-            for (int q = 0; q < 16; q += 8) {
-                uint32_t wk[4], wv[4];
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 l4 = ptx::lds_f4(la + q4 * 16);
+                        const float4 d4 = ptx::lds_f4(da + q4 * 16);
+                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+                        float p[4], ds[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    wk[e] = ptx::pack_bf16x2(__uint_as_float(vk[q + 2 * e]) * 0.125f,
-                                             __uint_as_float(vk[q + 2 * e + 1]) * 0.125f);
-                    wv[e] = ptx::pack_bf16x2(__uint_as_float(vv[q + 2 * e]), __uint_as_float(vv[q + 2 * e + 1]));
+                        for (int e = 0; e < 4; ++e) {
+                            const int q = q4 * 4 + e;
+                            float x = ptx::ex2(fmaf(__uint_as_float(s[q]), sc, -lv[e] * kLog2e));
+                            if (kCausal && i * kT + col0 + q < key) x = 0.0f;
+                            p[e] = x;
+                            ds[e] = x * (__uint_as_float(dp[q]) - dv[e]);
+                        }
+                        pp[c * 8 + q4 * 2] = ptx::pack_bf16x2(p[0], p[1]);
+                        pp[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(p[2], p[3]);
+                        dd[c * 8 + q4 * 2] = ptx::pack_bf16x2(ds[0], ds[1]);
+                        dd[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(ds[2], ds[3]);
+                    }
                 }
-                *reinterpret_cast<uint4*>(dk + q) = make_uint4(wk[0], wk[1], wk[2], wk[3]);
-                *reinterpret_cast<uint4*>(dv + q) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bar[bSdpFree]);  // S^T / dP^T may be overwritten
+                bmark(dbg, 1, g);
+                if (g > 0) ptx::mbar_wait(&bar[bMm2], (g - 1) & 1);  // P^T / dS^T buffers free
+                bmark(dbg, 2, g);
+                ptx::tc_fence_after();
+                ptx::tmem_st_32x32b_x32(trow + tPT + sel * 32, pp);  // queries 64 sel .. +63 of key row r
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch) {
+                    const uint32_t off = static_cast<uint32_t>((ch ^ (r & 7)) << 4);
+                    ptx::sts_u4(drow + off, dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]);
+                }
+                ptx::tmem_st_wait();
+                ptx::fence_proxy_async();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bar[bPdsFull]);
+                bmark(dbg, 3, g);
             }
         }
+    } else if (warp >= 12) {
+        // ---------------- dQ flush (TMA reduce-add) + dK / dV epilogue ----------------
+        const int qw = warp & 3;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+        uint8_t* stage = smem + oDQ + qw * 4096;
+        const uint32_t sstage = ptx::smem_u32(stage);
+        const bool fdbg = g_attn_bwd_dbg != nullptr && warp == 12 && lane == 0;
+        int g = 0;
+        for (int n = blockIdx.x; n < items; n += gridDim.x) {
+            const Item it = item_of(n, bhn, nq, kCausal);
+            const int b = it.bh / heads, hd = it.bh % heads, row0 = b * seq;
+            for (int t = 0; t < it.iters; ++t, ++g) {
+                const int i = it.i0 + t;
+                ptx::mbar_wait(&bar[bMm2], g & 1);
+                bmark(fdbg, 6, g);
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(trow + tDQ + half * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (half == 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&bar[bDqFree]);
+                        bmark(fdbg, 7, g);
+                    }
+                    if (lane == 0) ptx::bulk_wait_read<0>();  // staging buffer read out by the last reduce
+                    __syncwarp();
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        ptx::sts_f4(sstage + ptx::swz128(lane, c), __uint_as_float(v[4 * c]),
+                                    __uint_as_float(v[4 * c + 1]), __uint_as_float(v[4 * c + 2]),
+                                    __uint_as_float(v[4 * c + 3]));
+                    ptx::fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_reduce_add_2d(&tm_dq, stage, hd * kD + half * 32, row0 + i * kT + qw * 32);
+                        ptx::bulk_commit();
+                    }
+                }
+                if (t == it.iters - 1) {
+                    // dK (x 1/8) and dV of key row qw*32 + lane of tile j
+                    const int key = it.j * kT + qw * 32 + lane;
+                    bf16* dk = dqkv + static_cast<size_t>(row0 + key) * 3 * h + h + hd * kD;
+                    bf16* dv = dk + h;
+#pragma unroll 1
+                    for (int half = 0; half < 2; ++half) {
+                        uint32_t vk[32], vv[32];
+                        ptx::tmem_ld_32x32b_x32(trow + tDK + half * 32, vk);
+                        ptx::tmem_ld_32x32b_x32(trow + tDV + half * 32, vv);
+                        ptx::tmem_ld_wait();
+                        if (half == 1) {
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(&bar[bKvAccFree]);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 32; q += 8) {
+                            uint32_t wk[4], wv[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                wk[e] = ptx::pack_bf16x2(__uint_as_float(vk[q + 2 * e]) * 0.125f,
+                                                         __uint_as_float(vk[q + 2 * e + 1]) * 0.125f);
+                                wv[e] = ptx::pack_bf16x2(__uint_as_float(vv[q + 2 * e]),
+                                                         __uint_as_float(vv[q + 2 * e + 1]));
+                            }
+                            *reinterpret_cast<uint4*>(dk + half * 32 + q) = make_uint4(wk[0], wk[1], wk[2], wk[3]);
+                            *reinterpret_cast<uint4*>(dv + half * 32 + q) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                        }
+                    }
+                }
+            }
+        }
+        if (lane == 0) ptx::bulk_wait<0>();
+        __syncwarp();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -272,52 +377,51 @@ __global__ void __launch_bounds__(640, 1)
     }
 }
 
-// delta[bh, i] = sum_d dO[t, hd*64+d] * O[t, hd*64+d]; one thread per (token, head).
+// delta[bh, i] = sum_d dO[t, hd*64+d] * O[t, hd*64+d]; also zeroes the fp32 dQ
+// accumulator slice of (t, hd).  Eight threads per (token, head), 16 B each.
 __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ delta,
-                             int tokens, int seq, int heads) {
+                             float* __restrict__ dq_acc, int tokens, int seq, int heads) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= tokens * heads) return;
-    const int t = idx / heads, hd = idx % heads;
+    const int pair = idx >> 3, sub = idx & 7;
+    const bool ok = pair < tokens * heads;  // no early return: the shuffles below need every lane
+    const int t = ok ? pair / heads : 0, hd = ok ? pair % heads : 0;
     const int h = heads * kD;
-    const bf16* po = o + static_cast<size_t>(t) * h + hd * kD;
-    const bf16* pd = dout + static_cast<size_t>(t) * h + hd * kD;
+    const size_t off = static_cast<size_t>(t) * h + hd * kD + sub * 8;
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    const uint4 a = ok ? *reinterpret_cast<const uint4*>(o + off) : z4;
+    const uint4 d = ok ? *reinterpret_cast<const uint4*>(dout + off) : z4;
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, dw[4] = {d.x, d.y, d.z, d.w};
     float acc = 0.0f;
 #pragma unroll
-    for (int c = 0; c < kD; c += 8) {
-        const uint4 a = *reinterpret_cast<const uint4*>(po + c);
-        const uint4 d = *reinterpret_cast<const uint4*>(pd + c);
-        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, dw[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 fa = ptx::unpack_bf16x2(aw[e]), fd = ptx::unpack_bf16x2(dw[e]);
-            acc = fmaf(fa.x, fd.x, fmaf(fa.y, fd.y, acc));
-        }
+    for (int e = 0; e < 4; ++e) {
+        const float2 fa = ptx::unpack_bf16x2(aw[e]), fd = ptx::unpack_bf16x2(dw[e]);
+        acc = fmaf(fa.x, fd.x, fmaf(fa.y, fd.y, acc));
     }
-    const int b = t / seq, i = t % seq;
-    delta[(static_cast<size_t>(b) * heads + hd) * seq + i] = acc;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if (!ok) return;
+    float4* z = reinterpret_cast<float4*>(dq_acc + off);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sub == 0) {
+        const int b = t / seq, i = t % seq;
+        delta[(static_cast<size_t>(b) * heads + hd) * seq + i] = acc;
+    }
 }
 
-// dq (bf16, x 1/8) = sum over key tiles j (<= query tile when causal) of dq_part[j].
-__global__ void k_attn_dq_sum(const float* __restrict__ part, bf16* __restrict__ dqkv, int tokens, int seq, int heads,
-                              int causal) {
-    const int h = heads * kD;
-    const size_t total = static_cast<size_t>(tokens) * h / 4;
+// dq (bf16, x 1/8) = the fp32 accumulator.
+__global__ void k_attn_dq_convert(const float* __restrict__ acc, bf16* __restrict__ dqkv, int tokens, int h) {
+    const size_t total = static_cast<size_t>(tokens) * h / 8;
     for (size_t v = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; v < total;
          v += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t e = v * 4;
+        const size_t e = v * 8;
         const int t = static_cast<int>(e / h), c = static_cast<int>(e % h);
-        const int qt = (t % seq) / kT;
-        const int nj = causal ? qt + 1 : seq / kT;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = 0; j < nj; ++j) {
-            const float4 x = *reinterpret_cast<const float4*>(part + static_cast<size_t>(j) * tokens * h + e);
-            acc.x += x.x;
-            acc.y += x.y;
-            acc.z += x.z;
-            acc.w += x.w;
-        }
-        *reinterpret_cast<uint2*>(dqkv + static_cast<size_t>(t) * 3 * h + c) =
-            make_uint2(ptx::pack_bf16x2(acc.x * 0.125f, acc.y * 0.125f), ptx::pack_bf16x2(acc.z * 0.125f, acc.w * 0.125f));
+        const float4 x = *reinterpret_cast<const float4*>(acc + e);
+        const float4 y = *reinterpret_cast<const float4*>(acc + e + 4);
+        *reinterpret_cast<uint4*>(dqkv + static_cast<size_t>(t) * 3 * h + c) =
+            make_uint4(ptx::pack_bf16x2(x.x * 0.125f, x.y * 0.125f), ptx::pack_bf16x2(x.z * 0.125f, x.w * 0.125f),
+                       ptx::pack_bf16x2(y.x * 0.125f, y.y * 0.125f), ptx::pack_bf16x2(y.z * 0.125f, y.w * 0.125f));
     }
 }
 
@@ -336,28 +440,36 @@ void set_smem_once() {
 
 }  // namespace
 
+void attention_bwd_debug_timing(unsigned long long* dev_buf) {
+    check_cuda(cudaMemcpyToSymbol(g_attn_bwd_dbg, &dev_buf, sizeof(dev_buf)), "cudaMemcpyToSymbol(g_attn_bwd_dbg)");
+}
+
 size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads) {
-    return static_cast<size_t>(seq / kT) * batch * seq * heads * kD;
+    return static_cast<size_t>(batch) * seq * heads * kD;  // the fp32 dQ accumulator
 }
 
 void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
-                      float* dq_part, int batch, int seq, int heads, bool causal, cudaStream_t s) {
+                      float* dq_acc, int batch, int seq, int heads, bool causal, cudaStream_t s) {
     const int h = heads * kD;
     const int tokens = batch * seq;
-    k_attn_delta<<<(tokens * heads + 255) / 256, 256, 0, s>>>(o, dout, delta, tokens, seq, heads);
+    const int pairs = tokens * heads;
+    k_attn_delta<<<(pairs * 8 + 255) / 256, 256, 0, s>>>(o, dout, delta, dq_acc, tokens, seq, heads);
     const CUtensorMap tq = make_tmap_bf16_2d(qkv, 3ull * h, static_cast<uint64_t>(tokens), 3ll * h, 64, kT);
     const CUtensorMap tdo = make_tmap_bf16_2d(dout, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 64, kT);
-    dim3 grid(batch * heads, seq / kT);
+    const CUtensorMap tdq = make_tmap_f32_2d(dq_acc, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 32, 32);
+    const int bhn = batch * heads;
+    const int items = bhn * (seq / kT);
+    const int grid = std::min(items, num_sms());
     if (causal) {
         set_smem_once<true>();
-        k_attn_bwd_tc<true><<<grid, 640, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
+        k_attn_bwd_tc<true><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, lse, delta, dqkv, seq, heads, bhn);
     } else {
         set_smem_once<false>();
-        k_attn_bwd_tc<false><<<grid, 640, kSmem, s>>>(tq, tdo, lse, delta, dqkv, dq_part, seq, heads);
+        k_attn_bwd_tc<false><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, lse, delta, dqkv, seq, heads, bhn);
     }
-    const size_t vecs = static_cast<size_t>(tokens) * h / 4;
-    k_attn_dq_sum<<<static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 32u)), 256, 0, s>>>(
-        dq_part, dqkv, tokens, seq, heads, causal ? 1 : 0);
+    const size_t vecs = static_cast<size_t>(tokens) * h / 8;
+    k_attn_dq_convert<<<static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 16u)), 256, 0, s>>>(
+        dq_acc, dqkv, tokens, h);
     check_cuda(cudaGetLastError(), "attention_bwd_tc");
 }
 

@@ -4,6 +4,7 @@
 #include <memory>
 
 #include "capi_internal.h"
+#include "block_profiler.h"
 #include "engine.h"
 #include "nccl_dl.h"
 #include "p2bw.h"
@@ -26,6 +27,33 @@ void check_stage(p2bw::Engine& e, int stage) {
     if (stage < 0 || stage >= e.depth()) throw std::invalid_argument("stage out of range");
 }
 
+p2bw::EngineConfig config_from_desc(const p2bw_desc& dd) {
+    const p2bw_desc* d = &dd;
+    p2bw::EngineConfig c;
+    c.model_kind = d->model_kind;
+    c.policy = d->policy;
+    c.depth = d->depth;
+    c.microbatches = d->microbatches;
+    c.microbatch_size = d->microbatch_size;
+    c.layers = d->layers;
+    c.dim = d->dim;
+    c.hidden = d->hidden;
+    c.heads = d->heads;
+    c.seq_len = d->seq_len;
+    c.vocab = d->vocab;
+    c.causal = d->causal;
+    c.head_rows = d->head_rows;
+    c.lr = d->learning_rate;
+    c.momentum = d->momentum;
+    c.seed = d->seed;
+    if (d->devices != nullptr) c.devices.assign(d->devices, d->devices + d->depth);
+    c.first_local = d->first_local_stage;
+    c.local_count = d->local_stages;
+    if (c.lr < 0) throw p2bw::Error("learning rate must be >= 0");
+    if (c.momentum < 0 || c.momentum >= 1) throw p2bw::Error("momentum must be in [0, 1)");
+    return c;
+}
+
 }  // namespace
 
 extern "C" {
@@ -36,31 +64,21 @@ int p2bw_engine_create(const p2bw_desc* d, p2bw_engine** out) {
         if (d->width != 1 && d->width != 0)
             throw p2bw::Error("width > 1 runs one replica per process (see DESIGN.md); "
                               "this engine instance drives a single pipeline");
-        p2bw::EngineConfig c;
-        c.model_kind = d->model_kind;
-        c.policy = d->policy;
-        c.depth = d->depth;
-        c.microbatches = d->microbatches;
-        c.microbatch_size = d->microbatch_size;
-        c.layers = d->layers;
-        c.dim = d->dim;
-        c.hidden = d->hidden;
-        c.heads = d->heads;
-        c.seq_len = d->seq_len;
-        c.vocab = d->vocab;
-        c.causal = d->causal;
-        c.head_rows = d->head_rows;
-        c.lr = d->learning_rate;
-        c.momentum = d->momentum;
-        c.seed = d->seed;
-        if (d->devices != nullptr) c.devices.assign(d->devices, d->devices + d->depth);
-        c.first_local = d->first_local_stage;
-        c.local_count = d->local_stages;
-        if (c.lr < 0) throw p2bw::Error("learning rate must be >= 0");
-        if (c.momentum < 0 || c.momentum >= 1) throw p2bw::Error("momentum must be in [0, 1)");
         auto e = std::make_unique<p2bw_engine>();
-        e->impl = std::make_unique<p2bw::Engine>(c);
+        e->impl = std::make_unique<p2bw::Engine>(config_from_desc(*d));
         *out = e.release();
+    });
+}
+
+int p2bw_profile_blocks(const p2bw_desc* d, const int* microbatch_sizes, int n_sizes, int warmup, int iters,
+                        const char* name, char** out_json) {
+    return guarded([&] {
+        if (d == nullptr || microbatch_sizes == nullptr || out_json == nullptr)
+            throw std::invalid_argument("NULL argument");
+        if (n_sizes < 1) throw std::invalid_argument("no microbatch sizes");
+        const std::vector<int> sizes(microbatch_sizes, microbatch_sizes + n_sizes);
+        *out_json = p2bw::dup_string(p2bw::profile_transformer_blocks(config_from_desc(*d), sizes, warmup, iters,
+                                                                      name ? name : "p2bw-transformer"));
     });
 }
 
@@ -226,6 +244,17 @@ int p2bw_engine_connect_stage(p2bw_engine* eng, const void* blob, size_t bytes) 
 
 int p2bw_engine_sync(p2bw_engine* eng) {
     return guarded([&] { eng_of(eng).sync(); });
+}
+
+int p2bw_engine_set_trace(p2bw_engine* eng, int on) {
+    return guarded([&] { eng_of(eng).set_trace(on != 0); });
+}
+
+int p2bw_engine_trace_report(p2bw_engine* eng, char** out_json) {
+    return guarded([&] {
+        if (out_json == nullptr) throw std::invalid_argument("NULL argument");
+        *out_json = p2bw::dup_string(eng_of(eng).trace_report());
+    });
 }
 
 int p2bw_engine_counters(p2bw_engine* eng, p2bw_counters* out) {

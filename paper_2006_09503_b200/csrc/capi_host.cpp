@@ -27,7 +27,7 @@ struct p2bw_schedule {
 
 using p2bw::guarded;
 
-namespace {
+namespace p2bw {
 
 char* dup_string(const std::string& s) {
     char* out = static_cast<char*>(std::malloc(s.size() + 1));
@@ -35,6 +35,12 @@ char* dup_string(const std::string& s) {
     std::memcpy(out, s.c_str(), s.size() + 1);
     return out;
 }
+
+}  // namespace p2bw
+
+using p2bw::dup_string;
+
+namespace {
 
 pipesim::PipelinePolicy as_policy(int p) {
     if (p < P2BW_POLICY_NONE || p > P2BW_POLICY_2BW)

@@ -11,6 +11,9 @@ namespace p2bw {
 
 void set_last_error(const std::string& msg);
 
+// malloc'ed NUL-terminated copy, released by the caller with p2bw_free.
+char* dup_string(const std::string& s);
+
 // Runs fn; maps p2bw::Error / std::exception to P2BW_ERR and records the message
 // for p2bw_last_error() (thread-local, reference wording preserved).
 template <class Fn>

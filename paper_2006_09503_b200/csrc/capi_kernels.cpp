@@ -90,7 +90,10 @@ extern "C" int p2bw_kernel_softmax_xent(void* logits, const void* targets, int r
 }
 
 extern "C" int p2bw_debug_attention_timing(void* dev_buf) {
-    return guarded([&] { attention_debug_timing(static_cast<unsigned long long*>(dev_buf)); });
+    return guarded([&] {
+        attention_debug_timing(static_cast<unsigned long long*>(dev_buf));
+        attention_bwd_debug_timing(static_cast<unsigned long long*>(dev_buf));
+    });
 }
 
 extern "C" int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream) {

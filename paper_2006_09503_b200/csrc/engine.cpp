@@ -20,8 +20,10 @@
 
 #include <algorithm>
 #include <cstring>
+#include <nlohmann/json.hpp>
 
 #include "nccl_dl.h"
+#include "pipesim/schedule.hpp"
 #include "transport.h"
 
 namespace p2bw {
@@ -241,6 +243,8 @@ void Engine::wait_flag(const uint32_t* flag, uint32_t value, cudaStream_t s) {
 }
 
 void Engine::free_buffers() {
+    for (TraceRec& r : trace_) cudaEventDestroy(r.e0), cudaEventDestroy(r.e1);
+    trace_.clear();
     for (Stage& st : stages_) {
         if (!st.local) {
             if (st.block_mapped) cudaIpcCloseMemHandle(st.block);
@@ -502,6 +506,8 @@ void Engine::begin(const std::vector<Program>& programs) {
     }
     sync();
     ev_.reset(new EventTable(stages_.size()));
+    for (TraceRec& r : trace_) cudaEventDestroy(r.e0), cudaEventDestroy(r.e1);
+    trace_.clear();
     progs_ = programs;
     total_ops_ = 0;
     done_ops_ = 0;
@@ -540,6 +546,7 @@ void Engine::issue(int upto_batch) {
             while (st.ptr < prog.size() && st.updates_issued < target) {
                 const OpRec& op = prog[st.ptr];
                 if (!ready(st, op)) break;
+                if (trace_on_) trace_begin(st);
                 switch (op.kind) {
                     case P2BW_OP_FORWARD: issue_forward(st, op); break;
                     case P2BW_OP_BACKWARD: issue_backward(st, op); break;
@@ -560,6 +567,7 @@ void Engine::issue(int upto_batch) {
                         throw Error("op kind " + std::to_string(op.kind) +
                                     " is not executable by the stage executor");
                 }
+                if (trace_on_) trace_end(st, op);
                 st.ptr += 1;
                 done_ops_ += 1;
                 stats_.ops_executed += 1;
@@ -640,6 +648,140 @@ void Engine::read_version(int s, int version, void* host, size_t bytes) {
     DeviceGuard g(st.device);
     st.model->read_weights(it->second, host, bytes, st.stream);
     check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
+}
+
+void Engine::trace_begin(Stage& st) {
+    check_cuda(cudaEventCreate(&trace_open_), "cudaEventCreate(trace)");
+    check_cuda(cudaEventRecord(trace_open_, st.stream), "cudaEventRecord(trace)");
+}
+
+void Engine::trace_end(Stage& st, const OpRec& op) {
+    TraceRec r{};
+    r.stage = st.index;
+    r.kind = op.kind;
+    r.microbatch = op.microbatch;
+    r.version = op.weight_version;
+    r.versions_held = static_cast<int>(st.version_slot.size());
+    r.stashes = static_cast<int>(st.stash_version.size());
+    r.e0 = trace_open_;
+    trace_open_ = nullptr;
+    check_cuda(cudaEventCreate(&r.e1), "cudaEventCreate(trace)");
+    check_cuda(cudaEventRecord(r.e1, st.stream), "cudaEventRecord(trace)");
+    trace_.push_back(r);
+}
+
+namespace {
+
+std::string op_name(int kind) { return pipesim::to_string(static_cast<pipesim::OpKind>(kind)); }
+
+std::string policy_name(int p) { return pipesim::to_string(static_cast<pipesim::PipelinePolicy>(p)); }
+
+}  // namespace
+
+std::string Engine::trace_report() {
+    if (trace_.empty()) throw Error("no traced run: enable tracing before begin()");
+    sync();
+    using json = nlohmann::json;
+    const int d = cfg_.depth;
+    // time base: the begin() event of the first local stage on each device
+    std::map<int, cudaEvent_t> base;
+    for (const Stage& st : stages_)
+        if (st.local && !base.count(st.device)) base[st.device] = st.t0;
+    struct Entry {
+        int worker, kind, mb, ver, versions, stashes;
+        double start, end;
+    };
+    std::vector<Entry> tl;
+    tl.reserve(trace_.size());
+    for (const TraceRec& r : trace_) {
+        const Stage& st = stages_[static_cast<size_t>(r.stage)];
+        DeviceGuard g(st.device);
+        float a = 0.0f, b = 0.0f;
+        check_cuda(cudaEventElapsedTime(&a, base[st.device], r.e0), "cudaEventElapsedTime(trace)");
+        check_cuda(cudaEventElapsedTime(&b, base[st.device], r.e1), "cudaEventElapsedTime(trace)");
+        tl.push_back({r.stage, r.kind, r.microbatch, r.version, r.versions_held, r.stashes, a * 1e-3, b * 1e-3});
+    }
+    // steady state from the batch-boundary updates of the last stage, excluding the
+    // first and last batch (simulator.cpp:298-309)
+    const int per_batch = cfg_.policy == P2BW_POLICY_1F1B ? cfg_.microbatches : 1;
+    std::vector<std::vector<double>> upd(static_cast<size_t>(d));
+    for (const Entry& e : tl)
+        if (e.kind == P2BW_OP_UPDATE) upd[static_cast<size_t>(e.worker)].push_back(e.end);
+    auto batch_update_time = [&](int s, int t) {
+        const auto& u = upd[static_cast<size_t>(s)];
+        const size_t idx = static_cast<size_t>(t) * per_batch - 1;
+        if (idx >= u.size()) throw Error("missing batch updates in program");
+        return u[idx];
+    };
+    int last = d - 1;
+    while (last >= 0 && !stages_[static_cast<size_t>(last)].local) --last;
+    const int num_batches = static_cast<int>(upd[static_cast<size_t>(last)].size()) / per_batch;
+    int replicas = 1;
+    for (const Stage& st : stages_)
+        if (st.local) replicas = std::max(replicas, st.replicas);
+    const double global_batch = static_cast<double>(cfg_.microbatch_size) * cfg_.microbatches * replicas;
+    double steady = 0.0, throughput = 0.0, bubble = 0.0;
+    if (num_batches >= 3) {
+        steady = (batch_update_time(last, num_batches - 1) - batch_update_time(last, 1)) / (num_batches - 2);
+        throughput = steady > 0 ? global_batch / steady : 0.0;
+        double window = 0.0, busy = 0.0;  // simulator.cpp:311-329
+        for (int s = 0; s < d; ++s) {
+            if (!stages_[static_cast<size_t>(s)].local) continue;
+            const double w0 = batch_update_time(s, 1), w1 = batch_update_time(s, num_batches - 1);
+            window += w1 - w0;
+            for (const Entry& e : tl) {
+                if (e.worker != s) continue;
+                if (e.kind != P2BW_OP_FORWARD && e.kind != P2BW_OP_BACKWARD && e.kind != P2BW_OP_RECOMPUTE) continue;
+                const double lo = std::max(e.start, w0), hi = std::min(e.end, w1);
+                if (hi > lo) busy += hi - lo;
+            }
+        }
+        bubble = window > 0.0 ? 1.0 - busy / window : 0.0;
+    }
+    std::stable_sort(tl.begin(), tl.end(), [](const Entry& a, const Entry& b) {
+        if (a.worker != b.worker) return a.worker < b.worker;
+        return a.start < b.start;
+    });
+    json doc;
+    doc["policy"] = policy_name(cfg_.policy);
+    doc["config"] = {{"width", replicas},
+                     {"depth", d},
+                     {"microbatch_size", cfg_.microbatch_size},
+                     {"recompute", false},
+                     {"grad_accum", std::max(cfg_.microbatches / d, 1)}};
+    doc["num_batches"] = num_batches;
+    doc["throughput"] = throughput;
+    doc["bubble_fraction"] = bubble;
+    doc["steady_batch_time"] = steady;
+    doc["measured"] = true;
+    doc["timeline"] = json::array();
+    for (const Entry& e : tl) {
+        const bool comm = e.kind == P2BW_OP_ALLREDUCE || (e.kind >= P2BW_OP_ACT_SEND && e.kind <= P2BW_OP_GRAD_RECV);
+        doc["timeline"].push_back({{"worker", e.worker},
+                                   {"lane", comm ? "comm" : "compute"},
+                                   {"op", op_name(e.kind)},
+                                   {"mb", e.mb},
+                                   {"ver", e.ver},
+                                   {"start", e.start},
+                                   {"end", e.end}});
+    }
+    doc["memory"] = json::array();
+    for (int s = 0; s < d; ++s) {
+        json jt = json::array();
+        const Stage& st = stages_[static_cast<size_t>(s)];
+        if (st.local) {
+            const double vb = st.model->version_bytes(), sb = st.model->stash_bytes();
+            for (const Entry& e : tl) {
+                if (e.worker != s) continue;
+                jt.push_back({{"time", e.end},
+                              {"versions", e.versions},
+                              {"stashes", e.stashes},
+                              {"bytes", e.versions * vb + e.stashes * sb}});
+            }
+        }
+        doc["memory"].push_back(std::move(jt));
+    }
+    return doc.dump(2);
 }
 
 }  // namespace p2bw

@@ -98,6 +98,9 @@ public:
         (void)host, (void)first_mb, (void)count, (void)s;
         throw Error("this stage computes no fp32 loss");
     }
+    // Bytes one weight version / one stash slot occupies (memory trace of a measured run).
+    virtual double version_bytes() const { return static_cast<double>(weight_bytes_public()); }
+    virtual double stash_bytes() const { return 0.0; }
     // fp32 master weights (models that keep one), public layout.
     virtual void read_master(void* host, size_t bytes) {
         (void)host, (void)bytes;
@@ -163,6 +166,13 @@ public:
         st.model->copy_losses_async(host, first_mb, count, st.stream);
     }
     bool is_local(int s) const { return s >= 0 && s < cfg_.depth && stages_[static_cast<size_t>(s)].local; }
+    // Measured timeline: with tracing on, every issued op of a
+    // local stage is bracketed by CUDA events; trace_report() renders the last run
+    // as the reference's SimReport document (simulator.cpp:356-390) with
+    // throughput, steady batch time and bubble fraction computed exactly as
+    // simulate() does (simulator.cpp:298-329), from measured times.
+    void set_trace(bool on) { trace_on_ = on; }
+    std::string trace_report();
     // CUDA IPC hand-off between processes (one process per stage group).
     StageBlob export_stage(int s);
     void connect_stage(const StageBlob& blob);
@@ -207,6 +217,14 @@ private:
         cudaEvent_t t0 = nullptr, t1 = nullptr;
     };
 
+    struct TraceRec {
+        int stage, kind, microbatch, version;
+        int versions_held, stashes;  // after the op (host bookkeeping)
+        cudaEvent_t e0, e1;
+    };
+    void trace_begin(Stage& st);
+    void trace_end(Stage& st, const OpRec& op);
+
     void issue_forward(Stage& st, const OpRec& op);
     void issue_backward(Stage& st, const OpRec& op);
     void issue_update(Stage& st);
@@ -230,6 +248,9 @@ private:
     std::unique_ptr<struct EventTable, EventTableDeleter> ev_;
     RunStats stats_;
     bool snapshots_on_ = false;
+    bool trace_on_ = false;
+    std::vector<TraceRec> trace_;
+    cudaEvent_t trace_open_ = nullptr;  // e0 of the op being issued
     long long mb_base_ = 0;  // microbatches of earlier runs (flag sequence numbers)
     int run_max_mb_ = 0;
 };

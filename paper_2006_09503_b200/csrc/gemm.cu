@@ -46,7 +46,7 @@ struct GemmCfg {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kBBytes = (BN / kCl) * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kTmemCols = 2 * BN;  // 256 or 512: a power of two
+    static constexpr int kTmemCols = BN == 128 ? 256 : 512;  // 2 x BN accumulator columns, a power of two
     static constexpr int kEpiBytes = 4 * 2 * kEpiBuf;  // 4 epilogue warps x 2 buffers
     static constexpr int kFixed = kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int kStages0 = (227 * 1024 - kFixed) / kStageBytes;
@@ -82,29 +82,8 @@ struct EpiMaps {
     CUtensorMap aux;  // residual (StoreBF16) or u (DGeluBF16), bf16
 };
 
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(ptx::smem_u32(src))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
-    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(ptx::smem_u32(src))
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-
 // Byte offset of 16-byte chunk j of row r in a 128 B-row SW128 staging buffer.
-__device__ __forceinline__ int swz(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+
 
 // kCl == 2: a CTA pair (cluster of 2) computes one 256 x BN tile with cta_group::2
 // MMAs issued by the even CTA: each CTA TMA-loads its own 128 A rows and half of the
@@ -117,6 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ EpiMaps em, const KParams p) {
     using Cfg = GemmCfg<BN, kCl>;
     constexpr int S = Cfg::kStages;
+    static_assert(!(kBMN && kCl == 2 && (BN / 2) % 64 != 0), "MN-major B halves must be whole 64-column atoms");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -310,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* buf = ebuf + slot * kEpiBuf;
                 // the buffer's previous bulk store must have finished reading it
                 if (lane == 0) {
-                    if (two_out) bulk_wait_read<0>();
-                    else bulk_wait_read<1>();
+                    if (two_out) ptx::bulk_wait_read<0>();
+                    else ptx::bulk_wait_read<1>();
                 }
                 __syncwarp();
                 if (need_aux) {
@@ -337,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (kF32) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        *reinterpret_cast<float4*>(buf + swz(lane, j)) =
+                        *reinterpret_cast<float4*>(buf + ptx::swz128(lane, j)) =
                             make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
                 } else {
                     if (need_aux) ptx::mbar_wait(&aux_bar[q], aux_phase), aux_phase ^= 1;
@@ -357,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (kKind == EpiKind::DGeluBF16) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const uint4 uu = *reinterpret_cast<const uint4*>(buf + swz(lane, j));
+                            const uint4 uu = *reinterpret_cast<const uint4*>(buf + ptx::swz128(lane, j));
                             const uint32_t uw[4] = {uu.x, uu.y, uu.z, uu.w};
 #pragma unroll
                             for (int t = 0; t < 4; ++t) {
@@ -381,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     x[8 * j + 2 * t] = r.x;
                                     x[8 * j + 2 * t + 1] = r.y;
                                 }
-                                *reinterpret_cast<uint4*>(pbuf + swz(lane, j)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                                *reinterpret_cast<uint4*>(pbuf + ptx::swz128(lane, j)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
                             }
                         }
                         if (e.gelu) {
@@ -391,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (need_aux) {
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const uint4 rr = *reinterpret_cast<const uint4*>(buf + swz(lane, j));
+                                const uint4 rr = *reinterpret_cast<const uint4*>(buf + ptx::swz128(lane, j));
                                 const uint32_t rw[4] = {rr.x, rr.y, rr.z, rr.w};
 #pragma unroll
                                 for (int t = 0; t < 4; ++t) {
@@ -404,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        *reinterpret_cast<uint4*>(buf + swz(lane, j)) =
+                        *reinterpret_cast<uint4*>(buf + ptx::swz128(lane, j)) =
                             make_uint4(ptx::pack_bf16x2(x[8 * j], x[8 * j + 1]),
                                        ptx::pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
                                        ptx::pack_bf16x2(x[8 * j + 4], x[8 * j + 5]),
@@ -413,10 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) {
-                    if (reduce) tma_reduce_add_2d(&em.d, buf, col0, r0);
-                    else tma_store_2d(&em.d, buf, col0, r0);
-                    if (two_out) tma_store_2d(&em.pre, ebuf + (slot ^ 1) * kEpiBuf, col0, r0);
-                    bulk_commit();
+                    if (reduce) ptx::tma_reduce_add_2d(&em.d, buf, col0, r0);
+                    else ptx::tma_store_2d(&em.d, buf, col0, r0);
+                    if (two_out) ptx::tma_store_2d(&em.pre, ebuf + (slot ^ 1) * kEpiBuf, col0, r0);
+                    ptx::bulk_commit();
                 }
                 if (!two_out) slot ^= 1;
             }
@@ -431,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
-        if (lane == 0) bulk_wait_read<0>();
+        if (lane == 0) ptx::bulk_wait_read<0>();
         __syncwarp();
     }
     ptx::tc_fence_before();
@@ -531,10 +511,17 @@ void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& e
 template <int BN, int kCl>
 void dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em,
                     const KParams& p, cudaStream_t s) {
-    if (!amn && !bmn) dispatch_epi<BN, false, false, kCl>(ta, tb, em, p, s);
-    else if (!amn && bmn) dispatch_epi<BN, false, true, kCl>(ta, tb, em, p, s);
-    else if (amn && !bmn) dispatch_epi<BN, true, false, kCl>(ta, tb, em, p, s);
-    else dispatch_epi<BN, true, true, kCl>(ta, tb, em, p, s);
+    if (!amn && !bmn) {
+        dispatch_epi<BN, false, false, kCl>(ta, tb, em, p, s);
+    } else if (amn && !bmn) {
+        dispatch_epi<BN, true, false, kCl>(ta, tb, em, p, s);
+    } else if constexpr (kCl == 2 && (BN / 2) % 64 != 0) {
+        throw Error("gemm: no CTA-pair tile with MN-major B for this BN");
+    } else if (!amn) {
+        dispatch_epi<BN, false, true, kCl>(ta, tb, em, p, s);
+    } else {
+        dispatch_epi<BN, true, true, kCl>(ta, tb, em, p, s);
+    }
 }
 
 struct TileChoice {
@@ -542,24 +529,26 @@ struct TileChoice {
     int cl;
 };
 
-// Tile shape and cluster size minimising a two-resource cost model: per k-block a
-// tile needs max(MMA cycles = 2 BN, L2->SM cycles = bytes / ~45 B/clk), where a
-// 2-CTA cluster halves the B bytes; whole waves of SM (pairs) are paid for.
-TileChoice choose_tile(int m, int n, int k) {
+// Tile shape and cluster size, from the B200 sweeps (scripts/gemm_sweep.py,
+// profiles/r1_gemm_sweep_*.json).  With L2->SMEM feed the binding resource, 128 x 256
+// tiles beat 128 x 128 everywhere; the CTA-pair 256 x 256 tile (half of B per CTA)
+// wins 5-10% once N.K is large.  Outputs whose width is a multiple of 192 but not of
+// 256 (N = 768: every dgrad and the proj / fc2 forwards of a hidden-768 model) waste
+// a third of the last wave with 256-wide tiles; 128 x 192 single-CTA tiles recover
+// 3-13% there.  fp32 (wgrad, split-K) outputs keep the 256-wide tiles.
+TileChoice choose_tile(int m, int n, int k, bool f32_out) {
     if (const char* env = std::getenv("P2BW_GEMM_TILE")) {  // tuning knob: "bn,cl"
         int bn = 0, cl = 0;
-        if (std::sscanf(env, "%d,%d", &bn, &cl) == 2 && (bn == 128 || bn == 256) && (cl == 1 || cl == 2))
+        if (std::sscanf(env, "%d,%d", &bn, &cl) == 2 && (bn == 128 || bn == 192 || bn == 256) && (cl == 1 || cl == 2))
             return {bn, cl};
     }
-    // Measured on B200 (scripts/gemm_sweep.py, profiles/gemm_sweep_r1.json): 128 x 256
-    // tiles beat 128 x 128 on every stage shape, including N = 768 where they leave a
-    // partial wave.  The CTA-pair 256 x 256 tile (half of B per CTA: 6 stages instead
-    // of 4) wins 5-10% once N.K is large (fc1/fc2, all wgrads) and loses a few % on the
-    // short N = K = 768 GEMMs, where the deeper ring never fills.
     if (n < 256) return {128, 1};
+    if (!f32_out && n % 256 != 0 && n % 192 == 0) return {192, 1};
     const bool pair = m > kBM && static_cast<double>(n) * k >= 1.5e6;
     return {256, pair ? 2 : 1};
 }
+
+bool tile_ok(int bn, int cl, bool bmn) { return !(bmn && cl == 2 && (bn / 2) % 64 != 0); }
 
 }  // namespace
 
@@ -567,6 +556,12 @@ CUtensorMap make_tmap_bf16_2d(const bf16* ptr, uint64_t inner, uint64_t outer, i
                               uint32_t box_inner, uint32_t box_outer) {
     if (box_inner != 64) throw Error("tensor maps here use a 64-element (128 B) swizzled inner box");
     return make_map(ptr, inner, outer, ld_elems, box_outer);
+}
+
+CUtensorMap make_tmap_f32_2d(const float* ptr, uint64_t inner, uint64_t outer, int64_t ld_elems, uint32_t box_inner,
+                             uint32_t box_outer) {
+    if (box_inner != 32) throw Error("fp32 tensor maps here use a 32-element (128 B) swizzled inner box");
+    return make_map_t(ptr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, inner, outer, ld_elems, box_inner, box_outer);
 }
 
 void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
@@ -578,9 +573,10 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         throw Error("gemm: fp32 epilogue supports beta 0 (store) or 1 (TMA reduce-add) only");
     if ((epi.ldd % 8) != 0 || (epi.residual && epi.ldr % 8 != 0))
         throw Error("gemm: output leading dims must be multiples of 8");
-    const TileChoice tc = choose_tile(m, n, k);
-    const int bn = tc.bn, cl = tc.cl;
     const bool amn = a.major == Major::MN, bmn = b.major == Major::MN;
+    TileChoice tc = choose_tile(m, n, k, epi.kind == EpiKind::StoreF32);
+    if (!tile_ok(tc.bn, tc.cl, bmn)) tc.cl = 1;
+    const int bn = tc.bn, cl = tc.cl;
     // A: rows = m (tile kBM), B: rows = n (tile bn; each CTA of a pair loads bn / 2).
     // K-major maps put k innermost.
     const CUtensorMap ta = amn ? make_map(a.ptr, m, k, a.ld, kBK) : make_map(a.ptr, k, m, a.ld, kBM);
@@ -630,6 +626,8 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
                       stream);
     if (bn == 256 && cl == 2) dispatch_major<256, 2>(amn, bmn, ta, tb, em, p, stream);
     else if (bn == 256) dispatch_major<256, 1>(amn, bmn, ta, tb, em, p, stream);
+    else if (bn == 192 && cl == 2) dispatch_major<192, 2>(amn, bmn, ta, tb, em, p, stream);
+    else if (bn == 192) dispatch_major<192, 1>(amn, bmn, ta, tb, em, p, stream);
     else if (cl == 2) dispatch_major<128, 2>(amn, bmn, ta, tb, em, p, stream);
     else dispatch_major<128, 1>(amn, bmn, ta, tb, em, p, stream);
 }

@@ -132,6 +132,7 @@ public:
         *dtype = 1;
     }
     size_t boundary_bytes() const override { return act_ * sizeof(double); }
+    double stash_bytes() const override { return static_cast<double>(layers_) * act_ * sizeof(double); }
     size_t weight_bytes_public() const override { return layers_ * mat_ * sizeof(double); }
     int data_capacity() const override { return capacity_; }
 

@@ -80,6 +80,8 @@ public:
     size_t num_params() const override { return nparam_; }
     size_t boundary_bytes() const override { return static_cast<size_t>(T_) * h_ * sizeof(bf16); }
     size_t weight_bytes_public() const override { return nparam_ * sizeof(float); }
+    double version_bytes() const override { return static_cast<double>(nparam_) * sizeof(bf16); }
+    double stash_bytes() const override { return stash_bytes_; }
     int data_capacity() const override { return capacity_; }
     void bind_stream(cudaStream_t s) override { stream_ = s; }
     void grad_buffer(void** ptr, size_t* count, int* dtype) override {
@@ -346,6 +348,8 @@ private:
         for (bf16* w : wbf_) check_cuda(cudaMemset(w, 0, nparam_ * sizeof(bf16)), "memset");
         slots_.resize(static_cast<size_t>(sslots_));
         const size_t stat = static_cast<size_t>(b_) * heads_ * seq_;
+        const double tbytes = static_cast<double>(T) * h * sizeof(bf16);
+        stash_bytes_ = layers_ * (16.0 * tbytes + 16.0 * T + 4.0 * stat) + (last_ ? 2.0 * tbytes : 0.0);
         for (Slot& st : slots_) {
             for (int l = 0; l < layers_; ++l) {
                 st.x.push_back(l == 0 && !first_ ? nullptr : dalloc<bf16>(T * h));
@@ -470,6 +474,7 @@ private:
     float* red_scratch_ = nullptr;
     float* row_loss_ = nullptr;
     int* head_idx_ = nullptr;
+    double stash_bytes_ = 0.0;
     int capacity_ = 0;
     int* ids_ = nullptr;
     int* tgt_ = nullptr;

@@ -50,6 +50,8 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int
 bool attention_tc_supported(int seq);
 // Debug: per-CTA phase timestamps of the tcgen05 forward into dev_buf[cta * 16 + slot] (null: off).
 void attention_debug_timing(unsigned long long* dev_buf);
+// Debug: phase timestamps of the tcgen05 attention backward (64 per CTA, null: off).
+void attention_bwd_debug_timing(unsigned long long* dev_buf);
 void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
                       cudaStream_t s);
 size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads);

@@ -210,6 +210,21 @@ class Desc(C.Structure):
 STAGE_BLOB_BYTES = 128  # P2BW_STAGE_BLOB_BYTES
 
 
+def profile_blocks(*, layers: int, hidden: int, heads: int, seq_len: int, vocab: int, causal: int = 0,
+                   head_rows: int = 0, microbatch_sizes=(1, 2, 4, 8), warmup: int = 2, iters: int = 5,
+                   name: str = "p2bw-transformer", seed: int = 1) -> str:
+    """B200 block profiler (p2bw_profile_blocks): the transformer's per-block fwd / bwd
+    times, weight and activation bytes measured on the current GPU, as the reference's
+    profile document (profile.cpp:162-193) -- the input of plan() / partition_equal()."""
+    d = Desc(MODEL_TRANSFORMER, int(PipelinePolicy.TwoBW), 1, 1, 1, 1, layers, 0, hidden, heads, seq_len,
+             vocab, causal, head_rows, 0.0, 0.0, seed, None, 0, 0)
+    sizes = (C.c_int * len(microbatch_sizes))(*microbatch_sizes)
+    p = C.c_void_p()
+    _call("p2bw_profile_blocks", C.byref(d), sizes, len(microbatch_sizes), warmup, iters, name.encode(),
+          C.byref(p))
+    return _take_string(p)
+
+
 class Counters(C.Structure):
     _fields_ = [("version_consistent", C.c_int), ("max_versions_held", C.c_int),
                 ("ops_executed", C.c_longlong), ("last_run_ms", C.c_double)]
@@ -293,6 +308,16 @@ class Engine:
 
     def sync(self):
         _call("p2bw_engine_sync", self.h)
+
+    def set_trace(self, on: bool = True):
+        """Bracket every issued op with CUDA events (takes effect at the next begin / run)."""
+        _call("p2bw_engine_set_trace", self.h, int(on))
+
+    def trace_report(self) -> dict:
+        """The last traced run as the reference's SimReport document (measured times)."""
+        p = C.c_void_p()
+        _call("p2bw_engine_trace_report", self.h, C.byref(p))
+        return json.loads(_take_string(p))
 
     def is_local(self, stage: int) -> bool:
         out = C.c_int()

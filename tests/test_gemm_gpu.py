@@ -111,3 +111,35 @@ def test_gemm_wgrad_split_k(m, n, k, beta):
     torch.cuda.synchronize()
     ref = beta * d0 + A.float() @ B.float().t()
     assert (d - ref).abs().max().item() < 2e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("tile", ["128,1", "128,2", "192,1", "192,2", "256,1", "256,2"])
+@pytest.mark.parametrize("am,bm,kind", [(0, 0, 0), (0, 1, 0), (1, 1, 1), (0, 1, 2)])
+def test_gemm_every_tile(monkeypatch, tile, am, bm, kind):
+    """Every (BN, cluster) tile the shape-based chooser may pick, on a ragged shape,
+    for the forward (bf16 + bias), dgrad (bf16 / dGELU) and wgrad (fp32) layouts.
+    Pair tiles whose B half is not whole 64-column atoms fall back to one CTA."""
+    monkeypatch.setenv("P2BW_GEMM_TILE", tile)
+    m, n, k = 1000, 768, 704
+    gen = torch.Generator(device="cuda").manual_seed(17 + am + 2 * bm + 4 * kind)
+    A, a, lda = _operand(m, k, am, gen)
+    B, b, ldb = _operand(n, k, bm, gen)
+    ref = A.float() @ B.float().t()
+    if kind == 1:
+        d = torch.zeros(m, n, device="cuda")
+        epi = GemmEpilogue(kind=1, d=d.data_ptr(), ldd=n, alpha=1.0, beta=0.0)
+    elif kind == 2:
+        u = torch.randn(m, n, device="cuda", generator=gen).to(torch.bfloat16)
+        d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        epi = GemmEpilogue(kind=2, d=d.data_ptr(), ldd=n, aux=u.data_ptr(), alpha=1.0)
+        uf = u.float().requires_grad_(True)
+        ref = ref * torch.autograd.grad(gelu_tanh(uf).sum(), uf)[0]
+    else:
+        bias = torch.randn(n, device="cuda", generator=gen).to(torch.bfloat16)
+        d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        epi = GemmEpilogue(kind=0, d=d.data_ptr(), ldd=n, bias=bias.data_ptr(), alpha=1.0)
+        ref = ref + bias.float()
+    _gemm(a, lda, am, b, ldb, bm, m, n, k, epi)
+    torch.cuda.synchronize()
+    tol = 1e-3 if kind == 1 else 0.02
+    assert (d.float() - ref).abs().max().item() <= tol * ref.abs().max().item()

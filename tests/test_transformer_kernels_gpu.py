@@ -34,7 +34,10 @@ def ref_attention(qkv, b, s, nh, causal):
 
 
 @pytest.mark.parametrize("b,s,nh,causal", [(2, 128, 2, True), (2, 128, 2, False), (1, 512, 4, True),
-                                           (3, 512, 2, False), (2, 96, 3, True)])
+                                           (3, 512, 2, False), (2, 96, 3, True),
+                                           # more work items than SMs: the persistent backward's
+                                           # cross-item pipeline (K/V ring, dK/dV hand-off)
+                                           (16, 512, 12, False), (8, 384, 12, True)])
 def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
     h = nh * 64
     g = torch.Generator(device="cuda").manual_seed(b * 1000 + s + nh)
