@@ -62,9 +62,11 @@ constexpr int kThreads = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
 // barrier indices
+// S^T and dP^T are released separately (bSFree / bDpFree) as soon as the elementwise
+// warps have them in registers, so the next tile's S^T / dP^T MMAs overlap the exp work.
 constexpr int bKvFull = 0, bKvEmpty = 2, bQFull = 4, bQEmpty = 4 + kQS, bSdpFull = 4 + 2 * kQS,
-              bSdpFree = bSdpFull + 1, bPdsFull = bSdpFull + 2, bMm2 = bSdpFull + 3, bDqFree = bSdpFull + 4,
-              bKvAccFree = bSdpFull + 5, kNumBars = bSdpFull + 6;
+              bSFree = bSdpFull + 1, bPdsFull = bSdpFull + 2, bMm2 = bSdpFull + 3, bDqFree = bSdpFull + 4,
+              bKvAccFree = bSdpFull + 5, bDpFree = bSdpFull + 6, kNumBars = bSdpFull + 7;
 // P^T lives in TMEM as bf16 (two per 32-bit column) and feeds dV = P^T dO as the
 // tcgen05 A operand straight from TMEM.
 constexpr uint32_t tS = 0, tDP = 128, tDV = 256, tDK = 320, tDQ = 384, tPT = 448;
@@ -101,7 +103,7 @@ __device__ __forceinline__ Item item_of(int n, int bhn, int nq, bool causal) {
 template <bool kCausal>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                  const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
+                  const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ nl2,
                   const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int heads, int bhn) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -119,7 +121,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&tm_do);
         ptx::tma_prefetch_desc(&tm_dq);
         for (int q = 0; q < kNumBars; ++q) {
-            const uint32_t cnt = (q == bSdpFree || q == bPdsFull) ? 8 : (q == bDqFree || q == bKvAccFree) ? 4 : 1;
+            const uint32_t cnt =
+                (q == bSFree || q == bDpFree || q == bPdsFull) ? 8 : (q == bDqFree || q == bKvAccFree) ? 4 : 1;
             ptx::mbar_init(&bar[q], cnt);
         }
         ptx::fence_mbar_init();
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tma_load_2d(smem + oQ + qb * kTile, &tm_qkv, full, hd * kD, row0 + i * kT);
                     ptx::tma_load_2d(smem + oDO + qb * kTile, &tm_do, full, hd * kD, row0 + i * kT);
                     const size_t so = static_cast<size_t>(it.bh) * seq + i * kT;
-                    bulk_load(sbase + oLse + qb * kT * 4, lse + so, kT * 4, full);
+                    bulk_load(sbase + oLse + qb * kT * 4, nl2 + so, kT * 4, full);
                     bulk_load(sbase + oDel + qb * kT * 4, delta + so, kT * 4, full);
                 }
             }
@@ -204,15 +207,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int qb = g % kQS;
                     const uint32_t aQ = sbase + oQ + qb * kTile, aDO = sbase + oDO + qb * kTile;
                     ptx::mbar_wait(&bar[bQFull + qb], (g / kQS) & 1);
-                    if (g > 0) ptx::mbar_wait(&bar[bSdpFree], (g - 1) & 1);
+                    if (g > 0) ptx::mbar_wait(&bar[bSFree], (g - 1) & 1);
                     ptx::tc_fence_after();
 #pragma unroll
-                    for (int kk = 0; kk < kD / 16; ++kk) {
+                    for (int kk = 0; kk < kD / 16; ++kk)
                         ptx::umma_bf16(tmem + tS, ptx::sdesc_sw128(aK + kk * 32, 16, 1024),
                                        ptx::sdesc_sw128(aQ + kk * 32, 16, 1024), id_sq, kk > 0);
+                    if (g > 0) ptx::mbar_wait(&bar[bDpFree], (g - 1) & 1);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < kD / 16; ++kk)
                         ptx::umma_bf16(tmem + tDP, ptx::sdesc_sw128(aV + kk * 32, 16, 1024),
                                        ptx::sdesc_sw128(aDO + kk * 32, 16, 1024), id_sq, kk > 0);
-                    }
                     ptx::umma_commit(&bar[bSdpFull]);
                     bmark(g_attn_bwd_dbg != nullptr, 4, g);
                     if (have) issue_mm2(prev);
@@ -245,25 +251,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {  // 16 query columns per TMEM load (register budget)
                     const int col0 = sel * 64 + c * 16;
-                    uint32_t s[16], dp[16];
-                    ptx::tmem_ld_32x32b_x16(trow + tS + col0, s);
-                    ptx::tmem_ld_32x32b_x16(trow + tDP + col0, dp);
+                    uint32_t sv[16], dv[16];
+                    ptx::tmem_ld_32x32b_x16(trow + tS + col0, sv);
+                    ptx::tmem_ld_32x32b_x16(trow + tDP + col0, dv);
                     ptx::tmem_ld_wait();
-                    const uint32_t la = sbase + oLse + qb * kT * 4 + col0 * 4;
+                    const uint32_t la = sbase + oLse + qb * kT * 4 + col0 * 4;  // -lse log2(e)
                     const uint32_t da = sbase + oDel + qb * kT * 4 + col0 * 4;
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
                         const float4 l4 = ptx::lds_f4(la + q4 * 16);
                         const float4 d4 = ptx::lds_f4(da + q4 * 16);
-                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
                         float p[4], ds[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int q = q4 * 4 + e;
-                            float x = ptx::ex2(fmaf(__uint_as_float(s[q]), sc, -lv[e] * kLog2e));
+                            float x = ptx::ex2(fmaf(__uint_as_float(sv[q]), sc, lv[e]));
                             if (kCausal && i * kT + col0 + q < key) x = 0.0f;
                             p[e] = x;
-                            ds[e] = x * (__uint_as_float(dp[q]) - dv[e]);
+                            ds[e] = x * (__uint_as_float(dv[q]) - dl[e]);
                         }
                         pp[c * 8 + q4 * 2] = ptx::pack_bf16x2(p[0], p[1]);
                         pp[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(p[2], p[3]);
@@ -273,7 +279,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&bar[bSdpFree]);  // S^T / dP^T may be overwritten
+                if (lane == 0) {  // S^T / dP^T may be overwritten by the next tile's MMAs
+                    ptx::mbar_arrive(&bar[bSFree]);
+                    ptx::mbar_arrive(&bar[bDpFree]);
+                }
                 bmark(dbg, 1, g);
                 if (g > 0) ptx::mbar_wait(&bar[bMm2], (g - 1) & 1);  // P^T / dS^T buffers free
                 bmark(dbg, 2, g);
@@ -377,10 +386,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// delta[bh, i] = sum_d dO[t, hd*64+d] * O[t, hd*64+d]; also zeroes the fp32 dQ
-// accumulator slice of (t, hd).  Eight threads per (token, head), 16 B each.
-__global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ delta,
-                             float* __restrict__ dq_acc, int tokens, int seq, int heads) {
+// delta[bh, i] = sum_d dO[t, hd*64+d] * O[t, hd*64+d] and nl2 = -lse log2(e); also
+// zeroes the fp32 dQ accumulator slice of (t, hd).  Eight threads per (token, head).
+__global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
+                             float* __restrict__ delta, float* __restrict__ nl2, float* __restrict__ dq_acc, int tokens,
+                             int seq, int heads) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     const int pair = idx >> 3, sub = idx & 7;
     const bool ok = pair < tokens * heads;  // no early return: the shuffles below need every lane
@@ -406,7 +416,9 @@ __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict_
     z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sub == 0) {
         const int b = t / seq, i = t % seq;
-        delta[(static_cast<size_t>(b) * heads + hd) * seq + i] = acc;
+        const size_t si = (static_cast<size_t>(b) * heads + hd) * seq + i;
+        delta[si] = acc;
+        nl2[si] = -lse[si] * kLog2e;  // exp(s/8 - lse) = exp2(s log2(e)/8 + nl2)
     }
 }
 
@@ -445,7 +457,8 @@ void attention_bwd_debug_timing(unsigned long long* dev_buf) {
 }
 
 size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads) {
-    return static_cast<size_t>(batch) * seq * heads * kD;  // the fp32 dQ accumulator
+    // the fp32 dQ accumulator, then -lse log2(e) per (sequence, head, query)
+    return static_cast<size_t>(batch) * seq * heads * kD + static_cast<size_t>(batch) * heads * seq;
 }
 
 void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
@@ -453,7 +466,8 @@ void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const fl
     const int h = heads * kD;
     const int tokens = batch * seq;
     const int pairs = tokens * heads;
-    k_attn_delta<<<(pairs * 8 + 255) / 256, 256, 0, s>>>(o, dout, delta, dq_acc, tokens, seq, heads);
+    float* nl2 = dq_acc + static_cast<size_t>(tokens) * h;
+    k_attn_delta<<<(pairs * 8 + 255) / 256, 256, 0, s>>>(o, dout, lse, delta, nl2, dq_acc, tokens, seq, heads);
     const CUtensorMap tq = make_tmap_bf16_2d(qkv, 3ull * h, static_cast<uint64_t>(tokens), 3ll * h, 64, kT);
     const CUtensorMap tdo = make_tmap_bf16_2d(dout, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 64, kT);
     const CUtensorMap tdq = make_tmap_f32_2d(dq_acc, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 32, 32);
@@ -462,10 +476,10 @@ void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const fl
     const int grid = std::min(items, num_sms());
     if (causal) {
         set_smem_once<true>();
-        k_attn_bwd_tc<true><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, lse, delta, dqkv, seq, heads, bhn);
+        k_attn_bwd_tc<true><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, nl2, delta, dqkv, seq, heads, bhn);
     } else {
         set_smem_once<false>();
-        k_attn_bwd_tc<false><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, lse, delta, dqkv, seq, heads, bhn);
+        k_attn_bwd_tc<false><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, nl2, delta, dqkv, seq, heads, bhn);
     }
     const size_t vecs = static_cast<size_t>(tokens) * h / 8;
     k_attn_dq_convert<<<static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 16u)), 256, 0, s>>>(

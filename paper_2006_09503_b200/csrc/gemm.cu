@@ -40,11 +40,14 @@ constexpr int kThreads = 256;
 constexpr int kEpiBuf = 32 * 128;  // one staging buffer: 32 rows x 128 B (TMA box, SW128)
 
 // kCl == 2 is the CTA-pair (cta_group::2) mode: each CTA holds its own 128 rows of A
-// and HALF of the B tile, so the same SMEM carries a deeper stage ring.
+// and HALF of the B tile, so the same SMEM carries a deeper stage ring.  kCl == 4 is
+// two such pairs side by side along N sharing their A rows: each CTA TMA-multicasts
+// half of its A tile into itself and the matching CTA of the other pair, which
+// halves the L2 -> SMEM bytes of A (the GEMMs are L2-feed bound at 256 x 256 tiles).
 template <int BN, int kCl>
 struct GemmCfg {
     static constexpr int kABytes = kBM * kBK * 2;
-    static constexpr int kBBytes = (BN / kCl) * kBK * 2;
+    static constexpr int kBBytes = (BN / (kCl >= 2 ? 2 : 1)) * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = BN == 128 ? 256 : 512;  // 2 x BN accumulator columns, a power of two
     static constexpr int kEpiBytes = 4 * 2 * kEpiBuf;  // 4 epilogue warps x 2 buffers
@@ -96,7 +99,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ EpiMaps em, const KParams p) {
     using Cfg = GemmCfg<BN, kCl>;
     constexpr int S = Cfg::kStages;
-    static_assert(!(kBMN && kCl == 2 && (BN / 2) % 64 != 0), "MN-major B halves must be whole 64-column atoms");
+    static_assert(!(kBMN && kCl >= 2 && (BN / 2) % 64 != 0), "MN-major B halves must be whole 64-column atoms");
+    constexpr bool kPair = kCl >= 2;        // cta_group::2 MMAs over a CTA pair
+    constexpr int kNP = kCl == 4 ? 2 : 1;   // pairs side by side along N
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -117,13 +122,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kblocks = (p.k + kBK - 1) / kBK;
     // work item w: tile group (w % num_tiles) -- kCl vertically adjacent M tiles of one
     // N tile, this CTA taking M tile kCl*g + rank -- and K slice (w / num_tiles)
-    const int rank = kCl == 2 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
-    const int tiles_mg = (tiles_m + kCl - 1) / kCl;
-    const int num_tiles = tiles_mg * tiles_n;
+    const int rank = kPair ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+    const int prank = rank & 1, pair = rank >> 1;  // rank inside the pair, pair index along N
+    const int tiles_mg = kPair ? (tiles_m + 1) / 2 : tiles_m;
+    const int tiles_ng = (tiles_n + kNP - 1) / kNP;
+    const int num_tiles = tiles_mg * tiles_ng;
     const int num_work = num_tiles * p.splits;
     const int kb_per = (kblocks + p.splits - 1) / p.splits;
     const int w0 = blockIdx.x / kCl, wstep = gridDim.x / kCl;
-    constexpr uint16_t kMask = kCl == 2 ? 0x3 : 0x1;
+    const uint16_t pair_mask = static_cast<uint16_t>(kPair ? (0x3 << (2 * pair)) : 0x1);  // my pair's CTAs
+    constexpr uint16_t kAllMask = kCl == 4 ? 0xF : (kCl == 2 ? 0x3 : 0x1);
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmap_a);
@@ -131,21 +139,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&em.d);
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], 1);  // the (leader's) MMA commit frees a stage
+            ptx::mbar_init(&empty_bar[s], kNP);  // every pair leader's MMA commit frees a stage
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull_bar[i], 1);
-            ptx::mbar_init(&tempty_bar[i], 4 * kCl);  // pair mode: both CTAs' epilogues
+            ptx::mbar_init(&tempty_bar[i], kPair ? 8 : 4);  // pair mode: both CTAs' epilogues
         }
         for (int i = 0; i < 4; ++i) ptx::mbar_init(&aux_bar[i], 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) {
-        if constexpr (kCl == 2) ptx::tmem_alloc_2sm<Cfg::kTmemCols>(tmem_slot);
+        if constexpr (kPair) ptx::tmem_alloc_2sm<Cfg::kTmemCols>(tmem_slot);
         else ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
     }
     ptx::tc_fence_before();
-    if constexpr (kCl == 2) ptx::cluster_sync();  // peer barriers initialised before any multicast
+    if constexpr (kPair) ptx::cluster_sync();  // peer barriers initialised before any multicast
     else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -156,8 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             for (int w = w0; w < num_work; w += wstep) {
                 const int tile = w % num_tiles;
-                const int m0 = ((tile % tiles_mg) * kCl + rank) * kBM;
-                const int n0 = (tile / tiles_mg) * BN;
+                const int m0 = ((tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
+                const int n0 = ((tile / tiles_mg) * kNP + pair) * BN;
                 const int kb0 = (w / num_tiles) * kb_per;
                 const int kb1 = min(kblocks, kb0 + kb_per);
                 for (int kb = kb0; kb < kb1; ++kb) {
@@ -165,7 +173,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* da = s_a + stage * Cfg::kABytes;
                     uint8_t* db = s_b + stage * Cfg::kBBytes;
                     const int k0 = kb * kBK;
-                    if constexpr (kCl == 2) {
+                    if constexpr (kCl == 4) {
+                        // A: my half of the shared A tile, multicast into me and my
+                        // counterpart in the other pair; B: my half of my pair's B tile.
+                        // Everything completes on each destination pair leader's barrier.
+                        if (prank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+                        const uint16_t amask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2)));
+                        if constexpr (kAMN)
+                            ptx::tma_load_2d_2sm_mc(da + pair * 64 * kBK * 2, &tmap_a, &full_bar[stage], m0 + pair * 64,
+                                                    k0, amask);
+                        else
+                            ptx::tma_load_2d_2sm_mc(da + pair * 64 * 128, &tmap_a, &full_bar[stage], k0, m0 + pair * 64,
+                                                    amask);
+                        const int nb = n0 + prank * (BN / 2);
+                        if constexpr (kBMN) {
+#pragma unroll
+                            for (int j = 0; j < BN / 128; ++j)
+                                ptx::tma_load_2d_2sm(db + j * 64 * kBK * 2, &tmap_b, &full_bar[stage], nb + j * 64,
+                                                     k0);
+                        } else {
+                            ptx::tma_load_2d_2sm(db, &tmap_b, &full_bar[stage], k0, nb);
+                        }
+                    } else if constexpr (kCl == 2) {
                         // both CTAs' bytes complete on the leader's full barrier
                         if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
                         if constexpr (kAMN) {
@@ -210,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // pair mode: the even CTA issues for both
-            constexpr uint32_t idesc = ptx::idesc_bf16(kBM * kCl, BN, kAMN, kBMN);
+        if (lane == 0 && prank == 0) {  // pair mode: the even CTA issues for both
+            constexpr uint32_t idesc = ptx::idesc_bf16(kBM * (kPair ? 2 : 1), BN, kAMN, kBMN);
             // K-major SW128: rows of 128 B, 8-row groups 1024 B apart; a K step of 16
             // elements is +32 B inside the swizzle atom.  MN-major SW128: 64-element MN
             // groups one TMA box (kBK rows x 128 B) apart, 8-row K groups 1024 B apart;
@@ -240,17 +269,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t ad = ptx::sdesc_sw128(a_addr + kk * a_kstep, a_lbo, a_sbo);
                         const uint64_t bd = ptx::sdesc_sw128(b_addr + kk * b_kstep, b_lbo, b_sbo);
                         const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
-                        if constexpr (kCl == 2) ptx::umma_bf16_2sm(d_tmem, ad, bd, idesc, accum);
+                        if constexpr (kPair) ptx::umma_bf16_2sm(d_tmem, ad, bd, idesc, accum);
                         else ptx::umma_bf16(d_tmem, ad, bd, idesc, accum);
                     }
-                    if constexpr (kCl == 2) ptx::umma_commit_2sm_mc(&empty_bar[stage], kMask);
+                    // the stage is free once every pair that reads it (kCl == 4: both,
+                    // through the shared A halves) has consumed it
+                    if constexpr (kPair) ptx::umma_commit_2sm_mc(&empty_bar[stage], kAllMask);
                     else ptx::umma_commit(&empty_bar[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                if constexpr (kCl == 2) ptx::umma_commit_2sm_mc(&tfull_bar[acc], kMask);
+                if constexpr (kPair) ptx::umma_commit_2sm_mc(&tfull_bar[acc], pair_mask);
                 else ptx::umma_commit(&tfull_bar[acc]);
                 if (++acc == 2) {
                     acc = 0;
@@ -276,8 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         for (int w = w0; w < num_work; w += wstep) {
             const int tile = w % num_tiles;
-            const int m0 = ((tile % tiles_mg) * kCl + rank) * kBM;
-            const int n0 = (tile / tiles_mg) * BN;
+            const int m0 = ((tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
+            const int n0 = ((tile / tiles_mg) * kNP + pair) * BN;
             const int r0 = m0 + q * 32;
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
@@ -403,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (kCl == 2) ptx::mbar_arrive_cluster(&tempty_bar[acc], 0);
+                if constexpr (kPair) ptx::mbar_arrive_cluster(&tempty_bar[acc], 2 * pair);  // my pair leader
                 else ptx::mbar_arrive(&tempty_bar[acc]);
             }
             if (++acc == 2) {
@@ -415,11 +446,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
     }
     ptx::tc_fence_before();
-    if constexpr (kCl == 2) ptx::cluster_sync();  // no CTA exits while its peer may still signal it
+    if constexpr (kPair) ptx::cluster_sync();  // no CTA exits while its peer may still signal it
     else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        if constexpr (kCl == 2) ptx::tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
+        if constexpr (kPair) ptx::tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
         else ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
     }
 }
@@ -479,8 +510,10 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, con
                    "cudaFuncSetAttribute(gemm smem)");
         configured.fetch_or(bit);
     }
-    const int tiles_mg = ((p.m + kBM - 1) / kBM + kCl - 1) / kCl;
-    const int work = tiles_mg * ((p.n + BN - 1) / BN) * p.splits;
+    const int tiles_m = (p.m + kBM - 1) / kBM, tiles_n = (p.n + BN - 1) / BN;
+    const int tiles_mg = kCl >= 2 ? (tiles_m + 1) / 2 : tiles_m;
+    const int tiles_ng = kCl == 4 ? (tiles_n + 1) / 2 : tiles_n;
+    const int work = tiles_mg * tiles_ng * p.splits;
     const int slots = num_sms() / kCl;
     const int grid = kCl * (work < slots ? work : slots);
     cudaLaunchConfig_t cfg{};
@@ -515,7 +548,7 @@ void dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap
         dispatch_epi<BN, false, false, kCl>(ta, tb, em, p, s);
     } else if (amn && !bmn) {
         dispatch_epi<BN, true, false, kCl>(ta, tb, em, p, s);
-    } else if constexpr (kCl == 2 && (BN / 2) % 64 != 0) {
+    } else if constexpr (kCl >= 2 && (BN / 2) % 64 != 0) {
         throw Error("gemm: no CTA-pair tile with MN-major B for this BN");
     } else if (!amn) {
         dispatch_epi<BN, false, true, kCl>(ta, tb, em, p, s);
@@ -527,28 +560,66 @@ void dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap
 struct TileChoice {
     int bn;
     int cl;
+    int splits;
 };
 
-// Tile shape and cluster size, from the B200 sweeps (scripts/gemm_sweep.py,
-// profiles/r1_gemm_sweep_*.json).  With L2->SMEM feed the binding resource, 128 x 256
-// tiles beat 128 x 128 everywhere; the CTA-pair 256 x 256 tile (half of B per CTA)
-// wins 5-10% once N.K is large.  Outputs whose width is a multiple of 192 but not of
-// 256 (N = 768: every dgrad and the proj / fc2 forwards of a hidden-768 model) waste
-// a third of the last wave with 256-wide tiles; 128 x 192 single-CTA tiles recover
-// 3-13% there.  fp32 (wgrad, split-K) outputs keep the 256-wide tiles.
-TileChoice choose_tile(int m, int n, int k, bool f32_out) {
-    if (const char* env = std::getenv("P2BW_GEMM_TILE")) {  // tuning knob: "bn,cl"
-        int bn = 0, cl = 0;
-        if (std::sscanf(env, "%d,%d", &bn, &cl) == 2 && (bn == 128 || bn == 192 || bn == 256) && (cl == 1 || cl == 2))
-            return {bn, cl};
-    }
-    if (n < 256) return {128, 1};
-    if (!f32_out && n % 256 != 0 && n % 192 == 0) return {192, 1};
-    const bool pair = m > kBM && static_cast<double>(n) * k >= 1.5e6;
-    return {256, pair ? 2 : 1};
+bool tile_ok(int bn, int cl, bool bmn) { return !(bmn && cl >= 2 && (bn / 2) % 64 != 0); }
+
+// Steady-state speed of a tile shape relative to the 256 x 256 CTA-pair tile, from the
+// B200 sweeps (scripts/gemm_sweep.py, profiles/r1_gemm_sweep_*.json, corrected for
+// each shape's wave efficiency): 128 x 256 0.95, 128 x 192 0.86, 128 x 128 0.67,
+// pair 256 x 192 0.89, pair 256 x 128 0.64.  (4-CTA clusters sharing A by TMA
+// multicast measured slower on every stage shape and are only reachable by the knob.)
+double tile_speed(int bn, int cl) {
+    if (cl == 2) return bn == 256 ? 1.0 : (bn == 192 ? 0.89 : 0.64);
+    return bn == 256 ? 0.95 : (bn == 192 ? 0.86 : 0.67);
 }
 
-bool tile_ok(int bn, int cl, bool bmn) { return !(bmn && cl == 2 && (bn / 2) % 64 != 0); }
+// Tile shape, cluster and split-K minimising a wave-quantised time model:
+//   time = waves * (k-blocks per unit * tile time per k-block + per-unit overhead)
+// where a unit is one output tile (or K slice of it) of one CTA (pair), waves =
+// ceil(units / (SMs / cluster)), the per-unit overhead (pipeline fill + the epilogue
+// of the last unit) is ~3 k-blocks, and split-K slices pay one more for their fp32
+// reduce-add.  The ragged last wave is what this decides: 96 pair tiles of a
+// [8192 x 768] output on 74 SM pairs run as two waves at 65% occupancy, 256 128 x 192
+// tiles as two waves at 86%.  fp32 (wgrad) outputs keep 256-wide tiles, which the
+// sweeps favour for MN-major operands, and choose only their split count.
+TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn) {
+    const int kblocks = (k + kBK - 1) / kBK;
+    if (const char* env = std::getenv("P2BW_GEMM_TILE")) {  // tuning knob: "bn,cl[,splits]"
+        int bn = 0, cl = 0, sp = 0;
+        const int got = std::sscanf(env, "%d,%d,%d", &bn, &cl, &sp);
+        if (got >= 2 && (bn == 128 || bn == 192 || bn == 256) && (cl == 1 || cl == 2 || cl == 4))
+            return {bn, cl, f32_out && got == 3 && sp >= 1 ? std::min(sp, kblocks) : 1};
+    }
+    const int sms = num_sms();
+    TileChoice best{256, 1, 1};
+    double best_t = 1e300;
+    for (int bn : {256, 192, 128}) {
+        if (f32_out && bn != 256) continue;
+        for (int cl : {2, 1}) {
+            if (!tile_ok(bn, cl, bmn) || (cl == 2 && m <= kBM)) continue;
+            const int tiles_m = (m + kBM - 1) / kBM;
+            const int tiles = (cl == 2 ? (tiles_m + 1) / 2 : tiles_m) * ((n + bn - 1) / bn);
+            const int max_split = f32_out ? std::max(1, kblocks / 8) : 1;
+            const double per_kb = (bn / 256.0) / tile_speed(bn, cl);
+            for (int sp = 1; sp <= max_split; ++sp) {
+                const int kb_per = (kblocks + sp - 1) / sp;
+                const int s_eff = (kblocks + kb_per - 1) / kb_per;
+                if (s_eff != sp) continue;  // no empty slices
+                const long units = static_cast<long>(tiles) * s_eff;
+                const long slots = sms / cl;
+                const long waves = (units + slots - 1) / slots;
+                const double t = waves * (kb_per * per_kb + 3.0 + (s_eff > 1 ? 1.0 : 0.0));
+                if (t < best_t - 1e-9) {
+                    best_t = t;
+                    best = {bn, cl, s_eff};
+                }
+            }
+        }
+    }
+    return best;
+}
 
 }  // namespace
 
@@ -574,13 +645,14 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     if ((epi.ldd % 8) != 0 || (epi.residual && epi.ldr % 8 != 0))
         throw Error("gemm: output leading dims must be multiples of 8");
     const bool amn = a.major == Major::MN, bmn = b.major == Major::MN;
-    TileChoice tc = choose_tile(m, n, k, epi.kind == EpiKind::StoreF32);
+    TileChoice tc = choose_tile(m, n, k, epi.kind == EpiKind::StoreF32, bmn);
     if (!tile_ok(tc.bn, tc.cl, bmn)) tc.cl = 1;
     const int bn = tc.bn, cl = tc.cl;
     // A: rows = m (tile kBM), B: rows = n (tile bn; each CTA of a pair loads bn / 2).
     // K-major maps put k innermost.
-    const CUtensorMap ta = amn ? make_map(a.ptr, m, k, a.ld, kBK) : make_map(a.ptr, k, m, a.ld, kBM);
-    const CUtensorMap tb = bmn ? make_map(b.ptr, n, k, b.ld, kBK) : make_map(b.ptr, k, n, b.ld, bn / cl);
+    // kCl == 4: each CTA multicasts half (64 rows) of the A tile
+    const CUtensorMap ta = amn ? make_map(a.ptr, m, k, a.ld, kBK) : make_map(a.ptr, k, m, a.ld, cl == 4 ? kBM / 2 : kBM);
+    const CUtensorMap tb = bmn ? make_map(b.ptr, n, k, b.ld, kBK) : make_map(b.ptr, k, n, b.ld, bn / (cl >= 2 ? 2 : 1));
     EpiMaps em{};
     if (epi.kind == EpiKind::StoreF32) {
         em.d = make_map_t(epi.d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, n, m, epi.ldd, 32, 32);
@@ -597,16 +669,8 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     }
     // Split-K for fp32 (wgrad) GEMMs whose output has too few tiles to fill the
     // SMs: every K slice reduce-adds into D (pre-zeroed when beta == 0).
-    int splits = 1;
+    const int splits = epi.kind == EpiKind::StoreF32 ? tc.splits : 1;
     if (epi.kind == EpiKind::StoreF32) {
-        const int tiles = ((m + kBM - 1) / kBM) * ((n + bn - 1) / bn);
-        const int kblocks = (k + kBK - 1) / kBK;
-        if (tiles < 2 * num_sms() && kblocks >= 16) {
-            splits = std::min(kblocks / 8, (2 * num_sms() + tiles - 1) / tiles);
-            splits = std::max(splits, 1);
-            const int kb_per = (kblocks + splits - 1) / splits;
-            splits = (kblocks + kb_per - 1) / kb_per;  // no empty slices
-        }
         if (splits > 1 && epi.beta == 0.0f) {
             if (epi.ldd == n) {
                 check_cuda(cudaMemsetAsync(epi.d, 0, static_cast<size_t>(m) * n * sizeof(float), stream), "memset");
@@ -624,7 +688,10 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     prof::Scope scope(cls, 2.0 * m * n * k,
                       2.0 * (static_cast<double>(m) * k + static_cast<double>(n) * k) + out_bytes * m * n, 1,
                       stream);
-    if (bn == 256 && cl == 2) dispatch_major<256, 2>(amn, bmn, ta, tb, em, p, stream);
+    if (bn == 256 && cl == 4) dispatch_major<256, 4>(amn, bmn, ta, tb, em, p, stream);
+    else if (bn == 192 && cl == 4) dispatch_major<192, 4>(amn, bmn, ta, tb, em, p, stream);
+    else if (bn == 128 && cl == 4) dispatch_major<128, 4>(amn, bmn, ta, tb, em, p, stream);
+    else if (bn == 256 && cl == 2) dispatch_major<256, 2>(amn, bmn, ta, tb, em, p, stream);
     else if (bn == 256) dispatch_major<256, 1>(amn, bmn, ta, tb, em, p, stream);
     else if (bn == 192 && cl == 2) dispatch_major<192, 2>(amn, bmn, ta, tb, em, p, stream);
     else if (bn == 192) dispatch_major<192, 1>(amn, bmn, ta, tb, em, p, stream);

@@ -98,13 +98,26 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMa
         : "memory");
 }
 
-// Arrive on the mbarrier at the same SMEM offset in cluster CTA `cta`.
+// 2-SM multicast TMA load: the bytes land at the same SMEM offset in every CTA of
+// cta_mask and complete on the mbarrier of each destination's pair leader.
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                   int32_t c1, uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(cta_mask)
+        : "memory");
+}
+
+// Arrive on the mbarrier at the same SMEM offset in cluster CTA `cta` (release at CTA
+// scope: the callers order TMEM reads with tcgen05 fences, not memory; a cluster-scope
+// release compiles to MEMBAR.ALL.GPU and stalls on the epilogue's in-flight stores).
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
     asm volatile(
         "{\n"
         ".reg .b32 ra;\n"
         "mapa.shared::cluster.u32 ra, %0, %1;\n"
-        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(cta)
         : "memory");

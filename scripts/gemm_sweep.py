@@ -41,7 +41,7 @@ ms = e0.elapsed_time(e1) / 20
 print(json.dumps({"name": name, "tflops": round(2 * m * n * k / ms / 1e9, 1)}))
 '''
 rows = {}
-for cfg in ["auto", "128,1", "128,2", "192,1", "192,2", "256,1", "256,2", "cublas"]:
+for cfg in os.environ.get("SWEEP_CFGS", "auto 128,1 128,2 192,1 192,2 256,1 256,2 cublas").split():
     env = dict(os.environ)
     if cfg == "cublas":
         env["SWEEP_CUBLAS"] = "1"

@@ -113,12 +113,14 @@ def test_gemm_wgrad_split_k(m, n, k, beta):
     assert (d - ref).abs().max().item() < 2e-3 * ref.abs().max().item()
 
 
-@pytest.mark.parametrize("tile", ["128,1", "128,2", "192,1", "192,2", "256,1", "256,2"])
+@pytest.mark.parametrize("tile", ["128,1", "128,2", "192,1", "192,2", "256,1", "256,2", "128,4", "192,4", "256,4"])
 @pytest.mark.parametrize("am,bm,kind", [(0, 0, 0), (0, 1, 0), (1, 1, 1), (0, 1, 2)])
 def test_gemm_every_tile(monkeypatch, tile, am, bm, kind):
     """Every (BN, cluster) tile the shape-based chooser may pick, on a ragged shape,
     for the forward (bf16 + bias), dgrad (bf16 / dGELU) and wgrad (fp32) layouts.
-    Pair tiles whose B half is not whole 64-column atoms fall back to one CTA."""
+    Pair tiles whose B half is not whole 64-column atoms fall back to one CTA.  The
+    4-CTA clusters (two pairs sharing A through TMA multicast) leave the second pair
+    of the last N group past N when the tile count along N is odd."""
     monkeypatch.setenv("P2BW_GEMM_TILE", tile)
     m, n, k = 1000, 768, 704
     gen = torch.Generator(device="cuda").manual_seed(17 + am + 2 * bm + 4 * kind)
@@ -143,3 +145,19 @@ def test_gemm_every_tile(monkeypatch, tile, am, bm, kind):
     torch.cuda.synchronize()
     tol = 1e-3 if kind == 1 else 0.02
     assert (d.float() - ref).abs().max().item() <= tol * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("tile", ["256,4", "192,4"])
+@pytest.mark.parametrize("m,n,k", [(8192, 768, 3072), (4096, 2304, 768), (2304, 768, 8192)])
+def test_gemm_multicast_cluster_large(monkeypatch, tile, m, n, k):
+    """4-CTA clusters on stage-sized shapes (many K blocks, several waves)."""
+    monkeypatch.setenv("P2BW_GEMM_TILE", tile)
+    gen = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A, a, lda = _operand(m, k, 0, gen)
+    B, b, ldb = _operand(n, k, 0, gen)
+    d = torch.zeros(m, n, device="cuda")
+    epi = GemmEpilogue(kind=1, d=d.data_ptr(), ldd=n, alpha=1.0, beta=0.0)
+    _gemm(a, lda, 0, b, ldb, 0, m, n, k, epi)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    assert (d - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
