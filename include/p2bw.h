@@ -262,6 +262,11 @@ typedef struct {
     const void* aux;
     float alpha;
     float beta;
+    /* Optional fp32 workspace of >= m*n floats (NULL: none).  Lets a plain bf16 store
+     * (kind 0 without bias / GELU / residual) with few output tiles and a long K run
+     * split-K into it and be cast to bf16 afterwards. */
+    void* workspace;
+    long long workspace_floats;
 } p2bw_gemm_epilogue;
 
 /* D[m x n] = A[m x k] . B[n x k]^T on tcgen05 tensor cores (bf16 in, fp32 acc).

@@ -34,6 +34,8 @@ class GemmEpilogue(C.Structure):
         ("aux", C.c_void_p),
         ("alpha", C.c_float),
         ("beta", C.c_float),
+        ("workspace", C.c_void_p),
+        ("workspace_floats", C.c_longlong),
     ]
 
 

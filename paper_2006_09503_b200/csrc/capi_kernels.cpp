@@ -27,6 +27,8 @@ extern "C" int p2bw_kernel_gemm_bf16(const void* a, long long lda, int a_major, 
         e.aux = static_cast<const bf16*>(epi->aux);
         e.alpha = epi->alpha;
         e.beta = epi->beta;
+        e.workspace = static_cast<float*>(epi->workspace);
+        e.workspace_floats = epi->workspace_floats;
         gemm_bf16(A, B, m, n, k, e, static_cast<cudaStream_t>(stream));
     });
 }

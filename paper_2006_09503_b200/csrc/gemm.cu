@@ -455,6 +455,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// d[r, c] = bf16(ws[r * n + c]) for an fp32 split-K workspace.
+__global__ void k_cast_f32_bf16_2d(const float* __restrict__ ws, int m, int n, bf16* __restrict__ d, int64_t ldd) {
+    const int nv = n / 4;
+    for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < static_cast<int64_t>(m) * nv;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(v / nv), c = static_cast<int>(v % nv) * 4;
+        const float4 x = *reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * n + c);
+        *reinterpret_cast<uint2*>(d + r * ldd + c) = make_uint2(ptx::pack_bf16x2(x.x, x.y), ptx::pack_bf16x2(x.z, x.w));
+    }
+}
+
+void cast_f32_bf16_2d(const float* ws, int m, int n, bf16* d, int64_t ldd, cudaStream_t s) {
+    const int64_t vec = static_cast<int64_t>(m) * (n / 4);
+    k_cast_f32_bf16_2d<<<static_cast<int>(std::min<int64_t>((vec + 255) / 256, 148 * 16)), 256, 0, s>>>(ws, m, n, d,
+                                                                                                         ldd);
+    check_cuda(cudaGetLastError(), "cast_f32_bf16_2d");
+}
+
 // ---- host side -------------------------------------------------------------
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -561,6 +579,7 @@ struct TileChoice {
     int bn;
     int cl;
     int splits;
+    double t;  // modelled time, in 256 x 256 pair k-block units
 };
 
 bool tile_ok(int bn, int cl, bool bmn) { return !(bmn && cl >= 2 && (bn / 2) % 64 != 0); }
@@ -584,16 +603,16 @@ double tile_speed(int bn, int cl) {
 // [8192 x 768] output on 74 SM pairs run as two waves at 65% occupancy, 256 128 x 192
 // tiles as two waves at 86%.  fp32 (wgrad) outputs keep 256-wide tiles, which the
 // sweeps favour for MN-major operands, and choose only their split count.
-TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn) {
+TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_split) {
     const int kblocks = (k + kBK - 1) / kBK;
     if (const char* env = std::getenv("P2BW_GEMM_TILE")) {  // tuning knob: "bn,cl[,splits]"
         int bn = 0, cl = 0, sp = 0;
         const int got = std::sscanf(env, "%d,%d,%d", &bn, &cl, &sp);
         if (got >= 2 && (bn == 128 || bn == 192 || bn == 256) && (cl == 1 || cl == 2 || cl == 4))
-            return {bn, cl, f32_out && got == 3 && sp >= 1 ? std::min(sp, kblocks) : 1};
+            return {bn, cl, allow_split && got == 3 && sp >= 1 ? std::min(sp, kblocks) : 1, 0.0};
     }
     const int sms = num_sms();
-    TileChoice best{256, 1, 1};
+    TileChoice best{256, 1, 1, 1e300};
     double best_t = 1e300;
     for (int bn : {256, 192, 128}) {
         if (f32_out && bn != 256) continue;
@@ -601,7 +620,7 @@ TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn) {
             if (!tile_ok(bn, cl, bmn) || (cl == 2 && m <= kBM)) continue;
             const int tiles_m = (m + kBM - 1) / kBM;
             const int tiles = (cl == 2 ? (tiles_m + 1) / 2 : tiles_m) * ((n + bn - 1) / bn);
-            const int max_split = f32_out ? std::max(1, kblocks / 8) : 1;
+            const int max_split = allow_split ? std::max(1, kblocks / 8) : 1;
             const double per_kb = (bn / 256.0) / tile_speed(bn, cl);
             for (int sp = 1; sp <= max_split; ++sp) {
                 const int kb_per = (kblocks + sp - 1) / sp;
@@ -613,7 +632,7 @@ TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn) {
                 const double t = waves * (kb_per * per_kb + 3.0 + (s_eff > 1 ? 1.0 : 0.0));
                 if (t < best_t - 1e-9) {
                     best_t = t;
-                    best = {bn, cl, s_eff};
+                    best = {bn, cl, s_eff, t};
                 }
             }
         }
@@ -645,7 +664,29 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     if ((epi.ldd % 8) != 0 || (epi.residual && epi.ldr % 8 != 0))
         throw Error("gemm: output leading dims must be multiples of 8");
     const bool amn = a.major == Major::MN, bmn = b.major == Major::MN;
-    TileChoice tc = choose_tile(m, n, k, epi.kind == EpiKind::StoreF32, bmn);
+    const bool f32 = epi.kind == EpiKind::StoreF32;
+    TileChoice tc = choose_tile(m, n, k, f32, bmn, f32);
+    // Plain bf16 stores with few output tiles and a long K (the LM-head dgrad: 1232 x 768
+    // over K = 30592 fills 60 SMs with 128 x 128 tiles) run split-K into the caller's
+    // fp32 workspace and are cast afterwards, when the model says that wins.
+    const bool plain = epi.kind == EpiKind::StoreBF16 && !epi.bias && !epi.residual && !epi.gelu && !epi.preact;
+    if (plain && epi.workspace != nullptr && epi.workspace_floats >= static_cast<int64_t>(m) * n &&
+        std::getenv("P2BW_GEMM_TILE") == nullptr) {
+        TileChoice ts = choose_tile(m, n, k, true, bmn, true);
+        // memset + cast: ~10 B per output at HBM speed, in k-block units (~0.26 us each)
+        ts.t += 10.0 * m * n / 6.5e12 / 0.26e-6;
+        if (ts.splits > 1 && ts.t < tc.t) {
+            GemmEpilogue f;
+            f.kind = EpiKind::StoreF32;
+            f.d = epi.workspace;
+            f.ldd = n;
+            f.alpha = epi.alpha;
+            f.beta = 0.0f;
+            gemm_bf16(a, b, m, n, k, f, stream);
+            cast_f32_bf16_2d(epi.workspace, m, n, static_cast<bf16*>(epi.d), epi.ldd, stream);
+            return;
+        }
+    }
     if (!tile_ok(tc.bn, tc.cl, bmn)) tc.cl = 1;
     const int bn = tc.bn, cl = tc.cl;
     // A: rows = m (tile kBM), B: rows = n (tile bn; each CTA of a pair loads bn / 2).
@@ -669,7 +710,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     }
     // Split-K for fp32 (wgrad) GEMMs whose output has too few tiles to fill the
     // SMs: every K slice reduce-adds into D (pre-zeroed when beta == 0).
-    const int splits = epi.kind == EpiKind::StoreF32 ? tc.splits : 1;
+    const int splits = f32 ? tc.splits : 1;
     if (epi.kind == EpiKind::StoreF32) {
         if (splits > 1 && epi.beta == 0.0f) {
             if (epi.ldd == n) {

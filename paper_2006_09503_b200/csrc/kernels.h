@@ -40,6 +40,10 @@ struct GemmEpilogue {
     const bf16* aux = nullptr;       // u for DGeluBF16, [M x ldd]
     float alpha = 1.0f;
     float beta = 0.0f;
+    // Optional fp32 [M x N] workspace: a plain bf16 store (no bias / GELU / residual)
+    // with few output tiles and a long K may then run split-K into it and be cast.
+    float* workspace = nullptr;
+    int64_t workspace_floats = 0;
 };
 
 // D[M x N] = A[M x K] . B[N x K]^T on tcgen05 (TMA -> SMEM -> UMMA -> TMEM -> epilogue).

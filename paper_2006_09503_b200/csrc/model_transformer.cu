@@ -228,7 +228,8 @@ public:
         if (last_) {
             // logits now hold dloss/dlogits (softmax_xent ran in the forward)
             bf16* dxf = R_ < T_ ? gH_ : gA_;
-            gemm_store_mn_b(st.logits, vp_, W + off_head_, h_, R_, h_, vp_, dxf, s);
+            gemm_store_mn_b(st.logits, vp_, W + off_head_, h_, R_, h_, vp_, dxf, s, head_ws_,
+                            static_cast<int64_t>(R_) * h_);
             gemm_wgrad(st.logits, vp_, st.xf, h_, vp_, h_, R_, grad_ + off_head_, beta, s);
             bf16* dsrc = dxf;
             bf16* dhead = R_ < T_ ? gB_ : gA_;
@@ -385,6 +386,7 @@ private:
         attn_scratch_ = dalloc<float>(attention_bwd_scratch_floats(b_, seq_, heads_));
         if (last_) {
             row_loss_ = dalloc<float>(static_cast<size_t>(R_));
+            head_ws_ = dalloc<float>(static_cast<size_t>(R_) * h);
             if (R_ < T_) gH_ = dalloc<bf16>(static_cast<size_t>(R_) * h);
             // evenly spaced head positions, identical for every sequence of every microbatch
             std::vector<int> idx(static_cast<size_t>(R_));
@@ -426,11 +428,13 @@ private:
 
     // dgrad: D[m x n] = A[m x k] . B where B is stored [k x n] (weights [out x in]).
     void gemm_store_mn_b(const bf16* a, int lda, const bf16* w, int ldw, int m, int n, int k, bf16* d,
-                         cudaStream_t s) const {
+                         cudaStream_t s, float* ws = nullptr, int64_t ws_floats = 0) const {
         GemmEpilogue e;
         e.kind = EpiKind::StoreBF16;
         e.d = d;
         e.ldd = n;
+        e.workspace = ws;  // split-K over the vocabulary for the LM-head dgrad
+        e.workspace_floats = ws_floats;
         gemm_bf16({a, lda, Major::K}, {w, ldw, Major::MN}, m, n, k, e, s);
     }
 
@@ -473,6 +477,7 @@ private:
     float* attn_scratch_ = nullptr;
     float* red_scratch_ = nullptr;
     float* row_loss_ = nullptr;
+    float* head_ws_ = nullptr;
     int* head_idx_ = nullptr;
     double stash_bytes_ = 0.0;
     int capacity_ = 0;

@@ -108,37 +108,38 @@ __global__ void k_embed_bwd_pos(const bf16* __restrict__ dx0, float* __restrict_
 
 // Second phase of the deterministic column reductions, for up to 3 statistics at
 // once (blockIdx.y): out_y[c] (=|+=) sum_{p < parts} part[(y * parts + p) * n + c] in a
-// fixed order.  32 columns x 8 part lanes per CTA; eight independent accumulators
-// keep eight L2 loads in flight per thread (the phase is latency-, not byte-bound).
+// fixed order.  8 columns x 32 part lanes per CTA, so even a 768-wide statistic
+// spreads over 96 CTAs; each thread keeps its (parts / 32) loads in flight at once
+// (the phase is latency-, not byte-bound: it was 7 us at 24 CTAs x 8 part lanes).
 struct ReduceOut {
     float* out[3];
 };
 
 __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ part, int parts, int n,
                                                       ReduceOut outs, int overwrite) {
-    __shared__ float red[8][33];
-    const int col = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int lane8 = threadIdx.x >> 5;
+    __shared__ float red[32][9];
+    const int cl = threadIdx.x & 7, plane = threadIdx.x >> 3;
+    const int col = blockIdx.x * 8 + cl;
     const float* base = part + static_cast<size_t>(blockIdx.y) * parts * n;
-    float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    float acc = 0.0f;
     if (col < n) {
-        int p = lane8;
-        for (; p + 56 < parts; p += 64) {
-            float v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = base[static_cast<size_t>(p + 8 * u) * n + col];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) a[u] += v[u];
+        int p = plane;
+        for (; p + 96 < parts; p += 128) {
+            const float v0 = base[static_cast<size_t>(p) * n + col], v1 = base[static_cast<size_t>(p + 32) * n + col];
+            const float v2 = base[static_cast<size_t>(p + 64) * n + col], v3 = base[static_cast<size_t>(p + 96) * n + col];
+            acc += v0;
+            acc += v1;
+            acc += v2;
+            acc += v3;
         }
-        for (int u = 0; p < parts; p += 8, ++u) a[u & 7] += base[static_cast<size_t>(p) * n + col];
+        for (; p < parts; p += 32) acc += base[static_cast<size_t>(p) * n + col];
     }
-    const float acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-    red[lane8][threadIdx.x & 31] = acc;
+    red[plane][cl] = acc;
     __syncthreads();
-    if (lane8 == 0 && col < n) {
+    if (plane == 0 && col < n) {
         float s = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s += red[i][threadIdx.x & 31];
+        for (int i = 0; i < 32; ++i) s += red[i][cl];
         float* out = outs.out[blockIdx.y];
         out[col] = overwrite ? s : out[col] + s;
     }
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
 
 void reduce_parts(const float* part, int parts, int n, float* out, bool overwrite, cudaStream_t s) {
     ReduceOut o{{out, nullptr, nullptr}};
-    k_reduce_parts<<<dim3((n + 31) / 32, 1), 256, 0, s>>>(part, parts, n, o, overwrite ? 1 : 0);
+    k_reduce_parts<<<dim3((n + 7) / 8, 1), 256, 0, s>>>(part, parts, n, o, overwrite ? 1 : 0);
 }
 
 // Column statistics of a bf16 matrix, per row-block partials (block = 32 column
@@ -216,15 +217,31 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
     if (warp >= rows) return;
     const int hv = h / 8;
     const bf16* xr = x + static_cast<size_t>(warp) * h;
-    float v[NV][8];
-    float sum = 0.0f;
+    // gamma / beta are issued with the row (packed bf16), so their latency overlaps the
+    // row's instead of following the two reductions
+    uint4 xp[NV], gp[NV], bp[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         const int vi = lane + 32 * i;
         if (vi < hv) {
-            load8(xr + vi * 8, v[i]);
+            xp[i] = *reinterpret_cast<const uint4*>(xr + vi * 8);
+            gp[i] = *reinterpret_cast<const uint4*>(g + vi * 8);
+            bp[i] = *reinterpret_cast<const uint4*>(b + vi * 8);
+        }
+    }
+    float v[NV][8];
+    float sum = 0.0f;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) sum += v[i][q];
+    for (int i = 0; i < NV; ++i) {
+        if (lane + 32 * i < hv) {
+            const uint32_t w[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float2 f = ptx::unpack_bf16x2(w[t]);
+                v[i][2 * t] = f.x;
+                v[i][2 * t + 1] = f.y;
+                sum += f.x + f.y;
+            }
         }
     }
     const float mu = warp_sum(sum) / h;
@@ -239,11 +256,15 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
     for (int i = 0; i < NV; ++i) {
         const int vi = lane + 32 * i;
         if (vi < hv) {
-            float gg[8], bb[8], o[8];
-            load8(g + vi * 8, gg);
-            load8(b + vi * 8, bb);
+            const uint32_t gw[4] = {gp[i].x, gp[i].y, gp[i].z, gp[i].w};
+            const uint32_t bw[4] = {bp[i].x, bp[i].y, bp[i].z, bp[i].w};
+            float o[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = (v[i][q] - mu) * rs * gg[q] + bb[q];
+            for (int t = 0; t < 4; ++t) {
+                const float2 gf = ptx::unpack_bf16x2(gw[t]), bf = ptx::unpack_bf16x2(bw[t]);
+                o[2 * t] = (v[i][2 * t] - mu) * rs * gf.x + bf.x;
+                o[2 * t + 1] = (v[i][2 * t + 1] - mu) * rs * gf.y + bf.y;
+            }
             store8(y + static_cast<size_t>(warp) * h + vi * 8, o);
         }
     }
@@ -261,21 +282,82 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
 //   stat 2 (kSum): sum_r bf16(dx)  -- the bias gradient of the linear layer whose
 //                  output gradient dx is (saves a separate pass over dx).
 // dx may alias dy: each warp reads its whole row before writing it.  Row r goes
-// to warp r mod (grid warps): deterministic.  Row data stays packed bf16 in
-// registers between the two passes.
+// to warp r mod (grid warps): deterministic.
+// The column accumulators take most of the register file, so rows are not double-
+// buffered in registers: each warp cp.async-prefetches its NEXT row (x, dy, dres,
+// mean, rstd) into a private SMEM slot while it works on the current one, which
+// keeps a row's DRAM latency off the per-row dependency chain (the kernel was
+// latency-bound at ~1.4 TB/s with 3.5 rows per warp).  gamma is staged once per CTA.
 // 16 warps per SM for h <= 768; wide rows (more accumulators per lane) get 8 warps
 // and the full 255-register budget.
 __host__ __device__ constexpr int ln_bwd_threads(int nv) { return nv >= 4 ? 256 : 512; }
+
+// per-warp staging: 2 buffers x {x, dy, dres} rows (bf16) + {mean, rstd}
+__host__ __device__ constexpr int ln_bwd_buf_bytes(int h) { return 3 * h * 2 + 16; }
+inline size_t ln_bwd_smem_bytes(int nv, int h) {
+    const int warps = ln_bwd_threads(nv) / 32;
+    const size_t staging = static_cast<size_t>(warps) * 2 * ln_bwd_buf_bytes(h) + static_cast<size_t>(h) * 4;
+    const size_t red = static_cast<size_t>(warps) * h * 4;
+    return std::max(staging, red);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
 
 template <int NV, bool kSum>
 __global__ void __launch_bounds__(ln_bwd_threads(NV), 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
              bf16* dx, int rows, int h, float* __restrict__ part) {
-    extern __shared__ float red[];  // [kWarps][h]
+    extern __shared__ __align__(16) uint8_t ln_smem[];
+    float* red = reinterpret_cast<float*>(ln_smem);  // [kWarps][h], after the row loop
     constexpr int kThreads = ln_bwd_threads(NV), kWarps = kThreads / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int hv = h / 8;
+    const bool has_res = dres != nullptr;
+    const int bufb = ln_bwd_buf_bytes(h);
+    const uint32_t s0 = ptx::smem_u32(ln_smem);
+    const uint32_t wbase = s0 + static_cast<uint32_t>(warp * 2 * bufb);
+    const uint32_t sgam = s0 + static_cast<uint32_t>(kWarps * 2 * bufb);  // gamma, fp32 [h]
+    for (int c = threadIdx.x; c < h; c += kThreads)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sgam + c * 4), "f"(__bfloat162float(g[c])) : "memory");
+    auto prefetch = [&](int r, int buf) {
+        const uint32_t b = wbase + static_cast<uint32_t>(buf * bufb);
+        const size_t ro = static_cast<size_t>(r) * h;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int vi = lane + 32 * i;
+            if (vi < hv) {
+                cp_async16(b + vi * 16, x + ro + vi * 8);
+                cp_async16(b + 2 * h + vi * 16, dy + ro + vi * 8);
+                if (has_res) cp_async16(b + 4 * h + vi * 16, dres + ro + vi * 8);
+            }
+        }
+        if (lane == 0) {
+            cp_async4(b + 6 * h, mean + r);
+            cp_async4(b + 6 * h + 4, rstd + r);
+        }
+        cp_async_commit();
+    };
     float ag[NV][8], ab[NV][8], as[kSum ? NV : 1][8];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -286,25 +368,36 @@ __global__ void __launch_bounds__(ln_bwd_threads(NV), 1)
             if constexpr (kSum) as[i][q] = 0.0f;
         }
     }
-    for (int r = blockIdx.x * kWarps + warp; r < rows; r += gridDim.x * kWarps) {
-        const float mu = mean[r], rs = rstd[r];
+    __syncthreads();  // gamma staged
+    const int stride = gridDim.x * kWarps;
+    int r = blockIdx.x * kWarps + warp;
+    if (r < rows) prefetch(r, 0);
+    for (int it = 0; r < rows; r += stride, ++it) {
+        const int buf = it & 1;
+        if (r + stride < rows) prefetch(r + stride, buf ^ 1);
+        else cp_async_commit();  // empty group: keeps "all but the newest" == this row
+        cp_async_wait<1>();
+        __syncwarp();
+        const uint32_t b = wbase + static_cast<uint32_t>(buf * bufb);
+        const float mu = lds_f(b + 6 * h), rs = lds_f(b + 6 * h + 4);
         uint4 xp[NV], dp[NV];
         float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             const int vi = lane + 32 * i;
             if (vi < hv) {
-                xp[i] = *reinterpret_cast<const uint4*>(x + static_cast<size_t>(r) * h + vi * 8);
-                dp[i] = *reinterpret_cast<const uint4*>(dy + static_cast<size_t>(r) * h + vi * 8);
+                xp[i] = lds_u4(b + vi * 16);
+                dp[i] = lds_u4(b + 2 * h + vi * 16);
             }
         }
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-            if (lane + 32 * i < hv) {
+            const int vi = lane + 32 * i;
+            if (vi < hv) {
                 const uint32_t xw[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
                 const uint32_t dw[4] = {dp[i].x, dp[i].y, dp[i].z, dp[i].w};
-                float gv[8];  // gamma: re-read per row from L1 (keeps registers for the sums)
-                load8(g + (lane + 32 * i) * 8, gv);
+                const float4 g0 = ptx::lds_f4(sgam + vi * 32), g1 = ptx::lds_f4(sgam + vi * 32 + 16);
+                const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
@@ -326,19 +419,24 @@ __global__ void __launch_bounds__(ln_bwd_threads(NV), 1)
             if (vi < hv) {
                 const uint32_t xw[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
                 const uint32_t dw[4] = {dp[i].x, dp[i].y, dp[i].z, dp[i].w};
-                float gv[8], o[8];
-                load8(g + vi * 8, gv);
+                const float4 g0 = ptx::lds_f4(sgam + vi * 32), g1 = ptx::lds_f4(sgam + vi * 32 + 16);
+                const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                float o[8];
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
                     o[2 * t] = rs * (df.x * gv[2 * t] - m1 - (xf.x - mu) * rs * m2);
                     o[2 * t + 1] = rs * (df.y * gv[2 * t + 1] - m1 - (xf.y - mu) * rs * m2);
                 }
-                if (dres != nullptr) {
-                    float rv[8];
-                    load8(dres + static_cast<size_t>(r) * h + vi * 8, rv);
+                if (has_res) {
+                    const uint4 rp = lds_u4(b + 4 * h + vi * 16);
+                    const uint32_t rw[4] = {rp.x, rp.y, rp.z, rp.w};
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) o[q] += rv[q];
+                    for (int t = 0; t < 4; ++t) {
+                        const float2 rf = ptx::unpack_bf16x2(rw[t]);
+                        o[2 * t] += rf.x;
+                        o[2 * t + 1] += rf.y;
+                    }
                 }
                 const uint4 packed = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
                                                 ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
@@ -354,7 +452,10 @@ __global__ void __launch_bounds__(ln_bwd_threads(NV), 1)
                 }
             }
         }
+        __syncwarp();  // this buffer is the target of the prefetch two rows on
     }
+    cp_async_wait<0>();
+    __syncthreads();  // staging area becomes the reduction buffer
     // block reduction over the warps, one statistic at a time, fixed order
     for (int st = 0; st < (kSum ? 3 : 2); ++st) {
 #pragma unroll
@@ -576,13 +677,13 @@ template <int NV, bool kSum>
 void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
     constexpr int kThreads = ln_bwd_threads(NV);
-    const size_t smem = static_cast<size_t>(kThreads / 32) * h * sizeof(float);
+    const size_t smem = ln_bwd_smem_bytes(NV, h);
     static std::atomic<uint32_t> configured{0};
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     if ((configured.load() & (1u << (dev & 31))) == 0) {
         check_cuda(cudaFuncSetAttribute(k_ln_bwd<NV, kSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        16 * 2048 * static_cast<int>(sizeof(float))),
+                                        static_cast<int>(ln_bwd_smem_bytes(NV, NV * 256))),
                    "cudaFuncSetAttribute(ln bwd smem)");
         configured.fetch_or(1u << (dev & 31));
     }
@@ -611,7 +712,7 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
     if (dsum) dispatch_ln_bwd<true>(nv, grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
     else dispatch_ln_bwd<false>(nv, grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
     ReduceOut o{{dg, db, dsum}};
-    k_reduce_parts<<<dim3((h + 31) / 32, dsum ? 3 : 2), 256, 0, s>>>(scratch, grid, h, o, overwrite ? 1 : 0);
+    k_reduce_parts<<<dim3((h + 7) / 8, dsum ? 3 : 2), 256, 0, s>>>(scratch, grid, h, o, overwrite ? 1 : 0);
     check_cuda(cudaGetLastError(), "layernorm_bwd");
 }
 

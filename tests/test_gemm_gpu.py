@@ -161,3 +161,24 @@ def test_gemm_multicast_cluster_large(monkeypatch, tile, m, n, k):
     torch.cuda.synchronize()
     ref = A.float() @ B.float().t()
     assert (d - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("m,n,k,bm", [(1232, 768, 30592, 1), (300, 256, 8192, 0)])
+def test_gemm_bf16_split_k_workspace(m, n, k, bm):
+    """A plain bf16 store with few output tiles and a long K (the LM-head dgrad) runs
+    split-K into the fp32 workspace and is cast: same result as the direct store."""
+    gen = torch.Generator(device="cuda").manual_seed(m + k)
+    A, a, lda = _operand(m, k, 0, gen)
+    B, b, ldb = _operand(n, k, bm, gen)
+    ws = torch.full((m * n,), 3.0, device="cuda")
+    d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    epi = GemmEpilogue(kind=0, d=d.data_ptr(), ldd=n, alpha=0.5, workspace=ws.data_ptr(), workspace_floats=m * n)
+    _gemm(a, lda, 0, b, ldb, bm, m, n, k, epi)
+    d2 = torch.empty_like(d)
+    epi2 = GemmEpilogue(kind=0, d=d2.data_ptr(), ldd=n, alpha=0.5)
+    _gemm(a, lda, 0, b, ldb, bm, m, n, k, epi2)
+    torch.cuda.synchronize()
+    ref = 0.5 * (A.float() @ B.float().t())
+    scale = ref.abs().max().item()
+    assert (d.float() - ref).abs().max().item() <= 0.01 * scale
+    assert (d2.float() - ref).abs().max().item() <= 0.01 * scale
