@@ -137,6 +137,11 @@ typedef struct {
      * p2bw_engine_export_stage / p2bw_engine_connect_stage before the first run. */
     int first_local_stage;
     int local_stages;
+    /* Activation recomputation (the planner's r flag, planner.cpp:21-22; timed by
+     * simulate() as a Recompute op before each Backward, simulator.cpp:242-247):
+     * a Forward keeps only the stage input, the Backward re-runs the stage forward
+     * into one shared workspace first.  Numerics are unchanged. */
+    int recompute;
 } p2bw_desc;
 
 typedef struct {

@@ -49,6 +49,7 @@ p2bw::EngineConfig config_from_desc(const p2bw_desc& dd) {
     if (d->devices != nullptr) c.devices.assign(d->devices, d->devices + d->depth);
     c.first_local = d->first_local_stage;
     c.local_count = d->local_stages;
+    c.recompute = d->recompute != 0;
     if (c.lr < 0) throw p2bw::Error("learning rate must be >= 0");
     if (c.momentum < 0 || c.momentum >= 1) throw p2bw::Error("momentum must be in [0, 1)");
     return c;

@@ -406,6 +406,10 @@ void Engine::issue_backward(Stage& st, const OpRec& op) {
         if (k > pv.grad_slots) wait_on(ev_->bwd[s - 1], k - pv.grad_slots, st.stream);
         g_out = pv.grad_ring[(k - 1) % pv.grad_slots];
     }
+    if (cfg_.recompute) {  // Recompute op (simulator.cpp:242-247): the stage input is in its ring slot
+        st.model->recompute(k, wslot, sslot, s > 0 ? st.act_ring[sslot] : nullptr, st.stream);
+        if (trace_on_) trace_split(st, OpRec{P2BW_OP_RECOMPUTE, k, op.weight_version});
+    }
     st.model->backward(k, wslot, sslot, g_in, g_out, st.grad_count == 0, st.stream);
     record(ev_->bwd[s], k, st.stream);
     // Backward k released this stage's act slot and grad slot of microbatch k:
@@ -668,6 +672,11 @@ void Engine::trace_end(Stage& st, const OpRec& op) {
     check_cuda(cudaEventCreate(&r.e1), "cudaEventCreate(trace)");
     check_cuda(cudaEventRecord(r.e1, st.stream), "cudaEventRecord(trace)");
     trace_.push_back(r);
+}
+
+void Engine::trace_split(Stage& st, const OpRec& first_part) {
+    trace_end(st, first_part);
+    trace_begin(st);
 }
 
 namespace {

@@ -48,6 +48,9 @@ struct EngineConfig {
     // local_count); 0 = all stages.  Remote neighbours are reached through CUDA IPC
     // (export_stage / connect_stage).
     int first_local = 0, local_count = 0;
+    // Activation recomputation: forwards keep only the stage input; each backward
+    // first re-runs the stage forward (Recompute op, simulator.cpp:242-247).
+    bool recompute = false;
 };
 
 // Receive-side block of one stage, exported over CUDA IPC to its neighbours'
@@ -78,6 +81,12 @@ public:
     //   first: first backward since the last update (gradient buffer is overwritten)
     virtual void backward(int k, int wslot, int sslot, const void* g_in, void* g_out,
                           bool first, cudaStream_t s) = 0;
+    // Recompute op: re-run the forward of microbatch k (weights wslot, input x_in, the
+    // stage's ring slot; nullptr on stage 0) so that backward() finds its activations.
+    virtual void recompute(int k, int wslot, int sslot, const void* x_in, cudaStream_t s) {
+        (void)k, (void)wslot, (void)sslot, (void)x_in, (void)s;
+        throw Error("this stage model does not support activation recomputation");
+    }
     // Fused optimizer: new version into dst_slot from src_slot (may alias).
     virtual void update(int src_slot, int dst_slot, int grad_count, cudaStream_t s) = 0;
     // Host <-> device weights of one version slot, in the model's public layout.
@@ -224,6 +233,7 @@ private:
     };
     void trace_begin(Stage& st);
     void trace_end(Stage& st, const OpRec& op);
+    void trace_split(Stage& st, const OpRec& first_part);  // close first_part, open the rest
 
     void issue_forward(Stage& st, const OpRec& op);
     void issue_backward(Stage& st, const OpRec& op);

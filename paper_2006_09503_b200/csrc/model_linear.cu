@@ -168,6 +168,12 @@ public:
                                    cudaMemcpyDeviceToHost, s), "D2H loss");
     }
 
+    // Recompute op: the forward again into the same stash slot (the output goes to a
+    // scratch row block; the loss path reads out_).  Bit-identical by construction.
+    void recompute(int k, int wslot, int sslot, const void* x_in, cudaStream_t s) override {
+        forward(k, wslot, sslot, x_in, gtmp_, s);
+    }
+
     void forward(int k, int wslot, int sslot, const void* x_in, void* x_out, cudaStream_t s) override {
         const double* cur = stage0_ ? data_x(k) : static_cast<const double*>(x_in);
         xin_[static_cast<size_t>(sslot)] = cur;

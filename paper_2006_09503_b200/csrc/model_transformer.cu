@@ -54,7 +54,7 @@ class TransformerStage final : public StageModel {
 public:
     TransformerStage(const EngineConfig& c, int stage, int lo, int hi, int sslots, int wslots)
         : cfg_(c), stage_(stage), lo_(lo), layers_(hi - lo), first_(stage == 0), last_(stage == c.depth - 1),
-          sslots_(sslots), wslots_(wslots) {
+          sslots_(c.recompute ? 1 : sslots), wslots_(wslots), recompute_(c.recompute) {
         h_ = c.hidden;
         heads_ = c.heads;
         seq_ = c.seq_len;
@@ -81,7 +81,8 @@ public:
     size_t boundary_bytes() const override { return static_cast<size_t>(T_) * h_ * sizeof(bf16); }
     size_t weight_bytes_public() const override { return nparam_ * sizeof(float); }
     double version_bytes() const override { return static_cast<double>(nparam_) * sizeof(bf16); }
-    double stash_bytes() const override { return stash_bytes_; }
+    // with recomputation a microbatch's stash is its input (the ring slot)
+    double stash_bytes() const override { return recompute_ ? static_cast<double>(boundary_bytes()) : stash_bytes_; }
     int data_capacity() const override { return capacity_; }
     void bind_stream(cudaStream_t s) override { stream_ = s; }
     void grad_buffer(void** ptr, size_t* count, int* dtype) override {
@@ -183,9 +184,16 @@ public:
         }
     }
 
+    // With recomputation every microbatch shares stash slot 0: a Forward only produces
+    // its output (and loss); the Backward's Recompute refills the slot first.
+    void recompute(int k, int wslot, int sslot, const void* x_in, cudaStream_t s) override {
+        if (!recompute_) throw Error("recompute op on a stage built without activation recomputation");
+        forward(k, wslot, sslot, x_in, last_ ? nullptr : rc_out_, s);
+    }
+
     void forward(int k, int wslot, int sslot, const void* x_in, void* x_out, cudaStream_t s) override {
         const bf16* W = wbf_[wslot];
-        Slot& st = slots_[sslot];
+        Slot& st = slots_[recompute_ ? 0 : sslot];
         const bf16* cur;
         if (first_) {
             embed_fwd(data_ids(k), W + off_tok_, W + off_pos_, st.x[0], T_, seq_, h_, s);
@@ -222,7 +230,7 @@ public:
     void backward(int k, int wslot, int sslot, const void* g_in, void* g_out, bool first,
                   cudaStream_t s) override {
         const bf16* W = wbf_[wslot];
-        Slot& st = slots_[sslot];
+        Slot& st = slots_[recompute_ ? 0 : sslot];
         const float beta = first ? 0.0f : 1.0f;
         const bf16* g = static_cast<const bf16*>(g_in);
         if (last_) {
@@ -377,6 +385,7 @@ private:
                 st.logits = dalloc<bf16>(R * static_cast<size_t>(vp_));
             }
         }
+        if (recompute_ && !last_) rc_out_ = dalloc<bf16>(T * h);  // the Recompute's discarded output
         gA_ = dalloc<bf16>(T * h);
         gB_ = dalloc<bf16>(T * h);
         gX_ = dalloc<bf16>(T * h);
@@ -464,6 +473,8 @@ private:
     int stage_, lo_, layers_;
     bool first_, last_;
     int sslots_, wslots_;
+    bool recompute_ = false;
+    bf16* rc_out_ = nullptr;
     int h_ = 0, heads_ = 0, seq_ = 0, b_ = 0, vocab_ = 0, vp_ = 0, T_ = 0, R_ = 0, rows_per_seq_ = 0;
     cudaStream_t stream_ = nullptr;
     std::vector<void*> allocs_;
