@@ -201,7 +201,7 @@ def run_ours(args, c):
                    microbatch_size=c["b"], layers=c["layers"], hidden=c["hidden"], heads=c["heads"],
                    seq_len=c["seq"], vocab=c["vocab"], causal=int(c["causal"]), head_rows=c["head_rows"],
                    learning_rate=1e-3, momentum=0.9, seed=1234,  # replicas start identical
-                   local_stages=local_stages, recompute=args.recompute)
+                   local_stages=local_stages, recompute=args.recompute, optimizer=args.optimizer)
     eng.init_weights()
     my_stages = [s for s in range(depth) if eng.is_local(s)]
     has_loss = eng.is_local(depth - 1)
@@ -351,7 +351,7 @@ def run_ours(args, c):
                    "head_rows_per_seq": c["head_rows"] or c["seq"], "microbatch_size": c["b"],
                    "microbatches_m": m, "global_batch": width * c["b"] * m,
                    "parallelism": par, "inputs": "value: token batches resident in HBM; e2e: per-step host copies",
-                   "policy": "2bw", "recompute": bool(args.recompute),
+                   "policy": "2bw", "recompute": bool(args.recompute), "optimizer": args.optimizer,
                    "l2": "working set (activations >> 126 MB L2) exceeds L2 every step"},
         "e2e": {"value": round(value_e2e, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "wall_s": round(wall, 3),
@@ -383,6 +383,8 @@ def main():
     ap.add_argument("--config", default="bert-base", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adam"],
+                    help="WeightUpdate optimizer: the reference's momentum SGD (default) or Adam")
     ap.add_argument("--recompute", action="store_true",
                     help="activation recomputation (the planner's r flag): stash stage inputs only")
     ap.add_argument("--depth", type=int, default=0,

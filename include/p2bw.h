@@ -142,7 +142,16 @@ typedef struct {
      * a Forward keeps only the stage input, the Backward re-runs the stage forward
      * into one shared workspace first.  Numerics are unchanged. */
     int recompute;
+    /* Optimizer of the WeightUpdate op: P2BW_OPT_MOMENTUM_SGD is the reference's
+     * momentum SGD with (1 - beta) dampening (semantics.cpp:153-165); P2BW_OPT_ADAM is
+     * Adam with bias correction (the paper's optimizer, absent from
+     * the reference): beta1 = momentum, beta2, eps; transformer stages only. */
+    int optimizer;
+    double beta2;
+    double eps;
 } p2bw_desc;
+
+enum { P2BW_OPT_MOMENTUM_SGD = 0, P2BW_OPT_ADAM = 1 };
 
 typedef struct {
     int version_consistent; /* PipelinedResult::version_consistent */

@@ -190,8 +190,13 @@ def loss_fn(P: dict, ids: torch.Tensor, targets: torch.Tensor, spec: Spec) -> to
 
 
 def train(params: dict, spec: Spec, ids: np.ndarray, targets: np.ndarray, lr: float, beta: float,
-          m: int, T: int, delayed: bool = True, dtype=torch.float64):
+          m: int, T: int, delayed: bool = True, dtype=torch.float64, optimizer: str = "sgd",
+          beta2: float = 0.999, eps: float = 1e-8):
     """reference_loop (semantics.cpp:167-184) on the transformer loss.
+
+    optimizer "sgd": the reference's momentum SGD with dampening (semantics.cpp:153-165);
+    "adam": Adam with bias correction (beta1 = beta) -- the paper's optimizer
+    (PAPER.md:605-607), not in the reference: unpinned, restated here.
 
     ids: [m*T, b*seq] int, targets: [m*T, R] int.  Returns (trajectory of param
     dicts W^(0..T), per-microbatch losses measured at the weights each batch's
@@ -199,6 +204,7 @@ def train(params: dict, spec: Spec, ids: np.ndarray, targets: np.ndarray, lr: fl
     W = {k: torch.tensor(v, dtype=dtype) for k, v in params.items()}
     traj = [{k: v.clone() for k, v in W.items()}]
     vel = {k: torch.zeros_like(v) for k, v in W.items()}
+    vel2 = {k: torch.zeros_like(v) for k, v in W.items()}
     losses = []
     for t in range(1, T + 1):
         ev = traj[max(t - 2, 0) if delayed else t - 1]
@@ -209,14 +215,20 @@ def train(params: dict, spec: Spec, ids: np.ndarray, targets: np.ndarray, lr: fl
             loss = loss_fn(P, torch.as_tensor(ids[kk], dtype=torch.long),
                            torch.as_tensor(targets[kk], dtype=torch.long), spec)
             loss.backward()
-            losses.append(float(loss))
+            losses.append(float(loss.detach()))
             for k in grads:
                 if P[k].grad is not None:
                     grads[k] += P[k].grad
         for k in W:
             g = grads[k] / m
             vel[k] = beta * vel[k] + (1.0 - beta) * g
-            W[k] = W[k] + (-lr) * vel[k]
+            if optimizer == "adam":
+                vel2[k] = beta2 * vel2[k] + (1.0 - beta2) * g * g
+                mh = vel[k] / (1.0 - beta ** t)
+                vh = vel2[k] / (1.0 - beta2 ** t)
+                W[k] = W[k] - lr * mh / (torch.sqrt(vh) + eps)
+            else:
+                W[k] = W[k] + (-lr) * vel[k]
         traj.append({k: v.clone() for k, v in W.items()})
     return traj, np.array(losses)
 

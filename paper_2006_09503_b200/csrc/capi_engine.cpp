@@ -50,6 +50,15 @@ p2bw::EngineConfig config_from_desc(const p2bw_desc& dd) {
     c.first_local = d->first_local_stage;
     c.local_count = d->local_stages;
     c.recompute = d->recompute != 0;
+    c.optimizer = d->optimizer;
+    if (c.optimizer != P2BW_OPT_MOMENTUM_SGD && c.optimizer != P2BW_OPT_ADAM)
+        throw std::invalid_argument("unknown optimizer " + std::to_string(c.optimizer));
+    if (c.optimizer == P2BW_OPT_ADAM) {
+        c.beta2 = d->beta2;
+        c.eps = d->eps;
+        if (!(c.beta2 >= 0 && c.beta2 < 1) || !(c.eps > 0)) throw p2bw::Error("Adam needs beta2 in [0, 1) and eps > 0");
+        if (c.model_kind != P2BW_MODEL_TRANSFORMER) throw p2bw::Error("Adam is available for transformer stages only");
+    }
     if (c.lr < 0) throw p2bw::Error("learning rate must be >= 0");
     if (c.momentum < 0 || c.momentum >= 1) throw p2bw::Error("momentum must be in [0, 1)");
     return c;

@@ -51,6 +51,9 @@ struct EngineConfig {
     // Activation recomputation: forwards keep only the stage input; each backward
     // first re-runs the stage forward (Recompute op, simulator.cpp:242-247).
     bool recompute = false;
+    // WeightUpdate optimizer: P2BW_OPT_MOMENTUM_SGD (reference) or P2BW_OPT_ADAM
+    int optimizer = 0;
+    double beta2 = 0.999, eps = 1e-8;
 };
 
 // Receive-side block of one stage, exported over CUDA IPC to its neighbours'

@@ -115,6 +115,8 @@ public:
         }
         cast_f32_bf16(master_, wbf_[0], nparam_, s);
         check_cuda(cudaMemsetAsync(vel_, 0, nparam_ * sizeof(float), s), "memset vel");
+        if (vel2_) check_cuda(cudaMemsetAsync(vel2_, 0, nparam_ * sizeof(float), s), "memset vel2");
+        adam_step_ = 0;
         check_cuda(cudaStreamSynchronize(s), "init sync");
     }
 
@@ -123,6 +125,8 @@ public:
         check_cuda(cudaMemcpy(master_, host, bytes, cudaMemcpyHostToDevice), "H2D master");
         cast_f32_bf16(master_, wbf_[wslot], nparam_, stream_);
         check_cuda(cudaMemsetAsync(vel_, 0, nparam_ * sizeof(float), stream_), "memset vel");
+        if (vel2_) check_cuda(cudaMemsetAsync(vel2_, 0, nparam_ * sizeof(float), stream_), "memset vel2");
+        adam_step_ = 0;
         check_cuda(cudaStreamSynchronize(stream_), "load sync");
     }
 
@@ -296,6 +300,12 @@ public:
 
     void update(int src_slot, int dst_slot, int grad_count, cudaStream_t s) override {
         (void)src_slot;  // the fp32 master always holds the latest version
+        if (cfg_.optimizer == P2BW_OPT_ADAM) {
+            adam_update(master_, vel_, vel2_, grad_, wbf_[dst_slot], nparam_, 1.0f / grad_count,
+                        static_cast<float>(cfg_.lr), static_cast<float>(cfg_.momentum), static_cast<float>(cfg_.beta2),
+                        static_cast<float>(cfg_.eps), ++adam_step_, s);
+            return;
+        }
         sgd_momentum_update(master_, vel_, grad_, wbf_[dst_slot], nparam_, 1.0f / grad_count,
                             static_cast<float>(cfg_.lr), static_cast<float>(cfg_.momentum), s);
     }
@@ -348,6 +358,10 @@ private:
         const size_t T = static_cast<size_t>(T_), h = static_cast<size_t>(h_);
         master_ = dalloc<float>(nparam_);
         vel_ = dalloc<float>(nparam_);
+        if (cfg_.optimizer == P2BW_OPT_ADAM) {
+            vel2_ = dalloc<float>(nparam_);
+            check_cuda(cudaMemset(vel2_, 0, nparam_ * sizeof(float)), "memset");
+        }
         grad_ = dalloc<float>(nparam_);
         scratch_f32_ = dalloc<float>(nparam_);
         for (int i = 0; i < wslots_; ++i) wbf_.push_back(dalloc<bf16>(nparam_));
@@ -481,6 +495,8 @@ private:
     std::vector<LayerOff> lay_;
     size_t off_tok_ = 0, off_pos_ = 0, off_lnfg_ = 0, off_lnfb_ = 0, off_head_ = 0, nparam_ = 0;
     float *master_ = nullptr, *vel_ = nullptr, *grad_ = nullptr, *scratch_f32_ = nullptr;
+    float* vel2_ = nullptr;  // Adam second moment
+    int adam_step_ = 0;
     std::vector<bf16*> wbf_;
     std::vector<Slot> slots_;
     bf16 *gA_ = nullptr, *gB_ = nullptr, *gX_ = nullptr, *g3_ = nullptr, *g4_ = nullptr, *gH_ = nullptr;

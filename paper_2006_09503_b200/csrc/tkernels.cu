@@ -583,6 +583,32 @@ __global__ void k_sgd(float4* __restrict__ w, float4* __restrict__ v, const floa
     }
 }
 
+// Adam with bias correction: g = grad / count; m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+// w -= lr * (m / c1) / (sqrt(v / c2) + eps), c1 = 1 - b1^t, c2 = 1 - b2^t.
+__global__ void k_adam(float4* __restrict__ w, float4* __restrict__ m1, float4* __restrict__ m2,
+                       const float4* __restrict__ g, uint2* __restrict__ out, size_t n4, float inv_count, float lr,
+                       float b1, float b2, float eps, float inv_c1, float inv_c2) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float4 gg = g[i];
+        float4 a = m1[i], b = m2[i], ww = w[i];
+        const float gv[4] = {gg.x * inv_count, gg.y * inv_count, gg.z * inv_count, gg.w * inv_count};
+        float* ap = &a.x;
+        float* bp = &b.x;
+        float* wp = &ww.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            ap[e] = b1 * ap[e] + (1.0f - b1) * gv[e];
+            bp[e] = b2 * bp[e] + (1.0f - b2) * gv[e] * gv[e];
+            wp[e] -= lr * (ap[e] * inv_c1) / (sqrtf(bp[e] * inv_c2) + eps);
+        }
+        m1[i] = a;
+        m2[i] = b;
+        w[i] = ww;
+        out[i] = make_uint2(ptx::pack_bf16x2(ww.x, ww.y), ptx::pack_bf16x2(ww.z, ww.w));
+    }
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z += 0x9e3779b97f4a7c15ULL;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -753,6 +779,20 @@ void sgd_momentum_update(float* master, float* vel, const float* grad, bf16* out
                                               reinterpret_cast<const float4*>(grad),
                                               reinterpret_cast<uint2*>(out_bf16), n / 4, inv_count, lr, beta);
     check_cuda(cudaGetLastError(), "sgd_momentum_update");
+}
+
+void adam_update(float* master, float* m1, float* m2, const float* grad, bf16* out_bf16, size_t n, float inv_count,
+                 float lr, float b1, float b2, float eps, int step, cudaStream_t s) {
+    if (n % 4 != 0) throw Error("optimizer: parameter count must be a multiple of 4");
+    // reads w, m, v, g (16 B) + writes w, m, v (12 B) + bf16 copy (2 B) = 30 B/param
+    prof::Scope scope("optimizer", 0.0, 30.0 * static_cast<double>(n), 1, s);
+    const float inv_c1 = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(b1), step)));
+    const float inv_c2 = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(b2), step)));
+    k_adam<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<float4*>(master), reinterpret_cast<float4*>(m1),
+                                               reinterpret_cast<float4*>(m2), reinterpret_cast<const float4*>(grad),
+                                               reinterpret_cast<uint2*>(out_bf16), n / 4, inv_count, lr, b1, b2, eps,
+                                               inv_c1, inv_c2);
+    check_cuda(cudaGetLastError(), "adam_update");
 }
 
 void init_uniform(float* w, size_t n, uint64_t seed, uint64_t uid, float half_width, cudaStream_t s) {

@@ -67,6 +67,11 @@ void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float
 void sgd_momentum_update(float* master, float* vel, const float* grad, bf16* out_bf16, size_t n,
                          float inv_count, float lr, float beta, cudaStream_t s);
 
+// Adam (bias-corrected, step = 1-based update count) on the flat fp32 master; m1 / m2
+// are the first / second moment buffers.
+void adam_update(float* master, float* m1, float* m2, const float* grad, bf16* out_bf16, size_t n, float inv_count,
+                 float lr, float b1, float b2, float eps, int step, cudaStream_t s);
+
 // Deterministic synthetic init: w = (u - 0.5) * 2a with u from splitmix64(seed, uid, i).
 void init_uniform(float* w, size_t n, uint64_t seed, uint64_t uid, float half_width, cudaStream_t s);
 void fill_f32(float* w, size_t n, float v, cudaStream_t s);

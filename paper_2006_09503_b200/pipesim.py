@@ -205,7 +205,7 @@ class Desc(C.Structure):
                 ("vocab", C.c_int), ("causal", C.c_int), ("head_rows", C.c_int),
                 ("learning_rate", C.c_double), ("momentum", C.c_double), ("seed", C.c_ulonglong),
                 ("devices", C.POINTER(C.c_int)), ("first_local_stage", C.c_int), ("local_stages", C.c_int),
-                ("recompute", C.c_int)]
+                ("recompute", C.c_int), ("optimizer", C.c_int), ("beta2", C.c_double), ("eps", C.c_double)]
 
 
 STAGE_BLOB_BYTES = 128  # P2BW_STAGE_BLOB_BYTES
@@ -218,7 +218,7 @@ def profile_blocks(*, layers: int, hidden: int, heads: int, seq_len: int, vocab:
     times, weight and activation bytes measured on the current GPU, as the reference's
     profile document (profile.cpp:162-193) -- the input of plan() / partition_equal()."""
     d = Desc(MODEL_TRANSFORMER, int(PipelinePolicy.TwoBW), 1, 1, 1, 1, layers, 0, hidden, heads, seq_len,
-             vocab, causal, head_rows, 0.0, 0.0, seed, None, 0, 0, 0)
+             vocab, causal, head_rows, 0.0, 0.0, seed, None, 0, 0, 0, OPT_MOMENTUM_SGD, 0.999, 1e-8)
     sizes = (C.c_int * len(microbatch_sizes))(*microbatch_sizes)
     p = C.c_void_p()
     _call("p2bw_profile_blocks", C.byref(d), sizes, len(microbatch_sizes), warmup, iters, name.encode(),
@@ -233,6 +233,8 @@ class Counters(C.Structure):
 
 MODEL_LINEAR_F64 = 0
 MODEL_TRANSFORMER = 1
+OPT_MOMENTUM_SGD = 0  # P2BW_OPT_*
+OPT_ADAM = 1
 
 
 class Engine:
@@ -248,12 +250,13 @@ class Engine:
                  seq_len: int = 0, vocab: int = 0, causal: int = 0, head_rows: int = 0,
                  learning_rate: float = 0.0, momentum: float = 0.0, seed: int = 0,
                  devices: list[int] | None = None, local_stages: tuple[int, int] | None = None,
-                 recompute: bool = False):
+                 recompute: bool = False, optimizer: str = "sgd", beta2: float = 0.999, eps: float = 1e-8):
         self._devs = (C.c_int * depth)(*devices) if devices else None
         first, count = local_stages if local_stages is not None else (0, 0)
         d = Desc(model_kind, int(policy), depth, 1, microbatches, microbatch_size, layers, dim, hidden,
                  heads, seq_len, vocab, causal, head_rows, learning_rate, momentum, seed,
-                 C.cast(self._devs, C.POINTER(C.c_int)) if self._devs else None, first, count, int(recompute))
+                 C.cast(self._devs, C.POINTER(C.c_int)) if self._devs else None, first, count, int(recompute),
+                 {"sgd": OPT_MOMENTUM_SGD, "adam": OPT_ADAM}[optimizer], beta2, eps)
         self.h = C.c_void_p()
         _call("p2bw_engine_create", C.byref(d), C.byref(self.h))
         self.depth = depth

@@ -82,3 +82,40 @@ def test_depths_agree_with_each_other():
         st = TO.unflatten_stage(f4[s], spec, 4, s)
         for name, v in st.items():
             assert np.allclose(v, full1[name], rtol=2e-2, atol=2e-4), (s, name)
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_transformer_2bw_adam_matches_delayed_oracle(depth):
+    """Adam on the WeightUpdate op (the paper's optimizer, not in the
+    reference): the 2BW pipeline against the oracle's delay-1 loop with Adam."""
+    spec = TO.Spec(layers=2, hidden=128, heads=2, seq=128, vocab=500, batch=2, causal=True, head_rows=0)
+    m, T, lr, b1, b2, eps, seed = 2, 4, 2e-3, 0.9, 0.99, 1e-8, 77
+    ids, tg = TO.synthetic_batch(spec, m * T, seed + 1)
+    eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
+                   microbatch_size=spec.batch, layers=spec.layers, hidden=spec.hidden, heads=spec.heads,
+                   seq_len=spec.seq, vocab=spec.vocab, causal=1, learning_rate=lr, momentum=b1, seed=seed,
+                   optimizer="adam", beta2=b2, eps=eps)
+    eng.init_weights()
+    eng.set_data(ids, tg, 1, m * T)
+    eng.run_schedule(T)
+    eng.sync()
+    losses = eng.losses(1, m * T)
+    finals = [eng.read_master(s) for s in range(depth)]
+    eng.close()
+    params = TO.init_params(spec, seed)
+    traj, ref_losses = TO.train(params, spec, ids, tg, lr, b1, m, T, delayed=True, optimizer="adam", beta2=b2,
+                                eps=eps)
+    _, sgd_losses = TO.train(params, spec, ids, tg, lr, b1, m, T, delayed=True)
+    assert np.all(np.abs(losses - ref_losses) <= LOSS_RTOL * np.abs(ref_losses)), (losses, ref_losses)
+    assert np.max(np.abs(ref_losses - sgd_losses)) > 5 * np.max(np.abs(losses - ref_losses))  # Adam is visible
+    for s in range(depth):
+        w0 = TO.flatten_stage(params, spec, depth, s).astype(np.float64)
+        ref = TO.flatten_stage({k: v.numpy() for k, v in traj[-1].items()}, spec, depth, s).astype(np.float64)
+        d_gpu, d_ref = finals[s] - w0, ref - w0
+        assert np.linalg.norm(d_gpu - d_ref) <= 0.1 * np.linalg.norm(d_ref)
+
+
+def test_adam_rejected_on_linear_chain():
+    with pytest.raises(Exception, match="transformer stages only"):
+        P.Engine(model_kind=P.MODEL_LINEAR_F64, policy=P.PipelinePolicy.TwoBW, depth=1, microbatches=1,
+                 microbatch_size=2, layers=2, dim=4, learning_rate=0.1, momentum=0.9, optimizer="adam")
