@@ -119,3 +119,24 @@ def test_adam_rejected_on_linear_chain():
     with pytest.raises(Exception, match="transformer stages only"):
         P.Engine(model_kind=P.MODEL_LINEAR_F64, policy=P.PipelinePolicy.TwoBW, depth=1, microbatches=1,
                  microbatch_size=2, layers=2, dim=4, learning_rate=0.1, momentum=0.9, optimizer="adam")
+
+
+def test_transformer_1f1b_weight_stashing():
+    """PipeDream-1F1B on the transformer: one update per microbatch,
+    weight stashing (a microbatch's backward uses the version its forward used,
+    semantics.cpp:307-310) with at most d + 1 live versions; the version bookkeeping
+    itself is pinned bit-exactly on the linear chain (test_engine_linear_gpu)."""
+    spec = TO.Spec(layers=4, hidden=128, heads=2, seq=128, vocab=500, batch=2, causal=True, head_rows=0)
+    depth, m, T = 4, 4, 3
+    ids, tg = TO.synthetic_batch(spec, m * T, 5)
+    eng = make_engine(spec, depth, m, 0.05, 0.9, 3, policy=P.PipelinePolicy.PipeDream1F1B)
+    eng.init_weights()
+    eng.set_data(ids, tg, 1, m * T)
+    eng.run_schedule(T)
+    eng.sync()
+    losses = eng.losses(1, m * T)
+    c = eng.counters()
+    eng.close()
+    assert c.version_consistent
+    assert 2 <= c.max_versions_held <= depth + 1
+    assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
