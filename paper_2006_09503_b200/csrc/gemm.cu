@@ -9,11 +9,13 @@
 //   dgrad    dX = dY . W      A = dY (K-major),  B = W (MN-major)
 //   wgrad    dW += dY^T . X   A = dY (MN-major), B = X (MN-major), fp32 += epilogue
 //
-// Roles (256 threads, 1 CTA per SM, grid = min(tiles, #SMs), static round-robin tiles):
+// Roles (384 threads, 1 CTA per SM, grid = min(tiles, #SMs), static round-robin tiles):
 //   warp 0  : TMA producer  (one lane)   global -> SMEM ring of kStages stages
 //   warp 1  : MMA issuer    (one lane)   tcgen05.mma 128 x BN x 16, commit -> mbarriers
 //   warp 2  : TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
-//   warps 4-7: epilogue     tcgen05.ld -> registers -> fused bias/GELU/residual -> global
+//   warps 4-11: epilogue    tcgen05.ld -> registers -> fused bias/GELU/residual -> global
+//                           (two warps per TMEM lane quarter on alternate 64-column
+//                           chunks: the GELU / dGELU epilogues outran the mainloop)
 // The epilogue of tile i overlaps the main loop of tile i+1 through the two TMEM buffers.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -36,7 +38,11 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes = one swizzle row
-constexpr int kThreads = 256;
+// Epilogue warps per CTA (kEW): 4 (one per TMEM lane quarter) for the plain bf16 and
+// fp32 (wgrad) stores, 8 (two per quarter on alternate 64-column chunks) for the GELU /
+// dGELU / residual epilogues, which outran the mainloop with 4 (fc1 forward 670 vs
+// 1145 TF/s plain).  More epilogue SMEM costs stages, hence the split.
+__host__ __device__ constexpr int gemm_threads(int kEW) { return 128 + 32 * kEW; }
 constexpr int kEpiBuf = 32 * 128;  // one staging buffer: 32 rows x 128 B (TMA box, SW128)
 
 // kCl == 2 is the CTA-pair (cta_group::2) mode: each CTA holds its own 128 rows of A
@@ -44,13 +50,13 @@ constexpr int kEpiBuf = 32 * 128;  // one staging buffer: 32 rows x 128 B (TMA b
 // two such pairs side by side along N sharing their A rows: each CTA TMA-multicasts
 // half of its A tile into itself and the matching CTA of the other pair, which
 // halves the L2 -> SMEM bytes of A (the GEMMs are L2-feed bound at 256 x 256 tiles).
-template <int BN, int kCl>
+template <int BN, int kCl, int kEW>
 struct GemmCfg {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kBBytes = (BN / (kCl >= 2 ? 2 : 1)) * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = BN == 128 ? 256 : 512;  // 2 x BN accumulator columns, a power of two
-    static constexpr int kEpiBytes = 4 * 2 * kEpiBuf;  // 4 epilogue warps x 2 buffers
+    static constexpr int kEpiBytes = kEW * 2 * kEpiBuf;  // epilogue warps x 2 buffers
     static constexpr int kFixed = kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int kStages0 = (227 * 1024 - kFixed) / kStageBytes;
     static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
@@ -93,11 +99,11 @@ struct EpiMaps {
 // B tile into its SMEM (completing on the leader's full barrier), the accumulator
 // rows land in each CTA's own TMEM, and both epilogues release the leader's TMEM
 // buffer through remote mbarrier arrivals.
-template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl, int kEW>
+__global__ void __launch_bounds__(gemm_threads(kEW), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ EpiMaps em, const KParams p) {
-    using Cfg = GemmCfg<BN, kCl>;
+    using Cfg = GemmCfg<BN, kCl, kEW>;
     constexpr int S = Cfg::kStages;
     static_assert(!(kBMN && kCl >= 2 && (BN / 2) % 64 != 0), "MN-major B halves must be whole 64-column atoms");
     constexpr bool kPair = kCl >= 2;        // cta_group::2 MMAs over a CTA pair
@@ -112,8 +118,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty_bar = full_bar + S;
     uint64_t* tfull_bar = empty_bar + S;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;  // [2]
-    uint64_t* aux_bar = tempty_bar + 2;    // [4] per epilogue warp
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4);
+    uint64_t* aux_bar = tempty_bar + 2;    // [kEW] per epilogue warp
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEW);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -143,9 +149,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull_bar[i], 1);
-            ptx::mbar_init(&tempty_bar[i], kPair ? 8 : 4);  // pair mode: both CTAs' epilogues
+            ptx::mbar_init(&tempty_bar[i], kPair ? 2 * kEW : kEW);  // pair: both CTAs' epilogues
         }
-        for (int i = 0; i < 4; ++i) ptx::mbar_init(&aux_bar[i], 1);
+        for (int i = 0; i < kEW; ++i) ptx::mbar_init(&aux_bar[i], 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) {
@@ -293,9 +299,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Epilogue: warp q owns tile rows [32q, 32q+32) (its TMEM lane quarter).  Each
         // chunk of 128 B per row (64 bf16 / 32 fp32 columns) goes TMEM -> registers ->
         // fused math -> swizzled SMEM -> one TMA bulk-tensor store (or reduce-add).
-        const int q = warp & 3;
+        const int q = warp & 3;           // TMEM lane quarter (warp % 4, as tcgen05.ld requires)
+        const int ew = warp - 4;          // epilogue warp index
+        const int ch = ew >> 2;           // which alternate chunks of the tile's columns
         const GemmEpilogue& e = p.epi;
-        uint8_t* ebuf = s_epi + q * 2 * kEpiBuf;
+        uint8_t* ebuf = s_epi + ew * 2 * kEpiBuf;
         constexpr bool kF32 = kKind == EpiKind::StoreF32;
         constexpr int W = kF32 ? 32 : 64;  // columns per chunk
         const bool need_aux = kKind == EpiKind::DGeluBF16 || (kKind == EpiKind::StoreBF16 && e.residual != nullptr);
@@ -315,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t tbase =
                 tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-            for (int c = 0; c < BN / W; ++c) {
+            for (int c = ch; c < BN / W; c += kEW / 4) {
                 const int col0 = n0 + c * W;
                 if (col0 >= p.n || r0 >= p.m) continue;  // warp-uniform: whole chunk out of range
                 uint8_t* buf = ebuf + slot * kEpiBuf;
@@ -327,8 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (need_aux) {
                     if (lane == 0) {
-                        ptx::mbar_arrive_expect_tx(&aux_bar[q], kEpiBuf);
-                        ptx::tma_load_2d(buf, &em.aux, &aux_bar[q], col0, r0);
+                        ptx::mbar_arrive_expect_tx(&aux_bar[ew], kEpiBuf);
+                        ptx::tma_load_2d(buf, &em.aux, &aux_bar[ew], col0, r0);
                     }
                 }
                 float x[W];
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         *reinterpret_cast<float4*>(buf + ptx::swz128(lane, j)) =
                             make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
                 } else {
-                    if (need_aux) ptx::mbar_wait(&aux_bar[q], aux_phase), aux_phase ^= 1;
+                    if (need_aux) ptx::mbar_wait(&aux_bar[ew], aux_phase), aux_phase ^= 1;
                     if (kKind == EpiKind::StoreBF16 && e.bias != nullptr) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
@@ -515,10 +523,10 @@ CUtensorMap make_map(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld
     return make_map_t(ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, inner, outer, ld_elems, 64, box_outer);
 }
 
-template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl>
+template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl, int kEW>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p, cudaStream_t s) {
-    using Cfg = GemmCfg<BN, kCl>;
-    auto kern = gemm_tc_kernel<BN, kAMN, kBMN, kKind, kCl>;
+    using Cfg = GemmCfg<BN, kCl, kEW>;
+    auto kern = gemm_tc_kernel<BN, kAMN, kBMN, kKind, kCl, kEW>;
     static std::atomic<uint32_t> configured{0};  // one attribute call per device
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
@@ -536,7 +544,7 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, con
     const int grid = kCl * (work < slots ? work : slots);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(gemm_threads(kEW));
     cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -553,9 +561,12 @@ template <int BN, bool kAMN, bool kBMN, int kCl>
 void dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p,
                   cudaStream_t s) {
     switch (p.epi.kind) {
-        case EpiKind::StoreBF16: launch<BN, kAMN, kBMN, EpiKind::StoreBF16, kCl>(ta, tb, em, p, s); break;
-        case EpiKind::StoreF32: launch<BN, kAMN, kBMN, EpiKind::StoreF32, kCl>(ta, tb, em, p, s); break;
-        case EpiKind::DGeluBF16: launch<BN, kAMN, kBMN, EpiKind::DGeluBF16, kCl>(ta, tb, em, p, s); break;
+        case EpiKind::StoreBF16:
+            if (p.epi.gelu || p.epi.residual) launch<BN, kAMN, kBMN, EpiKind::StoreBF16, kCl, 8>(ta, tb, em, p, s);
+            else launch<BN, kAMN, kBMN, EpiKind::StoreBF16, kCl, 4>(ta, tb, em, p, s);
+            break;
+        case EpiKind::StoreF32: launch<BN, kAMN, kBMN, EpiKind::StoreF32, kCl, 4>(ta, tb, em, p, s); break;
+        case EpiKind::DGeluBF16: launch<BN, kAMN, kBMN, EpiKind::DGeluBF16, kCl, 8>(ta, tb, em, p, s); break;
     }
 }
 

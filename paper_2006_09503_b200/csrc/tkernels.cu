@@ -166,12 +166,11 @@ __global__ void __launch_bounds__(256) k_colstats(const bf16* __restrict__ dy, c
     const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
     float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (col < n) {
+        if constexpr (kLn) {
 #pragma unroll 4
-        for (int r = r0 + rl; r < r1; r += 8) {
-            float g[8];
-            load8(dy + static_cast<size_t>(r) * ld + col, g);
-            if constexpr (kLn) {
-                float xv[8];
+            for (int r = r0 + rl; r < r1; r += 8) {
+                float g[8], xv[8];
+                load8(dy + static_cast<size_t>(r) * ld + col, g);
                 load8(x + static_cast<size_t>(r) * ld + col, xv);
                 const float mu = mean[r], rs = rstd[r];
 #pragma unroll
@@ -179,7 +178,28 @@ __global__ void __launch_bounds__(256) k_colstats(const bf16* __restrict__ dy, c
                     a0[q] = fmaf(g[q], (xv[q] - mu) * rs, a0[q]);
                     a1[q] += g[q];
                 }
-            } else {
+            }
+        } else {
+            // eight rows' 16-byte vectors in flight per thread (the pass is latency-bound)
+            int r = r0 + rl;
+            for (; r + 56 < r1; r += 64) {
+                uint4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const uint4*>(dy + static_cast<size_t>(r + 8 * u) * ld + col);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float2 f = ptx::unpack_bf16x2(w[t]);
+                        a0[2 * t] += f.x;
+                        a0[2 * t + 1] += f.y;
+                    }
+                }
+            }
+            for (; r < r1; r += 8) {
+                float g[8];
+                load8(dy + static_cast<size_t>(r) * ld + col, g);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) a0[q] += g[q];
             }
@@ -200,10 +220,10 @@ __global__ void __launch_bounds__(256) k_colstats(const bf16* __restrict__ dy, c
     }
 }
 
-// Row blocks so that the grid has >= ~4 CTAs per SM; each block still sees >= 16 rows.
+// Row blocks so that the grid fills every SM with 8 CTAs; each block still sees >= 16 rows.
 int colsum_row_blocks(int rows, int n) {
     const int col_blocks = (n + 255) / 256;
-    const int want = (4 * 148 + col_blocks - 1) / col_blocks;
+    const int want = (8 * 148 + col_blocks - 1) / col_blocks;
     return std::max(1, std::min(want, (rows + 15) / 16));
 }
 
@@ -274,207 +294,176 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
     }
 }
 
-// Fused LayerNorm backward.  Row part (warp per row):
+// Fused LayerNorm backward.  Row part:
 //   dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) (+ dres),  dxh = dy * g
-// Column part, accumulated in registers over the rows a warp visits and reduced
-// over the block's warps in SMEM -> one partial per block and statistic:
+// Column part, accumulated in registers over the rows a thread visits and reduced
+// over the CTA in SMEM -> one partial per CTA and statistic:
 //   stat 0: sum_r dy * xh  (d gamma)     stat 1: sum_r dy  (d beta)
 //   stat 2 (kSum): sum_r bf16(dx)  -- the bias gradient of the linear layer whose
 //                  output gradient dx is (saves a separate pass over dx).
-// dx may alias dy: each warp reads its whole row before writing it.  Row r goes
-// to warp r mod (grid warps): deterministic.
-// The column accumulators take most of the register file, so rows are not double-
-// buffered in registers: each warp cp.async-prefetches its NEXT row (x, dy, dres,
-// mean, rstd) into a private SMEM slot while it works on the current one, which
-// keeps a row's DRAM latency off the per-row dependency chain (the kernel was
-// latency-bound at ~1.4 TB/s with 3.5 rows per warp).  gamma is staged once per CTA.
-// 16 warps per SM for h <= 768; wide rows (more accumulators per lane) get 8 warps
-// and the full 255-register budget.
-__host__ __device__ constexpr int ln_bwd_threads(int nv) { return nv >= 4 ? 256 : 512; }
+// A row is spread over a GROUP of wpr = ceil(h / 256) warps, one 8-column vector per
+// lane, so each lane keeps only 8 columns of accumulators (24 registers) and a CTA of
+// 768 threads holds G = 24 / wpr rows in flight, each prefetching its next row into
+// registers while it works on the current one.  The two row sums are combined across
+// the group's warps through SMEM (named barrier per group, fixed order: every warp of
+// the group sees identical sums; deterministic).  dx may alias dy: each lane reads
+// its vector of a row before writing it.
+constexpr int kLnBwdThreads = 768;  // 85 registers per thread; G = 24 / wpr row groups
 
-// per-warp staging: 2 buffers x {x, dy, dres} rows (bf16) + {mean, rstd}
-__host__ __device__ constexpr int ln_bwd_buf_bytes(int h) { return 3 * h * 2 + 16; }
-inline size_t ln_bwd_smem_bytes(int nv, int h) {
-    const int warps = ln_bwd_threads(nv) / 32;
-    const size_t staging = static_cast<size_t>(warps) * 2 * ln_bwd_buf_bytes(h) + static_cast<size_t>(h) * 4;
-    const size_t red = static_cast<size_t>(warps) * h * 4;
-    return std::max(staging, red);
-}
+struct LnBwdShape {
+    int wpr;  // warps per row
+    int G;    // row groups per CTA
+};
 
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* g) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ float lds_f(uint32_t a) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-    return v;
+inline LnBwdShape ln_bwd_shape(int h) {
+    const int hv = h / 8;
+    const int wpr = (hv + 31) / 32;
+    int G = (kLnBwdThreads / 32) / wpr;
+    if (wpr > 1) G = std::min(G, 15);  // named barriers 1..15
+    return {wpr, G};
 }
 
-template <int NV, bool kSum>
-__global__ void __launch_bounds__(ln_bwd_threads(NV), 1)
+inline size_t ln_bwd_smem_bytes(int h) {
+    const LnBwdShape sh = ln_bwd_shape(h);
+    return (static_cast<size_t>(sh.G) * h + static_cast<size_t>(sh.G) * 2 * sh.wpr * 2) * sizeof(float);
+}
+
+__device__ __forceinline__ void group_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <bool kSum>
+__global__ void __launch_bounds__(kLnBwdThreads, 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
-             bf16* dx, int rows, int h, float* __restrict__ part) {
-    extern __shared__ __align__(16) uint8_t ln_smem[];
-    float* red = reinterpret_cast<float*>(ln_smem);  // [kWarps][h], after the row loop
-    constexpr int kThreads = ln_bwd_threads(NV), kWarps = kThreads / 32;
+             bf16* dx, int rows, int h, int wpr, int G, float* __restrict__ part) {
+    extern __shared__ float ln_smem[];  // red [G][h], then the row-sum exchange [G][2][wpr][2]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = warp / wpr, wi = warp % wpr;
     const int hv = h / 8;
+    const int vi = wi * 32 + lane;  // my 8-column vector of every row
+    const bool act = grp < G && vi < hv;
     const bool has_res = dres != nullptr;
-    const int bufb = ln_bwd_buf_bytes(h);
-    const uint32_t s0 = ptx::smem_u32(ln_smem);
-    const uint32_t wbase = s0 + static_cast<uint32_t>(warp * 2 * bufb);
-    const uint32_t sgam = s0 + static_cast<uint32_t>(kWarps * 2 * bufb);  // gamma, fp32 [h]
-    for (int c = threadIdx.x; c < h; c += kThreads)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sgam + c * 4), "f"(__bfloat162float(g[c])) : "memory");
-    auto prefetch = [&](int r, int buf) {
-        const uint32_t b = wbase + static_cast<uint32_t>(buf * bufb);
-        const size_t ro = static_cast<size_t>(r) * h;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv) {
-                cp_async16(b + vi * 16, x + ro + vi * 8);
-                cp_async16(b + 2 * h + vi * 16, dy + ro + vi * 8);
-                if (has_res) cp_async16(b + 4 * h + vi * 16, dres + ro + vi * 8);
-            }
+    float* xs = ln_smem + static_cast<size_t>(G) * h;
+    float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (act) load8(g + vi * 8, gv);
+    float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0}, as[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    const int stride = gridDim.x * G;
+    int r = blockIdx.x * G + grp;
+    uint4 xp = z4, dp = z4, rp = z4;
+    float mu = 0.0f, rs = 0.0f;
+    if (grp < G && r < rows) {
+        const size_t o = static_cast<size_t>(r) * h + vi * 8;
+        if (act) {
+            xp = *reinterpret_cast<const uint4*>(x + o);
+            dp = *reinterpret_cast<const uint4*>(dy + o);
+            if (has_res) rp = *reinterpret_cast<const uint4*>(dres + o);
         }
-        if (lane == 0) {
-            cp_async4(b + 6 * h, mean + r);
-            cp_async4(b + 6 * h + 4, rstd + r);
-        }
-        cp_async_commit();
-    };
-    float ag[NV][8], ab[NV][8], as[kSum ? NV : 1][8];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            ag[i][q] = 0.0f;
-            ab[i][q] = 0.0f;
-            if constexpr (kSum) as[i][q] = 0.0f;
-        }
+        mu = mean[r];
+        rs = rstd[r];
     }
-    __syncthreads();  // gamma staged
-    const int stride = gridDim.x * kWarps;
-    int r = blockIdx.x * kWarps + warp;
-    if (r < rows) prefetch(r, 0);
-    for (int it = 0; r < rows; r += stride, ++it) {
-        const int buf = it & 1;
-        if (r + stride < rows) prefetch(r + stride, buf ^ 1);
-        else cp_async_commit();  // empty group: keeps "all but the newest" == this row
-        cp_async_wait<1>();
-        __syncwarp();
-        const uint32_t b = wbase + static_cast<uint32_t>(buf * bufb);
-        const float mu = lds_f(b + 6 * h), rs = lds_f(b + 6 * h + 4);
-        uint4 xp[NV], dp[NV];
+    for (int it = 0; grp < G && r < rows; r += stride, ++it) {
+        // prefetch the next row of this group (independent loads, in flight during the math)
+        uint4 nx = z4, nd = z4, nr = z4;
+        float nmu = 0.0f, nrs = 0.0f;
+        if (r + stride < rows) {
+            const size_t o = static_cast<size_t>(r + stride) * h + vi * 8;
+            if (act) {
+                nx = *reinterpret_cast<const uint4*>(x + o);
+                nd = *reinterpret_cast<const uint4*>(dy + o);
+                if (has_res) nr = *reinterpret_cast<const uint4*>(dres + o);
+            }
+            nmu = mean[r + stride];
+            nrs = rstd[r + stride];
+        }
+        float xh[8], dg[8];
         float s1 = 0.0f, s2 = 0.0f;
+        {
+            const uint32_t xw[4] = {xp.x, xp.y, xp.z, xp.w}, dw[4] = {dp.x, dp.y, dp.z, dp.w};
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv) {
-                xp[i] = lds_u4(b + vi * 16);
-                dp[i] = lds_u4(b + 2 * h + vi * 16);
+            for (int t = 0; t < 4; ++t) {
+                const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
+                xh[2 * t] = (xf.x - mu) * rs;
+                xh[2 * t + 1] = (xf.y - mu) * rs;
+                dg[2 * t] = df.x * gv[2 * t];
+                dg[2 * t + 1] = df.y * gv[2 * t + 1];
+                if (act) {  // column statistics (inactive lanes hold zero data anyway)
+                    ag[2 * t] = fmaf(df.x, xh[2 * t], ag[2 * t]);
+                    ag[2 * t + 1] = fmaf(df.y, xh[2 * t + 1], ag[2 * t + 1]);
+                    ab[2 * t] += df.x;
+                    ab[2 * t + 1] += df.y;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                s1 += dg[q];
+                s2 += dg[q] * xh[q];
             }
         }
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        if (wpr > 1) {
+            float* slot = xs + (static_cast<size_t>(grp) * 2 + (it & 1)) * wpr * 2;
+            if (lane == 0) {
+                slot[wi * 2] = s1;
+                slot[wi * 2 + 1] = s2;
+            }
+            group_bar(1 + grp, wpr * 32);
+            s1 = 0.0f;
+            s2 = 0.0f;
+            for (int w = 0; w < wpr; ++w) {
+                s1 += slot[w * 2];
+                s2 += slot[w * 2 + 1];
+            }
+        }
+        const float m1 = s1 / h, m2 = s2 / h;
+        if (act) {
+            float o[8];
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv) {
-                const uint32_t xw[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
-                const uint32_t dw[4] = {dp[i].x, dp[i].y, dp[i].z, dp[i].w};
-                const float4 g0 = ptx::lds_f4(sgam + vi * 32), g1 = ptx::lds_f4(sgam + vi * 32 + 16);
-                const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            for (int q = 0; q < 8; ++q) o[q] = rs * (dg[q] - m1 - xh[q] * m2);
+            if (has_res) {
+                const uint32_t rw[4] = {rp.x, rp.y, rp.z, rp.w};
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
-                    const float xh0 = (xf.x - mu) * rs, xh1 = (xf.y - mu) * rs;
-                    const float d0 = df.x * gv[2 * t], d1 = df.y * gv[2 * t + 1];
-                    s1 += d0 + d1;
-                    s2 += d0 * xh0 + d1 * xh1;
-                    ag[i][2 * t] = fmaf(df.x, xh0, ag[i][2 * t]);
-                    ag[i][2 * t + 1] = fmaf(df.y, xh1, ag[i][2 * t + 1]);
-                    ab[i][2 * t] += df.x;
-                    ab[i][2 * t + 1] += df.y;
+                    const float2 rf = ptx::unpack_bf16x2(rw[t]);
+                    o[2 * t] += rf.x;
+                    o[2 * t + 1] += rf.y;
                 }
             }
-        }
-        const float m1 = warp_sum(s1) / h, m2 = warp_sum(s2) / h;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv) {
-                const uint32_t xw[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
-                const uint32_t dw[4] = {dp[i].x, dp[i].y, dp[i].z, dp[i].w};
-                const float4 g0 = ptx::lds_f4(sgam + vi * 32), g1 = ptx::lds_f4(sgam + vi * 32 + 16);
-                const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-                float o[8];
+            const uint4 packed = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
+                                            ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
+            *reinterpret_cast<uint4*>(dx + static_cast<size_t>(r) * h + vi * 8) = packed;
+            if constexpr (kSum) {  // the bias gradient sums what the next GEMM reads: bf16(dx)
+                const uint32_t pw[4] = {packed.x, packed.y, packed.z, packed.w};
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
-                    o[2 * t] = rs * (df.x * gv[2 * t] - m1 - (xf.x - mu) * rs * m2);
-                    o[2 * t + 1] = rs * (df.y * gv[2 * t + 1] - m1 - (xf.y - mu) * rs * m2);
-                }
-                if (has_res) {
-                    const uint4 rp = lds_u4(b + 4 * h + vi * 16);
-                    const uint32_t rw[4] = {rp.x, rp.y, rp.z, rp.w};
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const float2 rf = ptx::unpack_bf16x2(rw[t]);
-                        o[2 * t] += rf.x;
-                        o[2 * t + 1] += rf.y;
-                    }
-                }
-                const uint4 packed = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
-                                                ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
-                *reinterpret_cast<uint4*>(dx + static_cast<size_t>(r) * h + vi * 8) = packed;
-                if constexpr (kSum) {  // the bias gradient sums what the next GEMM reads: bf16(dx)
-                    const uint32_t pw[4] = {packed.x, packed.y, packed.z, packed.w};
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const float2 pf = ptx::unpack_bf16x2(pw[t]);
-                        as[i][2 * t] += pf.x;
-                        as[i][2 * t + 1] += pf.y;
-                    }
+                    const float2 pf = ptx::unpack_bf16x2(pw[t]);
+                    as[2 * t] += pf.x;
+                    as[2 * t + 1] += pf.y;
                 }
             }
         }
-        __syncwarp();  // this buffer is the target of the prefetch two rows on
+        xp = nx;
+        dp = nd;
+        rp = nr;
+        mu = nmu;
+        rs = nrs;
     }
-    cp_async_wait<0>();
-    __syncthreads();  // staging area becomes the reduction buffer
-    // block reduction over the warps, one statistic at a time, fixed order
+    // CTA reduction over the row groups, one statistic at a time, fixed order
     for (int st = 0; st < (kSum ? 3 : 2); ++st) {
+        __syncthreads();
+        if (act) {
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const int vi = lane + 32 * i;
-            if (vi < hv) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    red[warp * h + vi * 8 + q] = st == 0 ? ag[i][q] : (st == 1 ? ab[i][q] : as[kSum ? i : 0][q]);
-            }
+            for (int q = 0; q < 8; ++q)
+                ln_smem[static_cast<size_t>(grp) * h + vi * 8 + q] = st == 0 ? ag[q] : (st == 1 ? ab[q] : as[q]);
         }
         __syncthreads();
-        for (int c = threadIdx.x; c < h; c += kThreads) {
+        for (int c = threadIdx.x; c < h; c += blockDim.x) {
             float sum = 0.0f;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) sum += red[w * h + c];
+            for (int gg = 0; gg < G; ++gg) sum += ln_smem[static_cast<size_t>(gg) * h + c];
             part[(static_cast<size_t>(st) * gridDim.x + blockIdx.x) * h + c] = sum;
         }
-        __syncthreads();
     }
 }
 
@@ -699,33 +688,21 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 
 size_t layernorm_bwd_scratch_floats(int rows, int h) { return static_cast<size_t>(ln_bwd_blocks(rows)) * h * 3; }
 
-template <int NV, bool kSum>
+template <bool kSum>
 void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
-    constexpr int kThreads = ln_bwd_threads(NV);
-    const size_t smem = ln_bwd_smem_bytes(NV, h);
+    const LnBwdShape sh = ln_bwd_shape(h);
+    const size_t smem = ln_bwd_smem_bytes(h);
     static std::atomic<uint32_t> configured{0};
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     if ((configured.load() & (1u << (dev & 31))) == 0) {
-        check_cuda(cudaFuncSetAttribute(k_ln_bwd<NV, kSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ln_bwd_smem_bytes(NV, NV * 256))),
+        check_cuda(cudaFuncSetAttribute(k_ln_bwd<kSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ln_bwd_smem_bytes(2048))),
                    "cudaFuncSetAttribute(ln bwd smem)");
         configured.fetch_or(1u << (dev & 31));
     }
-    k_ln_bwd<NV, kSum><<<grid, kThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, part);
-}
-
-template <bool kSum>
-void dispatch_ln_bwd(int nv, int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd,
-                     const bf16* g, const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
-    switch (nv) {
-        case 1: launch_ln_bwd<1, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
-        case 2: launch_ln_bwd<2, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
-        case 3: launch_ln_bwd<3, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
-        case 4: launch_ln_bwd<4, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
-        default: launch_ln_bwd<8, kSum>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s); break;
-    }
+    k_ln_bwd<kSum><<<grid, kLnBwdThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, sh.wpr, sh.G, part);
 }
 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
@@ -734,9 +711,8 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
     prof::Scope scope("layernorm_bwd", 0.0, (dres ? 8.0 : 6.0) * rows * h + 8.0 * rows, 2, s);
     const int grid = ln_bwd_blocks(rows);
-    const int nv = (h / 8 + 31) / 32;
-    if (dsum) dispatch_ln_bwd<true>(nv, grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
-    else dispatch_ln_bwd<false>(nv, grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
+    if (dsum) launch_ln_bwd<true>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
+    else launch_ln_bwd<false>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
     ReduceOut o{{dg, db, dsum}};
     k_reduce_parts<<<dim3((h + 7) / 8, dsum ? 3 : 2), 256, 0, s>>>(scratch, grid, h, o, overwrite ? 1 : 0);
     check_cuda(cudaGetLastError(), "layernorm_bwd");
