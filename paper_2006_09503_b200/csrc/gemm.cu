@@ -63,19 +63,24 @@ struct GemmCfg {
     static constexpr int kSmemBytes = kStages * kStageBytes + kFixed;
 };
 
+// tanh-GELU and its derivative in the fewest FP ops (the epilogue is issue-bound):
+//   u = x (k0 + k0 k1 x^2), t = tanh(u), gelu = 0.5 x (1 + t)
+//   gelu' = 0.5 (1 + t) + 0.5 x (1 - t^2) (k0 + 3 k0 k1 x^2)
 __device__ __forceinline__ float gelu_fwd(float x) {
-    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    constexpr float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
     float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(k0 * (x + k1 * x * x * x)));
-    return 0.5f * x * (1.0f + t);
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(x * fmaf(x * x, k01, k0)));
+    const float hx = 0.5f * x;
+    return fmaf(hx, t, hx);
 }
 
 __device__ __forceinline__ float gelu_bwd(float x) {
-    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    constexpr float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
     const float x2 = x * x;
     float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(k0 * (x + k1 * x * x2)));
-    return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x2);
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(x * fmaf(x2, k01, k0)));
+    const float a = 0.5f * x * fmaf(x2, 3.0f * k01, k0);
+    return fmaf(a, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
 }
 
 struct KParams {
@@ -345,12 +350,16 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                     ptx::tmem_ld_32x32b_x32(tbase + c * W, v);
                     ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(v[j]) * e.alpha;
+                    for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(v[j]);
                     if constexpr (W == 64) {
                         ptx::tmem_ld_32x32b_x32(tbase + c * W + 32, v);
                         ptx::tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) x[32 + j] = __uint_as_float(v[j]) * e.alpha;
+                        for (int j = 0; j < 32; ++j) x[32 + j] = __uint_as_float(v[j]);
+                    }
+                    if (e.alpha != 1.0f) {  // warp-uniform; the stage GEMMs all use alpha 1
+#pragma unroll
+                        for (int j = 0; j < W; ++j) x[j] *= e.alpha;
                     }
                 }
                 if constexpr (kF32) {

@@ -317,7 +317,8 @@ struct LnBwdShape {
 
 inline LnBwdShape ln_bwd_shape(int h) {
     const int hv = h / 8;
-    const int wpr = (hv + 31) / 32;
+    int wpr = (hv + 31) / 32;
+    if (wpr > 4) wpr = 8;  // instantiated group widths: 1, 2, 3, 4, 8
     int G = (kLnBwdThreads / 32) / wpr;
     if (wpr > 1) G = std::min(G, 15);  // named barriers 1..15
     return {wpr, G};
@@ -332,11 +333,11 @@ __device__ __forceinline__ void group_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-template <bool kSum>
+template <bool kSum, int wpr>
 __global__ void __launch_bounds__(kLnBwdThreads, 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
-             bf16* dx, int rows, int h, int wpr, int G, float* __restrict__ part) {
+             bf16* dx, int rows, int h, int G, float* __restrict__ part) {
     extern __shared__ float ln_smem[];  // red [G][h], then the row-sum exchange [G][2][wpr][2]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = warp / wpr, wi = warp % wpr;
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     const int vi = wi * 32 + lane;  // my 8-column vector of every row
     const bool act = grp < G && vi < hv;
     const bool has_res = dres != nullptr;
+    const float inv_h = 1.0f / static_cast<float>(h);
     float* xs = ln_smem + static_cast<size_t>(G) * h;
     float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (act) load8(g + vi * 8, gv);
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
         }
         s1 = warp_sum(s1);
         s2 = warp_sum(s2);
-        if (wpr > 1) {
+        if constexpr (wpr > 1) {
             float* slot = xs + (static_cast<size_t>(grp) * 2 + (it & 1)) * wpr * 2;
             if (lane == 0) {
                 slot[wi * 2] = s1;
@@ -412,12 +414,13 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
             group_bar(1 + grp, wpr * 32);
             s1 = 0.0f;
             s2 = 0.0f;
+#pragma unroll
             for (int w = 0; w < wpr; ++w) {
                 s1 += slot[w * 2];
                 s2 += slot[w * 2 + 1];
             }
         }
-        const float m1 = s1 / h, m2 = s2 / h;
+        const float m1 = s1 * inv_h, m2 = s2 * inv_h;
         if (act) {
             float o[8];
 #pragma unroll
@@ -693,16 +696,19 @@ void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, c
                    const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
     const LnBwdShape sh = ln_bwd_shape(h);
     const size_t smem = ln_bwd_smem_bytes(h);
-    static std::atomic<uint32_t> configured{0};
-    int dev = 0;
-    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    if ((configured.load() & (1u << (dev & 31))) == 0) {
-        check_cuda(cudaFuncSetAttribute(k_ln_bwd<kSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ln_bwd_smem_bytes(2048))),
-                   "cudaFuncSetAttribute(ln bwd smem)");
-        configured.fetch_or(1u << (dev & 31));
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024)
+            check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                       "cudaFuncSetAttribute(ln bwd smem)");
+        kern<<<grid, kLnBwdThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, sh.G, part);
+    };
+    switch (sh.wpr) {
+        case 1: go(k_ln_bwd<kSum, 1>); break;
+        case 2: go(k_ln_bwd<kSum, 2>); break;
+        case 3: go(k_ln_bwd<kSum, 3>); break;
+        case 4: go(k_ln_bwd<kSum, 4>); break;
+        default: go(k_ln_bwd<kSum, 8>); break;
     }
-    k_ln_bwd<kSum><<<grid, kLnBwdThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, sh.wpr, sh.G, part);
 }
 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
