@@ -5,8 +5,8 @@
 //
 //   UMMA  S^T  = K_j Q_i^T          128 x 128 fp32, TMEM [0, 128)
 //   UMMA  dP^T = V_j dO_i^T         TMEM [128, 256)
-//   SIMT  P^T  = exp(S^T/8 - lse_i), dS^T = P^T (dP^T - delta_i)   (8 warps, thread =
-//         key row, warp half = 64 query columns); P^T goes back into TMEM as packed
+//   SIMT  P^T  = exp(S^T/8 - lse_i), dS^T = P^T (dP^T - delta_i)   (16 warps, thread =
+//         key row, warp = 32 query columns); P^T goes back into TMEM as packed
 //         bf16 [448, 512), dS^T into SMEM in the UMMA K-major SW128 layout
 //   UMMA  dV_j += P^T dO_i          TMEM [256, 320)   (A = P^T from TMEM, dO_i MN-major)
 //   UMMA  dK_j += dS^T Q_i          TMEM [320, 384)   (Q_i read MN-major)
@@ -14,8 +14,9 @@
 //   flush dQ_i|j: TMEM -> SMEM (SW128) -> TMA reduce-add into an fp32 dQ accumulator
 //         (L2-resident, zeroed by the delta kernel; k_attn_dq_convert casts it)
 //
-// Warp roles (16 warps): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4-11
-// elementwise, 12-15 dQ flush + dK/dV epilogue of an item's last query tile.
+// Warp roles (24 warps): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4-19
+// elementwise (four per TMEM lane quarter, 32 query columns each), 20-23 dQ flush +
+// dK/dV epilogue of an item's last query tile.
 // K/V (per item) are double-buffered and Q/dO/lse/delta (per query tile) triple-
 // buffered, so TMA runs ahead across items; the S/dP MMAs of tile g+1 are issued before the dV/dK/dQ MMAs
 // of tile g, so the exp work of g+1 overlaps them.  The same SMEM bytes serve as
@@ -58,7 +59,8 @@ constexpr int oLse = oDQ + 4 * 4096;    // [kQS][128] f32
 constexpr int oDel = oLse + kQS * kT * 4; // [kQS][128] f32
 constexpr int oBar = oDel + kQS * kT * 4;
 constexpr int kSmem = oBar + 256 + 1024;
-constexpr int kThreads = 512;
+constexpr int kElemWarps = 16;  // four per TMEM lane quarter, 32 query columns each
+constexpr int kThreads = 128 + 32 * kElemWarps + 128;  // roles + elementwise + dQ flush
 constexpr float kLog2e = 1.4426950408889634f;
 
 // barrier indices
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&tm_dq);
         for (int q = 0; q < kNumBars; ++q) {
             const uint32_t cnt =
-                (q == bSFree || q == bDpFree || q == bPdsFull) ? 8 : (q == bDqFree || q == bKvAccFree) ? 4 : 1;
+                (q == bSFree || q == bDpFree || q == bPdsFull) ? kElemWarps : (q == bDqFree || q == bKvAccFree) ? 4 : 1;
             ptx::mbar_init(&bar[q], cnt);
         }
         ptx::fence_mbar_init();
@@ -228,14 +230,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (have) issue_mm2(prev);
         }
-    } else if (warp >= 4 && warp < 12) {
+    } else if (warp >= 4 && warp < 4 + kElemWarps) {
         // ---------------- elementwise: P^T, dS^T ----------------
         const int qw = warp & 3;
-        const int sel = (warp - 4) >> 2;  // query columns [64 sel, 64 sel + 64) = UMMA block sel
+        const int sel = (warp - 4) >> 2;  // query columns [32 sel, 32 sel + 32): UMMA block sel / 2
         const int r = qw * 32 + lane;     // key row within the tile
         const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
         const float sc = 0.125f * kLog2e;
-        const uint32_t drow = sbase + oDSt + sel * kTile + r * 128;
+        const uint32_t drow = sbase + oDSt + (sel >> 1) * kTile + r * 128;  // + 64 B for odd sel
         const bool dbg = g_attn_bwd_dbg != nullptr && warp == 4 && lane == 0;
         int g = 0;
         for (int n = blockIdx.x; n < items; n += gridDim.x) {
@@ -247,10 +249,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bmark(dbg, 0, g);
                 ptx::mbar_wait(&bar[bQFull + qb], (g / kQS) & 1);  // lse / delta visible
                 ptx::tc_fence_after();
-                uint32_t pp[32], dd[32];  // bf16x2: 64 P^T and 64 dS^T values of row r
+                uint32_t pp[16], dd[16];  // bf16x2: 32 P^T and 32 dS^T values of row r
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {  // 16 query columns per TMEM load (register budget)
-                    const int col0 = sel * 64 + c * 16;
+                for (int c = 0; c < 2; ++c) {  // 16 query columns per TMEM load (register budget)
+                    const int col0 = sel * 32 + c * 16;
                     uint32_t sv[16], dv[16];
                     ptx::tmem_ld_32x32b_x16(trow + tS + col0, sv);
                     ptx::tmem_ld_32x32b_x16(trow + tDP + col0, dv);
@@ -287,10 +289,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (g > 0) ptx::mbar_wait(&bar[bMm2], (g - 1) & 1);  // P^T / dS^T buffers free
                 bmark(dbg, 2, g);
                 ptx::tc_fence_after();
-                ptx::tmem_st_32x32b_x32(trow + tPT + sel * 32, pp);  // queries 64 sel .. +63 of key row r
+                ptx::tmem_st_32x32b_x16(trow + tPT + sel * 16, pp);  // queries 32 sel .. +31 of key row r
 #pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    const uint32_t off = static_cast<uint32_t>((ch ^ (r & 7)) << 4);
+                for (int ch = 0; ch < 4; ++ch) {
+                    const int cc = (sel & 1) * 4 + ch;  // 16-byte chunk of the 128-byte row
+                    const uint32_t off = static_cast<uint32_t>((cc ^ (r & 7)) << 4);
                     ptx::sts_u4(drow + off, dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]);
                 }
                 ptx::tmem_st_wait();
@@ -301,13 +304,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bmark(dbg, 3, g);
             }
         }
-    } else if (warp >= 12) {
+    } else if (warp >= 4 + kElemWarps) {
         // ---------------- dQ flush (TMA reduce-add) + dK / dV epilogue ----------------
         const int qw = warp & 3;
         const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
         uint8_t* stage = smem + oDQ + qw * 4096;
         const uint32_t sstage = ptx::smem_u32(stage);
-        const bool fdbg = g_attn_bwd_dbg != nullptr && warp == 12 && lane == 0;
+        const bool fdbg = g_attn_bwd_dbg != nullptr && warp == 4 + kElemWarps && lane == 0;
         int g = 0;
         for (int n = blockIdx.x; n < items; n += gridDim.x) {
             const Item it = item_of(n, bhn, nq, kCausal);
