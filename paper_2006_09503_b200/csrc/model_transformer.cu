@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "profiler.h"
 #include "tkernels.h"
 
 namespace p2bw {
@@ -74,6 +75,10 @@ public:
     }
 
     ~TransformerStage() override {
+        if (side_stream_) cudaStreamSynchronize(side_stream_);
+        for (cudaEvent_t e : ev_)
+            if (e) cudaEventDestroy(e);
+        if (side_stream_) cudaStreamDestroy(side_stream_);
         for (void* p : allocs_) cudaFree(p);
     }
 
@@ -237,12 +242,16 @@ public:
         Slot& st = slots_[recompute_ ? 0 : sslot];
         const float beta = first ? 0.0f : 1.0f;
         const bf16* g = static_cast<const bf16*>(g_in);
+        // With per-launch profiling on, the weight gradients stay on the main stream so
+        // that every kernel's event-timed duration is its own (the roofline report).
+        side_ = prof::enabled() ? s : side_stream_;
+        fork(kEvStart, s);  // the side stream follows the previous update (grad_ overwrite with beta 0)
         if (last_) {
             // logits now hold dloss/dlogits (softmax_xent ran in the forward)
             bf16* dxf = R_ < T_ ? gH_ : gA_;
             gemm_store_mn_b(st.logits, vp_, W + off_head_, h_, R_, h_, vp_, dxf, s, head_ws_,
                             static_cast<int64_t>(R_) * h_);
-            gemm_wgrad(st.logits, vp_, st.xf, h_, vp_, h_, R_, grad_ + off_head_, beta, s);
+            gemm_wgrad(st.logits, vp_, st.xf, h_, vp_, h_, R_, grad_ + off_head_, beta, side_);
             bf16* dsrc = dxf;
             bf16* dhead = R_ < T_ ? gB_ : gA_;
             // the LNf gradient is the top layer's FC2 output gradient: its column sum is
@@ -256,35 +265,52 @@ public:
             }
             g = gA_;
         }
+        // Weight gradients run on a side stream, concurrently with the dgrad / attention /
+        // LayerNorm chain of the main stream (they are off the critical path and fill
+        // the ragged last waves of the main chain's kernels).  fork(e): the side stream
+        // waits for main's progress; done(e) marks a side task; wait_side(e) holds main
+        // before it overwrites a buffer that side task reads.
         for (int l = layers_ - 1; l >= 0; --l) {
             const LayerOff& o = lay_[l];
             const bf16* x = l == 0 ? st.xin0 : st.x[l];
+            fork(kEvG, s);  // g (this layer's output gradient) is ready
             // FC2 (+ GELU'): du = (g W2) * gelu'(u)
+            wait_side(kEvDoneB, s);  // g4_ free (previous layer's W1 / b1 gradients)
             gemm_dgelu(g, h_, W + o.w2, 4 * h_, T_, 4 * h_, h_, st.u[l], g4_, s);
-            gemm_wgrad(g, h_, st.a[l], 4 * h_, h_, 4 * h_, T_, grad_ + o.w2, beta, s);
+            gemm_wgrad(g, h_, st.a[l], 4 * h_, h_, 4 * h_, T_, grad_ + o.w2, beta, side_);
             // b2: fused into the LayerNorm backward that produced g (LNf or the layer
             // above's LN1); only the gradient received from the next stage needs a pass
-            if (l == layers_ - 1 && !last_) colsum_bf16(g, T_, h_, h_, grad_ + o.b2, first, red_scratch_, s);
+            if (l == layers_ - 1 && !last_) colsum_bf16(g, T_, h_, h_, grad_ + o.b2, first, side_red_, side_);
+            done(kEvDoneA);
+            fork(kEvG4, s);
             // FC1: dxn2 = du W1
             gemm_store_mn_b(g4_, 4 * h_, W + o.w1, h_, T_, h_, 4 * h_, gX_, s);
-            gemm_wgrad(g4_, 4 * h_, st.xn2[l], h_, 4 * h_, h_, T_, grad_ + o.w1, beta, s);
-            colsum_bf16(g4_, T_, 4 * h_, 4 * h_, grad_ + o.b1, first, red_scratch_, s);
+            gemm_wgrad(g4_, 4 * h_, st.xn2[l], h_, 4 * h_, h_, T_, grad_ + o.w1, beta, side_);
+            colsum_bf16(g4_, T_, 4 * h_, 4 * h_, grad_ + o.b1, first, side_red_, side_);
+            done(kEvDoneB);
             // LN2 (+ residual): dx1 = LN2'(dxn2) + g
             // (+ bo = colsum(dx1), fused)
+            wait_side(kEvDoneC, s);  // gB_ free (previous layer's Wo gradient)
             layernorm_bwd(gX_, st.x1[l], st.mean2[l], st.rstd2[l], W + o.ln2g, g, gB_, grad_ + o.ln2g,
                           grad_ + o.ln2b, first, T_, h_, red_scratch_, s, grad_ + o.bo);
+            fork(kEvGB, s);
             // proj: do = dx1 Wo
             gemm_store_mn_b(gB_, h_, W + o.wo, h_, T_, h_, h_, gX_, s);
-            gemm_wgrad(gB_, h_, st.o[l], h_, h_, h_, T_, grad_ + o.wo, beta, s);
+            gemm_wgrad(gB_, h_, st.o[l], h_, h_, h_, T_, grad_ + o.wo, beta, side_);
+            done(kEvDoneC);
             // attention
+            wait_side(kEvDoneD, s);  // g3_ free (previous layer's Wqkv / bqkv gradients)
             attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
                           cfg_.causal != 0, s);
+            fork(kEvG3, s);
             // QKV: dxn1 = dqkv Wqkv
             gemm_store_mn_b(g3_, 3 * h_, W + o.wqkv, h_, T_, h_, 3 * h_, gX_, s);
-            gemm_wgrad(g3_, 3 * h_, st.xn1[l], h_, 3 * h_, h_, T_, grad_ + o.wqkv, beta, s);
-            colsum_bf16(g3_, T_, 3 * h_, 3 * h_, grad_ + o.bqkv, first, red_scratch_, s);
+            gemm_wgrad(g3_, 3 * h_, st.xn1[l], h_, 3 * h_, h_, T_, grad_ + o.wqkv, beta, side_);
+            colsum_bf16(g3_, T_, 3 * h_, 3 * h_, grad_ + o.bqkv, first, side_red_, side_);
+            done(kEvDoneD);
             // LN1 (+ residual): dx = LN1'(dxn1) + dx1
             bf16* dst = (l > 0 || first_) ? gA_ : static_cast<bf16*>(g_out);
+            wait_side(kEvDoneA, s);  // g (gA_) read by this layer's W2 gradient
             // (+ b2 of the layer below = colsum(dx), fused)
             layernorm_bwd(gX_, x, st.mean1[l], st.rstd1[l], W + o.ln1g, gB_, dst, grad_ + o.ln1g, grad_ + o.ln1b,
                           first, T_, h_, red_scratch_, s, l > 0 ? grad_ + lay_[l - 1].b2 : nullptr);
@@ -296,7 +322,18 @@ public:
                            "memset dtok");
             embed_bwd(data_ids(k), g, grad_ + off_tok_, grad_ + off_pos_, T_, seq_, h_, first, s);
         }
+        done(kEvEnd);
+        wait_side(kEvEnd, s);  // every weight gradient of this microbatch is in grad_
     }
+
+    // side-stream plumbing of backward()
+    enum { kEvStart, kEvG, kEvG4, kEvGB, kEvG3, kEvDoneA, kEvDoneB, kEvDoneC, kEvDoneD, kEvEnd, kNumEv };
+    void fork(int e, cudaStream_t s) {
+        check_cuda(cudaEventRecord(ev_[e], s), "cudaEventRecord(fork)");
+        check_cuda(cudaStreamWaitEvent(side_, ev_[e], 0), "cudaStreamWaitEvent(fork)");
+    }
+    void done(int e) { check_cuda(cudaEventRecord(ev_[e], side_), "cudaEventRecord(side)"); }
+    void wait_side(int e, cudaStream_t s) { check_cuda(cudaStreamWaitEvent(s, ev_[e], 0), "cudaStreamWaitEvent(side)"); }
 
     void update(int src_slot, int dst_slot, int grad_count, cudaStream_t s) override {
         (void)src_slot;  // the fp32 master always holds the latest version
@@ -423,6 +460,10 @@ private:
         const size_t red = std::max({layernorm_bwd_scratch_floats(T_, h_), colsum_scratch_floats(T_, 4 * h_),
                                      layernorm_bwd_scratch_floats(R_, h_)});
         red_scratch_ = dalloc<float>(red);
+        side_red_ = dalloc<float>(std::max(colsum_scratch_floats(T_, 4 * h_), colsum_scratch_floats(T_, h_)));
+        check_cuda(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking), "cudaStreamCreate(side)");
+        side_ = side_stream_;
+        for (cudaEvent_t& e : ev_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     }
 
     const int* data_ids(int k) const {
@@ -503,6 +544,10 @@ private:
     float* delta_ = nullptr;
     float* attn_scratch_ = nullptr;
     float* red_scratch_ = nullptr;
+    float* side_red_ = nullptr;       // colsum partials of the side stream
+    cudaStream_t side_stream_ = nullptr;  // weight-gradient stream of backward()
+    cudaStream_t side_ = nullptr;         // side_stream_, or the main stream while profiling
+    cudaEvent_t ev_[kNumEv] = {};
     float* row_loss_ = nullptr;
     float* head_ws_ = nullptr;
     int* head_idx_ = nullptr;
