@@ -281,6 +281,14 @@ typedef struct {
      * split-K into it and be cast to bf16 afterwards. */
     void* workspace;
     long long workspace_floats;
+    /* Optional (kind 1 with an MN-major A only -- the wgrad): bias_grad[r] (=|+=)
+     * sum over K of A[r, :], i.e. the bias gradient of the layer whose output
+     * gradient A is, summed from the A tiles the GEMM already stages in SMEM;
+     * bias_scratch holds >= (K / 512 + 1) * m floats of per-split partials. */
+    void* bias_grad;
+    int bias_grad_accumulate;
+    void* bias_scratch;
+    long long bias_scratch_floats;
 } p2bw_gemm_epilogue;
 
 /* D[m x n] = A[m x k] . B[n x k]^T on tcgen05 tensor cores (bf16 in, fp32 acc).

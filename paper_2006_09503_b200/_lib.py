@@ -36,6 +36,10 @@ class GemmEpilogue(C.Structure):
         ("beta", C.c_float),
         ("workspace", C.c_void_p),
         ("workspace_floats", C.c_longlong),
+        ("bias_grad", C.c_void_p),
+        ("bias_grad_accumulate", C.c_int),
+        ("bias_scratch", C.c_void_p),
+        ("bias_scratch_floats", C.c_longlong),
     ]
 
 

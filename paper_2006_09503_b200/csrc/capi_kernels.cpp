@@ -29,6 +29,10 @@ extern "C" int p2bw_kernel_gemm_bf16(const void* a, long long lda, int a_major, 
         e.beta = epi->beta;
         e.workspace = static_cast<float*>(epi->workspace);
         e.workspace_floats = epi->workspace_floats;
+        e.bias_grad = static_cast<float*>(epi->bias_grad);
+        e.bias_grad_accumulate = epi->bias_grad_accumulate != 0;
+        e.bias_scratch = static_cast<float*>(epi->bias_scratch);
+        e.bias_scratch_floats = epi->bias_scratch_floats;
         gemm_bf16(A, B, m, n, k, e, static_cast<cudaStream_t>(stream));
     });
 }

@@ -29,6 +29,7 @@
 #include <string>
 
 #include "kernels.h"
+#include "tkernels.h"
 #include "profiler.h"
 #include "ptx.cuh"
 #include "util.h"
@@ -87,6 +88,7 @@ struct KParams {
     int m, n, k;
     int splits;  // split-K factor (fp32 reduce-add epilogue only)
     GemmEpilogue epi;
+    float* rsum;  // row sums of A (bias gradient partials [splits][m]) or nullptr
 };
 
 // Output / side-input tensor maps of the epilogue (32-row boxes, 128 B rows, SW128).
@@ -150,7 +152,8 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
         ptx::tma_prefetch_desc(&em.d);
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], kNP);  // every pair leader's MMA commit frees a stage
+            // every pair leader's MMA commit frees a stage (+ the two row-sum warps)
+            ptx::mbar_init(&empty_bar[s], kNP + (p.rsum != nullptr ? 2 : 0));
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull_bar[i], 1);
@@ -297,6 +300,66 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
+                }
+            }
+        }
+    } else if ((warp == 2 || warp == 3) && p.rsum != nullptr) {
+        // Row sums of A while it sits in SMEM (the bias gradient rides on the wgrad):
+        // warp 2 + j sums A box j (64 rows of the tile) over this unit's K blocks.  Only
+        // units in the first N tile sum (each A element counts once); every unit still
+        // releases its stages.  Box layout (MN-major SW128): K row k is 128 B of 64 row
+        // values, 16-byte chunk c at position c ^ (k & 7).  Lane: the 8 rows of chunk
+        // lane & 7, K rows k = lane >> 3 (mod 4).
+        if constexpr (kAMN && kKind == EpiKind::StoreF32 && !kPair) {
+            const int j = warp - 2;
+            const int c = lane & 7;  // 16-byte chunk: rows 8c .. 8c+7 of the box; K rows of lane >> 3 (mod 4)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int w = w0; w < num_work; w += wstep) {
+                const int tile = w % num_tiles;
+                const int m0 = (tile % tiles_mg) * kBM;
+                const bool active = tile / tiles_mg == 0;  // n0 == 0
+                const int kb0 = (w / num_tiles) * kb_per;
+                const int kb1 = min(kblocks, kb0 + kb_per);
+                float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full_bar[stage], phase);
+                    if (active) {
+                        const uint32_t box = ptx::smem_u32(s_a + stage * Cfg::kABytes + j * 64 * kBK * 2);
+#pragma unroll 4
+                        for (int k = lane >> 3; k < kBK; k += 4) {
+                            uint32_t v[4];
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                                         : "r"(box + k * 128 + ((c ^ (k & 7)) << 4)));
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const float2 f = ptx::unpack_bf16x2(v[t]);
+                                acc[2 * t] += f.x;
+                                acc[2 * t + 1] += f.y;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&empty_bar[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (active) {  // combine the four K-row phases (lanes c, c+8, c+16, c+24)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        acc[q] += __shfl_down_sync(0xffffffffu, acc[q], 16);
+                        acc[q] += __shfl_down_sync(0xffffffffu, acc[q], 8);
+                    }
+                    const int r = m0 + j * 64 + 8 * lane;
+                    if (lane < 8 && r < p.m) {
+                        float* dst = p.rsum + static_cast<size_t>(w / num_tiles) * p.m + r;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (r + q < p.m) dst[q] = acc[q];
+                    }
                 }
             }
         }
@@ -623,7 +686,7 @@ double tile_speed(int bn, int cl) {
 // [8192 x 768] output on 74 SM pairs run as two waves at 65% occupancy, 256 128 x 192
 // tiles as two waves at 86%.  fp32 (wgrad) outputs keep 256-wide tiles, which the
 // sweeps favour for MN-major operands, and choose only their split count.
-TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_split) {
+TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_split, bool single_cta = false) {
     const int kblocks = (k + kBK - 1) / kBK;
     if (const char* env = std::getenv("P2BW_GEMM_TILE")) {  // tuning knob: "bn,cl[,splits]"
         int bn = 0, cl = 0, sp = 0;
@@ -637,10 +700,10 @@ TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_s
     for (int bn : {256, 192, 128}) {
         if (f32_out && bn != 256) continue;
         for (int cl : {2, 1}) {
-            if (!tile_ok(bn, cl, bmn) || (cl == 2 && m <= kBM)) continue;
+            if (!tile_ok(bn, cl, bmn) || (cl == 2 && m <= kBM) || (cl == 2 && single_cta)) continue;
             const int tiles_m = (m + kBM - 1) / kBM;
             const int tiles = (cl == 2 ? (tiles_m + 1) / 2 : tiles_m) * ((n + bn - 1) / bn);
-            const int max_split = allow_split ? std::max(1, kblocks / 8) : 1;
+            const int max_split = allow_split ? std::max(1, kblocks / 8) : 1;  // >= 8 k-blocks (512) per slice
             const double per_kb = (bn / 256.0) / tile_speed(bn, cl);
             for (int sp = 1; sp <= max_split; ++sp) {
                 const int kb_per = (kblocks + sp - 1) / sp;
@@ -685,7 +748,9 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         throw Error("gemm: output leading dims must be multiples of 8");
     const bool amn = a.major == Major::MN, bmn = b.major == Major::MN;
     const bool f32 = epi.kind == EpiKind::StoreF32;
-    TileChoice tc = choose_tile(m, n, k, f32, bmn, f32);
+    const bool want_rsum = epi.bias_grad != nullptr;
+    if (want_rsum && !(f32 && amn)) throw Error("gemm: bias_grad needs an fp32 store with an MN-major A (wgrad)");
+    TileChoice tc = choose_tile(m, n, k, f32, bmn, f32, want_rsum);
     // Plain bf16 stores with few output tiles and a long K (the LM-head dgrad: 1232 x 768
     // over K = 30592 fills 60 SMs with 128 x 128 tiles) run split-K into the caller's
     // fp32 workspace and are cast afterwards, when the model says that wins.
@@ -708,6 +773,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         }
     }
     if (!tile_ok(tc.bn, tc.cl, bmn)) tc.cl = 1;
+    if (want_rsum) tc.cl = 1;  // the row-sum warps read a local full barrier (no CTA pairs)
     const int bn = tc.bn, cl = tc.cl;
     // A: rows = m (tile kBM), B: rows = n (tile bn; each CTA of a pair loads bn / 2).
     // K-major maps put k innermost.
@@ -742,7 +808,13 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
             }
         }
     }
-    KParams p{m, n, k, splits, epi};
+    float* rsum = nullptr;
+    if (want_rsum) {
+        if (epi.bias_scratch == nullptr || epi.bias_scratch_floats < static_cast<int64_t>(splits) * m)
+            throw Error("gemm: bias_scratch must hold splits * M floats");
+        rsum = epi.bias_scratch;
+    }
+    KParams p{m, n, k, splits, epi, rsum};
     const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
     // profiler class by pass: forward (K-major x K-major), dgrad (B MN-major), wgrad (both MN-major)
     const char* cls = amn ? "gemm_wgrad" : (bmn ? "gemm_dgrad" : "gemm_fwd");
@@ -758,6 +830,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     else if (bn == 192) dispatch_major<192, 1>(amn, bmn, ta, tb, em, p, stream);
     else if (cl == 2) dispatch_major<128, 2>(amn, bmn, ta, tb, em, p, stream);
     else dispatch_major<128, 1>(amn, bmn, ta, tb, em, p, stream);
+    if (want_rsum) reduce_partials(rsum, splits, m, epi.bias_grad, !epi.bias_grad_accumulate, stream);
 }
 
 int num_sms() {

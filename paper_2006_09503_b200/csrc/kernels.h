@@ -44,6 +44,14 @@ struct GemmEpilogue {
     // with few output tiles and a long K may then run split-K into it and be cast.
     float* workspace = nullptr;
     int64_t workspace_floats = 0;
+    // wgrad only (fp32 store, A MN-major): bias_grad[r] (=|+=) sum over K of A[r, :] --
+    // the bias gradient of the layer whose output gradient A is -- summed from the A
+    // tiles already in SMEM by two otherwise idle warps; bias_scratch holds >= splits * M
+    // floats of partials (splits <= K / 512).
+    float* bias_grad = nullptr;
+    bool bias_grad_accumulate = false;
+    float* bias_scratch = nullptr;
+    int64_t bias_scratch_floats = 0;
 };
 
 // D[M x N] = A[M x K] . B[N x K]^T on tcgen05 (TMA -> SMEM -> UMMA -> TMEM -> epilogue).

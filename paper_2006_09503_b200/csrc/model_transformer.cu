@@ -286,6 +286,8 @@ public:
             // FC1: dxn2 = du W1
             gemm_store_mn_b(g4_, 4 * h_, W + o.w1, h_, T_, h_, 4 * h_, gX_, s);
             gemm_wgrad(g4_, 4 * h_, st.xn2[l], h_, 4 * h_, h_, T_, grad_ + o.w1, beta, side_);
+            // b1 = colsum(du) as its own pass: summing the A tiles inside the wgrad GEMM
+            // (GemmEpilogue::bias_grad) measured no faster, as it rules out CTA-pair tiles
             colsum_bf16(g4_, T_, 4 * h_, 4 * h_, grad_ + o.b1, first, side_red_, side_);
             done(kEvDoneB);
             // LN2 (+ residual): dx1 = LN2'(dxn2) + g
@@ -460,7 +462,11 @@ private:
         const size_t red = std::max({layernorm_bwd_scratch_floats(T_, h_), colsum_scratch_floats(T_, 4 * h_),
                                      layernorm_bwd_scratch_floats(R_, h_)});
         red_scratch_ = dalloc<float>(red);
-        side_red_ = dalloc<float>(std::max(colsum_scratch_floats(T_, 4 * h_), colsum_scratch_floats(T_, h_)));
+        // colsum partials of the side stream, and the wgrad bias partials (splits x rows,
+        // splits <= T / 512)
+        side_red_floats_ = static_cast<int64_t>(std::max({colsum_scratch_floats(T_, 4 * h_), colsum_scratch_floats(T_, h_),
+                                                          static_cast<size_t>(T_ / 512 + 1) * 4 * h}));
+        side_red_ = dalloc<float>(static_cast<size_t>(side_red_floats_));
         check_cuda(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking), "cudaStreamCreate(side)");
         side_ = side_stream_;
         for (cudaEvent_t& e : ev_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
@@ -513,14 +519,21 @@ private:
     }
 
     // wgrad: G[m x n] (=|+=) dY^T X with dY [tokens x m] and X [tokens x n], fp32 out.
+    // bias (optional): bias (=|+=) column sums of dY, computed inside the GEMM.
     void gemm_wgrad(const bf16* dy, int lddy, const bf16* x, int ldx, int m, int n, int tokens, float* g,
-                    float beta, cudaStream_t s) const {
+                    float beta, cudaStream_t s, float* bias = nullptr, bool bias_overwrite = false) const {
         GemmEpilogue e;
         e.kind = EpiKind::StoreF32;
         e.d = g;
         e.ldd = n;
         e.alpha = 1.0f;
         e.beta = beta;
+        if (bias != nullptr) {
+            e.bias_grad = bias;
+            e.bias_grad_accumulate = !bias_overwrite;
+            e.bias_scratch = side_red_;
+            e.bias_scratch_floats = side_red_floats_;
+        }
         gemm_bf16({dy, lddy, Major::MN}, {x, ldx, Major::MN}, m, n, tokens, e, s);
     }
 
@@ -544,7 +557,8 @@ private:
     float* delta_ = nullptr;
     float* attn_scratch_ = nullptr;
     float* red_scratch_ = nullptr;
-    float* side_red_ = nullptr;       // colsum partials of the side stream
+    float* side_red_ = nullptr;       // colsum / wgrad-bias partials of the side stream
+    int64_t side_red_floats_ = 0;
     cudaStream_t side_stream_ = nullptr;  // weight-gradient stream of backward()
     cudaStream_t side_ = nullptr;         // side_stream_, or the main stream while profiling
     cudaEvent_t ev_[kNumEv] = {};

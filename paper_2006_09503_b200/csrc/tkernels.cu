@@ -233,64 +233,80 @@ template <int NV>
 __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g, const bf16* __restrict__ b,
                          bf16* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd, int rows,
                          int h) {
+    // two rows per warp: both rows' loads (and gamma / beta) are in flight together and
+    // the two rows' reductions interleave (the kernel was latency-bound at one row)
+    constexpr int R = 2;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= rows) return;
+    const int row0 = warp * R;
+    if (row0 >= rows) return;
     const int hv = h / 8;
-    const bf16* xr = x + static_cast<size_t>(warp) * h;
-    // gamma / beta are issued with the row (packed bf16), so their latency overlaps the
-    // row's instead of following the two reductions
-    uint4 xp[NV], gp[NV], bp[NV];
+    uint4 xp[R][NV], gp[NV], bp[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         const int vi = lane + 32 * i;
         if (vi < hv) {
-            xp[i] = *reinterpret_cast<const uint4*>(xr + vi * 8);
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr)
+                if (row0 + rr < rows) xp[rr][i] = *reinterpret_cast<const uint4*>(x + static_cast<size_t>(row0 + rr) * h + vi * 8);
             gp[i] = *reinterpret_cast<const uint4*>(g + vi * 8);
             bp[i] = *reinterpret_cast<const uint4*>(b + vi * 8);
         }
     }
-    float v[NV][8];
-    float sum = 0.0f;
+    float v[R][NV][8];
+    float sum[R], mu[R], var[R], rs[R];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        if (lane + 32 * i < hv) {
-            const uint32_t w[4] = {xp[i].x, xp[i].y, xp[i].z, xp[i].w};
+    for (int rr = 0; rr < R; ++rr) {
+        sum[rr] = 0.0f;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const float2 f = ptx::unpack_bf16x2(w[t]);
-                v[i][2 * t] = f.x;
-                v[i][2 * t + 1] = f.y;
-                sum += f.x + f.y;
+        for (int i = 0; i < NV; ++i) {
+            if (lane + 32 * i < hv) {
+                const uint32_t w[4] = {xp[rr][i].x, xp[rr][i].y, xp[rr][i].z, xp[rr][i].w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 f = ptx::unpack_bf16x2(w[t]);
+                    v[rr][i][2 * t] = f.x;
+                    v[rr][i][2 * t + 1] = f.y;
+                    sum[rr] += f.x + f.y;
+                }
             }
         }
     }
-    const float mu = warp_sum(sum) / h;
-    float var = 0.0f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i)
-        if (lane + 32 * i < hv)
+    for (int rr = 0; rr < R; ++rr) mu[rr] = warp_sum(sum[rr]) / h;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) var += (v[i][q] - mu) * (v[i][q] - mu);
-    const float rs = rsqrtf(warp_sum(var) / h + 1e-5f);
+    for (int rr = 0; rr < R; ++rr) {
+        var[rr] = 0.0f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int vi = lane + 32 * i;
-        if (vi < hv) {
-            const uint32_t gw[4] = {gp[i].x, gp[i].y, gp[i].z, gp[i].w};
-            const uint32_t bw[4] = {bp[i].x, bp[i].y, bp[i].z, bp[i].w};
-            float o[8];
+        for (int i = 0; i < NV; ++i)
+            if (lane + 32 * i < hv)
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const float2 gf = ptx::unpack_bf16x2(gw[t]), bf = ptx::unpack_bf16x2(bw[t]);
-                o[2 * t] = (v[i][2 * t] - mu) * rs * gf.x + bf.x;
-                o[2 * t + 1] = (v[i][2 * t + 1] - mu) * rs * gf.y + bf.y;
-            }
-            store8(y + static_cast<size_t>(warp) * h + vi * 8, o);
-        }
+                for (int q = 0; q < 8; ++q) var[rr] += (v[rr][i][q] - mu[rr]) * (v[rr][i][q] - mu[rr]);
     }
-    if (lane == 0) {
-        mean[warp] = mu;
-        rstd[warp] = rs;
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) rs[rr] = rsqrtf(warp_sum(var[rr]) / h + 1e-5f);
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+        if (row0 + rr >= rows) break;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int vi = lane + 32 * i;
+            if (vi < hv) {
+                const uint32_t gw[4] = {gp[i].x, gp[i].y, gp[i].z, gp[i].w};
+                const uint32_t bw[4] = {bp[i].x, bp[i].y, bp[i].z, bp[i].w};
+                float o[8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 gf = ptx::unpack_bf16x2(gw[t]), bf = ptx::unpack_bf16x2(bw[t]);
+                    o[2 * t] = (v[rr][i][2 * t] - mu[rr]) * rs[rr] * gf.x + bf.x;
+                    o[2 * t + 1] = (v[rr][i][2 * t + 1] - mu[rr]) * rs[rr] * gf.y + bf.y;
+                }
+                store8(y + static_cast<size_t>(row0 + rr) * h + vi * 8, o);
+            }
+        }
+        if (lane == 0) {
+            mean[row0 + rr] = mu[rr];
+            rstd[row0 + rr] = rs[rr];
+        }
     }
 }
 
@@ -678,7 +694,7 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
     prof::Scope scope("layernorm_fwd", 0.0, 4.0 * rows * h + 8.0 * rows, 1, s);
     const int nv = (h / 8 + 31) / 32;
-    const int grid = (rows + 7) / 8;
+    const int grid = (rows + 15) / 16;  // 8 warps x 2 rows
     switch (nv) {
         case 1: k_ln_fwd<1><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, rows, h); break;
         case 2: k_ln_fwd<2><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, rows, h); break;
@@ -722,6 +738,11 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
     ReduceOut o{{dg, db, dsum}};
     k_reduce_parts<<<dim3((h + 7) / 8, dsum ? 3 : 2), 256, 0, s>>>(scratch, grid, h, o, overwrite ? 1 : 0);
     check_cuda(cudaGetLastError(), "layernorm_bwd");
+}
+
+void reduce_partials(const float* part, int parts, int n, float* out, bool overwrite, cudaStream_t s) {
+    reduce_parts(part, parts, n, out, overwrite, s);
+    check_cuda(cudaGetLastError(), "reduce_partials");
 }
 
 size_t colsum_scratch_floats(int rows, int n) { return static_cast<size_t>(colsum_row_blocks(rows, n)) * n; }

@@ -67,6 +67,9 @@ void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float
 void sgd_momentum_update(float* master, float* vel, const float* grad, bf16* out_bf16, size_t n,
                          float inv_count, float lr, float beta, cudaStream_t s);
 
+// out[c] (=|+=) sum_{p < parts} part[p * n + c], fixed order (deterministic).
+void reduce_partials(const float* part, int parts, int n, float* out, bool overwrite, cudaStream_t s);
+
 // Adam (bias-corrected, step = 1-based update count) on the flat fp32 master; m1 / m2
 // are the first / second moment buffers.
 void adam_update(float* master, float* m1, float* m2, const float* grad, bf16* out_bf16, size_t n, float inv_count,

@@ -182,3 +182,26 @@ def test_gemm_bf16_split_k_workspace(m, n, k, bm):
     scale = ref.abs().max().item()
     assert (d.float() - ref).abs().max().item() <= 0.01 * scale
     assert (d2.float() - ref).abs().max().item() <= 0.01 * scale
+
+
+@pytest.mark.parametrize("accumulate", [0, 1])
+@pytest.mark.parametrize("m,n,k", [(3072, 768, 8192), (2304, 768, 8192), (200, 256, 1000)])
+def test_gemm_wgrad_fused_bias_grad(m, n, k, accumulate):
+    """The wgrad GEMM also sums its A operand's rows (the bias gradient of the layer
+    whose output gradient A is) from the SMEM tiles: bias (=|+=) A.sum(K)."""
+    gen = torch.Generator(device="cuda").manual_seed(m + n + k + accumulate)
+    A, a, lda = _operand(m, k, 1, gen)
+    B, b, ldb = _operand(n, k, 1, gen)
+    d = torch.zeros(m, n, device="cuda")
+    bias0 = torch.randn(m, device="cuda", generator=gen)
+    bias = bias0.clone()
+    scratch = torch.zeros((k // 512 + 1) * m, device="cuda")
+    epi = GemmEpilogue(kind=1, d=d.data_ptr(), ldd=n, alpha=1.0, beta=0.0, bias_grad=bias.data_ptr(),
+                       bias_grad_accumulate=accumulate, bias_scratch=scratch.data_ptr(),
+                       bias_scratch_floats=scratch.numel())
+    _gemm(a, lda, 1, b, ldb, 1, m, n, k, epi)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    assert (d - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
+    bref = A.float().sum(1) + (bias0 if accumulate else 0)
+    assert (bias - bref).abs().max().item() <= 1e-3 * (1 + bref.abs().max().item())
