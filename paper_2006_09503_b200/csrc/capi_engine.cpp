@@ -127,9 +127,16 @@ int p2bw_engine_set_data(p2bw_engine* eng, const void* inputs, const void* targe
         if (first_mb < 1) throw std::invalid_argument("microbatch ids are 1-based");
         // Inputs feed stage 0, targets the last stage (they may be the same stage);
         // a process without either stage ignores the call.
-        if (e.is_local(0)) e.model(0).set_data(inputs, e.depth() == 1 ? targets : nullptr, first_mb, count);
-        if (e.depth() > 1 && e.is_local(e.depth() - 1))
+        if (e.is_local(0)) {
+            e.before_data_set(0);
+            e.model(0).set_data(inputs, e.depth() == 1 ? targets : nullptr, first_mb, count);
+            e.note_data_set(0);
+        }
+        if (e.depth() > 1 && e.is_local(e.depth() - 1)) {
+            e.before_data_set(e.depth() - 1);
             e.model(e.depth() - 1).set_data(nullptr, targets, first_mb, count);
+            e.note_data_set(e.depth() - 1);
+        }
     });
 }
 

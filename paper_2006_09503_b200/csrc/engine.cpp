@@ -24,6 +24,7 @@
 
 #include "nccl_dl.h"
 #include "pipesim/schedule.hpp"
+#include "profiler.h"
 #include "transport.h"
 
 namespace p2bw {
@@ -94,6 +95,13 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     // its next forward without waiting for this stage's oldest backward.
     const int per = cfg_.layers / cfg_.depth;
     stages_.resize(static_cast<size_t>(cfg_.depth));
+    // Forward of microbatch k+1 overlaps the Backward of k on its own stream
+    // (transformer stages; recomputation re-runs forwards inside the Backward into a
+    // single shared slot, so it keeps one stream).  P2BW_SERIAL_STAGE=1 turns it off.
+    // A function of the configuration only: every process derives the same ring sizes.
+    const char* serial = std::getenv("P2BW_SERIAL_STAGE");
+    const bool overlap =
+        cfg_.model_kind == P2BW_MODEL_TRANSFORMER && !cfg_.recompute && !(serial && serial[0] == '1');
     try {
         for (int s = 0; s < cfg_.depth; ++s) {
             Stage& st = stages_[s];
@@ -109,6 +117,8 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
                 default: inflight = std::max(warm, 1); break;
             }
             st.stash_slots = inflight + (s > 0 ? 1 : 0);
+            // one more slot lets Forward k+1 (own stream) run while Backward k holds its slot
+            if (overlap) st.stash_slots = std::max(st.stash_slots, 2 + (s > 0 ? 1 : 0));
             st.grad_slots = st.stash_slots;
             st.weight_slots = weight_slots_for(cfg_.policy, cfg_.depth);
             st.local = s >= lo_local && s < hi_local;
@@ -116,6 +126,10 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             DeviceGuard g(st.device);
             check_cuda(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking),
                        "cudaStreamCreate");
+            if (overlap) {
+                check_cuda(cudaStreamCreateWithFlags(&st.fstream, cudaStreamNonBlocking), "cudaStreamCreate(fwd)");
+                check_cuda(cudaEventCreateWithFlags(&st.data_ev, cudaEventDisableTiming), "cudaEventCreate(data)");
+            }
             check_cuda(cudaEventCreate(&st.t0), "cudaEventCreate");
             check_cuda(cudaEventCreate(&st.t1), "cudaEventCreate");
             if (cfg_.model_kind == P2BW_MODEL_LINEAR_F64) {
@@ -268,6 +282,10 @@ void Engine::free_buffers() {
         st.model.reset();
         if (st.comm) nccl_comm_destroy(static_cast<ncclComm_t>(st.comm));
         st.comm = nullptr;
+        if (st.fstream) cudaStreamSynchronize(st.fstream), cudaStreamDestroy(st.fstream);
+        st.fstream = nullptr;
+        if (st.data_ev) cudaEventDestroy(st.data_ev);
+        st.data_ev = nullptr;
         if (st.t0) cudaEventDestroy(st.t0);
         if (st.t1) cudaEventDestroy(st.t1);
         if (st.stream) cudaStreamDestroy(st.stream);
@@ -350,20 +368,35 @@ void Engine::issue_forward(Stage& st, const OpRec& op) {
     const int sslot = (k - 1) % st.stash_slots;
     const bool prev_remote = s > 0 && !stages_[s - 1].local;
     const bool next_remote = s + 1 < d && !stages_[s + 1].local;
-    if (prev_remote) wait_flag(&st.flags[kActReady], seq(k), st.stream);
-    else if (s > 0) wait_on(ev_->fwd[s - 1], k, st.stream);
+    const cudaStream_t fs = op_stream(st, P2BW_OP_FORWARD);
+    if (st.fstream) {
+        // what the single stream ordered implicitly: the update that produced version
+        // v, the backward that last held this stash slot, and this stage's data
+        const int u = v - st.version_base;  // 1-based update of this run (<= 0: earlier run)
+        if (u >= 1) {
+            const auto& ue = ev_->upd[static_cast<size_t>(s)];
+            if (u > static_cast<int>(ue.size())) throw Error("internal: forward before its version's update");
+            check_cuda(cudaStreamWaitEvent(fs, ue[static_cast<size_t>(u - 1)], 0), "cudaStreamWaitEvent(version)");
+        }
+        if (k > st.stash_slots) wait_on(ev_->bwd[s], k - st.stash_slots, fs);
+        check_cuda(cudaStreamWaitEvent(fs, st.data_ev, 0), "cudaStreamWaitEvent(data)");
+    }
+    if (prev_remote) wait_flag(&st.flags[kActReady], seq(k), fs);
+    else if (s > 0) wait_on(ev_->fwd[s - 1], k, fs);
     void* x_out = nullptr;
     if (next_remote) {  // staging slot, freed by the copy of microbatch k - 2
-        if (k > 2) wait_on(ev_->cpf[s], k - 2, st.stream);
+        if (k > 2) wait_on(ev_->cpf[s], k - 2, fs);
         x_out = st.send_act[(k - 1) % 2];
     } else if (s + 1 < d) {
         const Stage& nx = stages_[s + 1];
-        if (k > nx.stash_slots) wait_on(ev_->bwd[s + 1], k - nx.stash_slots, st.stream);
+        if (k > nx.stash_slots) wait_on(ev_->bwd[s + 1], k - nx.stash_slots, fs);
         x_out = nx.act_ring[(k - 1) % nx.stash_slots];
     }
     const void* x_in = s > 0 ? st.act_ring[sslot] : nullptr;
-    st.model->forward(k, vit->second, sslot, x_in, x_out, st.stream);
-    record(ev_->fwd[s], k, st.stream);
+    if (trace_on_ && trace_open_) check_cuda(cudaEventRecord(trace_open_, fs), "cudaEventRecord(trace)");  // after the waits
+    st.model->forward(k, vit->second, sslot, x_in, x_out, fs);
+    record(ev_->fwd[s], k, fs);
+    st.last_fwd = std::max(st.last_fwd, k);
     if (next_remote) {  // copy into the next process's ring once its slot is free
         const Stage& nx = stages_[s + 1];
         const cudaStream_t c = st.copy_fwd;
@@ -391,6 +424,7 @@ void Engine::issue_backward(Stage& st, const OpRec& op) {
     const int sslot = (k - 1) % st.stash_slots;
     const bool prev_remote = s > 0 && !stages_[s - 1].local;
     const bool next_remote = s + 1 < d && !stages_[s + 1].local;
+    if (st.fstream) wait_on(ev_->fwd[s], k, st.stream);  // its own Forward (other stream)
     const void* g_in = nullptr;
     if (s + 1 < d) {
         if (next_remote) wait_flag(&st.flags[kGradReady], seq(k), st.stream);
@@ -406,6 +440,7 @@ void Engine::issue_backward(Stage& st, const OpRec& op) {
         if (k > pv.grad_slots) wait_on(ev_->bwd[s - 1], k - pv.grad_slots, st.stream);
         g_out = pv.grad_ring[(k - 1) % pv.grad_slots];
     }
+    if (trace_on_ && trace_open_) check_cuda(cudaEventRecord(trace_open_, st.stream), "cudaEventRecord(trace)");
     if (cfg_.recompute) {  // Recompute op (simulator.cpp:242-247): the stage input is in its ring slot
         st.model->recompute(k, wslot, sslot, s > 0 ? st.act_ring[sslot] : nullptr, st.stream);
         if (trace_on_) trace_split(st, OpRec{P2BW_OP_RECOMPUTE, k, op.weight_version});
@@ -475,6 +510,9 @@ void Engine::issue_update(Stage& st) {
     if (dst_slot < 0)
         throw Error("stage " + std::to_string(st.index) + ": no free weight buffer for version " +
                     std::to_string(src_version + 1));
+    // the new version's buffer may be one an in-flight Forward (own stream) still reads
+    if (st.fstream && st.last_fwd > 0 && ev_->fwd[static_cast<size_t>(st.index)].count(st.last_fwd))
+        wait_on(ev_->fwd[static_cast<size_t>(st.index)], st.last_fwd, st.stream);
     // gradients are summed over grad_count microbatches (and over the replicas by
     // the AllReduce): divide by both (semantics.cpp:338-340; PAPER §3 "w replicas")
     st.model->update(src_slot, dst_slot, st.grad_count * st.replicas, st.stream);
@@ -529,6 +567,7 @@ void Engine::begin(const std::vector<Program>& programs) {
         st.bwd_issued.clear();
         st.snaps.clear();
         st.updates_issued = 0;
+        st.last_fwd = 0;
         st.version_base = st.updates_done;
         DeviceGuard g(st.device);
         check_cuda(cudaEventRecord(st.t0, st.stream), "cudaEventRecord");
@@ -550,7 +589,7 @@ void Engine::issue(int upto_batch) {
             while (st.ptr < prog.size() && st.updates_issued < target) {
                 const OpRec& op = prog[st.ptr];
                 if (!ready(st, op)) break;
-                if (trace_on_) trace_begin(st);
+                if (trace_on_) trace_begin(st, op);
                 switch (op.kind) {
                     case P2BW_OP_FORWARD: issue_forward(st, op); break;
                     case P2BW_OP_BACKWARD: issue_backward(st, op); break;
@@ -617,6 +656,7 @@ void Engine::sync() {
         if (!st.local) continue;
         DeviceGuard g(st.device);
         check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
+        if (st.fstream) check_cuda(cudaStreamSynchronize(st.fstream), "cudaStreamSynchronize");
         if (st.copy_fwd) check_cuda(cudaStreamSynchronize(st.copy_fwd), "cudaStreamSynchronize");
         if (st.copy_bwd) check_cuda(cudaStreamSynchronize(st.copy_bwd), "cudaStreamSynchronize");
     }
@@ -636,6 +676,7 @@ double Engine::elapsed_ms_last_run() {
 
 std::vector<double> Engine::losses(int first_mb, int count) {
     Stage& st = local_stage(cfg_.depth - 1);
+    if (st.fstream) check_cuda(cudaStreamSynchronize(st.fstream), "cudaStreamSynchronize");
     std::vector<double> out(static_cast<size_t>(count));
     DeviceGuard g(st.device);
     st.model->read_losses(out.data(), first_mb, count, st.stream);
@@ -654,9 +695,9 @@ void Engine::read_version(int s, int version, void* host, size_t bytes) {
     check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
 }
 
-void Engine::trace_begin(Stage& st) {
+void Engine::trace_begin(Stage& st, const OpRec& op) {
     check_cuda(cudaEventCreate(&trace_open_), "cudaEventCreate(trace)");
-    check_cuda(cudaEventRecord(trace_open_, st.stream), "cudaEventRecord(trace)");
+    check_cuda(cudaEventRecord(trace_open_, op_stream(st, op.kind)), "cudaEventRecord(trace)");
 }
 
 void Engine::trace_end(Stage& st, const OpRec& op) {
@@ -670,13 +711,45 @@ void Engine::trace_end(Stage& st, const OpRec& op) {
     r.e0 = trace_open_;
     trace_open_ = nullptr;
     check_cuda(cudaEventCreate(&r.e1), "cudaEventCreate(trace)");
-    check_cuda(cudaEventRecord(r.e1, st.stream), "cudaEventRecord(trace)");
+    check_cuda(cudaEventRecord(r.e1, op_stream(st, op.kind)), "cudaEventRecord(trace)");
     trace_.push_back(r);
+}
+
+void Engine::copy_losses_async(float* host, int first_mb, int count) {
+    Stage& st = local_stage(cfg_.depth - 1);
+    DeviceGuard g(st.device);
+    if (st.fstream && ev_) {  // the losses are written by the Forwards (forward stream)
+        const auto& fe = ev_->fwd[static_cast<size_t>(st.index)];
+        const int last = first_mb + count - 1;
+        if (fe.count(last)) wait_on(fe, last, st.stream);
+        else if (st.last_fwd > 0 && fe.count(st.last_fwd)) wait_on(fe, st.last_fwd, st.stream);
+    }
+    st.model->copy_losses_async(host, first_mb, count, st.stream);
+}
+
+cudaStream_t Engine::op_stream(const Stage& st, int kind) const {
+    return kind == P2BW_OP_FORWARD && st.fstream && !prof::enabled() ? st.fstream : st.stream;
+}
+
+void Engine::before_data_set(int s) {
+    Stage& st = local_stage(s);
+    if (!st.fstream || !ev_ || st.last_fwd < 1) return;
+    const auto& fe = ev_->fwd[static_cast<size_t>(st.index)];
+    if (!fe.count(st.last_fwd)) return;
+    DeviceGuard g(st.device);
+    wait_on(fe, st.last_fwd, st.stream);
+}
+
+void Engine::note_data_set(int s) {
+    Stage& st = local_stage(s);
+    if (!st.data_ev) return;
+    DeviceGuard g(st.device);
+    check_cuda(cudaEventRecord(st.data_ev, st.stream), "cudaEventRecord(data)");
 }
 
 void Engine::trace_split(Stage& st, const OpRec& first_part) {
     trace_end(st, first_part);
-    trace_begin(st);
+    trace_begin(st, OpRec{P2BW_OP_BACKWARD, first_part.microbatch, first_part.weight_version});
 }
 
 namespace {

@@ -173,10 +173,12 @@ public:
     double elapsed_ms_last_run();
     // Losses of microbatches [first_mb, first_mb + count) (last stage), after sync.
     std::vector<double> losses(int first_mb, int count);
-    void copy_losses_async(float* host, int first_mb, int count) {
-        Stage& st = local_stage(cfg_.depth - 1);
-        st.model->copy_losses_async(host, first_mb, count, st.stream);
-    }
+    void copy_losses_async(float* host, int first_mb, int count);
+    // Around the host's refill of stage s's data ring (H2D copies on its stream):
+    // before_data_set orders the copies after every Forward issued so far (they read
+    // the ring slots being overwritten); note_data_set lets later Forwards wait for them.
+    void before_data_set(int s);
+    void note_data_set(int s);
     bool is_local(int s) const { return s >= 0 && s < cfg_.depth && stages_[static_cast<size_t>(s)].local; }
     // Measured timeline: with tracing on, every issued op of a
     // local stage is bracketed by CUDA events; trace_report() renders the last run
@@ -199,7 +201,10 @@ private:
         bool local = true;
         bool connected = false;  // remote stage: its block is mapped into this process
         int lo = 0, hi = 0;
-        cudaStream_t stream = nullptr;
+        cudaStream_t stream = nullptr;   // Backward / WeightUpdate / AllReduce (and Forward unless fstream)
+        cudaStream_t fstream = nullptr;  // Forward, overlapping the previous microbatch's Backward
+        cudaEvent_t data_ev = nullptr;   // after the latest set_data copies (on `stream`)
+        int last_fwd = 0;                // latest microbatch whose Forward was issued
         std::unique_ptr<StageModel> model;
         int stash_slots = 1;
         int grad_slots = 1;
@@ -234,8 +239,11 @@ private:
         int versions_held, stashes;  // after the op (host bookkeeping)
         cudaEvent_t e0, e1;
     };
-    void trace_begin(Stage& st);
+    void trace_begin(Stage& st, const OpRec& op);
     void trace_end(Stage& st, const OpRec& op);
+    // Forwards run on the forward stream, except while per-launch profiling is on
+    // (the roofline wants every launch timed alone).
+    cudaStream_t op_stream(const Stage& st, int kind) const;
     void trace_split(Stage& st, const OpRec& first_part);  // close first_part, open the rest
 
     void issue_forward(Stage& st, const OpRec& op);
