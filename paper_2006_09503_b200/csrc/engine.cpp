@@ -128,7 +128,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
                        "cudaStreamCreate");
             if (overlap) {
                 check_cuda(cudaStreamCreateWithFlags(&st.fstream, cudaStreamNonBlocking), "cudaStreamCreate(fwd)");
-                check_cuda(cudaEventCreateWithFlags(&st.data_ev, cudaEventDisableTiming), "cudaEventCreate(data)");
+                check_cuda(cudaEventCreateWithFlags(&st.fsync, cudaEventDisableTiming), "cudaEventCreate(fsync)");
             }
             check_cuda(cudaEventCreate(&st.t0), "cudaEventCreate");
             check_cuda(cudaEventCreate(&st.t1), "cudaEventCreate");
@@ -142,6 +142,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
                 throw Error("unknown model kind " + std::to_string(cfg_.model_kind));
             }
             st.model->bind_stream(st.stream);
+            if (st.fstream) st.model->bind_data_stream(st.fstream);
             // Receive block: [act ring][grad ring][flags], one allocation so that a
             // single IPC handle exports it.
             const size_t nb = st.model->boundary_bytes();
@@ -284,8 +285,8 @@ void Engine::free_buffers() {
         st.comm = nullptr;
         if (st.fstream) cudaStreamSynchronize(st.fstream), cudaStreamDestroy(st.fstream);
         st.fstream = nullptr;
-        if (st.data_ev) cudaEventDestroy(st.data_ev);
-        st.data_ev = nullptr;
+        if (st.fsync) cudaEventDestroy(st.fsync);
+        st.fsync = nullptr;
         if (st.t0) cudaEventDestroy(st.t0);
         if (st.t1) cudaEventDestroy(st.t1);
         if (st.stream) cudaStreamDestroy(st.stream);
@@ -369,6 +370,10 @@ void Engine::issue_forward(Stage& st, const OpRec& op) {
     const bool prev_remote = s > 0 && !stages_[s - 1].local;
     const bool next_remote = s + 1 < d && !stages_[s + 1].local;
     const cudaStream_t fs = op_stream(st, P2BW_OP_FORWARD);
+    if (st.fstream && fs != st.fstream) {  // profiling: forwards on `stream`, data copies on fstream
+        check_cuda(cudaEventRecord(st.fsync, st.fstream), "cudaEventRecord(fsync)");
+        check_cuda(cudaStreamWaitEvent(fs, st.fsync, 0), "cudaStreamWaitEvent(fsync)");
+    }
     if (st.fstream) {
         // what the single stream ordered implicitly: the update that produced version
         // v, the backward that last held this stash slot, and this stage's data
@@ -379,7 +384,6 @@ void Engine::issue_forward(Stage& st, const OpRec& op) {
             check_cuda(cudaStreamWaitEvent(fs, ue[static_cast<size_t>(u - 1)], 0), "cudaStreamWaitEvent(version)");
         }
         if (k > st.stash_slots) wait_on(ev_->bwd[s], k - st.stash_slots, fs);
-        check_cuda(cudaStreamWaitEvent(fs, st.data_ev, 0), "cudaStreamWaitEvent(data)");
     }
     if (prev_remote) wait_flag(&st.flags[kActReady], seq(k), fs);
     else if (s > 0) wait_on(ev_->fwd[s - 1], k, fs);
@@ -447,6 +451,7 @@ void Engine::issue_backward(Stage& st, const OpRec& op) {
     }
     st.model->backward(k, wslot, sslot, g_in, g_out, st.grad_count == 0, st.stream);
     record(ev_->bwd[s], k, st.stream);
+    st.last_bwd = std::max(st.last_bwd, k);
     // Backward k released this stage's act slot and grad slot of microbatch k:
     // tell the remote producers (their flags live in their own blocks).
     if (prev_remote) signal_remote(&stages_[s - 1].flags[kNextBwd], seq(k), st.stream);
@@ -568,6 +573,7 @@ void Engine::begin(const std::vector<Program>& programs) {
         st.snaps.clear();
         st.updates_issued = 0;
         st.last_fwd = 0;
+        st.last_bwd = 0;
         st.version_base = st.updates_done;
         DeviceGuard g(st.device);
         check_cuda(cudaEventRecord(st.t0, st.stream), "cudaEventRecord");
@@ -733,18 +739,11 @@ cudaStream_t Engine::op_stream(const Stage& st, int kind) const {
 
 void Engine::before_data_set(int s) {
     Stage& st = local_stage(s);
-    if (!st.fstream || !ev_ || st.last_fwd < 1) return;
-    const auto& fe = ev_->fwd[static_cast<size_t>(st.index)];
-    if (!fe.count(st.last_fwd)) return;
+    if (!st.fstream || !ev_ || st.last_bwd < 1) return;
+    const auto& be = ev_->bwd[static_cast<size_t>(st.index)];
+    if (!be.count(st.last_bwd)) return;
     DeviceGuard g(st.device);
-    wait_on(fe, st.last_fwd, st.stream);
-}
-
-void Engine::note_data_set(int s) {
-    Stage& st = local_stage(s);
-    if (!st.data_ev) return;
-    DeviceGuard g(st.device);
-    check_cuda(cudaEventRecord(st.data_ev, st.stream), "cudaEventRecord(data)");
+    wait_on(be, st.last_bwd, st.fstream);
 }
 
 void Engine::trace_split(Stage& st, const OpRec& first_part) {

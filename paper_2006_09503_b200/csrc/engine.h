@@ -102,6 +102,8 @@ public:
         throw Error("this stage computes no loss");
     }
     virtual void bind_stream(cudaStream_t s) { (void)s; }
+    // Stream for set_data's host-to-device copies (default: the bound stream).
+    virtual void bind_data_stream(cudaStream_t s) { (void)s; }
     // The coalesced gradient buffer (all-reduced across data-parallel replicas).
     // dtype: 0 = fp32, 1 = fp64.
     virtual void grad_buffer(void** ptr, size_t* count, int* dtype) = 0;
@@ -174,11 +176,10 @@ public:
     // Losses of microbatches [first_mb, first_mb + count) (last stage), after sync.
     std::vector<double> losses(int first_mb, int count);
     void copy_losses_async(float* host, int first_mb, int count);
-    // Around the host's refill of stage s's data ring (H2D copies on its stream):
-    // before_data_set orders the copies after every Forward issued so far (they read
-    // the ring slots being overwritten); note_data_set lets later Forwards wait for them.
+    // Before the host refills stage s's data ring: with a forward stream the copies run
+    // on it (ordered before later Forwards), after every Backward issued so far (stage
+    // 0's embedding gradient reads the token ids of the slots being overwritten).
     void before_data_set(int s);
-    void note_data_set(int s);
     bool is_local(int s) const { return s >= 0 && s < cfg_.depth && stages_[static_cast<size_t>(s)].local; }
     // Measured timeline: with tracing on, every issued op of a
     // local stage is bracketed by CUDA events; trace_report() renders the last run
@@ -203,8 +204,9 @@ private:
         int lo = 0, hi = 0;
         cudaStream_t stream = nullptr;   // Backward / WeightUpdate / AllReduce (and Forward unless fstream)
         cudaStream_t fstream = nullptr;  // Forward, overlapping the previous microbatch's Backward
-        cudaEvent_t data_ev = nullptr;   // after the latest set_data copies (on `stream`)
         int last_fwd = 0;                // latest microbatch whose Forward was issued
+        int last_bwd = 0;                // latest microbatch whose Backward was issued
+        cudaEvent_t fsync = nullptr;     // joins the forward stream into `stream` (profiling)
         std::unique_ptr<StageModel> model;
         int stash_slots = 1;
         int grad_slots = 1;

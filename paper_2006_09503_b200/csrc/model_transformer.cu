@@ -90,6 +90,7 @@ public:
     double stash_bytes() const override { return recompute_ ? static_cast<double>(boundary_bytes()) : stash_bytes_; }
     int data_capacity() const override { return capacity_; }
     void bind_stream(cudaStream_t s) override { stream_ = s; }
+    void bind_data_stream(cudaStream_t s) override { data_stream_ = s; }
     void grad_buffer(void** ptr, size_t* count, int* dtype) override {
         *ptr = grad_;
         *count = nparam_;
@@ -172,12 +173,13 @@ public:
     // inputs: int32 [count][T] token ids (stage 0); targets: int32 [count][R] (last stage).
     void set_data(const void* inputs, const void* targets, int first_mb, int count) override {
         if (count < 1) throw Error("set_data: empty microbatch range");
+        const cudaStream_t ds = data_stream_ ? data_stream_ : stream_;
         if (capacity_ == 0) {
             capacity_ = std::max(count, 2 * cfg_.microbatches);
             ids_ = dalloc<int>(static_cast<size_t>(capacity_) * T_);
             tgt_ = dalloc<int>(static_cast<size_t>(capacity_) * R_);
             loss_ = dalloc<float>(static_cast<size_t>(capacity_));
-            check_cuda(cudaMemsetAsync(loss_, 0, sizeof(float) * capacity_, stream_), "memset loss");
+            check_cuda(cudaMemsetAsync(loss_, 0, sizeof(float) * capacity_, ds), "memset loss");
         }
         if (count > capacity_) throw Error("set_data: more microbatches than the data ring holds");
         for (int i = 0; i < count; ++i) {
@@ -185,11 +187,11 @@ public:
             if (inputs)
                 check_cuda(cudaMemcpyAsync(ids_ + static_cast<size_t>(slot) * T_,
                                            static_cast<const int*>(inputs) + static_cast<size_t>(i) * T_,
-                                           sizeof(int) * T_, cudaMemcpyHostToDevice, stream_), "H2D ids");
+                                           sizeof(int) * T_, cudaMemcpyHostToDevice, ds), "H2D ids");
             if (targets)
                 check_cuda(cudaMemcpyAsync(tgt_ + static_cast<size_t>(slot) * R_,
                                            static_cast<const int*>(targets) + static_cast<size_t>(i) * R_,
-                                           sizeof(int) * R_, cudaMemcpyHostToDevice, stream_), "H2D targets");
+                                           sizeof(int) * R_, cudaMemcpyHostToDevice, ds), "H2D targets");
         }
     }
 
@@ -545,6 +547,7 @@ private:
     bf16* rc_out_ = nullptr;
     int h_ = 0, heads_ = 0, seq_ = 0, b_ = 0, vocab_ = 0, vp_ = 0, T_ = 0, R_ = 0, rows_per_seq_ = 0;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t data_stream_ = nullptr;  // set_data copies (the forward stream), else stream_
     std::vector<void*> allocs_;
     std::vector<LayerOff> lay_;
     size_t off_tok_ = 0, off_pos_ = 0, off_lnfg_ = 0, off_lnfb_ = 0, off_head_ = 0, nparam_ = 0;
