@@ -386,26 +386,41 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             const int m0 = ((tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
             const int n0 = ((tile / tiles_mg) * kNP + pair) * BN;
             const int r0 = m0 + q * 32;
+            // Side inputs (residual / GELU pre-activation) do not depend on the
+            // accumulator: the warp's (<= 2) chunks of them are TMA-prefetched into its
+            // two staging buffers before waiting for the MMA, hiding their latency.
+            bool aux_pending = false;
+            if (need_aux) {
+                if (lane == 0) ptx::bulk_wait_read<0>();  // both buffers read out by earlier stores
+                __syncwarp();
+                int bytes = 0;
+                for (int c = ch, j = 0; c < BN / W && j < 2; c += kEW / 4, ++j)
+                    if (n0 + c * W < p.n && r0 < p.m) bytes += kEpiBuf;
+                aux_pending = bytes > 0;
+                if (lane == 0 && bytes > 0) {
+                    ptx::mbar_arrive_expect_tx(&aux_bar[ew], bytes);
+                    for (int c = ch, j = 0; c < BN / W && j < 2; c += kEW / 4, ++j)
+                        if (n0 + c * W < p.n && r0 < p.m)
+                            ptx::tma_load_2d(ebuf + j * kEpiBuf, &em.aux, &aux_bar[ew], n0 + c * W, r0);
+                }
+            }
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase =
                 tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+            int jj = 0;  // index of this warp's chunk within the tile
 #pragma unroll 1
-            for (int c = ch; c < BN / W; c += kEW / 4) {
+            for (int c = ch; c < BN / W; c += kEW / 4, ++jj) {
                 const int col0 = n0 + c * W;
                 if (col0 >= p.n || r0 >= p.m) continue;  // warp-uniform: whole chunk out of range
-                uint8_t* buf = ebuf + slot * kEpiBuf;
-                // the buffer's previous bulk store must have finished reading it
-                if (lane == 0) {
-                    if (two_out) ptx::bulk_wait_read<0>();
-                    else ptx::bulk_wait_read<1>();
-                }
-                __syncwarp();
-                if (need_aux) {
+                uint8_t* buf = ebuf + (need_aux ? jj : slot) * kEpiBuf;
+                if (!need_aux) {
+                    // the buffer's previous bulk store must have finished reading it
                     if (lane == 0) {
-                        ptx::mbar_arrive_expect_tx(&aux_bar[ew], kEpiBuf);
-                        ptx::tma_load_2d(buf, &em.aux, &aux_bar[ew], col0, r0);
+                        if (two_out) ptx::bulk_wait_read<0>();
+                        else ptx::bulk_wait_read<1>();
                     }
+                    __syncwarp();
                 }
                 float x[W];
                 {
@@ -431,7 +446,11 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                         *reinterpret_cast<float4*>(buf + ptx::swz128(lane, j)) =
                             make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
                 } else {
-                    if (need_aux) ptx::mbar_wait(&aux_bar[ew], aux_phase), aux_phase ^= 1;
+                    if (need_aux && aux_pending) {  // once per tile: both prefetched chunks
+                        ptx::mbar_wait(&aux_bar[ew], aux_phase);
+                        aux_phase ^= 1;
+                        aux_pending = false;
+                    }
                     if (kKind == EpiKind::StoreBF16 && e.bias != nullptr) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
