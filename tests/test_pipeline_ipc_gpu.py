@@ -118,3 +118,11 @@ def test_unconnected_remote_stage_is_an_error():
             eng.read_version(1, 0)
     finally:
         eng.close()
+
+
+def test_nccl_runtime_loads_on_the_gpu_box():
+    """The data-parallel path dlopens libnccl.so.2 (torch's copy) at run time: the
+    unique id that rank 0 shares with the replicas must come out of it."""
+    from paper_2006_09503_b200 import dist as D
+    a, b = D.nccl_unique_id(), D.nccl_unique_id()
+    assert len(a) == D.UNIQUE_ID_BYTES and a != b
