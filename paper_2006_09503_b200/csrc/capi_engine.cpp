@@ -130,10 +130,12 @@ int p2bw_engine_set_data(p2bw_engine* eng, const void* inputs, const void* targe
         if (e.is_local(0)) {
             e.before_data_set(0);
             e.model(0).set_data(inputs, e.depth() == 1 ? targets : nullptr, first_mb, count);
+            e.after_data_set(0, first_mb, count);
         }
         if (e.depth() > 1 && e.is_local(e.depth() - 1)) {
             e.before_data_set(e.depth() - 1);
             e.model(e.depth() - 1).set_data(nullptr, targets, first_mb, count);
+            e.after_data_set(e.depth() - 1, first_mb, count);
         }
     });
 }

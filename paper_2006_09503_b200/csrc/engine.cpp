@@ -128,7 +128,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
                        "cudaStreamCreate");
             if (overlap) {
                 check_cuda(cudaStreamCreateWithFlags(&st.fstream, cudaStreamNonBlocking), "cudaStreamCreate(fwd)");
-                check_cuda(cudaEventCreateWithFlags(&st.fsync, cudaEventDisableTiming), "cudaEventCreate(fsync)");
+                check_cuda(cudaStreamCreateWithFlags(&st.dstream, cudaStreamNonBlocking), "cudaStreamCreate(data)");
             }
             check_cuda(cudaEventCreate(&st.t0), "cudaEventCreate");
             check_cuda(cudaEventCreate(&st.t1), "cudaEventCreate");
@@ -142,7 +142,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
                 throw Error("unknown model kind " + std::to_string(cfg_.model_kind));
             }
             st.model->bind_stream(st.stream);
-            if (st.fstream) st.model->bind_data_stream(st.fstream);
+            if (st.dstream) st.model->bind_data_stream(st.dstream);
             // Receive block: [act ring][grad ring][flags], one allocation so that a
             // single IPC handle exports it.
             const size_t nb = st.model->boundary_bytes();
@@ -285,8 +285,8 @@ void Engine::free_buffers() {
         st.comm = nullptr;
         if (st.fstream) cudaStreamSynchronize(st.fstream), cudaStreamDestroy(st.fstream);
         st.fstream = nullptr;
-        if (st.fsync) cudaEventDestroy(st.fsync);
-        st.fsync = nullptr;
+        if (st.dstream) cudaStreamSynchronize(st.dstream), cudaStreamDestroy(st.dstream);
+        st.dstream = nullptr;
         if (st.t0) cudaEventDestroy(st.t0);
         if (st.t1) cudaEventDestroy(st.t1);
         if (st.stream) cudaStreamDestroy(st.stream);
@@ -302,9 +302,10 @@ struct EventTable {
     std::vector<std::map<int, cudaEvent_t>> fwd, bwd;
     std::vector<std::map<int, cudaEvent_t>> cpf, cpb;  // sends to remote neighbours done
     std::vector<std::vector<cudaEvent_t>> upd;
-    explicit EventTable(size_t d) : fwd(d), bwd(d), cpf(d), cpb(d), upd(d) {}
+    std::vector<std::map<int, cudaEvent_t>> data;  // data-ring copy of microbatch k done
+    explicit EventTable(size_t d) : fwd(d), bwd(d), cpf(d), cpb(d), upd(d), data(d) {}
     ~EventTable() {
-        for (auto* t : {&fwd, &bwd, &cpf, &cpb})
+        for (auto* t : {&fwd, &bwd, &cpf, &cpb, &data})
             for (auto& m : *t)
                 for (auto& kv : m) cudaEventDestroy(kv.second);
         for (auto& v : upd)
@@ -370,10 +371,8 @@ void Engine::issue_forward(Stage& st, const OpRec& op) {
     const bool prev_remote = s > 0 && !stages_[s - 1].local;
     const bool next_remote = s + 1 < d && !stages_[s + 1].local;
     const cudaStream_t fs = op_stream(st, P2BW_OP_FORWARD);
-    if (st.fstream && fs != st.fstream) {  // profiling: forwards on `stream`, data copies on fstream
-        check_cuda(cudaEventRecord(st.fsync, st.fstream), "cudaEventRecord(fsync)");
-        check_cuda(cudaStreamWaitEvent(fs, st.fsync, 0), "cudaStreamWaitEvent(fsync)");
-    }
+    if (st.fstream && ev_->data[static_cast<size_t>(s)].count(k))  // this microbatch's data copy
+        wait_on(ev_->data[static_cast<size_t>(s)], k, fs);
     if (st.fstream) {
         // what the single stream ordered implicitly: the update that produced version
         // v, the backward that last held this stash slot, and this stage's data
@@ -663,6 +662,7 @@ void Engine::sync() {
         DeviceGuard g(st.device);
         check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
         if (st.fstream) check_cuda(cudaStreamSynchronize(st.fstream), "cudaStreamSynchronize");
+        if (st.dstream) check_cuda(cudaStreamSynchronize(st.dstream), "cudaStreamSynchronize");
         if (st.copy_fwd) check_cuda(cudaStreamSynchronize(st.copy_fwd), "cudaStreamSynchronize");
         if (st.copy_bwd) check_cuda(cudaStreamSynchronize(st.copy_bwd), "cudaStreamSynchronize");
     }
@@ -739,11 +739,27 @@ cudaStream_t Engine::op_stream(const Stage& st, int kind) const {
 
 void Engine::before_data_set(int s) {
     Stage& st = local_stage(s);
-    if (!st.fstream || !ev_ || st.last_bwd < 1) return;
+    if (!st.dstream || !ev_ || st.last_bwd < 1) return;
     const auto& be = ev_->bwd[static_cast<size_t>(st.index)];
     if (!be.count(st.last_bwd)) return;
     DeviceGuard g(st.device);
-    wait_on(be, st.last_bwd, st.fstream);
+    wait_on(be, st.last_bwd, st.dstream);
+}
+
+void Engine::after_data_set(int s, int first_mb, int count) {
+    Stage& st = local_stage(s);
+    if (!st.dstream) return;
+    DeviceGuard g(st.device);
+    if (!ev_) {  // before the first run: nothing waits on events, finish the copies now
+        check_cuda(cudaStreamSynchronize(st.dstream), "cudaStreamSynchronize(data)");
+        return;
+    }
+    auto& de = ev_->data[static_cast<size_t>(st.index)];
+    for (int k = first_mb; k < first_mb + count; ++k) {
+        auto it = de.find(k);
+        if (it != de.end()) cudaEventDestroy(it->second), de.erase(it);
+        record(de, k, st.dstream);
+    }
 }
 
 void Engine::trace_split(Stage& st, const OpRec& first_part) {

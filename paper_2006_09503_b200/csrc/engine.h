@@ -176,10 +176,12 @@ public:
     // Losses of microbatches [first_mb, first_mb + count) (last stage), after sync.
     std::vector<double> losses(int first_mb, int count);
     void copy_losses_async(float* host, int first_mb, int count);
-    // Before the host refills stage s's data ring: with a forward stream the copies run
-    // on it (ordered before later Forwards), after every Backward issued so far (stage
-    // 0's embedding gradient reads the token ids of the slots being overwritten).
+    // Around the host's refill of stage s's data ring: with a forward stream the copies
+    // run on a data stream, after every Backward issued so far (stage 0's embedding
+    // gradient reads the token ids of the slots being overwritten), and each Forward
+    // waits only for the copy of its own microbatch (after_data_set records them).
     void before_data_set(int s);
+    void after_data_set(int s, int first_mb, int count);
     bool is_local(int s) const { return s >= 0 && s < cfg_.depth && stages_[static_cast<size_t>(s)].local; }
     // Measured timeline: with tracing on, every issued op of a
     // local stage is bracketed by CUDA events; trace_report() renders the last run
@@ -206,7 +208,7 @@ private:
         cudaStream_t fstream = nullptr;  // Forward, overlapping the previous microbatch's Backward
         int last_fwd = 0;                // latest microbatch whose Forward was issued
         int last_bwd = 0;                // latest microbatch whose Backward was issued
-        cudaEvent_t fsync = nullptr;     // joins the forward stream into `stream` (profiling)
+        cudaStream_t dstream = nullptr;  // set_data host-to-device copies (with fstream)
         std::unique_ptr<StageModel> model;
         int stash_slots = 1;
         int grad_slots = 1;
