@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 
+#include "launch.h"
 #include "profiler.h"
 #include "ptx.cuh"
 #include "tkernels.h"
@@ -98,6 +99,8 @@ __global__ void __launch_bounds__(kThreads, 4)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -272,10 +275,12 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
     dim3 grid(batch * heads, seq / kBQ);
     if (causal) {
         set_smem_once<true>();
-        k_attn_fwd_tc<true><<<grid, kThreads, kSmemTotal, s>>>(tq, tkv, o, lse, seq, heads);
+        launch_pdl(k_attn_fwd_tc<true>, grid, dim3(kThreads), kSmemTotal, s, "k_attn_fwd_tc", tq, tkv, o, lse, seq,
+                   heads);
     } else {
         set_smem_once<false>();
-        k_attn_fwd_tc<false><<<grid, kThreads, kSmemTotal, s>>>(tq, tkv, o, lse, seq, heads);
+        launch_pdl(k_attn_fwd_tc<false>, grid, dim3(kThreads), kSmemTotal, s, "k_attn_fwd_tc", tq, tkv, o, lse, seq,
+                   heads);
     }
     check_cuda(cudaGetLastError(), "attention_fwd_tc");
 }

@@ -31,6 +31,7 @@
 #include <atomic>
 
 #include "kernels.h"
+#include "launch.h"
 #include "profiler.h"
 #include "ptx.cuh"
 #include "tkernels.h"
@@ -139,6 +140,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -411,6 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
                              float* __restrict__ delta, float* __restrict__ nl2, float* __restrict__ dq_acc, int tokens,
                              int seq, int heads) {
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     const int pair = idx >> 3, sub = idx & 7;
     const bool ok = pair < tokens * heads;  // no early return: the shuffles below need every lane
@@ -444,6 +449,8 @@ __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict_
 
 // dq (bf16, x 1/8) = the fp32 accumulator.
 __global__ void k_attn_dq_convert(const float* __restrict__ acc, bf16* __restrict__ dqkv, int tokens, int h) {
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
     const size_t total = static_cast<size_t>(tokens) * h / 8;
     for (size_t v = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; v < total;
          v += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -487,7 +494,8 @@ void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const fl
     const int tokens = batch * seq;
     const int pairs = tokens * heads;
     float* nl2 = dq_acc + static_cast<size_t>(tokens) * h;
-    k_attn_delta<<<(pairs * 8 + 255) / 256, 256, 0, s>>>(o, dout, lse, delta, nl2, dq_acc, tokens, seq, heads);
+    launch_pdl(k_attn_delta, dim3((pairs * 8 + 255) / 256), dim3(256), 0, s, "k_attn_delta", o, dout, lse, delta, nl2,
+               dq_acc, tokens, seq, heads);
     const CUtensorMap tq = make_tmap_bf16_2d(qkv, 3ull * h, static_cast<uint64_t>(tokens), 3ll * h, 64, kT);
     const CUtensorMap tdo = make_tmap_bf16_2d(dout, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 64, kT);
     const CUtensorMap tdq = make_tmap_f32_2d(dq_acc, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 32, 32);
@@ -496,14 +504,16 @@ void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const fl
     const int grid = std::min(items, num_sms());
     if (causal) {
         set_smem_once<true>();
-        k_attn_bwd_tc<true><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, nl2, delta, dqkv, dq_acc, seq, heads, bhn);
+        launch_pdl(k_attn_bwd_tc<true>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq,
+                   static_cast<const float*>(nl2), static_cast<const float*>(delta), dqkv, dq_acc, seq, heads, bhn);
     } else {
         set_smem_once<false>();
-        k_attn_bwd_tc<false><<<grid, kThreads, kSmem, s>>>(tq, tdo, tdq, nl2, delta, dqkv, dq_acc, seq, heads, bhn);
+        launch_pdl(k_attn_bwd_tc<false>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq,
+                   static_cast<const float*>(nl2), static_cast<const float*>(delta), dqkv, dq_acc, seq, heads, bhn);
     }
     const size_t vecs = static_cast<size_t>(tokens) * h / 8;
-    k_attn_dq_convert<<<static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 16u)), 256, 0, s>>>(
-        dq_acc, dqkv, tokens, h);
+    launch_pdl(k_attn_dq_convert, dim3(static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 16u))), dim3(256),
+               0, s, "k_attn_dq_convert", static_cast<const float*>(dq_acc), dqkv, tokens, h);
     check_cuda(cudaGetLastError(), "attention_bwd_tc");
 }
 

@@ -29,6 +29,7 @@
 #include <string>
 
 #include "kernels.h"
+#include "launch.h"
 #include "tkernels.h"
 #include "profiler.h"
 #include "ptx.cuh"
@@ -171,6 +172,8 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
     else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    ptx::pdl_trigger();  // launch.h: the next kernel's prologue may overlap our tail
+    ptx::pdl_wait();     // the previous kernel's outputs (our operands) are complete
 
     if (warp == 0) {
         if (lane == 0) {
@@ -638,13 +641,15 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, con
     cfg.blockDim = dim3(gemm_threads(kEW));
     cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kCl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // launch.h
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     check_cuda(cudaLaunchKernelEx(&cfg, kern, ta, tb, em, p), "gemm_tc_kernel launch");
 }
 

@@ -357,6 +357,17 @@ __device__ __forceinline__ void sts_f4(uint32_t addr, float a, float b, float c,
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
+// ---- programmatic dependent launch (launch.h) ---------------------------------
+
+// Let the next kernel on the stream be scheduled (its CTAs then wait in pdl_wait).
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef P2BW_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// Wait until the previous kernel on the stream has completed and its writes are visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- misc --------------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -10,6 +10,7 @@
 
 #include "profiler.h"
 #include "ptx.cuh"
+#include "launch.h"
 #include "tkernels.h"
 #include "util.h"
 
@@ -117,6 +118,8 @@ struct ReduceOut {
 
 __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ part, int parts, int n,
                                                       ReduceOut outs, int overwrite) {
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
     __shared__ float red[32][9];
     const int cl = threadIdx.x & 7, plane = threadIdx.x >> 3;
     const int col = blockIdx.x * 8 + cl;
@@ -147,7 +150,8 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
 
 void reduce_parts(const float* part, int parts, int n, float* out, bool overwrite, cudaStream_t s) {
     ReduceOut o{{out, nullptr, nullptr}};
-    k_reduce_parts<<<dim3((n + 7) / 8, 1), 256, 0, s>>>(part, parts, n, o, overwrite ? 1 : 0);
+    launch_pdl(k_reduce_parts, dim3((n + 7) / 8, 1), dim3(256), 0, s, "k_reduce_parts", part, parts, n, o,
+               overwrite ? 1 : 0);
 }
 
 // Column statistics of a bf16 matrix, per row-block partials (block = 32 column
@@ -160,6 +164,8 @@ __global__ void __launch_bounds__(256) k_colstats(const bf16* __restrict__ dy, c
                                                   const float* __restrict__ mean, const float* __restrict__ rstd,
                                                   int rows, int n, int ld, int rows_per_block,
                                                   float* __restrict__ part0, float* __restrict__ part1) {
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
     __shared__ float red[8][256 + 8];
     const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
     const int col = blockIdx.x * 256 + cv * 8;
@@ -236,6 +242,8 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
     // two rows per warp: both rows' loads (and gamma / beta) are in flight together and
     // the two rows' reductions interleave (the kernel was latency-bound at one row)
     constexpr int R = 2;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int row0 = warp * R;
     if (row0 >= rows) return;
@@ -355,6 +363,8 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
              bf16* dx, int rows, int h, int G, float* __restrict__ part) {
     extern __shared__ float ln_smem[];  // red [G][h], then the row-sum exchange [G][2][wpr][2]
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = warp / wpr, wi = warp % wpr;
     const int hv = h / 8;
@@ -696,11 +706,11 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
     const int nv = (h / 8 + 31) / 32;
     const int grid = (rows + 15) / 16;  // 8 warps x 2 rows
     switch (nv) {
-        case 1: k_ln_fwd<1><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, rows, h); break;
-        case 2: k_ln_fwd<2><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, rows, h); break;
-        case 3: k_ln_fwd<3><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, rows, h); break;
-        case 4: k_ln_fwd<4><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, rows, h); break;
-        default: k_ln_fwd<8><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, rows, h); break;
+        case 1: launch_pdl(k_ln_fwd<1>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h); break;
+        case 2: launch_pdl(k_ln_fwd<2>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h); break;
+        case 3: launch_pdl(k_ln_fwd<3>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h); break;
+        case 4: launch_pdl(k_ln_fwd<4>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h); break;
+        default: launch_pdl(k_ln_fwd<8>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h); break;
     }
     check_cuda(cudaGetLastError(), "layernorm_fwd");
 }
@@ -716,7 +726,8 @@ void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, c
         if (smem > 48 * 1024)
             check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(ln bwd smem)");
-        kern<<<grid, kLnBwdThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, sh.G, part);
+        launch_pdl(kern, dim3(grid), dim3(kLnBwdThreads), smem, s, "k_ln_bwd", dy, x, mean, rstd, g, dres, dx, rows, h,
+                   sh.G, part);
     };
     switch (sh.wpr) {
         case 1: go(k_ln_bwd<kSum, 1>); break;
@@ -736,7 +747,8 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
     if (dsum) launch_ln_bwd<true>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
     else launch_ln_bwd<false>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, scratch, s);
     ReduceOut o{{dg, db, dsum}};
-    k_reduce_parts<<<dim3((h + 7) / 8, dsum ? 3 : 2), 256, 0, s>>>(scratch, grid, h, o, overwrite ? 1 : 0);
+    launch_pdl(k_reduce_parts, dim3((h + 7) / 8, dsum ? 3 : 2), dim3(256), 0, s, "k_reduce_parts",
+               static_cast<const float*>(scratch), grid, h, o, overwrite ? 1 : 0);
     check_cuda(cudaGetLastError(), "layernorm_bwd");
 }
 
@@ -753,8 +765,9 @@ void colsum_bf16(const bf16* x, int rows, int n, int ld, float* out, bool overwr
     prof::Scope scope("bias_grad", 0.0, 2.0 * rows * n + 8.0 * n, 2, s);
     const int rb = colsum_row_blocks(rows, n);
     const int rpb = (rows + rb - 1) / rb;
-    k_colstats<false><<<dim3((n + 255) / 256, rb), 256, 0, s>>>(x, nullptr, nullptr, nullptr, rows, n, ld, rpb,
-                                                                  scratch, nullptr);
+    launch_pdl(k_colstats<false>, dim3((n + 255) / 256, rb), dim3(256), 0, s, "k_colstats", x,
+               static_cast<const bf16*>(nullptr), static_cast<const float*>(nullptr),
+               static_cast<const float*>(nullptr), rows, n, ld, rpb, scratch, static_cast<float*>(nullptr));
     reduce_parts(scratch, rb, n, out, overwrite, s);
     check_cuda(cudaGetLastError(), "colsum");
 }
