@@ -129,6 +129,10 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             if (overlap) {
                 check_cuda(cudaStreamCreateWithFlags(&st.fstream, cudaStreamNonBlocking), "cudaStreamCreate(fwd)");
                 check_cuda(cudaStreamCreateWithFlags(&st.dstream, cudaStreamNonBlocking), "cudaStreamCreate(data)");
+                // 2BW: AllReduce + WeightUpdate of batch t on their own stream, overlapping the
+                // Backwards of batch t+1 (which accumulate into the other gradient buffer)
+                if (cfg_.policy == P2BW_POLICY_2BW)
+                    check_cuda(cudaStreamCreateWithFlags(&st.ustream, cudaStreamNonBlocking), "cudaStreamCreate(update)");
             }
             check_cuda(cudaEventCreate(&st.t0), "cudaEventCreate");
             check_cuda(cudaEventCreate(&st.t1), "cudaEventCreate");
@@ -143,6 +147,10 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             }
             st.model->bind_stream(st.stream);
             if (st.dstream) st.model->bind_data_stream(st.dstream);
+            if (st.ustream && !st.model->enable_grad_double_buffer()) {
+                cudaStreamDestroy(st.ustream);
+                st.ustream = nullptr;
+            }
             // Receive block: [act ring][grad ring][flags], one allocation so that a
             // single IPC handle exports it.
             const size_t nb = st.model->boundary_bytes();
@@ -287,6 +295,8 @@ void Engine::free_buffers() {
         st.fstream = nullptr;
         if (st.dstream) cudaStreamSynchronize(st.dstream), cudaStreamDestroy(st.dstream);
         st.dstream = nullptr;
+        if (st.ustream) cudaStreamSynchronize(st.ustream), cudaStreamDestroy(st.ustream);
+        st.ustream = nullptr;
         if (st.t0) cudaEventDestroy(st.t0);
         if (st.t1) cudaEventDestroy(st.t1);
         if (st.stream) cudaStreamDestroy(st.stream);
@@ -443,6 +453,12 @@ void Engine::issue_backward(Stage& st, const OpRec& op) {
         if (k > pv.grad_slots) wait_on(ev_->bwd[s - 1], k - pv.grad_slots, st.stream);
         g_out = pv.grad_ring[(k - 1) % pv.grad_slots];
     }
+    if (st.ustream && st.grad_count == 0) {
+        // first Backward of a batch: its gradient buffer was last read by the AllReduce /
+        // WeightUpdate two batches back (update stream)
+        const auto& ue = ev_->upd[static_cast<size_t>(s)];
+        if (ue.size() >= 2) check_cuda(cudaStreamWaitEvent(st.stream, ue[ue.size() - 2], 0), "cudaStreamWaitEvent(grad)");
+    }
     if (trace_on_ && trace_open_) check_cuda(cudaEventRecord(trace_open_, st.stream), "cudaEventRecord(trace)");
     if (cfg_.recompute) {  // Recompute op (simulator.cpp:242-247): the stage input is in its ring slot
         st.model->recompute(k, wslot, sslot, s > 0 ? st.act_ring[sslot] : nullptr, st.stream);
@@ -514,12 +530,13 @@ void Engine::issue_update(Stage& st) {
     if (dst_slot < 0)
         throw Error("stage " + std::to_string(st.index) + ": no free weight buffer for version " +
                     std::to_string(src_version + 1));
+    const cudaStream_t us = update_stream(st);  // after this batch's Backwards (update stream)
     // the new version's buffer may be one an in-flight Forward (own stream) still reads
     if (st.fstream && st.last_fwd > 0 && ev_->fwd[static_cast<size_t>(st.index)].count(st.last_fwd))
-        wait_on(ev_->fwd[static_cast<size_t>(st.index)], st.last_fwd, st.stream);
+        wait_on(ev_->fwd[static_cast<size_t>(st.index)], st.last_fwd, us);
     // gradients are summed over grad_count microbatches (and over the replicas by
     // the AllReduce): divide by both (semantics.cpp:338-340; PAPER §3 "w replicas")
-    st.model->update(src_slot, dst_slot, st.grad_count * st.replicas, st.stream);
+    st.model->update(src_slot, dst_slot, st.grad_count * st.replicas, us);
     st.updates_done += 1;
     st.version_slot[st.updates_done] = dst_slot;
     prune_versions(st);
@@ -528,14 +545,14 @@ void Engine::issue_update(Stage& st) {
     {
         cudaEvent_t e;
         check_cuda(cudaEventCreate(&e), "cudaEventCreate");
-        check_cuda(cudaEventRecord(e, st.stream), "cudaEventRecord");
+        check_cuda(cudaEventRecord(e, us), "cudaEventRecord");
         ev_->upd[static_cast<size_t>(st.index)].push_back(e);
     }
     stats_.max_versions_held =
         std::max(stats_.max_versions_held, static_cast<int>(st.version_slot.size()));
     if (snapshots_on_) {
         std::vector<uint8_t> buf(st.model->weight_bytes_public());
-        st.model->read_weights(dst_slot, buf.data(), buf.size(), st.stream);
+        st.model->read_weights(dst_slot, buf.data(), buf.size(), us);
         st.snaps.push_back(std::move(buf));
     }
 }
@@ -605,8 +622,9 @@ void Engine::issue(int upto_batch) {
                             size_t n = 0;
                             int dt = 0;
                             st.model->grad_buffer(&buf, &n, &dt);
+                            const cudaStream_t us = update_stream(st);
                             nccl_allreduce_sum(buf, n, dt == 1 ? ncclFloat64 : ncclFloat32,
-                                               static_cast<ncclComm_t>(st.comm), st.stream);
+                                               static_cast<ncclComm_t>(st.comm), us);
                         }
                         break;
                     case P2BW_OP_FLUSH:  // ordering is already implied by stream order
@@ -663,6 +681,7 @@ void Engine::sync() {
         check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
         if (st.fstream) check_cuda(cudaStreamSynchronize(st.fstream), "cudaStreamSynchronize");
         if (st.dstream) check_cuda(cudaStreamSynchronize(st.dstream), "cudaStreamSynchronize");
+        if (st.ustream) check_cuda(cudaStreamSynchronize(st.ustream), "cudaStreamSynchronize");
         if (st.copy_fwd) check_cuda(cudaStreamSynchronize(st.copy_fwd), "cudaStreamSynchronize");
         if (st.copy_bwd) check_cuda(cudaStreamSynchronize(st.copy_bwd), "cudaStreamSynchronize");
     }
@@ -692,6 +711,7 @@ std::vector<double> Engine::losses(int first_mb, int count) {
 
 void Engine::read_version(int s, int version, void* host, size_t bytes) {
     Stage& st = local_stage(s);
+    sync();  // updates may run on the update stream
     const auto it = st.version_slot.find(version);
     if (it == st.version_slot.end())
         throw Error("stage " + std::to_string(s) + " no longer holds weight version " +
@@ -731,6 +751,14 @@ void Engine::copy_losses_async(float* host, int first_mb, int count) {
         else if (st.last_fwd > 0 && fe.count(st.last_fwd)) wait_on(fe, st.last_fwd, st.stream);
     }
     st.model->copy_losses_async(host, first_mb, count, st.stream);
+}
+
+cudaStream_t Engine::update_stream(Stage& st) {
+    if (!st.ustream) return st.stream;
+    // the batch's gradient is complete once its last Backward (stage stream) is
+    if (st.last_bwd > 0 && ev_->bwd[static_cast<size_t>(st.index)].count(st.last_bwd))
+        wait_on(ev_->bwd[static_cast<size_t>(st.index)], st.last_bwd, st.ustream);
+    return st.ustream;
 }
 
 cudaStream_t Engine::op_stream(const Stage& st, int kind) const {

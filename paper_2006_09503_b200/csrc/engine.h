@@ -104,6 +104,10 @@ public:
     virtual void bind_stream(cudaStream_t s) { (void)s; }
     // Stream for set_data's host-to-device copies (default: the bound stream).
     virtual void bind_data_stream(cudaStream_t s) { (void)s; }
+    // Two coalesced-gradient buffers used alternately per batch, so the AllReduce and
+    // WeightUpdate of batch t (update stream) overlap the Backwards of batch t+1.
+    // Returns false if the model keeps a single buffer.
+    virtual bool enable_grad_double_buffer() { return false; }
     // The coalesced gradient buffer (all-reduced across data-parallel replicas).
     // dtype: 0 = fp32, 1 = fp64.
     virtual void grad_buffer(void** ptr, size_t* count, int* dtype) = 0;
@@ -209,6 +213,7 @@ private:
         int last_fwd = 0;                // latest microbatch whose Forward was issued
         int last_bwd = 0;                // latest microbatch whose Backward was issued
         cudaStream_t dstream = nullptr;  // set_data host-to-device copies (with fstream)
+        cudaStream_t ustream = nullptr;  // AllReduce + WeightUpdate (2BW with double-buffered gradients)
         std::unique_ptr<StageModel> model;
         int stash_slots = 1;
         int grad_slots = 1;
@@ -248,6 +253,8 @@ private:
     // Forwards run on the forward stream, except while per-launch profiling is on
     // (the roofline wants every launch timed alone).
     cudaStream_t op_stream(const Stage& st, int kind) const;
+    // Stream of AllReduce / WeightUpdate, ordered after the stage's last issued Backward.
+    cudaStream_t update_stream(Stage& st);
     void trace_split(Stage& st, const OpRec& first_part);  // close first_part, open the rest
 
     void issue_forward(Stage& st, const OpRec& op);

@@ -91,6 +91,13 @@ public:
     int data_capacity() const override { return capacity_; }
     void bind_stream(cudaStream_t s) override { stream_ = s; }
     void bind_data_stream(cudaStream_t s) override { data_stream_ = s; }
+    bool enable_grad_double_buffer() override {
+        if (!grad_bufs_[1]) {
+            grad_bufs_[1] = dalloc<float>(nparam_);
+            check_cuda(cudaMemset(grad_bufs_[1], 0, nparam_ * sizeof(float)), "memset");
+        }
+        return true;
+    }
     void grad_buffer(void** ptr, size_t* count, int* dtype) override {
         *ptr = grad_;
         *count = nparam_;
@@ -345,10 +352,20 @@ public:
             adam_update(master_, vel_, vel2_, grad_, wbf_[dst_slot], nparam_, 1.0f / grad_count,
                         static_cast<float>(cfg_.lr), static_cast<float>(cfg_.momentum), static_cast<float>(cfg_.beta2),
                         static_cast<float>(cfg_.eps), ++adam_step_, s);
+            flip_grad();
             return;
         }
         sgd_momentum_update(master_, vel_, grad_, wbf_[dst_slot], nparam_, 1.0f / grad_count,
                             static_cast<float>(cfg_.lr), static_cast<float>(cfg_.momentum), s);
+        flip_grad();
+    }
+
+    // Next batch accumulates into the other buffer (when double-buffered).
+    void flip_grad() {
+        if (grad_bufs_[1]) {
+            grad_cur_ ^= 1;
+            grad_ = grad_bufs_[grad_cur_];
+        }
     }
 
 private:
@@ -403,7 +420,7 @@ private:
             vel2_ = dalloc<float>(nparam_);
             check_cuda(cudaMemset(vel2_, 0, nparam_ * sizeof(float)), "memset");
         }
-        grad_ = dalloc<float>(nparam_);
+        grad_ = grad_bufs_[0] = dalloc<float>(nparam_);
         scratch_f32_ = dalloc<float>(nparam_);
         for (int i = 0; i < wslots_; ++i) wbf_.push_back(dalloc<bf16>(nparam_));
         check_cuda(cudaMemset(master_, 0, nparam_ * sizeof(float)), "memset");
@@ -553,6 +570,8 @@ private:
     size_t off_tok_ = 0, off_pos_ = 0, off_lnfg_ = 0, off_lnfb_ = 0, off_head_ = 0, nparam_ = 0;
     float *master_ = nullptr, *vel_ = nullptr, *grad_ = nullptr, *scratch_f32_ = nullptr;
     float* vel2_ = nullptr;  // Adam second moment
+    float* grad_bufs_[2] = {nullptr, nullptr};  // coalesced gradient, double-buffered per batch (2BW)
+    int grad_cur_ = 0;
     int adam_step_ = 0;
     std::vector<bf16*> wbf_;
     std::vector<Slot> slots_;
