@@ -29,3 +29,16 @@ for pol in (P.PipelinePolicy.TwoBW, P.PipelinePolicy.PipeDreamFlush):
     (out / f"plan_gpt2.2b_8xb200_{tag}.json").write_text(json.dumps(P.plan(prof, cluster, 512, pol), indent=1))
     (out / f"plan_gpt2.2b_8xb200_{tag}.txt").write_text(P.plan_text(prof, cluster, 512, pol))
 print(json.dumps({"profile_s": round(t1 - t0, 1), "plan_2bw": P.plan(prof, cluster, 512)["best"]}))
+
+# validate_plan-style closure (planner.cpp:101-120) on what one GPU can measure:
+# BERT-base blocks profiled here, planned for a 1-GPU "cluster", against the measured
+# bench throughput of the same configuration.
+prof_b = P.profile_blocks(layers=12, hidden=768, heads=12, seq_len=512, vocab=30522, causal=0, head_rows=77,
+                          microbatch_sizes=(4, 8, 16), warmup=2, iters=5, name="bert-base")
+one = json.dumps({"total_workers": 1, "gpus_per_server": 1, "bandwidth_high_gbps": 900.0,
+                  "bandwidth_low_gbps": 50.0, "memory_capacity_gb": 180.0})
+plan1 = P.plan(prof_b, one, 64)
+(out / "profile_bert-base_b200.json").write_text(prof_b)
+(out / "plan_bert-base_1xb200.json").write_text(json.dumps(plan1, indent=1))
+print(json.dumps({"bert_base_1gpu_predicted_samples_per_s": plan1["predicted_throughput"],
+                  "bert_base_1gpu_best": plan1["best"]}))
