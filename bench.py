@@ -318,8 +318,12 @@ def run_ours(args, c):
         if prof_json.exists():
             traffic = json.loads(prof_json.read_text()).get(args.config)
         roofline = {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, all GEMM launches of a step)",
-                    "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                    "frac": round(achieved / peak, 4), "peak_kind": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
+                    # the GEMMs run inside a long step (the sw_power_cap regime), so the
+                    # denominator is the sustained bf16 figure; the burst one is kept beside it
+                    "achieved": round(achieved, 1), "peak": peak_sus, "unit": "TFLOP/s",
+                    "frac": round(achieved / peak_sus, 4),
+                    "peak_kind": f"{peak_kind} sustained bf16 (MEASURED_PEAKS.json: back-to-back 8192^3 for 4 s)",
+                    "peak_burst": peak, "frac_of_burst": round(achieved / peak, 4),
                     "traffic": traffic,
                     "flops_per_launch": gemm["flops"] / max(gemm["launches"], 1),
                     "avg_launch_us": 1e3 * gemm["ms"] / max(gemm["launches"], 1),
