@@ -124,15 +124,14 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             st.local = s >= lo_local && s < hi_local;
             if (!st.local) continue;  // another process runs it; connect_stage maps its block
             DeviceGuard g(st.device);
-            check_cuda(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking),
-                       "cudaStreamCreate");
+            st.stream = make_stage_stream("main");
             if (overlap) {
-                check_cuda(cudaStreamCreateWithFlags(&st.fstream, cudaStreamNonBlocking), "cudaStreamCreate(fwd)");
-                check_cuda(cudaStreamCreateWithFlags(&st.dstream, cudaStreamNonBlocking), "cudaStreamCreate(data)");
+                st.fstream = make_stage_stream("fwd");
+                st.dstream = make_stage_stream("data");
                 // 2BW: AllReduce + WeightUpdate of batch t on their own stream, overlapping the
                 // Backwards of batch t+1 (which accumulate into the other gradient buffer)
                 if (cfg_.policy == P2BW_POLICY_2BW)
-                    check_cuda(cudaStreamCreateWithFlags(&st.ustream, cudaStreamNonBlocking), "cudaStreamCreate(update)");
+                    st.ustream = make_stage_stream("update");
             }
             check_cuda(cudaEventCreate(&st.t0), "cudaEventCreate");
             check_cuda(cudaEventCreate(&st.t1), "cudaEventCreate");

@@ -486,7 +486,7 @@ private:
         side_red_floats_ = static_cast<int64_t>(std::max({colsum_scratch_floats(T_, 4 * h_), colsum_scratch_floats(T_, h_),
                                                           static_cast<size_t>(T_ / 512 + 1) * 4 * h}));
         side_red_ = dalloc<float>(static_cast<size_t>(side_red_floats_));
-        check_cuda(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking), "cudaStreamCreate(side)");
+        side_stream_ = make_stage_stream("side");
         side_ = side_stream_;
         for (cudaEvent_t& e : ev_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     }
