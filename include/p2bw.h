@@ -316,6 +316,10 @@ int p2bw_kernel_layernorm_bwd(const void* dy, const void* x, const void* mean, c
 /* Debug: per-CTA phase clocks of the tcgen05 attention forward (16 uint64 per CTA)
  * and backward (64 uint64 per CTA) into a device buffer (NULL switches it off). */
 int p2bw_debug_attention_timing(void* dev_buf);
+/* Debug: per-CTA phase timestamps (%globaltimer ns) of the tcgen05 GEMM, 8 uint64 per
+ * CTA: entry, setup done, last load issued, first stage consumed, last MMA commit,
+ * first accumulator seen by the epilogue, epilogue done, teardown done (NULL = off). */
+int p2bw_debug_gemm_timing(void* dev_buf);
 /* Column sums of a bf16 matrix (bias gradients): out (=|+=) sum_r x[r, :]. */
 int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream);
 /* Fused softmax cross-entropy: logits [rows x vp] -> dlogits in place, row_loss [rows]. */

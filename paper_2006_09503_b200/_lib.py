@@ -105,6 +105,7 @@ def _signatures():
         ("p2bw_kernel_softmax_xent", i, [vp, vp, i, i, i, C.c_float, vp, vp]),
         ("p2bw_kernel_colsum", i, [vp, i, i, i, vp, i, vp]),
         ("p2bw_debug_attention_timing", i, [vp]),
+        ("p2bw_debug_gemm_timing", i, [vp]),
     ]
 
 

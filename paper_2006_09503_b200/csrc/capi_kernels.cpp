@@ -102,6 +102,10 @@ extern "C" int p2bw_debug_attention_timing(void* dev_buf) {
     });
 }
 
+extern "C" int p2bw_debug_gemm_timing(void* dev_buf) {
+    return guarded([&] { gemm_debug_timing(static_cast<unsigned long long*>(dev_buf)); });
+}
+
 extern "C" int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream) {
     return guarded([&] {
         float* scratch = nullptr;

@@ -102,6 +102,22 @@ struct EpiMaps {
 // Byte offset of 16-byte chunk j of row r in a 128 B-row SW128 staging buffer.
 
 
+// Phase timestamps (debug; null in production): p2bw_debug_gemm_timing.  Per CTA 8
+// u64 of %globaltimer (ns, comparable across SMs): [0] entry, [1] setup done (barriers,
+// TMEM, PDL wait), [2] producer issued its last load, [3] MMA saw its first full stage,
+// [4] MMA issued its last commit, [5] epilogue warp 4 saw its first accumulator,
+// [6] epilogue warp 4 done (stores read out), [7] teardown done.
+__device__ unsigned long long* g_gemm_dbg = nullptr;
+
+__device__ __forceinline__ void gmark(int k) {
+    unsigned long long* p = g_gemm_dbg;
+    if (p != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p[blockIdx.x * 8 + k] = t;
+    }
+}
+
 // kCl == 2: a CTA pair (cluster of 2) computes one 256 x BN tile with cta_group::2
 // MMAs issued by the even CTA: each CTA TMA-loads its own 128 A rows and half of the
 // B tile into its SMEM (completing on the leader's full barrier), the accumulator
@@ -146,6 +162,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
     const int w0 = blockIdx.x / kCl, wstep = gridDim.x / kCl;
     const uint16_t pair_mask = static_cast<uint16_t>(kPair ? (0x3 << (2 * pair)) : 0x1);  // my pair's CTAs
     constexpr uint16_t kAllMask = kCl == 4 ? 0xF : (kCl == 2 ? 0x3 : 0x1);
+    if (threadIdx.x == 0) gmark(0);
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmap_a);
@@ -174,6 +191,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
     const uint32_t tmem_base = *tmem_slot;
     ptx::pdl_trigger();  // launch.h: the next kernel's prologue may overlap our tail
     ptx::pdl_wait();     // the previous kernel's outputs (our operands) are complete
+    if (threadIdx.x == 0) gmark(1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -254,6 +272,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                     }
                 }
             }
+            gmark(2);
         }
     } else if (warp == 1) {
         if (lane == 0 && prank == 0) {  // pair mode: the even CTA issues for both
@@ -279,6 +298,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full_bar[stage], phase);
                     ptx::tc_fence_after();
+                    if (w == w0 && kb == kb0) gmark(3);
                     const uint32_t a_addr = ptx::smem_u32(s_a + stage * Cfg::kABytes);
                     const uint32_t b_addr = ptx::smem_u32(s_b + stage * Cfg::kBBytes);
 #pragma unroll
@@ -305,6 +325,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                     acc_phase ^= 1;
                 }
             }
+            gmark(4);
         }
     } else if ((warp == 2 || warp == 3) && p.rsum != nullptr) {
         // Row sums of A while it sits in SMEM (the bias gradient rides on the wgrad):
@@ -409,6 +430,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             }
             ptx::mbar_wait(&tfull_bar[acc], acc_phase);
             ptx::tc_fence_after();
+            if (ew == 0 && lane == 0 && w == w0) gmark(5);
             const uint32_t tbase =
                 tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
             int jj = 0;  // index of this warp's chunk within the tile
@@ -546,6 +568,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
         }
         if (lane == 0) ptx::bulk_wait_read<0>();
         __syncwarp();
+        if (ew == 0 && lane == 0) gmark(6);
     }
     ptx::tc_fence_before();
     if constexpr (kPair) ptx::cluster_sync();  // no CTA exits while its peer may still signal it
@@ -555,7 +578,16 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
         if constexpr (kPair) ptx::tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
         else ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
     }
+    if (threadIdx.x == 0) gmark(7);
 }
+
+}  // namespace
+
+void gemm_debug_timing(unsigned long long* dev_buf) {
+    check_cuda(cudaMemcpyToSymbol(g_gemm_dbg, &dev_buf, sizeof(dev_buf)), "cudaMemcpyToSymbol(g_gemm_dbg)");
+}
+
+namespace {
 
 // d[r, c] = bf16(ws[r * n + c]) for an fp32 split-K workspace.
 __global__ void k_cast_f32_bf16_2d(const float* __restrict__ ws, int m, int n, bf16* __restrict__ d, int64_t ldd) {

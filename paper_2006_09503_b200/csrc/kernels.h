@@ -56,6 +56,9 @@ struct GemmEpilogue {
 
 // D[M x N] = A[M x K] . B[N x K]^T on tcgen05 (TMA -> SMEM -> UMMA -> TMEM -> epilogue).
 // Requirements: N % 32 == 0, leading dims multiple of 8 elements, 16-byte aligned pointers.
+// Debug: per-CTA phase timestamps of the GEMM kernel (8 u64 per CTA; null = off).
+void gemm_debug_timing(unsigned long long* dev_buf);
+
 void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
                const GemmEpilogue& epi, cudaStream_t stream);
 

@@ -263,7 +263,8 @@ class Engine:
 
     def close(self):
         if getattr(self, "h", None):
-            _lib.lib().p2bw_engine_destroy(self.h)
+            if _lib is not None:  # None during interpreter shutdown: the process teardown frees it
+                _lib.lib().p2bw_engine_destroy(self.h)
             self.h = None
 
     __del__ = close
