@@ -28,6 +28,21 @@
 #include "tkernels.h"
 
 namespace p2bw {
+
+namespace {
+// Timing diagnostic only (P2BW_DEBUG_DUP bit mask): issue a kernel class twice to read
+// its marginal cost inside the overlapped step.  1 LN fwd, 2 LN bwd, 4 bias colsum,
+// 8 attention fwd, 16 attention bwd, 32 the QKV GEMM.  Duplicates are idempotent except for the
+// accumulated gradients they double -- never set outside timing runs.
+int debug_dup(int bit) {
+    static const int mask = [] {
+        const char* e = std::getenv("P2BW_DEBUG_DUP");
+        return e ? std::atoi(e) : 0;
+    }();
+    return (mask & bit) ? 2 : 1;
+}
+}  // namespace
+
 namespace {
 
 constexpr int kHeadDim = 64;
@@ -222,11 +237,11 @@ public:
         st.xin0 = cur;
         for (int l = 0; l < layers_; ++l) {
             const LayerOff& o = lay_[l];
-            layernorm_fwd(cur, W + o.ln1g, W + o.ln1b, st.xn1[l], st.mean1[l], st.rstd1[l], T_, h_, s);
-            gemm_store(st.xn1[l], h_, T_, W + o.wqkv, 3 * h_, h_, st.qkv[l], W + o.bqkv, nullptr, false, nullptr, s);
-            attention_fwd(st.qkv[l], st.o[l], st.lse[l], b_, seq_, heads_, cfg_.causal != 0, s);
+            for (int dup_ = 0; dup_ < debug_dup(1); ++dup_) layernorm_fwd(cur, W + o.ln1g, W + o.ln1b, st.xn1[l], st.mean1[l], st.rstd1[l], T_, h_, s);
+            for (int dup_ = 0; dup_ < debug_dup(32); ++dup_) gemm_store(st.xn1[l], h_, T_, W + o.wqkv, 3 * h_, h_, st.qkv[l], W + o.bqkv, nullptr, false, nullptr, s);
+            for (int dup_ = 0; dup_ < debug_dup(8); ++dup_) attention_fwd(st.qkv[l], st.o[l], st.lse[l], b_, seq_, heads_, cfg_.causal != 0, s);
             gemm_store(st.o[l], h_, T_, W + o.wo, h_, h_, st.x1[l], W + o.bo, cur, false, nullptr, s);
-            layernorm_fwd(st.x1[l], W + o.ln2g, W + o.ln2b, st.xn2[l], st.mean2[l], st.rstd2[l], T_, h_, s);
+            for (int dup_ = 0; dup_ < debug_dup(1); ++dup_) layernorm_fwd(st.x1[l], W + o.ln2g, W + o.ln2b, st.xn2[l], st.mean2[l], st.rstd2[l], T_, h_, s);
             gemm_store(st.xn2[l], h_, T_, W + o.w1, 4 * h_, h_, st.a[l], W + o.b1, nullptr, true, st.u[l], s);
             bf16* dst = l + 1 < layers_ ? st.x[l + 1] : (last_ ? st.xl : static_cast<bf16*>(x_out));
             gemm_store(st.a[l], 4 * h_, T_, W + o.w2, h_, 4 * h_, dst, W + o.b2, st.x1[l], false, nullptr, s);
@@ -297,12 +312,12 @@ public:
             gemm_wgrad(g4_, 4 * h_, st.xn2[l], h_, 4 * h_, h_, T_, grad_ + o.w1, beta, side_);
             // b1 = colsum(du) as its own pass: summing the A tiles inside the wgrad GEMM
             // (GemmEpilogue::bias_grad) measured no faster, as it rules out CTA-pair tiles
-            colsum_bf16(g4_, T_, 4 * h_, 4 * h_, grad_ + o.b1, first, side_red_, side_);
+            for (int dup_ = 0; dup_ < debug_dup(4); ++dup_) colsum_bf16(g4_, T_, 4 * h_, 4 * h_, grad_ + o.b1, first, side_red_, side_);
             done(kEvDoneB);
             // LN2 (+ residual): dx1 = LN2'(dxn2) + g
             // (+ bo = colsum(dx1), fused)
             wait_side(kEvDoneC, s);  // gB_ free (previous layer's Wo gradient)
-            layernorm_bwd(gX_, st.x1[l], st.mean2[l], st.rstd2[l], W + o.ln2g, g, gB_, grad_ + o.ln2g,
+            for (int dup_ = 0; dup_ < debug_dup(2); ++dup_) layernorm_bwd(gX_, st.x1[l], st.mean2[l], st.rstd2[l], W + o.ln2g, g, gB_, grad_ + o.ln2g,
                           grad_ + o.ln2b, first, T_, h_, red_scratch_, s, grad_ + o.bo);
             fork(kEvGB, s);
             // proj: do = dx1 Wo
@@ -311,19 +326,19 @@ public:
             done(kEvDoneC);
             // attention
             wait_side(kEvDoneD, s);  // g3_ free (previous layer's Wqkv / bqkv gradients)
-            attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
+            for (int dup_ = 0; dup_ < debug_dup(16); ++dup_) attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
                           cfg_.causal != 0, s);
             fork(kEvG3, s);
             // QKV: dxn1 = dqkv Wqkv
             gemm_store_mn_b(g3_, 3 * h_, W + o.wqkv, h_, T_, h_, 3 * h_, gX_, s);
             gemm_wgrad(g3_, 3 * h_, st.xn1[l], h_, 3 * h_, h_, T_, grad_ + o.wqkv, beta, side_);
-            colsum_bf16(g3_, T_, 3 * h_, 3 * h_, grad_ + o.bqkv, first, side_red_, side_);
+            for (int dup_ = 0; dup_ < debug_dup(4); ++dup_) colsum_bf16(g3_, T_, 3 * h_, 3 * h_, grad_ + o.bqkv, first, side_red_, side_);
             done(kEvDoneD);
             // LN1 (+ residual): dx = LN1'(dxn1) + dx1
             bf16* dst = (l > 0 || first_) ? gA_ : static_cast<bf16*>(g_out);
             wait_side(kEvDoneA, s);  // g (gA_) read by this layer's W2 gradient
             // (+ b2 of the layer below = colsum(dx), fused)
-            layernorm_bwd(gX_, x, st.mean1[l], st.rstd1[l], W + o.ln1g, gB_, dst, grad_ + o.ln1g, grad_ + o.ln1b,
+            for (int dup_ = 0; dup_ < debug_dup(2); ++dup_) layernorm_bwd(gX_, x, st.mean1[l], st.rstd1[l], W + o.ln1g, gB_, dst, grad_ + o.ln1g, grad_ + o.ln1b,
                           first, T_, h_, red_scratch_, s, l > 0 ? grad_ + lay_[l - 1].b2 : nullptr);
             g = dst;
         }

@@ -348,21 +348,44 @@ inline LnBwdShape ln_bwd_shape(int h) {
     return {wpr, G};
 }
 
+// SMEM: red [G][h] fp32 | row-sum exchange [G][2][wpr][2] fp32 | row ring [G][NS] x
+// {x, dy, dres} bf16 rows | ring barriers [G][NS].
+inline size_t ln_bwd_fixed_bytes(int h) {
+    const LnBwdShape sh = ln_bwd_shape(h);
+    const size_t f = (static_cast<size_t>(sh.G) * h + static_cast<size_t>(sh.G) * 2 * sh.wpr * 2) * sizeof(float);
+    return (f + 127) & ~static_cast<size_t>(127);
+}
+
+inline int ln_bwd_ring_depth(int h) {
+    const LnBwdShape sh = ln_bwd_shape(h);
+    const size_t per = static_cast<size_t>(sh.G) * (3ull * h * 2 + 8);
+    const size_t room = 220 * 1024 - ln_bwd_fixed_bytes(h);
+    return static_cast<int>(std::max<size_t>(2, std::min<size_t>(4, room / per)));
+}
+
 inline size_t ln_bwd_smem_bytes(int h) {
     const LnBwdShape sh = ln_bwd_shape(h);
-    return (static_cast<size_t>(sh.G) * h + static_cast<size_t>(sh.G) * 2 * sh.wpr * 2) * sizeof(float);
+    return ln_bwd_fixed_bytes(h) + static_cast<size_t>(sh.G) * ln_bwd_ring_depth(h) * (3ull * h * 2 + 8);
 }
 
 __device__ __forceinline__ void group_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// LayerNorm backward + residual, persistent: 148 CTAs x G row groups of wpr warps (one
+// row per group at a time, lane = one 8-column vector).  Each group streams its rows
+// (r, r + G * grid, ...) through an NS-deep SMEM ring filled by 1D bulk copies (x, dy,
+// dres rows: NS rows in flight per group without holding them in registers -- the
+// register-prefetch version kept one row in flight and ran at ~2.7 TB/s).
+//   dx = rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)) + dres
+// plus per-CTA partial column sums of dy*xhat (dgamma), dy (dbeta) and, kSum, bf16(dx).
 template <bool kSum, int wpr>
 __global__ void __launch_bounds__(kLnBwdThreads, 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
-             bf16* dx, int rows, int h, int G, float* __restrict__ part) {
-    extern __shared__ float ln_smem[];  // red [G][h], then the row-sum exchange [G][2][wpr][2]
+             bf16* dx, int rows, int h, int G, int NS, int fixed_bytes, float* __restrict__ part) {
+    extern __shared__ __align__(128) uint8_t ln_raw[];
+    float* ln_smem = reinterpret_cast<float*>(ln_raw);
     ptx::pdl_trigger();
     ptx::pdl_wait();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -373,37 +396,55 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     const bool has_res = dres != nullptr;
     const float inv_h = 1.0f / static_cast<float>(h);
     float* xs = ln_smem + static_cast<size_t>(G) * h;
+    const int row_bytes = h * 2;
+    const int stage_bytes = 3 * row_bytes;
+    uint8_t* ring = ln_raw + fixed_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(G) * NS * stage_bytes);
+    const int stride = gridDim.x * G;
+    const int r0 = blockIdx.x * G + grp;
+    const bool leader = grp < G && wi == 0 && lane == 0;
+    auto issue = [&](int i) {  // row i of this group into its ring slot i % NS
+        const int rr = r0 + i * stride;
+        if (rr >= rows) return;
+        uint64_t* bar = &bars[grp * NS + i % NS];
+        uint8_t* dst = ring + (static_cast<size_t>(grp) * NS + i % NS) * stage_bytes;
+        const size_t o = static_cast<size_t>(rr) * h;
+        ptx::mbar_arrive_expect_tx(bar, (has_res ? 3 : 2) * row_bytes);
+        ptx::bulk_load_1d(dst, x + o, row_bytes, bar);
+        ptx::bulk_load_1d(dst + row_bytes, dy + o, row_bytes, bar);
+        if (has_res) ptx::bulk_load_1d(dst + 2 * row_bytes, dres + o, row_bytes, bar);
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < G * NS; ++i) ptx::mbar_init(&bars[i], 1);
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    if (leader)
+        for (int i = 0; i < NS; ++i) issue(i);
     float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (act) load8(g + vi * 8, gv);
     float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0}, as[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
-    const int stride = gridDim.x * G;
-    int r = blockIdx.x * G + grp;
-    uint4 xp = z4, dp = z4, rp = z4;
+    int r = r0;
     float mu = 0.0f, rs = 0.0f;
     if (grp < G && r < rows) {
-        const size_t o = static_cast<size_t>(r) * h + vi * 8;
-        if (act) {
-            xp = *reinterpret_cast<const uint4*>(x + o);
-            dp = *reinterpret_cast<const uint4*>(dy + o);
-            if (has_res) rp = *reinterpret_cast<const uint4*>(dres + o);
-        }
         mu = mean[r];
         rs = rstd[r];
     }
     for (int it = 0; grp < G && r < rows; r += stride, ++it) {
-        // prefetch the next row of this group (independent loads, in flight during the math)
-        uint4 nx = z4, nd = z4, nr = z4;
         float nmu = 0.0f, nrs = 0.0f;
         if (r + stride < rows) {
-            const size_t o = static_cast<size_t>(r + stride) * h + vi * 8;
-            if (act) {
-                nx = *reinterpret_cast<const uint4*>(x + o);
-                nd = *reinterpret_cast<const uint4*>(dy + o);
-                if (has_res) nr = *reinterpret_cast<const uint4*>(dres + o);
-            }
             nmu = mean[r + stride];
             nrs = rstd[r + stride];
+        }
+        const int slot = it % NS;
+        ptx::mbar_wait(&bars[grp * NS + slot], static_cast<uint32_t>((it / NS) & 1));
+        const uint8_t* src = ring + (static_cast<size_t>(grp) * NS + slot) * stage_bytes + vi * 16;
+        uint4 xp = z4, dp = z4, rp = z4;
+        if (act) {
+            xp = *reinterpret_cast<const uint4*>(src);
+            dp = *reinterpret_cast<const uint4*>(src + row_bytes);
+            if (has_res) rp = *reinterpret_cast<const uint4*>(src + 2 * row_bytes);
         }
         float xh[8], dg[8];
         float s1 = 0.0f, s2 = 0.0f;
@@ -432,20 +473,23 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
         s1 = warp_sum(s1);
         s2 = warp_sum(s2);
         if constexpr (wpr > 1) {
-            float* slot = xs + (static_cast<size_t>(grp) * 2 + (it & 1)) * wpr * 2;
+            float* sl = xs + (static_cast<size_t>(grp) * 2 + (it & 1)) * wpr * 2;
             if (lane == 0) {
-                slot[wi * 2] = s1;
-                slot[wi * 2 + 1] = s2;
+                sl[wi * 2] = s1;
+                sl[wi * 2 + 1] = s2;
             }
-            group_bar(1 + grp, wpr * 32);
+            group_bar(1 + grp, wpr * 32);  // also: every warp of the group has read the slot
             s1 = 0.0f;
             s2 = 0.0f;
 #pragma unroll
             for (int w = 0; w < wpr; ++w) {
-                s1 += slot[w * 2];
-                s2 += slot[w * 2 + 1];
+                s1 += sl[w * 2];
+                s2 += sl[w * 2 + 1];
             }
+        } else {
+            __syncwarp();
         }
+        if (leader) issue(it + NS);  // refill the slot just read
         const float m1 = s1 * inv_h, m2 = s2 * inv_h;
         if (act) {
             float o[8];
@@ -473,9 +517,6 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
                 }
             }
         }
-        xp = nx;
-        dp = nd;
-        rp = nr;
         mu = nmu;
         rs = nrs;
     }
@@ -727,7 +768,7 @@ void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, c
             check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(ln bwd smem)");
         launch_pdl(kern, dim3(grid), dim3(kLnBwdThreads), smem, s, "k_ln_bwd", dy, x, mean, rstd, g, dres, dx, rows, h,
-                   sh.G, part);
+                   sh.G, ln_bwd_ring_depth(h), static_cast<int>(ln_bwd_fixed_bytes(h)), part);
     };
     switch (sh.wpr) {
         case 1: go(k_ln_bwd<kSum, 1>); break;
