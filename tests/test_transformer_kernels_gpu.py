@@ -62,7 +62,8 @@ def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
     assert err < 3e-2 * max(1.0, ref.abs().max().item()), err
 
 
-@pytest.mark.parametrize("rows,h", [(300, 256), (1024, 768), (64, 1024), (33, 1920)])
+@pytest.mark.parametrize("rows,h", [(300, 256), (1024, 768), (64, 1024), (33, 1920),
+                                    (20000, 768), (5000, 2048), (9001, 256)])  # ring wrap-around
 @pytest.mark.parametrize("with_dsum", [False, True])
 def test_layernorm_fwd_bwd_vs_torch(rows, h, with_dsum):
     g = torch.Generator(device="cuda").manual_seed(rows + h)
