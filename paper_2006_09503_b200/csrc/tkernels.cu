@@ -356,12 +356,10 @@ inline size_t ln_bwd_fixed_bytes(int h) {
     return (f + 127) & ~static_cast<size_t>(127);
 }
 
-inline int ln_bwd_ring_depth(int h) {
-    const LnBwdShape sh = ln_bwd_shape(h);
-    const size_t per = static_cast<size_t>(sh.G) * (3ull * h * 2 + 8);
-    const size_t room = 220 * 1024 - ln_bwd_fixed_bytes(h);
-    return static_cast<int>(std::max<size_t>(2, std::min<size_t>(4, room / per)));
-}
+// ring depth: G * 3 rows * h * 2 B ~ 24 * 256 * 6 B = 36 KB per slot for every h
+// (G ~ 24 / ceil(h / 256)), so four slots always fit beside the reduction buffer
+constexpr int kLnRing = 4;
+inline int ln_bwd_ring_depth(int) { return kLnRing; }
 
 inline size_t ln_bwd_smem_bytes(int h) {
     const LnBwdShape sh = ln_bwd_shape(h);
@@ -383,7 +381,8 @@ template <bool kSum, int wpr>
 __global__ void __launch_bounds__(kLnBwdThreads, 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
-             bf16* dx, int rows, int h, int G, int NS, int fixed_bytes, float* __restrict__ part) {
+             bf16* dx, int rows, int h, int G, int fixed_bytes, float* __restrict__ part) {
+    constexpr int NS = kLnRing;
     extern __shared__ __align__(128) uint8_t ln_raw[];
     float* ln_smem = reinterpret_cast<float*>(ln_raw);
     ptx::pdl_trigger();
@@ -403,11 +402,12 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     const int stride = gridDim.x * G;
     const int r0 = blockIdx.x * G + grp;
     const bool leader = grp < G && wi == 0 && lane == 0;
-    auto issue = [&](int i) {  // row i of this group into its ring slot i % NS
-        const int rr = r0 + i * stride;
+    uint8_t* my_ring = ring + static_cast<size_t>(grp) * NS * stage_bytes;
+    uint64_t* my_bars = bars + grp * NS;
+    auto issue = [&](int rr, int slot) {  // row rr into ring slot `slot`
         if (rr >= rows) return;
-        uint64_t* bar = &bars[grp * NS + i % NS];
-        uint8_t* dst = ring + (static_cast<size_t>(grp) * NS + i % NS) * stage_bytes;
+        uint64_t* bar = &my_bars[slot];
+        uint8_t* dst = my_ring + slot * stage_bytes;
         const size_t o = static_cast<size_t>(rr) * h;
         ptx::mbar_arrive_expect_tx(bar, (has_res ? 3 : 2) * row_bytes);
         ptx::bulk_load_1d(dst, x + o, row_bytes, bar);
@@ -420,7 +420,8 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     }
     __syncthreads();
     if (leader)
-        for (int i = 0; i < NS; ++i) issue(i);
+#pragma unroll
+        for (int i = 0; i < NS; ++i) issue(r0 + i * stride, i);
     float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (act) load8(g + vi * 8, gv);
     float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0}, as[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -431,15 +432,16 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
         mu = mean[r];
         rs = rstd[r];
     }
+    int slot = 0;
+    uint32_t phase = 0;
     for (int it = 0; grp < G && r < rows; r += stride, ++it) {
         float nmu = 0.0f, nrs = 0.0f;
         if (r + stride < rows) {
             nmu = mean[r + stride];
             nrs = rstd[r + stride];
         }
-        const int slot = it % NS;
-        ptx::mbar_wait(&bars[grp * NS + slot], static_cast<uint32_t>((it / NS) & 1));
-        const uint8_t* src = ring + (static_cast<size_t>(grp) * NS + slot) * stage_bytes + vi * 16;
+        ptx::mbar_wait(&my_bars[slot], phase);
+        const uint8_t* src = my_ring + slot * stage_bytes + vi * 16;
         uint4 xp = z4, dp = z4, rp = z4;
         if (act) {
             xp = *reinterpret_cast<const uint4*>(src);
@@ -489,7 +491,11 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
         } else {
             __syncwarp();
         }
-        if (leader) issue(it + NS);  // refill the slot just read
+        if (leader) issue(r + NS * stride, slot);  // refill the slot just read
+        if (++slot == NS) {
+            slot = 0;
+            phase ^= 1;
+        }
         const float m1 = s1 * inv_h, m2 = s2 * inv_h;
         if (act) {
             float o[8];
@@ -768,7 +774,7 @@ void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, c
             check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(ln bwd smem)");
         launch_pdl(kern, dim3(grid), dim3(kLnBwdThreads), smem, s, "k_ln_bwd", dy, x, mean, rstd, g, dres, dx, rows, h,
-                   sh.G, ln_bwd_ring_depth(h), static_cast<int>(ln_bwd_fixed_bytes(h)), part);
+                   sh.G, static_cast<int>(ln_bwd_fixed_bytes(h)), part);
     };
     switch (sh.wpr) {
         case 1: go(k_ln_bwd<kSum, 1>); break;
