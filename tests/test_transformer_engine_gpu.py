@@ -70,6 +70,27 @@ def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows, seq):
         assert gap > 2 * err, (s, gap, err)  # 2BW is distinguishable from vanilla at this tolerance
 
 
+@pytest.mark.parametrize("depth,layers,batch", [(1, 2, 1), (2, 2, 1), (1, 1, 16)])
+def test_bench_width_layers_match_delayed_oracle(depth, layers, batch):
+    """The bench's layer shape (BERT-base: hidden 768, 12 heads, seq 512, 77 MLM rows per
+    sequence) through the whole engine: the production GEMM tiles (CTA pairs, split-K,
+    fused epilogues), the tcgen05 attention at seq 512, the LayerNorm ring and the
+    side-stream weight gradients, against the float64 oracle.  batch 16 is the bench's
+    microbatch (8192 tokens: the exact tile / split choices of the measured step)."""
+    spec = TO.Spec(layers=layers, hidden=768, heads=12, seq=512, vocab=1000, batch=batch, causal=False,
+                   head_rows=77)
+    m, T, lr, beta, seed = 2, 3, 0.05, 0.9, 99
+    params, ids, tg, losses, finals, c = run_case(spec, depth, m, T, lr, beta, seed)
+    assert c.max_versions_held == 2
+    traj, ref_losses = TO.train(params, spec, ids, tg, lr, beta, m, T, delayed=True)
+    assert np.all(np.abs(losses - ref_losses) <= LOSS_RTOL * np.abs(ref_losses)), (losses, ref_losses)
+    for s in range(depth):
+        w0 = TO.flatten_stage(params, spec, depth, s).astype(np.float64)
+        ref = TO.flatten_stage({k: v.numpy() for k, v in traj[-1].items()}, spec, depth, s).astype(np.float64)
+        err = np.linalg.norm((finals[s] - w0) - (ref - w0)) / np.linalg.norm(ref - w0)
+        assert err < DELTA_RTOL, (s, err)
+
+
 def test_depths_agree_with_each_other():
     spec = TO.Spec(layers=4, hidden=128, heads=2, seq=64, vocab=300, batch=2, causal=True)
     m, T = 4, 3
