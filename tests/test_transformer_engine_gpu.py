@@ -70,15 +70,17 @@ def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows, seq):
         assert gap > 2 * err, (s, gap, err)  # 2BW is distinguishable from vanilla at this tolerance
 
 
-@pytest.mark.parametrize("depth,layers,batch", [(1, 2, 1), (2, 2, 1), (1, 1, 16)])
-def test_bench_width_layers_match_delayed_oracle(depth, layers, batch):
+@pytest.mark.parametrize("depth,layers,batch,hidden,causal,head_rows",
+                         [(1, 2, 1, 768, False, 77), (2, 2, 1, 768, False, 77), (1, 1, 16, 768, False, 77),
+                          (2, 2, 2, 1024, True, 0)])  # the last: GPT-24 / BERT-large width, causal LM head
+def test_bench_width_layers_match_delayed_oracle(depth, layers, batch, hidden, causal, head_rows):
     """The bench's layer shape (BERT-base: hidden 768, 12 heads, seq 512, 77 MLM rows per
     sequence) through the whole engine: the production GEMM tiles (CTA pairs, split-K,
     fused epilogues), the tcgen05 attention at seq 512, the LayerNorm ring and the
     side-stream weight gradients, against the float64 oracle.  batch 16 is the bench's
     microbatch (8192 tokens: the exact tile / split choices of the measured step)."""
-    spec = TO.Spec(layers=layers, hidden=768, heads=12, seq=512, vocab=1000, batch=batch, causal=False,
-                   head_rows=77)
+    spec = TO.Spec(layers=layers, hidden=hidden, heads=hidden // 64, seq=512, vocab=1000, batch=batch,
+                   causal=causal, head_rows=head_rows)
     m, T, lr, beta, seed = 2, 3, 0.05, 0.9, 99
     params, ids, tg, losses, finals, c = run_case(spec, depth, m, T, lr, beta, seed)
     assert c.max_versions_held == 2
