@@ -612,6 +612,107 @@ __global__ void __launch_bounds__(256) k_softmax_xent(bf16* __restrict__ logits,
     }
 }
 
+// Register-resident variant (vp <= 256 * 8 * NVT): the row is read from HBM once into
+// packed bf16 registers; max, then sum of exp2, then the gradient are computed from
+// registers (the two-pass kernel above reads every row twice).  Same row loss and
+// gradient definitions; the max is exact, so only the summation order differs.
+// bf16x2 -> 2 x f32 that the compiler may not hoist or merge across the passes below
+// (a hoisted fp32 copy of the row would double its register footprint)
+__device__ __forceinline__ float2 unpack_bf16x2_opaque(uint32_t w) {
+    uint32_t lo, hi;
+    asm volatile("shl.b32 %0, %1, 16;" : "=r"(lo) : "r"(w));
+    asm volatile("and.b32 %0, %1, 0xffff0000;" : "=r"(hi) : "r"(w));
+    return make_float2(__uint_as_float(lo), __uint_as_float(hi));
+}
+
+template <int NVT>
+__global__ void __launch_bounds__(256) k_softmax_xent_reg(bf16* __restrict__ logits, const int* __restrict__ targets,
+                                                          int vocab, int vp, float grad_scale,
+                                                          float* __restrict__ row_loss) {
+    __shared__ float red[8];
+    __shared__ float s_b;
+    const int row = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    bf16* lr = logits + static_cast<size_t>(row) * vp;
+    const int tgt = targets[row];
+    const int nv = vp / 8;
+    constexpr uint32_t kNegInf2 = 0xFF80FF80u;  // two bf16 -inf: padded columns drop out of every pass
+    uint4 u[NVT];
+#pragma unroll
+    for (int k = 0; k < NVT; ++k) {
+        const int v = threadIdx.x + 256 * k;
+        u[k] = v < nv ? *reinterpret_cast<const uint4*>(lr + v * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+        if (v < nv && v * 8 + 8 > vocab) {  // the vector that straddles the vocabulary end
+            uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+            for (int q = 0; q < 8; ++q)
+                if (v * 8 + q >= vocab) w[q / 2] = (q & 1) ? ((w[q / 2] & 0xFFFFu) | 0xFF800000u) : ((w[q / 2] & 0xFFFF0000u) | 0xFF80u);
+            u[k] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+    const float t_tgt = __bfloat162float(lr[tgt]) * kLog2e;
+    auto block_reduce = [&](float x, bool is_max) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float y = __shfl_xor_sync(0xffffffffu, x, o);
+            x = is_max ? fmaxf(x, y) : x + y;
+        }
+        if (lane == 0) red[warp] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float r = red[0];
+            for (int w = 1; w < 8; ++w) r = is_max ? fmaxf(r, red[w]) : r + red[w];
+            s_b = r;
+        }
+        __syncthreads();
+        const float r = s_b;
+        __syncthreads();  // red / s_b reused by the next reduction
+        return r;
+    };
+    // pass 1: row max
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < NVT; ++k) {
+        const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float2 f = unpack_bf16x2_opaque(w[t]);
+            m = fmaxf(m, fmaxf(f.x, f.y));
+        }
+    }
+    const float M = block_reduce(m, true) * kLog2e;
+    // pass 2: sum of exp2(t - M)
+    float sum = 0.0f;
+#pragma unroll
+    for (int k = 0; k < NVT; ++k) {
+        const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float2 f = unpack_bf16x2_opaque(w[t]);
+            sum += exp2f(fmaf(f.x, kLog2e, -M)) + exp2f(fmaf(f.y, kLog2e, -M));
+        }
+    }
+    const float S = block_reduce(sum, false);
+    const float lse2 = M + log2f(S);
+    if (threadIdx.x == 0) row_loss[row] = (lse2 - t_tgt) / kLog2e;
+    // pass 3: dlogits = (softmax - onehot) * grad_scale, in place
+#pragma unroll
+    for (int k = 0; k < NVT; ++k) {
+        const int v = threadIdx.x + 256 * k;
+        if (v < nv) {
+            const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+            float x[8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float2 f = unpack_bf16x2_opaque(w[t]);
+                x[2 * t] = exp2f(fmaf(f.x, kLog2e, -lse2)) * grad_scale;
+                x[2 * t + 1] = exp2f(fmaf(f.y, kLog2e, -lse2)) * grad_scale;
+            }
+            const int d = tgt - v * 8;
+            if (d >= 0 && d < 8) x[d] -= grad_scale;
+            store8(lr + v * 8, x);
+        }
+    }
+}
+
 __global__ void k_sum_scaled(const float* __restrict__ in, int n, float scale, float* __restrict__ out) {
     __shared__ float red[256];
     float acc = 0.0f;
@@ -823,7 +924,10 @@ void softmax_xent(bf16* logits, const int* targets, int rows, int vocab, int vp,
                   float* row_loss, cudaStream_t s) {
     if (vp % 8 != 0) throw Error("softmax_xent: padded vocab must be a multiple of 8");
     prof::Scope scope("softmax_xent", 0.0, 4.0 * rows * static_cast<double>(vp) + 8.0 * rows, 1, s);
-    k_softmax_xent<<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
+    const int nvt = (vp / 8 + 255) / 256;  // 16-byte vectors per thread for a register-resident row
+    if (nvt <= 16) k_softmax_xent_reg<16><<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
+    else if (nvt <= 32) k_softmax_xent_reg<32><<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
+    else k_softmax_xent<<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
     check_cuda(cudaGetLastError(), "softmax_xent");
 }
 

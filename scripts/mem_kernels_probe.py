@@ -64,4 +64,10 @@ t = bench(lambda: call("p2bw_kernel_layernorm_bwd", P(dy), P(x), P(mean), P(rstd
 out["ln_bwd_us"], out["ln_bwd_gbs"] = round(t, 2), round(8 * T * h / t / 1e3, 1)
 t = bench(lambda: call("p2bw_kernel_colsum", P(u), T, 4 * h, 4 * h, P(bias), 1, s))
 out["colsum_us"], out["colsum_gbs"] = round(t, 2), round(2 * T * 4 * h / t / 1e3, 1)
+R, V, VP = 16 * 77, 30522, 30592  # BERT-base MLM head rows of one microbatch
+logits = torch.randn(R, VP, device="cuda").to(torch.bfloat16)
+tg = torch.randint(0, V, (R,), device="cuda", dtype=torch.int32)
+rl = torch.empty(R, device="cuda")
+t = bench(lambda: call("p2bw_kernel_softmax_xent", P(logits), P(tg), R, V, VP, C.c_float(1.0), P(rl), s))
+out["xent_us"], out["xent_gbs"] = round(t, 2), round(4 * R * VP / t / 1e3, 1)
 print(json.dumps(out))
