@@ -101,7 +101,7 @@ def test_layernorm_fwd_bwd_vs_torch(rows, h, with_dsum):
         assert torch.all(ds == 5.0)
 
 
-@pytest.mark.parametrize("rows,vocab", [(64, 1000), (16, 51200), (130, 30522)])
+@pytest.mark.parametrize("rows,vocab", [(64, 1000), (16, 51200), (130, 30522), (3, 7), (8, 70001)])  # 70001: two-pass path
 def test_softmax_xent_vs_torch(rows, vocab):
     vp = (vocab + 127) // 128 * 128
     g = torch.Generator(device="cuda").manual_seed(rows + vocab)
