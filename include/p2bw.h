@@ -281,10 +281,11 @@ typedef struct {
      * split-K into it and be cast to bf16 afterwards. */
     void* workspace;
     long long workspace_floats;
-    /* Optional (kind 1 with an MN-major A only -- the wgrad): bias_grad[r] (=|+=)
-     * sum over K of A[r, :], i.e. the bias gradient of the layer whose output
-     * gradient A is, summed from the A tiles the GEMM already stages in SMEM;
-     * bias_scratch holds >= (K / 512 + 1) * m floats of per-split partials. */
+    /* Optional: the bias gradient of the layer whose output gradient A is, summed
+     * from the A tiles the GEMM already stages in SMEM.  MN-major A (the wgrad, kind 1):
+     * bias_grad[r] (=|+=) sum over K of A[r, :], bias_scratch >= (K / 512 + 1) * m
+     * floats.  K-major A (the dgrad, any kind): bias_grad[c] (=|+=) sum over M of
+     * A[:, c], bias_scratch >= 2 * ceil(m / 128) * k floats. */
     void* bias_grad;
     int bias_grad_accumulate;
     void* bias_scratch;

@@ -386,6 +386,62 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                     }
                 }
             }
+        } else if constexpr (!kAMN && !kPair) {
+            // Column sums of a K-major A over the tile's rows (the bias gradient rides on
+            // the dgrad, whose A is the layer's output gradient): per stage, the 64
+            // columns of the A box summed over its 128 rows, one partial row per warp
+            // and M tile.  Box layout (K-major SW128): row r is 128 B of 64 K values,
+            // 16-byte chunk c at position c ^ (r & 7).  Lane L of the 64: chunk L & 7 of
+            // rows (L >> 3) + 8 t, so its swizzled chunk position is fixed.
+            const int L = (warp - 2) * 32 + lane;
+            const int c = L & 7, rg = L >> 3;
+            const uint32_t sw = static_cast<uint32_t>((c ^ rg) << 4);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int w = w0; w < num_work; w += wstep) {
+                const int tile = w % num_tiles;
+                const int mt = tile % tiles_mg;
+                const bool active = tile / tiles_mg == 0;  // n0 == 0: each A element counts once
+                const int kb0 = (w / num_tiles) * kb_per;
+                const int kb1 = min(kblocks, kb0 + kb_per);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full_bar[stage], phase);
+                    if (active) {
+                        const uint32_t box = ptx::smem_u32(s_a + stage * Cfg::kABytes) + sw;
+                        float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 4
+                        for (int t = 0; t < kBM / 8; ++t) {
+                            uint32_t v[4];
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                                         : "r"(box + (rg + 8 * t) * 128));
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float2 f = ptx::unpack_bf16x2(v[q]);
+                                acc[2 * q] += f.x;
+                                acc[2 * q + 1] += f.y;
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {  // the warp's four row groups of chunk c
+                            acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 8);
+                            acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
+                        }
+                        const int kc = kb * kBK + 8 * lane;
+                        if (lane < 8 && kc < p.k) {
+                            float* dst = p.rsum + static_cast<size_t>(mt * 2 + (warp - 2)) * p.k + kc;
+                            reinterpret_cast<float4*>(dst)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                            reinterpret_cast<float4*>(dst)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&empty_bar[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
         }
     } else if (warp >= 4) {
         // Epilogue: warp q owns tile rows [32q, 32q+32) (its TMEM lane quarter).  Each
@@ -804,14 +860,16 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         throw Error("gemm: output leading dims must be multiples of 8");
     const bool amn = a.major == Major::MN, bmn = b.major == Major::MN;
     const bool f32 = epi.kind == EpiKind::StoreF32;
-    const bool want_rsum = epi.bias_grad != nullptr;
-    if (want_rsum && !(f32 && amn)) throw Error("gemm: bias_grad needs an fp32 store with an MN-major A (wgrad)");
-    TileChoice tc = choose_tile(m, n, k, f32, bmn, f32, want_rsum);
+    const bool want_rsum = epi.bias_grad != nullptr && amn;   // wgrad: row sums of A over K
+    const bool want_csum = epi.bias_grad != nullptr && !amn;  // dgrad: column sums of A over M
+    if (want_rsum && !f32) throw Error("gemm: bias_grad with an MN-major A needs an fp32 store (wgrad)");
+    if (want_csum && k % 8 != 0) throw Error("gemm: bias_grad with a K-major A needs K % 8 == 0");
+    TileChoice tc = choose_tile(m, n, k, f32, bmn, f32, want_rsum || want_csum);
     // Plain bf16 stores with few output tiles and a long K (the LM-head dgrad: 1232 x 768
     // over K = 30592 fills 60 SMs with 128 x 128 tiles) run split-K into the caller's
     // fp32 workspace and are cast afterwards, when the model says that wins.
     const bool plain = epi.kind == EpiKind::StoreBF16 && !epi.bias && !epi.residual && !epi.gelu && !epi.preact;
-    if (plain && epi.workspace != nullptr && epi.workspace_floats >= static_cast<int64_t>(m) * n &&
+    if (plain && !want_csum && epi.workspace != nullptr && epi.workspace_floats >= static_cast<int64_t>(m) * n &&
         std::getenv("P2BW_GEMM_TILE") == nullptr) {
         TileChoice ts = choose_tile(m, n, k, true, bmn, true);
         // memset + cast: ~10 B per output at HBM speed, in k-block units (~0.26 us each)
@@ -829,7 +887,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         }
     }
     if (!tile_ok(tc.bn, tc.cl, bmn)) tc.cl = 1;
-    if (want_rsum) tc.cl = 1;  // the row-sum warps read a local full barrier (no CTA pairs)
+    if (want_rsum || want_csum) tc.cl = 1;  // the sum warps read a local full barrier (no CTA pairs)
     const int bn = tc.bn, cl = tc.cl;
     // A: rows = m (tile kBM), B: rows = n (tile bn; each CTA of a pair loads bn / 2).
     // K-major maps put k innermost.
@@ -865,9 +923,15 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         }
     }
     float* rsum = nullptr;
+    const int csum_parts = 2 * ((m + kBM - 1) / kBM);  // two warps' partial rows per M tile
     if (want_rsum) {
         if (epi.bias_scratch == nullptr || epi.bias_scratch_floats < static_cast<int64_t>(splits) * m)
             throw Error("gemm: bias_scratch must hold splits * M floats");
+        rsum = epi.bias_scratch;
+    }
+    if (want_csum) {
+        if (epi.bias_scratch == nullptr || epi.bias_scratch_floats < static_cast<int64_t>(csum_parts) * k)
+            throw Error("gemm: bias_scratch must hold 2 * ceil(M / 128) * K floats");
         rsum = epi.bias_scratch;
     }
     KParams p{m, n, k, splits, epi, rsum};
@@ -887,6 +951,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     else if (cl == 2) dispatch_major<128, 2>(amn, bmn, ta, tb, em, p, stream);
     else dispatch_major<128, 1>(amn, bmn, ta, tb, em, p, stream);
     if (want_rsum) reduce_partials(rsum, splits, m, epi.bias_grad, !epi.bias_grad_accumulate, stream);
+    if (want_csum) reduce_partials(rsum, csum_parts, k, epi.bias_grad, !epi.bias_grad_accumulate, stream);
 }
 
 int num_sms() {

@@ -44,10 +44,12 @@ struct GemmEpilogue {
     // with few output tiles and a long K may then run split-K into it and be cast.
     float* workspace = nullptr;
     int64_t workspace_floats = 0;
-    // wgrad only (fp32 store, A MN-major): bias_grad[r] (=|+=) sum over K of A[r, :] --
-    // the bias gradient of the layer whose output gradient A is -- summed from the A
-    // tiles already in SMEM by two otherwise idle warps; bias_scratch holds >= splits * M
-    // floats of partials (splits <= K / 512).
+    // The bias gradient of the layer whose output gradient A is, summed from the A tiles
+    // already in SMEM by two otherwise idle warps (single-CTA tiles):
+    //   A MN-major (wgrad, fp32 store): bias_grad[r] (=|+=) sum over K of A[r, :];
+    //     bias_scratch >= splits * M floats (splits <= K / 512);
+    //   A K-major (dgrad, any store): bias_grad[c] (=|+=) sum over M of A[:, c];
+    //     bias_scratch >= 2 * ceil(M / 128) * K floats.
     float* bias_grad = nullptr;
     bool bias_grad_accumulate = false;
     float* bias_scratch = nullptr;

@@ -205,3 +205,27 @@ def test_gemm_wgrad_fused_bias_grad(m, n, k, accumulate):
     assert (d - ref).abs().max().item() <= 2e-3 * ref.abs().max().item()
     bref = A.float().sum(1) + (bias0 if accumulate else 0)
     assert (bias - bref).abs().max().item() <= 1e-3 * (1 + bref.abs().max().item())
+
+
+@pytest.mark.parametrize("accumulate", [0, 1])
+@pytest.mark.parametrize("m,n,k", [(8192, 768, 3072), (8192, 768, 2304), (300, 256, 1000), (1000, 224, 64)])
+def test_gemm_dgrad_fused_bias_grad(m, n, k, accumulate):
+    """The dgrad GEMM (A K-major = the layer's output gradient, B MN-major = the weight)
+    also sums A over its rows from the SMEM tiles: bias (=|+=) A.sum(M) -- the bias
+    gradient the model used to compute in a separate column-sum pass."""
+    gen = torch.Generator(device="cuda").manual_seed(m + n + k + accumulate + 7)
+    A, a, lda = _operand(m, k, 0, gen)
+    B, b, ldb = _operand(n, k, 1, gen)
+    d = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    bias0 = torch.randn(k, device="cuda", generator=gen)
+    bias = bias0.clone()
+    scratch = torch.full((2 * ((m + 127) // 128) * k,), float("nan"), device="cuda")
+    epi = GemmEpilogue(kind=0, d=d.data_ptr(), ldd=n, alpha=1.0, beta=0.0, bias_grad=bias.data_ptr(),
+                       bias_grad_accumulate=accumulate, bias_scratch=scratch.data_ptr(),
+                       bias_scratch_floats=scratch.numel())
+    _gemm(a, lda, 0, b, ldb, 1, m, n, k, epi)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    assert (d.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+    bref = A.float().sum(0) + (bias0 if accumulate else 0)
+    assert (bias - bref).abs().max().item() <= 1e-3 * (1 + bref.abs().max().item())
