@@ -377,7 +377,7 @@ __device__ __forceinline__ void group_bar(int id, int threads) {
 // register-prefetch version kept one row in flight and ran at ~2.7 TB/s).
 //   dx = rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)) + dres
 // plus per-CTA partial column sums of dy*xhat (dgamma), dy (dbeta) and, kSum, bf16(dx).
-template <bool kSum, int wpr>
+template <bool kSum, int wpr, bool kRes>
 __global__ void __launch_bounds__(kLnBwdThreads, 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     const int hv = h / 8;
     const int vi = wi * 32 + lane;  // my 8-column vector of every row
     const bool act = grp < G && vi < hv;
-    const bool has_res = dres != nullptr;
+    constexpr bool has_res = kRes;  // residual gradient added to dx (compile-time: no per-row branches)
     const float inv_h = 1.0f / static_cast<float>(h);
     float* xs = ln_smem + static_cast<size_t>(G) * h;
     const int row_bytes = h * 2;
@@ -878,11 +878,11 @@ void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, c
                    sh.G, static_cast<int>(ln_bwd_fixed_bytes(h)), part);
     };
     switch (sh.wpr) {
-        case 1: go(k_ln_bwd<kSum, 1>); break;
-        case 2: go(k_ln_bwd<kSum, 2>); break;
-        case 3: go(k_ln_bwd<kSum, 3>); break;
-        case 4: go(k_ln_bwd<kSum, 4>); break;
-        default: go(k_ln_bwd<kSum, 8>); break;
+        case 1: dres ? go(k_ln_bwd<kSum, 1, true>) : go(k_ln_bwd<kSum, 1, false>); break;
+        case 2: dres ? go(k_ln_bwd<kSum, 2, true>) : go(k_ln_bwd<kSum, 2, false>); break;
+        case 3: dres ? go(k_ln_bwd<kSum, 3, true>) : go(k_ln_bwd<kSum, 3, false>); break;
+        case 4: dres ? go(k_ln_bwd<kSum, 4, true>) : go(k_ln_bwd<kSum, 4, false>); break;
+        default: dres ? go(k_ln_bwd<kSum, 8, true>) : go(k_ln_bwd<kSum, 8, false>); break;
     }
 }
 
