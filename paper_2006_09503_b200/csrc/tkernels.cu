@@ -98,7 +98,8 @@ __global__ void k_embed_bwd_pos(const bf16* __restrict__ dx0, float* __restrict_
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int p = static_cast<int>(i / hv), c = static_cast<int>(i % hv) * 8;
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int b = 0; b < batch; ++b) {
+#pragma unroll 8
+        for (int b = 0; b < batch; ++b) {  // unrolled: eight sequences' loads in flight
             float g[8];
             load8(dx0 + (static_cast<size_t>(b) * seq + p) * h + c, g);
 #pragma unroll
