@@ -194,7 +194,9 @@ void Engine::join_replicas(const void* ids, int nranks, int rank) {
     for (Stage& st : stages_) {
         if (!st.local) continue;
         if (st.comm) throw Error("stage already joined a replica group");
-        if (nranks == 1) continue;
+        // a single replica needs no communicator (AllReduce is then a no-op);
+        // P2BW_NCCL_SINGLE_RANK=1 builds one anyway so one-GPU tests run the NCCL path
+        if (nranks == 1 && std::getenv("P2BW_NCCL_SINGLE_RANK") == nullptr) continue;
         ncclUniqueId id;
         std::memcpy(&id, static_cast<const uint8_t*>(ids) + sizeof(ncclUniqueId) * st.index, sizeof(id));
         DeviceGuard g(st.device);

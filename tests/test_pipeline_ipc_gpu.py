@@ -126,3 +126,48 @@ def test_nccl_runtime_loads_on_the_gpu_box():
     from paper_2006_09503_b200 import dist as D
     a, b = D.nccl_unique_id(), D.nccl_unique_id()
     assert len(a) == D.UNIQUE_ID_BYTES and a != b
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_data_parallel_nccl_path_single_replica(depth):
+    """The data-parallel path end to end on one GPU: a width-1 NCCL communicator per
+    stage (ncclCommInitRank from the dlopened runtime, the AllReduce op's
+    ncclAllReduce on the update stream, the 1/width scale) must leave 2BW training
+    bit-identical to the engine without replicas -- the 8-GPU run differs only in
+    the communicator's size."""
+    import torch.distributed as dist
+
+    from paper_2006_09503_b200 import dist as D
+
+    spec = TO.Spec(layers=2, hidden=128, heads=2, seq=128, vocab=500, batch=2, causal=True)
+    m, T = 2, 4
+    ids, tg = TO.synthetic_batch(spec, m * T, 5)
+
+    def run(join):
+        eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
+                       microbatch_size=spec.batch, layers=spec.layers, hidden=spec.hidden, heads=spec.heads,
+                       seq_len=spec.seq, vocab=spec.vocab, causal=1, learning_rate=0.3, momentum=0.9, seed=11)
+        try:
+            eng.init_weights()
+            if join:
+                D.join_replicas(eng, depth)
+            eng.set_data(ids, tg, 1, m * T)
+            eng.run_schedule(T)
+            eng.sync()
+            return eng.losses(1, m * T), [eng.read_master(s) for s in range(depth)]
+        finally:
+            eng.close()
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    os.environ["P2BW_NCCL_SINGLE_RANK"] = "1"  # build the communicator even for one replica
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        l_dp, w_dp = run(True)
+    finally:
+        dist.destroy_process_group()
+        del os.environ["P2BW_NCCL_SINGLE_RANK"]
+    l_ref, w_ref = run(False)
+    assert np.array_equal(l_dp, l_ref)
+    for a, b in zip(w_dp, w_ref):
+        assert np.array_equal(a, b)
