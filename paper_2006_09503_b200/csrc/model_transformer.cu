@@ -310,8 +310,9 @@ public:
             // FC1: dxn2 = du W1
             gemm_store_mn_b(g4_, 4 * h_, W + o.w1, h_, T_, h_, 4 * h_, gX_, s);
             gemm_wgrad(g4_, 4 * h_, st.xn2[l], h_, 4 * h_, h_, T_, grad_ + o.w1, beta, side_);
-            // b1 = colsum(du) as its own pass: summing the A tiles inside the wgrad GEMM
-            // (GemmEpilogue::bias_grad) measured no faster, as it rules out CTA-pair tiles
+            // b1 = colsum(du) as its own side-stream pass: summing the A tiles inside the
+            // wgrad GEMM (GemmEpilogue::bias_grad) measured no faster, as it rules out
+            // CTA-pair tiles, and inside the FC1 dgrad 1.3% slower (critical path)
             for (int dup_ = 0; dup_ < debug_dup(4); ++dup_) colsum_bf16(g4_, T_, 4 * h_, 4 * h_, grad_ + o.b1, first, side_red_, side_);
             done(kEvDoneB);
             // LN2 (+ residual): dx1 = LN2'(dxn2) + g

@@ -333,11 +333,11 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
 //                  output gradient dx is (saves a separate pass over dx).
 // A row is spread over a GROUP of wpr = ceil(h / 256) warps, one 8-column vector per
 // lane, so each lane keeps only 8 columns of accumulators (24 registers) and a CTA of
-// 768 threads holds G = 24 / wpr rows in flight, each prefetching its next row into
-// registers while it works on the current one.  The two row sums are combined across
-// the group's warps through SMEM (named barrier per group, fixed order: every warp of
-// the group sees identical sums; deterministic).  dx may alias dy: each lane reads
-// its vector of a row before writing it.
+// 768 threads works on G = 24 / wpr rows at a time, each group streaming its rows
+// through an SMEM ring (k_ln_bwd below).  The two row sums are combined across the
+// group's warps through SMEM (named barrier per group, fixed order: every warp of the
+// group sees identical sums; deterministic).  dx may alias dy: a row is read (into
+// the ring) before it is written, and the ring only fetches rows not yet written.
 constexpr int kLnBwdThreads = 768;  // 85 registers per thread; G = 24 / wpr row groups
 
 struct LnBwdShape {
