@@ -25,13 +25,16 @@ inline void check_cuda(cudaError_t e, const char* what) {
 
 // A stage's streams by role ("main" = the stage stream, "fwd", "data", "side" =
 // weight gradients, "update").  Lower = more urgent, clamped to the device range.
-// Default: side -2, main -1, the rest 0 -- weight-gradient GEMMs take the SMs a
-// dgrad / attention / LayerNorm tail frees before the next Forward does (BERT-base,
-// 8 paired runs on two boxes: +0.6-0.8% over equal priorities; every other ordering
-// tried was neutral or slower).  P2BW_STREAM_PRIO="main=-2,fwd=-1,..." replaces the
-// whole table (roles it omits get 0).
+// Default: side -3, main -2, fwd -1, the rest 0 -- weight-gradient GEMMs take the SMs
+// a dgrad / attention / LayerNorm tail frees, then the stage stream's chain, then the
+// next Forward (BERT-base paired runs: side-first +0.6-0.8% over equal priorities;
+// fwd above data / update a further ~+0.3%; main or side demoted: -1.2 to -1.8%).
+// P2BW_STREAM_PRIO="main=-2,fwd=-1,..." replaces the whole table (omitted roles: 0).
 inline cudaStream_t make_stage_stream(const char* role) {
-    int prio = std::strcmp(role, "side") == 0 ? -2 : std::strcmp(role, "main") == 0 ? -1 : 0;
+    int prio = std::strcmp(role, "side") == 0   ? -3
+               : std::strcmp(role, "main") == 0 ? -2
+               : std::strcmp(role, "fwd") == 0  ? -1
+                                                : 0;
     if (const char* e = std::getenv("P2BW_STREAM_PRIO")) {
         prio = 0;
         const size_t n = std::strlen(role);
