@@ -4,9 +4,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
 
 One "step" is one 2BW batch (m microbatches of b sequences, every stage's
-weight update included) of the workload named by --config (default: configs[1],
-the BERT-base-sized encoder, 12 layers / hidden 768 / seq 512) with synthetic
-token data.  Under torchrun (N > 1) every rank drives one GPU; rank 0 prints
+weight update included) of the workload named by --config with synthetic token
+data.  Default: configs[3], the GPT-style 2.2B decoder (48 layers, hidden 1920,
+seq 512, V 51200) at the reference planner's per-GPU choice for 8 x B200 (w 8,
+d 1, b 16, m 4) -- the largest configuration one GPU runs (the other configs are
+--config choices and parity-test shapes).  Under torchrun (N > 1) every rank drives one GPU; rank 0 prints
 ONE JSON line.  By default N GPUs run N data-parallel replicas of the whole
 pipeline (width N); --depth D > 1 under torchrun runs one pipeline stage per
 process (gpu = stage * width + replica, width = N / D) with CUDA-IPC stage
@@ -21,7 +23,10 @@ the C-ABI in which each step's token ids / targets are copied host->device
 from pinned memory and its losses device->host inside the timed region.  `roofline` comes from a second, profiled pass of the same workload
 (per-launch CUDA events around every stage kernel).  `cpu_baseline` times the
 reference's own pipelined_execute (oracle/_ref/ref_tool, built from
-/root/reference) on the linear-chain analog of the config on this host.
+/root/reference) on the linear-chain analog of the config on this host, and
+`same_config` times that same linear chain on the GPU through the production
+path (P2BW_MODEL_LINEAR_BF16: the tcgen05 GEMMs, fused optimizer and streams the
+transformer uses), so one ratio in the line compares like with like.
 """
 from __future__ import annotations
 
@@ -55,6 +60,11 @@ CONFIGS = {
     # configs[2]: BERT-large, depth 8 x m 8 on 8 GPUs (per-GPU work: 3 layers)
     "bert-large": dict(layers=24, hidden=1024, heads=16, seq=512, vocab=30522, causal=False, head_rows=77,
                        b=8, m=8, depth=1),
+    # configs[3]: GPT-style 2.2B decoder (h 1920, 48 layers, 30 x 64 heads, V 51200) at the
+    # planner's per-GPU choice on 8 x B200 (w 8, d 1, b 16, m 4:
+    # profiles/r1_plan_gpt2.2b_8xb200_2bw.txt, planner.cpp:45-99)
+    "gpt-2.2b": dict(layers=48, hidden=1920, heads=30, seq=512, vocab=51200, causal=True, head_rows=0,
+                     b=16, m=4, depth=1),
     # configs[4]: 24-layer GPT (h 1024, V 51200, causal LM head on every position)
     "gpt-24": dict(layers=24, hidden=1024, heads=16, seq=512, vocab=51200, causal=True, head_rows=0,
                    b=8, m=4, depth=1),
@@ -118,12 +128,26 @@ def peaks():
 
 # ---- CPU baseline: the reference's own trainer on the linear-chain analog --------------
 
+REF_GFLOPS_EST = 2.5  # the reference's fp64 loops on one core (SURVEY §6 probe: 2.0-3.0)
+
+
+def cpu_layers(c, target_s: float = 8.0) -> int:
+    """Layers of the linear-chain analog one CPU sample runs: all of them when that takes
+    <= target_s on one core, else fewer (the time is linear in the layer count; the
+    result is scaled to the full depth)."""
+    per_layer = 6.0 * c["hidden"] ** 2 * c["seq"] / (REF_GFLOPS_EST * 1e9)
+    return max(1, min(c["layers"], int(target_s / per_layer)))
+
+
 def cpu_sample(c, procs: int = 1, microbatches: int = 1) -> dict:
-    """ToyModel::make(dim=h, layers=L, cols=seq (one sequence per microbatch)), 2BW, depth 1,
-    timed by oracle/_ref/ref_tool (the reference compiled from its own sources)."""
+    """The reference's own 2BW trainer on the config's linear-chain analog: ToyModel::make(
+    dim=h, layers=L', cols=seq) -- one sequence (seq columns) per microbatch -- 2BW, d 1,
+    timed by oracle/_ref/ref_tool (the reference compiled from its own sources), L' <= L
+    layers (cpu_layers) with the time scaled by L / L'."""
     dim, L, cols = c["hidden"], c["layers"], c["seq"]
+    Ls = cpu_layers(c)
     if REF_TOOL.exists():
-        cmd = [str(REF_TOOL), "time", str(dim), str(L), str(cols), str(microbatches), "1", "1", "1"]
+        cmd = [str(REF_TOOL), "time", str(dim), str(Ls), str(cols), str(microbatches), "1", "1", "1"]
         t0 = time.time()
         ps = [subprocess.Popen(cmd, stdout=subprocess.PIPE, text=True) for _ in range(procs)]
         outs = [json.loads(p.communicate()[0]) for p in ps]
@@ -132,16 +156,18 @@ def cpu_sample(c, procs: int = 1, microbatches: int = 1) -> dict:
         kind = "reference"
     else:  # the oracle port (numpy restatement of semantics.cpp), single process
         from oracle import pipesim_oracle as O
-        model = O.ToyModel.make(dim, L, cols, microbatches, 1)
+        model = O.ToyModel.make(dim, Ls, cols, microbatches, 1)
         t0 = time.time()
         O.pipelined_execute(model, 0.01, 0.9, microbatches, 1, O.TWOBW, 1)
         sec = wall = time.time() - t0
         procs, kind = 1, "port"
+    full = sec * L / Ls
     samples = procs * microbatches  # one sequence (seq columns) per microbatch
-    return {"value": samples / sec, "unit": "samples/s", "cores": procs, "kind": kind,
-            "sample": f"pipelined_execute(ToyModel dim={dim} layers={L} cols={cols}, 2BW d=1, "
-                      f"m={microbatches} T=1) x {procs} process(es), fp64, {sec:.2f} s",
-            "seconds": sec, "wall_s": wall}
+    return {"value": samples / full, "unit": "samples/s", "cores": procs, "kind": kind,
+            "sample": f"pipelined_execute(ToyModel dim={dim} layers={Ls} cols={cols}, 2BW d=1, "
+                      f"m={microbatches} T=1) x {procs} process(es), fp64, {sec:.2f} s"
+                      + (f", scaled x{L}/{Ls} to the config's {L} layers" if Ls < L else ""),
+            "seconds": full, "wall_s": wall}
 
 
 def run_reference(args, c):
@@ -171,13 +197,65 @@ def run_reference(args, c):
     return 0
 
 
+# ---- same-config leg: the reference's own workload on the production GPU path ----------
+
+# The linear-chain ToyModel the reference trains (semantics.cpp:85-109) at BERT-base's
+# width: dim 768, 12 layers, one 512-column sequence per sample.  (Deeper / wider analogs
+# leave the bf16 range: ToyModel's I + 0.2 U grows activations ~sqrt(1 + dim / 300) per
+# layer, 2.7x at dim 1920 -- 1e20 after 48 layers -- so the gradients overflow.)
+SAME = dict(hidden=768, layers=12, seq=512, b=16, m=4)
+
+
+def linear_same_config(steps: int, warm: int, cpu: bool) -> dict:
+    """2BW samples/s of the SAME workload on both sides: the reference's pipelined_execute
+    on the host cores (ref_tool, one process per core, fp64) and the engine's bf16
+    production path (P2BW_MODEL_LINEAR_BF16: tcgen05 GEMMs, fused optimizer, the
+    transformer's streams) with ToyModel::make's data generated on the device."""
+    from paper_2006_09503_b200 import _lib
+    from paper_2006_09503_b200 import pipesim as P
+    c = SAME
+    cols = c["seq"] * c["b"]
+    eng = P.Engine(model_kind=P.MODEL_LINEAR_BF16, policy=P.PipelinePolicy.TwoBW, depth=1, microbatches=c["m"],
+                   microbatch_size=cols, layers=c["layers"], dim=c["hidden"], learning_rate=1e-7, momentum=0.9,
+                   seed=12345)
+    eng.init_weights()
+    eng.make_toy_data(1, 2 * c["m"])  # the data ring (2 batches), resident
+    eng.sync()
+    total = warm + steps + 1
+    l0 = _lib.lib().p2bw_launch_count()
+    eng.begin(total)
+    for t in range(1, total + 1):
+        eng.issue(t)
+    eng.finish()
+    eng.sync()
+    launches = _lib.lib().p2bw_launch_count() - l0
+    ms = eng.update_elapsed_ms(0, warm, warm + steps)
+    losses = eng.losses(1, 2 * c["m"])
+    eng.close()
+    gpu = c["b"] * c["m"] * steps / (ms / 1e3)
+    flops = 3 * 2 * c["hidden"] ** 2 * c["seq"] * c["layers"]  # per sample: fwd + dgrad + wgrad
+    out = {"workload": f"ToyModel linear chain (semantics.cpp:85-109): dim {c['hidden']}, {c['layers']} layers, "
+                       f"{c['seq']} columns per sample, 2BW d=1, m={c['m']}",
+           "gpu": {"value": round(gpu, 1), "unit": "samples/s", "dtype": "bf16 (fp32 master)",
+                   "microbatch": f"{c['b']} samples = {cols} columns", "ms_per_step": round(ms / steps, 3),
+                   "tflops": round(gpu * flops / 1e12, 1), "gpu_launches_per_step": round(launches / total, 1),
+                   "losses_finite": bool(np.all(np.isfinite(losses)))},
+           "parity": "tests/test_linear_bf16_gpu.py: trajectories vs the reference's pipelined_execute"}
+    if cpu:
+        procs = os.cpu_count() or 1
+        r = cpu_sample(dict(c, vocab=0, heads=0), procs=procs, microbatches=1)
+        out["cpu_reference"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out["gpu_over_cpu"] = round(gpu / r["value"], 1)
+    return out
+
+
 # ---- our engine ---------------------------------------------------------------------
 
 def run_ours(args, c):
     import torch
     from paper_2006_09503_b200 import _lib
     from paper_2006_09503_b200 import pipesim as P
-    from oracle import transformer_oracle as TO  # synthetic-data generator only (host numpy)
+    from paper_2006_09503_b200 import synthetic as S
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -193,7 +271,7 @@ def run_ours(args, c):
         local_stages = (stage, 1)
     else:
         width, local_stages = world, None
-    spec = TO.Spec(layers=c["layers"], hidden=c["hidden"], heads=c["heads"], seq=c["seq"], vocab=c["vocab"],
+    spec = S.TransformerSpec(layers=c["layers"], hidden=c["hidden"], heads=c["heads"], seq=c["seq"], vocab=c["vocab"],
                    batch=c["b"], causal=c["causal"], head_rows=c["head_rows"])
     m, steps, warm = c["m"], args.steps, args.warmup
     total_batches = warm + steps + 1
@@ -214,7 +292,7 @@ def run_ours(args, c):
     T, R = c["b"] * c["seq"], c["b"] * (c["head_rows"] or c["seq"])
     pool = 4
     replica = D.grid(world, rank, depth)[1] if pipelined else rank
-    ids_np, tg_np = TO.synthetic_batch(spec, m * pool, 99 + replica)
+    ids_np, tg_np = S.token_batch(spec, m * pool, 99 + replica)
     ids = torch.from_numpy(ids_np).pin_memory()
     tgs = torch.from_numpy(tg_np).pin_memory()
     loss_host = torch.zeros(total_batches * m, dtype=torch.float32).pin_memory()
@@ -345,18 +423,27 @@ def run_ours(args, c):
     if world == 1 and not args.no_cpu_baseline:
         r = cpu_sample(c, procs=1, microbatches=1)
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    same = None
+    if world == 1 and not args.no_same_config:
+        same = linear_same_config(steps, warm, cpu=not args.no_cpu_baseline)
 
     line = {
         "metric": "2BW training samples/sec", "value": round(value, 2), "unit": "samples/s", "n_gpus": world,
         "steps": steps, "warmup": warm, "ms_per_step": round(ms / steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic tokens (uniform ids, seeded), random-init weights",
+        "data": "synthetic tokens: ids uniform over [0, V) from splitmix64 (SURVEY 8(d)); random-init weights",
         "config": {"workload": args.config, "layers": c["layers"], "hidden": c["hidden"], "heads": c["heads"],
                    "seq_len": c["seq"], "vocab": c["vocab"], "causal": c["causal"],
                    "head_rows_per_seq": c["head_rows"] or c["seq"], "microbatch_size": c["b"],
                    "microbatches_m": m, "global_batch": width * c["b"] * m,
                    "parallelism": par, "inputs": "value: token batches resident in HBM; e2e: per-step host copies",
                    "policy": "2bw", "recompute": bool(args.recompute), "optimizer": args.optimizer,
+                   "head": ("causal LM: next-token targets at every position, untied LM head" if c["causal"] else
+                            f"masked LM, simplified: {c['head_rows']} evenly spaced positions per sequence (the same "
+                            "in every sequence) replaced by [MASK] (id V-1) with the original ids as targets; no "
+                            "80/10/10 split, untied LM head"),
+                   "reproducibility": "not bit-reproducible run to run: the token-embedding gradient uses vector "
+                                      "atomics and attention dQ a TMA reduce-add (fp32 summation order only)",
                    "l2": "working set (activations >> 126 MB L2) exceeds L2 every step"},
         "e2e": {"value": round(value_e2e, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "wall_s": round(wall, 3),
@@ -368,7 +455,7 @@ def run_ours(args, c):
         "mfu": round(mfu, 4), "flops_per_sample": fps,
         "roofline": roofline, "kernel_breakdown": breakdown,
         "kernel_ms_per_step": round(tot_ms / steps, 3) if classes else None,
-        "cpu_baseline": cpu, "clocks": clk,
+        "cpu_baseline": cpu, "same_config": same, "clocks": clk,
         "loss_first_last": [float(losses[0]), float(losses[-1])] if has_loss else None,
     }
     print(json.dumps(line), flush=True)
@@ -385,9 +472,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="bert-base", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="gpt-2.2b", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-same-config", action="store_true",
+                    help="skip the same-workload leg (reference linear chain on CPU and on the bf16 GPU path)")
     ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adam"],
                     help="WeightUpdate optimizer: the reference's momentum SGD (default) or Adam")
     ap.add_argument("--recompute", action="store_true",

@@ -65,7 +65,10 @@ enum {
 /* Stage model families the executor can run. */
 enum {
     P2BW_MODEL_LINEAR_F64 = 0,  /* the reference ToyModel (semantics.hpp:31-43), fp64, bit-exact */
-    P2BW_MODEL_TRANSFORMER = 1  /* pre-LN transformer blocks, bf16 tcgen05 kernels, fp32 master */
+    P2BW_MODEL_TRANSFORMER = 1, /* pre-LN transformer blocks, bf16 tcgen05 kernels, fp32 master */
+    P2BW_MODEL_LINEAR_BF16 = 2  /* the ToyModel on the production path: bf16 tcgen05 GEMMs, fp32
+                                   master / momentum / gradient, fused optimizer, the transformer's
+                                   streams; same public fp64 layout as P2BW_MODEL_LINEAR_F64 */
 };
 
 /* == pipesim::ScheduledOp (schedule.hpp:40-46). */
@@ -149,6 +152,12 @@ typedef struct {
     int optimizer;
     double beta2;
     double eps;
+    /* Gradient normalisation of the fp64 linear chain.  0: pipelined_execute's -- sum the
+     * batch's microbatch gradients, divide by grad_count at the update (semantics.cpp:329,
+     * 338-340).  1: reference_loop's -- scale each microbatch's gradient by 1/m as it is
+     * accumulated and apply the sum (semantics.cpp:145); the two agree bit for bit only
+     * when m is a power of two. */
+    int loop_scaling;
 } p2bw_desc;
 
 enum { P2BW_OPT_MOMENTUM_SGD = 0, P2BW_OPT_ADAM = 1 };
@@ -167,13 +176,20 @@ void p2bw_engine_destroy(p2bw_engine* eng);
 int p2bw_engine_stage_weight_bytes(p2bw_engine* eng, int stage, size_t* bytes);
 /* Initial weights (version 0) of one stage (host buffer, borrowed). */
 int p2bw_engine_load_stage_weights(p2bw_engine* eng, int stage, const void* host, size_t bytes);
-/* Deterministic initial weights from desc->seed (transformer). */
+/* Deterministic initial weights from desc->seed (transformer: scaled-uniform init;
+ * bf16 linear chain: ToyModel::make's W_l = I + 0.2 U, semantics.cpp:89-95). */
 int p2bw_engine_init_weights(p2bw_engine* eng);
 /* Microbatches [first_mb, first_mb+count), 1-based like ScheduledOp::microbatch.
  * Linear: inputs/targets fp64 [count][dim*b] column-major (ToyModel::dataset).
  * Transformer: int32 token ids / targets [count][b*seq_len]. */
 int p2bw_engine_set_data(p2bw_engine* eng, const void* inputs, const void* targets, int first_mb,
                          int count);
+/* P2BW_MODEL_LINEAR_BF16: microbatches [first_mb, first_mb+count) of ToyModel::make's
+ * dataset (semantics.cpp:85-109) for desc->seed, generated on the device draw for draw
+ * from the same splitmix64 stream (x exact up to the bf16 rounding; y = A x by the bf16
+ * GEMM) -- the bench's same-config workload without a host-side dataset.  The matching
+ * initial weights come from p2bw_engine_init_weights. */
+int p2bw_engine_make_toy_data(p2bw_engine* eng, int first_mb, int count);
 /* Interpret one program per stage (n_ops[s] ops at programs[s]).  Asynchronous. */
 int p2bw_engine_run(p2bw_engine* eng, const p2bw_op* const* programs, const size_t* n_ops,
                     int snapshot_updates);

@@ -22,7 +22,6 @@ and the same deterministic initialiser (init_uniform in tkernels.cu).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -30,24 +29,11 @@ import torch
 _M64 = (1 << 64) - 1
 
 
-@dataclass
-class Spec:
-    layers: int
-    hidden: int
-    heads: int
-    seq: int
-    vocab: int
-    batch: int            # sequences per microbatch (b)
-    causal: bool = True
-    head_rows: int = 0    # 0: every position
-
-    @property
-    def vp(self):
-        return (self.vocab + 127) // 128 * 128
-
-    @property
-    def rows_per_seq(self):
-        return self.head_rows if self.head_rows > 0 else self.seq
+# The configuration type and the synthetic data are the package's (the bench feeds the
+# same batches); the oracle only restates the arithmetic.
+from paper_2006_09503_b200.synthetic import TransformerSpec as Spec  # noqa: E402
+from paper_2006_09503_b200.synthetic import head_positions  # noqa: E402,F401
+from paper_2006_09503_b200.synthetic import token_batch as synthetic_batch  # noqa: E402,F401
 
 
 def _a64(n):
@@ -151,13 +137,6 @@ def unflatten_stage(flat: np.ndarray, spec: Spec, depth: int, s: int) -> dict:
     return {name: flat[off:off + int(np.prod(shape))].reshape(shape) for name, (off, shape) in lay.items()}
 
 
-def head_positions(spec: Spec) -> np.ndarray:
-    """model_transformer.cu alloc_all: evenly spaced head rows, same per sequence."""
-    r = spec.rows_per_seq
-    per_seq = np.array([(j * spec.seq) // r for j in range(r)], dtype=np.int64)
-    return np.concatenate([bb * spec.seq + per_seq for bb in range(spec.batch)])
-
-
 def _gelu(x):
     return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
 
@@ -231,18 +210,3 @@ def train(params: dict, spec: Spec, ids: np.ndarray, targets: np.ndarray, lr: fl
                 W[k] = W[k] + (-lr) * vel[k]
         traj.append({k: v.clone() for k, v in W.items()})
     return traj, np.array(losses)
-
-
-def synthetic_batch(spec: Spec, count: int, seed: int):
-    """Token ids uniform over [0, vocab) and next-token (GPT) / same-position
-    (BERT-style MLM) targets, from splitmix64(seed) -- the data the bench feeds."""
-    rng = np.random.default_rng(seed)
-    T = spec.batch * spec.seq
-    ids = rng.integers(0, spec.vocab, size=(count, T), dtype=np.int32)
-    rows = head_positions(spec)
-    if spec.causal:
-        nxt = np.roll(ids.reshape(count, spec.batch, spec.seq), -1, axis=2).reshape(count, T)
-        tg = nxt[:, rows]
-    else:
-        tg = rng.integers(0, spec.vocab, size=(count, len(rows)), dtype=np.int32)
-    return ids, tg.astype(np.int32)

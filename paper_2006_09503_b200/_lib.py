@@ -73,6 +73,7 @@ def _signatures():
         ("p2bw_engine_load_stage_weights", i, [vp, i, vp, sz]),
         ("p2bw_engine_init_weights", i, [vp]),
         ("p2bw_engine_set_data", i, [vp, vp, vp, i, i]),
+        ("p2bw_engine_make_toy_data", i, [vp, i, i]),
         ("p2bw_engine_run", i, [vp, vp, vp, i]),
         ("p2bw_engine_run_schedule", i, [vp, i, i]),
         ("p2bw_engine_begin", i, [vp, i]),

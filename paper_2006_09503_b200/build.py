@@ -23,12 +23,31 @@ LIB = PKG / "libp2bw.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-# nlohmann/json (header-only, the JSON library the reference's profile I/O uses)
-JSON_INC = os.environ.get(
-    "P2BW_JSON_INCLUDE",
-    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty")
-COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-          f"-I{CSRC}", f"-I{INCLUDE}", f"-I{JSON_INC}"]
+
+
+def find_json_include() -> str:
+    """Directory holding nlohmann/json.hpp (header-only; the JSON library the reference's
+    profile / plan I/O uses, profile.cpp:6).  P2BW_JSON_INCLUDE wins; otherwise the usual
+    system prefixes and the copies Python packages vendor (cudnn-frontend ships one)."""
+    env = os.environ.get("P2BW_JSON_INCLUDE")
+    cands = [env] if env else []
+    cands += ["/usr/include", "/usr/local/include"]
+    for sp in sys.path:
+        if sp and os.path.isdir(sp):
+            cands += [os.path.join(sp, "include", "cudnn_frontend", "thirdparty"),
+                      os.path.join(sp, "nvidia", "cudnn", "include")]
+    cands += [os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}",
+                           "site-packages", "include", "cudnn_frontend", "thirdparty")]
+    for c in cands:
+        if c and os.path.isfile(os.path.join(c, "nlohmann", "json.hpp")):
+            return c
+    raise RuntimeError("nlohmann/json.hpp not found: install nlohmann-json (header-only) or point "
+                       "P2BW_JSON_INCLUDE at the directory that contains nlohmann/json.hpp")
+
+
+def _common() -> list[str]:
+    return ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+            f"-I{CSRC}", f"-I{INCLUDE}", f"-I{find_json_include()}"]
 
 
 def _sources() -> list[Path]:
@@ -44,7 +63,7 @@ def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
     obj = BUILD / (src.name + ".o")
     if obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *ARCH, *_common(), "-c", str(src), "-o", str(obj)]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,4 +1,4 @@
-// Softmax attention forward on tcgen05 tensor cores (head dim 64, seq <= 512,
+// Softmax attention forward on tcgen05 tensor cores (head dim 64,
 // seq % 128 == 0): key blocks of 64 with a lazy online softmax, P kept in TMEM as the
 // A operand of O += P V, 128 TMEM columns and ~50 KB SMEM per CTA so that four CTAs
 // share each SM (one's softmax overlaps the others' MMAs and loads).
@@ -259,8 +259,6 @@ void set_smem_once() {
 }
 
 }  // namespace
-
-bool attention_tc_supported(int seq) { return seq >= 128 && seq <= 512 && seq % 128 == 0; }
 
 void attention_debug_timing(unsigned long long* dev_buf) {
     check_cuda(cudaMemcpyToSymbol(g_attn_dbg, &dev_buf, sizeof(dev_buf)), "cudaMemcpyToSymbol(g_attn_dbg)");

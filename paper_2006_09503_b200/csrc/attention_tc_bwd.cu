@@ -1,5 +1,5 @@
-// Softmax attention backward on tcgen05 tensor cores (head dim 64, seq % 128 == 0,
-// seq <= 512).  Persistent and key-outer: one CTA per SM walks work items
+// Softmax attention backward on tcgen05 tensor cores (head dim 64, seq % 128 == 0).
+// Persistent and key-outer: one CTA per SM walks work items
 // (128-key tile j, sequence, head) -- j-major, so causal items with the most query
 // tiles go first -- and for each item the query tiles i that can see it:
 //

@@ -105,7 +105,13 @@ std::string profile_transformer_blocks(const EngineConfig& base, const std::vect
                                 al(4 * h) + al(4 * h * h) + al(h);
     const double emb_params = al(vp * h) + al(seq * h);
     const double head_params = 2 * al(h) + al(vp * h);
-    constexpr double kBytesPerParam = 4.0;  // the fp32 coalesced gradient that AllReduce moves
+    // weight_bytes: the cost model charges required_versions x weight_bytes per stage
+    // (costmodel.cpp:93-99) and has no term for optimizer or gradient state, so the field
+    // carries the 2BW stage's whole parameter state split over its two versions: fp32
+    // master + momentum (8 B) + two fp32 coalesced-gradient buffers (8 B) + two bf16
+    // versions (4 B) = 20 B/param / 2.  (allreduce_seconds, costmodel.cpp:23-27, then
+    // prices 10 B/param where NCCL moves the 4 B/param fp32 gradient: conservative.)
+    constexpr double kBytesPerParam = 10.0;
 
     cudaStream_t s = nullptr;
     check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate(profile)");

@@ -51,6 +51,9 @@ p2bw::EngineConfig config_from_desc(const p2bw_desc& dd) {
     c.local_count = d->local_stages;
     c.recompute = d->recompute != 0;
     c.optimizer = d->optimizer;
+    c.loop_scaling = d->loop_scaling != 0;
+    if (c.loop_scaling && c.model_kind != P2BW_MODEL_LINEAR_F64)
+        throw p2bw::Error("loop_scaling applies to the fp64 linear chain only");
     if (c.optimizer != P2BW_OPT_MOMENTUM_SGD && c.optimizer != P2BW_OPT_ADAM)
         throw std::invalid_argument("unknown optimizer " + std::to_string(c.optimizer));
     if (c.optimizer == P2BW_OPT_ADAM) {
@@ -108,7 +111,7 @@ int p2bw_engine_load_stage_weights(p2bw_engine* eng, int stage, const void* host
         auto& e = eng_of(eng);
         check_stage(e, stage);
         if (host == nullptr) throw std::invalid_argument("host buffer is NULL");
-        e.model(stage).load_weights(0, host, bytes);
+        e.load_stage_weights(stage, host, bytes);
     });
 }
 
@@ -136,6 +139,23 @@ int p2bw_engine_set_data(p2bw_engine* eng, const void* inputs, const void* targe
             e.before_data_set(e.depth() - 1);
             e.model(e.depth() - 1).set_data(nullptr, targets, first_mb, count);
             e.after_data_set(e.depth() - 1, first_mb, count);
+        }
+    });
+}
+
+int p2bw_engine_make_toy_data(p2bw_engine* eng, int first_mb, int count) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        if (first_mb < 1) throw std::invalid_argument("microbatch ids are 1-based");
+        const uint64_t seed = e.config().seed;
+        // inputs on stage 0, targets on the last stage (one stage plays both at depth 1)
+        std::vector<int> stages{0};
+        if (e.depth() > 1) stages.push_back(e.depth() - 1);
+        for (int s : stages) {
+            if (!e.is_local(s)) continue;
+            e.before_data_set(s);
+            e.model(s).make_toy_data(seed, first_mb, count);
+            e.after_data_set(s, first_mb, count);
         }
     });
 }

@@ -101,7 +101,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     // A function of the configuration only: every process derives the same ring sizes.
     const char* serial = std::getenv("P2BW_SERIAL_STAGE");
     const bool overlap =
-        cfg_.model_kind == P2BW_MODEL_TRANSFORMER && !cfg_.recompute && !(serial && serial[0] == '1');
+        cfg_.model_kind != P2BW_MODEL_LINEAR_F64 && !cfg_.recompute && !(serial && serial[0] == '1');
     try {
         for (int s = 0; s < cfg_.depth; ++s) {
             Stage& st = stages_[s];
@@ -138,6 +138,9 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             if (cfg_.model_kind == P2BW_MODEL_LINEAR_F64) {
                 st.model = make_linear_f64_stage(cfg_, s, st.lo, st.hi, st.stash_slots,
                                                  st.weight_slots);
+            } else if (cfg_.model_kind == P2BW_MODEL_LINEAR_BF16) {
+                st.model = make_linear_bf16_stage(cfg_, s, st.lo, st.hi, st.stash_slots,
+                                                  st.weight_slots);
             } else if (cfg_.model_kind == P2BW_MODEL_TRANSFORMER) {
                 st.model = make_transformer_stage(cfg_, s, st.lo, st.hi, st.stash_slots,
                                                   st.weight_slots);
@@ -553,7 +556,7 @@ void Engine::issue_update(Stage& st) {
         std::max(stats_.max_versions_held, static_cast<int>(st.version_slot.size()));
     if (snapshots_on_) {
         std::vector<uint8_t> buf(st.model->weight_bytes_public());
-        st.model->read_weights(dst_slot, buf.data(), buf.size(), us);
+        st.model->snapshot_weights(dst_slot, buf.data(), buf.size(), us);
         st.snaps.push_back(std::move(buf));
     }
 }
@@ -708,6 +711,16 @@ std::vector<double> Engine::losses(int first_mb, int count) {
     st.model->read_losses(out.data(), first_mb, count, st.stream);
     check_cuda(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
     return out;
+}
+
+void Engine::load_stage_weights(int s, const void* host, size_t bytes) {
+    Stage& st = local_stage(s);
+    sync();
+    DeviceGuard g(st.device);
+    const int slot = st.version_slot.at(st.updates_done);
+    st.model->load_weights(slot, host, bytes);
+    st.version_slot.clear();
+    st.version_slot[st.updates_done] = slot;
 }
 
 void Engine::read_version(int s, int version, void* host, size_t bytes) {
@@ -870,11 +883,14 @@ std::string Engine::trace_report() {
     });
     json doc;
     doc["policy"] = policy_name(cfg_.policy);
+    // ParallelConfig (profile.hpp:49-62) has m = depth * grad_accum; when m is not a
+    // multiple of d, grad_accum is rounded down and the exact m rides beside it
     doc["config"] = {{"width", replicas},
                      {"depth", d},
                      {"microbatch_size", cfg_.microbatch_size},
-                     {"recompute", false},
-                     {"grad_accum", std::max(cfg_.microbatches / d, 1)}};
+                     {"recompute", cfg_.recompute},
+                     {"grad_accum", std::max(cfg_.microbatches / d, 1)},
+                     {"microbatches_per_batch", cfg_.microbatches}};
     doc["num_batches"] = num_batches;
     doc["throughput"] = throughput;
     doc["bubble_fraction"] = bubble;

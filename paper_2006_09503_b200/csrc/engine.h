@@ -54,6 +54,9 @@ struct EngineConfig {
     // WeightUpdate optimizer: P2BW_OPT_MOMENTUM_SGD (reference) or P2BW_OPT_ADAM
     int optimizer = 0;
     double beta2 = 0.999, eps = 1e-8;
+    // fp64 linear chain: reference_loop's per-microbatch 1/m gradient scaling
+    // (semantics.cpp:145) instead of pipelined_execute's sum / count (:338-340).
+    bool loop_scaling = false;
 };
 
 // Receive-side block of one stage, exported over CUDA IPC to its neighbours'
@@ -95,6 +98,11 @@ public:
     // Host <-> device weights of one version slot, in the model's public layout.
     virtual void load_weights(int wslot, const void* host, size_t bytes) = 0;
     virtual void read_weights(int wslot, void* host, size_t bytes, cudaStream_t s) = 0;
+    // Trajectory snapshot of the version just written into wslot (semantics.cpp:363-373);
+    // mixed-precision models return their fp32 master (the bf16 version is its rounding).
+    virtual void snapshot_weights(int wslot, void* host, size_t bytes, cudaStream_t s) {
+        read_weights(wslot, host, bytes, s);
+    }
     virtual size_t weight_bytes_public() const = 0;
     // Per-microbatch training loss (last stage only), indexed like the data ring.
     virtual void read_losses(double* host, int first_mb, int count, cudaStream_t s) {
@@ -130,11 +138,18 @@ public:
         throw Error("this model takes its initial weights from the caller");
     }
     virtual void set_data(const void* inputs, const void* targets, int first_mb, int count) = 0;
+    // Dataset microbatches generated on the device from a seed (linear chain: ToyModel::make).
+    virtual void make_toy_data(uint64_t seed, int first_mb, int count) {
+        (void)seed, (void)first_mb, (void)count;
+        throw Error("this stage model has no device-side toy dataset");
+    }
     virtual int data_capacity() const = 0;
 };
 
 std::unique_ptr<StageModel> make_linear_f64_stage(const EngineConfig& cfg, int stage, int lo,
                                                    int hi, int stash_slots, int weight_slots);
+std::unique_ptr<StageModel> make_linear_bf16_stage(const EngineConfig& cfg, int stage, int lo,
+                                                    int hi, int stash_slots, int weight_slots);
 std::unique_ptr<StageModel> make_transformer_stage(const EngineConfig& cfg, int stage, int lo,
                                                     int hi, int stash_slots, int weight_slots);
 
@@ -154,6 +169,9 @@ public:
     const EngineConfig& config() const { return cfg_; }
     int depth() const { return cfg_.depth; }
     StageModel& model(int s) { return *local_stage(s).model; }
+    // Initial weights of stage s: written into the buffer of its latest version, which
+    // then becomes the stage's only live version.
+    void load_stage_weights(int s, const void* host, size_t bytes);
 
     // Interpret one program per stage (asynchronous; call sync() to wait).
     void run(const std::vector<Program>& programs);

@@ -73,9 +73,11 @@ struct Run {
     std::vector<double> losses;  // per microbatch
 };
 
-// The linear-chain model executed by the GPU engine (fp64 parity mode).
+// The linear-chain model executed by the GPU engine: fp64 parity mode, or the bf16
+// production path; loop_scaling selects reference_loop's 1/m gradient scaling.
 Run run_on_engine(const ToyModel& model, const TrainerConfig& cfg, PipelinePolicy policy,
-                  int depth, bool want_losses) {
+                  int depth, bool want_losses, EnginePrecision precision = EnginePrecision::Fp64Exact,
+                  bool loop_scaling = false) {
     cfg.validate();
     const int layers = model.num_layers();
     if (depth < 1 || layers % depth != 0)
@@ -92,7 +94,8 @@ Run run_on_engine(const ToyModel& model, const TrainerConfig& cfg, PipelinePolic
 
     const std::vector<int> devs = stage_devices(depth);
     p2bw_desc d{};
-    d.model_kind = P2BW_MODEL_LINEAR_F64;
+    d.model_kind = precision == EnginePrecision::Bf16TensorCore ? P2BW_MODEL_LINEAR_BF16 : P2BW_MODEL_LINEAR_F64;
+    d.loop_scaling = loop_scaling ? 1 : 0;
     d.policy = static_cast<int>(policy);
     d.depth = depth;
     d.width = 1;
@@ -244,14 +247,18 @@ void TrainerConfig::validate() const {
 
 // ---- trainers on the GPU engine ---------------------------------------------
 
-// Vanilla minibatch SGD == a one-stage flushed pipeline (version t-1 for batch t).
+// Vanilla minibatch SGD == a one-stage flushed pipeline (version t-1 for batch t),
+// with reference_loop's per-microbatch 1/m scaling (semantics.cpp:145): bit-identical
+// to the reference for every m.
 Trajectory reference_vanilla(const ToyModel& model, const TrainerConfig& cfg) {
-    return run_on_engine(model, cfg, PipelinePolicy::GPipe, 1, false).result.trajectory;
+    return run_on_engine(model, cfg, PipelinePolicy::GPipe, 1, false, EnginePrecision::Fp64Exact, true)
+        .result.trajectory;
 }
 
 // Delay-1 SGD == a one-stage 2BW pipeline (version max(t-2,0) for batch t).
 Trajectory reference_2bw(const ToyModel& model, const TrainerConfig& cfg) {
-    return run_on_engine(model, cfg, PipelinePolicy::TwoBW, 1, false).result.trajectory;
+    return run_on_engine(model, cfg, PipelinePolicy::TwoBW, 1, false, EnginePrecision::Fp64Exact, true)
+        .result.trajectory;
 }
 
 PipelinedResult pipelined_execute(const ToyModel& model, const TrainerConfig& cfg,
@@ -259,12 +266,19 @@ PipelinedResult pipelined_execute(const ToyModel& model, const TrainerConfig& cf
     return run_on_engine(model, cfg, policy, depth, false).result;
 }
 
+PipelinedResult pipelined_execute(const ToyModel& model, const TrainerConfig& cfg,
+                                  PipelinePolicy policy, int depth, EnginePrecision precision) {
+    return run_on_engine(model, cfg, policy, depth, false, precision).result;
+}
+
 // semantics.cpp:377-388, with per-batch losses measured by the engine's forward passes.
 LossCurves loss_curve_compare(const ToyModel& model, const TrainerConfig& cfg) {
     LossCurves curves;
     const int m = cfg.microbatches_per_batch;
-    curves.vanilla = batch_losses(run_on_engine(model, cfg, PipelinePolicy::GPipe, 1, true).losses, m);
-    curves.twobw = batch_losses(run_on_engine(model, cfg, PipelinePolicy::TwoBW, 1, true).losses, m);
+    curves.vanilla = batch_losses(
+        run_on_engine(model, cfg, PipelinePolicy::GPipe, 1, true, EnginePrecision::Fp64Exact, true).losses, m);
+    curves.twobw = batch_losses(
+        run_on_engine(model, cfg, PipelinePolicy::TwoBW, 1, true, EnginePrecision::Fp64Exact, true).losses, m);
     for (double v : curves.vanilla) curves.loss_scale = std::max(curves.loss_scale, v);
     for (size_t i = curves.vanilla.size() / 2; i < curves.vanilla.size(); ++i)
         curves.tail_max_gap = std::max(curves.tail_max_gap, std::abs(curves.vanilla[i] - curves.twobw[i]));

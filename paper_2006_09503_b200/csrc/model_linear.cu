@@ -50,16 +50,18 @@ __global__ void k_matmul_tn(const double* __restrict__ w, const double* __restri
     }
 }
 
-// grad (=|+=) G X^T  (G, X: n x c; grad: n x n).  The product is formed first and
-// then added, like axpy(1.0, matmul_nt(g, in), grad_sum).
+// grad (=|+=) scale * G X^T  (G, X: n x c; grad: n x n).  The product is formed first
+// and then added, like axpy(1.0, matmul_nt(g, in), grad_sum) (semantics.cpp:329), or
+// axpy(1.0 / m, ...) in reference_loop (semantics.cpp:145) when scale != 1.
 __global__ void k_wgrad_nt(const double* __restrict__ g, const double* __restrict__ x,
-                           double* __restrict__ grad, int n, int c, int overwrite) {
+                           double* __restrict__ grad, int n, int c, int overwrite, double scale) {
     const long total = static_cast<long>(n) * n;
     for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<long>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
         double acc = 0.0;
         for (int k = 0; k < c; ++k) acc = __dadd_rn(acc, __dmul_rn(g[static_cast<long>(k) * n + i], x[static_cast<long>(k) * n + j]));
+        if (scale != 1.0) acc = __dmul_rn(scale, acc);
         grad[idx] = overwrite ? __dadd_rn(0.0, acc) : __dadd_rn(grad[idx], acc);
     }
 }
@@ -108,7 +110,8 @@ public:
     LinearF64Stage(const EngineConfig& cfg, int stage, int lo, int hi, int sslots, int wslots)
         : n_(cfg.dim), cols_(cfg.microbatch_size), layers_(hi - lo), stage0_(stage == 0),
           stageL_(stage == cfg.depth - 1), sslots_(sslots), wslots_(wslots), lr_(cfg.lr),
-          beta_(cfg.momentum) {
+          beta_(cfg.momentum), loop_scale_(cfg.loop_scaling ? 1.0 / cfg.microbatches : 1.0),
+          loop_scaling_(cfg.loop_scaling) {
         if (n_ < 1 || cols_ < 1) throw Error("toy model dimensions must be >= 1");
         mat_ = static_cast<size_t>(n_) * n_;
         act_ = static_cast<size_t>(n_) * cols_;
@@ -136,20 +139,40 @@ public:
     size_t weight_bytes_public() const override { return layers_ * mat_ * sizeof(double); }
     int data_capacity() const override { return capacity_; }
 
+    void bind_stream(cudaStream_t s) override { stream_ = s; }
+
+    // Dataset microbatches [first_mb, first_mb + count).  Growing the buffers keeps the
+    // microbatches already uploaded; the copies are ordered on the stage stream, so a
+    // call between runs never races the kernels still reading the old contents.
     void set_data(const void* inputs, const void* targets, int first_mb, int count) override {
         if (count < 1) throw Error("set_data: empty microbatch range");
         if (first_mb + count - 1 > capacity_) {
+            check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+            const int cap = first_mb + count - 1;
+            double *x = nullptr, *y = nullptr, *loss = nullptr;
+            alloc(&x, static_cast<size_t>(cap) * act_);
+            alloc(&y, static_cast<size_t>(cap) * act_);
+            alloc(&loss, static_cast<size_t>(cap));
+            check_cuda(cudaMemset(loss, 0, sizeof(double) * cap), "cudaMemset");
+            if (capacity_ > 0) {
+                const size_t keep = static_cast<size_t>(capacity_) * act_ * sizeof(double);
+                check_cuda(cudaMemcpy(x, x_, keep, cudaMemcpyDeviceToDevice), "D2D x");
+                check_cuda(cudaMemcpy(y, y_, keep, cudaMemcpyDeviceToDevice), "D2D y");
+                check_cuda(cudaMemcpy(loss, loss_, sizeof(double) * capacity_, cudaMemcpyDeviceToDevice), "D2D loss");
+            }
+            // stage 0's stash points into the dataset for in-flight microbatches: rebase it
+            for (auto& p : xin_)
+                if (p != nullptr && x_ != nullptr && p >= x_ && p < x_ + static_cast<size_t>(capacity_) * act_)
+                    p = x + (p - x_);
             for (double* p : {x_, y_, loss_}) cudaFree(p);
-                capacity_ = first_mb + count - 1;
-            alloc(&x_, static_cast<size_t>(capacity_) * act_);
-            alloc(&y_, static_cast<size_t>(capacity_) * act_);
-            alloc(&loss_, static_cast<size_t>(capacity_));
-            check_cuda(cudaMemset(loss_, 0, sizeof(double) * capacity_), "cudaMemset");
+            x_ = x, y_ = y, loss_ = loss;
+            capacity_ = cap;
         }
         const size_t off = static_cast<size_t>(first_mb - 1) * act_;
         const size_t bytes = static_cast<size_t>(count) * act_ * sizeof(double);
-        if (inputs) check_cuda(cudaMemcpy(x_ + off, inputs, bytes, cudaMemcpyHostToDevice), "H2D x");
-        if (targets) check_cuda(cudaMemcpy(y_ + off, targets, bytes, cudaMemcpyHostToDevice), "H2D y");
+        if (inputs) check_cuda(cudaMemcpyAsync(x_ + off, inputs, bytes, cudaMemcpyHostToDevice, stream_), "H2D x");
+        if (targets) check_cuda(cudaMemcpyAsync(y_ + off, targets, bytes, cudaMemcpyHostToDevice, stream_), "H2D y");
+        check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");  // host buffers are borrowed
     }
 
     void load_weights(int wslot, const void* host, size_t bytes) override {
@@ -204,7 +227,7 @@ public:
         for (int l = layers_ - 1; l >= 0; --l) {
             const double* in = l == 0 ? xin_[static_cast<size_t>(sslot)] : stash_ptr(sslot, l);
             k_wgrad_nt<<<blocks_for(static_cast<long>(mat_)), kThreads, 0, s>>>(
-                g, in, gsum_ + static_cast<size_t>(l) * mat_, n_, cols_, first ? 1 : 0);
+                g, in, gsum_ + static_cast<size_t>(l) * mat_, n_, cols_, first ? 1 : 0, loop_scale_);
             if (l > 0 || !stage0_) {
                 double* dst = l == 0 ? static_cast<double*>(g_out) : gtmp_ + static_cast<size_t>(flip) * act_;
                 flip ^= 1;
@@ -216,6 +239,7 @@ public:
     }
 
     void update(int src_slot, int dst_slot, int count, cudaStream_t s) override {
+        if (loop_scaling_) count = 1;  // reference_loop applies the pre-scaled sum (semantics.cpp:145, :163)
         const long total = static_cast<long>(layers_ * mat_);
         k_update<<<blocks_for(total), kThreads, 0, s>>>(wslot_ptr(src_slot, 0), wslot_ptr(dst_slot, 0), vel_,
                                                         gsum_, total, static_cast<double>(count), lr_, beta_);
@@ -238,6 +262,9 @@ private:
     bool stage0_, stageL_;
     int sslots_, wslots_;
     double lr_, beta_;
+    double loop_scale_;
+    bool loop_scaling_;
+    cudaStream_t stream_ = nullptr;
     size_t mat_ = 0, act_ = 0;
     int capacity_ = 0;
     double *w_ = nullptr, *vel_ = nullptr, *gsum_ = nullptr, *stash_ = nullptr, *gtmp_ = nullptr,

@@ -80,7 +80,8 @@ public:
         T_ = b_ * seq_;
         if (h_ <= 0 || heads_ <= 0 || h_ != heads_ * kHeadDim)
             throw Error("transformer: hidden must equal heads * 64");
-        if (seq_ < 1 || seq_ > 512) throw Error("transformer: seq_len must be in [1, 512]");
+        if (!attention_tc_supported(seq_))
+            throw Error("transformer: seq_len must be a positive multiple of 128 (tcgen05 attention tiles)");
         if (b_ < 1 || vocab_ < 2) throw Error("transformer: bad microbatch size or vocab");
         rows_per_seq_ = c.head_rows > 0 ? c.head_rows : seq_;
         if (rows_per_seq_ > seq_) throw Error("transformer: head_rows exceeds seq_len");
@@ -160,9 +161,16 @@ public:
 
     void read_weights(int wslot, void* host, size_t bytes, cudaStream_t s) override {
         if (bytes != weight_bytes_public()) throw Error("read_weights: size mismatch");
-        cast_bf16_f32(wbf_[wslot], scratch_f32_, nparam_, s);
-        check_cuda(cudaMemcpyAsync(host, scratch_f32_, bytes, cudaMemcpyDeviceToHost, s), "D2H weights");
+        // bf16 -> host, widened there (no parameter-sized device scratch)
+        std::vector<uint16_t> raw(nparam_);
+        check_cuda(cudaMemcpyAsync(raw.data(), wbf_[wslot], nparam_ * sizeof(bf16), cudaMemcpyDeviceToHost, s),
+                   "D2H weights");
         check_cuda(cudaStreamSynchronize(s), "read sync");
+        float* out = static_cast<float*>(host);
+        for (size_t i = 0; i < nparam_; ++i) {
+            const uint32_t bits = static_cast<uint32_t>(raw[i]) << 16;
+            std::memcpy(out + i, &bits, sizeof(float));
+        }
     }
 
     void read_master(void* host, size_t bytes) override {
@@ -437,7 +445,6 @@ private:
             check_cuda(cudaMemset(vel2_, 0, nparam_ * sizeof(float)), "memset");
         }
         grad_ = grad_bufs_[0] = dalloc<float>(nparam_);
-        scratch_f32_ = dalloc<float>(nparam_);
         for (int i = 0; i < wslots_; ++i) wbf_.push_back(dalloc<bf16>(nparam_));
         check_cuda(cudaMemset(master_, 0, nparam_ * sizeof(float)), "memset");
         check_cuda(cudaMemset(vel_, 0, nparam_ * sizeof(float)), "memset");
@@ -584,7 +591,7 @@ private:
     std::vector<void*> allocs_;
     std::vector<LayerOff> lay_;
     size_t off_tok_ = 0, off_pos_ = 0, off_lnfg_ = 0, off_lnfb_ = 0, off_head_ = 0, nparam_ = 0;
-    float *master_ = nullptr, *vel_ = nullptr, *grad_ = nullptr, *scratch_f32_ = nullptr;
+    float *master_ = nullptr, *vel_ = nullptr, *grad_ = nullptr;
     float* vel2_ = nullptr;  // Adam second moment
     float* grad_bufs_[2] = {nullptr, nullptr};  // coalesced gradient, double-buffered per batch (2BW)
     int grad_cur_ = 0;

@@ -46,7 +46,7 @@ void sum_scaled(const float* row_loss, int rows, float scale, float* loss_out, c
 // Attention over qkv [T x 3h] (q | k | v, heads of 64), output o [T x h], lse [b*nh*seq].
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
                    cudaStream_t s);
-// tcgen05 forward (attention_tc.cu) for seq % 128 == 0, seq <= 512; attention_fwd dispatches.
+// The tcgen05 kernels cover seq % 128 == 0 (attention.cu rejects anything else).
 bool attention_tc_supported(int seq);
 // Debug: per-CTA phase timestamps of the tcgen05 forward into dev_buf[cta * 16 + slot] (null: off).
 void attention_debug_timing(unsigned long long* dev_buf);

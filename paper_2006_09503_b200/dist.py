@@ -60,22 +60,30 @@ def grid(world: int, rank: int, depth: int) -> tuple[int, int, int]:
     return rank // width, rank % width, width
 
 
-def join_replicas(engine, depth: int, pipelined: bool = False) -> None:
-    """Join this process's stages to their data-parallel replica groups.
-
-    pipelined=False: every process runs a whole pipeline (width = world).
-    pipelined=True: one stage per process laid out by :func:`grid`."""
+def _engine_join(engine, ids: bytes, width: int, replica: int) -> None:
     import ctypes as C
 
     from . import _lib
+    arr = (C.c_ubyte * len(ids)).from_buffer_copy(ids)
+    _lib.check(_lib.lib().p2bw_engine_join_replicas(engine.h, arr, width, replica))
+
+
+def join_replicas(engine, depth: int, pipelined: bool = False, make_id: Callable[[], bytes] | None = None,
+                  join: Callable | None = None) -> None:
+    """Join this process's stages to their data-parallel replica groups.
+
+    pipelined=False: every process runs a whole pipeline (width = world).
+    pipelined=True: one stage per process laid out by :func:`grid`.
+    Every replica of every stage receives the same `depth` unique ids (one NCCL
+    communicator per stage, rank = replica index); make_id / join default to the
+    engine's (p2bw_nccl_unique_id / p2bw_engine_join_replicas)."""
     world, rank = dist.get_world_size(), dist.get_rank()
     if pipelined:
         _, replica, width = grid(world, rank, depth)
     else:
         replica, width = rank, world
-    ids = share_unique_ids(depth, nccl_unique_id)
-    arr = (C.c_ubyte * len(ids)).from_buffer_copy(ids)
-    _lib.check(_lib.lib().p2bw_engine_join_replicas(engine.h, arr, width, replica))
+    ids = share_unique_ids(depth, make_id or nccl_unique_id)
+    (join or _engine_join)(engine, ids, width, replica)
 
 
 def connect_pipeline(engine, depth: int) -> None:

@@ -205,7 +205,8 @@ class Desc(C.Structure):
                 ("vocab", C.c_int), ("causal", C.c_int), ("head_rows", C.c_int),
                 ("learning_rate", C.c_double), ("momentum", C.c_double), ("seed", C.c_ulonglong),
                 ("devices", C.POINTER(C.c_int)), ("first_local_stage", C.c_int), ("local_stages", C.c_int),
-                ("recompute", C.c_int), ("optimizer", C.c_int), ("beta2", C.c_double), ("eps", C.c_double)]
+                ("recompute", C.c_int), ("optimizer", C.c_int), ("beta2", C.c_double), ("eps", C.c_double),
+                ("loop_scaling", C.c_int)]
 
 
 STAGE_BLOB_BYTES = 128  # P2BW_STAGE_BLOB_BYTES
@@ -218,7 +219,7 @@ def profile_blocks(*, layers: int, hidden: int, heads: int, seq_len: int, vocab:
     times, weight and activation bytes measured on the current GPU, as the reference's
     profile document (profile.cpp:162-193) -- the input of plan() / partition_equal()."""
     d = Desc(MODEL_TRANSFORMER, int(PipelinePolicy.TwoBW), 1, 1, 1, 1, layers, 0, hidden, heads, seq_len,
-             vocab, causal, head_rows, 0.0, 0.0, seed, None, 0, 0, 0, OPT_MOMENTUM_SGD, 0.999, 1e-8)
+             vocab, causal, head_rows, 0.0, 0.0, seed, None, 0, 0, 0, OPT_MOMENTUM_SGD, 0.999, 1e-8, 0)
     sizes = (C.c_int * len(microbatch_sizes))(*microbatch_sizes)
     p = C.c_void_p()
     _call("p2bw_profile_blocks", C.byref(d), sizes, len(microbatch_sizes), warmup, iters, name.encode(),
@@ -233,6 +234,7 @@ class Counters(C.Structure):
 
 MODEL_LINEAR_F64 = 0
 MODEL_TRANSFORMER = 1
+MODEL_LINEAR_BF16 = 2  # the ToyModel on the production bf16 / tcgen05 path
 OPT_MOMENTUM_SGD = 0  # P2BW_OPT_*
 OPT_ADAM = 1
 
@@ -250,13 +252,14 @@ class Engine:
                  seq_len: int = 0, vocab: int = 0, causal: int = 0, head_rows: int = 0,
                  learning_rate: float = 0.0, momentum: float = 0.0, seed: int = 0,
                  devices: list[int] | None = None, local_stages: tuple[int, int] | None = None,
-                 recompute: bool = False, optimizer: str = "sgd", beta2: float = 0.999, eps: float = 1e-8):
+                 recompute: bool = False, optimizer: str = "sgd", beta2: float = 0.999, eps: float = 1e-8,
+                 loop_scaling: bool = False):
         self._devs = (C.c_int * depth)(*devices) if devices else None
         first, count = local_stages if local_stages is not None else (0, 0)
         d = Desc(model_kind, int(policy), depth, 1, microbatches, microbatch_size, layers, dim, hidden,
                  heads, seq_len, vocab, causal, head_rows, learning_rate, momentum, seed,
                  C.cast(self._devs, C.POINTER(C.c_int)) if self._devs else None, first, count, int(recompute),
-                 {"sgd": OPT_MOMENTUM_SGD, "adam": OPT_ADAM}[optimizer], beta2, eps)
+                 {"sgd": OPT_MOMENTUM_SGD, "adam": OPT_ADAM}[optimizer], beta2, eps, int(loop_scaling))
         self.h = C.c_void_p()
         _call("p2bw_engine_create", C.byref(d), C.byref(self.h))
         self.depth = depth
@@ -287,6 +290,11 @@ class Engine:
         tp = np.ascontiguousarray(targets) if targets is not None else None
         _call("p2bw_engine_set_data", self.h, ip.ctypes.data_as(C.c_void_p) if ip is not None else None,
               tp.ctypes.data_as(C.c_void_p) if tp is not None else None, first_mb, count)
+
+    def make_toy_data(self, first_mb: int, count: int):
+        """Device-side ToyModel::make dataset for microbatches [first_mb, first_mb+count)
+        (bf16 linear chain; seed from the engine's description)."""
+        _call("p2bw_engine_make_toy_data", self.h, first_mb, count)
 
     def run_schedule(self, num_batches: int, snapshots: bool = False):
         _call("p2bw_engine_run_schedule", self.h, num_batches, int(snapshots))
@@ -360,9 +368,11 @@ class Engine:
               C.c_size_t(n))
         return out
 
-    def read_master(self, s: int) -> np.ndarray:
+    def read_master(self, s: int, dtype=np.float32) -> np.ndarray:
+        """fp32 master weights in the model's public layout (transformer: fp32 flat vector;
+        linear chains: fp64 column-major matrices, pass dtype=np.float64)."""
         n = self.stage_weight_bytes(s)
-        out = np.empty(n // 4, dtype=np.float32)
+        out = np.empty(n // np.dtype(dtype).itemsize, dtype=dtype)
         _call("p2bw_engine_read_master", self.h, s, out.ctypes.data_as(C.c_void_p), C.c_size_t(n))
         return out
 
@@ -409,8 +419,16 @@ class PipelinedResult:
 
 
 def pipelined_execute(model: ToyModel, cfg: TrainerConfig, policy: PipelinePolicy, depth: int,
-                      devices: list[int] | None = None, with_losses: bool = False) -> PipelinedResult:
-    """semantics.hpp:73-74, executed by the B200 stage executor (fp64 linear stages)."""
+                      devices: list[int] | None = None, with_losses: bool = False,
+                      precision: str = "fp64", loop_scaling: bool = False) -> PipelinedResult:
+    """semantics.hpp:73-74, executed by the B200 stage executor.
+
+    precision "fp64": the fp64 linear stages, bit-identical to the reference;
+    "bf16": the production path (bf16 tcgen05 GEMMs, fp32 master / momentum / gradient,
+    the fused optimizer, the transformer's streams) -- trajectories are the fp32 master
+    weights after every update, within a bf16 tolerance of the reference.
+    loop_scaling (fp64 only): reference_loop's per-microbatch 1/m gradient scaling
+    (semantics.cpp:145) instead of pipelined_execute's sum / count (:338-340)."""
     L = model.num_layers
     if L % depth:
         raise PipesimError(f"block count {L} not divisible by depth {depth}")
@@ -418,9 +436,11 @@ def pipelined_execute(model: ToyModel, cfg: TrainerConfig, policy: PipelinePolic
     if len(model.dataset) < m * T:
         raise PipesimError("toy dataset has too few microbatches for the requested run")
     per = L // depth
-    eng = Engine(model_kind=MODEL_LINEAR_F64, policy=policy, depth=depth, microbatches=m,
+    kind = {"fp64": MODEL_LINEAR_F64, "bf16": MODEL_LINEAR_BF16}[precision]
+    eng = Engine(model_kind=kind, policy=policy, depth=depth, microbatches=m,
                  microbatch_size=model.microbatch_samples, layers=L, dim=model.dim,
-                 learning_rate=cfg.learning_rate, momentum=cfg.momentum, devices=devices)
+                 learning_rate=cfg.learning_rate, momentum=cfg.momentum, devices=devices,
+                 loop_scaling=loop_scaling)
     try:
         for s in range(depth):
             eng.load_stage_weights(s, np.concatenate(
@@ -448,10 +468,12 @@ def pipelined_execute(model: ToyModel, cfg: TrainerConfig, policy: PipelinePolic
 
 
 def reference_vanilla(model: ToyModel, cfg: TrainerConfig):
-    """Vanilla SGD == one-stage GPipe on the engine (semantics.cpp:188-190)."""
-    return pipelined_execute(model, cfg, PipelinePolicy.GPipe, 1).trajectory
+    """Vanilla SGD == one-stage GPipe on the engine with reference_loop's 1/m scaling
+    (semantics.cpp:145, 188-190): bit-identical to the reference for every m."""
+    return pipelined_execute(model, cfg, PipelinePolicy.GPipe, 1, loop_scaling=True).trajectory
 
 
 def reference_2bw(model: ToyModel, cfg: TrainerConfig):
-    """Delay-1 SGD == one-stage 2BW on the engine (semantics.cpp:192-194)."""
-    return pipelined_execute(model, cfg, PipelinePolicy.TwoBW, 1).trajectory
+    """Delay-1 SGD == one-stage 2BW on the engine with reference_loop's 1/m scaling
+    (semantics.cpp:145, 192-194)."""
+    return pipelined_execute(model, cfg, PipelinePolicy.TwoBW, 1, loop_scaling=True).trajectory

@@ -24,3 +24,19 @@ def toy():
     meta = json.loads((GOLDEN / "toy_trajectories.json").read_text())
     arrs = np.load(GOLDEN / "toy_trajectories.npz")
     return [(m, arrs[f"traj_{i}"]) for i, m in enumerate(meta)]
+
+
+@lru_cache(None)
+def loops():
+    """reference_loop trajectories (ref_tool loop) at m = 3..6, vanilla and delayed."""
+    meta = json.loads((GOLDEN / "loop_trajectories.json").read_text())
+    arrs = np.load(GOLDEN / "loop_trajectories.npz")
+    return [(m, arrs[f"traj_{i}"]) for i, m in enumerate(meta)]
+
+
+@lru_cache(None)
+def linear_bf16():
+    """Reference pipelined_execute at the configs' widths, sampled (make_golden.py BF16_GRID)."""
+    meta = json.loads((GOLDEN / "linear_bf16.json").read_text())
+    arrs = np.load(GOLDEN / "linear_bf16.npz")
+    return [(m, {k.split(".", 1)[1]: arrs[k] for k in arrs.files if k.startswith(m["name"] + ".")}) for m in meta]

@@ -67,7 +67,81 @@ TOY_EXTRA = [dict(dim=16, layers=4, b=8, seed=424242, lr=0.05, beta=0.9, m=4, T=
              dict(dim=8, layers=4, b=4, seed=99, lr=0.05, beta=0.9, m=4, T=5, policy=2, depth=4)]
 
 
+# reference_loop (semantics.cpp:167-184) at power-of-two and other m: its per-microbatch
+# 1/m scaling (:145) differs from pipelined_execute's sum / count (:338-340) in the last bits
+# when m is not a power of two.
+LOOP_GRID = [dict(dim=8, layers=4, b=4, seed=31, lr=0.05, beta=0.9, m=m, T=5, delayed=dl)
+             for m in (3, 4, 5, 6) for dl in (0, 1)]
+
+# The production (bf16 tcgen05) path against the reference at the configs' widths:
+# reference pipelined_execute trajectories (2BW unless stated) plus the vanilla-SGD
+# trajectory (reference_vanilla) for the margin.  Stored as sampled entries of
+# Delta W(t) = W(t) - W(0) (the full matrices are too large to commit) and the exact
+# Frobenius norms of Delta W(t) and of Delta W(t) - Delta W_vanilla(t).
+BF16_GRID = [
+    dict(name="c1_d2", dim=256, layers=4, b=128, seed=7, lr=0.05, beta=0.9, m=4, T=6, policy=4, depth=2),
+    dict(name="m3_d2", dim=256, layers=8, b=256, seed=11, lr=1e-3, beta=0.9, m=3, T=5, policy=4, depth=2),
+    dict(name="m5_d4", dim=256, layers=8, b=256, seed=13, lr=1e-3, beta=0.9, m=5, T=4, policy=4, depth=4),
+    dict(name="m8_d8", dim=256, layers=8, b=128, seed=17, lr=1e-3, beta=0.9, m=8, T=4, policy=4, depth=8),
+    dict(name="1f1b_d4", dim=256, layers=4, b=128, seed=19, lr=0.05, beta=0.9, m=4, T=4, policy=2, depth=4),
+    dict(name="c2_d4", dim=768, layers=12, b=512, seed=23, lr=1e-7, beta=0.9, m=4, T=4, policy=4, depth=4),
+    dict(name="c2_m6_d1", dim=768, layers=12, b=512, seed=29, lr=1e-7, beta=0.9, m=6, T=4, policy=4, depth=1),
+    dict(name="c3_d8", dim=1024, layers=8, b=256, seed=37, lr=1.5e-6, beta=0.9, m=8, T=4, policy=4, depth=8),
+]
+BF16_SAMPLES = 1024  # entries of Delta W per layer (relative norms: ~2% sampling error)
+
+
+def _ref_run(args, shape):
+    with tempfile.TemporaryDirectory() as tmp:
+        path = Path(tmp) / "traj.bin"
+        out = tool(*args, path)
+        return np.fromfile(path, dtype=np.float64).reshape(shape), out
+
+
+def _bf16_case(c):
+    L, n2 = c["layers"], c["dim"] ** 2
+    common = (c["dim"], L, c["b"], c["seed"], repr(c["lr"]), repr(c["beta"]), c["m"], c["T"])
+    traj, info = _ref_run(("toy", *common, c["policy"], c["depth"]), (c["T"] + 1, L, n2))
+    van, _ = _ref_run(("loop", *common, 0), (c["T"] + 1, L, n2))
+    rng = np.random.default_rng(c["seed"])
+    idx = np.stack([np.sort(rng.choice(n2, BF16_SAMPLES, replace=False)) for _ in range(L)]).astype(np.int32)
+    d_ref = traj - traj[0]
+    d_van = van - van[0]
+    pick = lambda a: np.stack([a[:, l, idx[l]] for l in range(L)], axis=1)  # [T+1, L, S]
+    return dict(idx=idx, d_ref=pick(d_ref).astype(np.float32), d_van=pick(d_van)[-1].astype(np.float32),
+                norm_ref=np.sqrt((d_ref ** 2).sum(axis=(1, 2))),
+                norm_gap=np.sqrt(((d_ref - d_van) ** 2).sum(axis=(1, 2)))), json.loads(info)
+
+
+def bf16_goldens():
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        results = list(ex.map(_bf16_case, BF16_GRID))
+    arrays, meta = {}, []
+    for c, (arr, info) in zip(BF16_GRID, results):
+        for k, v in arr.items():
+            arrays[f"{c['name']}.{k}"] = v
+        meta.append(dict(c, **info))
+    np.savez_compressed(OUT / "linear_bf16.npz", **arrays)
+    json.dump(meta, open(OUT / "linear_bf16.json", "w"), indent=1)
+
+
+def loop_goldens():
+    arrays, meta = {}, []
+    for idx, c in enumerate(LOOP_GRID):
+        traj, _ = _ref_run(("loop", c["dim"], c["layers"], c["b"], c["seed"], repr(c["lr"]), repr(c["beta"]),
+                            c["m"], c["T"], c["delayed"]), (c["T"] + 1, c["layers"], c["dim"] ** 2))
+        arrays[f"traj_{idx}"] = traj
+        meta.append(c)
+    np.savez_compressed(OUT / "loop_trajectories.npz", **arrays)
+    json.dump(meta, open(OUT / "loop_trajectories.json", "w"), indent=1)
+
+
 def main():
+    if "--bf16" in sys.argv:
+        return bf16_goldens()
+    if "--loop" in sys.argv:
+        return loop_goldens()
     sched = {f"{p}/{d}/{m}/{T}": schedule_text(p, d, m, T) for p, d, m, T in SMALL_SCHEDULES}
     sweep = {f"{p}/{d}/{m}/{T}": hashlib.sha256(schedule_text(p, d, m, T).encode()).hexdigest()
              for p, d, m, T in SWEEP_SCHEDULES}

@@ -78,3 +78,97 @@ def test_pipeline_rank_grid():
     assert grid(8, 5, 1) == (0, 5, 8)
     with pytest.raises(ValueError):
         grid(6, 0, 4)
+
+
+class _FakeEngine:
+    """Stands in for the engine's stage-blob and replica-join entry points (no GPU):
+    records what connect_pipeline / join_replicas hand it."""
+
+    def __init__(self, depth, local):
+        self.depth, self.local = depth, local
+        self.connected, self.joined = [], None
+
+    def is_local(self, s):
+        return s == self.local
+
+    def export_stage(self, s):
+        assert s == self.local
+        return bytes([s]) * 128
+
+    def connect_stage(self, blob):
+        self.connected.append(blob[0])
+
+
+def _pipeline_worker(rank, world, port, depth, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2006_09503_b200 import dist as D
+    stage, replica, width = D.grid(world, rank, depth)
+    eng = _FakeEngine(depth, stage)
+    D.connect_pipeline(eng, depth)
+    ids_seen = []
+    D.join_replicas(eng, depth, pipelined=True, make_id=lambda: os.urandom(128),
+                    join=lambda e, ids, w, r: ids_seen.append((ids, w, r)))
+    q.put((rank, stage, replica, sorted(eng.connected), ids_seen[0][0], ids_seen[0][1], ids_seen[0][2]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,depth", [(2, 2), (4, 2), (4, 4)])
+def test_connect_pipeline_and_replica_groups_gloo(world, depth):
+    """connect_pipeline's blob exchange (semantics.cpp:299 / :333 hand-offs across
+    processes) and join_replicas' id sharing under world-size 2 / 4: each process
+    connects exactly its stage's neighbours of the SAME replica, and every replica of a
+    stage gets the same communicator id at rank = replica (gpu = stage * width + replica)."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, world, port, depth, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    width = world // depth
+    ids = {o[4] for o in out}
+    assert len(ids) == 1 and len(next(iter(ids))) == 128 * depth  # one id per stage, shared by all
+    for rank, stage, replica, connected, _, w, r in out:
+        assert (stage, replica) == (rank // width, rank % width)
+        assert connected == [s for s in (stage - 1, stage + 1) if 0 <= s < depth]
+        assert (w, r) == (width, replica)
+
+
+def _allreduce_worker(rank, world, port, q):
+    """The AllReduce op's arithmetic across w replicas on gloo: each replica's gradient
+    of its column shard, summed by the collective and divided by count * w at the
+    update (engine.cpp issue_update), equals the wide-microbatch gradient."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    model = O.ToyModel.make(6, 3, 8, 4, 5)
+    cols = 8 // world
+    sub = O.ToyModel(model.dim, model.weights,
+                     [(x[:, rank * cols:(rank + 1) * cols], y[:, rank * cols:(rank + 1) * cols]) for x, y in model.dataset])
+    g, _ = O._batch_gradient(sub, model.weights, 1, 4)  # mean over the m microbatches
+    flat = torch.from_numpy(np.concatenate([x.flatten() for x in g]))
+    dist.all_reduce(flat)
+    q.put((rank, (flat / world).numpy()))
+    dist.destroy_process_group()
+
+
+def test_allreduce_average_equals_wide_microbatch_gloo():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_allreduce_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    model = O.ToyModel.make(6, 3, 8, 4, 5)
+    g_one, _ = O._batch_gradient(model, model.weights, 1, 4)
+    want = np.concatenate([x.flatten() for x in g_one])
+    assert np.array_equal(out[0], out[1])
+    assert np.allclose(out[0], want, rtol=1e-12, atol=1e-14)

@@ -93,3 +93,61 @@ def test_reference_semantics_and_acceptance_suites_on_gpu_engine():
     r = subprocess.run([str(BIN / "dropin_gpu_tests")], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "failed: 0 | assertions:" in r.stdout
+
+
+@pytest.mark.parametrize("idx", range(len(G.loops())))
+def test_engine_reference_loops_bit_identical_at_any_m(idx):
+    """reference_vanilla / reference_2bw (semantics.cpp:188-194) on the engine: with
+    reference_loop's per-microbatch 1/m scaling (:145) they match the reference's loop
+    goldens bit for bit at m = 3..6, where pipelined_execute's sum / count (:338-340)
+    differs from them in the last bits."""
+    meta, ref = G.loops()[idx]
+    model = O.ToyModel.make(meta["dim"], meta["layers"], meta["b"], meta["m"] * meta["T"], meta["seed"])
+    toy = P.ToyModel(model.dim, model.weights, model.dataset)
+    cfg = P.TrainerConfig(meta["lr"], meta["beta"], meta["m"], meta["T"])
+    fn = P.reference_2bw if meta["delayed"] else P.reference_vanilla
+    assert O.max_rel_diff(_flat(fn(toy, cfg)), ref) == 0.0
+    pol = P.PipelinePolicy.TwoBW if meta["delayed"] else P.PipelinePolicy.GPipe
+    piped = _flat(P.pipelined_execute(toy, cfg, pol, 1).trajectory)
+    gap = O.max_rel_diff(piped, ref)
+    assert (gap == 0.0) if meta["m"] in (1, 2, 4, 8) else (0.0 < gap < 1e-12)
+
+
+def test_load_stage_weights_after_a_run_replaces_the_live_version():
+    """A reload between runs lands in the latest version's buffer: the next
+    run starts from the loaded weights whichever slot 2BW left them in."""
+    model = O.ToyModel.make(8, 2, 4, 12, 5)
+    eng = P.Engine(model_kind=P.MODEL_LINEAR_F64, policy=P.PipelinePolicy.TwoBW, depth=1, microbatches=2,
+                   microbatch_size=4, layers=2, dim=8, learning_rate=0.05, momentum=0.0)
+    w0 = np.concatenate([w.flatten(order="F") for w in model.weights])
+    xs = np.concatenate([x.flatten(order="F") for x, _ in model.dataset])
+    ys = np.concatenate([y.flatten(order="F") for _, y in model.dataset])
+    eng.load_stage_weights(0, w0)
+    eng.set_data(xs, ys, 1, 12)
+    eng.run_schedule(3)  # 3 updates: version 3 lives in slot 1
+    eng.sync()
+    eng.load_stage_weights(0, w0)
+    got = eng.read_version(0, 3)
+    eng.close()
+    assert np.array_equal(got, w0)
+
+
+def test_set_data_in_pieces_keeps_earlier_microbatches():
+    """Ranged set_data: growing the dataset keeps what was uploaded before."""
+    meta, ref = G.toy()[0]
+    model = O.ToyModel.make(meta["dim"], meta["layers"], meta["b"], meta["m"] * meta["T"], meta["seed"])
+    n = meta["m"] * meta["T"]
+    eng = P.Engine(model_kind=P.MODEL_LINEAR_F64, policy=P.PipelinePolicy(meta["policy"]), depth=meta["depth"],
+                   microbatches=meta["m"], microbatch_size=meta["b"], layers=meta["layers"], dim=meta["dim"],
+                   learning_rate=meta["lr"], momentum=meta["beta"])
+    per = meta["layers"] // meta["depth"]
+    for s in range(meta["depth"]):
+        eng.load_stage_weights(s, np.concatenate([w.flatten(order="F") for w in model.weights[s * per:(s + 1) * per]]))
+    for k in range(1, n + 1):  # one microbatch per call
+        x, y = model.dataset[k - 1]
+        eng.set_data(x.flatten(order="F"), y.flatten(order="F"), k, 1)
+    eng.run_schedule(meta["T"], snapshots=True)
+    eng.sync()
+    last = np.concatenate([eng.snapshot(s, meta["T"]).reshape(per, -1) for s in range(meta["depth"])])
+    eng.close()
+    assert O.max_rel_diff(last, ref[-1]) == 0.0

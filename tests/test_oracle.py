@@ -135,3 +135,33 @@ def test_oracle_matches_live_reference_toy(tmp_path):
     model = O.ToyModel.make(dim, L, b, m * T, seed)
     traj, _, _ = O.pipelined_execute(model, lr, beta, m, T, pol, d)
     assert O.max_rel_diff(O.flat_trajectory(traj), ref) == 0.0
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_oracle_reference_loop_bit_identical_at_any_m(idx):
+    """reference_loop (semantics.cpp:167-184) restated: bit-identical to the reference at
+    m = 3..6.  pipelined_execute sums the microbatch gradients and divides by the count at
+    the update (:338-340) while reference_loop scales each by 1/m (:145): the two agree to
+    the last bit only for power-of-two m, and otherwise within a few ulps."""
+    meta, ref = G.loops()[idx]
+    model = O.ToyModel.make(meta["dim"], meta["layers"], meta["b"], meta["m"] * meta["T"], meta["seed"])
+    traj, _ = O.reference_loop(model, meta["lr"], meta["beta"], meta["m"], meta["T"], bool(meta["delayed"]))
+    assert O.max_rel_diff(O.flat_trajectory(traj), ref) == 0.0
+    pol = O.TWOBW if meta["delayed"] else O.GPIPE
+    piped, _, _ = O.pipelined_execute(model, meta["lr"], meta["beta"], meta["m"], meta["T"], pol, 1)
+    gap = O.max_rel_diff(O.flat_trajectory(piped), ref)
+    if meta["m"] & (meta["m"] - 1) == 0:
+        assert gap == 0.0
+    else:
+        assert 0.0 < gap < 1e-12, gap
+
+
+def test_package_splitmix64_matches_reference_toy_model():
+    """paper_2006_09503_b200.synthetic.toy_model is ToyModel::make bit for bit (the
+    oracle's scalar splitmix64 restatement, itself pinned by the trajectories above)."""
+    from paper_2006_09503_b200 import synthetic as S
+    for dim, L, b, nmb, seed in ((4, 2, 2, 3, 12345), (16, 3, 8, 2, 7), (32, 1, 5, 4, 2 ** 63 + 5)):
+        m = O.ToyModel.make(dim, L, b, nmb, seed)
+        ws, data = S.toy_model(dim, L, b, nmb, seed)
+        assert all(np.array_equal(a, c) for a, c in zip(m.weights, ws))
+        assert all(np.array_equal(a[0], c[0]) and np.array_equal(a[1], c[1]) for a, c in zip(m.dataset, data))

@@ -42,10 +42,9 @@ def run_case(spec, depth, m, T, lr, beta, seed):
     return params, ids, tg, losses, finals, c
 
 
-@pytest.mark.parametrize("depth,causal,head_rows,seq", [(1, True, 0, 64), (2, True, 0, 64), (2, False, 16, 64),
-                                                        (2, True, 0, 128), (1, False, 20, 256)])
+@pytest.mark.parametrize("depth,causal,head_rows,seq", [(1, True, 0, 128), (2, True, 0, 128), (2, False, 16, 128),
+                                                        (1, False, 20, 256)])
 def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows, seq):
-    # seq 64 runs the CUDA-core attention, seq % 128 == 0 the tcgen05 attention
     spec = TO.Spec(layers=2, hidden=128, heads=2, seq=seq, vocab=500, batch=2, causal=causal, head_rows=head_rows)
     m, T, lr, beta, seed = 2, 4, 0.5, 0.9, 1234
     params, ids, tg, losses, finals, c = run_case(spec, depth, m, T, lr, beta, seed)
@@ -70,31 +69,37 @@ def test_transformer_2bw_matches_delayed_oracle(depth, causal, head_rows, seq):
         assert gap > 2 * err, (s, gap, err)  # 2BW is distinguishable from vanilla at this tolerance
 
 
-@pytest.mark.parametrize("depth,layers,batch,hidden,causal,head_rows",
-                         [(1, 2, 1, 768, False, 77), (2, 2, 1, 768, False, 77), (1, 1, 16, 768, False, 77),
-                          (2, 2, 2, 1024, True, 0)])  # the last: GPT-24 / BERT-large width, causal LM head
-def test_bench_width_layers_match_delayed_oracle(depth, layers, batch, hidden, causal, head_rows):
-    """The bench's layer shape (BERT-base: hidden 768, 12 heads, seq 512, 77 MLM rows per
-    sequence) through the whole engine: the production GEMM tiles (CTA pairs, split-K,
-    fused epilogues), the tcgen05 attention at seq 512, the LayerNorm ring and the
-    side-stream weight gradients, against the float64 oracle.  batch 16 is the bench's
-    microbatch (8192 tokens: the exact tile / split choices of the measured step)."""
-    spec = TO.Spec(layers=layers, hidden=hidden, heads=hidden // 64, seq=512, vocab=1000, batch=batch,
+@pytest.mark.parametrize("depth,layers,batch,hidden,causal,head_rows,vocab",
+                         [(1, 2, 1, 768, False, 77, 1000), (2, 2, 1, 768, False, 77, 1000),
+                          (1, 1, 16, 768, False, 77, 1000),
+                          (2, 2, 2, 1024, True, 0, 1000),     # GPT-24 / BERT-large width, causal LM head
+                          (1, 4, 2, 768, False, 77, 30522),   # BERT-base: the bench's full MLM head
+                          (2, 2, 1, 1920, True, 0, 51200)])   # GPT-2.2B width, 30 heads, V 51200
+def test_bench_width_layers_match_delayed_oracle(depth, layers, batch, hidden, causal, head_rows, vocab):
+    """The configs' layer shapes (BERT-base: hidden 768, 12 heads, seq 512, 77 MLM rows per
+    sequence; GPT-24 / BERT-large 1024; GPT-2.2B 1920 with its 51200-way head) through the
+    whole engine: the production GEMM tiles (CTA pairs, split-K, fused epilogues), the
+    tcgen05 attention at seq 512, the LayerNorm ring and the side-stream weight
+    gradients, against the float64 oracle.  batch 16 is the bench's BERT microbatch
+    (8192 tokens: the exact tile / split choices of the measured step)."""
+    spec = TO.Spec(layers=layers, hidden=hidden, heads=hidden // 64, seq=512, vocab=vocab, batch=batch,
                    causal=causal, head_rows=head_rows)
     m, T, lr, beta, seed = 2, 3, 0.05, 0.9, 99
     params, ids, tg, losses, finals, c = run_case(spec, depth, m, T, lr, beta, seed)
     assert c.max_versions_held == 2
     traj, ref_losses = TO.train(params, spec, ids, tg, lr, beta, m, T, delayed=True)
+    print(f"h {hidden} V {vocab}: max loss rel err {np.max(np.abs(losses - ref_losses) / np.abs(ref_losses)):.2e}")
     assert np.all(np.abs(losses - ref_losses) <= LOSS_RTOL * np.abs(ref_losses)), (losses, ref_losses)
     for s in range(depth):
         w0 = TO.flatten_stage(params, spec, depth, s).astype(np.float64)
         ref = TO.flatten_stage({k: v.numpy() for k, v in traj[-1].items()}, spec, depth, s).astype(np.float64)
         err = np.linalg.norm((finals[s] - w0) - (ref - w0)) / np.linalg.norm(ref - w0)
+        print(f"  stage {s}: delta err {err:.4f}")
         assert err < DELTA_RTOL, (s, err)
 
 
 def test_depths_agree_with_each_other():
-    spec = TO.Spec(layers=4, hidden=128, heads=2, seq=64, vocab=300, batch=2, causal=True)
+    spec = TO.Spec(layers=4, hidden=128, heads=2, seq=128, vocab=300, batch=2, causal=True)
     m, T = 4, 3
     _, _, _, l1, f1, _ = run_case(spec, 1, m, T, 0.3, 0.9, 77)
     _, _, _, l4, f4, _ = run_case(spec, 4, m, T, 0.3, 0.9, 77)

@@ -34,11 +34,12 @@ def ref_attention(qkv, b, s, nh, causal):
 
 
 @pytest.mark.parametrize("b,s,nh,causal", [(2, 128, 2, True), (2, 128, 2, False), (1, 512, 4, True),
-                                           (3, 512, 2, False), (2, 96, 3, True),
+                                           (3, 512, 2, False), (2, 1024, 3, True), (1, 2048, 2, False),
                                            # more work items than SMs: the persistent backward's
                                            # cross-item pipeline (K/V ring, dK/dV hand-off)
                                            (16, 512, 12, False), (8, 384, 12, True)])
 def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
+    """One tcgen05 implementation per pass, for every seq % 128 == 0 (no CUDA-core path)."""
     h = nh * 64
     g = torch.Generator(device="cuda").manual_seed(b * 1000 + s + nh)
     qkv = (torch.randn(b * s, 3 * h, device="cuda", generator=g) * 0.8).to(torch.bfloat16)
@@ -60,6 +61,14 @@ def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
     ref = ref_in.grad
     err = (dqkv.float() - ref).abs().max().item()
     assert err < 3e-2 * max(1.0, ref.abs().max().item()), err
+
+
+def test_attention_rejects_untiled_sequence_length():
+    qkv = torch.zeros(2 * 96, 3 * 128, device="cuda", dtype=torch.bfloat16)
+    o = torch.empty(2 * 96, 128, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(2 * 2 * 96, device="cuda", dtype=torch.float32)
+    with pytest.raises(Exception, match="multiple of 128"):
+        call("p2bw_kernel_attention_fwd", ptr(qkv), ptr(o), ptr(lse), 2, 96, 2, 1, stream())
 
 
 @pytest.mark.parametrize("rows,h", [(300, 256), (1024, 768), (64, 1024), (33, 1920),
