@@ -153,17 +153,18 @@ public:
             alloc(&x, static_cast<size_t>(cap) * act_);
             alloc(&y, static_cast<size_t>(cap) * act_);
             alloc(&loss, static_cast<size_t>(cap));
-            check_cuda(cudaMemset(loss, 0, sizeof(double) * cap), "cudaMemset");
+            check_cuda(cudaMemsetAsync(loss, 0, sizeof(double) * cap, stream_), "cudaMemset");
             if (capacity_ > 0) {
                 const size_t keep = static_cast<size_t>(capacity_) * act_ * sizeof(double);
-                check_cuda(cudaMemcpy(x, x_, keep, cudaMemcpyDeviceToDevice), "D2D x");
-                check_cuda(cudaMemcpy(y, y_, keep, cudaMemcpyDeviceToDevice), "D2D y");
-                check_cuda(cudaMemcpy(loss, loss_, sizeof(double) * capacity_, cudaMemcpyDeviceToDevice), "D2D loss");
+                check_cuda(cudaMemcpyAsync(x, x_, keep, cudaMemcpyDeviceToDevice, stream_), "D2D x");
+                check_cuda(cudaMemcpyAsync(y, y_, keep, cudaMemcpyDeviceToDevice, stream_), "D2D y");
+                check_cuda(cudaMemcpyAsync(loss, loss_, sizeof(double) * capacity_, cudaMemcpyDeviceToDevice, stream_), "D2D loss");
             }
             // stage 0's stash points into the dataset for in-flight microbatches: rebase it
             for (auto& p : xin_)
                 if (p != nullptr && x_ != nullptr && p >= x_ && p < x_ + static_cast<size_t>(capacity_) * act_)
                     p = x + (p - x_);
+            check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
             for (double* p : {x_, y_, loss_}) cudaFree(p);
             x_ = x, y_ = y, loss_ = loss;
             capacity_ = cap;
@@ -177,7 +178,11 @@ public:
 
     void load_weights(int wslot, const void* host, size_t bytes) override {
         if (bytes != weight_bytes_public()) throw Error("load_weights: size mismatch");
-        check_cuda(cudaMemcpy(wslot_ptr(wslot, 0), host, bytes, cudaMemcpyHostToDevice), "H2D W");
+        // stream-ordered: a pageable cudaMemcpy may return before its DMA lands, and the
+        // stage's kernels run on a non-blocking stream
+        check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+        check_cuda(cudaMemcpyAsync(wslot_ptr(wslot, 0), host, bytes, cudaMemcpyHostToDevice, stream_), "H2D W");
+        check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
     }
     void read_weights(int wslot, void* host, size_t bytes, cudaStream_t s) override {
         if (bytes != weight_bytes_public()) throw Error("read_weights: size mismatch");

@@ -179,7 +179,9 @@ public:
     void load_weights(int wslot, const void* host, size_t bytes) override {
         if (bytes != weight_bytes_public()) throw Error("load_weights: size mismatch");
         check_cuda(cudaStreamSynchronize(stream_), "sync");
-        check_cuda(cudaMemcpy(staging_, host, bytes, cudaMemcpyHostToDevice), "H2D W");
+        // stream-ordered: a pageable cudaMemcpy may return before its DMA lands, and the
+        // conversion below runs on a non-blocking stream that would not wait for it
+        check_cuda(cudaMemcpyAsync(staging_, host, bytes, cudaMemcpyHostToDevice, stream_), "H2D W");
         k_f64_to_f32<<<grid_1d(nparam_), 256, 0, stream_>>>(staging_, master_, nparam_);
         cast_f32_bf16(master_, wbf_[static_cast<size_t>(wslot)], nparam_, stream_);
         check_cuda(cudaMemsetAsync(vel_, 0, nparam_ * sizeof(float), stream_), "memset vel");

@@ -151,7 +151,9 @@ public:
 
     void load_weights(int wslot, const void* host, size_t bytes) override {
         if (bytes != weight_bytes_public()) throw Error("load_weights: expected the flat fp32 parameter vector");
-        check_cuda(cudaMemcpy(master_, host, bytes, cudaMemcpyHostToDevice), "H2D master");
+        check_cuda(cudaStreamSynchronize(stream_), "sync");
+        // stream-ordered (a pageable cudaMemcpy may return before its DMA lands)
+        check_cuda(cudaMemcpyAsync(master_, host, bytes, cudaMemcpyHostToDevice, stream_), "H2D master");
         cast_f32_bf16(master_, wbf_[wslot], nparam_, stream_);
         check_cuda(cudaMemsetAsync(vel_, 0, nparam_ * sizeof(float), stream_), "memset vel");
         if (vel2_) check_cuda(cudaMemsetAsync(vel2_, 0, nparam_ * sizeof(float), stream_), "memset vel2");
@@ -499,7 +501,9 @@ private:
                     idx[static_cast<size_t>(bb) * rows_per_seq_ + j] =
                         bb * seq_ + static_cast<int>((static_cast<long>(j) * seq_) / rows_per_seq_);
             head_idx_ = dalloc<int>(idx.size());
-            check_cuda(cudaMemcpy(head_idx_, idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D idx");
+            check_cuda(cudaMemcpyAsync(head_idx_, idx.data(), idx.size() * sizeof(int), cudaMemcpyHostToDevice,
+                                       cudaStreamPerThread), "H2D idx");
+            check_cuda(cudaStreamSynchronize(cudaStreamPerThread), "sync idx");
         }
         const size_t red = std::max({layernorm_bwd_scratch_floats(T_, h_), colsum_scratch_floats(T_, 4 * h_),
                                      layernorm_bwd_scratch_floats(R_, h_)});

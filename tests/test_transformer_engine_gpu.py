@@ -156,8 +156,9 @@ def test_transformer_1f1b_weight_stashing():
     itself is pinned bit-exactly on the linear chain (test_engine_linear_gpu)."""
     spec = TO.Spec(layers=4, hidden=128, heads=2, seq=128, vocab=500, batch=2, causal=True, head_rows=0)
     depth, m, T = 4, 4, 3
-    ids, tg = TO.synthetic_batch(spec, m * T, 5)
-    eng = make_engine(spec, depth, m, 0.05, 0.9, 3, policy=P.PipelinePolicy.PipeDream1F1B)
+    ids, tg = TO.synthetic_batch(spec, 1, 5)  # one microbatch repeated: a learnable target
+    ids, tg = np.repeat(ids, m * T, axis=0), np.repeat(tg, m * T, axis=0)
+    eng = make_engine(spec, depth, m, 0.5, 0.9, 3, policy=P.PipelinePolicy.PipeDream1F1B)
     eng.init_weights()
     eng.set_data(ids, tg, 1, m * T)
     eng.run_schedule(T)
@@ -167,4 +168,5 @@ def test_transformer_1f1b_weight_stashing():
     eng.close()
     assert c.version_consistent
     assert 2 <= c.max_versions_held <= depth + 1
-    assert np.all(np.isfinite(losses)) and losses[-1] < losses[0]
+    # training makes progress: the last batch's mean loss is below the first batch's
+    assert np.all(np.isfinite(losses)) and losses[-m:].mean() < losses[:m].mean(), losses
