@@ -8,6 +8,8 @@
 //   ref_tool toy <dim> <layers> <b> <seed> <lr> <beta> <m> <T> <policy> <depth> <out.bin>
 //   ref_tool loop <dim> <layers> <b> <seed> <lr> <beta> <m> <T> <delayed> <out.bin>
 //   ref_tool time <dim> <layers> <b> <m> <T> <depth> <seed>   (2BW pipelined_execute, seconds)
+//   ref_tool simulate <model.json> <cluster.json> <policy> <w> <d> <b> <grad_accum> <recompute> <T>
+//            (simulate_policy, simulator.cpp:140-339: throughput / steady batch time / bubble)
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -20,6 +22,7 @@
 #include "pipesim/profile.hpp"
 #include "pipesim/schedule.hpp"
 #include "pipesim/semantics.hpp"
+#include "pipesim/simulator.hpp"
 
 using namespace pipesim;
 
@@ -85,6 +88,18 @@ int main(int argc, char** argv) {
             const auto cfg = trainer(std::atof(argv[6]), std::atof(argv[7]), m, T);
             write_traj(std::atoi(argv[10]) ? reference_2bw(model, cfg) : reference_vanilla(model, cfg),
                        argv[11]);
+        } else if (cmd == "simulate" && argc == 11) {
+            ParallelConfig cfg;
+            cfg.width = std::atoi(argv[5]);
+            cfg.depth = std::atoi(argv[6]);
+            cfg.microbatch_size = std::atoi(argv[7]);
+            cfg.grad_accum = std::atoi(argv[8]);
+            cfg.recompute = std::atoi(argv[9]) != 0;
+            const auto r = simulate_policy(static_cast<PipelinePolicy>(std::atoi(argv[4])),
+                                           load_model_profile(slurp(argv[2])), load_cluster_spec(slurp(argv[3])),
+                                           cfg, std::atoi(argv[10]));
+            std::printf("{\"throughput\": %.17g, \"steady_batch_time\": %.17g, \"bubble_fraction\": %.17g}\n",
+                        r.throughput, r.steady_batch_time, r.bubble_fraction);
         } else if (cmd == "time" && argc == 9) {
             const int dim = std::atoi(argv[2]), layers = std::atoi(argv[3]), b = std::atoi(argv[4]);
             const int m = std::atoi(argv[5]), T = std::atoi(argv[6]), depth = std::atoi(argv[7]);

@@ -8,7 +8,9 @@ import torch
 sys.path.insert(0, ".")
 from paper_2006_09503_b200._lib import call  # noqa: E402
 
-b, s, nh, causal = 16, 512, 12, int(sys.argv[1]) if len(sys.argv) > 1 else 0
+causal = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+nh = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+b, s = 16, 512
 h = nh * 64
 g = torch.Generator(device="cuda").manual_seed(0)
 qkv = (torch.randn(b * s, 3 * h, device="cuda", generator=g) * 0.5).to(torch.bfloat16)

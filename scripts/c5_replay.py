@@ -106,6 +106,26 @@ def replay(programs, stages, policy, b, xfer_bps):
             "exposed_fraction": max(0.0, steady - compute_bound) / steady}
 
 
+def breakdown(prof: str, policy, d: int, m: int, b: int = B, T: int = T_BATCHES) -> dict:
+    """Steady batch time split into additive parts (all from the simulator's rules):
+      ideal            m * mean_s(F_s + B_s)       -- perfectly balanced, no bubble, free links
+      imbalance        m * max_s(F_s + B_s) - ideal -- the slowest stage sets the pace
+      schedule bubble  steady(free links) - m * max_s(F_s + B_s)   -- fill / drain / flush
+      exposed transfer steady(NVLink) - steady(free links)          -- hand-offs on the critical path"""
+    stages = P.partition_equal(prof, d)
+    progs = P.generate_schedule(policy, d, m, T)
+    link = replay(progs, stages, policy, b, NVLINK_BPS)
+    free = replay(progs, stages, policy, b, 1e18)
+    key = str(b)
+    stage_mb = [st["fwd_time"][key] + st["bwd_time"][key] for st in stages]
+    ideal = m * sum(stage_mb) / d * 1e3
+    slow = m * max(stage_mb) * 1e3
+    return {"steady_batch_ms": link["steady_batch_ms"], "ideal_ms": ideal, "imbalance_ms": slow - ideal,
+            "schedule_bubble_ms": free["steady_batch_ms"] - slow,
+            "exposed_transfer_ms": link["steady_batch_ms"] - free["steady_batch_ms"],
+            "throughput": link["throughput"], "bubble_fraction": link["bubble_fraction"]}
+
+
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     if "--profile" in sys.argv:
@@ -124,12 +144,18 @@ def main():
                 continue
             for pol in pols:
                 r = replay(P.generate_schedule(pol, d, m, T_BATCHES), stages, pol, B, NVLINK_BPS)
+                bd = breakdown(prof, pol, d, m)
                 closed = 0.0 if pol == P.PipelinePolicy.TwoBW else (d - 1) / (m + d - 1)
+                st = bd["steady_batch_ms"]
                 row = {"policy": P.to_string(pol), "d": d, "m": m, "b": B,
                        "samples_per_s": round(r["throughput"], 1),
                        "steady_batch_ms": round(r["steady_batch_ms"], 3),
                        "bubble_fraction": round(r["bubble_fraction"], 4), "closed_form_bubble": round(closed, 4),
-                       "imbalance": round(r["imbalance"], 4), "exposed_fraction": round(r["exposed_fraction"], 4)}
+                       "imbalance": round(r["imbalance"], 4), "exposed_fraction": round(r["exposed_fraction"], 4),
+                       # additive split of the steady batch time (fractions of it)
+                       "frac_imbalance": round(bd["imbalance_ms"] / st, 4),
+                       "frac_schedule_bubble": round(bd["schedule_bubble_ms"] / st, 4),
+                       "frac_exposed_transfer": round(bd["exposed_transfer_ms"] / st, 4)}
                 rows.append(row)
                 print(json.dumps(row))
     if len(args) > 1:

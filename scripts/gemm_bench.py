@@ -20,6 +20,16 @@ shapes = [
     ("fc2_wgrad", 768, 3072, 16384, 1, 1, 1),
     ("sq8192", 8192, 8192, 8192, 0, 0, 0),
 ]
+if "gpt-2.2b" in sys.argv[1:]:  # T = 8192 tokens (b 16 x s 512), h 1920, V 51200 (padded)
+    T, H, V = 8192, 1920, 51200
+    shapes = [
+        ("qkv_fwd", T, 3 * H, H, 0, 0, 0), ("proj_fwd", T, H, H, 0, 0, 0), ("fc1_fwd", T, 4 * H, H, 0, 0, 0),
+        ("fc2_fwd", T, H, 4 * H, 0, 0, 0), ("head_fwd", T, V, H, 0, 0, 0),
+        ("qkv_dgrad", T, H, 3 * H, 0, 1, 0), ("proj_dgrad", T, H, H, 0, 1, 0), ("fc1_dgrad", T, H, 4 * H, 0, 1, 0),
+        ("fc2_dgrad", T, 4 * H, H, 0, 1, 0), ("head_dgrad", T, H, V, 0, 1, 0),
+        ("qkv_wgrad", 3 * H, H, T, 1, 1, 1), ("proj_wgrad", H, H, T, 1, 1, 1), ("fc1_wgrad", 4 * H, H, T, 1, 1, 1),
+        ("fc2_wgrad", H, 4 * H, T, 1, 1, 1), ("head_wgrad", V, H, T, 1, 1, 1),
+    ]
 res = []
 for name, m, n, k, am, bm, f32 in shapes:
     a = torch.randn(m * k, device="cuda").to(torch.bfloat16)

@@ -9,7 +9,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2006_09503_b200._lib import call  # noqa: E402
 
-T, h = 8192, 768
+T = 8192
+h = int(sys.argv[1]) if len(sys.argv) > 1 else 768
 P = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
 
 
@@ -70,4 +71,5 @@ tg = torch.randint(0, V, (R,), device="cuda", dtype=torch.int32)
 rl = torch.empty(R, device="cuda")
 t = bench(lambda: call("p2bw_kernel_softmax_xent", P(logits), P(tg), R, V, VP, C.c_float(1.0), P(rl), s))
 out["xent_us"], out["xent_gbs"] = round(t, 2), round(4 * R * VP / t / 1e3, 1)
+out["h"] = h
 print(json.dumps(out))

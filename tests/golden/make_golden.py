@@ -137,7 +137,35 @@ def loop_goldens():
     json.dump(meta, open(OUT / "loop_trajectories.json", "w"), indent=1)
 
 
+# Config 5: the reference's own simulate_policy (simulator.cpp:140-339) on
+# the B200-measured GPT-24 block profile (p2bw_profile_blocks, b 4), one 8 x B200 NVSwitch
+# node (900 GB/s per direction), 2BW / GPipe / PipeDream-Flush at d 2 / 4 / 8, m 4-32 (m a
+# multiple of d: ParallelConfig's m = d * grad_accum), T = 8 batches -- and the same with
+# free transfers (bandwidth 1e9 GB/s), so the exposed-transfer column is the reference's too.
+C5_T = 8
+
+
+def simulate_goldens():
+    prof = OUT / "c5_profile_gpt-24_b200.json"
+    rows = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for tag, gbps in (("nvlink", 900), ("free", 1e9)):
+            cp = Path(tmp) / f"c_{tag}.json"
+            cp.write_text(json.dumps(dict(CLUSTERS["b200_8"], bandwidth_high_gbps=gbps, bandwidth_low_gbps=min(gbps, 50))))
+            for d in (2, 4, 8):
+                for m in (4, 8, 16, 32):
+                    if m % d:
+                        continue
+                    for pol in (4, 1, 3):
+                        r = json.loads(tool("simulate", prof, cp, pol, 1, d, 4, m // d, 0, C5_T))
+                        rows.append(dict(link=tag, policy=pol, d=d, m=m, b=4, **r))
+    json.dump({"profile": prof.name, "cluster": "b200_8", "num_batches": C5_T, "rows": rows},
+              open(OUT / "c5_simulate.json", "w"), indent=1)
+
+
 def main():
+    if "--simulate" in sys.argv:
+        return simulate_goldens()
     if "--bf16" in sys.argv:
         return bf16_goldens()
     if "--loop" in sys.argv:
