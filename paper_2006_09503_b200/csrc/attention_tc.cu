@@ -1,13 +1,44 @@
-// Softmax attention forward on tcgen05 tensor cores (head dim 64,
-// seq % 128 == 0): key blocks of 64 with a lazy online softmax, P kept in TMEM as the
-// A operand of O += P V, 128 TMEM columns and ~50 KB SMEM per CTA so that four CTAs
-// share each SM (one's softmax overlaps the others' MMAs and loads).
+// Softmax attention forward on tcgen05 tensor cores (head dim 64, seq % 128 == 0).
+//
+// Persistent: one CTA per SM walks a stream of work units (sequence, head, 128-query
+// tile), causal units longest first.  Key blocks are 128 wide and S is double-buffered in
+// TMEM, so the tensor pipe computes S_{j+1} = Q K_{j+1}^T while the softmax warps turn
+// S_j into P_j; O is double-buffered too, so a unit's epilogue runs after the next
+// unit's first block instead of waiting for its last PV:
+//
+//   UMMA  S_j = Q K_j^T           128 x 128 fp32 -> TMEM buffer j % 2
+//   SIMT  16 warps: warp (lane quarter q, key quarter c) owns query rows 32q..32q+31 and
+//         keys 32c..32c+31 of the block (four warps per SM sub-partition hide each
+//         other's TMEM and barrier latencies); the four key quarters of a row exchange
+//         their maxima through SMEM (one 128-thread named barrier per lane quarter).
+//         Lazy online softmax: the running max only moves when a block max exceeds it
+//         by > 2^8 (then O and the row-sum partials are rescaled, O in TMEM).
+//         P = exp2(S/8 log2 e - m) -> bf16 -> TMEM over the first 64 columns of S_j's
+//         buffer; 3/8 of the exponentials run on the FMA pipe (exp2_poly2), the scale /
+//         shift and the row sums as packed fp32 pairs (FFMA2 / FADD2)
+//   UMMA  O += P_j V_j            A = P from TMEM, B = V_j (MN-major) from SMEM
+//
+// MMA issue order: S_0, S_1, PV_0, S_2, PV_1, ... (S_{j+1} goes into the buffer PV_{j-1}
+// has finished reading: the tensor pipe executes in order).  Under a causal mask only
+// the last block of a unit (the diagonal) is masked, at 32-key granularity per warp.
+// The epilogue divides by l = sum P and writes O (bf16) and lse = (m + log2 l) / log2 e.
+//
+// Budget (B200, per 128 x 128 block): MMA ~620 clk (S 4 x 64 + PV 8 x 45: an M = 128
+// tcgen05.mma costs >= ~45 clk whatever its N, scripts/micro/umma_rate.cu), 16384
+// exponentials at 16 / clk on the MUFU (scripts/micro/mufu_rate.cu) -> 640 clk with
+// 3/8 of them on the FMA pipe, TMEM reads ~1 KB / clk (scripts/micro/tmem_rate.cu).
+// Measured (scripts/attn_bench.py, B200): GPT-2.2B shape (b 16, s 512, 30 heads,
+// causal) 60 us = 268 TF/s (previous 4-CTAs-per-SM kernel: 88 us); BERT-base
+// (non-causal, 12 heads) 38 us = 336 TF/s.  The per-block period (~2100 clk,
+// scripts/attn_timing.py) is the softmax warps' latency chain (TMEM load -> max ->
+// exchange -> exponentials -> TMEM store), issue-active ~50%.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
 
+#include "kernels.h"
 #include "launch.h"
 #include "profiler.h"
 #include "ptx.cuh"
@@ -21,80 +52,158 @@ CUtensorMap make_tmap_bf16_2d(const bf16* ptr, uint64_t inner, uint64_t outer, i
 
 namespace {
 
-constexpr int kBQ = 128;   // query rows per CTA
-constexpr int kBK = 64;    // keys per block
+constexpr int kT = 128;          // query rows per unit, keys per block
 constexpr int kD = 64;
-constexpr int kThreads = 256;  // 4 role warps + 4 softmax warps (one per TMEM lane quarter)
-constexpr int kRowBytes = 128;                 // one 64-element bf16 row
-constexpr int kQBytes = kBQ * kRowBytes;       // 16 KB
-constexpr int kKVBytes = kBK * kRowBytes;      // 8 KB
-constexpr int kSmemQ = 0;
-constexpr int kSmemK = kSmemQ + kQBytes;       // [2] key blocks
-constexpr int kSmemV = kSmemK + 2 * kKVBytes;  // [2]
-constexpr int kSmemBar = kSmemV + 2 * kKVBytes;
-constexpr int kSmemTotal = kSmemBar + 128 + 1024;  // + barriers + alignment slack (~50 KB: 4 CTAs per SM)
+constexpr int kTile = kT * 128;  // 16 KB: 128 rows of 64 bf16 (128 B, SW128)
+constexpr int kNS = 4;           // K / V stages
+// warps: 0 TMA producer | 1 MMA issuer | 2 TMEM allocator | 3 idle | 4-19 softmax
+// (warp 4 + 4c + q: lane quarter q, key quarter c)
+constexpr int kKq = 4;  // key quarters per row
+constexpr int kThreads = 128 + kKq * 128;
+constexpr int oQ = 0, oK = 2 * kTile, oV = oK + kNS * kTile, oXch = oV + kNS * kTile;  // Q [2] | K | V
+constexpr int oXl = oXch + 2 * kKq * kT * 4;  // row-max exchange [2 parity][key quarter][128 rows]
+constexpr int oBar = oXl + kKq * kT * 4;      // row-sum exchange [key quarter][128 rows] (epilogue)
+// S full, P full, O full, O empty: [2] each.  P full is per S buffer: warps of different
+// lane quarters are not synchronised with each other, so one may already arrive for block
+// g + 1 while another has not arrived for block g.
+constexpr int bQFull = 0, bQEmpty = 2, bKvFull = 4, bKvEmpty = 4 + kNS, bSFull = 4 + 2 * kNS, bPFull = bSFull + 2,
+              bOFull = bPFull + 2, bOEmpty = bPFull + 4, kNumBars = bPFull + 6;
+constexpr int kSmem = oBar + kNumBars * 8 + 16 + 1024;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescale = 8.0f;  // lazy rescale threshold (log2 units): P <= 2^8 between rescales
-// TMEM (128 columns per CTA, so four CTAs share an SM): S block [0, 64) -- P overwrites
-// its first 32 columns in place as packed bf16 -- and the O accumulator [64, 128).
-constexpr uint32_t tS = 0, tO = 64;
+// TMEM: S / P buffers at 0 and 128; O double-buffered at 256 and 384,
+// so a unit's epilogue runs after the next unit's first block instead of stalling on its
+// last PV
+constexpr uint32_t tO = 256;
 
-// Phase timestamps of every CTA (debug; null in production): p2bw_debug_attention_timing.
-// Per CTA 16 u64: [4 j + 0] softmax warp 4 saw S_j, [4 j + 1] its max done, [4 j + 2]
-// its P_j stored, [4 j + 3] MMA thread issued PV_j (j < 4).
-__device__ unsigned long long* g_attn_dbg = nullptr;
+struct Unit {
+    int bh, qt, n;  // (sequence, head), query tile, key blocks
+};
 
-__device__ __forceinline__ void fmark(bool on, int j, int k) {
-    if (on && j < 4) g_attn_dbg[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 4 * j + k] = clock64();
+__device__ __forceinline__ Unit unit_of(int u, int bhn, int nq, bool causal) {
+    Unit r;
+    const int grp = u / bhn;
+    r.bh = u % bhn;
+    r.qt = causal ? nq - 1 - grp : grp;  // causal: longest units first
+    r.n = causal ? r.qt + 1 : nq;
+    return r;
 }
 
-// One CTA per (sequence, head, 128-query tile); four CTAs per SM hide each other's
-// MMA / softmax latencies.  Keys stream in blocks of 64 (K/V double-buffered by TMA):
-//   UMMA  S = Q K_j^T                 128 x 64 fp32 -> TMEM
-//   SIMT  one thread per query row owns the whole block row: lazy online softmax
-//         (the running max m only moves when a row's block max exceeds it by > 2^8,
-//         and then O and l are rescaled, O in TMEM by the same thread);
-//         P = exp2(S*scale - m) -> bf16 -> TMEM over S
-//   UMMA  O += P V_j                  A = P from TMEM, B = V_j (MN-major) from SMEM
-// The epilogue divides by l = sum P and writes O (bf16) and lse = (m + log2 l) / log2 e.
+// Phase timestamps (debug; null in production): p2bw_debug_attention_timing.  Per CTA
+// 64 u64: [8 s + e] for series s and the CTA's first 8 key blocks e.
+__device__ unsigned long long* g_attn_dbg = nullptr;
+
+__device__ __forceinline__ void fmark(int series, int e) {
+    if (g_attn_dbg != nullptr && e < 8) g_attn_dbg[blockIdx.x * 64 + series * 8 + e] = clock64();
+}
+
+// max over 32 values (4 independent FMNMX3 chains, then combined)
+__device__ __forceinline__ float max32(const uint32_t (&v)[32]) {
+    float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 32; e += 8) {
+        a0 = ptx::fmax3(a0, __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+        a1 = ptx::fmax3(a1, __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+        a2 = ptx::fmax3(a2, __uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
+        a3 = ptx::fmax3(a3, __uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
+    }
+    return ptx::fmax3(a0, a1, fmaxf(a2, a3));
+}
+
+// Diagonal block, 32-key chunk k of the block (keys 32k .. 32k+31) in warp quarter qw
+// (query rows 32qw .. 32qw+31): visible if k < qw, partly (key 32k + e for lane >= e) if
+// k == qw, masked if k > qw -- warp-uniform except on the one partial chunk.
+enum ChunkMode { kFull = 0, kPartial = 1, kEmpty = 2 };
+__device__ __forceinline__ int chunk_mode(bool diag, int k, int qw) {
+    return !diag || k < qw ? kFull : (k == qw ? kPartial : kEmpty);
+}
+__device__ __forceinline__ void mask_partial(uint32_t (&v)[32], int lane) {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+        if (e > lane) v[e] = __float_as_uint(-INFINITY);
+}
+
+// 2^x for a pair of x <= 8 on the FMA pipe: x = j + f, j = rint(x) (magic-number add),
+// 2^f by a degree-3 fit on [-1/2, 1/2] (max relative error 7.7e-5, far below bf16's
+// 3.9e-3), and 2^j added to the exponent bits with one IMAD per value -- the low bits of
+// t = x + 1.5 * 2^23 hold j, and (bits(t) << 23) drops the magic's own exponent bits.
+// x is clamped at -125 (the result is then ~0, as exp2 would give).
+__device__ __forceinline__ unsigned long long exp2_poly2(float x0, float x1) {
+    constexpr float kMagic = 12582912.0f;
+    const unsigned long long x = ptx::f2(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+    const unsigned long long t = ptx::fadd2(x, ptx::f2(kMagic, kMagic));
+    const unsigned long long jn = ptx::fadd2(ptx::f2(kMagic, kMagic), ptx::ffma2(t, ptx::f2(-1.0f, -1.0f), 0ull));
+    const unsigned long long fr = ptx::fadd2(x, jn);  // x - j
+    unsigned long long p = ptx::ffma2(ptx::f2(0.05508868396282196f, 0.05508868396282196f), fr,
+                                      ptx::f2(0.24260404706001282f, 0.24260404706001282f));
+    p = ptx::ffma2(p, fr, ptx::f2(0.6932762265205383f, 0.6932762265205383f));
+    p = ptx::ffma2(p, fr, ptx::f2(0.9999289512634277f, 0.9999289512634277f));
+    const float2 pf = ptx::f2_split(p), tf = ptx::f2_split(t);
+    return ptx::f2(__int_as_float(__float_as_int(pf.x) + (__float_as_int(tf.x) << 23)),
+                   __int_as_float(__float_as_int(pf.y) + (__float_as_int(tf.y) << 23)));
+}
+
+// 32 keys of a row: p = exp2(s sc - m) with the scale / shift and the row sums as packed
+// fp32 pairs (FFMA2 / FADD2); kPoly: pairs 2, 5 and 7 of every 8 (3/8 of the values) on
+// the FMA pipe, the rest on the MUFU (whose ex2(-inf) is exactly 0: the masked chunk).
+template <bool kPoly>
+__device__ __forceinline__ void exp_chunk(const uint32_t (&v)[32], unsigned long long sc2, unsigned long long nm2,
+                                          unsigned long long& la, unsigned long long& lb, uint32_t (&pk)[16]) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const unsigned long long x = ptx::ffma2(ptx::f2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1])),
+                                                sc2, nm2);
+        const float2 xf = ptx::f2_split(x);
+        unsigned long long p;
+        if (kPoly && (q % 8 == 2 || q % 8 == 5 || q % 8 == 7)) p = exp2_poly2(xf.x, xf.y);
+        else p = ptx::f2(ptx::ex2(xf.x), ptx::ex2(xf.y));
+        if (q & 1) lb = ptx::fadd2(lb, p);
+        else la = ptx::fadd2(la, p);
+        const float2 pf = ptx::f2_split(p);
+        pk[q] = ptx::pack_bf16x2(pf.x, pf.y);
+    }
+}
+
+__device__ __forceinline__ void exp_chunk_mode(const uint32_t (&v)[32], int mode, unsigned long long sc2,
+                                               unsigned long long nm2, unsigned long long& la, unsigned long long& lb,
+                                               uint32_t (&pk)[16]) {
+    if (mode == kFull) {
+        exp_chunk<true>(v, sc2, nm2, la, lb, pk);
+    } else if (mode == kPartial) {
+        exp_chunk<false>(v, sc2, nm2, la, lb, pk);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) pk[q] = 0u;
+    }
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 template <bool kCausal>
-__global__ void __launch_bounds__(kThreads, 4)
-    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
-                  bf16* __restrict__ out, float* __restrict__ lse, int seq, int heads) {
+__global__ void __launch_bounds__(kThreads, 1)
+    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int seq,
+                  int heads, int bhn) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-    uint64_t* bar_q = bar + 0;
-    uint64_t* kv_full = bar + 1;   // [2]
-    uint64_t* kv_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;
-    uint64_t* p_full = bar + 6;    // 4 arrivals
-    uint64_t* o_done = bar + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+    const uint32_t sbase = ptx::smem_u32(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + oBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kNumBars);
+    float* xch = reinterpret_cast<float*>(smem + oXch);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int bh = blockIdx.x, b = bh / heads, hd = bh % heads;
-    // causal: the longest query tiles (most key blocks) are scheduled first
-    const int qt = kCausal ? static_cast<int>(gridDim.y) - 1 - static_cast<int>(blockIdx.y) : blockIdx.y;
-    const int q0 = qt * kBQ;
-    const int nb = kCausal ? (q0 + kBQ) / kBK : seq / kBK;  // key blocks this tile sees
+    const int nq = seq / kT;
+    const int units = bhn * nq;
     const int h = heads * kD;
-    const int row0 = b * seq;
+    const int G = static_cast<int>(gridDim.x);
 
     if (warp == 0 && lane == 0) {
-        ptx::tma_prefetch_desc(&tm_q);
-        ptx::tma_prefetch_desc(&tm_kv);
-        ptx::mbar_init(bar_q, 1);
-        for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&kv_full[i], 1);
-            ptx::mbar_init(&kv_empty[i], 1);
-        }
-        ptx::mbar_init(s_full, 1);
-        ptx::mbar_init(p_full, 4);
-        ptx::mbar_init(o_done, 1);
+        ptx::tma_prefetch_desc(&tm);
+        for (int i = 0; i < kNumBars; ++i) ptx::mbar_init(&bar[i], (i == bPFull || i == bPFull + 1 || i == bOEmpty || i == bOEmpty + 1) ? 4 * kKq : 1);
         ptx::fence_mbar_init();
     }
-    if (warp == 2) ptx::tmem_alloc<128>(tmem_slot);
+    if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -102,146 +211,195 @@ __global__ void __launch_bounds__(kThreads, 4)
     ptx::pdl_trigger();
     ptx::pdl_wait();
 
-    if (warp == 0) {
-        if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(bar_q, kQBytes);
-            ptx::tma_load_2d(smem + kSmemQ, &tm_q, bar_q, hd * kD, row0 + q0);
-            for (int j = 0; j < nb; ++j) {
-                const int buf = j & 1;
-                ptx::mbar_wait(&kv_empty[buf], ((j >> 1) & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(&kv_full[buf], 2 * kKVBytes);
-                ptx::tma_load_2d(smem + kSmemK + buf * kKVBytes, &tm_kv, &kv_full[buf], h + hd * kD, row0 + j * kBK);
-                ptx::tma_load_2d(smem + kSmemV + buf * kKVBytes, &tm_kv, &kv_full[buf], 2 * h + hd * kD,
-                                 row0 + j * kBK);
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        int qc = 0, kc = 0;
+        for (int u = blockIdx.x; u < units; u += G, ++qc) {
+            const Unit un = unit_of(u, bhn, nq, kCausal);
+            const int row0 = (un.bh / heads) * seq, hd = un.bh % heads;
+            const int qb = qc & 1;
+            ptx::mbar_wait(&bar[bQEmpty + qb], ((qc >> 1) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(&bar[bQFull + qb], kTile);
+            ptx::tma_load_2d(smem + oQ + qb * kTile, &tm, &bar[bQFull + qb], hd * kD, row0 + un.qt * kT);
+            for (int j = 0; j < un.n; ++j, ++kc) {
+                const int st = kc % kNS;
+                ptx::mbar_wait(&bar[bKvEmpty + st], ((kc / kNS) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&bar[bKvFull + st], 2 * kTile);
+                ptx::tma_load_2d(smem + oK + st * kTile, &tm, &bar[bKvFull + st], h + hd * kD, row0 + j * kT);
+                ptx::tma_load_2d(smem + oV + st * kTile, &tm, &bar[bKvFull + st], 2 * h + hd * kD, row0 + j * kT);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t q_addr = ptx::smem_u32(smem + kSmemQ);
-            constexpr uint32_t id_s = ptx::idesc_bf16(128, kBK, false, false);
-            constexpr uint32_t id_pv = ptx::idesc_bf16(128, kD, false, true);
-            ptx::mbar_wait(bar_q, 0);
-            for (int j = 0; j < nb; ++j) {
-                const int buf = j & 1;
-                const uint32_t k_addr = ptx::smem_u32(smem + kSmemK + buf * kKVBytes);
-                const uint32_t v_addr = ptx::smem_u32(smem + kSmemV + buf * kKVBytes);
-                ptx::mbar_wait(&kv_full[buf], (j >> 1) & 1);
-                ptx::tc_fence_after();
-                // S_j overwrites P_{j-1}: in issue order after PV_{j-1}, which reads it
-#pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk)
-                    ptx::umma_bf16(tmem + tS, ptx::sdesc_sw128(q_addr + kk * 32, 16, 1024),
-                                   ptx::sdesc_sw128(k_addr + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-                ptx::umma_commit(s_full);
-                ptx::mbar_wait(p_full, j & 1);
-                ptx::tc_fence_after();
-                fmark(g_attn_dbg != nullptr, j, 3);
-#pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk)
-                    ptx::umma_bf16_ts(tmem + tO, tmem + tS + kk * 8, ptx::sdesc_sw128(v_addr + kk * 2048, 8192, 1024),
-                                      id_pv, (j | kk) != 0 ? 1u : 0u);
-                ptx::umma_commit(&kv_empty[buf]);
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer: S_0, S_1, PV_0, S_2, PV_1, ... over all units ----------------
+        constexpr uint32_t id_s = ptx::idesc_bf16(128, kT, false, false);
+        constexpr uint32_t id_pv = ptx::idesc_bf16(128, kD, false, true);
+        // the CTA's key blocks numbered g = 0, 1, ... across its units
+        int su = blockIdx.x, sj = 0, sq = 0, sn = 0, sg = 0;  // next S: unit, block, unit count, length, g
+        auto issue_s = [&]() {
+            if (sj == 0) {
+                sn = unit_of(su, bhn, nq, kCausal).n;
+                ptx::mbar_wait(&bar[bQFull + (sq & 1)], (sq >> 1) & 1);
             }
-            ptx::umma_commit(o_done);
+            const int st = sg % kNS;
+            ptx::mbar_wait(&bar[bKvFull + st], (sg / kNS) & 1);
+            ptx::tc_fence_after();
+            const uint32_t q_addr = sbase + oQ + (sq & 1) * kTile, k_addr = sbase + oK + st * kTile;
+            const uint32_t dst = tmem + (sg & 1) * 128;
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk)
+                ptx::umma_bf16(dst, ptx::sdesc_sw128(q_addr + kk * 32, 16, 1024),
+                               ptx::sdesc_sw128(k_addr + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+            ptx::umma_commit(&bar[bSFull + (sg & 1)]);
+            fmark(0, sg);
+            sg += 1;
+            if (++sj == sn) {  // next unit
+                sj = 0;
+                sq += 1;
+                su += G;
+            }
+        };
+        int pu = blockIdx.x, pj = 0, pq = 0, pn = 0, g = 0;  // next PV
+        if (pu < units) {
+            pn = unit_of(pu, bhn, nq, kCausal).n;
+            issue_s();
+        }
+        while (pu < units) {
+            if (su < units) issue_s();  // S_{g+1}: its buffer's P_{g-1} was read by PV_{g-1}
+            ptx::mbar_wait(&bar[bPFull + (g & 1)], (g >> 1) & 1);
+            const int ob = pq & 1;
+            if (pj == 0 && pq > 1) ptx::mbar_wait(&bar[bOEmpty + ob], ((pq - 2) >> 1) & 1);  // O of unit pq - 2 read
+            ptx::tc_fence_after();
+            const int st = g % kNS;
+            const uint32_t v_addr = sbase + oV + st * kTile;
+            const uint32_t pa = tmem + (g & 1) * 128;
+#pragma unroll
+            for (int kk = 0; kk < kT / 16; ++kk)
+                ptx::umma_bf16_ts(tmem + tO + ob * 128, pa + kk * 8, ptx::sdesc_sw128(v_addr + kk * 2048, 8192, 1024),
+                                  id_pv, (pj | kk) != 0 ? 1u : 0u);
+            ptx::umma_commit(&bar[bKvEmpty + st]);  // also: PV_g complete (the softmax's O rescale)
+            fmark(7, g);
+            g += 1;
+            if (++pj == pn) {
+                ptx::umma_commit(&bar[bOFull + ob]);
+                ptx::umma_commit(&bar[bQEmpty + (pq & 1)]);
+                pj = 0;
+                pq += 1;
+                pu += G;
+                if (pu < units) pn = unit_of(pu, bhn, nq, kCausal).n;
+            }
         }
     } else if (warp >= 4) {
-        const int qw = warp & 3;           // TMEM lane quarter
-        const int r = qw * 32 + lane;      // query row within the tile
-        const int i = q0 + r;
-        const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+        // ---------------- softmax: 16 warps, (lane quarter, key quarter) ----------------
+        const int qw = warp & 3, kq = (warp - 4) >> 2;
+        const int r = qw * 32 + lane;  // query row within the unit's tile
+        const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
         const float sc = 0.125f * kLog2e;
-        const bool dbg = g_attn_dbg != nullptr && warp == 4 && lane == 0;
-        float m = -INFINITY;  // running max (log2 domain)
-        float l = 0.0f;       // row sum at max m
-        for (int j = 0; j < nb; ++j) {
-            ptx::mbar_wait(s_full, j & 1);
-            fmark(dbg, j, 0);
+        const bool mk = warp == 4 && lane == 0;
+        // epilogue of unit (count pc, tile un, max m): O / l (bf16) and lse; O is released as
+        // soon as it is in registers
+        float* xl = reinterpret_cast<float*>(smem + oXl);
+        auto epilogue = [&](int pc, const Unit& un, float pm, float lq) {
+            const int ob = pc & 1;
+            const uint32_t ot = tmem + lane_off + tO + ob * 128;
+            xl[kq * kT + r] = lq;  // the row sum from the four key quarters' partials
+            ptx::mbar_wait(&bar[bOFull + ob], (pc >> 1) & 1);
             ptx::tc_fence_after();
-            const int kbase = j * kBK;
-            const bool diag = kCausal && kbase + kBK > q0;  // block crosses the diagonal
-            // block max of the row
-            float bm = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(trow + tS + c * 32, v);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (!diag || kbase + c * 32 + e <= i) bm = fmaxf(bm, __uint_as_float(v[e]));
-            }
-            bm *= sc;
-            const float m_new = bm > m + kRescale ? bm : m;  // lazy: only large increases move m
-            const bool moved = m_new != m;
-            const float f = moved ? (m == -INFINITY ? 0.0f : ptx::ex2(m - m_new)) : 1.0f;
-            l *= f;
-            m = m_new;
-            fmark(dbg, j, 1);
-            if (j > 0 && __any_sync(0xffffffffu, moved)) {
-                // rescale the O row (rows that did not move scale by 1); PV_{j-1} has
-                // completed: S_j's commit covers every earlier MMA
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t o[32];
-                    ptx::tmem_ld_32x32b_x32(trow + tO + c * 32, o);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-                    ptx::tmem_st_32x32b_x32(trow + tO + c * 32, o);
-                }
-            }
-            // P = exp2(S * sc - m) -> bf16 -> TMEM over S (keys 0-31 -> columns 0-15,
-            // 32-63 -> 16-31, each written after its S columns were read)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(trow + tS + c * 32, v);
-                ptx::tmem_ld_wait();
-                uint32_t pk[16];
-#pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                    float p0 = ptx::ex2(fmaf(__uint_as_float(v[e]), sc, -m));
-                    float p1 = ptx::ex2(fmaf(__uint_as_float(v[e + 1]), sc, -m));
-                    if (diag && kbase + c * 32 + e > i) p0 = 0.0f;
-                    if (diag && kbase + c * 32 + e + 1 > i) p1 = 0.0f;
-                    l += p0 + p1;
-                    pk[e / 2] = ptx::pack_bf16x2(p0, p1);
-                }
-                ptx::tmem_st_32x32b_x16(trow + tS + c * 16, pk);
-            }
-            ptx::tmem_st_wait();
+            uint32_t o[16];
+            ptx::tmem_ld_32x32b_x16(ot + kq * 16, o);
+            ptx::tmem_ld_wait();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(p_full);
-            fmark(dbg, j, 2);
-        }
-        // epilogue: O / l, lse
-        ptx::mbar_wait(o_done, 0);
-        ptx::tc_fence_after();
-        const float inv = 1.0f / l;
-        bf16* orow = out + static_cast<size_t>(row0 + i) * h + hd * kD;
+            if (lane == 0) ptx::mbar_arrive(&bar[bOEmpty + ob]);
+            named_bar(5 + qw, 32 * kKq);
+            const float l = (xl[r] + xl[kT + r]) + (xl[2 * kT + r] + xl[3 * kT + r]);
+            named_bar(5 + qw, 32 * kKq);  // read before the next epilogue writes
+            const float inv = 1.0f / l;
+            const int i = un.qt * kT + r;
+            bf16* orow = out + static_cast<size_t>((un.bh / heads) * seq + i) * h + (un.bh % heads) * kD + kq * 16;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            uint32_t o[32];
-            ptx::tmem_ld_32x32b_x32(trow + tO + c * 32, o);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint4 w = make_uint4(
+            for (int q = 0; q < 2; ++q)
+                *reinterpret_cast<uint4*>(orow + 8 * q) = make_uint4(
                     ptx::pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
                     ptx::pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
                     ptx::pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
                     ptx::pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
-                *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = w;
+            if (kq == 0) lse[static_cast<size_t>(un.bh) * seq + i] = (pm + log2f(l)) / kLog2e;
+        };
+        int g = 0, oc = 0;
+        bool pending = false;  // the previous unit's epilogue, run after this unit's first block
+        Unit pun{};
+        float pm_prev = 0.0f, pl_prev = 0.0f;
+        for (int u = blockIdx.x; u < units; u += G, ++oc) {
+            const Unit un = unit_of(u, bhn, nq, kCausal);
+            const uint32_t ot = tmem + lane_off + tO + (oc & 1) * 128;  // this unit's O
+            float m = -INFINITY;  // running max (log2 domain)
+            unsigned long long la = 0ull, lb = 0ull;  // this key quarter's row sum at max m (two pairs)
+            for (int j = 0; j < un.n; ++j, ++g) {
+                const uint32_t sb = tmem + lane_off + (g & 1) * 128;  // this block's S / P buffer
+                ptx::mbar_wait(&bar[bSFull + (g & 1)], (g >> 1) & 1);
+                if (mk) fmark(1, g);
+                ptx::tc_fence_after();
+                const int md = chunk_mode(kCausal && j == un.n - 1, kq, qw);
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(sb + kq * 32, v);
+                ptx::tmem_ld_wait();
+                if (md == kPartial) mask_partial(v, lane);
+                const float pm = md == kEmpty ? -INFINITY : max32(v);
+                // the row's four key quarters exchange maxima; after this barrier every warp
+                // has read its S, so P may overwrite any of the buffer's first 64 columns
+                float* xm = xch + (g & 1) * kKq * kT;
+                xm[kq * kT + r] = pm;
+                named_bar(1 + qw, 32 * kKq);
+                const float bm = fmaxf(fmaxf(xm[r], xm[kT + r]), fmaxf(xm[2 * kT + r], xm[3 * kT + r])) * sc;
+                if (mk) fmark(2, g);
+                const float m_new = bm > m + kRescale ? bm : m;  // lazy: only large increases move m
+                const bool moved = m_new != m;
+                const float f = moved ? (m == -INFINITY ? 0.0f : ptx::ex2(m - m_new)) : 1.0f;
+                if (moved) {
+                    la = ptx::ffma2(la, ptx::f2(f, f), 0ull);
+                    lb = ptx::ffma2(lb, ptx::f2(f, f), 0ull);
+                }
+                m = m_new;
+                const unsigned long long sc2 = ptx::f2(sc, sc), nm2 = ptx::f2(-m, -m);
+                uint32_t pk[16];
+                exp_chunk_mode(v, md, sc2, nm2, la, lb, pk);
+                ptx::tmem_st_32x32b_x16(sb + kq * 16, pk);  // keys 32 kq .. -> P columns 16 kq ..
+                if (j > 0 && __any_sync(0xffffffffu, moved)) {
+                    // rescale this row's quarter of O once PV_{g-1} is
+                    // complete (its commit is the K/V release of block g-1; the next completion
+                    // of that barrier needs P_{g+kNS-1}, so its phase cannot have moved on)
+                    ptx::mbar_wait(&bar[bKvEmpty + (g - 1) % kNS], ((g - 1) / kNS) & 1);
+                    ptx::tc_fence_after();
+                    uint32_t o[16];
+                    ptx::tmem_ld_32x32b_x16(ot + kq * 16, o);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                    ptx::tmem_st_32x32b_x16(ot + kq * 16, o);
+                }
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bar[bPFull + (g & 1)]);
+                if (mk) fmark(3, g);
+                if (j == 0 && pending) {
+                    epilogue(oc - 1, pun, pm_prev, pl_prev);
+                    pending = false;
+                }
             }
+            pending = true;
+            pun = un;
+            pm_prev = m;
+            const float2 lfa = ptx::f2_split(la), lfb = ptx::f2_split(lb);
+            pl_prev = (lfa.x + lfa.y) + (lfb.x + lfb.y);
         }
-        lse[static_cast<size_t>(bh) * seq + i] = (m + log2f(l)) / kLog2e;
+        if (pending) epilogue(oc - 1, pun, pm_prev, pl_prev);
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<128>(tmem);
+        ptx::tmem_dealloc<512>(tmem);
     }
 }
 
@@ -253,7 +411,7 @@ void set_smem_once() {
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const uint32_t bit = 1u << (dev & 31);
     if (done.load() & bit) return;
-    check_cuda(cudaFuncSetAttribute(k_attn_fwd_tc<kCausal>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal),
+    check_cuda(cudaFuncSetAttribute(k_attn_fwd_tc<kCausal>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem),
                "cudaFuncSetAttribute(k_attn_fwd_tc)");
     done.fetch_or(bit);
 }
@@ -268,17 +426,18 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
                       cudaStream_t s) {
     const int h = heads * kD;
     const uint64_t rows = static_cast<uint64_t>(batch) * seq;
-    const CUtensorMap tq = make_tmap_bf16_2d(qkv, 3ull * h, rows, 3ll * h, 64, kBQ);
-    const CUtensorMap tkv = make_tmap_bf16_2d(qkv, 3ull * h, rows, 3ll * h, 64, kBK);
-    dim3 grid(batch * heads, seq / kBQ);
+    const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * h, rows, 3ll * h, 64, kT);
+    const int bhn = batch * heads;
+    const int units = bhn * (seq / kT);
+    const int grid = std::max(1, std::min(num_sms(), units));
     if (causal) {
         set_smem_once<true>();
-        launch_pdl(k_attn_fwd_tc<true>, grid, dim3(kThreads), kSmemTotal, s, "k_attn_fwd_tc", tq, tkv, o, lse, seq,
-                   heads);
+        launch_pdl(k_attn_fwd_tc<true>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_fwd_tc", tm, o, lse, seq, heads,
+                   bhn);
     } else {
         set_smem_once<false>();
-        launch_pdl(k_attn_fwd_tc<false>, grid, dim3(kThreads), kSmemTotal, s, "k_attn_fwd_tc", tq, tkv, o, lse, seq,
-                   heads);
+        launch_pdl(k_attn_fwd_tc<false>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_fwd_tc", tm, o, lse, seq,
+                   heads, bhn);
     }
     check_cuda(cudaGetLastError(), "attention_fwd_tc");
 }

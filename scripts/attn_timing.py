@@ -1,5 +1,6 @@
-"""Phase timing of the tcgen05 attention forward (diagnostic): clock64 marks of the
-first 4 key blocks of every CTA (attention_tc.cu g_attn_dbg)."""
+"""Phase timing of the persistent tcgen05 attention forward (diagnostic): clock64 marks of
+the first 8 key blocks of each slot of every CTA (attention_tc.cu g_attn_dbg).
+    python scripts/attn_timing.py [causal] [heads]"""
 import ctypes as C
 import sys
 
@@ -8,9 +9,11 @@ import torch
 sys.path.insert(0, ".")
 from paper_2006_09503_b200._lib import call  # noqa: E402
 
-b, s, nh, causal = 16, 512, 12, int(sys.argv[1]) if len(sys.argv) > 1 else 0
+causal = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+nh = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+b, s = 16, 512
 h = nh * 64
-qkv = torch.randn(b * s, 3 * h, device="cuda").to(torch.bfloat16)
+qkv = (torch.randn(b * s, 3 * h, device="cuda") * 0.5).to(torch.bfloat16)
 o = torch.empty(b * s, h, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(b * nh * s, device="cuda")
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -24,15 +27,16 @@ for _ in range(10):
     fwd()
 e1.record()
 torch.cuda.synchronize()
-ctas = b * nh * (s // 128)
-print(f"attention fwd: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us per launch ({ctas} CTAs)")
-dbg = torch.zeros(ctas * 16, dtype=torch.int64, device="cuda")
+print(f"attention fwd: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us per launch")
+dbg = torch.zeros(148 * 64, dtype=torch.int64, device="cuda")
 call("p2bw_debug_attention_timing", P(dbg))
 fwd()
 torch.cuda.synchronize()
 call("p2bw_debug_attention_timing", None)
-d = dbg.view(ctas, 4, 4).cpu().double()
-t0 = d[:, 0, 0:1]
-print("per key block j (median cycles from S_0 seen): S seen | pass 1 done | P stored | PV issued")
-for j in range(4):
-    print(f"j={j}: " + " ".join(f"{(d[:, j, k:k + 1] - t0).median().item():8.0f}" for k in range(4)))
+d = dbg.view(148, 8, 8).cpu().double()  # [cta][series][e]
+t0 = d[:, 0, 0:1]  # slot 0 only
+names = ["S issued", "S seen", "max exch", "P arrived", "-", "-", "-", "PV issued"]
+print("median cycles from the first S issue, per block e of the slot's stream")
+print("      " + " ".join(f"{n:>12s}" for n in names))
+for e in range(8):
+    print(f"e={e}: " + " ".join(f"{(d[:, k, e:e + 1] - t0).median().item():12.0f}" for k in range(8)))

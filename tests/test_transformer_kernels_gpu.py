@@ -37,7 +37,10 @@ def ref_attention(qkv, b, s, nh, causal):
                                            (3, 512, 2, False), (2, 1024, 3, True), (1, 2048, 2, False),
                                            # more work items than SMs: the persistent backward's
                                            # cross-item pipeline (K/V ring, dK/dV hand-off)
-                                           (16, 512, 12, False), (8, 384, 12, True)])
+                                           (16, 512, 12, False), (8, 384, 12, True),
+                                           # one unit (the second slot idle), an odd unit count,
+                                           # and the GPT-2.2B step's shape (30 heads, causal)
+                                           (1, 128, 1, True), (1, 384, 1, False), (16, 512, 30, True)])
 def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
     """One tcgen05 implementation per pass, for every seq % 128 == 0 (no CUDA-core path)."""
     h = nh * 64
@@ -174,3 +177,31 @@ def test_layernorm_bwd_in_place():
     assert (dg - wr.grad).abs().max().item() < 1e-2 * max(1.0, wr.grad.abs().max().item())
     assert (db - br.grad).abs().max().item() < 1e-2 * max(1.0, br.grad.abs().max().item())
     assert (ds - buf.float().sum(0)).abs().max().item() < 1e-3 * max(1.0, buf.float().sum(0).abs().max().item())
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_fwd_bit_stable_under_concurrent_load(causal):
+    """The persistent forward's warps of different TMEM lane quarters run unsynchronised
+    (only the four key-quarter warps of a row meet at the max exchange); under a
+    concurrent kernel on another stream they drift apart.  The kernel has no atomics, so
+    every repeat must reproduce the quiet run bit for bit (a barrier-phase race -- an
+    arrival for block g + 1 counted towards block g -- shows up here as garbage)."""
+    b, s, nh = 16, 512, 12
+    h = nh * 64
+    g = torch.Generator(device="cuda").manual_seed(11)
+    qkv = (torch.randn(b * s, 3 * h, device="cuda", generator=g) * 0.8).to(torch.bfloat16)
+    o0 = torch.empty(b * s, h, device="cuda", dtype=torch.bfloat16)
+    l0 = torch.empty(b * nh * s, device="cuda", dtype=torch.float32)
+    call("p2bw_kernel_attention_fwd", ptr(qkv), ptr(o0), ptr(l0), b, s, nh, int(causal), stream())
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    x = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    for _ in range(10):
+        o = torch.empty_like(o0)
+        lse = torch.empty_like(l0)
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                y = x @ x  # noqa: F841 -- contention only
+        call("p2bw_kernel_attention_fwd", ptr(qkv), ptr(o), ptr(lse), b, s, nh, int(causal), stream())
+        torch.cuda.synchronize()
+        assert torch.equal(o, o0) and torch.equal(lse, l0)
