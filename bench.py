@@ -258,10 +258,16 @@ def run_ours(args, c):
     from paper_2006_09503_b200 import synthetic as S
 
     rank, world, local = dist_env()
+    ngpu = torch.cuda.device_count()
+    shared = world > ngpu  # more ranks than GPUs: ranks share devices (a plumbing check, not a scaling number)
+    local = local % ngpu
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:  # NCCL refuses two ranks on one device; the engine's data path does not use it
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2006_09503_b200 import dist as D
 
     depth = args.depth or (c["depth"] if world == 1 else 1)
@@ -285,8 +291,9 @@ def run_ours(args, c):
     has_loss = eng.is_local(depth - 1)
     if pipelined:
         D.connect_pipeline(eng, depth)
-    if width > 1:
-        D.join_replicas(eng, depth, pipelined=pipelined)  # NCCL per stage over its w replicas
+    transport = None
+    if width > 1:  # one node: fused all-reduce + update over CUDA-IPC peer memory; else NCCL
+        transport = D.join_replicas(eng, depth, pipelined=pipelined)
 
     # synthetic token batches in pinned host memory (one batch = m microbatches)
     T, R = c["b"] * c["seq"], c["b"] * (c["head_rows"] or c["seq"])
@@ -417,7 +424,9 @@ def run_ours(args, c):
     if pipelined:
         par += " (one stage per process, CUDA-IPC stage hand-offs over NVLink)"
     if width > 1:
-        par += " (NCCL all-reduce of the coalesced gradient at each AllReduce op)"
+        par += (" (AllReduce fused into WeightUpdate: reduce-scatter + optimizer + all-gather of the new version "
+                "over CUDA-IPC peer memory, one kernel per replica)" if transport == "ipc" else
+                " (NCCL all-reduce of the coalesced gradient at each AllReduce op)")
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -458,6 +467,8 @@ def run_ours(args, c):
         "cpu_baseline": cpu, "same_config": same, "clocks": clk,
         "loss_first_last": [float(losses[0]), float(losses[-1])] if has_loss else None,
     }
+    if shared:
+        line["shared_gpus"] = f"{world} ranks on {ngpu} GPU(s): a plumbing check, not a scaling measurement"
     print(json.dumps(line), flush=True)
     return 0
 

@@ -213,6 +213,18 @@ int p2bw_engine_update_elapsed_ms(p2bw_engine* eng, int stage, int u0, int u1, d
  * by count * w -- the replicas' average, as costmodel.cpp:23-27 prices it. */
 int p2bw_nccl_unique_id(void* out, size_t bytes);
 int p2bw_engine_join_replicas(p2bw_engine* eng, const void* ids, int nranks, int rank);
+/* Data-parallel replicas on one node without NCCL: every replica exports each local
+ * stage (p2bw_engine_export_replica), the blobs are exchanged (any transport), and each
+ * stage joins with the blobs of its w replicas in replica order.  The AllReduce op
+ * (schedule.cpp:80-84) is then fused into WeightUpdate: one kernel per replica sums its
+ * shard of every replica's coalesced gradient over CUDA-IPC peer memory (NVLink),
+ * applies the optimizer to that shard and stores the new version of the shard into
+ * every replica -- the update the reference prices as allreduce + apply
+ * (costmodel.cpp:23-27, semantics.cpp:335-350), divided by count * w.  Replicas may
+ * share a GPU (one process each).  nranks <= 8. */
+#define P2BW_REPLICA_BLOB_BYTES 1024
+int p2bw_engine_export_replica(p2bw_engine* eng, int stage, void* blob, size_t bytes);
+int p2bw_engine_join_replicas_ipc(p2bw_engine* eng, int stage, const void* blobs, int nranks, int rank);
 /* Cross-process pipelines: the reference interprets all stages in one loop
  * (semantics.cpp:270-361); here each process interprets its own stages and the
  * hand-offs of out_act (:299) / grad_to_prev (:333) to a stage in another process

@@ -82,6 +82,8 @@ def _signatures():
         ("p2bw_engine_update_elapsed_ms", i, [vp, i, i, i, C.POINTER(C.c_double)]),
         ("p2bw_nccl_unique_id", i, [vp, sz]),
         ("p2bw_engine_join_replicas", i, [vp, vp, i, i]),
+        ("p2bw_engine_export_replica", i, [vp, i, vp, sz]),
+        ("p2bw_engine_join_replicas_ipc", i, [vp, i, vp, i, i]),
         ("p2bw_engine_is_local", i, [vp, i, C.POINTER(C.c_int)]),
         ("p2bw_engine_export_stage", i, [vp, i, vp, sz]),
         ("p2bw_engine_connect_stage", i, [vp, vp, sz]),

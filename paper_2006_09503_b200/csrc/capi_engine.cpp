@@ -279,6 +279,33 @@ int p2bw_engine_connect_stage(p2bw_engine* eng, const void* blob, size_t bytes) 
     });
 }
 
+int p2bw_engine_export_replica(p2bw_engine* eng, int stage, void* blob, size_t bytes) {
+    static_assert(sizeof(p2bw::ReplicaBlob) <= P2BW_REPLICA_BLOB_BYTES, "replica blob does not fit");
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (blob == nullptr || bytes != P2BW_REPLICA_BLOB_BYTES)
+            throw std::invalid_argument("replica blob buffer must be P2BW_REPLICA_BLOB_BYTES bytes");
+        const p2bw::ReplicaBlob b = e.export_replica(stage);
+        std::memset(blob, 0, bytes);
+        std::memcpy(blob, &b, sizeof(b));
+    });
+}
+
+int p2bw_engine_join_replicas_ipc(p2bw_engine* eng, int stage, const void* blobs, int nranks, int rank) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        check_stage(e, stage);
+        if (blobs == nullptr) throw std::invalid_argument("blobs is NULL");
+        if (nranks < 1 || nranks > p2bw::kMaxReplicas) throw std::invalid_argument("nranks must be in [1, 8]");
+        std::vector<p2bw::ReplicaBlob> v(static_cast<size_t>(nranks));
+        for (int q = 0; q < nranks; ++q)
+            std::memcpy(&v[static_cast<size_t>(q)], static_cast<const uint8_t*>(blobs) + q * P2BW_REPLICA_BLOB_BYTES,
+                        sizeof(p2bw::ReplicaBlob));
+        e.join_replicas_ipc(stage, v, rank);
+    });
+}
+
 int p2bw_engine_sync(p2bw_engine* eng) {
     return guarded([&] { eng_of(eng).sync(); });
 }

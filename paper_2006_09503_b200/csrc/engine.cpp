@@ -263,6 +263,109 @@ void Engine::connect_stage(const StageBlob& b) {
     st.connected = true;
 }
 
+ReplicaBlob Engine::export_replica(int s) {
+    Stage& st = local_stage(s);
+    DeviceGuard g(st.device);
+    ReplicaBlob b{};
+    static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(b.block_ipc), "IPC handle size");
+    b.magic = kReplicaBlobMagic;
+    b.stage = s;
+    b.weight_slots = st.weight_slots;
+    b.weight_bytes = st.model->weight_bytes_public();
+    cudaIpcMemHandle_t h;
+    check_cuda(cudaIpcGetMemHandle(&h, st.block), "cudaIpcGetMemHandle(block)");
+    std::memcpy(b.block_ipc, &h, sizeof(h));
+    b.flag_off = static_cast<uint64_t>(reinterpret_cast<const uint8_t*>(st.flags) -
+                                       static_cast<const uint8_t*>(st.block));
+    const std::vector<void*> bufs = st.model->replica_buffers();
+    if (bufs.empty()) throw Error("this stage model cannot join a peer-memory replica group");
+    if (bufs.size() > static_cast<size_t>(kMaxReplicaBufs)) throw Error("too many replica buffers");
+    b.nbuf = static_cast<int>(bufs.size());
+    for (size_t i = 0; i < bufs.size(); ++i) {
+        if (!bufs[i]) continue;
+        size_t off = 0;
+        void* base = allocation_base(bufs[i], &off);
+        check_cuda(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle(replica buffer)");
+        std::memcpy(b.buf_ipc[i], &h, sizeof(h));
+        b.buf_off[i] = off;
+        b.buf_present[i] = 1;
+    }
+    return b;
+}
+
+void Engine::join_replicas_ipc(int s, const std::vector<ReplicaBlob>& blobs, int rank) {
+    Stage& st = local_stage(s);
+    const int w = static_cast<int>(blobs.size());
+    if (w < 1 || w > kMaxReplicas || rank < 0 || rank >= w) throw Error("bad data-parallel rank / size");
+    if (st.comm || st.ipc_group) throw Error("stage already joined a replica group");
+    if (w == 1) return;  // AllReduce is a no-op (semantics.cpp:351-354)
+    DeviceGuard g(st.device);
+    const std::vector<void*> mine = st.model->replica_buffers();
+    std::map<std::string, void*> opened;  // one mapping per exported allocation
+    auto open = [&](const char* ipc) -> void* {
+        const std::string key(ipc, 64);
+        auto it = opened.find(key);
+        if (it != opened.end()) return it->second;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, ipc, sizeof(h));
+        void* p = nullptr;
+        check_cuda(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(replica)");
+        st.ipc_opened.push_back(p);
+        opened[key] = p;
+        return p;
+    };
+    st.peer_bufs.assign(static_cast<size_t>(w), {});
+    st.peer_flags.assign(static_cast<size_t>(w), nullptr);
+    for (int q = 0; q < w; ++q) {
+        const ReplicaBlob& b = blobs[static_cast<size_t>(q)];
+        if (b.magic != kReplicaBlobMagic || b.stage != s)
+            throw Error("replica blob " + std::to_string(q) + " is not stage " + std::to_string(s) + "'s");
+        if (b.weight_bytes != st.model->weight_bytes_public() || b.weight_slots != st.weight_slots ||
+            b.nbuf != static_cast<int>(mine.size()))
+            throw Error("replica " + std::to_string(q) + " of stage " + std::to_string(s) + " has a different shape");
+        if (q == rank) {
+            st.peer_bufs[static_cast<size_t>(q)] = mine;
+            continue;
+        }
+        std::vector<void*> v(static_cast<size_t>(b.nbuf), nullptr);
+        for (int i = 0; i < b.nbuf; ++i)
+            if (b.buf_present[i]) v[static_cast<size_t>(i)] = static_cast<uint8_t*>(open(b.buf_ipc[i])) + b.buf_off[i];
+        st.peer_bufs[static_cast<size_t>(q)] = std::move(v);
+        st.peer_flags[static_cast<size_t>(q)] =
+            reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(open(b.block_ipc)) + b.flag_off);
+    }
+    st.ipc_group = true;
+    st.replica_rank = rank;
+    st.replicas = w;
+}
+
+// WeightUpdate of a peer-memory replica group, on the update stream `us`:
+//   1. tell every peer this replica's gradient is complete (and its in-flight Forwards no
+//      longer read the destination slot the peers are about to write);
+//   2. wait until every peer said the same;
+//   3. the fused reduce-scatter + optimizer + all-gather kernel (this replica's shard);
+//   4. tell every peer, wait for every peer: all shards of the new version have landed
+//      here and nobody reads this replica's gradient buffer any more.
+// Flags are sequence numbers in each replica's own block (peers write them, the owner
+// waits with a stream memory op: no SM spins).
+void Engine::issue_update_replicas(Stage& st, int src_slot, int dst_slot, cudaStream_t us) {
+    const int w = st.replicas, r = st.replica_rank;
+    const uint32_t n = ++st.ar_seq;
+    std::vector<uint32_t*> ready, done;
+    for (int q = 0; q < w; ++q)
+        if (q != r) {
+            ready.push_back(st.peer_flags[static_cast<size_t>(q)] + kReplicaReady + r);
+            done.push_back(st.peer_flags[static_cast<size_t>(q)] + kReplicaDone + r);
+        }
+    stream_signal_many(ready.data(), static_cast<int>(ready.size()), n, us);
+    for (int q = 0; q < w; ++q)
+        if (q != r) stream_wait_geq(st.flags + kReplicaReady + q, n, us);
+    st.model->update_replicas(src_slot, dst_slot, st.grad_count * w, st.peer_bufs, r, us);
+    stream_signal_many(done.data(), static_cast<int>(done.size()), n, us);
+    for (int q = 0; q < w; ++q)
+        if (q != r) stream_wait_geq(st.flags + kReplicaDone + q, n, us);
+}
+
 void Engine::signal_remote(uint32_t* flag, uint32_t value, cudaStream_t s) { stream_signal(flag, value, s); }
 
 void Engine::wait_flag(const uint32_t* flag, uint32_t value, cudaStream_t s) {
@@ -295,6 +398,12 @@ void Engine::free_buffers() {
         st.model.reset();
         if (st.comm) nccl_comm_destroy(static_cast<ncclComm_t>(st.comm));
         st.comm = nullptr;
+        if (st.ustream) cudaStreamSynchronize(st.ustream);
+        for (void* p : st.ipc_opened) cudaIpcCloseMemHandle(p);
+        st.ipc_opened.clear();
+        st.peer_bufs.clear();
+        st.peer_flags.clear();
+        st.ipc_group = false;
         if (st.fstream) cudaStreamSynchronize(st.fstream), cudaStreamDestroy(st.fstream);
         st.fstream = nullptr;
         if (st.dstream) cudaStreamSynchronize(st.dstream), cudaStreamDestroy(st.dstream);
@@ -540,7 +649,8 @@ void Engine::issue_update(Stage& st) {
         wait_on(ev_->fwd[static_cast<size_t>(st.index)], st.last_fwd, us);
     // gradients are summed over grad_count microbatches (and over the replicas by
     // the AllReduce): divide by both (semantics.cpp:338-340; PAPER §3 "w replicas")
-    st.model->update(src_slot, dst_slot, st.grad_count * st.replicas, us);
+    if (st.ipc_group) issue_update_replicas(st, src_slot, dst_slot, us);
+    else st.model->update(src_slot, dst_slot, st.grad_count * st.replicas, us);
     st.updates_done += 1;
     st.version_slot[st.updates_done] = dst_slot;
     prune_versions(st);
@@ -621,7 +731,8 @@ void Engine::issue(int upto_batch) {
                     case P2BW_OP_BACKWARD: issue_backward(st, op); break;
                     case P2BW_OP_UPDATE: issue_update(st); break;
                     case P2BW_OP_ALLREDUCE:  // sum the coalesced gradient over the w replicas
-                        if (st.comm) {       // (w == 1: no-op, semantics.cpp:351-354)
+                        if (st.comm) {       // (w == 1: no-op, semantics.cpp:351-354; peer-memory
+                                             // groups reduce inside WeightUpdate)
                             void* buf = nullptr;
                             size_t n = 0;
                             int dt = 0;

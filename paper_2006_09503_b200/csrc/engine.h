@@ -69,6 +69,22 @@ struct StageBlob {
     uint64_t act_off, grad_off, flag_off;  // byte offsets inside the block
 };
 
+// One stage of one data-parallel replica, for the peer-memory replica group
+// (Engine::join_replicas_ipc): CUDA IPC handles of the stage's flag block and of the
+// buffers StageModel::replica_buffers() lists.
+constexpr int kMaxReplicaBufs = 12;
+struct ReplicaBlob {
+    uint32_t magic;
+    int32_t stage, nbuf, weight_slots;
+    uint64_t weight_bytes;  // public weight bytes of the stage (shape check)
+    char block_ipc[64];
+    uint64_t flag_off;
+    char buf_ipc[kMaxReplicaBufs][64];
+    uint64_t buf_off[kMaxReplicaBufs];
+    uint8_t buf_present[kMaxReplicaBufs];
+};
+constexpr uint32_t kReplicaBlobMagic = 0x42523250u;  // "P2RB"
+
 // One pipeline stage's model slice: parameters, version buffers, stash and the
 // kernels of the Forward / Backward / WeightUpdate ops.
 class StageModel {
@@ -119,6 +135,20 @@ public:
     // The coalesced gradient buffer (all-reduced across data-parallel replicas).
     // dtype: 0 = fp32, 1 = fp64.
     virtual void grad_buffer(void** ptr, size_t* count, int* dtype) = 0;
+    // Data-parallel replicas on one node (Engine::join_replicas_ipc, CUDA IPC): the
+    // buffers the fused AllReduce + WeightUpdate touches in every replica, in a fixed
+    // order: [0], [1] coalesced gradient buffers (null when single), [2] fp32 master
+    // (null when the versions are the master), [3 + i] weight slot i.
+    virtual std::vector<void*> replica_buffers() { return {}; }
+    // WeightUpdate with the AllReduce fused in (replica `rank` owns parameter shard
+    // `rank`): sum the shard of every replica's current gradient, update its optimizer
+    // state, store the new version of the shard into every replica.  peers[q] is
+    // replica q's replica_buffers() as mapped in this process (peers[rank]: local).
+    virtual void update_replicas(int src_slot, int dst_slot, int count, const std::vector<std::vector<void*>>& peers,
+                                 int rank, cudaStream_t s) {
+        (void)src_slot, (void)dst_slot, (void)count, (void)peers, (void)rank, (void)s;
+        throw Error("this stage model has no fused replica update");
+    }
     // Asynchronous D2H of fp32 losses into (pinned) host memory, stream-ordered.
     virtual void copy_losses_async(float* host, int first_mb, int count, cudaStream_t s) {
         (void)host, (void)first_mb, (void)count, (void)s;
@@ -215,10 +245,19 @@ public:
     // CUDA IPC hand-off between processes (one process per stage group).
     StageBlob export_stage(int s);
     void connect_stage(const StageBlob& blob);
+    // Data-parallel replicas of stage s on one node, one process each, without NCCL:
+    // blobs[q] = replica q's export_replica(s).  The AllReduce op then happens inside
+    // WeightUpdate: one fused kernel reduce-scatters the coalesced gradients over peer
+    // memory, applies the optimizer to this replica's shard and all-gathers the new
+    // version (StageModel::update_replicas), between two stream-ordered flag barriers.
+    ReplicaBlob export_replica(int s);
+    void join_replicas_ipc(int s, const std::vector<ReplicaBlob>& blobs, int rank);
 
 private:
     // Flags in a stage's receive block (seq numbers, monotonically increasing).
     enum Flag { kActReady = 0, kGradReady = 1, kNextBwd = 2, kPrevBwd = 3, kNumFlags = 4 };
+    // replica-group barriers: kReplicaReady + q / kReplicaDone + q written by replica q
+    static constexpr int kReplicaReady = 16, kReplicaDone = 32;
 
     struct Stage {
         int index = 0;
@@ -252,6 +291,13 @@ private:
         int updates_issued = 0;  // in the current run
         void* comm = nullptr;    // ncclComm_t over this stage's data-parallel replicas
         int replicas = 1;
+        // peer-memory replica group (join_replicas_ipc)
+        bool ipc_group = false;
+        int replica_rank = 0;
+        std::vector<std::vector<void*>> peer_bufs;  // [replica] -> replica_buffers() mapped here
+        std::vector<uint32_t*> peer_flags;          // [replica] -> its flag block (null for this one)
+        std::vector<void*> ipc_opened;              // bases to cudaIpcCloseMemHandle
+        uint32_t ar_seq = 0;                        // fused all-reduce updates so far (flag values)
         int version_base = 0;    // updates_done at begin()
         std::map<int, int> version_slot;  // live version -> weight slot
         std::map<int, int> stash_version; // in-flight microbatch -> version
@@ -278,6 +324,7 @@ private:
     void issue_forward(Stage& st, const OpRec& op);
     void issue_backward(Stage& st, const OpRec& op);
     void issue_update(Stage& st);
+    void issue_update_replicas(Stage& st, int src_slot, int dst_slot, cudaStream_t us);
     bool ready(const Stage& st, const OpRec& op) const;
     int resolve_version(const Stage& st, const OpRec& op) const;
     void prune_versions(Stage& st);

@@ -105,6 +105,28 @@ __global__ void k_update(const double* __restrict__ wsrc, double* __restrict__ w
     }
 }
 
+// Data-parallel replicas (Engine::join_replicas_ipc): the AllReduce fused into the
+// update.  This replica owns elements [lo, hi); gsum is the replicas' sum in replica
+// order, then k_update's arithmetic; the new weights go to every replica's dst slot.
+constexpr int kMaxRep = 8;
+struct F64Peers {
+    const double* g[kMaxRep];
+    double* wdst[kMaxRep];
+};
+__global__ void k_update_replicas(F64Peers p, int nrep, const double* __restrict__ wsrc, double* __restrict__ vel,
+                                  long lo, long hi, double count, double lr, double beta) {
+    for (long i = lo + blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < hi;
+         i += static_cast<long>(gridDim.x) * blockDim.x) {
+        double gs = p.g[0][i];
+        for (int q = 1; q < nrep; ++q) gs = __dadd_rn(gs, p.g[q][i]);
+        const double g = __ddiv_rn(gs, count);
+        const double v = __dadd_rn(__dmul_rn(beta, vel[i]), __dmul_rn(__dsub_rn(1.0, beta), g));
+        vel[i] = v;
+        const double w = __dadd_rn(wsrc[i], __dmul_rn(-lr, v));
+        for (int q = 0; q < nrep; ++q) p.wdst[q][i] = w;
+    }
+}
+
 class LinearF64Stage final : public StageModel {
 public:
     LinearF64Stage(const EngineConfig& cfg, int stage, int lo, int hi, int sslots, int wslots)
@@ -249,6 +271,28 @@ public:
         k_update<<<blocks_for(total), kThreads, 0, s>>>(wslot_ptr(src_slot, 0), wslot_ptr(dst_slot, 0), vel_,
                                                         gsum_, total, static_cast<double>(count), lr_, beta_);
         check_cuda(cudaGetLastError(), "linear update");
+    }
+
+    std::vector<void*> replica_buffers() override {
+        std::vector<void*> v{gsum_, nullptr, nullptr};
+        for (int i = 0; i < wslots_; ++i) v.push_back(wslot_ptr(i, 0));
+        return v;
+    }
+    void update_replicas(int src_slot, int dst_slot, int count, const std::vector<std::vector<void*>>& peers,
+                         int rank, cudaStream_t s) override {
+        if (loop_scaling_) count = 1;
+        const int w = static_cast<int>(peers.size());
+        if (w < 1 || w > kMaxRep) throw Error("replica update: bad width");
+        F64Peers p{};
+        for (int q = 0; q < w; ++q) {
+            p.g[q] = static_cast<const double*>(peers[q].at(0));
+            p.wdst[q] = static_cast<double*>(peers[q].at(3 + static_cast<size_t>(dst_slot)));
+        }
+        const long total = static_cast<long>(layers_ * mat_);
+        const long lo = total * rank / w, hi = total * (rank + 1) / w;
+        k_update_replicas<<<blocks_for(std::max(hi - lo, 1L)), kThreads, 0, s>>>(
+            p, w, wslot_ptr(src_slot, 0), vel_, lo, hi, static_cast<double>(count), lr_, beta_);
+        check_cuda(cudaGetLastError(), "linear update (replicas)");
     }
 
 private:

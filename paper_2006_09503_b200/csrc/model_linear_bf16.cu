@@ -175,6 +175,30 @@ public:
         *dtype = 0;
     }
 
+    std::vector<void*> replica_buffers() override {
+        std::vector<void*> v{grad_bufs_[0], grad_bufs_[1], master_};
+        for (bf16* w : wbf_) v.push_back(w);
+        return v;
+    }
+    void update_replicas(int src_slot, int dst_slot, int grad_count, const std::vector<std::vector<void*>>& peers,
+                         int rank, cudaStream_t s) override {
+        (void)src_slot;
+        ReplicaShard r;
+        r.w = static_cast<int>(peers.size());
+        r.rank = rank;
+        for (int q = 0; q < r.w && q < kMaxReplicas; ++q) {
+            r.grad[q] = static_cast<const float*>(peers[q].at(static_cast<size_t>(grad_cur_)));
+            r.master[q] = static_cast<float*>(peers[q].at(2));
+            r.version[q] = static_cast<bf16*>(peers[q].at(3 + static_cast<size_t>(dst_slot)));
+        }
+        sgd_momentum_update_replicas(r, vel_, nparam_, 1.0f / static_cast<float>(grad_count),
+                                     static_cast<float>(cfg_.lr), static_cast<float>(cfg_.momentum), s);
+        if (grad_bufs_[1]) {
+            grad_cur_ ^= 1;
+            grad_ = grad_bufs_[grad_cur_];
+        }
+    }
+
     // Public layout: fp64 column-major matrices of the stage's layers (like LinearF64Stage).
     void load_weights(int wslot, const void* host, size_t bytes) override {
         if (bytes != weight_bytes_public()) throw Error("load_weights: size mismatch");

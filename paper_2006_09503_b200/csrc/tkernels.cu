@@ -325,6 +325,107 @@ __global__ void k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
     }
 }
 
+// Wide rows (h > 1024): a row is spread over WPR warps, each lane holding VPL 8-column
+// vectors (vector k * 32 * WPR + warp * 32 + lane: coalesced), so a lane keeps 8 VPL
+// values in registers instead of the one-warp kernel's h / 32 (h 1920: 60 -> 16, ~170 ->
+// ~60 registers, four times the rows in flight).  The CTA's 8 warps work on 8 / WPR rows
+// at a time and grid-stride over the rows with the next row's vectors loaded before the
+// current row's two reductions (mean, then the centred variance -- exact two-pass, as the
+// one-warp kernel), combined across a row's warps through SMEM under a named barrier.
+template <int VPL, int WPR>
+__global__ void __launch_bounds__(256) k_ln_fwd_wide(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                     const bf16* __restrict__ b, bf16* __restrict__ y,
+                                                     float* __restrict__ mean, float* __restrict__ rstd, int rows,
+                                                     int h) {
+    constexpr int RPC = 8 / WPR;  // rows per CTA step
+    __shared__ float red[2][2][RPC][WPR];  // [parity][stat][row group][warp]
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = warp / WPR, wi = warp % WPR;
+    const int hv = h / 8;
+    const float inv_h = 1.0f / static_cast<float>(h);
+    int vi[VPL];
+    bool ok[VPL];
+    uint4 gp[VPL], bp[VPL], cur[VPL], nxt[VPL];
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+        vi[k] = k * 32 * WPR + wi * 32 + lane;
+        ok[k] = vi[k] < hv;
+        gp[k] = ok[k] ? *reinterpret_cast<const uint4*>(g + vi[k] * 8) : z4;
+        bp[k] = ok[k] ? *reinterpret_cast<const uint4*>(b + vi[k] * 8) : z4;
+    }
+    const int step = gridDim.x * RPC;
+    int r = blockIdx.x * RPC + grp;
+    auto load = [&](int rr, uint4 (&dst)[VPL]) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+            dst[k] = (rr < rows && ok[k]) ? *reinterpret_cast<const uint4*>(x + static_cast<size_t>(rr) * h + vi[k] * 8)
+                                          : z4;
+    };
+    load(r, cur);
+    for (int it = 0; r - grp < rows; r += step, ++it) {
+        load(r + step, nxt);  // the next row in flight during this row's reductions
+        float v[VPL][8];
+        float s1 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const uint32_t w[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float2 f = ptx::unpack_bf16x2(w[t]);
+                v[k][2 * t] = f.x;
+                v[k][2 * t + 1] = f.y;
+                s1 += f.x + f.y;
+            }
+        }
+        s1 = warp_sum(s1);
+        float(*sl)[RPC][WPR] = red[it & 1];
+        if (lane == 0) sl[0][grp][wi] = s1;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
+        float tot = 0.0f;
+#pragma unroll
+        for (int w = 0; w < WPR; ++w) tot += sl[0][grp][w];
+        const float mu = tot * inv_h;
+        float s2 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+            if (ok[k])
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s2 += (v[k][q] - mu) * (v[k][q] - mu);
+        s2 = warp_sum(s2);
+        if (lane == 0) sl[1][grp][wi] = s2;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
+        float var = 0.0f;
+#pragma unroll
+        for (int w = 0; w < WPR; ++w) var += sl[1][grp][w];
+        const float rs = rsqrtf(var * inv_h + 1e-5f);
+        if (r < rows) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                if (!ok[k]) continue;
+                const uint32_t gw[4] = {gp[k].x, gp[k].y, gp[k].z, gp[k].w};
+                const uint32_t bw[4] = {bp[k].x, bp[k].y, bp[k].z, bp[k].w};
+                float o[8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 gf = ptx::unpack_bf16x2(gw[t]), bf = ptx::unpack_bf16x2(bw[t]);
+                    o[2 * t] = (v[k][2 * t] - mu) * rs * gf.x + bf.x;
+                    o[2 * t + 1] = (v[k][2 * t + 1] - mu) * rs * gf.y + bf.y;
+                }
+                store8(y + static_cast<size_t>(r) * h + vi[k] * 8, o);
+            }
+            if (wi == 0 && lane == 0) {
+                mean[r] = mu;
+                rstd[r] = rs;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) cur[k] = nxt[k];
+    }
+}
+
 // Fused LayerNorm backward.  Row part:
 //   dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) (+ dres),  dxh = dy * g
 // Column part, accumulated in registers over the rows a thread visits and reduced
@@ -366,8 +467,16 @@ inline size_t ln_bwd_fixed_bytes(int h) {
 // ring depth: G * 3 rows * h * 2 B ~ 24 * 256 * 6 B = 36 KB per slot for every h
 // (G ~ 24 / ceil(h / 256)), so up to four slots fit beside the reduction buffer; the
 // depth barely matters (the per-row reduction chain, not memory latency, bounds it)
-constexpr int kLnRing = 2;  // measured 1 / 2 / 3 / 4 slots: 16.1 / 16.0 / 16.2 / 16.5 us (BERT-base)
-inline int ln_bwd_ring_depth(int) { return kLnRing; }
+// BERT-base (h 768, G 8 groups): 1 / 2 / 3 / 4 slots measured 16.1 / 16.0 / 16.2 / 16.5 us.
+// Wide rows leave few groups per CTA (h 1920: G 3), so the ring deepens until ~16 rows
+// per SM are in flight (Little's law at ~6.5 TB/s and ~1 us of latency: ~45 KB per SM).
+inline int ln_bwd_ring_depth(int h) {
+    const int G = ln_bwd_shape(h).G;
+    int ns = std::max(2, std::min(8, (16 + G - 1) / G));
+    const size_t per_slot = static_cast<size_t>(G) * (3ull * h * 2 + 8);
+    while (ns > 2 && ln_bwd_fixed_bytes(h) + ns * per_slot > 200u * 1024u) --ns;
+    return ns;
+}
 
 inline size_t ln_bwd_smem_bytes(int h) {
     const LnBwdShape sh = ln_bwd_shape(h);
@@ -389,8 +498,7 @@ template <bool kSum, int wpr, bool kRes>
 __global__ void __launch_bounds__(kLnBwdThreads, 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
-             bf16* dx, int rows, int h, int G, int fixed_bytes, float* __restrict__ part) {
-    constexpr int NS = kLnRing;
+             bf16* dx, int rows, int h, int G, int fixed_bytes, int NS, float* __restrict__ part) {
     extern __shared__ __align__(128) uint8_t ln_raw[];
     float* ln_smem = reinterpret_cast<float*>(ln_raw);
     ptx::pdl_trigger();
@@ -428,7 +536,6 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     }
     __syncthreads();
     if (leader)
-#pragma unroll
         for (int i = 0; i < NS; ++i) issue(r0 + i * stride, i);
     float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (act) load8(g + vi * 8, gv);
@@ -783,6 +890,60 @@ __global__ void k_adam(float4* __restrict__ w, float4* __restrict__ m1, float4* 
     }
 }
 
+// The AllReduce fused into the optimizer over peer memory (tkernels.h ReplicaShard).
+struct ShardArgs {
+    const float4* g[kMaxReplicas];
+    float4* w[kMaxReplicas];
+    uint2* out[kMaxReplicas];
+};
+
+template <bool kAdam>
+__global__ void k_opt_replicas(ShardArgs a, int nrep, int rank, float4* __restrict__ s1, float4* __restrict__ s2,
+                               size_t lo, size_t hi, float inv_count, float lr, float b1, float b2, float eps,
+                               float inv_c1, float inv_c2) {
+    for (size_t i = lo + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < hi;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        float4 gq[kMaxReplicas];
+#pragma unroll
+        for (int q = 0; q < kMaxReplicas; ++q)  // every replica's loads in flight together
+            if (q < nrep) gq[q] = a.g[q][i];
+        float4 gg = gq[0];
+#pragma unroll
+        for (int q = 1; q < kMaxReplicas; ++q)
+            if (q < nrep) gg.x += gq[q].x, gg.y += gq[q].y, gg.z += gq[q].z, gg.w += gq[q].w;
+        float4 ww = a.w[rank][i], m = s1[i];
+        float* mp = &m.x;
+        float* wp = &ww.x;
+        const float gv[4] = {gg.x * inv_count, gg.y * inv_count, gg.z * inv_count, gg.w * inv_count};
+        if constexpr (kAdam) {
+            float4 v = s2[i];
+            float* vp = &v.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                mp[e] = b1 * mp[e] + (1.0f - b1) * gv[e];
+                vp[e] = b2 * vp[e] + (1.0f - b2) * gv[e] * gv[e];
+                wp[e] -= lr * (mp[e] * inv_c1) / (sqrtf(vp[e] * inv_c2) + eps);
+            }
+            s2[i] = v;
+        } else {
+            const float damp = 1.0f - b1;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                mp[e] = b1 * mp[e] + damp * gv[e];
+                wp[e] -= lr * mp[e];
+            }
+        }
+        s1[i] = m;
+        const uint2 o = make_uint2(ptx::pack_bf16x2(ww.x, ww.y), ptx::pack_bf16x2(ww.z, ww.w));
+#pragma unroll
+        for (int q = 0; q < kMaxReplicas; ++q)
+            if (q < nrep) {
+                a.w[q][i] = ww;
+                a.out[q][i] = o;
+            }
+    }
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z += 0x9e3779b97f4a7c15ULL;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -860,6 +1021,19 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
     if (h % 8 != 0 || h > 2048) throw Error("layernorm: hidden must be a multiple of 8 and <= 2048");
     prof::Scope scope("layernorm_fwd", 0.0, 4.0 * rows * h + 8.0 * rows, 1, s);
     const int nv = (h / 8 + 31) / 32;
+    if (nv > 4) {  // h > 1024: a row over WPR warps of two vectors per lane
+        const int wpr = (h / 8 + 63) / 64;
+        const int rpc = wpr <= 2 ? 8 / 2 : (wpr <= 4 ? 2 : 1);
+        const int grid = std::max(1, std::min((rows + rpc - 1) / rpc, 148 * 8));
+        if (wpr <= 2)
+            launch_pdl(k_ln_fwd_wide<2, 2>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h);
+        else if (wpr <= 4)
+            launch_pdl(k_ln_fwd_wide<2, 4>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h);
+        else
+            launch_pdl(k_ln_fwd_wide<2, 8>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h);
+        check_cuda(cudaGetLastError(), "layernorm_fwd");
+        return;
+    }
     const int grid = (rows + 7) / 8;  // 8 warps x 1 row
     switch (nv) {
         case 1: launch_pdl(k_ln_fwd<1>, dim3(grid), dim3(256), 0, s, "k_ln_fwd", x, g, b, y, mean, rstd, rows, h); break;
@@ -883,7 +1057,7 @@ void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, c
             check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(ln bwd smem)");
         launch_pdl(kern, dim3(grid), dim3(kLnBwdThreads), smem, s, "k_ln_bwd", dy, x, mean, rstd, g, dres, dx, rows, h,
-                   sh.G, static_cast<int>(ln_bwd_fixed_bytes(h)), part);
+                   sh.G, static_cast<int>(ln_bwd_fixed_bytes(h)), ln_bwd_ring_depth(h), part);
     };
     switch (sh.wpr) {
         case 1: dres ? go(k_ln_bwd<kSum, 1, true>) : go(k_ln_bwd<kSum, 1, false>); break;
@@ -968,6 +1142,45 @@ void adam_update(float* master, float* m1, float* m2, const float* grad, bf16* o
                                                reinterpret_cast<uint2*>(out_bf16), n / 4, inv_count, lr, b1, b2, eps,
                                                inv_c1, inv_c2);
     check_cuda(cudaGetLastError(), "adam_update");
+}
+
+namespace {
+template <bool kAdam>
+void opt_replicas(const ReplicaShard& r, float* s1, float* s2, size_t n, float inv_count, float lr, float b1,
+                  float b2, float eps, float inv_c1, float inv_c2, cudaStream_t s) {
+    if (n % 4 != 0) throw Error("optimizer: parameter count must be a multiple of 4");
+    if (r.w < 1 || r.w > kMaxReplicas || r.rank < 0 || r.rank >= r.w)
+        throw Error("replica update: bad width / rank");
+    ShardArgs a{};
+    for (int q = 0; q < r.w; ++q) {
+        if (!r.grad[q] || !r.master[q] || !r.version[q]) throw Error("replica update: missing peer buffer");
+        a.g[q] = reinterpret_cast<const float4*>(r.grad[q]);
+        a.w[q] = reinterpret_cast<float4*>(r.master[q]);
+        a.out[q] = reinterpret_cast<uint2*>(r.version[q]);
+    }
+    const size_t n4 = n / 4;
+    const size_t lo = n4 * static_cast<size_t>(r.rank) / r.w, hi = n4 * static_cast<size_t>(r.rank + 1) / r.w;
+    // per shard parameter: w gradient reads, the local state (w, m[, v]) read + written,
+    // w fp32 master + w bf16 version stores
+    const double per = 4.0 * r.w + (kAdam ? 24.0 : 16.0) + 6.0 * r.w;
+    prof::Scope scope("optimizer", 0.0, per * 4.0 * static_cast<double>(hi - lo), 1, s);
+    k_opt_replicas<kAdam><<<grid_for(hi - lo, 256), 256, 0, s>>>(a, r.w, r.rank, reinterpret_cast<float4*>(s1),
+                                                                  reinterpret_cast<float4*>(s2), lo, hi, inv_count, lr,
+                                                                  b1, b2, eps, inv_c1, inv_c2);
+    check_cuda(cudaGetLastError(), "optimizer (replicas)");
+}
+}  // namespace
+
+void sgd_momentum_update_replicas(const ReplicaShard& r, float* vel, size_t n, float inv_count, float lr,
+                                  float beta, cudaStream_t s) {
+    opt_replicas<false>(r, vel, nullptr, n, inv_count, lr, beta, 0.0f, 0.0f, 1.0f, 1.0f, s);
+}
+
+void adam_update_replicas(const ReplicaShard& r, float* m1, float* m2, size_t n, float inv_count, float lr,
+                          float b1, float b2, float eps, int step, cudaStream_t s) {
+    const float inv_c1 = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(b1), step)));
+    const float inv_c2 = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(b2), step)));
+    opt_replicas<true>(r, m1, m2, n, inv_count, lr, b1, b2, eps, inv_c1, inv_c2, s);
 }
 
 void init_uniform(float* w, size_t n, uint64_t seed, uint64_t uid, float half_width, cudaStream_t s) {

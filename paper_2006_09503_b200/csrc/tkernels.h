@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "util.h"
 
 namespace p2bw {
 
@@ -66,6 +67,25 @@ void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float
 //   g = grad / count; v = beta v + (1-beta) g; w -= lr v; out_bf16 = bf16(w)
 void sgd_momentum_update(float* master, float* vel, const float* grad, bf16* out_bf16, size_t n,
                          float inv_count, float lr, float beta, cudaStream_t s);
+
+// Data-parallel replicas on one node (CUDA IPC; Engine::join_replicas_ipc): the
+// AllReduce op fused into the optimizer.  Replica `rank` of `w` owns parameter shard
+// [rank n / w, (rank + 1) n / w) (in 4-element vectors): it sums that shard of every
+// replica's coalesced gradient (peer loads over NVLink, replica order 0 .. w-1 -- one
+// writer per element, so every replica ends bit-identical), updates the shard's
+// optimizer state (local) and stores the new fp32 master and bf16 version of the shard
+// into every replica (peer stores): reduce-scatter, update and all-gather in one pass,
+// (w - 1) / w x (4 + 4 + 2) bytes per parameter over the links.
+struct ReplicaShard {
+    const float* grad[kMaxReplicas];
+    float* master[kMaxReplicas];
+    bf16* version[kMaxReplicas];
+    int w = 1, rank = 0;
+};
+void sgd_momentum_update_replicas(const ReplicaShard& r, float* vel, size_t n, float inv_count, float lr,
+                                  float beta, cudaStream_t s);
+void adam_update_replicas(const ReplicaShard& r, float* m1, float* m2, size_t n, float inv_count, float lr,
+                          float b1, float b2, float eps, int step, cudaStream_t s);
 
 // out[c] (=|+=) sum_{p < parts} part[p * n + c], fixed order (deterministic).
 void reduce_partials(const float* part, int parts, int n, float* out, bool overwrite, cudaStream_t s);

@@ -45,7 +45,48 @@ WaitValueFn wait_fn() {
     return fn;
 }
 
+struct FlagList {
+    uint32_t* f[8];
+};
+
+__global__ void k_signal_many(FlagList l, int n, uint32_t value) {
+    __threadfence_system();
+    if (static_cast<int>(threadIdx.x) < n)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(l.f[threadIdx.x]), "r"(value) : "memory");
+}
+
+using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
 }  // namespace
+
+void stream_signal_many(uint32_t* const* flags, int n, uint32_t value, cudaStream_t s) {
+    if (n <= 0) return;
+    if (n > 8) throw Error("stream_signal_many: at most 8 flags");
+    FlagList l{};
+    for (int i = 0; i < n; ++i) l.f[i] = flags[i];
+    k_signal_many<<<1, 32, 0, s>>>(l, n, value);
+    check_cuda(cudaGetLastError(), "k_signal_many launch");
+    prof::add_launches(1);
+}
+
+void* allocation_base(const void* p, size_t* offset) {
+    static AddrRangeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* q = nullptr;
+        cudaDriverEntryPointQueryResult r{};
+        check_cuda(cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &q, 12000, cudaEnableDefault, &r),
+                   "cudaGetDriverEntryPointByVersion(cuMemGetAddressRange)");
+        if (q == nullptr || r != cudaDriverEntryPointSuccess) throw Error("cuMemGetAddressRange is unavailable");
+        fn = reinterpret_cast<AddrRangeFn>(q);
+    });
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    const CUresult e = fn(&base, &size, reinterpret_cast<CUdeviceptr>(p));
+    if (e != CUDA_SUCCESS) throw Error("cuMemGetAddressRange failed: " + std::to_string(static_cast<int>(e)));
+    *offset = static_cast<size_t>(reinterpret_cast<CUdeviceptr>(p) - base);
+    return reinterpret_cast<void*>(base);
+}
 
 void stream_signal(uint32_t* flag, uint32_t value, cudaStream_t s) {
     k_signal<<<1, 1, 0, s>>>(flag, value);

@@ -10,6 +10,9 @@
 
 namespace p2bw {
 
+// Data-parallel replicas of one stage in a peer-memory group (Engine::join_replicas_ipc).
+constexpr int kMaxReplicas = 8;
+
 // Every failure inside libp2bw.so is a p2bw::Error; the C-ABI converts it to a
 // nonzero status plus p2bw_last_error() text (mirrors pipesim::Error, error.hpp:9-12).
 class Error : public std::runtime_error {

@@ -1,9 +1,11 @@
 """Multi-process plumbing for pipelines and data-parallel replicas.
 
 torch.distributed is only plumbing here: rendezvous, the exchange of NCCL
-unique ids and of CUDA-IPC stage blobs, and max-over-ranks timing.  The data
-path is the engine's: stage hand-offs over CUDA IPC (p2bw_engine_connect_stage)
-and the NCCL all-reduce at the AllReduce op (p2bw_engine_join_replicas).
+unique ids and of CUDA-IPC blobs, and max-over-ranks timing.  The data path is
+the engine's: stage hand-offs over CUDA IPC (p2bw_engine_connect_stage) and the
+replicas' gradient reduction -- on one node a fused reduce-scatter + optimizer +
+all-gather kernel over CUDA-IPC peer memory (p2bw_engine_join_replicas_ipc),
+across nodes the NCCL all-reduce at the AllReduce op (p2bw_engine_join_replicas).
 
 Rank layout (profile.cpp:99-101): gpu = stage * width + replica."""
 from __future__ import annotations
@@ -68,22 +70,58 @@ def _engine_join(engine, ids: bytes, width: int, replica: int) -> None:
     _lib.check(_lib.lib().p2bw_engine_join_replicas(engine.h, arr, width, replica))
 
 
+def one_node() -> bool:
+    """Every rank runs on this host (CUDA IPC reaches all of them)."""
+    import socket
+    names: list = [None] * dist.get_world_size()
+    dist.all_gather_object(names, socket.gethostname())
+    return len(set(names)) == 1
+
+
 def join_replicas(engine, depth: int, pipelined: bool = False, make_id: Callable[[], bytes] | None = None,
-                  join: Callable | None = None) -> None:
+                  join: Callable | None = None, transport: str = "auto") -> str:
     """Join this process's stages to their data-parallel replica groups.
 
     pipelined=False: every process runs a whole pipeline (width = world).
     pipelined=True: one stage per process laid out by :func:`grid`.
-    Every replica of every stage receives the same `depth` unique ids (one NCCL
-    communicator per stage, rank = replica index); make_id / join default to the
-    engine's (p2bw_nccl_unique_id / p2bw_engine_join_replicas)."""
+    transport: "ipc" -- peer-memory groups (one node; the AllReduce fused into the
+    update kernel); "nccl" -- every replica of every stage receives the same `depth`
+    unique ids (one NCCL communicator per stage, rank = replica index; make_id / join
+    default to the engine's p2bw_nccl_unique_id / p2bw_engine_join_replicas);
+    "auto" -- ipc when every rank is on this host.  Returns the transport used."""
     world, rank = dist.get_world_size(), dist.get_rank()
     if pipelined:
         _, replica, width = grid(world, rank, depth)
     else:
         replica, width = rank, world
+    if transport == "auto":
+        transport = "ipc" if (make_id is None and join is None and one_node()) else "nccl"
+    if transport == "ipc":
+        join_replicas_ipc(engine, depth, pipelined)
+        return "ipc"
     ids = share_unique_ids(depth, make_id or nccl_unique_id)
     (join or _engine_join)(engine, ids, width, replica)
+    return "nccl"
+
+
+def join_replicas_ipc(engine, depth: int, pipelined: bool = False) -> None:
+    """Peer-memory replica groups: each process exports its local stages
+    (p2bw_engine_export_replica); every stage joins with the blobs of its replicas in
+    replica order.  Collective over the default group."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if pipelined:
+        _, replica, width = grid(world, rank, depth)
+    else:
+        replica, width = rank, world
+    mine = {s: engine.export_replica(s) for s in range(depth) if engine.is_local(s)}
+    gathered: list = [None] * world
+    dist.all_gather_object(gathered, (replica, mine))
+    for s in mine:
+        group = {rep: blobs[s] for rep, blobs in gathered if s in blobs}
+        if sorted(group) != list(range(width)):
+            raise RuntimeError(f"stage {s}: replicas {sorted(group)} found, expected {width}")
+        engine.join_replicas_ipc(s, [group[q] for q in range(width)], replica)
+    dist.barrier()
 
 
 def connect_pipeline(engine, depth: int) -> None:

@@ -210,6 +210,7 @@ class Desc(C.Structure):
 
 
 STAGE_BLOB_BYTES = 128  # P2BW_STAGE_BLOB_BYTES
+REPLICA_BLOB_BYTES = 1024  # P2BW_REPLICA_BLOB_BYTES
 
 
 def profile_blocks(*, layers: int, hidden: int, heads: int, seq_len: int, vocab: int, causal: int = 0,
@@ -342,6 +343,20 @@ class Engine:
         buf = (C.c_char * STAGE_BLOB_BYTES)()
         _call("p2bw_engine_export_stage", self.h, stage, buf, C.c_size_t(STAGE_BLOB_BYTES))
         return bytes(buf)
+
+    def export_replica(self, stage: int) -> bytes:
+        """CUDA-IPC description of this replica's stage for a peer-memory replica group."""
+        buf = (C.c_char * REPLICA_BLOB_BYTES)()
+        _call("p2bw_engine_export_replica", self.h, stage, buf, C.c_size_t(REPLICA_BLOB_BYTES))
+        return bytes(buf)
+
+    def join_replicas_ipc(self, stage: int, blobs: list[bytes], rank: int):
+        """Stage `stage` joins the group of its len(blobs) replicas (blobs in replica order):
+        the AllReduce is then fused into WeightUpdate over peer memory (no NCCL)."""
+        if any(len(b) != REPLICA_BLOB_BYTES for b in blobs):
+            raise ValueError("replica blobs must be %d bytes" % REPLICA_BLOB_BYTES)
+        buf = (C.c_char * (REPLICA_BLOB_BYTES * len(blobs))).from_buffer_copy(b"".join(blobs))
+        _call("p2bw_engine_join_replicas_ipc", self.h, stage, buf, len(blobs), rank)
 
     def connect_stage(self, blob: bytes):
         if len(blob) != STAGE_BLOB_BYTES:

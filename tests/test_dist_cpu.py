@@ -172,3 +172,56 @@ def test_allreduce_average_equals_wide_microbatch_gloo():
     want = np.concatenate([x.flatten() for x in g_one])
     assert np.array_equal(out[0], out[1])
     assert np.allclose(out[0], want, rtol=1e-12, atol=1e-14)
+
+
+class _FakeReplicaEngine:
+    """Stands in for export_replica / join_replicas_ipc (no GPU)."""
+
+    def __init__(self, depth, local_stages, tag):
+        self.depth, self.local_stages, self.tag = depth, local_stages, tag
+        self.joined = {}
+
+    def is_local(self, s):
+        return s in self.local_stages
+
+    def export_replica(self, s):
+        return bytes([s, self.tag]) * 512
+
+    def join_replicas_ipc(self, s, blobs, rank):
+        self.joined[s] = ([b[1] for b in blobs], rank)
+
+
+def _ipc_group_worker(rank, world, port, depth, pipelined, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2006_09503_b200 import dist as D
+    local = [D.grid(world, rank, depth)[0]] if pipelined else list(range(depth))
+    eng = _FakeReplicaEngine(depth, local, tag=rank)
+    used = D.join_replicas(eng, depth, pipelined=pipelined, transport="ipc")
+    q.put((rank, used, eng.joined))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,depth,pipelined", [(2, 1, False), (4, 2, False), (4, 2, True), (4, 1, True)])
+def test_ipc_replica_groups_gloo(world, depth, pipelined):
+    """join_replicas(transport="ipc"): every local stage joins with the blobs of exactly
+    its replicas, in replica order, at rank = its replica index (pipelined: gpu = stage *
+    width + replica; data parallel: every process holds every stage, replica = rank)."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_group_worker, args=(r, world, port, depth, pipelined, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2006_09503_b200.dist import grid
+    for rank, used, joined in out:
+        assert used == "ipc"
+        if pipelined:
+            stage, replica, width = grid(world, rank, depth)
+            assert joined == {stage: ([stage * width + q for q in range(width)], replica)}
+        else:
+            assert joined == {s: (list(range(world)), rank) for s in range(depth)}

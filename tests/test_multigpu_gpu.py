@@ -80,7 +80,7 @@ def test_nccl_replicas_equal_wide_microbatch(tmp_path, precision, depth):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "_replica_worker.py"), "--out", str(tmp_path), "--depth", str(depth),
-           "--precision", precision]
+           "--precision", precision, "--transport", "nccl"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     got = [np.load(tmp_path / f"rank{i}.npz")["weights"] for i in range(2)]

@@ -74,7 +74,7 @@ def test_attention_rejects_untiled_sequence_length():
         call("p2bw_kernel_attention_fwd", ptr(qkv), ptr(o), ptr(lse), 2, 96, 2, 1, stream())
 
 
-@pytest.mark.parametrize("rows,h", [(300, 256), (1024, 768), (64, 1024), (33, 1920),
+@pytest.mark.parametrize("rows,h", [(300, 256), (1024, 768), (64, 1024), (33, 1920), (4099, 1920), (2500, 1280),
                                     (20000, 768), (5000, 2048), (9001, 256)])  # ring wrap-around
 @pytest.mark.parametrize("with_dsum", [False, True])
 def test_layernorm_fwd_bwd_vs_torch(rows, h, with_dsum):
