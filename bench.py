@@ -390,6 +390,13 @@ def run_ours(args, c):
     barrier()
     eng.close()
 
+    pipe = None
+    if world > 1 and not pipelined and not args.no_pipeline_leg:
+        try:
+            pipe = pipeline_leg(args, c, world, rank, local)
+        except Exception as e:  # noqa: BLE001 -- the data-parallel line stands on its own
+            pipe = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     if rank != 0:
         return 0
     tot_ms = sum(k["ms"] for k in classes) or 1.0
@@ -469,8 +476,86 @@ def run_ours(args, c):
     }
     if shared:
         line["shared_gpus"] = f"{world} ranks on {ngpu} GPU(s): a plumbing check, not a scaling measurement"
+    if pipe is not None:
+        line["pipeline"] = pipe
     print(json.dumps(line), flush=True)
     return 0
+
+
+def pipeline_leg(args, c, world: int, rank: int, local: int) -> dict:
+    """N > 1, data-parallel default run: the same workload ALSO as one pipeline of depth N
+    (one stage per process, width 1; CUDA-IPC stage hand-offs over NVLink) -- the
+    configs' stated pipelines (C2 d 4, C3 d 8) next to the planner's data-parallel choice.
+    Reports samples/s (update events, max over ranks), the per-stage bubble fraction of a
+    traced run (stage idle time inside the steady window: schedule bubble + exposed
+    hand-offs, simulator.cpp:311-329 on measured times), the bytes each boundary moves per
+    microbatch and a device-to-device copy of that size between two of this node's GPUs."""
+    import torch
+    from paper_2006_09503_b200 import dist as D
+    from paper_2006_09503_b200 import pipesim as P
+    from paper_2006_09503_b200 import synthetic as S
+
+    depth = world
+    if c["layers"] % depth:
+        return {"skipped": f"{c['layers']} layers do not split over {depth} stages"}
+    m = max(c["m"], depth)  # 2BW needs m >= d (schedule.cpp:153-156)
+    stage, _, _ = D.grid(world, rank, depth)
+    spec = S.TransformerSpec(layers=c["layers"], hidden=c["hidden"], heads=c["heads"], seq=c["seq"], vocab=c["vocab"],
+                             batch=c["b"], causal=c["causal"], head_rows=c["head_rows"])
+    eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
+                   microbatch_size=c["b"], layers=c["layers"], hidden=c["hidden"], heads=c["heads"],
+                   seq_len=c["seq"], vocab=c["vocab"], causal=int(c["causal"]), head_rows=c["head_rows"],
+                   learning_rate=1e-3, momentum=0.9, seed=1234, local_stages=(stage, 1))
+    try:
+        eng.init_weights()
+        D.connect_pipeline(eng, depth)
+        ids, tg = S.token_batch(spec, 2 * m, 99)
+        eng.set_data(ids, tg, 1, 2 * m)  # the ring (2 batches) stays resident
+        steps, warm = args.steps, args.warmup
+        total = warm + steps + 1
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        eng.begin(total)
+        eng.issue(total)
+        eng.finish()
+        eng.sync()
+        ms = D.max_over_ranks(eng.update_elapsed_ms(stage, warm, warm + steps))
+        value = c["b"] * m * steps / (ms / 1e3)
+        # one traced run: per-stage busy / idle inside the steady window
+        eng.set_trace(True)
+        eng.begin(4)
+        eng.issue(4)
+        eng.finish()
+        eng.sync()
+        rep = eng.trace_report()
+        bubble = D.max_over_ranks(float(rep.get("bubble_fraction", 0.0)))
+        torch.distributed.barrier()
+    finally:
+        eng.close()
+    boundary = c["b"] * c["seq"] * c["hidden"] * 2  # bf16 activation (and gradient) per microbatch
+    link = None
+    if rank == 0 and torch.cuda.device_count() > 1:  # one hand-off's bytes between two GPUs
+        a = torch.empty(boundary // 2, dtype=torch.bfloat16, device="cuda:0")
+        b = torch.empty_like(a, device="cuda:1")
+        for _ in range(3):
+            b.copy_(a)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 20 * 1e3
+        link = {"bytes": boundary, "us": round(us, 2), "gbs": round(boundary / us / 1e3, 1),
+                "peak_gbs_per_direction": 900.0}
+    return {"workload": f"{args.config} as one 2BW pipeline: depth {depth}, width 1, m {m}, b {c['b']}",
+            "value": round(value, 2), "unit": "samples/s", "ms_per_step": round(ms / steps, 3),
+            "stage_bubble_fraction_max": round(bubble, 4),
+            "boundary_bytes_per_microbatch_per_direction": boundary,
+            "handoff": "producer kernel -> local staging slot -> copy stream into the neighbour's ring (CUDA IPC) "
+                       "-> sequence flag (cuStreamWaitValue32 on the consumer's stream)",
+            "d2d_copy_of_one_boundary": link}
 
 
 class KernelClass(C.Structure):
@@ -492,6 +577,8 @@ def main():
                     help="WeightUpdate optimizer: the reference's momentum SGD (default) or Adam")
     ap.add_argument("--recompute", action="store_true",
                     help="activation recomputation (the planner's r flag): stash stage inputs only")
+    ap.add_argument("--no-pipeline-leg", action="store_true",
+                    help="N > 1: skip the depth-N pipeline measured beside the data-parallel line")
     ap.add_argument("--depth", type=int, default=0,
                     help="pipeline depth (default: the config's on 1 GPU, 1 = data parallel on N GPUs)")
     args = ap.parse_args()

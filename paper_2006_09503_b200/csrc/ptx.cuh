@@ -441,6 +441,15 @@ __device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsign
     return d;
 }
 
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// bf16x2 -> an fp32 pair (low half first): two integer ops, no conversion instruction
+__device__ __forceinline__ unsigned long long bf2_to_f2(uint32_t u) {
+    return f2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
 // Three-input max (one FMNMX3 on sm_100).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float d;
@@ -451,6 +460,11 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ uint32_t f2_to_bf2(unsigned long long v) {
+    const float2 f = f2_split(v);
+    return pack_bf16x2(f.x, f.y);
 }
 
 __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {

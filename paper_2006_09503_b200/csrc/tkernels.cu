@@ -347,14 +347,22 @@ __global__ void __launch_bounds__(256) k_ln_fwd_wide(const bf16* __restrict__ x,
     const float inv_h = 1.0f / static_cast<float>(h);
     int vi[VPL];
     bool ok[VPL];
-    uint4 gp[VPL], bp[VPL], cur[VPL], nxt[VPL];
+    // packed fp32 pairs (FFMA2 / FADD2 / FMUL2) throughout: half the FP instructions
+    unsigned long long g2[VPL][4], b2[VPL][4];
+    uint4 cur[VPL], nxt[VPL];
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
         vi[k] = k * 32 * WPR + wi * 32 + lane;
         ok[k] = vi[k] < hv;
-        gp[k] = ok[k] ? *reinterpret_cast<const uint4*>(g + vi[k] * 8) : z4;
-        bp[k] = ok[k] ? *reinterpret_cast<const uint4*>(b + vi[k] * 8) : z4;
+        const uint4 gp = ok[k] ? *reinterpret_cast<const uint4*>(g + vi[k] * 8) : z4;
+        const uint4 bp = ok[k] ? *reinterpret_cast<const uint4*>(b + vi[k] * 8) : z4;
+        const uint32_t gw[4] = {gp.x, gp.y, gp.z, gp.w}, bw[4] = {bp.x, bp.y, bp.z, bp.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            g2[k][t] = ptx::bf2_to_f2(gw[t]);
+            b2[k][t] = ptx::bf2_to_f2(bw[t]);
+        }
     }
     const int step = gridDim.x * RPC;
     int r = blockIdx.x * RPC + grp;
@@ -367,20 +375,19 @@ __global__ void __launch_bounds__(256) k_ln_fwd_wide(const bf16* __restrict__ x,
     load(r, cur);
     for (int it = 0; r - grp < rows; r += step, ++it) {
         load(r + step, nxt);  // the next row in flight during this row's reductions
-        float v[VPL][8];
-        float s1 = 0.0f;
+        unsigned long long v[VPL][4];
+        unsigned long long a1 = 0ull;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
             const uint32_t w[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                const float2 f = ptx::unpack_bf16x2(w[t]);
-                v[k][2 * t] = f.x;
-                v[k][2 * t + 1] = f.y;
-                s1 += f.x + f.y;
+                v[k][t] = ptx::bf2_to_f2(w[t]);
+                a1 = ptx::fadd2(a1, v[k][t]);
             }
         }
-        s1 = warp_sum(s1);
+        const float2 f1 = ptx::f2_split(a1);
+        const float s1 = warp_sum(f1.x + f1.y);
         float(*sl)[RPC][WPR] = red[it & 1];
         if (lane == 0) sl[0][grp][wi] = s1;
         asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
@@ -388,13 +395,18 @@ __global__ void __launch_bounds__(256) k_ln_fwd_wide(const bf16* __restrict__ x,
 #pragma unroll
         for (int w = 0; w < WPR; ++w) tot += sl[0][grp][w];
         const float mu = tot * inv_h;
-        float s2 = 0.0f;
+        const unsigned long long nmu2 = ptx::f2(-mu, -mu);
+        unsigned long long a2 = 0ull;
 #pragma unroll
         for (int k = 0; k < VPL; ++k)
             if (ok[k])
 #pragma unroll
-                for (int q = 0; q < 8; ++q) s2 += (v[k][q] - mu) * (v[k][q] - mu);
-        s2 = warp_sum(s2);
+                for (int t = 0; t < 4; ++t) {
+                    const unsigned long long d = ptx::fadd2(v[k][t], nmu2);
+                    a2 = ptx::ffma2(d, d, a2);
+                }
+        const float2 f2v = ptx::f2_split(a2);
+        const float s2 = warp_sum(f2v.x + f2v.y);
         if (lane == 0) sl[1][grp][wi] = s2;
         asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
         float var = 0.0f;
@@ -402,19 +414,17 @@ __global__ void __launch_bounds__(256) k_ln_fwd_wide(const bf16* __restrict__ x,
         for (int w = 0; w < WPR; ++w) var += sl[1][grp][w];
         const float rs = rsqrtf(var * inv_h + 1e-5f);
         if (r < rows) {
+            const unsigned long long rs2 = ptx::f2(rs, rs);
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 if (!ok[k]) continue;
-                const uint32_t gw[4] = {gp[k].x, gp[k].y, gp[k].z, gp[k].w};
-                const uint32_t bw[4] = {bp[k].x, bp[k].y, bp[k].z, bp[k].w};
-                float o[8];
+                uint32_t ow[4];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float2 gf = ptx::unpack_bf16x2(gw[t]), bf = ptx::unpack_bf16x2(bw[t]);
-                    o[2 * t] = (v[k][2 * t] - mu) * rs * gf.x + bf.x;
-                    o[2 * t + 1] = (v[k][2 * t + 1] - mu) * rs * gf.y + bf.y;
+                for (int t = 0; t < 4; ++t) {  // ((v - mu) rstd) g + b
+                    const unsigned long long xh = ptx::fmul2(ptx::fadd2(v[k][t], nmu2), rs2);
+                    ow[t] = ptx::f2_to_bf2(ptx::ffma2(xh, g2[k][t], b2[k][t]));
                 }
-                store8(y + static_cast<size_t>(r) * h + vi[k] * 8, o);
+                *reinterpret_cast<uint4*>(y + static_cast<size_t>(r) * h + vi[k] * 8) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
             }
             if (wi == 0 && lane == 0) {
                 mean[r] = mu;
@@ -537,9 +547,16 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     __syncthreads();
     if (leader)
         for (int i = 0; i < NS; ++i) issue(r0 + i * stride, i);
-    float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (act) load8(g + vi * 8, gv);
-    float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0}, as[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // the row math runs on packed fp32 pairs (FFMA2 / FADD2 / FMUL2): the kernel is issue-
+    // bound, so half the FP instructions per element is what moves it
+    unsigned long long g2[4] = {0ull, 0ull, 0ull, 0ull};
+    if (act) {
+        const uint4 gp = *reinterpret_cast<const uint4*>(g + vi * 8);
+        g2[0] = ptx::bf2_to_f2(gp.x), g2[1] = ptx::bf2_to_f2(gp.y), g2[2] = ptx::bf2_to_f2(gp.z),
+        g2[3] = ptx::bf2_to_f2(gp.w);
+    }
+    unsigned long long ag[4] = {0ull, 0ull, 0ull, 0ull}, ab[4] = {0ull, 0ull, 0ull, 0ull},
+                       as[4] = {0ull, 0ull, 0ull, 0ull};  // (0.0f, 0.0f) pairs
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
     int r = r0;
     float mu = 0.0f, rs = 0.0f;
@@ -563,29 +580,25 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
             dp = *reinterpret_cast<const uint4*>(src + row_bytes);
             if (has_res) rp = *reinterpret_cast<const uint4*>(src + 2 * row_bytes);
         }
-        float xh[8], dg[8];
-        float s1 = 0.0f, s2 = 0.0f;
+        unsigned long long xh[4], dg[4];
+        float s1, s2;
         {
             const uint32_t xw[4] = {xp.x, xp.y, xp.z, xp.w}, dw[4] = {dp.x, dp.y, dp.z, dp.w};
+            const unsigned long long rs2 = ptx::f2(rs, rs), sh2 = ptx::f2(-mu * rs, -mu * rs);
+            unsigned long long a1 = 0ull, a2 = 0ull;
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                const float2 xf = ptx::unpack_bf16x2(xw[t]), df = ptx::unpack_bf16x2(dw[t]);
-                xh[2 * t] = (xf.x - mu) * rs;
-                xh[2 * t + 1] = (xf.y - mu) * rs;
-                dg[2 * t] = df.x * gv[2 * t];
-                dg[2 * t + 1] = df.y * gv[2 * t + 1];
-                if (act) {  // column statistics (inactive lanes hold zero data anyway)
-                    ag[2 * t] = fmaf(df.x, xh[2 * t], ag[2 * t]);
-                    ag[2 * t + 1] = fmaf(df.y, xh[2 * t + 1], ag[2 * t + 1]);
-                    ab[2 * t] += df.x;
-                    ab[2 * t + 1] += df.y;
-                }
+                const unsigned long long x2 = ptx::bf2_to_f2(xw[t]), d2 = ptx::bf2_to_f2(dw[t]);
+                xh[t] = ptx::ffma2(x2, rs2, sh2);  // (x - mu) rstd
+                dg[t] = ptx::fmul2(d2, g2[t]);
+                ag[t] = ptx::ffma2(d2, xh[t], ag[t]);  // inactive lanes hold zero data
+                ab[t] = ptx::fadd2(ab[t], d2);
+                a1 = ptx::fadd2(a1, dg[t]);
+                a2 = ptx::ffma2(dg[t], xh[t], a2);
             }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                s1 += dg[q];
-                s2 += dg[q] * xh[q];
-            }
+            const float2 f1 = ptx::f2_split(a1), f2v = ptx::f2_split(a2);
+            s1 = f1.x + f1.y;
+            s2 = f2v.x + f2v.y;
         }
         s1 = warp_sum(s1);
         s2 = warp_sum(s2);
@@ -611,32 +624,20 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
             slot = 0;
             phase ^= 1;
         }
-        const float m1 = s1 * inv_h, m2 = s2 * inv_h;
         if (act) {
-            float o[8];
+            // dx = rstd (dg - m1 - xh m2) = dg rstd + xh (-rstd m2) + (-rstd m1)
+            const float c1 = -rs * s1 * inv_h, c2 = -rs * s2 * inv_h;
+            const unsigned long long rs2 = ptx::f2(rs, rs), c12 = ptx::f2(c1, c1), c22 = ptx::f2(c2, c2);
+            const uint32_t rw[4] = {rp.x, rp.y, rp.z, rp.w};
+            uint32_t ow[4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) o[q] = rs * (dg[q] - m1 - xh[q] * m2);
-            if (has_res) {
-                const uint32_t rw[4] = {rp.x, rp.y, rp.z, rp.w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float2 rf = ptx::unpack_bf16x2(rw[t]);
-                    o[2 * t] += rf.x;
-                    o[2 * t + 1] += rf.y;
-                }
+            for (int t = 0; t < 4; ++t) {
+                unsigned long long o = ptx::ffma2(xh[t], c22, ptx::ffma2(dg[t], rs2, c12));
+                if (has_res) o = ptx::fadd2(o, ptx::bf2_to_f2(rw[t]));
+                ow[t] = ptx::f2_to_bf2(o);
+                if constexpr (kSum) as[t] = ptx::fadd2(as[t], ptx::bf2_to_f2(ow[t]));  // what the next GEMM reads
             }
-            const uint4 packed = make_uint4(ptx::pack_bf16x2(o[0], o[1]), ptx::pack_bf16x2(o[2], o[3]),
-                                            ptx::pack_bf16x2(o[4], o[5]), ptx::pack_bf16x2(o[6], o[7]));
-            *reinterpret_cast<uint4*>(dx + static_cast<size_t>(r) * h + vi * 8) = packed;
-            if constexpr (kSum) {  // the bias gradient sums what the next GEMM reads: bf16(dx)
-                const uint32_t pw[4] = {packed.x, packed.y, packed.z, packed.w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float2 pf = ptx::unpack_bf16x2(pw[t]);
-                    as[2 * t] += pf.x;
-                    as[2 * t + 1] += pf.y;
-                }
-            }
+            *reinterpret_cast<uint4*>(dx + static_cast<size_t>(r) * h + vi * 8) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
         mu = nmu;
         rs = nrs;
@@ -646,8 +647,11 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
         __syncthreads();
         if (act) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                ln_smem[static_cast<size_t>(grp) * h + vi * 8 + q] = st == 0 ? ag[q] : (st == 1 ? ab[q] : as[q]);
+            for (int t = 0; t < 4; ++t) {
+                const float2 v = ptx::f2_split(st == 0 ? ag[t] : (st == 1 ? ab[t] : as[t]));
+                ln_smem[static_cast<size_t>(grp) * h + vi * 8 + 2 * t] = v.x;
+                ln_smem[static_cast<size_t>(grp) * h + vi * 8 + 2 * t + 1] = v.y;
+            }
         }
         __syncthreads();
         for (int c = threadIdx.x; c < h; c += blockDim.x) {
