@@ -482,6 +482,24 @@ def run_ours(args, c):
     return 0
 
 
+def flop_profile(c) -> str:
+    """The config's blocks as a reference profile document (profile.cpp:162-193) with
+    times proportional to their algorithmic FLOPs: block 0 also carries
+    the embedding, the last block the LM head and its loss -- what partition_balanced
+    needs to move layers off the last stage (the head of the GPT configs costs ~2 layers)."""
+    L, h, s, V = c["layers"], c["hidden"], c["seq"], c["vocab"]
+    layer = 3 * (24 * s * h * h + 4 * s * s * h * (0.5 if c["causal"] else 1.0))
+    head = 6 * (c["head_rows"] or s) * h * V
+    unit = 1e12  # "ms" per FLOP scale; only ratios matter
+    blocks = []
+    for i in range(L):
+        f = layer + (head if i == L - 1 else 0.0)
+        blocks.append({"fwd_ms": {str(c["b"]): f / 3 / unit}, "bwd_ms": {str(c["b"]): 2 * f / 3 / unit},
+                       "weight_bytes": 1.0, "act_total_bytes": {str(c["b"]): 1.0},
+                       "act_input_bytes": {str(c["b"]): 1.0}, "act_boundary_bytes": {str(c["b"]): 2.0}})
+    return json.dumps({"model": "flops", "blocks": blocks})
+
+
 def pipeline_leg(args, c, world: int, rank: int, local: int) -> dict:
     """N > 1, data-parallel default run: the same workload ALSO as one pipeline of depth N
     (one stage per process, width 1; CUDA-IPC stage hand-offs over NVLink) -- the
@@ -490,22 +508,39 @@ def pipeline_leg(args, c, world: int, rank: int, local: int) -> dict:
     traced run (stage idle time inside the steady window: schedule bubble + exposed
     hand-offs, simulator.cpp:311-329 on measured times), the bytes each boundary moves per
     microbatch and a device-to-device copy of that size between two of this node's GPUs."""
+    from paper_2006_09503_b200 import dist as D
+    from paper_2006_09503_b200 import pipesim as P
+
+    depth = world
+    if c["layers"] < depth:
+        return {"skipped": f"{c['layers']} layers cannot fill {depth} stages"}
+    m = max(c["m"], depth)  # 2BW needs m >= d (schedule.cpp:153-156)
+    stage, _, _ = D.grid(world, rank, depth)
+    out = {"workload": f"{args.config} as one 2BW pipeline: depth {depth}, width 1, m {m}, b {c['b']}",
+           "unit": "samples/s", "boundary_bytes_per_microbatch_per_direction": c["b"] * c["seq"] * c["hidden"] * 2,
+           "handoff": "producer kernel -> local staging slot -> copy stream into the neighbour's ring (CUDA IPC) "
+                      "-> sequence flag (cuStreamWaitValue32 on the consumer's stream)"}
+    split = P.stage_layers_from_bounds(P.partition_balanced(flop_profile(c), depth, c["b"]))
+    runs = ([("equal", None)] if c["layers"] % depth == 0 else []) + [("balanced", split)]
+    for name, layers in runs:
+        r = _pipeline_run(args, c, depth, m, stage, layers)
+        out[name] = dict(r, stage_layers=layers or [c["layers"] // depth] * depth)
+    out["value"] = max(out[name]["value"] for name, _ in runs)
+    out["d2d_copy_of_one_boundary"] = _link_probe(rank, out["boundary_bytes_per_microbatch_per_direction"])
+    return out
+
+
+def _pipeline_run(args, c, depth, m, stage, layers) -> dict:
     import torch
     from paper_2006_09503_b200 import dist as D
     from paper_2006_09503_b200 import pipesim as P
     from paper_2006_09503_b200 import synthetic as S
-
-    depth = world
-    if c["layers"] % depth:
-        return {"skipped": f"{c['layers']} layers do not split over {depth} stages"}
-    m = max(c["m"], depth)  # 2BW needs m >= d (schedule.cpp:153-156)
-    stage, _, _ = D.grid(world, rank, depth)
     spec = S.TransformerSpec(layers=c["layers"], hidden=c["hidden"], heads=c["heads"], seq=c["seq"], vocab=c["vocab"],
                              batch=c["b"], causal=c["causal"], head_rows=c["head_rows"])
     eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
                    microbatch_size=c["b"], layers=c["layers"], hidden=c["hidden"], heads=c["heads"],
                    seq_len=c["seq"], vocab=c["vocab"], causal=int(c["causal"]), head_rows=c["head_rows"],
-                   learning_rate=1e-3, momentum=0.9, seed=1234, local_stages=(stage, 1))
+                   learning_rate=1e-3, momentum=0.9, seed=1234, local_stages=(stage, 1), stage_layers=layers)
     try:
         eng.init_weights()
         D.connect_pipeline(eng, depth)
@@ -532,7 +567,13 @@ def pipeline_leg(args, c, world: int, rank: int, local: int) -> dict:
         torch.distributed.barrier()
     finally:
         eng.close()
-    boundary = c["b"] * c["seq"] * c["hidden"] * 2  # bf16 activation (and gradient) per microbatch
+    return {"value": round(value, 2), "ms_per_step": round(ms / steps, 3),
+            "stage_bubble_fraction_max": round(bubble, 4)}
+
+
+def _link_probe(rank: int, boundary: int):
+    """Device-to-device copy of one boundary tensor between two of this node's GPUs."""
+    import torch
     link = None
     if rank == 0 and torch.cuda.device_count() > 1:  # one hand-off's bytes between two GPUs
         a = torch.empty(boundary // 2, dtype=torch.bfloat16, device="cuda:0")
@@ -549,13 +590,7 @@ def pipeline_leg(args, c, world: int, rank: int, local: int) -> dict:
         us = e0.elapsed_time(e1) / 20 * 1e3
         link = {"bytes": boundary, "us": round(us, 2), "gbs": round(boundary / us / 1e3, 1),
                 "peak_gbs_per_direction": 900.0}
-    return {"workload": f"{args.config} as one 2BW pipeline: depth {depth}, width 1, m {m}, b {c['b']}",
-            "value": round(value, 2), "unit": "samples/s", "ms_per_step": round(ms / steps, 3),
-            "stage_bubble_fraction_max": round(bubble, 4),
-            "boundary_bytes_per_microbatch_per_direction": boundary,
-            "handoff": "producer kernel -> local staging slot -> copy stream into the neighbour's ring (CUDA IPC) "
-                       "-> sequence flag (cuStreamWaitValue32 on the consumer's stream)",
-            "d2d_copy_of_one_boundary": link}
+    return link
 
 
 class KernelClass(C.Structure):

@@ -113,6 +113,10 @@ int p2bw_plan(const char* model_json, const char* cluster_json, long long max_ba
  * {fwd_time, bwd_time, weight_bytes, act_total_bytes, act_input_bytes,
  *  act_output_bytes} in SI units (seconds, bytes), keys = microbatch sizes. */
 int p2bw_partition_equal(const char* model_json, int d, char** out_json);
+/* B200 extension: pipesim::partition_balanced (include/pipesim/profile.hpp) -- the d + 1
+ * block boundaries of the contiguous split minimising the slowest stage's fwd + bwd
+ * time at microbatch size b, as a JSON array. */
+int p2bw_partition_balanced(const char* model_json, int d, int b, char** out_json);
 
 /* ---- the stage executor: pipelined_execute (semantics.hpp:73-74) ---------- */
 
@@ -158,6 +162,13 @@ typedef struct {
      * accumulated and apply the sum (semantics.cpp:145); the two agree bit for bit only
      * when m is a power of two. */
     int loop_scaling;
+    /* Layers per stage (depth entries), or NULL for the reference's equal split
+     * (partition_equal, profile.cpp:104-131; requires layers % depth == 0).  A B200
+     * extension: p2bw_partition_balanced picks the split whose slowest stage is fastest,
+     * so the first / last stages, which also carry the embedding / LM head, get fewer
+     * layers.  Weights depend only on the global layer index, so a run is comparable
+     * across splits. */
+    const int* stage_layers;
 } p2bw_desc;
 
 enum { P2BW_OPT_MOMENTUM_SGD = 0, P2BW_OPT_ADAM = 1 };

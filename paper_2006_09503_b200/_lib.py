@@ -67,6 +67,7 @@ def _signatures():
         ("p2bw_policy_parse", i, [cp, pi]),
         ("p2bw_plan", i, [cp, cp, ll, i, i, pvp]),
         ("p2bw_partition_equal", i, [cp, i, pvp]),
+        ("p2bw_partition_balanced", i, [cp, i, i, pvp]),
         ("p2bw_engine_create", i, [vp, pvp]),
         ("p2bw_engine_destroy", None, [vp]),
         ("p2bw_engine_stage_weight_bytes", i, [vp, i, psz]),

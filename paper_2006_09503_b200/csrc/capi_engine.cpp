@@ -52,6 +52,7 @@ p2bw::EngineConfig config_from_desc(const p2bw_desc& dd) {
     c.recompute = d->recompute != 0;
     c.optimizer = d->optimizer;
     c.loop_scaling = d->loop_scaling != 0;
+    if (d->stage_layers != nullptr) c.stage_layers.assign(d->stage_layers, d->stage_layers + d->depth);
     if (c.loop_scaling && c.model_kind != P2BW_MODEL_LINEAR_F64)
         throw p2bw::Error("loop_scaling applies to the fp64 linear chain only");
     if (c.optimizer != P2BW_OPT_MOMENTUM_SGD && c.optimizer != P2BW_OPT_ADAM)

@@ -163,6 +163,15 @@ int p2bw_plan(const char* model_json, const char* cluster_json, long long max_ba
     });
 }
 
+int p2bw_partition_balanced(const char* model_json, int d, int b, char** out_json) {
+    return guarded([&] {
+        need(model_json, "model_json");
+        need(out_json, "out_json");
+        const auto bounds = pipesim::partition_balanced(pipesim::load_model_profile(model_json), d, b);
+        *out_json = dup_string(nlohmann::json(bounds).dump());
+    });
+}
+
 int p2bw_partition_equal(const char* model_json, int d, char** out_json) {
     return guarded([&] {
         need(model_json, "model_json");

@@ -53,9 +53,19 @@ int weight_slots_for(int policy, int depth) {
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     if (cfg_.depth < 1) throw Error("depth must be >= 1");
     if (cfg_.layers < 1) throw Error("layer count must be >= 1");
-    if (cfg_.layers % cfg_.depth != 0)
-        throw Error("block count " + std::to_string(cfg_.layers) + " not divisible by depth " +
-                    std::to_string(cfg_.depth));
+    if (cfg_.stage_layers.empty()) {
+        if (cfg_.layers % cfg_.depth != 0)
+            throw Error("block count " + std::to_string(cfg_.layers) + " not divisible by depth " +
+                        std::to_string(cfg_.depth));
+    } else {
+        int sum = 0;
+        for (int n : cfg_.stage_layers) {
+            if (n < 1) throw Error("every stage needs at least one layer");
+            sum += n;
+        }
+        if (static_cast<int>(cfg_.stage_layers.size()) != cfg_.depth || sum != cfg_.layers)
+            throw Error("stage_layers must hold depth entries summing to the layer count");
+    }
     if (cfg_.microbatches < 1) throw Error("m must be >= 1");
     if (cfg_.policy == P2BW_POLICY_2BW && cfg_.microbatches < cfg_.depth)
         throw Error("2bw requires m >= d (m=" + std::to_string(cfg_.microbatches) +
@@ -107,8 +117,13 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
             Stage& st = stages_[s];
             st.index = s;
             st.device = cfg_.devices[s];
-            st.lo = s * per;
-            st.hi = st.lo + per;
+            if (cfg_.stage_layers.empty()) {
+                st.lo = s * per;
+                st.hi = st.lo + per;
+            } else {
+                st.lo = s == 0 ? 0 : stages_[static_cast<size_t>(s) - 1].hi;
+                st.hi = st.lo + cfg_.stage_layers[static_cast<size_t>(s)];
+            }
             const int warm = std::min(cfg_.depth - s, cfg_.microbatches);
             int inflight;
             switch (cfg_.policy) {

@@ -57,6 +57,9 @@ struct EngineConfig {
     // fp64 linear chain: reference_loop's per-microbatch 1/m gradient scaling
     // (semantics.cpp:145) instead of pipelined_execute's sum / count (:338-340).
     bool loop_scaling = false;
+    // Layers per stage (B200 extension, e.g. from pipesim::partition_balanced); empty:
+    // the reference's equal split, which needs layers % depth == 0.
+    std::vector<int> stage_layers;
 };
 
 // Receive-side block of one stage, exported over CUDA IPC to its neighbours'

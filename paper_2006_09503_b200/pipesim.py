@@ -196,6 +196,18 @@ def partition_equal(model_json: str, d: int) -> list[dict]:
     return json.loads(_take_string(p))
 
 
+def partition_balanced(model_json: str, d: int, b: int) -> list[int]:
+    """B200 extension: the d + 1 block boundaries of the contiguous split whose slowest
+    stage (fwd + bwd at microbatch size b) is fastest (pipesim::partition_balanced)."""
+    p = C.c_void_p()
+    _call("p2bw_partition_balanced", model_json.encode(), d, b, C.byref(p))
+    return json.loads(_take_string(p))
+
+
+def stage_layers_from_bounds(bounds: list[int]) -> list[int]:
+    return [hi - lo for lo, hi in zip(bounds[:-1], bounds[1:])]
+
+
 # ---- the stage executor ---------------------------------------------------------------
 
 class Desc(C.Structure):
@@ -206,7 +218,7 @@ class Desc(C.Structure):
                 ("learning_rate", C.c_double), ("momentum", C.c_double), ("seed", C.c_ulonglong),
                 ("devices", C.POINTER(C.c_int)), ("first_local_stage", C.c_int), ("local_stages", C.c_int),
                 ("recompute", C.c_int), ("optimizer", C.c_int), ("beta2", C.c_double), ("eps", C.c_double),
-                ("loop_scaling", C.c_int)]
+                ("loop_scaling", C.c_int), ("stage_layers", C.POINTER(C.c_int))]
 
 
 STAGE_BLOB_BYTES = 128  # P2BW_STAGE_BLOB_BYTES
@@ -254,13 +266,15 @@ class Engine:
                  learning_rate: float = 0.0, momentum: float = 0.0, seed: int = 0,
                  devices: list[int] | None = None, local_stages: tuple[int, int] | None = None,
                  recompute: bool = False, optimizer: str = "sgd", beta2: float = 0.999, eps: float = 1e-8,
-                 loop_scaling: bool = False):
+                 loop_scaling: bool = False, stage_layers: list[int] | None = None):
         self._devs = (C.c_int * depth)(*devices) if devices else None
+        self._split = (C.c_int * depth)(*stage_layers) if stage_layers else None
         first, count = local_stages if local_stages is not None else (0, 0)
         d = Desc(model_kind, int(policy), depth, 1, microbatches, microbatch_size, layers, dim, hidden,
                  heads, seq_len, vocab, causal, head_rows, learning_rate, momentum, seed,
                  C.cast(self._devs, C.POINTER(C.c_int)) if self._devs else None, first, count, int(recompute),
-                 {"sgd": OPT_MOMENTUM_SGD, "adam": OPT_ADAM}[optimizer], beta2, eps, int(loop_scaling))
+                 {"sgd": OPT_MOMENTUM_SGD, "adam": OPT_ADAM}[optimizer], beta2, eps, int(loop_scaling),
+                 C.cast(self._split, C.POINTER(C.c_int)) if self._split else None)
         self.h = C.c_void_p()
         _call("p2bw_engine_create", C.byref(d), C.byref(self.h))
         self.depth = depth

@@ -18,8 +18,14 @@ Beside them: the closed-form pipeline bubble, the stage imbalance (slowest stage
 per-microbatch F + B over the mean) and the exposed time (steady batch time minus
 the slowest stage's m (F + B): flush bubble + transfers on the critical path).
 
+With --balanced, 2BW is replayed twice per (d, m): on partition_equal's split and on
+partition_balanced's (the B200 extension: the contiguous split whose slowest stage is
+fastest -- the last stage also carries the 51200-way LM head), to show what the
+imbalance term becomes.
+
   python scripts/c5_replay.py --profile out_profile.json      # on a GPU box
   python scripts/c5_replay.py profile.json [out.json]         # anywhere
+  python scripts/c5_replay.py --balanced profile.json [out.json]
 """
 import json
 import sys
@@ -106,13 +112,28 @@ def replay(programs, stages, policy, b, xfer_bps):
             "exposed_fraction": max(0.0, steady - compute_bound) / steady}
 
 
-def breakdown(prof: str, policy, d: int, m: int, b: int = B, T: int = T_BATCHES) -> dict:
+def stages_from_bounds(prof: str, bounds: list) -> list:
+    """partition_equal's stage records (seconds, bytes) for an arbitrary contiguous split."""
+    blocks = json.loads(prof)["blocks"]
+    out = []
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        st = {"fwd_time": {}, "bwd_time": {}, "act_output_bytes": {}}
+        tail = blocks[hi - 1]
+        for key in tail["fwd_ms"]:
+            st["fwd_time"][key] = sum(blocks[i]["fwd_ms"][key] for i in range(lo, hi)) * 1e-3
+            st["bwd_time"][key] = sum(blocks[i]["bwd_ms"][key] for i in range(lo, hi)) * 1e-3
+            st["act_output_bytes"][key] = tail["act_boundary_bytes"][key] - tail["act_input_bytes"][key]
+        out.append(st)
+    return out
+
+
+def breakdown(prof: str, policy, d: int, m: int, b: int = B, T: int = T_BATCHES, bounds=None) -> dict:
     """Steady batch time split into additive parts (all from the simulator's rules):
       ideal            m * mean_s(F_s + B_s)       -- perfectly balanced, no bubble, free links
       imbalance        m * max_s(F_s + B_s) - ideal -- the slowest stage sets the pace
       schedule bubble  steady(free links) - m * max_s(F_s + B_s)   -- fill / drain / flush
       exposed transfer steady(NVLink) - steady(free links)          -- hand-offs on the critical path"""
-    stages = P.partition_equal(prof, d)
+    stages = P.partition_equal(prof, d) if bounds is None else stages_from_bounds(prof, bounds)
     progs = P.generate_schedule(policy, d, m, T)
     link = replay(progs, stages, policy, b, NVLINK_BPS)
     free = replay(progs, stages, policy, b, 1e18)
@@ -135,6 +156,28 @@ def main():
             f.write(prof)
         return
     prof = open(args[0]).read()
+    if "--balanced" in sys.argv:
+        rows = []
+        pol = P.PipelinePolicy.TwoBW
+        for d in (2, 4, 8):
+            bal = P.partition_balanced(prof, d, B)
+            for m in (d, 2 * d):
+                for name, bounds in (("equal", None), ("balanced", bal)):
+                    bd = breakdown(prof, pol, d, m, bounds=bounds)
+                    st = bd["steady_batch_ms"]
+                    row = {"partition": name, "stage_layers": None if bounds is None else P.stage_layers_from_bounds(bounds),
+                           "d": d, "m": m, "b": B, "samples_per_s": round(bd["throughput"], 1),
+                           "steady_batch_ms": round(st, 3), "bubble_fraction": round(bd["bubble_fraction"], 4),
+                           "frac_imbalance": round(bd["imbalance_ms"] / st, 4),
+                           "frac_schedule_bubble": round(bd["schedule_bubble_ms"] / st, 4),
+                           "frac_exposed_transfer": round(bd["exposed_transfer_ms"] / st, 4)}
+                    rows.append(row)
+                    print(json.dumps(row))
+        if len(args) > 1:
+            with open(args[1], "w") as f:
+                json.dump({"workload": "gpt-24, b 4, 2BW on d B200s: partition_equal vs partition_balanced "
+                                       "(B200-measured blocks, simulator rules)", "rows": rows}, f, indent=1)
+        return
     pols = (P.PipelinePolicy.TwoBW, P.PipelinePolicy.GPipe, P.PipelinePolicy.PipeDreamFlush)
     rows = []
     for d in (2, 4, 8):

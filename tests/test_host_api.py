@@ -110,3 +110,37 @@ def test_partition_equal_matches_oracle_exactly():
             assert {int(k): v for k, v in g["act_output_bytes"].items()} == r.act_output
     with pytest.raises(P.PipesimError, match="does not divide"):
         P.partition_equal(mj, 5)
+
+
+def _profile_doc(times, b=4):
+    import json as _json
+    return _json.dumps({"model": "t", "blocks": [
+        {"fwd_ms": {str(b): t}, "bwd_ms": {str(b): 2 * t}, "weight_bytes": 1, "act_total_bytes": {str(b): 1},
+         "act_input_bytes": {str(b): 1}, "act_boundary_bytes": {str(b): 1}} for t in times]})
+
+
+def _brute_best(times, d):
+    import itertools
+    n = len(times)
+    best = None
+    for cuts in itertools.combinations(range(1, n), d - 1):
+        b = [0, *cuts, n]
+        worst = max(sum(times[lo:hi]) for lo, hi in zip(b[:-1], b[1:]))
+        best = worst if best is None else min(best, worst)
+    return best
+
+
+@pytest.mark.parametrize("times,d", [([1.0] * 8, 4), ([1.0] * 7 + [2.5], 4), ([1.3] + [1.0] * 22 + [2.5], 8),
+                                     ([0.5, 3.0, 1.0, 1.0, 0.2, 2.0, 1.0], 3), ([1.0] * 5, 5)])
+def test_partition_balanced_is_optimal(times, d):
+    """B200 extension beside partition_equal (profile.cpp:104-131): the split minimises the
+    slowest stage (checked by brute force), and uniform blocks give the equal split."""
+    bounds = P.partition_balanced(_profile_doc(times), d, 4)
+    assert bounds[0] == 0 and bounds[-1] == len(times) and len(bounds) == d + 1
+    assert all(hi > lo for lo, hi in zip(bounds[:-1], bounds[1:]))
+    worst = max(3 * sum(times[lo:hi]) for lo, hi in zip(bounds[:-1], bounds[1:]))
+    assert abs(worst - 3 * _brute_best(times, d)) < 1e-9
+    if len(set(times)) == 1 and len(times) % d == 0:
+        assert bounds == [i * len(times) // d for i in range(d + 1)]
+    with pytest.raises(Exception, match="exceeds block count"):
+        P.partition_balanced(_profile_doc(times), len(times) + 1, 4)

@@ -13,7 +13,12 @@ from paper_2006_09503_b200 import pipesim as P
 pytestmark = pytest.mark.gpu
 
 LOSS_RTOL = 1e-2      # per-microbatch loss, bf16 activations vs float64
-DELTA_RTOL = 6e-2     # ||dW_gpu - dW_ref|| / ||dW_ref|| over each stage's parameters
+# ||dW_gpu - dW_ref|| / ||dW_ref|| over each stage's parameters.  Measured on B200 (round 2,
+# profiles/r2_engine_parity_errors.txt): 0.006-0.008 at h 128-1024, 0.0104 at h 1920 with
+# the 51200-way head -- the bf16 rounding of activations and weight versions, which grows
+# slowly with the reduction lengths.  2e-2 keeps a ~2x margin over the worst case, and
+# 2BW's distance from vanilla SGD (the `gap` below, >= 0.11) stays >= 5x above it.
+DELTA_RTOL = 2e-2
 
 
 def make_engine(spec, depth, m, lr, beta, seed, policy=P.PipelinePolicy.TwoBW):
@@ -170,3 +175,47 @@ def test_transformer_1f1b_weight_stashing():
     assert 2 <= c.max_versions_held <= depth + 1
     # training makes progress: the last batch's mean loss is below the first batch's
     assert np.all(np.isfinite(losses)) and losses[-m:].mean() < losses[:m].mean(), losses
+
+
+@pytest.mark.parametrize("split", [[1, 3], [3, 1], [1, 1, 2], [2, 1, 1]])
+def test_unequal_stage_split_matches_one_stage(split):
+    """Stages of unequal layer counts (p2bw_desc.stage_layers, the B200 extension that
+    pipesim::partition_balanced feeds): the same layer math, so the 2BW run matches
+    the one-stage run within bf16 rounding and the delayed oracle within DELTA_RTOL."""
+    spec = TO.Spec(layers=4, hidden=128, heads=2, seq=128, vocab=500, batch=2, causal=True, head_rows=0)
+    m, T, lr, beta, seed = 3, 3, 0.5, 0.9, 4321
+    ids, tg = TO.synthetic_batch(spec, m * T, seed + 1)
+    out = {}
+    for name, depth, layers in [("one", 1, None), ("split", len(split), split)]:
+        eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
+                       microbatch_size=spec.batch, layers=spec.layers, hidden=spec.hidden, heads=spec.heads,
+                       seq_len=spec.seq, vocab=spec.vocab, causal=1, learning_rate=lr, momentum=beta, seed=seed,
+                       stage_layers=layers)
+        eng.init_weights()
+        w0 = np.concatenate([eng.read_master(s) for s in range(depth)])
+        eng.set_data(ids, tg, 1, m * T)
+        eng.run_schedule(T)
+        eng.sync()
+        out[name] = (w0, np.concatenate([eng.read_master(s) for s in range(depth)]), eng.losses(1, m * T))
+        eng.close()
+    (w0a, wa, la), (w0b, wb, lb) = out["one"], out["split"]
+    assert np.array_equal(w0a, w0b)  # weights depend on the global layer index only
+    err = np.linalg.norm((wb - w0b) - (wa - w0a)) / np.linalg.norm(wa - w0a)
+    assert err < 1e-2, err
+    assert np.allclose(la, lb, rtol=LOSS_RTOL)
+    params = TO.init_params(spec, seed)
+    traj, ref_losses = TO.train(params, spec, ids, tg, lr, beta, m, T, delayed=True)
+    ref = np.concatenate([TO.flatten_stage({k: v.numpy() for k, v in traj[-1].items()}, spec, 1, 0)])
+    w0r = TO.flatten_stage(params, spec, 1, 0)
+    assert np.linalg.norm((wb - w0b) - (ref - w0r)) / np.linalg.norm(ref - w0r) < DELTA_RTOL
+
+
+def test_stage_split_validation():
+    with pytest.raises(Exception, match="stage_layers"):
+        P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=2, microbatches=2,
+                 microbatch_size=2, layers=4, hidden=128, heads=2, seq_len=128, vocab=500, causal=1,
+                 stage_layers=[1, 2])
+    with pytest.raises(Exception, match="at least one layer"):
+        P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=2, microbatches=2,
+                 microbatch_size=2, layers=4, hidden=128, heads=2, seq_len=128, vocab=500, causal=1,
+                 stage_layers=[0, 4])
