@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "launch.h"
@@ -403,6 +404,271 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---- forward, two query tiles per work unit (thread = query row) --------------------
+//
+// A work unit is two 128-query tiles A and B of one (sequence, head) -- causal: tiles p
+// and nq-1-p (every unit then costs nq + 1 key blocks), else 2p and 2p+1 -- sharing
+// each K / V block.  Two softmax warpgroups, one per tile, one thread per query row
+// holding the whole 128-key row (no cross-warp max exchange), ping-pong with the
+// tensor pipe: while group A turns S_A(j) into P_A(j), the pipe runs PV_B(j-1) and
+// S_B(j); while group B works, PV_A(j) and S_A(j+1).  TMEM: S_A | S_B (P over their
+// first 64 columns) | O_A[2] | O_B[2] (double-buffered per unit, so a unit's epilogue
+// overlaps the next unit).  Since S_X(j) is issued after PV_X(j-1), its commit also
+// says O_X holds PV_X(j-1): a lazy rescale of O needs no extra wait.
+namespace f2 {
+constexpr int kThreads = 384;  // 0 TMA | 1 MMA | 2 TMEM alloc | 3 idle | 4-7 tile A | 8-11 tile B
+constexpr int kNS = 4;         // K / V stages
+constexpr int oQ = 0;          // [2 unit buffers][2 tiles]
+constexpr int oK = oQ + 4 * kTile, oV = oK + kNS * kTile, oBar = oV + kNS * kTile;
+constexpr int bQFull = 0, bQEmpty = 2, bKvFull = 4, bKvEmpty = 4 + kNS, bSFull = 4 + 2 * kNS, bPFull = bSFull + 2,
+              bOFull = bPFull + 2, bOEmpty = bOFull + 4, kNumBars = bOEmpty + 4;  // O*: [tile][buffer]
+constexpr int kSmem = oBar + kNumBars * 8 + 16 + 1024;
+constexpr uint32_t tOBase = 256;  // O_X[b] at 256 + 128 X + 64 b
+
+struct Unit {
+    int bh, i[2], n[2];  // query tile and key-block count per tile (n = 0: no tile)
+};
+
+__device__ __forceinline__ Unit unit_of(int u, int bhn, int nq, bool causal) {
+    Unit r;
+    const int npair = nq / 2;
+    if (u < bhn * npair) {
+        const int p = u / bhn;
+        r.bh = u % bhn;
+        r.i[0] = causal ? p : 2 * p;
+        r.i[1] = causal ? nq - 1 - p : 2 * p + 1;
+    } else {  // odd nq: the middle (causal) / last tile alone
+        r.bh = u - bhn * npair;
+        r.i[0] = causal ? npair : nq - 1;
+        r.i[1] = -1;
+    }
+    r.n[0] = causal ? r.i[0] + 1 : nq;
+    r.n[1] = r.i[1] < 0 ? 0 : (causal ? r.i[1] + 1 : nq);
+    return r;
+}
+}  // namespace f2
+
+template <bool kCausal>
+__global__ void __launch_bounds__(f2::kThreads, 1)
+    k_attn_fwd_tc2(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int seq,
+                   int heads, int bhn) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = ptx::smem_u32(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + f2::oBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + f2::kNumBars);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nq = seq / kT;
+    const int units = bhn * (nq / 2 + (nq & 1));
+    const int h = heads * kD;
+    const int G = static_cast<int>(gridDim.x);
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tm);
+        for (int i = 0; i < f2::kNumBars; ++i)
+            ptx::mbar_init(&bar[i], (i >= f2::bPFull && i < f2::bPFull + 2) || (i >= f2::bOEmpty && i < f2::bOEmpty + 4) ? 4 : 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        int uc = 0, kc = 0;
+        for (int u = blockIdx.x; u < units; u += G, ++uc) {
+            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
+            const int row0 = (un.bh / heads) * seq, hd = un.bh % heads;
+            const int qb = uc & 1;
+            ptx::mbar_wait(&bar[f2::bQEmpty + qb], ((uc >> 1) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(&bar[f2::bQFull + qb], (un.n[1] > 0 ? 2 : 1) * kTile);
+            for (int x = 0; x < 2; ++x)
+                if (un.n[x] > 0)
+                    ptx::tma_load_2d(smem + f2::oQ + (qb * 2 + x) * kTile, &tm, &bar[f2::bQFull + qb], hd * kD,
+                                     row0 + un.i[x] * kT);
+            const int nmax = max(un.n[0], un.n[1]);
+            for (int j = 0; j < nmax; ++j, ++kc) {
+                const int st = kc % f2::kNS;
+                ptx::mbar_wait(&bar[f2::bKvEmpty + st], ((kc / f2::kNS) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&bar[f2::bKvFull + st], 2 * kTile);
+                ptx::tma_load_2d(smem + f2::oK + st * kTile, &tm, &bar[f2::bKvFull + st], h + hd * kD, row0 + j * kT);
+                ptx::tma_load_2d(smem + f2::oV + st * kTile, &tm, &bar[f2::bKvFull + st], 2 * h + hd * kD, row0 + j * kT);
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t id_s = ptx::idesc_bf16(128, kT, false, false);
+        constexpr uint32_t id_pv = ptx::idesc_bf16(128, kD, false, true);
+        int uc = 0, kc = 0;
+        int pc[2] = {0, 0}, oc[2] = {0, 0};  // P handshakes seen, units finished, per tile
+        auto issue_s = [&](int x, uint32_t q_addr, int st) {
+            const uint32_t k_addr = sbase + f2::oK + st * kTile;
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk)
+                ptx::umma_bf16(tmem + 128 * x, ptx::sdesc_sw128(q_addr + kk * 32, 16, 1024),
+                               ptx::sdesc_sw128(k_addr + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+            ptx::umma_commit(&bar[f2::bSFull + x]);
+        };
+        for (int u = blockIdx.x; u < units; u += G, ++uc) {
+            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
+            const int qb = uc & 1;
+            const int nmax = max(un.n[0], un.n[1]);
+            const uint32_t aQ[2] = {sbase + f2::oQ + (qb * 2) * kTile, sbase + f2::oQ + (qb * 2 + 1) * kTile};
+            ptx::mbar_wait(&bar[f2::bQFull + qb], (uc >> 1) & 1);
+            ptx::mbar_wait(&bar[f2::bKvFull + kc % f2::kNS], (kc / f2::kNS) & 1);
+            ptx::tc_fence_after();
+            for (int x = 0; x < 2; ++x)
+                if (un.n[x] > 0) issue_s(x, aQ[x], kc % f2::kNS);
+            for (int j = 0; j < nmax; ++j) {
+                const int st = (kc + j) % f2::kNS, stn = (kc + j + 1) % f2::kNS;
+                if (j + 1 < nmax) ptx::mbar_wait(&bar[f2::bKvFull + stn], ((kc + j + 1) / f2::kNS) & 1);
+                for (int x = 0; x < 2; ++x) {
+                    if (j >= un.n[x]) continue;
+                    const int ob = oc[x] & 1;
+                    ptx::mbar_wait(&bar[f2::bPFull + x], pc[x] & 1);
+                    ++pc[x];
+                    if (j == 0 && oc[x] >= 2)  // this O buffer's previous unit has been read out
+                        ptx::mbar_wait(&bar[f2::bOEmpty + 2 * x + ob], ((oc[x] >> 1) + 1) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t v_addr = sbase + f2::oV + st * kTile;
+#pragma unroll
+                    for (int kk = 0; kk < kT / 16; ++kk)
+                        ptx::umma_bf16_ts(tmem + f2::tOBase + 128 * x + 64 * ob, tmem + 128 * x + kk * 8,
+                                          ptx::sdesc_sw128(v_addr + kk * 2048, 8192, 1024), id_pv,
+                                          (j | kk) != 0 ? 1u : 0u);
+                    if (j + 1 < un.n[x]) {
+                        issue_s(x, aQ[x], stn);  // S_X(j+1) over P_X(j): after PV_X(j) (in order)
+                    } else {
+                        ptx::umma_commit(&bar[f2::bOFull + 2 * x + ob]);
+                        ++oc[x];
+                    }
+                }
+                ptx::umma_commit(&bar[f2::bKvEmpty + st]);
+            }
+            ptx::umma_commit(&bar[f2::bQEmpty + qb]);
+            kc += nmax;
+        }
+    } else if (warp >= 4) {
+        // ---------------- softmax: warpgroup x, thread = query row ----------------
+        const int x = (warp - 4) >> 2, qw = warp & 3;
+        const int r = qw * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+        const uint32_t sb = tmem + lane_off + 128 * x;
+        const float sc = 0.125f * kLog2e;
+        const unsigned long long sc2 = ptx::f2(sc, sc);
+        int sc_seen = 0, oc = 0;
+        for (int u = blockIdx.x; u < units; u += G) {
+            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
+            const int n = un.n[x];
+            if (n == 0) continue;
+            const int ob = oc & 1;
+            const uint32_t ot = tmem + lane_off + f2::tOBase + 128 * x + 64 * ob;
+            float m = -INFINITY;
+            unsigned long long la = 0ull, lb = 0ull;
+            for (int j = 0; j < n; ++j) {
+                ptx::mbar_wait(&bar[f2::bSFull + x], sc_seen & 1);
+                ++sc_seen;
+                ptx::tc_fence_after();
+                const bool diag = kCausal && j == n - 1;
+                // pass 1: the row max over 128 keys (two 32-column loads in flight)
+                float bm = -INFINITY;
+#pragma unroll
+                for (int c2 = 0; c2 < 4; c2 += 2) {
+                    uint32_t v0[32], v1[32];
+                    const int md0 = chunk_mode(diag, c2, qw), md1 = chunk_mode(diag, c2 + 1, qw);
+                    if (md0 != kEmpty) ptx::tmem_ld_32x32b_x32(sb + 32 * c2, v0);
+                    if (md1 != kEmpty) ptx::tmem_ld_32x32b_x32(sb + 32 * (c2 + 1), v1);
+                    ptx::tmem_ld_wait();
+                    if (md0 == kPartial) mask_partial(v0, lane);
+                    if (md1 == kPartial) mask_partial(v1, lane);
+                    if (md0 != kEmpty) bm = fmaxf(bm, max32(v0));
+                    if (md1 != kEmpty) bm = fmaxf(bm, max32(v1));
+                }
+                bm *= sc;
+                const float m_new = bm > m + kRescale ? bm : m;  // lazy: only large increases move m
+                if (m_new != m) {
+                    const float f = m == -INFINITY ? 0.0f : ptx::ex2(m - m_new);
+                    la = ptx::ffma2(la, ptx::f2(f, f), 0ull);
+                    lb = ptx::ffma2(lb, ptx::f2(f, f), 0ull);
+                    if (j > 0) {  // O holds PV(j-1): S(j) was issued after it
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf) {
+                            uint32_t o[32];
+                            ptx::tmem_ld_32x32b_x32(ot + 32 * hf, o);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                            ptx::tmem_st_32x32b_x32(ot + 32 * hf, o);
+                        }
+                    }
+                    m = m_new;
+                }
+                const unsigned long long nm2 = ptx::f2(-m, -m);
+                // pass 2: P = exp2(S sc - m) -> bf16 over the first 64 columns (chunk c -> [16c, 16c+16),
+                // never ahead of the S columns still to be read)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int md = chunk_mode(diag, c, qw);
+                    uint32_t pk[16];
+                    if (md == kEmpty) {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) pk[q] = 0u;
+                    } else {
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(sb + 32 * c, v);
+                        ptx::tmem_ld_wait();
+                        if (md == kPartial) mask_partial(v, lane);
+                        exp_chunk_mode(v, md, sc2, nm2, la, lb, pk);
+                    }
+                    ptx::tmem_st_32x32b_x16(sb + 16 * c, pk);
+                }
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bar[f2::bPFull + x]);
+            }
+            // epilogue: O / l (bf16) and lse of query row i * 128 + r
+            ptx::mbar_wait(&bar[f2::bOFull + 2 * x + ob], (oc >> 1) & 1);
+            ptx::tc_fence_after();
+            uint32_t o0[32], o1[32];
+            ptx::tmem_ld_32x32b_x32(ot, o0);
+            ptx::tmem_ld_32x32b_x32(ot + 32, o1);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&bar[f2::bOEmpty + 2 * x + ob]);
+            const float2 lfa = ptx::f2_split(la), lfb = ptx::f2_split(lb);
+            const float l = (lfa.x + lfa.y) + (lfb.x + lfb.y);
+            const float inv = 1.0f / l;
+            const int i = un.i[x] * kT + r;
+            bf16* orow = out + static_cast<size_t>((un.bh / heads) * seq + i) * h + (un.bh % heads) * kD;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t* src = q < 2 ? o0 + 16 * q : o1 + 16 * (q - 2);
+                uint32_t w[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    w[e] = ptx::pack_bf16x2(__uint_as_float(src[2 * e]) * inv, __uint_as_float(src[2 * e + 1]) * inv);
+                *reinterpret_cast<uint4*>(orow + 16 * q) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(orow + 16 * q + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+            lse[static_cast<size_t>(un.bh) * seq + i] = (m + log2f(l)) / kLog2e;
+            ++oc;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
 // One attribute call per (instantiation, device).
 template <bool kCausal>
 void set_smem_once() {
@@ -428,6 +694,33 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
     const uint64_t rows = static_cast<uint64_t>(batch) * seq;
     const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * h, rows, 3ll * h, 64, kT);
     const int bhn = batch * heads;
+    static const bool two_tile = [] {
+        const char* e = std::getenv("P2BW_ATTN_FWD");
+        return e && e[0] == '2';
+    }();
+    if (two_tile) {
+        const int nq = seq / kT;
+        const int units = bhn * (nq / 2 + (nq & 1));
+        const int grid = std::max(1, std::min(num_sms(), units));
+        static std::atomic<uint32_t> done{0};
+        int dev = 0;
+        check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+        if (!(done.load() & (1u << (dev & 31)))) {
+            check_cuda(cudaFuncSetAttribute(k_attn_fwd_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            f2::kSmem), "cudaFuncSetAttribute(k_attn_fwd_tc2)");
+            check_cuda(cudaFuncSetAttribute(k_attn_fwd_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            f2::kSmem), "cudaFuncSetAttribute(k_attn_fwd_tc2)");
+            done.fetch_or(1u << (dev & 31));
+        }
+        if (causal)
+            launch_pdl(k_attn_fwd_tc2<true>, dim3(grid), dim3(f2::kThreads), f2::kSmem, s, "k_attn_fwd_tc", tm, o, lse,
+                       seq, heads, bhn);
+        else
+            launch_pdl(k_attn_fwd_tc2<false>, dim3(grid), dim3(f2::kThreads), f2::kSmem, s, "k_attn_fwd_tc", tm, o,
+                       lse, seq, heads, bhn);
+        check_cuda(cudaGetLastError(), "attention_fwd_tc");
+        return;
+    }
     const int units = bhn * (seq / kT);
     const int grid = std::max(1, std::min(num_sms(), units));
     if (causal) {
