@@ -406,10 +406,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---- forward, two query tiles per work unit (thread = query row) --------------------
 //
-// A work unit is two 128-query tiles A and B of one (sequence, head) -- causal: tiles p
-// and nq-1-p (every unit then costs nq + 1 key blocks), else 2p and 2p+1 -- sharing
-// each K / V block.  Two softmax warpgroups, one per tile, one thread per query row
-// holding the whole 128-key row (no cross-warp max exchange), ping-pong with the
+// A work unit is two 128-query tiles A and B.  Non-causal: tiles 2p and 2p+1 of one
+// (sequence, head), sharing each K / V block.  Causal: the same tile index i of two
+// (sequence, head) pairs, so both tiles see the same number of key blocks (i + 1) and
+// stay in lockstep (pairing tiles p and nq-1-p of one head instead left the longer one
+// running alone for most of its blocks: measured slower), each with its own K / V.
+// Units run longest first.  Two softmax warpgroups, one per tile, one thread per query
+// row holding the whole 128-key row (no cross-warp max exchange), ping-pong with the
 // tensor pipe: while group A turns S_A(j) into P_A(j), the pipe runs PV_B(j-1) and
 // S_B(j); while group B works, PV_A(j) and S_A(j+1).  TMEM: S_A | S_B (P over their
 // first 64 columns) | O_A[2] | O_B[2] (double-buffered per unit, so a unit's epilogue
@@ -417,33 +420,53 @@ __global__ void __launch_bounds__(kThreads, 1)
 // says O_X holds PV_X(j-1): a lazy rescale of O needs no extra wait.
 namespace f2 {
 constexpr int kThreads = 384;  // 0 TMA | 1 MMA | 2 TMEM alloc | 3 idle | 4-7 tile A | 8-11 tile B
-constexpr int kNS = 4;         // K / V stages
-constexpr int oQ = 0;          // [2 unit buffers][2 tiles]
-constexpr int oK = oQ + 4 * kTile, oV = oK + kNS * kTile, oBar = oV + kNS * kTile;
-constexpr int bQFull = 0, bQEmpty = 2, bKvFull = 4, bKvEmpty = 4 + kNS, bSFull = 4 + 2 * kNS, bPFull = bSFull + 2,
-              bOFull = bPFull + 2, bOEmpty = bOFull + 4, kNumBars = bOEmpty + 4;  // O*: [tile][buffer]
+constexpr int kKvBytes = 8 * kTile;  // the K / V ring: 4 stages of K + V (shared), 2 of K_A V_A K_B V_B
+constexpr int oQ = 0;                // [2 unit buffers][2 tiles]
+constexpr int oKv = oQ + 4 * kTile, oBar = oKv + kKvBytes;
+constexpr int kMaxNS = 4;
+constexpr int bQFull = 0, bQEmpty = 2, bKvFull = 4, bKvEmpty = 4 + kMaxNS, bSFull = 4 + 2 * kMaxNS,
+              bPFull = bSFull + 2, bOFull = bPFull + 2, bOEmpty = bOFull + 4, kNumBars = bOEmpty + 4;  // O*: [tile][buffer]
 constexpr int kSmem = oBar + kNumBars * 8 + 16 + 1024;
 constexpr uint32_t tOBase = 256;  // O_X[b] at 256 + 128 X + 64 b
 
 struct Unit {
-    int bh, i[2], n[2];  // query tile and key-block count per tile (n = 0: no tile)
+    int bh[2], i[2], n[2];  // (sequence, head), query tile and key-block count per tile (n = 0: no tile)
 };
 
-__device__ __forceinline__ Unit unit_of(int u, int bhn, int nq, bool causal) {
+// kSep (causal): tiles of two heads, same query tile index; else two tiles of one head
+template <bool kSep>
+__device__ __forceinline__ int num_units(int bhn, int nq) {
+    return kSep ? nq * ((bhn + 1) / 2) : bhn * (nq / 2 + (nq & 1));
+}
+
+template <bool kSep>
+__device__ __forceinline__ Unit unit_of(int u, int bhn, int nq) {
     Unit r;
+    if (kSep) {
+        const int hp = (bhn + 1) / 2;
+        const int i = nq - 1 - u / hp, pb = u % hp;  // longest (last query tile) first
+        r.bh[0] = 2 * pb;
+        r.bh[1] = 2 * pb + 1 < bhn ? 2 * pb + 1 : -1;
+        r.i[0] = r.i[1] = i;
+        r.n[0] = i + 1;
+        r.n[1] = r.bh[1] < 0 ? 0 : i + 1;
+        if (r.bh[1] < 0) r.i[1] = -1;
+        return r;
+    }
     const int npair = nq / 2;
     if (u < bhn * npair) {
         const int p = u / bhn;
-        r.bh = u % bhn;
-        r.i[0] = causal ? p : 2 * p;
-        r.i[1] = causal ? nq - 1 - p : 2 * p + 1;
-    } else {  // odd nq: the middle (causal) / last tile alone
-        r.bh = u - bhn * npair;
-        r.i[0] = causal ? npair : nq - 1;
+        r.bh[0] = r.bh[1] = u % bhn;
+        r.i[0] = 2 * p;
+        r.i[1] = 2 * p + 1;
+        r.n[0] = r.n[1] = nq;
+    } else {  // odd nq: the last tile alone
+        r.bh[0] = r.bh[1] = u - bhn * npair;
+        r.i[0] = nq - 1;
         r.i[1] = -1;
+        r.n[0] = nq;
+        r.n[1] = 0;
     }
-    r.n[0] = causal ? r.i[0] + 1 : nq;
-    r.n[1] = r.i[1] < 0 ? 0 : (causal ? r.i[1] + 1 : nq);
     return r;
 }
 }  // namespace f2
@@ -460,7 +483,10 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int nq = seq / kT;
-    const int units = bhn * (nq / 2 + (nq & 1));
+    constexpr bool kSep = kCausal;
+    constexpr int kNS = kSep ? 2 : 4;                      // K / V stages in the ring
+    constexpr int kStage = (kSep ? 4 : 2) * kTile;         // K_A V_A [K_B V_B]
+    const int units = f2::num_units<kSep>(bhn, nq);
     const int h = heads * kD;
     const int G = static_cast<int>(gridDim.x);
 
@@ -482,22 +508,26 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
         // ---------------- TMA producer ----------------
         int uc = 0, kc = 0;
         for (int u = blockIdx.x; u < units; u += G, ++uc) {
-            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
-            const int row0 = (un.bh / heads) * seq, hd = un.bh % heads;
+            const f2::Unit un = f2::unit_of<kSep>(u, bhn, nq);
             const int qb = uc & 1;
             ptx::mbar_wait(&bar[f2::bQEmpty + qb], ((uc >> 1) & 1) ^ 1);
             ptx::mbar_arrive_expect_tx(&bar[f2::bQFull + qb], (un.n[1] > 0 ? 2 : 1) * kTile);
             for (int x = 0; x < 2; ++x)
                 if (un.n[x] > 0)
-                    ptx::tma_load_2d(smem + f2::oQ + (qb * 2 + x) * kTile, &tm, &bar[f2::bQFull + qb], hd * kD,
-                                     row0 + un.i[x] * kT);
+                    ptx::tma_load_2d(smem + f2::oQ + (qb * 2 + x) * kTile, &tm, &bar[f2::bQFull + qb],
+                                     (un.bh[x] % heads) * kD, (un.bh[x] / heads) * seq + un.i[x] * kT);
             const int nmax = max(un.n[0], un.n[1]);
+            const int nkv = kSep && un.n[1] > 0 ? 2 : 1;  // K / V sets per block
             for (int j = 0; j < nmax; ++j, ++kc) {
-                const int st = kc % f2::kNS;
-                ptx::mbar_wait(&bar[f2::bKvEmpty + st], ((kc / f2::kNS) & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(&bar[f2::bKvFull + st], 2 * kTile);
-                ptx::tma_load_2d(smem + f2::oK + st * kTile, &tm, &bar[f2::bKvFull + st], h + hd * kD, row0 + j * kT);
-                ptx::tma_load_2d(smem + f2::oV + st * kTile, &tm, &bar[f2::bKvFull + st], 2 * h + hd * kD, row0 + j * kT);
+                const int st = kc % kNS;
+                ptx::mbar_wait(&bar[f2::bKvEmpty + st], ((kc / kNS) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&bar[f2::bKvFull + st], 2 * nkv * kTile);
+                for (int x = 0; x < nkv; ++x) {
+                    const int row0 = (un.bh[x] / heads) * seq, hd = un.bh[x] % heads;
+                    uint8_t* dst = smem + f2::oKv + st * kStage + 2 * x * kTile;
+                    ptx::tma_load_2d(dst, &tm, &bar[f2::bKvFull + st], h + hd * kD, row0 + j * kT);
+                    ptx::tma_load_2d(dst + kTile, &tm, &bar[f2::bKvFull + st], 2 * h + hd * kD, row0 + j * kT);
+                }
             }
         }
     } else if (warp == 1 && lane == 0) {
@@ -506,27 +536,41 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
         constexpr uint32_t id_pv = ptx::idesc_bf16(128, kD, false, true);
         int uc = 0, kc = 0;
         int pc[2] = {0, 0}, oc[2] = {0, 0};  // P handshakes seen, units finished, per tile
+        // K of tile x in stage st (own set when the tiles are of different heads)
+        auto kv_addr = [&](int x, int st) { return sbase + f2::oKv + st * kStage + (kSep ? 2 * x * kTile : 0); };
         auto issue_s = [&](int x, uint32_t q_addr, int st) {
-            const uint32_t k_addr = sbase + f2::oK + st * kTile;
+            const uint32_t k_addr = kv_addr(x, st);
 #pragma unroll
             for (int kk = 0; kk < kD / 16; ++kk)
                 ptx::umma_bf16(tmem + 128 * x, ptx::sdesc_sw128(q_addr + kk * 32, 16, 1024),
                                ptx::sdesc_sw128(k_addr + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
             ptx::umma_commit(&bar[f2::bSFull + x]);
         };
-        for (int u = blockIdx.x; u < units; u += G, ++uc) {
-            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
-            const int qb = uc & 1;
-            const int nmax = max(un.n[0], un.n[1]);
-            const uint32_t aQ[2] = {sbase + f2::oQ + (qb * 2) * kTile, sbase + f2::oQ + (qb * 2 + 1) * kTile};
-            ptx::mbar_wait(&bar[f2::bQFull + qb], (uc >> 1) & 1);
-            ptx::mbar_wait(&bar[f2::bKvFull + kc % f2::kNS], (kc / f2::kNS) & 1);
+        // The next unit's S_X(0) is issued right after PV_X of this unit's last block (its
+        // buffer then holds nothing live), not after the whole unit: the softmax group
+        // starts the next unit while the other group finishes this one.
+        bool next_ready = false;  // the next unit's Q and first K / V block have landed
+        auto wait_unit_inputs = [&](int ucn, int kcn) {
+            ptx::mbar_wait(&bar[f2::bQFull + (ucn & 1)], (ucn >> 1) & 1);
+            ptx::mbar_wait(&bar[f2::bKvFull + kcn % kNS], (kcn / kNS) & 1);
             ptx::tc_fence_after();
+        };
+        auto q_addr = [&](int ucn, int x) { return sbase + f2::oQ + ((ucn & 1) * 2 + x) * kTile; };
+        if (static_cast<int>(blockIdx.x) < units) {  // the first unit's S(0)
+            const f2::Unit un = f2::unit_of<kSep>(blockIdx.x, bhn, nq);
+            wait_unit_inputs(0, 0);
             for (int x = 0; x < 2; ++x)
-                if (un.n[x] > 0) issue_s(x, aQ[x], kc % f2::kNS);
+                if (un.n[x] > 0) issue_s(x, q_addr(0, x), 0);
+        }
+        for (int u = blockIdx.x; u < units; u += G, ++uc) {
+            const f2::Unit un = f2::unit_of<kSep>(u, bhn, nq);
+            const int nmax = max(un.n[0], un.n[1]);
+            const bool has_next = u + G < units;
+            const f2::Unit nx = has_next ? f2::unit_of<kSep>(u + G, bhn, nq) : un;
+            next_ready = false;
             for (int j = 0; j < nmax; ++j) {
-                const int st = (kc + j) % f2::kNS, stn = (kc + j + 1) % f2::kNS;
-                if (j + 1 < nmax) ptx::mbar_wait(&bar[f2::bKvFull + stn], ((kc + j + 1) / f2::kNS) & 1);
+                const int st = (kc + j) % kNS, stn = (kc + j + 1) % kNS;
+                if (j + 1 < nmax) ptx::mbar_wait(&bar[f2::bKvFull + stn], ((kc + j + 1) / kNS) & 1);
                 for (int x = 0; x < 2; ++x) {
                     if (j >= un.n[x]) continue;
                     const int ob = oc[x] & 1;
@@ -535,23 +579,35 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
                     if (j == 0 && oc[x] >= 2)  // this O buffer's previous unit has been read out
                         ptx::mbar_wait(&bar[f2::bOEmpty + 2 * x + ob], ((oc[x] >> 1) + 1) & 1);
                     ptx::tc_fence_after();
-                    const uint32_t v_addr = sbase + f2::oV + st * kTile;
+                    const uint32_t v_addr = kv_addr(x, st) + kTile;
 #pragma unroll
                     for (int kk = 0; kk < kT / 16; ++kk)
                         ptx::umma_bf16_ts(tmem + f2::tOBase + 128 * x + 64 * ob, tmem + 128 * x + kk * 8,
                                           ptx::sdesc_sw128(v_addr + kk * 2048, 8192, 1024), id_pv,
                                           (j | kk) != 0 ? 1u : 0u);
                     if (j + 1 < un.n[x]) {
-                        issue_s(x, aQ[x], stn);  // S_X(j+1) over P_X(j): after PV_X(j) (in order)
+                        issue_s(x, q_addr(uc, x), stn);  // S_X(j+1) over P_X(j): after PV_X(j) (in order)
                     } else {
                         ptx::umma_commit(&bar[f2::bOFull + 2 * x + ob]);
                         ++oc[x];
+                        if (has_next && nx.n[x] > 0) {  // the next unit's S_X(0)
+                            if (!next_ready) {
+                                wait_unit_inputs(uc + 1, kc + nmax);
+                                next_ready = true;
+                            }
+                            issue_s(x, q_addr(uc + 1, x), (kc + nmax) % kNS);
+                        }
                     }
                 }
                 ptx::umma_commit(&bar[f2::bKvEmpty + st]);
             }
-            ptx::umma_commit(&bar[f2::bQEmpty + qb]);
+            ptx::umma_commit(&bar[f2::bQEmpty + (uc & 1)]);
             kc += nmax;
+            if (has_next) {  // a tile the next unit has and this one did not: its S(0) now
+                if (!next_ready) wait_unit_inputs(uc + 1, kc);
+                for (int x = 0; x < 2; ++x)
+                    if (un.n[x] == 0 && nx.n[x] > 0) issue_s(x, q_addr(uc + 1, x), kc % kNS);
+            }
         }
     } else if (warp >= 4) {
         // ---------------- softmax: warpgroup x, thread = query row ----------------
@@ -562,8 +618,40 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
         const float sc = 0.125f * kLog2e;
         const unsigned long long sc2 = ptx::f2(sc, sc);
         int sc_seen = 0, oc = 0;
+        // epilogue of a finished unit (count pc, tile row i0, head bh, max m, row sum l):
+        // O / l (bf16) and lse; run after the next unit's first block (O is double-buffered)
+        auto epilogue = [&](int pcn, int i0, int bh, float pm, float pl) {
+            const int ob = pcn & 1;
+            const uint32_t ot = tmem + lane_off + f2::tOBase + 128 * x + 64 * ob;
+            ptx::mbar_wait(&bar[f2::bOFull + 2 * x + ob], (pcn >> 1) & 1);
+            ptx::tc_fence_after();
+            uint32_t o0[32], o1[32];
+            ptx::tmem_ld_32x32b_x32(ot, o0);
+            ptx::tmem_ld_32x32b_x32(ot + 32, o1);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&bar[f2::bOEmpty + 2 * x + ob]);
+            const float inv = 1.0f / pl;
+            const int i = i0 * kT + r;
+            bf16* orow = out + static_cast<size_t>((bh / heads) * seq + i) * h + (bh % heads) * kD;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t* src = q < 2 ? o0 + 16 * q : o1 + 16 * (q - 2);
+                uint32_t w[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    w[e] = ptx::pack_bf16x2(__uint_as_float(src[2 * e]) * inv, __uint_as_float(src[2 * e + 1]) * inv);
+                *reinterpret_cast<uint4*>(orow + 16 * q) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(orow + 16 * q + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+            lse[static_cast<size_t>(bh) * seq + i] = (pm + log2f(pl)) / kLog2e;
+        };
+        bool pending = false;
+        int p_i = 0, p_bh = 0;
+        float p_m = 0.0f, p_l = 0.0f;
         for (int u = blockIdx.x; u < units; u += G) {
-            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
+            const f2::Unit un = f2::unit_of<kSep>(u, bhn, nq);
             const int n = un.n[x];
             if (n == 0) continue;
             const int ob = oc & 1;
@@ -631,35 +719,20 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&bar[f2::bPFull + x]);
+                if (j == 0 && pending) {
+                    epilogue(oc - 1, p_i, p_bh, p_m, p_l);
+                    pending = false;
+                }
             }
-            // epilogue: O / l (bf16) and lse of query row i * 128 + r
-            ptx::mbar_wait(&bar[f2::bOFull + 2 * x + ob], (oc >> 1) & 1);
-            ptx::tc_fence_after();
-            uint32_t o0[32], o1[32];
-            ptx::tmem_ld_32x32b_x32(ot, o0);
-            ptx::tmem_ld_32x32b_x32(ot + 32, o1);
-            ptx::tmem_ld_wait();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&bar[f2::bOEmpty + 2 * x + ob]);
             const float2 lfa = ptx::f2_split(la), lfb = ptx::f2_split(lb);
-            const float l = (lfa.x + lfa.y) + (lfb.x + lfb.y);
-            const float inv = 1.0f / l;
-            const int i = un.i[x] * kT + r;
-            bf16* orow = out + static_cast<size_t>((un.bh / heads) * seq + i) * h + (un.bh % heads) * kD;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t* src = q < 2 ? o0 + 16 * q : o1 + 16 * (q - 2);
-                uint32_t w[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    w[e] = ptx::pack_bf16x2(__uint_as_float(src[2 * e]) * inv, __uint_as_float(src[2 * e + 1]) * inv);
-                *reinterpret_cast<uint4*>(orow + 16 * q) = make_uint4(w[0], w[1], w[2], w[3]);
-                *reinterpret_cast<uint4*>(orow + 16 * q + 8) = make_uint4(w[4], w[5], w[6], w[7]);
-            }
-            lse[static_cast<size_t>(un.bh) * seq + i] = (m + log2f(l)) / kLog2e;
+            pending = true;
+            p_i = un.i[x];
+            p_bh = un.bh[x];
+            p_m = m;
+            p_l = (lfa.x + lfa.y) + (lfb.x + lfb.y);
             ++oc;
         }
+        if (pending) epilogue(oc - 1, p_i, p_bh, p_m, p_l);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -694,13 +767,18 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
     const uint64_t rows = static_cast<uint64_t>(batch) * seq;
     const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * h, rows, 3ll * h, 64, kT);
     const int bhn = batch * heads;
-    static const bool two_tile = [] {
+    // Non-causal: the two-tile kernel (BERT-base 39 -> 30 us per call).  Causal: the
+    // key-quarter kernel, which stays faster on the causal units' short key ranges (GPT-2.2B
+    // 59 us against 63-66 us for the two-tile kernel with either pairing); P2BW_ATTN_FWD=1 / 2
+    // forces one of them (A/B measurements).
+    static const int forced = [] {
         const char* e = std::getenv("P2BW_ATTN_FWD");
-        return e && e[0] == '2';
+        return e ? std::atoi(e) : 0;
     }();
+    const bool two_tile = forced == 2 || (forced == 0 && !causal);
     if (two_tile) {
         const int nq = seq / kT;
-        const int units = bhn * (nq / 2 + (nq & 1));
+        const int units = causal ? nq * ((bhn + 1) / 2) : bhn * (nq / 2 + (nq & 1));
         const int grid = std::max(1, std::min(num_sms(), units));
         static std::atomic<uint32_t> done{0};
         int dev = 0;

@@ -40,7 +40,10 @@ def ref_attention(qkv, b, s, nh, causal):
                                            (16, 512, 12, False), (8, 384, 12, True),
                                            # one unit (the second slot idle), an odd unit count,
                                            # and the GPT-2.2B step's shape (30 heads, causal)
-                                           (1, 128, 1, True), (1, 384, 1, False), (16, 512, 30, True)])
+                                           (1, 128, 1, True), (1, 384, 1, False), (16, 512, 30, True),
+                                           # odd (sequence, head) counts: the forward pairs two heads per
+                                           # causal unit, so one unit runs a single tile; odd tile counts
+                                           (3, 256, 3, True), (5, 384, 1, True), (3, 384, 3, False)])
 def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
     """One tcgen05 implementation per pass, for every seq % 128 == 0 (no CUDA-core path)."""
     h = nh * 64
