@@ -406,12 +406,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---- forward, two query tiles per work unit (thread = query row) --------------------
 //
-// A work unit is two 128-query tiles A and B.  Non-causal: tiles 2p and 2p+1 of one
-// (sequence, head), sharing each K / V block.  Causal: the same tile index i of two
-// (sequence, head) pairs, so both tiles see the same number of key blocks (i + 1) and
-// stay in lockstep (pairing tiles p and nq-1-p of one head instead left the longer one
-// running alone for most of its blocks: measured slower), each with its own K / V.
-// Units run longest first.  Two softmax warpgroups, one per tile, one thread per query
+// A work unit is two 128-query tiles A and B, 2p and 2p + 1 of one (sequence, head),
+// sharing each K / V block (causal: tile B sees one more block; longest units first).
+// It runs the non-causal attention; causal attention stays on the key-quarter kernel
+// above (see attention_fwd_tc).  Two softmax warpgroups, one per tile, one thread per query
 // row holding the whole 128-key row (no cross-warp max exchange), ping-pong with the
 // tensor pipe: while group A turns S_A(j) into P_A(j), the pipe runs PV_B(j-1) and
 // S_B(j); while group B works, PV_A(j) and S_A(j+1).  TMEM: S_A | S_B (P over their
@@ -420,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // says O_X holds PV_X(j-1): a lazy rescale of O needs no extra wait.
 namespace f2 {
 constexpr int kThreads = 384;  // 0 TMA | 1 MMA | 2 TMEM alloc | 3 idle | 4-7 tile A | 8-11 tile B
-constexpr int kKvBytes = 8 * kTile;  // the K / V ring: 4 stages of K + V (shared), 2 of K_A V_A K_B V_B
+constexpr int kKvBytes = 8 * kTile;  // the K / V ring: 4 stages of K + V
 constexpr int oQ = 0;                // [2 unit buffers][2 tiles]
 constexpr int oKv = oQ + 4 * kTile, oBar = oKv + kKvBytes;
 constexpr int kMaxNS = 4;
@@ -433,40 +431,24 @@ struct Unit {
     int bh[2], i[2], n[2];  // (sequence, head), query tile and key-block count per tile (n = 0: no tile)
 };
 
-// kSep (causal): tiles of two heads, same query tile index; else two tiles of one head
-template <bool kSep>
-__device__ __forceinline__ int num_units(int bhn, int nq) {
-    return kSep ? nq * ((bhn + 1) / 2) : bhn * (nq / 2 + (nq & 1));
-}
+__device__ __forceinline__ int num_units(int bhn, int nq) { return bhn * (nq / 2 + (nq & 1)); }
 
-template <bool kSep>
-__device__ __forceinline__ Unit unit_of(int u, int bhn, int nq) {
+// tiles 2p and 2p + 1 of one (sequence, head); causal: longest pairs first
+__device__ __forceinline__ Unit unit_of(int u, int bhn, int nq, bool causal) {
     Unit r;
-    if (kSep) {
-        const int hp = (bhn + 1) / 2;
-        const int i = nq - 1 - u / hp, pb = u % hp;  // longest (last query tile) first
-        r.bh[0] = 2 * pb;
-        r.bh[1] = 2 * pb + 1 < bhn ? 2 * pb + 1 : -1;
-        r.i[0] = r.i[1] = i;
-        r.n[0] = i + 1;
-        r.n[1] = r.bh[1] < 0 ? 0 : i + 1;
-        if (r.bh[1] < 0) r.i[1] = -1;
-        return r;
-    }
     const int npair = nq / 2;
     if (u < bhn * npair) {
-        const int p = u / bhn;
+        const int p = causal ? npair - 1 - u / bhn : u / bhn;  // causal: longest pairs first
         r.bh[0] = r.bh[1] = u % bhn;
         r.i[0] = 2 * p;
         r.i[1] = 2 * p + 1;
-        r.n[0] = r.n[1] = nq;
     } else {  // odd nq: the last tile alone
         r.bh[0] = r.bh[1] = u - bhn * npair;
         r.i[0] = nq - 1;
         r.i[1] = -1;
-        r.n[0] = nq;
-        r.n[1] = 0;
     }
+    r.n[0] = causal ? r.i[0] + 1 : nq;
+    r.n[1] = r.i[1] < 0 ? 0 : (causal ? r.i[1] + 1 : nq);
     return r;
 }
 }  // namespace f2
@@ -483,10 +465,9 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int nq = seq / kT;
-    constexpr bool kSep = kCausal;
-    constexpr int kNS = kSep ? 2 : 4;                      // K / V stages in the ring
-    constexpr int kStage = (kSep ? 4 : 2) * kTile;         // K_A V_A [K_B V_B]
-    const int units = f2::num_units<kSep>(bhn, nq);
+    constexpr int kNS = 4;                // K / V stages in the ring
+    constexpr int kStage = 2 * kTile;     // K, V of one block (shared by the two tiles)
+    const int units = f2::num_units(bhn, nq);
     const int h = heads * kD;
     const int G = static_cast<int>(gridDim.x);
 
@@ -508,7 +489,7 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
         // ---------------- TMA producer ----------------
         int uc = 0, kc = 0;
         for (int u = blockIdx.x; u < units; u += G, ++uc) {
-            const f2::Unit un = f2::unit_of<kSep>(u, bhn, nq);
+            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
             const int qb = uc & 1;
             ptx::mbar_wait(&bar[f2::bQEmpty + qb], ((uc >> 1) & 1) ^ 1);
             ptx::mbar_arrive_expect_tx(&bar[f2::bQFull + qb], (un.n[1] > 0 ? 2 : 1) * kTile);
@@ -517,17 +498,14 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
                     ptx::tma_load_2d(smem + f2::oQ + (qb * 2 + x) * kTile, &tm, &bar[f2::bQFull + qb],
                                      (un.bh[x] % heads) * kD, (un.bh[x] / heads) * seq + un.i[x] * kT);
             const int nmax = max(un.n[0], un.n[1]);
-            const int nkv = kSep && un.n[1] > 0 ? 2 : 1;  // K / V sets per block
+            const int row0 = (un.bh[0] / heads) * seq, hd = un.bh[0] % heads;
             for (int j = 0; j < nmax; ++j, ++kc) {
                 const int st = kc % kNS;
                 ptx::mbar_wait(&bar[f2::bKvEmpty + st], ((kc / kNS) & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(&bar[f2::bKvFull + st], 2 * nkv * kTile);
-                for (int x = 0; x < nkv; ++x) {
-                    const int row0 = (un.bh[x] / heads) * seq, hd = un.bh[x] % heads;
-                    uint8_t* dst = smem + f2::oKv + st * kStage + 2 * x * kTile;
-                    ptx::tma_load_2d(dst, &tm, &bar[f2::bKvFull + st], h + hd * kD, row0 + j * kT);
-                    ptx::tma_load_2d(dst + kTile, &tm, &bar[f2::bKvFull + st], 2 * h + hd * kD, row0 + j * kT);
-                }
+                ptx::mbar_arrive_expect_tx(&bar[f2::bKvFull + st], 2 * kTile);
+                uint8_t* dst = smem + f2::oKv + st * kStage;
+                ptx::tma_load_2d(dst, &tm, &bar[f2::bKvFull + st], h + hd * kD, row0 + j * kT);
+                ptx::tma_load_2d(dst + kTile, &tm, &bar[f2::bKvFull + st], 2 * h + hd * kD, row0 + j * kT);
             }
         }
     } else if (warp == 1 && lane == 0) {
@@ -536,8 +514,11 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
         constexpr uint32_t id_pv = ptx::idesc_bf16(128, kD, false, true);
         int uc = 0, kc = 0;
         int pc[2] = {0, 0}, oc[2] = {0, 0};  // P handshakes seen, units finished, per tile
-        // K of tile x in stage st (own set when the tiles are of different heads)
-        auto kv_addr = [&](int x, int st) { return sbase + f2::oKv + st * kStage + (kSep ? 2 * x * kTile : 0); };
+        // K of block stage st (V follows it); both tiles read the same block
+        auto kv_addr = [&](int x, int st) {
+            (void)x;
+            return sbase + f2::oKv + st * kStage;
+        };
         auto issue_s = [&](int x, uint32_t q_addr, int st) {
             const uint32_t k_addr = kv_addr(x, st);
 #pragma unroll
@@ -557,16 +538,16 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
         };
         auto q_addr = [&](int ucn, int x) { return sbase + f2::oQ + ((ucn & 1) * 2 + x) * kTile; };
         if (static_cast<int>(blockIdx.x) < units) {  // the first unit's S(0)
-            const f2::Unit un = f2::unit_of<kSep>(blockIdx.x, bhn, nq);
+            const f2::Unit un = f2::unit_of(blockIdx.x, bhn, nq, kCausal);
             wait_unit_inputs(0, 0);
             for (int x = 0; x < 2; ++x)
                 if (un.n[x] > 0) issue_s(x, q_addr(0, x), 0);
         }
         for (int u = blockIdx.x; u < units; u += G, ++uc) {
-            const f2::Unit un = f2::unit_of<kSep>(u, bhn, nq);
+            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
             const int nmax = max(un.n[0], un.n[1]);
             const bool has_next = u + G < units;
-            const f2::Unit nx = has_next ? f2::unit_of<kSep>(u + G, bhn, nq) : un;
+            const f2::Unit nx = has_next ? f2::unit_of(u + G, bhn, nq, kCausal) : un;
             next_ready = false;
             for (int j = 0; j < nmax; ++j) {
                 const int st = (kc + j) % kNS, stn = (kc + j + 1) % kNS;
@@ -651,7 +632,7 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
         int p_i = 0, p_bh = 0;
         float p_m = 0.0f, p_l = 0.0f;
         for (int u = blockIdx.x; u < units; u += G) {
-            const f2::Unit un = f2::unit_of<kSep>(u, bhn, nq);
+            const f2::Unit un = f2::unit_of(u, bhn, nq, kCausal);
             const int n = un.n[x];
             if (n == 0) continue;
             const int ob = oc & 1;
@@ -778,7 +759,7 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
     const bool two_tile = forced == 2 || (forced == 0 && !causal);
     if (two_tile) {
         const int nq = seq / kT;
-        const int units = causal ? nq * ((bhn + 1) / 2) : bhn * (nq / 2 + (nq & 1));
+        const int units = bhn * (nq / 2 + (nq & 1));
         const int grid = std::max(1, std::min(num_sms(), units));
         static std::atomic<uint32_t> done{0};
         int dev = 0;

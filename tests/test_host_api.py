@@ -144,3 +144,21 @@ def test_partition_balanced_is_optimal(times, d):
         assert bounds == [i * len(times) // d for i in range(d + 1)]
     with pytest.raises(Exception, match="exceeds block count"):
         P.partition_balanced(_profile_doc(times), len(times) + 1, 4)
+
+
+def test_bench_flop_profile_balances_the_lm_head():
+    """bench.py's pipeline leg: the GPT-2.2B blocks costed by algorithmic FLOPs put the
+    51200-way LM head (~2 layers) on the last block, so the balanced split at depth 8 gives
+    the last stage fewer layers and a slowest stage below the equal split's."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", Path(__file__).resolve().parents[1] / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    c = bench.CONFIGS["gpt-2.2b"]
+    doc = bench.flop_profile(c)
+    bounds = P.partition_balanced(doc, 8, c["b"])
+    layers = P.stage_layers_from_bounds(bounds)
+    assert sum(layers) == 48 and layers[-1] < 6
+    t = [b["fwd_ms"][str(c["b"])] + b["bwd_ms"][str(c["b"])] for b in json.loads(doc)["blocks"]]
+    worst = max(sum(t[lo:hi]) for lo, hi in zip(bounds[:-1], bounds[1:]))
+    assert worst < sum(t[42:48]) * 0.9
