@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(768, 1) k_mix(long long* out, int tiles) {
         out[blockIdx.x * 2 + 1] = n;
         ptx::mbar_arrive(&bar[4]);  // release the spinners
     } else if ((MASK & 32) && threadIdx.x >= 128 && (threadIdx.x & 31) == 0) {
-        ptx::mbar_wait(&bar[4], 0);  // 20 warps spinning on try_wait meanwhile
+        ptx::mbar_wait(&bar[4], 0);  // 20 warps spinning on try_wait meanwhile (lane 0 only)
+    } else if ((MASK & 64) && threadIdx.x >= 128) {
+        ptx::mbar_wait(&bar[4], 0);  // 20 warps, every lane polling the barrier
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -107,5 +109,6 @@ int main() {
     run<31>(d, "all + wait + fence per group");
     run<39>(d, "all + 20 warps spinning");
     run<63>(d, "all + wait/fence + 20 spinning");
+    run<7 | 64>(d, "all + 20 warps x 32 lanes polling");
     return 0;
 }
