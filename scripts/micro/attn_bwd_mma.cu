@@ -17,7 +17,19 @@ __global__ void __launch_bounds__(768, 1) k_mix(long long* out, int tiles) {
     __shared__ uint64_t bar[5];
     __shared__ uint32_t slot;
     const int warp = threadIdx.x / 32;
-    for (int i = threadIdx.x; i < 12 * kTile / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    for (int i = threadIdx.x; i < 12 * kTile / 4; i += blockDim.x) {
+        // bit 7: pseudo-random bf16 operands in [-2, 2) instead of all 1.0
+        uint32_t v = 0x3c003c00u;
+        if (MASK & 128) {
+            uint32_t x = (i + 1) * 2654435761u;
+            x ^= x >> 13;
+            x *= 0x5bd1e995u;
+            const uint32_t lo = 0x3f80u | (x & 0x007fu) | ((x >> 8) & 0x8000u) | ((x >> 9) & 0x0080u);
+            const uint32_t hi = 0x3f80u | ((x >> 16) & 0x007fu) | ((x >> 4) & 0x8000u) | ((x >> 20) & 0x0080u);
+            v = lo | (hi << 16);
+        }
+        reinterpret_cast<uint32_t*>(smem)[i] = v;
+    }
     if (threadIdx.x == 0) { for (int i = 0; i < 5; ++i) ptx::mbar_init(&bar[i], 1); ptx::fence_mbar_init(); }
     if (warp == 0) ptx::tmem_alloc<512>(&slot);
     ptx::fence_proxy_async();
@@ -78,6 +90,28 @@ __global__ void __launch_bounds__(768, 1) k_mix(long long* out, int tiles) {
         ptx::mbar_wait(&bar[4], 0);  // 20 warps spinning on try_wait meanwhile (lane 0 only)
     } else if ((MASK & 64) && threadIdx.x >= 128) {
         ptx::mbar_wait(&bar[4], 0);  // 20 warps, every lane polling the barrier
+    } else if ((MASK & 256) && threadIdx.x >= 128 && threadIdx.x < 640) {
+        // 16 warps streaming SMEM stores + loads (the elementwise / flush warps' traffic)
+        // into the upper 64 KB until the MMA thread finishes
+        uint4* region = reinterpret_cast<uint4*>(smem + 8 * kTile);  // 4096 x 16 B
+        uint32_t acc = 0;
+        for (int it = 0; !ptx::mbar_test(&bar[4], 0); ++it) {
+            const int idx = (threadIdx.x + it * 256) & 4095;
+            region[idx] = make_uint4(acc, acc + 1, acc + 2, acc + 3);
+            acc += region[idx ^ 128].x;
+        }
+        if (acc == 0xffffffffu) out[0] = acc;
+    } else if ((MASK & 512) && threadIdx.x >= 128 && threadIdx.x < 640) {
+        // 16 warps streaming tcgen05.ld of TMEM columns 0-255 (the S / dP reads)
+        const int w = threadIdx.x / 32;
+        uint32_t acc = 0;
+        for (int it = 0; !ptx::mbar_test(&bar[4], 0); ++it) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>((w & 3) * 32) << 16) + ((it * 32) & 255), v);
+            ptx::tmem_ld_wait();
+            acc += v[0] ^ v[31];
+        }
+        if (acc == 0x12345678u) out[0] = acc;
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -110,5 +144,8 @@ int main() {
     run<39>(d, "all + 20 warps spinning");
     run<63>(d, "all + wait/fence + 20 spinning");
     run<7 | 64>(d, "all + 20 warps x 32 lanes polling");
+    run<7 | 128>(d, "all, random operands");
+    run<7 | 256>(d, "all + 16 warps of SMEM ld/st");
+    run<7 | 512>(d, "all + 16 warps of TMEM loads");
     return 0;
 }
