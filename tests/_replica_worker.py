@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--precision", choices=["fp64", "bf16", "transformer"], default="fp64")
     ap.add_argument("--transport", choices=["ipc", "nccl"], default="nccl")
     ap.add_argument("--optimizer", choices=["sgd", "adam"], default="sgd")
+    ap.add_argument("--pipelined", action="store_true",
+                    help="one stage per process (gpu = stage * width + replica), CUDA-IPC hand-offs")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local % torch.cuda.device_count())
@@ -43,21 +45,30 @@ def main():
         return transformer(a, rank, world)
     dim, L, b, m, T, seed = (8, 4, 8, 4, 5, 31) if a.precision == "fp64" else (128, 4, 128, 4, 4, 31)
     toy = O.ToyModel.make(dim, L, b, m * T, seed)
-    cols = b // world
+    if a.pipelined:
+        stage, replica, width = D.grid(world, rank, a.depth)
+        mine = [stage]
+    else:
+        replica, width = rank, world
+        mine = list(range(a.depth))
+    cols = b // width
     kind = P.MODEL_LINEAR_F64 if a.precision == "fp64" else P.MODEL_LINEAR_BF16
     eng = P.Engine(model_kind=kind, policy=P.PipelinePolicy.TwoBW, depth=a.depth, microbatches=m,
-                   microbatch_size=cols, layers=L, dim=dim, learning_rate=0.05, momentum=0.9)
+                   microbatch_size=cols, layers=L, dim=dim, learning_rate=0.05, momentum=0.9,
+                   local_stages=(mine[0], 1) if a.pipelined else None)
     per = L // a.depth
-    for s in range(a.depth):
+    for s in mine:
         eng.load_stage_weights(s, np.concatenate([w.flatten(order="F") for w in toy.weights[s * per:(s + 1) * per]]))
-    assert D.join_replicas(eng, a.depth, transport=a.transport) == a.transport
-    xs = np.stack([x[:, rank * cols:(rank + 1) * cols].flatten(order="F") for x, _ in toy.dataset])
-    ys = np.stack([y[:, rank * cols:(rank + 1) * cols].flatten(order="F") for _, y in toy.dataset])
+    if a.pipelined:
+        D.connect_pipeline(eng, a.depth)
+    assert D.join_replicas(eng, a.depth, pipelined=a.pipelined, transport=a.transport) == a.transport
+    xs = np.stack([x[:, replica * cols:(replica + 1) * cols].flatten(order="F") for x, _ in toy.dataset])
+    ys = np.stack([y[:, replica * cols:(replica + 1) * cols].flatten(order="F") for _, y in toy.dataset])
     eng.set_data(xs, ys, 1, m * T)
     eng.run_schedule(T, snapshots=True)
     eng.sync()
-    w = np.concatenate([eng.snapshot(s, T) for s in range(a.depth)])
-    np.savez(os.path.join(a.out, f"rank{rank}.npz"), weights=w)
+    w = np.concatenate([eng.snapshot(s, T) for s in mine])
+    np.savez(os.path.join(a.out, f"rank{rank}.npz"), weights=w, stages=np.array(mine))
     dist.barrier()
     eng.close()
     dist.destroy_process_group()

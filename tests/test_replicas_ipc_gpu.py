@@ -62,6 +62,30 @@ def test_ipc_replicas_equal_wide_microbatch(tmp_path, precision, depth, width):
         assert np.linalg.norm((got[0] - w0) - (want - w0)) / np.linalg.norm(want - w0) < 2e-2
 
 
+@pytest.mark.parametrize("precision", ["fp64", "bf16"])
+def test_ipc_pipeline_of_replica_groups(tmp_path, precision):
+    """Depth 2 x width 2 as four processes, one stage each (gpu = stage * width + replica):
+    CUDA-IPC stage hand-offs inside each replica's pipeline AND a peer-memory replica group
+    per stage -- the layout `bench.py --depth 2` uses under torchrun.  Each stage's two
+    replicas end bit-identical and the whole equals one pipeline fed the wide microbatch."""
+    res = _launch(tmp_path, 4, "--depth", "2", "--precision", precision, "--pipelined")
+    by_stage = {}
+    for r in res:
+        by_stage.setdefault(int(r["stages"][0]), []).append(r["weights"])
+    for s, ws in by_stage.items():
+        assert np.array_equal(ws[0], ws[1]), s
+    got = np.concatenate([by_stage[0][0], by_stage[1][0]])
+    dim, L, b, m, T, seed = (8, 4, 8, 4, 5, 31) if precision == "fp64" else (128, 4, 128, 4, 4, 31)
+    model = O.ToyModel.make(dim, L, b, m * T, seed)
+    traj, _, _ = O.pipelined_execute(model, 0.05, 0.9, m, T, O.TWOBW, 2)
+    want = np.concatenate([w.flatten(order="F") for w in traj[-1]])
+    w0 = np.concatenate([w.flatten(order="F") for w in model.weights])
+    if precision == "fp64":
+        assert O.max_rel_diff(got, want) < 1e-12
+    else:
+        assert np.linalg.norm((got - w0) - (want - w0)) / np.linalg.norm(want - w0) < 2e-2
+
+
 def _transformer_run(depth, optimizer, shard=None):
     """One engine in this process on the wide batch (shard=None) or on replica `shard`'s
     half of it alone (no reduction: the control)."""
