@@ -206,6 +206,13 @@ int p2bw_engine_run(p2bw_engine* eng, const p2bw_op* const* programs, const size
                     int snapshot_updates);
 /* generate_schedule(desc->policy, d, m, num_batches) followed by p2bw_engine_run. */
 int p2bw_engine_run_schedule(p2bw_engine* eng, int num_batches, int snapshot_updates);
+/* CUDA-graph form of run_schedule (one process, no replica group; tracing and snapshots
+ * off): the run is captured across the stages' streams into one graph and launched
+ * `launches` times -- each launch after the first is another run of the same programs
+ * on the current weights (allowed when the run returns every stage's weight-version
+ * slots to their places, e.g. an even number of 2BW batches).  ms_per_launch: device
+ * time per launch. */
+int p2bw_engine_run_schedule_graph(p2bw_engine* eng, int num_batches, int launches, double* ms_per_launch);
 /* Streaming form of run_schedule: begin() installs generate_schedule(policy, d, m,
  * num_batches); issue(t) issues every stage's ops up to and including its weight
  * update of batch t (so batch t+1's data must already be set: 2BW forwards of the

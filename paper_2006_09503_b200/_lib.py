@@ -77,6 +77,7 @@ def _signatures():
         ("p2bw_engine_make_toy_data", i, [vp, i, i]),
         ("p2bw_engine_run", i, [vp, vp, vp, i]),
         ("p2bw_engine_run_schedule", i, [vp, i, i]),
+        ("p2bw_engine_run_schedule_graph", i, [vp, i, i, C.POINTER(C.c_double)]),
         ("p2bw_engine_begin", i, [vp, i]),
         ("p2bw_engine_issue", i, [vp, i]),
         ("p2bw_engine_finish", i, [vp]),

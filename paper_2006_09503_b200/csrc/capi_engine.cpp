@@ -178,6 +178,25 @@ int p2bw_engine_run(p2bw_engine* eng, const p2bw_op* const* programs, const size
     });
 }
 
+int p2bw_engine_run_schedule_graph(p2bw_engine* eng, int num_batches, int launches, double* ms_per_launch) {
+    return guarded([&] {
+        auto& e = eng_of(eng);
+        const auto& c = e.config();
+        const auto programs = pipesim::generate_schedule(
+            static_cast<pipesim::PipelinePolicy>(c.policy), c.depth, c.microbatches, num_batches);
+        std::vector<p2bw::Program> progs;
+        for (const auto& p : programs) {
+            p2bw::Program prog;
+            for (const auto& op : p.ops)
+                prog.push_back({static_cast<int>(op.kind), op.microbatch, op.weight_version});
+            progs.push_back(std::move(prog));
+        }
+        e.set_snapshot_every_update(false);
+        const double ms = e.run_graph(progs, launches);
+        if (ms_per_launch) *ms_per_launch = ms;
+    });
+}
+
 int p2bw_engine_run_schedule(p2bw_engine* eng, int num_batches, int snapshot_updates) {
     return guarded([&] {
         auto& e = eng_of(eng);

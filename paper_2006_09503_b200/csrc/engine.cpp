@@ -778,11 +778,104 @@ void Engine::issue(int upto_batch) {
 
 void Engine::finish() {
     if (done_ops_ != total_ops_) issue(1 << 30);
+    if (capturing_) return;  // run_graph times the launches instead
     for (Stage& st : stages_) {
         if (!st.local) continue;
         DeviceGuard g(st.device);
         check_cuda(cudaEventRecord(st.t1, st.stream), "cudaEventRecord");
     }
+}
+
+double Engine::run_graph(const std::vector<Program>& programs, int launches) {
+    if (launches < 1) throw Error("graph mode: launches must be >= 1");
+    if (trace_on_ || snapshots_on_) throw Error("graph mode: tracing and snapshots must be off");
+    Stage* origin_st = nullptr;
+    for (Stage& st : stages_) {
+        if (!st.local || st.comm || st.ipc_group)
+            throw Error("graph mode runs single-process engines without replica groups");
+        if (!origin_st) origin_st = &st;
+        else if (st.device != origin_st->device) throw Error("graph mode: all stages on one device");
+    }
+    // The graph bakes in the slots each update writes and each op reads, chosen from the
+    // pre-run state: a replay is another run only if the latest version sits in the same
+    // slot again afterwards (2BW: an even number of updates; flush policies: one slot).
+    std::vector<int> latest_before;
+    for (const Stage& st : stages_) latest_before.push_back(st.version_slot.at(st.updates_done));
+    begin(programs);
+    DeviceGuard g(origin_st->device);
+    const cudaStream_t origin = origin_st->stream;
+    std::vector<cudaStream_t> others;
+    for (Stage& st : stages_)
+        for (cudaStream_t x : {st.stream, st.fstream, st.dstream, st.ustream})
+            if (x && x != origin) others.push_back(x);
+    cudaEvent_t fork = nullptr;
+    std::vector<cudaEvent_t> joins(others.size(), nullptr);
+    check_cuda(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "cudaEventCreate");
+    for (auto& e : joins) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    check_cuda(cudaStreamBeginCapture(origin, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+    capturing_ = true;
+    try {
+        // every stream of the run joins the capture through the origin
+        check_cuda(cudaEventRecord(fork, origin), "cudaEventRecord(fork)");
+        for (cudaStream_t x : others) check_cuda(cudaStreamWaitEvent(x, fork, 0), "cudaStreamWaitEvent(fork)");
+        issue(1 << 30);
+        finish();
+        for (size_t i = 0; i < others.size(); ++i) {
+            check_cuda(cudaEventRecord(joins[i], others[i]), "cudaEventRecord(join)");
+            check_cuda(cudaStreamWaitEvent(origin, joins[i], 0), "cudaStreamWaitEvent(join)");
+        }
+        capturing_ = false;
+        check_cuda(cudaStreamEndCapture(origin, &graph), "cudaStreamEndCapture");
+        check_cuda(cudaGraphInstantiate(&exec, graph, 0), "cudaGraphInstantiate");
+    } catch (...) {
+        capturing_ = false;
+        cudaGraph_t partial = nullptr;
+        cudaStreamEndCapture(origin, &partial);
+        if (partial) cudaGraphDestroy(partial);
+        if (graph) cudaGraphDestroy(graph);
+        cudaEventDestroy(fork);
+        for (auto e : joins) cudaEventDestroy(e);
+        throw;
+    }
+    // more than one launch replays the run: the slots must have returned to their places
+    bool periodic = cfg_.policy != P2BW_POLICY_1F1B;  // 1F1B's stash-pinned versions: launch once
+    for (size_t i = 0; i < stages_.size(); ++i)
+        periodic = periodic && stages_[i].version_slot.at(stages_[i].updates_done) == latest_before[i];
+    if (launches > 1 && !periodic) {
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        cudaEventDestroy(fork);
+        for (auto e : joins) cudaEventDestroy(e);
+        throw Error("graph mode: this run does not return the weight-version slots to their places; launch it once");
+    }
+    cudaEvent_t e0, e1;
+    check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
+    check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
+    check_cuda(cudaEventRecord(e0, origin), "cudaEventRecord");
+    for (int i = 0; i < launches; ++i) check_cuda(cudaGraphLaunch(exec, origin), "cudaGraphLaunch");
+    check_cuda(cudaEventRecord(e1, origin), "cudaEventRecord");
+    check_cuda(cudaEventSynchronize(e1), "cudaEventSynchronize");
+    float ms = 0.0f;
+    check_cuda(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
+    // host bookkeeping: the extra launches are further runs of the same programs
+    for (Stage& st : stages_) {
+        const int upd = st.updates_done - st.version_base;
+        const int extra = upd * (launches - 1);
+        if (extra == 0) continue;
+        std::map<int, int> shifted;
+        for (const auto& kv : st.version_slot) shifted[kv.first + extra] = kv.second;
+        st.version_slot = std::move(shifted);
+        st.updates_done += extra;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    cudaEventDestroy(fork);
+    for (auto e : joins) cudaEventDestroy(e);
+    return static_cast<double>(ms) / launches;
 }
 
 void Engine::run(const std::vector<Program>& programs) {

@@ -214,6 +214,14 @@ public:
     void begin(const std::vector<Program>& programs);
     void issue(int upto_batch);
     void finish();
+    // CUDA-graph mode (one process, no replica group, tracing and snapshots off): the
+    // whole run is captured into one graph across the stages' streams and launched
+    // `launches` times.  Every launch after the first runs the same programs again on
+    // the current weights, exactly as another run() would, which needs each stage's
+    // version slots to be back where they started (an even number of 2BW updates per
+    // run; checked).  Returns the device ms per launch (events around the launches);
+    // the per-update events of a captured run are not timed.
+    double run_graph(const std::vector<Program>& programs, int launches);
     // Device time between a stage's u0-th and u1-th update of the current run.
     double update_elapsed_ms(int stage, int u0, int u1);
     // Data parallelism: stage s of this pipeline joins the communicator of its
@@ -352,6 +360,7 @@ private:
     std::vector<TraceRec> trace_;
     cudaEvent_t trace_open_ = nullptr;  // e0 of the op being issued
     long long mb_base_ = 0;  // microbatches of earlier runs (flag sequence numbers)
+    bool capturing_ = false;  // inside run_graph's stream capture
     int run_max_mb_ = 0;
 };
 

@@ -370,6 +370,10 @@ public:
         // weight gradients on the side stream (off the dgrad chain's critical path), as
         // in the transformer stage; per-launch profiling keeps them on the stage stream
         side_ = prof::enabled() ? s : side_stream_;
+        // ev_[0 / 1] were last recorded by the previous backward (joined at its end): re-record
+        // them after a fork so the first wait below refers to this backward (CUDA-graph capture)
+        fork(s);
+        for (int e = 0; e < 2; ++e) check_cuda(cudaEventRecord(ev_[e], side_), "cudaEventRecord(side)");
         int flip = 0;
         for (int l = layers_ - 1; l >= 0; --l) {
             const bf16* in = l == 0 ? xin_[static_cast<size_t>(sslot)] : stash_ptr(sslot, l);

@@ -280,6 +280,11 @@ public:
         // that every kernel's event-timed duration is its own (the roofline report).
         side_ = prof::enabled() ? s : side_stream_;
         fork(kEvStart, s);  // the side stream follows the previous update (grad_ overwrite with beta 0)
+        // The "side task done" events the main stream waits on before a side task of THIS
+        // backward re-records them were last recorded by the previous backward, whose end
+        // already joined the side stream: re-record them here (trivially complete) so no wait
+        // refers to work outside the current CUDA-graph capture (Engine::run_graph).
+        for (int e : {kEvDoneA, kEvDoneB, kEvDoneC, kEvDoneD}) done(e);
         if (last_) {
             // logits now hold dloss/dlogits (softmax_xent ran in the forward)
             bf16* dxf = R_ < T_ ? gH_ : gA_;

@@ -314,6 +314,12 @@ class Engine:
     def run_schedule(self, num_batches: int, snapshots: bool = False):
         _call("p2bw_engine_run_schedule", self.h, num_batches, int(snapshots))
 
+    def run_schedule_graph(self, num_batches: int, launches: int = 1) -> float:
+        """CUDA-graph run (p2bw_engine_run_schedule_graph): device ms per launch."""
+        ms = C.c_double()
+        _call("p2bw_engine_run_schedule_graph", self.h, num_batches, launches, C.byref(ms))
+        return ms.value
+
     def run(self, programs: list[StageProgram], snapshots: bool = False):
         arrs = [(_lib.Op * max(len(p.ops), 1))(*[_lib.Op(int(o.kind), o.microbatch, o.weight_version)
                                                  for o in p.ops]) for p in programs]

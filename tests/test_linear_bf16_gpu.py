@@ -148,3 +148,25 @@ def test_device_toy_model_matches_toymodel_make():
     dg, dw = np.concatenate(got) - w0, np.concatenate(want) - w0
     assert np.linalg.norm(dg - dw) / np.linalg.norm(dw) < 2e-2
     assert np.max(np.abs(la - lb) / lb) < 2e-2
+
+
+def test_graph_run_equals_eager_runs_linear_bf16():
+    """CUDA-graph mode on the bf16 linear chain (production GEMMs, k_sgd, side stream),
+    after an eager run: 2 launches of a 4-batch 2BW run equal 2 eager runs bit for bit
+    (no run-order-dependent reductions on this path)."""
+    outs = []
+    for mode in ("eager", "graph"):
+        eng = P.Engine(model_kind=P.MODEL_LINEAR_BF16, policy=P.PipelinePolicy.TwoBW, depth=2, microbatches=2,
+                       microbatch_size=128, layers=4, dim=128, learning_rate=1e-3, momentum=0.9, seed=9)
+        eng.init_weights()
+        eng.make_toy_data(1, 4)
+        eng.run_schedule(4)
+        if mode == "eager":
+            eng.run_schedule(4)
+            eng.run_schedule(4)
+        else:
+            eng.run_schedule_graph(4, 2)
+        eng.sync()
+        outs.append(np.concatenate([eng.read_version(s, 12) for s in range(2)]))  # 3 runs x 4 updates
+        eng.close()
+    assert np.array_equal(outs[0], outs[1])

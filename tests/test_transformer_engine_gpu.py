@@ -219,3 +219,50 @@ def test_stage_split_validation():
         P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=2, microbatches=2,
                  microbatch_size=2, layers=4, hidden=128, heads=2, seq_len=128, vocab=500, causal=1,
                  stage_layers=[0, 4])
+
+
+@pytest.mark.parametrize("depth", [1, 2])
+def test_graph_run_equals_eager_runs(depth):
+    """CUDA-graph mode (p2bw_engine_run_schedule_graph), after an eager run: the run captured
+    across the stage, forward, update and weight-gradient side streams, launched 3 times,
+    trains exactly as three eager runs of the same schedule (every launch after the first is another run on
+    the current weights; 2 batches per run return the 2BW version slots to their places)."""
+    spec = TO.Spec(layers=2, hidden=128, heads=2, seq=128, vocab=500, batch=2, causal=True, head_rows=0)
+    m, T, lr, beta, seed = 2, 2, 0.5, 0.9, 11
+    ids, tg = TO.synthetic_batch(spec, m * T, seed + 1)
+    out = {}
+    for mode in ("eager", "graph"):
+        eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=depth, microbatches=m,
+                       microbatch_size=spec.batch, layers=spec.layers, hidden=spec.hidden, heads=spec.heads,
+                       seq_len=spec.seq, vocab=spec.vocab, causal=1, learning_rate=lr, momentum=beta, seed=seed)
+        eng.init_weights()
+        eng.set_data(ids, tg, 1, m * T)
+        eng.run_schedule(T)  # an eager run first: the capture must not depend on its events
+        if mode == "eager":
+            for _ in range(3):
+                eng.run_schedule(T)
+        else:
+            ms = eng.run_schedule_graph(T, 3)
+            assert ms > 0
+        eng.sync()
+        out[mode] = (np.concatenate([eng.read_master(s) for s in range(depth)]), eng.losses(1, m * T))
+        eng.close()
+    we, le = out["eager"]
+    wg, lg = out["graph"]
+    # same kernels in the same order per stream; only the run-order-dependent fp32
+    # reductions (token-embedding gradient atomics, attention dQ) may differ
+    assert np.allclose(wg, we, rtol=1e-3, atol=1e-5), np.max(np.abs(wg - we))
+    assert np.allclose(lg, le, rtol=1e-3)
+
+
+def test_graph_mode_rejects_an_odd_2bw_run_replayed():
+    spec = TO.Spec(layers=2, hidden=128, heads=2, seq=128, vocab=500, batch=2, causal=True, head_rows=0)
+    eng = P.Engine(model_kind=P.MODEL_TRANSFORMER, policy=P.PipelinePolicy.TwoBW, depth=1, microbatches=2,
+                   microbatch_size=spec.batch, layers=spec.layers, hidden=spec.hidden, heads=spec.heads,
+                   seq_len=spec.seq, vocab=spec.vocab, causal=1, learning_rate=0.1, momentum=0.9, seed=3)
+    eng.init_weights()
+    ids, tg = TO.synthetic_batch(spec, 6, 4)
+    eng.set_data(ids, tg, 1, 4)
+    with pytest.raises(Exception, match="launch it once"):
+        eng.run_schedule_graph(3, 2)
+    eng.close()
