@@ -367,6 +367,12 @@ int p2bw_debug_attention_timing(void* dev_buf);
  * CTA: entry, setup done, last load issued, first stage consumed, last MMA commit,
  * first accumulator seen by the epilogue, epilogue done, teardown done (NULL = off). */
 int p2bw_debug_gemm_timing(void* dev_buf);
+/* Debug: the launch plan p2bw_kernel_gemm_bf16 makes for a shape (epilogue kind as in
+ * p2bw_gemm_epilogue, bias_grad != 0 for a fused bias gradient): out[4] = {BN, CTAs per
+ * cluster, split-K slices, tail-split K parts (1 = none)}.  The tail split runs the
+ * ragged last wave's tiles as K parts on idle SMs with an in-kernel fp32 fixup;
+ * P2BW_GEMM_TAIL=0 disables it. */
+int p2bw_debug_gemm_plan(int m, int n, int k, int a_major, int b_major, int kind, int bias_grad, int* out);
 /* Column sums of a bf16 matrix (bias gradients): out (=|+=) sum_r x[r, :]. */
 int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream);
 /* Fused softmax cross-entropy: logits [rows x vp] -> dlogits in place, row_loss [rows]. */

@@ -111,6 +111,7 @@ def _signatures():
         ("p2bw_kernel_colsum", i, [vp, i, i, i, vp, i, vp]),
         ("p2bw_debug_attention_timing", i, [vp]),
         ("p2bw_debug_gemm_timing", i, [vp]),
+        ("p2bw_debug_gemm_plan", i, [i, i, i, i, i, i, i, C.POINTER(C.c_int)]),
     ]
 
 

@@ -106,6 +106,11 @@ extern "C" int p2bw_debug_gemm_timing(void* dev_buf) {
     return guarded([&] { gemm_debug_timing(static_cast<unsigned long long*>(dev_buf)); });
 }
 
+extern "C" int p2bw_debug_gemm_plan(int m, int n, int k, int a_major, int b_major, int kind, int bias_grad,
+                                    int* out) {
+    return guarded([&] { gemm_plan(m, n, k, a_major != 0, b_major != 0, kind == 1, bias_grad != 0, out); });
+}
+
 extern "C" int p2bw_kernel_colsum(const void* x, int rows, int n, int ld, void* out, int overwrite, void* stream) {
     return guarded([&] {
         float* scratch = nullptr;

@@ -24,6 +24,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -90,7 +91,59 @@ struct KParams {
     int splits;  // split-K factor (fp32 reduce-add epilogue only)
     GemmEpilogue epi;
     float* rsum;  // row sums of A (bias gradient partials [splits][m]) or nullptr
+    // Tail split (bf16 epilogues, splits == 1): the last tail_tiles output tiles -- the
+    // ragged last wave -- are cut into tail_f K parts run by otherwise idle CTAs.  Parts
+    // 0 .. f-2 ("contributors") write fp32 partial accumulators to tail_ws and count
+    // themselves in tail_flags (per tile, CTA of the pair and epilogue warp); part f-1
+    // (the "finisher") waits for them, adds the partials and runs the fused epilogue.
+    int tail_tiles, tail_f;
+    float* tail_ws;
+    unsigned* tail_flags;
 };
+
+// One work unit: an output tile (group) over the K blocks [kb0, kb1).  role 0: a whole
+// tile or split-K slice; 1: tail contributor part; 2: tail finisher.  Units are numbered
+// full tiles first, then all contributors, then the finishers, and unit w runs on CTA
+// slot w % slots: every finisher sits on a higher slot than its contributors, so with
+// in-order CTA dispatch a spinning finisher never holds an SM its contributors need.
+struct Unit {
+    int tile, kb0, kb1, role, t, part;
+};
+
+__device__ __forceinline__ Unit unit_of(int w, int num_tiles, int kblocks, int kb_per, const KParams& p) {
+    Unit u;
+    const int full = num_tiles - p.tail_tiles;
+    if (p.tail_tiles == 0 || w < full) {
+        u.tile = w % num_tiles;
+        u.kb0 = (w / num_tiles) * kb_per;
+        u.kb1 = min(kblocks, u.kb0 + kb_per);
+        u.role = 0;
+        u.t = 0;
+        u.part = 0;
+        return u;
+    }
+    const int f = p.tail_f, j = w - full, nc = p.tail_tiles * (f - 1);
+    if (j < nc) {
+        u.t = j / (f - 1);
+        u.part = j % (f - 1);
+        u.role = 1;
+    } else {
+        u.t = j - nc;
+        u.part = f - 1;
+        u.role = 2;
+    }
+    u.tile = full + u.t;
+    const int kbp = (kblocks + f - 1) / f;
+    u.kb0 = u.part * kbp;
+    u.kb1 = min(kblocks, u.kb0 + kbp);
+    return u;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // Output / side-input tensor maps of the epilogue (32-row boxes, 128 B rows, SW128).
 struct EpiMaps {
@@ -157,7 +210,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
     const int tiles_mg = kPair ? (tiles_m + 1) / 2 : tiles_m;
     const int tiles_ng = (tiles_n + kNP - 1) / kNP;
     const int num_tiles = tiles_mg * tiles_ng;
-    const int num_work = num_tiles * p.splits;
+    const int num_work = p.tail_tiles > 0 ? num_tiles + p.tail_tiles * (p.tail_f - 1) : num_tiles * p.splits;
     const int kb_per = (kblocks + p.splits - 1) / p.splits;
     const int w0 = blockIdx.x / kCl, wstep = gridDim.x / kCl;
     const uint16_t pair_mask = static_cast<uint16_t>(kPair ? (0x3 << (2 * pair)) : 0x1);  // my pair's CTAs
@@ -198,12 +251,10 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int w = w0; w < num_work; w += wstep) {
-                const int tile = w % num_tiles;
-                const int m0 = ((tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
-                const int n0 = ((tile / tiles_mg) * kNP + pair) * BN;
-                const int kb0 = (w / num_tiles) * kb_per;
-                const int kb1 = min(kblocks, kb0 + kb_per);
-                for (int kb = kb0; kb < kb1; ++kb) {
+                const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);
+                const int m0 = ((u.tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
+                const int n0 = ((u.tile / tiles_mg) * kNP + pair) * BN;
+                for (int kb = u.kb0; kb < u.kb1; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* da = s_a + stage * Cfg::kABytes;
                     uint8_t* db = s_b + stage * Cfg::kBBytes;
@@ -290,8 +341,8 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int w = w0; w < num_work; w += wstep) {
-                const int kb0 = (w / num_tiles) * kb_per;
-                const int kb1 = min(kblocks, kb0 + kb_per);
+                const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);
+                const int kb0 = u.kb0, kb1 = u.kb1;
                 ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -339,7 +390,7 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             const int c = lane & 7;  // 16-byte chunk: rows 8c .. 8c+7 of the box; K rows of lane >> 3 (mod 4)
             int stage = 0;
             uint32_t phase = 0;
-            for (int w = w0; w < num_work; w += wstep) {
+            for (int w = w0; w < num_work; w += wstep) {  // (no tail split with row sums)
                 const int tile = w % num_tiles;
                 const int m0 = (tile % tiles_mg) * kBM;
                 const bool active = tile / tiles_mg == 0;  // n0 == 0
@@ -399,11 +450,10 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int w = w0; w < num_work; w += wstep) {
-                const int tile = w % num_tiles;
-                const int mt = tile % tiles_mg;
-                const bool active = tile / tiles_mg == 0;  // n0 == 0: each A element counts once
-                const int kb0 = (w / num_tiles) * kb_per;
-                const int kb1 = min(kblocks, kb0 + kb_per);
+                const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);  // tail parts: disjoint K blocks
+                const int mt = u.tile % tiles_mg;
+                const bool active = u.tile / tiles_mg == 0;  // n0 == 0: each A element counts once
+                const int kb0 = u.kb0, kb1 = u.kb1;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full_bar[stage], phase);
                     if (active) {
@@ -461,16 +511,20 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
         int slot = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        constexpr bool kTail = !kF32 && kCl <= 2;
+        constexpr int kP = kPair ? 2 : 1;
         for (int w = w0; w < num_work; w += wstep) {
-            const int tile = w % num_tiles;
+            const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);
+            const int tile = u.tile;
             const int m0 = ((tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
             const int n0 = ((tile / tiles_mg) * kNP + pair) * BN;
             const int r0 = m0 + q * 32;
+            const int role = kTail ? u.role : 0;
             // Side inputs (residual / GELU pre-activation) do not depend on the
             // accumulator: the warp's (<= 2) chunks of them are TMA-prefetched into its
             // two staging buffers before waiting for the MMA, hiding their latency.
             bool aux_pending = false;
-            if (need_aux) {
+            if (need_aux && role != 1) {
                 if (lane == 0) ptx::bulk_wait_read<0>();  // both buffers read out by earlier stores
                 __syncwarp();
                 int bytes = 0;
@@ -489,20 +543,26 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             if (ew == 0 && lane == 0 && w == w0) gmark(5);
             const uint32_t tbase =
                 tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+            // tail split: this warp's partial block (fp32, [BN / 4 column quads][128 rows]
+            // float4, so a warp's accesses are 512 contiguous bytes) and its arrival counter
+            unsigned* tflag = nullptr;
+            if constexpr (kTail) {
+                if (role != 0) tflag = p.tail_flags + (u.t * kP + prank) * kEW + ew;
+                if (role == 2) {  // finisher: wait for the f - 1 contributors of this tile
+                    if (lane == 0) {
+                        const unsigned want = static_cast<unsigned>(p.tail_f - 1);
+                        while (ld_acquire_u32(tflag) != want) __nanosleep(64);
+                        *tflag = 0u;  // re-armed for the next launch (all contributors are done)
+                    }
+                    __syncwarp();
+                }
+            }
             int jj = 0;  // index of this warp's chunk within the tile
 #pragma unroll 1
             for (int c = ch; c < BN / W; c += kEW / 4, ++jj) {
                 const int col0 = n0 + c * W;
                 if (col0 >= p.n || r0 >= p.m) continue;  // warp-uniform: whole chunk out of range
                 uint8_t* buf = ebuf + (need_aux ? jj : slot) * kEpiBuf;
-                if (!need_aux) {
-                    // the buffer's previous bulk store must have finished reading it
-                    if (lane == 0) {
-                        if (two_out) ptx::bulk_wait_read<0>();
-                        else ptx::bulk_wait_read<1>();
-                    }
-                    __syncwarp();
-                }
                 float x[W];
                 {
                     uint32_t v[32];
@@ -516,10 +576,46 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j) x[32 + j] = __uint_as_float(v[j]);
                     }
-                    if (e.alpha != 1.0f) {  // warp-uniform; the stage GEMMs all use alpha 1
+                }
+                if constexpr (kTail) {
+                    if (role != 0) {
+                        const int row = q * 32 + lane;
+                        if (role == 1) {
+                            float4* dst = reinterpret_cast<float4*>(
+                                p.tail_ws +
+                                (static_cast<size_t>((u.t * (p.tail_f - 1) + u.part) * kP + prank) * kBM * BN));
 #pragma unroll
-                        for (int j = 0; j < W; ++j) x[j] *= e.alpha;
+                            for (int j = 0; j < W / 4; ++j)
+                                __stcg(dst + (c * (W / 4) + j) * kBM + row,
+                                       make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+                            continue;
+                        }
+                        for (int part = 0; part < p.tail_f - 1; ++part) {  // fixed order: deterministic
+                            const float4* src = reinterpret_cast<const float4*>(
+                                p.tail_ws +
+                                (static_cast<size_t>((u.t * (p.tail_f - 1) + part) * kP + prank) * kBM * BN));
+#pragma unroll
+                            for (int j = 0; j < W / 4; ++j) {
+                                const float4 y = __ldcg(src + (c * (W / 4) + j) * kBM + row);
+                                x[4 * j] += y.x;
+                                x[4 * j + 1] += y.y;
+                                x[4 * j + 2] += y.z;
+                                x[4 * j + 3] += y.w;
+                            }
+                        }
                     }
+                }
+                if (e.alpha != 1.0f) {  // warp-uniform; the stage GEMMs all use alpha 1
+#pragma unroll
+                    for (int j = 0; j < W; ++j) x[j] *= e.alpha;
+                }
+                if (!need_aux) {
+                    // the buffer's previous bulk store must have finished reading it
+                    if (lane == 0) {
+                        if (two_out) ptx::bulk_wait_read<0>();
+                        else ptx::bulk_wait_read<1>();
+                    }
+                    __syncwarp();
                 }
                 if constexpr (kF32) {
 #pragma unroll
@@ -610,6 +706,13 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                     ptx::bulk_commit();
                 }
                 if (!two_out) slot ^= 1;
+            }
+            if constexpr (kTail) {
+                if (role == 1) {  // publish this warp's partial block
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) atomicAdd(tflag, 1u);
+                }
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -721,7 +824,8 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, con
     const int tiles_m = (p.m + kBM - 1) / kBM, tiles_n = (p.n + BN - 1) / BN;
     const int tiles_mg = kCl >= 2 ? (tiles_m + 1) / 2 : tiles_m;
     const int tiles_ng = kCl == 4 ? (tiles_n + 1) / 2 : tiles_n;
-    const int work = tiles_mg * tiles_ng * p.splits;
+    const int work = p.tail_tiles > 0 ? tiles_mg * tiles_ng + p.tail_tiles * (p.tail_f - 1)
+                                      : tiles_mg * tiles_ng * p.splits;
     const int slots = num_sms() / kCl;
     const int grid = kCl * (work < slots ? work : slots);
     cudaLaunchConfig_t cfg{};
@@ -775,7 +879,47 @@ struct TileChoice {
     int cl;
     int splits;
     double t;  // modelled time, in 256 x 256 pair k-block units
+    int tail_f = 1;  // tail split: K parts of each last-wave tile (1 = off)
 };
+
+// Tail-split workspace of one stream: the fp32 partials of at most one CTA per SM
+// (tail tiles x (f - 1) contributor parts x CTAs per tile <= SMs) of 128 x 256 floats,
+// and one arrival counter per (tail tile, CTA, epilogue warp) -- kept zero between
+// launches by the finishers.  Allocated on a stream's first tail-split GEMM, outside
+// graph capture (a capture without one runs the GEMM without the tail split).
+struct TailPool {
+    float* ws = nullptr;
+    unsigned* flags = nullptr;
+};
+
+TailPool tail_pool(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, TailPool>* pools = new std::map<std::pair<int, cudaStream_t>, TailPool>();
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = pools->find({dev, s});
+    if (it != pools->end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    check_cuda(cudaStreamIsCapturing(s, &cs), "cudaStreamIsCapturing");
+    if (cs != cudaStreamCaptureStatusNone) return TailPool{};
+    TailPool tp;
+    const size_t n_ws = static_cast<size_t>(num_sms()) * kBM * 256;
+    const size_t n_flags = static_cast<size_t>(num_sms()) * 8;
+    check_cuda(cudaMalloc(&tp.ws, n_ws * sizeof(float)), "cudaMalloc(gemm tail workspace)");
+    check_cuda(cudaMalloc(&tp.flags, n_flags * sizeof(unsigned)), "cudaMalloc(gemm tail flags)");
+    check_cuda(cudaMemset(tp.flags, 0, n_flags * sizeof(unsigned)), "cudaMemset(gemm tail flags)");
+    (*pools)[{dev, s}] = tp;
+    return tp;
+}
+
+bool tail_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("P2BW_GEMM_TAIL");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+}
 
 bool tile_ok(int bn, int cl, bool bmn) { return !(bmn && cl >= 2 && (bn / 2) % 64 != 0); }
 
@@ -798,7 +942,13 @@ double tile_speed(int bn, int cl) {
 // [8192 x 768] output on 74 SM pairs run as two waves at 65% occupancy, 256 128 x 192
 // tiles as two waves at 86%.  fp32 (wgrad) outputs keep 256-wide tiles, which the
 // sweeps favour for MN-major operands, and choose only their split count.
-TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_split, bool single_cta = false) {
+//
+// Tail split (bf16 outputs): the r tiles of a ragged last wave may instead run as f K
+// parts each on the idle slots (r f <= slots), the last wave then costing
+// ceil(kb / f) k-blocks plus the fp32 partial traffic through L2 (~128 KB written and
+// read per contributor CTA, ~7.5 k-block times per part at a 256-wide tile, measured).
+TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_split, bool single_cta = false,
+                       bool allow_tail = false) {
     const int kblocks = (k + kBK - 1) / kBK;
     if (const char* env = std::getenv("P2BW_GEMM_TILE")) {  // tuning knob: "bn,cl[,splits]"
         int bn = 0, cl = 0, sp = 0;
@@ -829,13 +979,44 @@ TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_s
                     best_t = t;
                     best = {bn, cl, s_eff, t};
                 }
+                if (allow_tail && sp == 1 && units % slots != 0) {
+                    const long full_waves = units / slots, r = units % slots;
+                    const int f = static_cast<int>(std::min<long>({4, slots / r, kblocks / 8}));
+                    if (f >= 2) {
+                        const double tt = full_waves * (kblocks * per_kb + 3.0) +
+                                          ((kblocks + f - 1) / f) * per_kb + 3.0 + 7.5 * f * (bn / 256.0);
+                        if (tt < best_t - 1e-9) {
+                            best_t = tt;
+                            best = {bn, cl, 1, tt, f};
+                        }
+                    }
+                }
             }
         }
     }
     return best;
 }
 
+// The launch plan of the main path: tile, cluster, split-K and tail split.
+TileChoice plan_tile(int m, int n, int k, bool bmn, bool f32, bool want_rsum, bool want_csum) {
+    const bool tail_ok = !f32 && !want_rsum && tail_enabled();
+    TileChoice tc = choose_tile(m, n, k, f32, bmn, f32, want_rsum || want_csum, tail_ok);
+    if (!tile_ok(tc.bn, tc.cl, bmn)) tc.cl = 1;
+    if (want_rsum || want_csum) tc.cl = 1;  // the sum warps read a local full barrier (no CTA pairs)
+    if (!f32) tc.splits = 1;
+    if (!tail_ok || tc.cl > 2) tc.tail_f = 1;
+    return tc;
+}
+
 }  // namespace
+
+void gemm_plan(int m, int n, int k, bool amn, bool bmn, bool f32, bool bias_grad, int out[4]) {
+    const TileChoice tc = plan_tile(m, n, k, bmn, f32, bias_grad && amn, bias_grad && !amn);
+    out[0] = tc.bn;
+    out[1] = tc.cl;
+    out[2] = tc.splits;
+    out[3] = tc.tail_f;
+}
 
 CUtensorMap make_tmap_bf16_2d(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld_elems,
                               uint32_t box_inner, uint32_t box_outer) {
@@ -864,7 +1045,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
     const bool want_csum = epi.bias_grad != nullptr && !amn;  // dgrad: column sums of A over M
     if (want_rsum && !f32) throw Error("gemm: bias_grad with an MN-major A needs an fp32 store (wgrad)");
     if (want_csum && k % 8 != 0) throw Error("gemm: bias_grad with a K-major A needs K % 8 == 0");
-    TileChoice tc = choose_tile(m, n, k, f32, bmn, f32, want_rsum || want_csum);
+    TileChoice tc = plan_tile(m, n, k, bmn, f32, want_rsum, want_csum);
     // Plain bf16 stores with few output tiles and a long K (the LM-head dgrad: 1232 x 768
     // over K = 30592 fills 60 SMs with 128 x 128 tiles) run split-K into the caller's
     // fp32 workspace and are cast afterwards, when the model says that wins.
@@ -886,9 +1067,19 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
             return;
         }
     }
-    if (!tile_ok(tc.bn, tc.cl, bmn)) tc.cl = 1;
-    if (want_rsum || want_csum) tc.cl = 1;  // the sum warps read a local full barrier (no CTA pairs)
     const int bn = tc.bn, cl = tc.cl;
+    int tail_tiles = 0, tail_f = 1;
+    TailPool tp{};
+    if (tc.tail_f >= 2) {
+        const int tiles_m = (m + kBM - 1) / kBM;
+        const int units = (cl == 2 ? (tiles_m + 1) / 2 : tiles_m) * ((n + bn - 1) / bn);
+        const int slots = num_sms() / cl;
+        tp = tail_pool(stream);
+        if (tp.ws != nullptr && units % slots != 0 && (units % slots) * tc.tail_f <= slots) {
+            tail_tiles = units % slots;
+            tail_f = tc.tail_f;
+        }
+    }
     // A: rows = m (tile kBM), B: rows = n (tile bn; each CTA of a pair loads bn / 2).
     // K-major maps put k innermost.
     // kCl == 4: each CTA multicasts half (64 rows) of the A tile
@@ -934,7 +1125,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
             throw Error("gemm: bias_scratch must hold 2 * ceil(M / 128) * K floats");
         rsum = epi.bias_scratch;
     }
-    KParams p{m, n, k, splits, epi, rsum};
+    KParams p{m, n, k, splits, epi, rsum, tail_tiles, tail_f, tp.ws, tp.flags};
     const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
     // profiler class by pass: forward (K-major x K-major), dgrad (B MN-major), wgrad (both MN-major)
     const char* cls = amn ? "gemm_wgrad" : (bmn ? "gemm_dgrad" : "gemm_fwd");

@@ -60,6 +60,9 @@ struct GemmEpilogue {
 // Requirements: N % 32 == 0, leading dims multiple of 8 elements, 16-byte aligned pointers.
 // Debug: per-CTA phase timestamps of the GEMM kernel (8 u64 per CTA; null = off).
 void gemm_debug_timing(unsigned long long* dev_buf);
+// The main-path launch plan of gemm_bf16 for a shape: {BN, cluster, split-K, tail K
+// parts (1 = no tail split)}.  (The plain-bf16 workspace split-K path is not included.)
+void gemm_plan(int m, int n, int k, bool amn, bool bmn, bool f32, bool bias_grad, int out[4]);
 
 void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
                const GemmEpilogue& epi, cudaStream_t stream);
