@@ -65,6 +65,10 @@ CONFIGS = {
     # profiles/r1_plan_gpt2.2b_8xb200_2bw.txt, planner.cpp:45-99)
     "gpt-2.2b": dict(layers=48, hidden=1920, heads=30, seq=512, vocab=51200, causal=True, head_rows=0,
                      b=16, m=4, depth=1),
+    # configs[3] at SURVEY a14's recommended head layout: 15 heads of 128 (the D = 128
+    # tcgen05 attention); same GEMMs and FLOPs
+    "gpt-2.2b-h128": dict(layers=48, hidden=1920, heads=15, seq=512, vocab=51200, causal=True, head_rows=0,
+                          b=16, m=4, depth=1),
     # configs[4]: 24-layer GPT (h 1024, V 51200, causal LM head on every position)
     "gpt-24": dict(layers=24, hidden=1024, heads=16, seq=512, vocab=51200, causal=True, head_rows=0,
                    b=8, m=4, depth=1),

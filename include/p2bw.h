@@ -352,6 +352,12 @@ int p2bw_kernel_attention_fwd(const void* qkv, void* o, void* lse, int batch, in
 int p2bw_kernel_attention_bwd(const void* qkv, const void* o, const void* dout, const void* lse,
                               void* dqkv, void* delta, int batch, int seq, int heads, int causal,
                               void* stream);
+/* The same for heads of head_dim = 64 or 128 columns (h = heads * head_dim). */
+int p2bw_kernel_attention_fwd_hd(const void* qkv, void* o, void* lse, int batch, int seq, int heads,
+                                 int head_dim, int causal, void* stream);
+int p2bw_kernel_attention_bwd_hd(const void* qkv, const void* o, const void* dout, const void* lse,
+                                 void* dqkv, void* delta, int batch, int seq, int heads, int head_dim,
+                                 int causal, void* stream);
 /* LayerNorm forward / backward (bf16 rows, fp32 stats and parameter gradients). */
 int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void* y, void* mean,
                               void* rstd, int rows, int h, void* stream);

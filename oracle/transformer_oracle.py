@@ -5,7 +5,8 @@ GELU / CE is unpinned), so this oracle fixes the math the B200 engine
 implements and checks it with torch CPU autograd in float64:
 
   pre-LN GPT-2 / BERT block, LayerNorm eps 1e-5, tanh-GELU, softmax attention
-  with head dim 64 and scale 1/8 (causal mask for GPT), token + position
+  with head dim hidden / heads (64 or 128) and scale 1/sqrt(head dim) (causal mask
+  for GPT), token + position
   embedding on stage 0, LNf + untied LM head + mean cross-entropy over the
   head rows (every position, or `head_rows` evenly spaced positions per
   sequence) on the last stage.
@@ -150,10 +151,11 @@ def loss_fn(P: dict, ids: torch.Tensor, targets: torch.Tensor, spec: Spec) -> to
         xn = torch.nn.functional.layer_norm(x, (h,), P[f"{l}.ln1g"], P[f"{l}.ln1b"], 1e-5)
         qkv = xn @ P[f"{l}.wqkv"].T + P[f"{l}.bqkv"]
         q, k, v = qkv.split(h, dim=1)
-        q = q.reshape(b, s, nh, 64).transpose(1, 2)
-        k = k.reshape(b, s, nh, 64).transpose(1, 2)
-        v = v.reshape(b, s, nh, 64).transpose(1, 2)
-        sc = (q @ k.transpose(-1, -2)) * 0.125
+        hd = h // nh
+        q = q.reshape(b, s, nh, hd).transpose(1, 2)
+        k = k.reshape(b, s, nh, hd).transpose(1, 2)
+        v = v.reshape(b, s, nh, hd).transpose(1, 2)
+        sc = (q @ k.transpose(-1, -2)) * hd ** -0.5
         if spec.causal:
             mask = torch.triu(torch.ones(s, s, dtype=torch.bool), 1)
             sc = sc.masked_fill(mask, float("-inf"))

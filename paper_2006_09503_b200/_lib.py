@@ -105,6 +105,8 @@ def _signatures():
         ("p2bw_kernel_gemm_bf16", i, [vp, ll, i, vp, ll, i, i, i, i, C.POINTER(GemmEpilogue), vp]),
         ("p2bw_kernel_attention_fwd", i, [vp, vp, vp, i, i, i, i, vp]),
         ("p2bw_kernel_attention_bwd", i, [vp, vp, vp, vp, vp, vp, i, i, i, i, vp]),
+        ("p2bw_kernel_attention_fwd_hd", i, [vp, vp, vp, i, i, i, i, i, vp]),
+        ("p2bw_kernel_attention_bwd_hd", i, [vp, vp, vp, vp, vp, vp, i, i, i, i, i, vp]),
         ("p2bw_kernel_layernorm_fwd", i, [vp, vp, vp, vp, vp, vp, i, i, vp]),
         ("p2bw_kernel_layernorm_bwd", i, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp]),
         ("p2bw_kernel_softmax_xent", i, [vp, vp, i, i, i, C.c_float, vp, vp]),

@@ -9,7 +9,8 @@
 namespace p2bw {
 namespace {
 
-void check_shape(int seq, int heads) {
+void check_shape(int seq, int heads, int head_dim) {
+    if (head_dim != 64 && head_dim != 128) throw Error("attention: head dim must be 64 or 128");
     if (!attention_tc_supported(seq))
         throw Error("attention: sequence length " + std::to_string(seq) +
                     " is not a positive multiple of 128 (the tcgen05 query / key tiles)");
@@ -21,24 +22,24 @@ void check_shape(int seq, int heads) {
 bool attention_tc_supported(int seq) { return seq >= 128 && seq % 128 == 0; }
 
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
-                   cudaStream_t s) {
-    check_shape(seq, heads);
-    const double flops = 4.0 * batch * heads * 64.0 * seq * seq * (causal ? 0.5 : 1.0);
-    prof::Scope scope("attention_fwd", flops, 2.0 * batch * seq * heads * 64.0 * 4, 1, s);
-    attention_fwd_tc(qkv, o, lse, batch, seq, heads, causal, s);
+                   cudaStream_t s, int head_dim) {
+    check_shape(seq, heads, head_dim);
+    const double flops = 4.0 * batch * heads * head_dim * seq * seq * (causal ? 0.5 : 1.0);
+    prof::Scope scope("attention_fwd", flops, 2.0 * batch * seq * heads * head_dim * 4.0, 1, s);
+    attention_fwd_tc(qkv, o, lse, batch, seq, heads, causal, s, head_dim);
 }
 
-size_t attention_bwd_scratch_floats(int batch, int seq, int heads) {
-    check_shape(seq, heads);
-    return attention_bwd_tc_scratch_floats(batch, seq, heads);
+size_t attention_bwd_scratch_floats(int batch, int seq, int heads, int head_dim) {
+    check_shape(seq, heads, head_dim);
+    return attention_bwd_tc_scratch_floats(batch, seq, heads, head_dim);
 }
 
 void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
-                   float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s) {
-    check_shape(seq, heads);
-    const double flops = 8.0 * batch * heads * 64.0 * seq * seq * (causal ? 0.5 : 1.0);
-    prof::Scope scope("attention_bwd", flops, 2.0 * batch * seq * heads * 64.0 * 8, 3, s);
-    attention_bwd_tc(qkv, o, dout, lse, dqkv, delta, scratch, batch, seq, heads, causal, s);
+                   float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s, int head_dim) {
+    check_shape(seq, heads, head_dim);
+    const double flops = 8.0 * batch * heads * head_dim * seq * seq * (causal ? 0.5 : 1.0);
+    prof::Scope scope("attention_bwd", flops, 2.0 * batch * seq * heads * head_dim * 8.0, 3, s);
+    attention_bwd_tc(qkv, o, dout, lse, dqkv, delta, scratch, batch, seq, heads, causal, s, head_dim);
 }
 
 }  // namespace p2bw

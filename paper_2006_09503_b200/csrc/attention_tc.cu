@@ -1,4 +1,4 @@
-// Softmax attention forward on tcgen05 tensor cores (head dim 64, seq % 128 == 0).
+// Softmax attention forward on tcgen05 tensor cores (head dim 64 or 128, seq % 128 == 0).
 //
 // Persistent: one CTA per SM walks a stream of work units (sequence, head, 128-query
 // tile), causal units longest first.  Key blocks are 128 wide and S is double-buffered in
@@ -76,6 +76,27 @@ constexpr float kRescale = 8.0f;  // lazy rescale threshold (log2 units): P <= 2
 // so a unit's epilogue runs after the next unit's first block instead of stalling on its
 // last PV
 constexpr uint32_t tO = 256;
+
+// Head-dim-dependent layout of the key-quarter kernel (head dim 64 or 128).  A 128-row
+// tile of D columns is D / 64 TMA boxes of 64 columns (128 B, SW128), kTile apart.
+// D = 128: O takes all 128 columns of each of its two TMEM buffers (S / P 0-255, O
+// 256-511) and only two K / V stages fit next to the double-buffered Q.
+template <int D>
+struct FL {
+    static constexpr int kBoxes = D / 64;
+    static constexpr int kTileD = kTile * kBoxes;
+    static constexpr int kNS = D == 64 ? 4 : 2;
+    static constexpr int oQ = 0, oK = 2 * kTileD, oV = oK + kNS * kTileD, oXch = oV + kNS * kTileD;
+    static constexpr int oXl = oXch + 2 * kKq * kT * 4;
+    static constexpr int oBar = oXl + kKq * kT * 4;
+    static constexpr int bQFull = 0, bQEmpty = 2, bKvFull = 4, bKvEmpty = 4 + kNS, bSFull = 4 + 2 * kNS,
+                         bPFull = bSFull + 2, bOFull = bPFull + 2, bOEmpty = bPFull + 4, kNumBars = bPFull + 6;
+    static constexpr int kSmem = oBar + kNumBars * 8 + 16 + 1024;
+    static constexpr int kOq = D / kKq;  // O columns per key-quarter warp
+    static constexpr float kScale = D == 64 ? 0.125f : 0.08838834764831845f;  // 1 / sqrt(D)
+};
+static_assert(FL<64>::kSmem == kSmem, "head-dim-64 layout unchanged");
+static_assert(FL<128>::kSmem <= 227 * 1024, "head-dim-128 layout fits in SMEM");
 
 struct Unit {
     int bh, qt, n;  // (sequence, head), query tile, key blocks
@@ -182,10 +203,16 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-template <bool kCausal>
+template <bool kCausal, int D>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int seq,
                   int heads, int bhn) {
+    using L = FL<D>;
+    constexpr int kD = D, kTileD = L::kTileD, kNS = L::kNS, kOq = L::kOq;
+    constexpr int oQ = L::oQ, oK = L::oK, oV = L::oV, oXch = L::oXch, oXl = L::oXl, oBar = L::oBar;
+    constexpr int bQFull = L::bQFull, bQEmpty = L::bQEmpty, bKvFull = L::bKvFull, bKvEmpty = L::bKvEmpty,
+                  bSFull = L::bSFull, bPFull = L::bPFull, bOFull = L::bOFull, bOEmpty = L::bOEmpty,
+                  kNumBars = L::kNumBars;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -220,14 +247,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row0 = (un.bh / heads) * seq, hd = un.bh % heads;
             const int qb = qc & 1;
             ptx::mbar_wait(&bar[bQEmpty + qb], ((qc >> 1) & 1) ^ 1);
-            ptx::mbar_arrive_expect_tx(&bar[bQFull + qb], kTile);
-            ptx::tma_load_2d(smem + oQ + qb * kTile, &tm, &bar[bQFull + qb], hd * kD, row0 + un.qt * kT);
+            ptx::mbar_arrive_expect_tx(&bar[bQFull + qb], kTileD);
+#pragma unroll
+            for (int x = 0; x < L::kBoxes; ++x)
+                ptx::tma_load_2d(smem + oQ + qb * kTileD + x * kTile, &tm, &bar[bQFull + qb], hd * kD + 64 * x,
+                                 row0 + un.qt * kT);
             for (int j = 0; j < un.n; ++j, ++kc) {
                 const int st = kc % kNS;
                 ptx::mbar_wait(&bar[bKvEmpty + st], ((kc / kNS) & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(&bar[bKvFull + st], 2 * kTile);
-                ptx::tma_load_2d(smem + oK + st * kTile, &tm, &bar[bKvFull + st], h + hd * kD, row0 + j * kT);
-                ptx::tma_load_2d(smem + oV + st * kTile, &tm, &bar[bKvFull + st], 2 * h + hd * kD, row0 + j * kT);
+                ptx::mbar_arrive_expect_tx(&bar[bKvFull + st], 2 * kTileD);
+#pragma unroll
+                for (int x = 0; x < L::kBoxes; ++x) {
+                    ptx::tma_load_2d(smem + oK + st * kTileD + x * kTile, &tm, &bar[bKvFull + st],
+                                     h + hd * kD + 64 * x, row0 + j * kT);
+                    ptx::tma_load_2d(smem + oV + st * kTileD + x * kTile, &tm, &bar[bKvFull + st],
+                                     2 * h + hd * kD + 64 * x, row0 + j * kT);
+                }
             }
         }
     } else if (warp == 1 && lane == 0) {
@@ -244,12 +279,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int st = sg % kNS;
             ptx::mbar_wait(&bar[bKvFull + st], (sg / kNS) & 1);
             ptx::tc_fence_after();
-            const uint32_t q_addr = sbase + oQ + (sq & 1) * kTile, k_addr = sbase + oK + st * kTile;
+            const uint32_t q_addr = sbase + oQ + (sq & 1) * kTileD, k_addr = sbase + oK + st * kTileD;
             const uint32_t dst = tmem + (sg & 1) * 128;
 #pragma unroll
-            for (int kk = 0; kk < kD / 16; ++kk)
-                ptx::umma_bf16(dst, ptx::sdesc_sw128(q_addr + kk * 32, 16, 1024),
-                               ptx::sdesc_sw128(k_addr + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < kD / 16; ++kk) {
+                const uint32_t off = (kk / 4) * kTile + (kk % 4) * 32;  // box kk / 4, 16 columns per step
+                ptx::umma_bf16(dst, ptx::sdesc_sw128(q_addr + off, 16, 1024),
+                               ptx::sdesc_sw128(k_addr + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+            }
             ptx::umma_commit(&bar[bSFull + (sg & 1)]);
             fmark(0, sg);
             sg += 1;
@@ -271,11 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (pj == 0 && pq > 1) ptx::mbar_wait(&bar[bOEmpty + ob], ((pq - 2) >> 1) & 1);  // O of unit pq - 2 read
             ptx::tc_fence_after();
             const int st = g % kNS;
-            const uint32_t v_addr = sbase + oV + st * kTile;
+            const uint32_t v_addr = sbase + oV + st * kTileD;
             const uint32_t pa = tmem + (g & 1) * 128;
+            // V MN-major: its 64-column boxes are the MN groups (LBO), 16 keys per step
+            constexpr uint32_t v_lbo = kD == 64 ? 8192 : kTile;
 #pragma unroll
             for (int kk = 0; kk < kT / 16; ++kk)
-                ptx::umma_bf16_ts(tmem + tO + ob * 128, pa + kk * 8, ptx::sdesc_sw128(v_addr + kk * 2048, 8192, 1024),
+                ptx::umma_bf16_ts(tmem + tO + ob * 128, pa + kk * 8, ptx::sdesc_sw128(v_addr + kk * 2048, v_lbo, 1024),
                                   id_pv, (pj | kk) != 0 ? 1u : 0u);
             ptx::umma_commit(&bar[bKvEmpty + st]);  // also: PV_g complete (the softmax's O rescale)
             fmark(7, g);
@@ -294,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qw = warp & 3, kq = (warp - 4) >> 2;
         const int r = qw * 32 + lane;  // query row within the unit's tile
         const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
-        const float sc = 0.125f * kLog2e;
+        const float sc = L::kScale * kLog2e;
         const bool mk = warp == 4 && lane == 0;
         // epilogue of unit (count pc, tile un, max m): O / l (bf16) and lse; O is released as
         // soon as it is in registers
@@ -305,8 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             xl[kq * kT + r] = lq;  // the row sum from the four key quarters' partials
             ptx::mbar_wait(&bar[bOFull + ob], (pc >> 1) & 1);
             ptx::tc_fence_after();
-            uint32_t o[16];
-            ptx::tmem_ld_32x32b_x16(ot + kq * 16, o);
+            uint32_t o[kOq];
+            if constexpr (kOq == 16) ptx::tmem_ld_32x32b_x16(ot + kq * kOq, o);
+            else ptx::tmem_ld_32x32b_x32(ot + kq * kOq, o);
             ptx::tmem_ld_wait();
             ptx::tc_fence_before();
             __syncwarp();
@@ -316,9 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar(5 + qw, 32 * kKq);  // read before the next epilogue writes
             const float inv = 1.0f / l;
             const int i = un.qt * kT + r;
-            bf16* orow = out + static_cast<size_t>((un.bh / heads) * seq + i) * h + (un.bh % heads) * kD + kq * 16;
+            bf16* orow = out + static_cast<size_t>((un.bh / heads) * seq + i) * h + (un.bh % heads) * kD + kq * kOq;
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
+            for (int q = 0; q < kOq / 8; ++q)
                 *reinterpret_cast<uint4*>(orow + 8 * q) = make_uint4(
                     ptx::pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
                     ptx::pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
@@ -371,12 +411,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // of that barrier needs P_{g+kNS-1}, so its phase cannot have moved on)
                     ptx::mbar_wait(&bar[bKvEmpty + (g - 1) % kNS], ((g - 1) / kNS) & 1);
                     ptx::tc_fence_after();
-                    uint32_t o[16];
-                    ptx::tmem_ld_32x32b_x16(ot + kq * 16, o);
+                    uint32_t o[kOq];
+                    if constexpr (kOq == 16) ptx::tmem_ld_32x32b_x16(ot + kq * kOq, o);
+                    else ptx::tmem_ld_32x32b_x32(ot + kq * kOq, o);
                     ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-                    ptx::tmem_st_32x32b_x16(ot + kq * 16, o);
+                    for (int e = 0; e < kOq; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                    if constexpr (kOq == 16) ptx::tmem_st_32x32b_x16(ot + kq * kOq, o);
+                    else ptx::tmem_st_32x32b_x32(ot + kq * kOq, o);
                 }
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
@@ -724,16 +766,33 @@ __global__ void __launch_bounds__(f2::kThreads, 1)
 }
 
 // One attribute call per (instantiation, device).
-template <bool kCausal>
+template <bool kCausal, int D>
 void set_smem_once() {
     static std::atomic<uint32_t> done{0};
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const uint32_t bit = 1u << (dev & 31);
     if (done.load() & bit) return;
-    check_cuda(cudaFuncSetAttribute(k_attn_fwd_tc<kCausal>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem),
+    check_cuda(cudaFuncSetAttribute(k_attn_fwd_tc<kCausal, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    FL<D>::kSmem),
                "cudaFuncSetAttribute(k_attn_fwd_tc)");
     done.fetch_or(bit);
+}
+
+template <int D>
+void launch_key_quarter(const CUtensorMap& tm, bf16* o, float* lse, int seq, int heads, int bhn, bool causal,
+                        cudaStream_t s) {
+    const int units = bhn * (seq / kT);
+    const int grid = std::max(1, std::min(num_sms(), units));
+    if (causal) {
+        set_smem_once<true, D>();
+        launch_pdl(k_attn_fwd_tc<true, D>, dim3(grid), dim3(kThreads), FL<D>::kSmem, s, "k_attn_fwd_tc", tm, o, lse,
+                   seq, heads, bhn);
+    } else {
+        set_smem_once<false, D>();
+        launch_pdl(k_attn_fwd_tc<false, D>, dim3(grid), dim3(kThreads), FL<D>::kSmem, s, "k_attn_fwd_tc", tm, o, lse,
+                   seq, heads, bhn);
+    }
 }
 
 }  // namespace
@@ -743,11 +802,16 @@ void attention_debug_timing(unsigned long long* dev_buf) {
 }
 
 void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
-                      cudaStream_t s) {
-    const int h = heads * kD;
+                      cudaStream_t s, int head_dim) {
+    const int h = heads * head_dim;
     const uint64_t rows = static_cast<uint64_t>(batch) * seq;
     const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * h, rows, 3ll * h, 64, kT);
     const int bhn = batch * heads;
+    if (head_dim == 128) {  // the key-quarter kernel at D = 128 (the two-tile kernel's TMEM is D = 64 only)
+        launch_key_quarter<128>(tm, o, lse, seq, heads, bhn, causal, s);
+        check_cuda(cudaGetLastError(), "attention_fwd_tc");
+        return;
+    }
     // Non-causal: the two-tile kernel (BERT-base 39 -> 30 us per call).  Causal: the
     // key-quarter kernel, which stays faster on the causal units' short key ranges (GPT-2.2B
     // 59 us against 63-66 us for the two-tile kernel with either pairing); P2BW_ATTN_FWD=1 / 2
@@ -780,17 +844,7 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
         check_cuda(cudaGetLastError(), "attention_fwd_tc");
         return;
     }
-    const int units = bhn * (seq / kT);
-    const int grid = std::max(1, std::min(num_sms(), units));
-    if (causal) {
-        set_smem_once<true>();
-        launch_pdl(k_attn_fwd_tc<true>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_fwd_tc", tm, o, lse, seq, heads,
-                   bhn);
-    } else {
-        set_smem_once<false>();
-        launch_pdl(k_attn_fwd_tc<false>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_fwd_tc", tm, o, lse, seq,
-                   heads, bhn);
-    }
+    launch_key_quarter<64>(tm, o, lse, seq, heads, bhn, causal, s);
     check_cuda(cudaGetLastError(), "attention_fwd_tc");
 }
 

@@ -1,4 +1,4 @@
-// Softmax attention backward on tcgen05 tensor cores (head dim 64, seq % 128 == 0).
+// Softmax attention backward on tcgen05 tensor cores (head dim 64 or 128, seq % 128 == 0).
 // Persistent and key-outer: one CTA per SM walks work items
 // (128-key tile j, sequence, head) -- j-major, so causal items with the most query
 // tiles go first -- and for each item the query tiles i that can see it:
@@ -409,15 +409,298 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---- head dim 128 -----------------------------------------------------------------
+//
+// The same key-outer item walk and operand tricks at D = 128, where the accumulators
+// alone fill TMEM: S^T [0, 128), dP^T [128, 256), dV [256, 384), dK [384, 512).  So
+//   * P^T goes to SMEM (K-major SW128, like dS^T) instead of TMEM, and
+//   * dQ_i|j = dS K_j reuses the S^T columns once the elementwise warps have read S^T:
+//     the next tile's S^T / dP^T wait for the dQ flush (no S/dP-ahead-of-mm2 overlap).
+// SMEM: K, V (one item) and Q, dO (one query tile) of 32 KB each, P^T and dS^T 32 KB,
+// dQ staging 16 KB: ~209 KB.  Numerics as at D = 64 (scale 1 / sqrt(128)).
+namespace d128 {
+constexpr int kD = 128;
+constexpr int kTileD = 2 * kTile;  // 128 rows x 128 bf16: two 64-column boxes kTile apart
+constexpr int oK = 0, oV = oK + kTileD, oQ = oV + kTileD, oDO = oQ + kTileD, oPT = oDO + kTileD,
+              oDSt = oPT + kTileD, oDQ = oDSt + kTileD, oLse = oDQ + 4 * 4096, oDel = oLse + kT * 4,
+              oBar = oDel + kT * 4;
+constexpr int bKvFull = 0, bKvEmpty = 1, bQFull = 2, bQEmpty = 3, bSdpFull = 4, bPdsFull = 5, bMm2 = 6,
+              bDqFree = 7, bKvAccFree = 8, kNumBars = 9;
+constexpr int kSmem = oBar + 256 + 1024;
+static_assert(kSmem <= 227 * 1024, "D = 128 backward SMEM");
+constexpr uint32_t tS = 0, tDP = 128, tDV = 256, tDK = 384, tDQ = 0;
+constexpr float kScale = 0.08838834764831845f;  // 1 / sqrt(128)
+}  // namespace d128
+
+template <bool kCausal>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_attn_bwd_tc128(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                     const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ nl2,
+                     const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int heads, int bhn) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = ptx::smem_u32(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + d128::oBar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + d128::kNumBars);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nq = seq / kT;
+    const int items = bhn * nq;
+    const int h = heads * d128::kD;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tm_qkv);
+        ptx::tma_prefetch_desc(&tm_do);
+        ptx::tma_prefetch_desc(&tm_dq);
+        for (int q = 0; q < d128::kNumBars; ++q)
+            ptx::mbar_init(&bar[q], q == d128::bPdsFull ? kElemWarps : (q == d128::bDqFree || q == d128::bKvAccFree) ? 4 : 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            int ln = 0, g = 0;
+            for (int n = blockIdx.x; n < items; n += gridDim.x, ++ln) {
+                const Item it = item_of(n, bhn, nq, kCausal);
+                const int b = it.bh / heads, hd = it.bh % heads, row0 = b * seq;
+                ptx::mbar_wait(&bar[d128::bKvEmpty], (ln & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&bar[d128::bKvFull], 2 * d128::kTileD);
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    ptx::tma_load_2d(smem + d128::oK + x * kTile, &tm_qkv, &bar[d128::bKvFull], h + hd * d128::kD + 64 * x,
+                                     row0 + it.j * kT);
+                    ptx::tma_load_2d(smem + d128::oV + x * kTile, &tm_qkv, &bar[d128::bKvFull], 2 * h + hd * d128::kD + 64 * x,
+                                     row0 + it.j * kT);
+                }
+                for (int t = 0; t < it.iters; ++t, ++g) {
+                    const int i = it.i0 + t;
+                    ptx::mbar_wait(&bar[d128::bQEmpty], (g & 1) ^ 1);
+                    uint64_t* full = &bar[d128::bQFull];
+                    ptx::mbar_arrive_expect_tx(full, 2 * d128::kTileD + 2 * kT * 4);
+#pragma unroll
+                    for (int x = 0; x < 2; ++x) {
+                        ptx::tma_load_2d(smem + d128::oQ + x * kTile, &tm_qkv, full, hd * d128::kD + 64 * x, row0 + i * kT);
+                        ptx::tma_load_2d(smem + d128::oDO + x * kTile, &tm_do, full, hd * d128::kD + 64 * x, row0 + i * kT);
+                    }
+                    const size_t so = static_cast<size_t>(it.bh) * seq + i * kT;
+                    bulk_load(sbase + d128::oLse, nl2 + so, kT * 4, full);
+                    bulk_load(sbase + d128::oDel, delta + so, kT * 4, full);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t id_sq = ptx::idesc_bf16(128, 128, false, false);  // S^T, dP^T (K = d)
+            constexpr uint32_t id_kv = ptx::idesc_bf16(128, 128, false, true);   // dV, dK: B MN-major
+            constexpr uint32_t id_q = ptx::idesc_bf16(128, 128, true, true);     // dQ: A and B MN-major
+            const uint32_t aK = sbase + d128::oK, aV = sbase + d128::oV, aQ = sbase + d128::oQ, aDO = sbase + d128::oDO;
+            const uint32_t aPT = sbase + d128::oPT, aDSt = sbase + d128::oDSt;
+            int ln = 0, g = 0;
+            for (int n = blockIdx.x; n < items; n += gridDim.x, ++ln) {
+                const Item it = item_of(n, bhn, nq, kCausal);
+                ptx::mbar_wait(&bar[d128::bKvFull], ln & 1);
+                for (int t = 0; t < it.iters; ++t, ++g) {
+                    ptx::mbar_wait(&bar[d128::bQFull], g & 1);
+                    if (g > 0) ptx::mbar_wait(&bar[d128::bDqFree], (g - 1) & 1);  // S^T columns (dQ) flushed
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < d128::kD / 16; ++kk) {
+                        const uint32_t off = (kk / 4) * kTile + (kk % 4) * 32;  // K-major over d
+                        ptx::umma_bf16(tmem + d128::tS, ptx::sdesc_sw128(aK + off, 16, 1024),
+                                       ptx::sdesc_sw128(aQ + off, 16, 1024), id_sq, kk > 0);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < d128::kD / 16; ++kk) {
+                        const uint32_t off = (kk / 4) * kTile + (kk % 4) * 32;
+                        ptx::umma_bf16(tmem + d128::tDP, ptx::sdesc_sw128(aV + off, 16, 1024),
+                                       ptx::sdesc_sw128(aDO + off, 16, 1024), id_sq, kk > 0);
+                    }
+                    ptx::umma_commit(&bar[d128::bSdpFull]);
+                    ptx::mbar_wait(&bar[d128::bPdsFull], g & 1);
+                    if (t == 0 && ln > 0) ptx::mbar_wait(&bar[d128::bKvAccFree], (ln - 1) & 1);
+                    ptx::tc_fence_after();
+                    const bool first = t == 0;
+#pragma unroll
+                    for (int kk = 0; kk < kT / 16; ++kk) {
+                        const uint32_t a_off = (kk / 4) * kTile + (kk % 4) * 32;  // K-major, 16 queries per step
+                        const uint32_t b_off = kk * 2048;                         // MN-major, 16 rows per step
+                        const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+                        ptx::umma_bf16(tmem + d128::tDV, ptx::sdesc_sw128(aPT + a_off, 16, 1024),
+                                       ptx::sdesc_sw128(aDO + b_off, kTile, 1024), id_kv, acc);
+                        ptx::umma_bf16(tmem + d128::tDK, ptx::sdesc_sw128(aDSt + a_off, 16, 1024),
+                                       ptx::sdesc_sw128(aQ + b_off, kTile, 1024), id_kv, acc);
+                        ptx::umma_bf16(tmem + d128::tDQ, ptx::sdesc_sw128(aDSt + b_off, kTile, 1024),
+                                       ptx::sdesc_sw128(aK + b_off, kTile, 1024), id_q, kk > 0 ? 1u : 0u);
+                    }
+                    ptx::umma_commit(&bar[d128::bMm2]);
+                    ptx::umma_commit(&bar[d128::bQEmpty]);
+                    if (t == it.iters - 1) ptx::umma_commit(&bar[d128::bKvEmpty]);
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 4 + kElemWarps) {
+        // ---------------- elementwise: P^T, dS^T -> SMEM ----------------
+        const int qw = warp & 3;
+        const int sel = (warp - 4) >> 2;  // query columns [32 sel, 32 sel + 32)
+        const int r = qw * 32 + lane;     // key row within the tile
+        const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+        const float sc = d128::kScale * kLog2e;
+        const uint32_t prow = sbase + d128::oPT + (sel >> 1) * kTile + r * 128;
+        const uint32_t drow = sbase + d128::oDSt + (sel >> 1) * kTile + r * 128;
+        int g = 0;
+        for (int n = blockIdx.x; n < items; n += gridDim.x) {
+            const Item it = item_of(n, bhn, nq, kCausal);
+            const int key = it.j * kT + r;
+            for (int t = 0; t < it.iters; ++t, ++g) {
+                const int i = it.i0 + t;
+                ptx::mbar_wait(&bar[d128::bSdpFull], g & 1);
+                ptx::mbar_wait(&bar[d128::bQFull], g & 1);  // lse / delta visible
+                ptx::tc_fence_after();
+                uint32_t pp[16], dd[16];
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int col0 = sel * 32 + c * 16;
+                    uint32_t sv[16], dv[16];
+                    ptx::tmem_ld_32x32b_x16(trow + d128::tS + col0, sv);
+                    ptx::tmem_ld_32x32b_x16(trow + d128::tDP + col0, dv);
+                    ptx::tmem_ld_wait();
+                    const uint32_t la = sbase + d128::oLse + col0 * 4, da = sbase + d128::oDel + col0 * 4;
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 l4 = ptx::lds_f4(la + q4 * 16);
+                        const float4 d4 = ptx::lds_f4(da + q4 * 16);
+                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
+                        float p[4], ds[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int q = q4 * 4 + e;
+                            float x = ptx::ex2(fmaf(__uint_as_float(sv[q]), sc, lv[e]));
+                            if (kCausal && i * kT + col0 + q < key) x = 0.0f;
+                            p[e] = x;
+                            ds[e] = x * (__uint_as_float(dv[q]) - dl[e]);
+                        }
+                        pp[c * 8 + q4 * 2] = ptx::pack_bf16x2(p[0], p[1]);
+                        pp[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(p[2], p[3]);
+                        dd[c * 8 + q4 * 2] = ptx::pack_bf16x2(ds[0], ds[1]);
+                        dd[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(ds[2], ds[3]);
+                    }
+                }
+                if (g > 0) ptx::mbar_wait(&bar[d128::bMm2], (g - 1) & 1);  // P^T / dS^T buffers free
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    const int cc = (sel & 1) * 4 + ch;  // 16-byte chunk of the 128-byte row
+                    const uint32_t off = static_cast<uint32_t>((cc ^ (r & 7)) << 4);
+                    ptx::sts_u4(prow + off, pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]);
+                    ptx::sts_u4(drow + off, dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]);
+                }
+                ptx::fence_proxy_async();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bar[d128::bPdsFull]);
+            }
+        }
+    } else if (warp >= 4 + kElemWarps) {
+        // ---------------- dQ flush (TMA reduce-add) + dK / dV epilogue ----------------
+        const int qw = warp & 3;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+        uint8_t* stage = smem + d128::oDQ + qw * 4096;
+        const uint32_t sstage = ptx::smem_u32(stage);
+        int g = 0;
+        for (int n = blockIdx.x; n < items; n += gridDim.x) {
+            const Item it = item_of(n, bhn, nq, kCausal);
+            const int b = it.bh / heads, hd = it.bh % heads, row0 = b * seq;
+            for (int t = 0; t < it.iters; ++t, ++g) {
+                const int i = it.i0 + t;
+                ptx::mbar_wait(&bar[d128::bMm2], g & 1);
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int q = 0; q < 4; ++q) {  // 32 columns at a time (768 threads: ~80 registers each)
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(trow + d128::tDQ + q * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (q == 3) {  // the S^T columns may take the next tile's S^T
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&bar[d128::bDqFree]);
+                    }
+                    if (lane == 0) ptx::bulk_wait_read<0>();  // staging buffer read out by the last reduce
+                    __syncwarp();
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        ptx::sts_f4(sstage + ptx::swz128(lane, c), __uint_as_float(v[4 * c]),
+                                    __uint_as_float(v[4 * c + 1]), __uint_as_float(v[4 * c + 2]),
+                                    __uint_as_float(v[4 * c + 3]));
+                    ptx::fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_reduce_add_2d(&tm_dq, stage, hd * d128::kD + q * 32, row0 + i * kT + qw * 32);
+                        ptx::bulk_commit();
+                    }
+                }
+                if (t == it.iters - 1) {
+                    // dK (x 1/sqrt(128)) and dV of key row qw*32 + lane of tile j
+                    const int key = it.j * kT + qw * 32 + lane;
+                    bf16* dk = dqkv + static_cast<size_t>(row0 + key) * 3 * h + h + hd * d128::kD;
+                    bf16* dv = dk + h;
+#pragma unroll 1
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t vk[32], vv[32];
+                        ptx::tmem_ld_32x32b_x32(trow + d128::tDK + q * 32, vk);
+                        ptx::tmem_ld_32x32b_x32(trow + d128::tDV + q * 32, vv);
+                        ptx::tmem_ld_wait();
+                        if (q == 3) {
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(&bar[d128::bKvAccFree]);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 32; c += 8) {
+                            uint32_t wk[4], wv[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                wk[e] = ptx::pack_bf16x2(__uint_as_float(vk[c + 2 * e]) * d128::kScale,
+                                                         __uint_as_float(vk[c + 2 * e + 1]) * d128::kScale);
+                                wv[e] = ptx::pack_bf16x2(__uint_as_float(vv[c + 2 * e]),
+                                                         __uint_as_float(vv[c + 2 * e + 1]));
+                            }
+                            *reinterpret_cast<uint4*>(dk + q * 32 + c) = make_uint4(wk[0], wk[1], wk[2], wk[3]);
+                            *reinterpret_cast<uint4*>(dv + q * 32 + c) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                        }
+                    }
+                }
+            }
+        }
+        if (lane == 0) ptx::bulk_wait<0>();
+        __syncwarp();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
 // delta[bh, i] = sum_d dO[t, hd*64+d] * O[t, hd*64+d] and nl2 = -lse log2(e); also
 // zeroes the fp32 dQ accumulator slice of (t, hd).  Eight threads per (token, head).
+template <int D>
 __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
                              float* __restrict__ delta, float* __restrict__ nl2, float* __restrict__ dq_acc, int tokens,
                              int seq, int heads) {
+    constexpr int kD = D, kSub = D / 8;  // threads per (token, head), 8 elements each
     ptx::pdl_trigger();
     ptx::pdl_wait();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int pair = idx >> 3, sub = idx & 7;
+    const int pair = idx / kSub, sub = idx % kSub;
     const bool ok = pair < tokens * heads;  // no early return: the shuffles below need every lane
     const int t = ok ? pair / heads : 0, hd = ok ? pair % heads : 0;
     const int h = heads * kD;
@@ -432,9 +715,8 @@ __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict_
         const float2 fa = ptx::unpack_bf16x2(aw[e]), fd = ptx::unpack_bf16x2(dw[e]);
         acc = fmaf(fa.x, fd.x, fmaf(fa.y, fd.y, acc));
     }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+#pragma unroll
+    for (int w = 1; w < kSub; w *= 2) acc += __shfl_xor_sync(0xffffffffu, acc, w);
     if (!ok) return;
     float4* z = reinterpret_cast<float4*>(dq_acc + off);
     z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -447,8 +729,10 @@ __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict_
     }
 }
 
-// dq (bf16, x 1/8) = the fp32 accumulator.
+// dq (bf16, x 1/sqrt(D)) = the fp32 accumulator.
+template <int D>
 __global__ void k_attn_dq_convert(const float* __restrict__ acc, bf16* __restrict__ dqkv, int tokens, int h) {
+    constexpr float kSc = D == 64 ? 0.125f : d128::kScale;
     ptx::pdl_trigger();
     ptx::pdl_wait();
     const size_t total = static_cast<size_t>(tokens) * h / 8;
@@ -459,20 +743,20 @@ __global__ void k_attn_dq_convert(const float* __restrict__ acc, bf16* __restric
         const float4 x = *reinterpret_cast<const float4*>(acc + e);
         const float4 y = *reinterpret_cast<const float4*>(acc + e + 4);
         *reinterpret_cast<uint4*>(dqkv + static_cast<size_t>(t) * 3 * h + c) =
-            make_uint4(ptx::pack_bf16x2(x.x * 0.125f, x.y * 0.125f), ptx::pack_bf16x2(x.z * 0.125f, x.w * 0.125f),
-                       ptx::pack_bf16x2(y.x * 0.125f, y.y * 0.125f), ptx::pack_bf16x2(y.z * 0.125f, y.w * 0.125f));
+            make_uint4(ptx::pack_bf16x2(x.x * kSc, x.y * kSc), ptx::pack_bf16x2(x.z * kSc, x.w * kSc),
+                       ptx::pack_bf16x2(y.x * kSc, y.y * kSc), ptx::pack_bf16x2(y.z * kSc, y.w * kSc));
     }
 }
 
-// One attribute call per (instantiation, device).
-template <bool kCausal>
-void set_smem_once() {
+// One attribute call per (kernel, device); Tag tells apart kernels of the same type.
+template <int Tag, typename K>
+void set_smem_once(K kern, int bytes) {
     static std::atomic<uint32_t> done{0};
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const uint32_t bit = 1u << (dev & 31);
     if (done.load() & bit) return;
-    check_cuda(cudaFuncSetAttribute(k_attn_bwd_tc<kCausal>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem),
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                "cudaFuncSetAttribute(k_attn_bwd_tc)");
     done.fetch_or(bit);
 }
@@ -483,37 +767,59 @@ void attention_bwd_debug_timing(unsigned long long* dev_buf) {
     check_cuda(cudaMemcpyToSymbol(g_attn_bwd_dbg, &dev_buf, sizeof(dev_buf)), "cudaMemcpyToSymbol(g_attn_bwd_dbg)");
 }
 
-size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads) {
+size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads, int head_dim) {
     // the fp32 dQ accumulator, then -lse log2(e) per (sequence, head, query)
-    return static_cast<size_t>(batch) * seq * heads * kD + static_cast<size_t>(batch) * heads * seq;
+    return static_cast<size_t>(batch) * seq * heads * head_dim + static_cast<size_t>(batch) * heads * seq;
 }
 
 void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
-                      float* dq_acc, int batch, int seq, int heads, bool causal, cudaStream_t s) {
-    const int h = heads * kD;
+                      float* dq_acc, int batch, int seq, int heads, bool causal, cudaStream_t s, int head_dim) {
+    const bool d128 = head_dim == 128;
+    const int h = heads * head_dim;
     const int tokens = batch * seq;
     const int pairs = tokens * heads;
     float* nl2 = dq_acc + static_cast<size_t>(tokens) * h;
-    launch_pdl(k_attn_delta, dim3((pairs * 8 + 255) / 256), dim3(256), 0, s, "k_attn_delta", o, dout, lse, delta, nl2,
-               dq_acc, tokens, seq, heads);
+    const int sub = head_dim / 8;
+    if (d128)
+        launch_pdl(k_attn_delta<128>, dim3((pairs * sub + 255) / 256), dim3(256), 0, s, "k_attn_delta", o, dout, lse,
+                   delta, nl2, dq_acc, tokens, seq, heads);
+    else
+        launch_pdl(k_attn_delta<64>, dim3((pairs * sub + 255) / 256), dim3(256), 0, s, "k_attn_delta", o, dout, lse,
+                   delta, nl2, dq_acc, tokens, seq, heads);
     const CUtensorMap tq = make_tmap_bf16_2d(qkv, 3ull * h, static_cast<uint64_t>(tokens), 3ll * h, 64, kT);
     const CUtensorMap tdo = make_tmap_bf16_2d(dout, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 64, kT);
     const CUtensorMap tdq = make_tmap_f32_2d(dq_acc, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 32, 32);
     const int bhn = batch * heads;
     const int items = bhn * (seq / kT);
     const int grid = std::min(items, num_sms());
-    if (causal) {
-        set_smem_once<true>();
-        launch_pdl(k_attn_bwd_tc<true>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq,
-                   static_cast<const float*>(nl2), static_cast<const float*>(delta), dqkv, dq_acc, seq, heads, bhn);
+    const float* cnl2 = nl2;
+    const float* cdelta = delta;
+    if (d128) {
+        if (causal) {
+            set_smem_once<0>(k_attn_bwd_tc128<true>, d128::kSmem);
+            launch_pdl(k_attn_bwd_tc128<true>, dim3(grid), dim3(kThreads), d128::kSmem, s, "k_attn_bwd_tc", tq, tdo,
+                       tdq, cnl2, cdelta, dqkv, seq, heads, bhn);
+        } else {
+            set_smem_once<1>(k_attn_bwd_tc128<false>, d128::kSmem);
+            launch_pdl(k_attn_bwd_tc128<false>, dim3(grid), dim3(kThreads), d128::kSmem, s, "k_attn_bwd_tc", tq, tdo,
+                       tdq, cnl2, cdelta, dqkv, seq, heads, bhn);
+        }
+    } else if (causal) {
+        set_smem_once<2>(k_attn_bwd_tc<true>, kSmem);
+        launch_pdl(k_attn_bwd_tc<true>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq, cnl2,
+                   cdelta, dqkv, dq_acc, seq, heads, bhn);
     } else {
-        set_smem_once<false>();
-        launch_pdl(k_attn_bwd_tc<false>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq,
-                   static_cast<const float*>(nl2), static_cast<const float*>(delta), dqkv, dq_acc, seq, heads, bhn);
+        set_smem_once<3>(k_attn_bwd_tc<false>, kSmem);
+        launch_pdl(k_attn_bwd_tc<false>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq, cnl2,
+                   cdelta, dqkv, dq_acc, seq, heads, bhn);
     }
     const size_t vecs = static_cast<size_t>(tokens) * h / 8;
-    launch_pdl(k_attn_dq_convert, dim3(static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 16u))), dim3(256),
-               0, s, "k_attn_dq_convert", static_cast<const float*>(dq_acc), dqkv, tokens, h);
+    const dim3 cgrid(static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 16u)));
+    const float* cacc = dq_acc;
+    if (d128)
+        launch_pdl(k_attn_dq_convert<128>, cgrid, dim3(256), 0, s, "k_attn_dq_convert", cacc, dqkv, tokens, h);
+    else
+        launch_pdl(k_attn_dq_convert<64>, cgrid, dim3(256), 0, s, "k_attn_dq_convert", cacc, dqkv, tokens, h);
     check_cuda(cudaGetLastError(), "attention_bwd_tc");
 }
 

@@ -43,25 +43,38 @@ const bf16* cb(const void* p) { return static_cast<const bf16*>(p); }
 bf16* mb(void* p) { return static_cast<bf16*>(p); }
 }  // namespace
 
+extern "C" int p2bw_kernel_attention_fwd_hd(const void* qkv, void* o, void* lse, int batch, int seq, int heads,
+                                            int head_dim, int causal, void* stream) {
+    return guarded([&] {
+        attention_fwd(cb(qkv), mb(o), static_cast<float*>(lse), batch, seq, heads, causal != 0, as_stream(stream),
+                      head_dim);
+    });
+}
+
 extern "C" int p2bw_kernel_attention_fwd(const void* qkv, void* o, void* lse, int batch, int seq, int heads,
                                          int causal, void* stream) {
+    return p2bw_kernel_attention_fwd_hd(qkv, o, lse, batch, seq, heads, 64, causal, stream);
+}
+
+extern "C" int p2bw_kernel_attention_bwd_hd(const void* qkv, const void* o, const void* dout, const void* lse,
+                                            void* dqkv, void* delta, int batch, int seq, int heads, int head_dim,
+                                            int causal, void* stream) {
     return guarded([&] {
-        attention_fwd(cb(qkv), mb(o), static_cast<float*>(lse), batch, seq, heads, causal != 0, as_stream(stream));
+        float* scratch = nullptr;
+        const size_t n = attention_bwd_scratch_floats(batch, seq, heads, head_dim);
+        if (n) check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch), n * sizeof(float), as_stream(stream)),
+                          "cudaMallocAsync");
+        attention_bwd(cb(qkv), cb(o), cb(dout), static_cast<const float*>(lse), mb(dqkv),
+                      static_cast<float*>(delta), scratch, batch, seq, heads, causal != 0, as_stream(stream),
+                      head_dim);
+        if (n) check_cuda(cudaFreeAsync(scratch, as_stream(stream)), "cudaFreeAsync");
     });
 }
 
 extern "C" int p2bw_kernel_attention_bwd(const void* qkv, const void* o, const void* dout, const void* lse,
                                          void* dqkv, void* delta, int batch, int seq, int heads, int causal,
                                          void* stream) {
-    return guarded([&] {
-        float* scratch = nullptr;
-        const size_t n = attention_bwd_scratch_floats(batch, seq, heads);
-        if (n) check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch), n * sizeof(float), as_stream(stream)),
-                          "cudaMallocAsync");
-        attention_bwd(cb(qkv), cb(o), cb(dout), static_cast<const float*>(lse), mb(dqkv),
-                      static_cast<float*>(delta), scratch, batch, seq, heads, causal != 0, as_stream(stream));
-        if (n) check_cuda(cudaFreeAsync(scratch, as_stream(stream)), "cudaFreeAsync");
-    });
+    return p2bw_kernel_attention_bwd_hd(qkv, o, dout, lse, dqkv, delta, batch, seq, heads, 64, causal, stream);
 }
 
 extern "C" int p2bw_kernel_layernorm_fwd(const void* x, const void* g, const void* b, void* y, void* mean,

@@ -45,7 +45,6 @@ int debug_dup(int bit) {
 
 namespace {
 
-constexpr int kHeadDim = 64;
 
 size_t align64(size_t n) { return (n + 63) & ~static_cast<size_t>(63); }
 
@@ -78,8 +77,9 @@ public:
         vocab_ = c.vocab;
         vp_ = static_cast<int>((static_cast<size_t>(vocab_) + 127) / 128 * 128);
         T_ = b_ * seq_;
-        if (h_ <= 0 || heads_ <= 0 || h_ != heads_ * kHeadDim)
-            throw Error("transformer: hidden must equal heads * 64");
+        if (h_ <= 0 || heads_ <= 0 || (h_ != heads_ * 64 && h_ != heads_ * 128))
+            throw Error("transformer: hidden must equal heads * 64 or heads * 128 (head dim 64 / 128)");
+        hd_ = h_ / heads_;
         if (!attention_tc_supported(seq_))
             throw Error("transformer: seq_len must be a positive multiple of 128 (tcgen05 attention tiles)");
         if (b_ < 1 || vocab_ < 2) throw Error("transformer: bad microbatch size or vocab");
@@ -249,7 +249,7 @@ public:
             const LayerOff& o = lay_[l];
             for (int dup_ = 0; dup_ < debug_dup(1); ++dup_) layernorm_fwd(cur, W + o.ln1g, W + o.ln1b, st.xn1[l], st.mean1[l], st.rstd1[l], T_, h_, s);
             for (int dup_ = 0; dup_ < debug_dup(32); ++dup_) gemm_store(st.xn1[l], h_, T_, W + o.wqkv, 3 * h_, h_, st.qkv[l], W + o.bqkv, nullptr, false, nullptr, s);
-            for (int dup_ = 0; dup_ < debug_dup(8); ++dup_) attention_fwd(st.qkv[l], st.o[l], st.lse[l], b_, seq_, heads_, cfg_.causal != 0, s);
+            for (int dup_ = 0; dup_ < debug_dup(8); ++dup_) attention_fwd(st.qkv[l], st.o[l], st.lse[l], b_, seq_, heads_, cfg_.causal != 0, s, hd_);
             gemm_store(st.o[l], h_, T_, W + o.wo, h_, h_, st.x1[l], W + o.bo, cur, false, nullptr, s);
             for (int dup_ = 0; dup_ < debug_dup(1); ++dup_) layernorm_fwd(st.x1[l], W + o.ln2g, W + o.ln2b, st.xn2[l], st.mean2[l], st.rstd2[l], T_, h_, s);
             gemm_store(st.xn2[l], h_, T_, W + o.w1, 4 * h_, h_, st.a[l], W + o.b1, nullptr, true, st.u[l], s);
@@ -343,7 +343,7 @@ public:
             // attention
             wait_side(kEvDoneD, s);  // g3_ free (previous layer's Wqkv / bqkv gradients)
             for (int dup_ = 0; dup_ < debug_dup(16); ++dup_) attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
-                          cfg_.causal != 0, s);
+                          cfg_.causal != 0, s, hd_);
             fork(kEvG3, s);
             // QKV: dxn1 = dqkv Wqkv
             gemm_store_mn_b(g3_, 3 * h_, W + o.wqkv, h_, T_, h_, 3 * h_, gX_, s);
@@ -520,7 +520,7 @@ private:
         g3_ = dalloc<bf16>(T * 3 * h);
         g4_ = dalloc<bf16>(T * 4 * h);
         delta_ = dalloc<float>(stat);
-        attn_scratch_ = dalloc<float>(attention_bwd_scratch_floats(b_, seq_, heads_));
+        attn_scratch_ = dalloc<float>(attention_bwd_scratch_floats(b_, seq_, heads_, hd_));
         if (last_) {
             row_loss_ = dalloc<float>(static_cast<size_t>(R_));
             head_ws_ = dalloc<float>(static_cast<size_t>(R_) * h);
@@ -620,7 +620,7 @@ private:
     int sslots_, wslots_;
     bool recompute_ = false;
     bf16* rc_out_ = nullptr;
-    int h_ = 0, heads_ = 0, seq_ = 0, b_ = 0, vocab_ = 0, vp_ = 0, T_ = 0, R_ = 0, rows_per_seq_ = 0;
+    int h_ = 0, heads_ = 0, hd_ = 64, seq_ = 0, b_ = 0, vocab_ = 0, vp_ = 0, T_ = 0, R_ = 0, rows_per_seq_ = 0;
     cudaStream_t stream_ = nullptr;
     cudaStream_t data_stream_ = nullptr;  // set_data copies (the forward stream), else stream_
     std::vector<void*> allocs_;

@@ -44,9 +44,10 @@ void softmax_xent(bf16* logits, const int* targets, int rows, int vocab, int vp,
 // loss_out = sum(row_loss[0:rows]) * scale  (one block, fixed order)
 void sum_scaled(const float* row_loss, int rows, float scale, float* loss_out, cudaStream_t s);
 
-// Attention over qkv [T x 3h] (q | k | v, heads of 64), output o [T x h], lse [b*nh*seq].
+// Attention over qkv [T x 3h] (q | k | v, heads of head_dim = 64 or 128), output o [T x h],
+// lse [b*nh*seq].
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
-                   cudaStream_t s);
+                   cudaStream_t s, int head_dim = 64);
 // The tcgen05 kernels cover seq % 128 == 0 (attention.cu rejects anything else).
 bool attention_tc_supported(int seq);
 // Debug: per-CTA phase timestamps of the tcgen05 forward into dev_buf[cta * 16 + slot] (null: off).
@@ -54,14 +55,16 @@ void attention_debug_timing(unsigned long long* dev_buf);
 // Debug: phase timestamps of the tcgen05 attention backward (64 per CTA, null: off).
 void attention_bwd_debug_timing(unsigned long long* dev_buf);
 void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, int heads, bool causal,
-                      cudaStream_t s);
-size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads);
+                      cudaStream_t s, int head_dim);
+size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads, int head_dim);
 void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv,
-                      float* delta, float* dq_part, int batch, int seq, int heads, bool causal, cudaStream_t s);
+                      float* delta, float* dq_part, int batch, int seq, int heads, bool causal, cudaStream_t s,
+                      int head_dim);
 // dqkv [T x 3h] from do [T x h]; delta: [b*nh*seq] floats; scratch: attention_bwd_scratch_floats.
-size_t attention_bwd_scratch_floats(int batch, int seq, int heads);
+size_t attention_bwd_scratch_floats(int batch, int seq, int heads, int head_dim = 64);
 void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv,
-                   float* delta, float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s);
+                   float* delta, float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s,
+                   int head_dim = 64);
 
 // Momentum SGD with dampening (semantics.cpp:153-165) on the flat fp32 master:
 //   g = grad / count; v = beta v + (1-beta) g; w -= lr v; out_bf16 = bf16(w)

@@ -103,6 +103,27 @@ def test_bench_width_layers_match_delayed_oracle(depth, layers, batch, hidden, c
         assert err < DELTA_RTOL, (s, err)
 
 
+@pytest.mark.parametrize("depth,layers,batch,hidden,heads,causal,vocab",
+                         [(2, 2, 2, 256, 2, True, 500),
+                          (1, 2, 1, 1920, 15, True, 51200)])  # GPT-2.2B at SURVEY a14's 15 x 128 heads
+def test_head_dim_128_matches_delayed_oracle(depth, layers, batch, hidden, heads, causal, vocab):
+    """Heads of 128 columns through the whole engine (the D = 128 tcgen05 attention
+    forward / backward) against the float64 oracle at the same head layout."""
+    spec = TO.Spec(layers=layers, hidden=hidden, heads=heads, seq=512, vocab=vocab, batch=batch, causal=causal,
+                   head_rows=0)
+    m, T, lr, beta, seed = 2, 3, 0.05, 0.9, 199
+    params, ids, tg, losses, finals, c = run_case(spec, depth, m, T, lr, beta, seed)
+    traj, ref_losses = TO.train(params, spec, ids, tg, lr, beta, m, T, delayed=True)
+    print(f"h {hidden} heads {heads}: max loss rel err {np.max(np.abs(losses - ref_losses) / np.abs(ref_losses)):.2e}")
+    assert np.all(np.abs(losses - ref_losses) <= LOSS_RTOL * np.abs(ref_losses)), (losses, ref_losses)
+    for s in range(depth):
+        w0 = TO.flatten_stage(params, spec, depth, s).astype(np.float64)
+        ref = TO.flatten_stage({k: v.numpy() for k, v in traj[-1].items()}, spec, depth, s).astype(np.float64)
+        err = np.linalg.norm((finals[s] - w0) - (ref - w0)) / np.linalg.norm(ref - w0)
+        print(f"  stage {s}: delta err {err:.4f}")
+        assert err < DELTA_RTOL, (s, err)
+
+
 def test_depths_agree_with_each_other():
     spec = TO.Spec(layers=4, hidden=128, heads=2, seq=128, vocab=300, batch=2, causal=True)
     m, T = 4, 3

@@ -21,10 +21,10 @@ def stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def ref_attention(qkv, b, s, nh, causal):
-    h = nh * 64
-    q, k, v = qkv.float().view(b, s, 3, nh, 64).permute(2, 0, 3, 1, 4)
-    sc = q @ k.transpose(-1, -2) * 0.125
+def ref_attention(qkv, b, s, nh, causal, hd=64):
+    h = nh * hd
+    q, k, v = qkv.float().view(b, s, 3, nh, hd).permute(2, 0, 3, 1, 4)
+    sc = q @ k.transpose(-1, -2) * hd ** -0.5
     if causal:
         sc = sc.masked_fill(torch.triu(torch.ones(s, s, dtype=torch.bool, device=qkv.device), 1), float("-inf"))
     p = torch.softmax(sc, -1)
@@ -67,6 +67,48 @@ def test_attention_fwd_bwd_vs_torch(b, s, nh, causal):
     ref = ref_in.grad
     err = (dqkv.float() - ref).abs().max().item()
     assert err < 3e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("b,s,nh,causal", [(2, 128, 2, True), (2, 128, 1, False), (1, 512, 4, True),
+                                           (3, 384, 2, False), (2, 1024, 3, True),
+                                           # more items than SMs (single-buffered K / V and Q / dO
+                                           # hand-offs across items), and GPT-2.2B at 15 x 128 heads
+                                           (16, 512, 8, False), (16, 512, 15, True), (5, 384, 1, True)])
+def test_attention_head_dim_128_vs_torch(b, s, nh, causal):
+    """Head dim 128 (SURVEY a14's 15 x 128-head GPT layout): the key-quarter forward at
+    D = 128 and the D = 128 backward (P^T through SMEM, dQ in the S^T columns)."""
+    hd, h = 128, nh * 128
+    g = torch.Generator(device="cuda").manual_seed(b * 1000 + s + nh + 77)
+    qkv = (torch.randn(b * s, 3 * h, device="cuda", generator=g) * 0.6).to(torch.bfloat16)
+    o = torch.empty(b * s, h, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b * nh * s, device="cuda", dtype=torch.float32)
+    call("p2bw_kernel_attention_fwd_hd", ptr(qkv), ptr(o), ptr(lse), b, s, nh, hd, int(causal), stream())
+    ref_in = qkv.float().requires_grad_(True)
+    ro, rl = ref_attention(ref_in, b, s, nh, causal, hd)
+    torch.cuda.synchronize()
+    assert (o.float() - ro).abs().max().item() < 2e-2
+    assert (lse - rl.detach()).abs().max().item() < 1e-2
+    dout = torch.randn(b * s, h, device="cuda", generator=g).to(torch.bfloat16)
+    dqkv = torch.empty_like(qkv)
+    delta = torch.empty(b * nh * s, device="cuda", dtype=torch.float32)
+    call("p2bw_kernel_attention_bwd_hd", ptr(qkv), ptr(o), ptr(dout), ptr(lse), ptr(dqkv), ptr(delta), b, s, nh,
+         hd, int(causal), stream())
+    ro.backward(dout.float())
+    torch.cuda.synchronize()
+    ref = ref_in.grad
+    for part, name in enumerate("qkv"):
+        d = dqkv.view(b * s, 3, h)[:, part].float()
+        r = ref.view(b * s, 3, h)[:, part]
+        err = (d - r).abs().max().item()
+        assert err < 3e-2 * max(1.0, r.abs().max().item()), (name, err)
+
+
+def test_attention_rejects_bad_head_dim():
+    qkv = torch.zeros(128, 3 * 96, device="cuda", dtype=torch.bfloat16)
+    o = torch.empty(128, 96, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(128, device="cuda", dtype=torch.float32)
+    with pytest.raises(Exception, match="head dim"):
+        call("p2bw_kernel_attention_fwd_hd", ptr(qkv), ptr(o), ptr(lse), 1, 128, 1, 96, 1, stream())
 
 
 def test_attention_rejects_untiled_sequence_length():
