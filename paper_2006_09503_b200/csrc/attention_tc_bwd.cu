@@ -415,7 +415,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // alone fill TMEM: S^T [0, 128), dP^T [128, 256), dV [256, 384), dK [384, 512).  So
 //   * P^T goes to SMEM (K-major SW128, like dS^T) instead of TMEM, and
 //   * dQ_i|j = dS K_j reuses the S^T columns once the elementwise warps have read S^T:
-//     the next tile's S^T / dP^T wait for the dQ flush (no S/dP-ahead-of-mm2 overlap).
+//     the next tile's S^T / dP^T wait for the dQ flush (no S/dP-ahead-of-mm2 overlap);
+//   * instead the tile is split in two phases: S^T is committed alone, so the exponentials
+//     (P^T -> SMEM) run while dP^T computes, and dV = P^T dO runs while dS^T is formed
+//     (GPT-2.2B shape 184 -> 167 us).  The same split measured neutral at D = 64, whose
+//     next-tile S / dP already overlap the dV / dK / dQ MMAs.
 // SMEM: K, V (one item) and Q, dO (one query tile) of 32 KB each, P^T and dS^T 32 KB,
 // dQ staging 16 KB: ~209 KB.  Numerics as at D = 64 (scale 1 / sqrt(128)).
 namespace d128 {
@@ -424,8 +428,8 @@ constexpr int kTileD = 2 * kTile;  // 128 rows x 128 bf16: two 64-column boxes k
 constexpr int oK = 0, oV = oK + kTileD, oQ = oV + kTileD, oDO = oQ + kTileD, oPT = oDO + kTileD,
               oDSt = oPT + kTileD, oDQ = oDSt + kTileD, oLse = oDQ + 4 * 4096, oDel = oLse + kT * 4,
               oBar = oDel + kT * 4;
-constexpr int bKvFull = 0, bKvEmpty = 1, bQFull = 2, bQEmpty = 3, bSdpFull = 4, bPdsFull = 5, bMm2 = 6,
-              bDqFree = 7, bKvAccFree = 8, kNumBars = 9;
+constexpr int bKvFull = 0, bKvEmpty = 1, bQFull = 2, bQEmpty = 3, bSFull = 4, bPFull = 5, bMm2 = 6,
+              bDqFree = 7, bKvAccFree = 8, bDpFull = 9, bDsFull = 10, kNumBars = 11;
 constexpr int kSmem = oBar + 256 + 1024;
 static_assert(kSmem <= 227 * 1024, "D = 128 backward SMEM");
 constexpr uint32_t tS = 0, tDP = 128, tDV = 256, tDK = 384, tDQ = 0;
@@ -453,7 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&tm_do);
         ptx::tma_prefetch_desc(&tm_dq);
         for (int q = 0; q < d128::kNumBars; ++q)
-            ptx::mbar_init(&bar[q], q == d128::bPdsFull ? kElemWarps : (q == d128::bDqFree || q == d128::bKvAccFree) ? 4 : 1);
+            ptx::mbar_init(&bar[q], (q == d128::bPFull || q == d128::bDsFull) ? kElemWarps
+                                    : (q == d128::bDqFree || q == d128::bKvAccFree) ? 4 : 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -518,26 +523,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::umma_bf16(tmem + d128::tS, ptx::sdesc_sw128(aK + off, 16, 1024),
                                        ptx::sdesc_sw128(aQ + off, 16, 1024), id_sq, kk > 0);
                     }
+                    ptx::umma_commit(&bar[d128::bSFull]);  // the exponentials start while dP^T runs
 #pragma unroll
                     for (int kk = 0; kk < d128::kD / 16; ++kk) {
                         const uint32_t off = (kk / 4) * kTile + (kk % 4) * 32;
                         ptx::umma_bf16(tmem + d128::tDP, ptx::sdesc_sw128(aV + off, 16, 1024),
                                        ptx::sdesc_sw128(aDO + off, 16, 1024), id_sq, kk > 0);
                     }
-                    ptx::umma_commit(&bar[d128::bSdpFull]);
-                    ptx::mbar_wait(&bar[d128::bPdsFull], g & 1);
-                    if (t == 0 && ln > 0) ptx::mbar_wait(&bar[d128::bKvAccFree], (ln - 1) & 1);
-                    ptx::tc_fence_after();
+                    ptx::umma_commit(&bar[d128::bDpFull]);
                     const bool first = t == 0;
+                    ptx::mbar_wait(&bar[d128::bPFull], g & 1);
+                    if (first && ln > 0) ptx::mbar_wait(&bar[d128::bKvAccFree], (ln - 1) & 1);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < kT / 16; ++kk)  // dV = P^T dO runs while dS^T is computed
+                        ptx::umma_bf16(tmem + d128::tDV, ptx::sdesc_sw128(aPT + (kk / 4) * kTile + (kk % 4) * 32, 16, 1024),
+                                       ptx::sdesc_sw128(aDO + kk * 2048, kTile, 1024), id_kv,
+                                       (!first || kk > 0) ? 1u : 0u);
+                    ptx::mbar_wait(&bar[d128::bDsFull], g & 1);
+                    ptx::tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < kT / 16; ++kk) {
                         const uint32_t a_off = (kk / 4) * kTile + (kk % 4) * 32;  // K-major, 16 queries per step
                         const uint32_t b_off = kk * 2048;                         // MN-major, 16 rows per step
-                        const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
-                        ptx::umma_bf16(tmem + d128::tDV, ptx::sdesc_sw128(aPT + a_off, 16, 1024),
-                                       ptx::sdesc_sw128(aDO + b_off, kTile, 1024), id_kv, acc);
                         ptx::umma_bf16(tmem + d128::tDK, ptx::sdesc_sw128(aDSt + a_off, 16, 1024),
-                                       ptx::sdesc_sw128(aQ + b_off, kTile, 1024), id_kv, acc);
+                                       ptx::sdesc_sw128(aQ + b_off, kTile, 1024), id_kv, (!first || kk > 0) ? 1u : 0u);
                         ptx::umma_bf16(tmem + d128::tDQ, ptx::sdesc_sw128(aDSt + b_off, kTile, 1024),
                                        ptx::sdesc_sw128(aK + b_off, kTile, 1024), id_q, kk > 0 ? 1u : 0u);
                     }
@@ -562,36 +572,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int key = it.j * kT + r;
             for (int t = 0; t < it.iters; ++t, ++g) {
                 const int i = it.i0 + t;
-                ptx::mbar_wait(&bar[d128::bSdpFull], g & 1);
+                ptx::mbar_wait(&bar[d128::bSFull], g & 1);
                 ptx::mbar_wait(&bar[d128::bQFull], g & 1);  // lse / delta visible
                 ptx::tc_fence_after();
-                uint32_t pp[16], dd[16];
+                // phase 1 (S^T only): P^T -> SMEM, so dV starts while dP^T is still computing
+                float pf[32];
+                uint32_t pk[16];
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const int col0 = sel * 32 + c * 16;
-                    uint32_t sv[16], dv[16];
+                    uint32_t sv[16];
                     ptx::tmem_ld_32x32b_x16(trow + d128::tS + col0, sv);
-                    ptx::tmem_ld_32x32b_x16(trow + d128::tDP + col0, dv);
                     ptx::tmem_ld_wait();
-                    const uint32_t la = sbase + d128::oLse + col0 * 4, da = sbase + d128::oDel + col0 * 4;
+                    const uint32_t la = sbase + d128::oLse + col0 * 4;
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
                         const float4 l4 = ptx::lds_f4(la + q4 * 16);
-                        const float4 d4 = ptx::lds_f4(da + q4 * 16);
-                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dl[4] = {d4.x, d4.y, d4.z, d4.w};
-                        float p[4], ds[4];
+                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int q = q4 * 4 + e;
                             float x = ptx::ex2(fmaf(__uint_as_float(sv[q]), sc, lv[e]));
                             if (kCausal && i * kT + col0 + q < key) x = 0.0f;
-                            p[e] = x;
-                            ds[e] = x * (__uint_as_float(dv[q]) - dl[e]);
+                            pf[c * 16 + q] = x;
                         }
-                        pp[c * 8 + q4 * 2] = ptx::pack_bf16x2(p[0], p[1]);
-                        pp[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(p[2], p[3]);
-                        dd[c * 8 + q4 * 2] = ptx::pack_bf16x2(ds[0], ds[1]);
-                        dd[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(ds[2], ds[3]);
+                        pk[c * 8 + q4 * 2] = ptx::pack_bf16x2(pf[c * 16 + q4 * 4], pf[c * 16 + q4 * 4 + 1]);
+                        pk[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(pf[c * 16 + q4 * 4 + 2], pf[c * 16 + q4 * 4 + 3]);
                     }
                 }
                 if (g > 0) ptx::mbar_wait(&bar[d128::bMm2], (g - 1) & 1);  // P^T / dS^T buffers free
@@ -599,13 +605,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ch = 0; ch < 4; ++ch) {
                     const int cc = (sel & 1) * 4 + ch;  // 16-byte chunk of the 128-byte row
                     const uint32_t off = static_cast<uint32_t>((cc ^ (r & 7)) << 4);
-                    ptx::sts_u4(prow + off, pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]);
-                    ptx::sts_u4(drow + off, dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]);
+                    ptx::sts_u4(prow + off, pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
                 }
                 ptx::fence_proxy_async();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&bar[d128::bPdsFull]);
+                if (lane == 0) ptx::mbar_arrive(&bar[d128::bPFull]);
+                // phase 2: dS^T = P^T (dP^T - delta) -> SMEM
+                ptx::mbar_wait(&bar[d128::bDpFull], g & 1);
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int col0 = sel * 32 + c * 16;
+                    uint32_t dv[16];
+                    ptx::tmem_ld_32x32b_x16(trow + d128::tDP + col0, dv);
+                    ptx::tmem_ld_wait();
+                    const uint32_t da = sbase + d128::oDel + col0 * 4;
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 d4 = ptx::lds_f4(da + q4 * 16);
+                        const float dl[4] = {d4.x, d4.y, d4.z, d4.w};
+                        float ds[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            ds[e] = pf[c * 16 + q4 * 4 + e] * (__uint_as_float(dv[q4 * 4 + e]) - dl[e]);
+                        pk[c * 8 + q4 * 2] = ptx::pack_bf16x2(ds[0], ds[1]);
+                        pk[c * 8 + q4 * 2 + 1] = ptx::pack_bf16x2(ds[2], ds[3]);
+                    }
+                }
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    const int cc = (sel & 1) * 4 + ch;
+                    const uint32_t off = static_cast<uint32_t>((cc ^ (r & 7)) << 4);
+                    ptx::sts_u4(drow + off, pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+                }
+                ptx::fence_proxy_async();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&bar[d128::bDsFull]);
             }
         }
     } else if (warp >= 4 + kElemWarps) {

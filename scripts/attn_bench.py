@@ -17,6 +17,22 @@ if len(sys.argv) > 1:
     SHAPES = [s for s in SHAPES if s[0] in sys.argv[1:]]
 
 
+def keep_async_pool():
+    """The C-ABI backward allocates its scratch per call with cudaMallocAsync; keep the
+    default pool's memory mapped between calls so the timing is the kernels'."""
+    try:
+        from cuda.bindings import driver as dr
+        from cuda.bindings import runtime as rt
+        err, pool = rt.cudaDeviceGetDefaultMemPool(torch.cuda.current_device())
+        rt.cudaMemPoolSetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrReleaseThreshold,
+                                   dr.cuuint64_t(2**64 - 1))
+    except Exception as e:  # noqa: BLE001
+        print(f"# mempool threshold not set: {e}", file=sys.stderr)
+
+
+keep_async_pool()
+
+
 def timeit(fn, iters=20, reps=5):
     """Best of `reps` averages (the C-ABI backward allocates its scratch per call with
     cudaMallocAsync, whose pool occasionally re-maps memory inside a window)."""
