@@ -6,11 +6,15 @@ mkdir -p gpurun_out/ev
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 > gpurun_out/ev/pytest_gpu.txt 2>&1; tail -3 gpurun_out/ev/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev/smoke.txt 2>&1; tail -1 gpurun_out/ev/smoke.txt
 timeout 900 python bench.py > gpurun_out/ev/bench.json 2> gpurun_out/ev/bench.err; tail -c 400 gpurun_out/ev/bench.json
-# one steady-state batch of the bench (~5000 launches after ~4 batches of warm-up)
+# one batch of the bench's resident pass (~5000 launches after weight initialisation)
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  --launch-skip 22000 -c 5100 --csv --log-file gpurun_out/ev/launches.csv \
+  --launch-skip 700 -c 5100 --kill yes --csv --log-file gpurun_out/ev/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-same-config > gpurun_out/ev/ncu_launch.log 2>&1; tail -1 gpurun_out/ev/ncu_launch.log
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_tc_kernel --launch-skip 2000 -c 3 \
   -f -o gpurun_out/ev/gemm_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-same-config > gpurun_out/ev/ncu_gemm.log 2>&1; tail -1 gpurun_out/ev/ncu_gemm.log
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_attn_bwd_tc|k_attn_fwd_tc|k_ln_bwd|k_ln_fwd_wide" --launch-skip 200 -c 4 \
   -f -o gpurun_out/ev/other_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-same-config > gpurun_out/ev/ncu_other.log 2>&1; tail -1 gpurun_out/ev/ncu_other.log
+# the other configurations' bench lines
+for c in bert-base bert-large gpt-24 small gpt-2.2b-h128; do
+  timeout 600 python bench.py --config $c > gpurun_out/ev/bench_$c.json 2> gpurun_out/ev/bench_$c.err; tail -c 200 gpurun_out/ev/bench_$c.json
+done
