@@ -99,7 +99,20 @@ struct KParams {
     int tail_tiles, tail_f;
     float* tail_ws;
     unsigned* tail_flags;
+    // Grouped raster: tiles walk N inside groups of `group_m` M tiles (0: M-fastest over
+    // the whole output), so the operand L2 can hold is the one re-read.
+    int group_m;
 };
+
+// Output tile (M-group index, N-group index) of tile number t.
+__device__ __forceinline__ int2 tile_mn(int t, int tiles_mg, int tiles_ng, int gm) {
+    if (gm <= 0) return make_int2(t % tiles_mg, t / tiles_mg);
+    const int per = gm * tiles_ng;
+    const int first = (t / per) * gm;
+    const int gsz = min(tiles_mg - first, gm);
+    const int r = t % per;
+    return make_int2(first + r % gsz, r / gsz);
+}
 
 // One work unit: an output tile (group) over the K blocks [kb0, kb1).  role 0: a whole
 // tile or split-K slice; 1: tail contributor part; 2: tail finisher.  Units are numbered
@@ -252,8 +265,9 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             uint32_t phase = 0;
             for (int w = w0; w < num_work; w += wstep) {
                 const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);
-                const int m0 = ((u.tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
-                const int n0 = ((u.tile / tiles_mg) * kNP + pair) * BN;
+                const int2 mn = tile_mn(u.tile, tiles_mg, tiles_ng, p.group_m);
+                const int m0 = (mn.x * (kPair ? 2 : 1) + prank) * kBM;
+                const int n0 = (mn.y * kNP + pair) * BN;
                 for (int kb = u.kb0; kb < u.kb1; ++kb) {
                     ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* da = s_a + stage * Cfg::kABytes;
@@ -392,8 +406,9 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             uint32_t phase = 0;
             for (int w = w0; w < num_work; w += wstep) {  // (no tail split with row sums)
                 const int tile = w % num_tiles;
-                const int m0 = (tile % tiles_mg) * kBM;
-                const bool active = tile / tiles_mg == 0;  // n0 == 0
+                const int2 mn = tile_mn(tile, tiles_mg, tiles_ng, p.group_m);
+                const int m0 = mn.x * kBM;
+                const bool active = mn.y == 0;  // n0 == 0
                 const int kb0 = (w / num_tiles) * kb_per;
                 const int kb1 = min(kblocks, kb0 + kb_per);
                 float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
@@ -451,8 +466,9 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             uint32_t phase = 0;
             for (int w = w0; w < num_work; w += wstep) {
                 const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);  // tail parts: disjoint K blocks
-                const int mt = u.tile % tiles_mg;
-                const bool active = u.tile / tiles_mg == 0;  // n0 == 0: each A element counts once
+                const int2 mn = tile_mn(u.tile, tiles_mg, tiles_ng, p.group_m);
+                const int mt = mn.x;
+                const bool active = mn.y == 0;  // n0 == 0: each A element counts once
                 const int kb0 = u.kb0, kb1 = u.kb1;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full_bar[stage], phase);
@@ -516,8 +532,9 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
         for (int w = w0; w < num_work; w += wstep) {
             const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);
             const int tile = u.tile;
-            const int m0 = ((tile % tiles_mg) * (kPair ? 2 : 1) + prank) * kBM;
-            const int n0 = ((tile / tiles_mg) * kNP + pair) * BN;
+            const int2 mn = tile_mn(tile, tiles_mg, tiles_ng, p.group_m);
+            const int m0 = (mn.x * (kPair ? 2 : 1) + prank) * kBM;
+            const int n0 = (mn.y * kNP + pair) * BN;
             const int r0 = m0 + q * 32;
             const int role = kTail ? u.role : 0;
             // Side inputs (residual / GELU pre-activation) do not depend on the
@@ -913,6 +930,14 @@ TailPool tail_pool(cudaStream_t s) {
     return tp;
 }
 
+bool raster_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("P2BW_GEMM_RASTER");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 bool tail_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("P2BW_GEMM_TAIL");
@@ -1125,7 +1150,16 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
             throw Error("gemm: bias_scratch must hold 2 * ceil(M / 128) * K floats");
         rsum = epi.bias_scratch;
     }
-    KParams p{m, n, k, splits, epi, rsum, tail_tiles, tail_f, tp.ws, tp.flags};
+    // Raster order by which operand L2 (126 MB) can keep: A resident -> M fastest (B is
+    // streamed once); else B resident -> N fastest within each M tile (A streamed once);
+    // else groups of ~sqrt(concurrent units) M tiles.  (M-fastest everywhere re-streamed a
+    // 126 MB wgrad A once per N column.)
+    int group_m = 0;
+    if (raster_enabled()) {
+        const double a_bytes = 2.0 * m * k, b_bytes = 2.0 * n * k, resident = 48e6;
+        if (a_bytes > resident) group_m = b_bytes <= resident ? 1 : 8;
+    }
+    KParams p{m, n, k, splits, epi, rsum, tail_tiles, tail_f, tp.ws, tp.flags, group_m};
     const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
     // profiler class by pass: forward (K-major x K-major), dgrad (B MN-major), wgrad (both MN-major)
     const char* cls = amn ? "gemm_wgrad" : (bmn ? "gemm_dgrad" : "gemm_fwd");

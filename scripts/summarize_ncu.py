@@ -23,21 +23,33 @@ def launches(path: str) -> str:
     text = open(path).read()
     start = text.find('"ID"')
     rows = list(csv.DictReader(io.StringIO(text[start:])))
-    tot = collections.defaultdict(lambda: [0, 0.0])
+    tot = collections.defaultdict(lambda: [0, 0.0, 0.0])  # launches, us, DRAM bytes
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for r in rows:
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
+        name = r.get("Metric Name")
         unit = r.get("Metric Unit", "")
         v = float(r["Metric Value"].replace(",", ""))
-        us = v / 1000.0 if unit == "ns" else (v * 1000.0 if unit == "ms" else v)
         k = short(r["Kernel Name"])
-        tot[k][0] += 1
-        tot[k][1] += us
+        if name == "gpu__time_duration.sum":
+            us = v / 1000.0 if unit == "ns" else (v * 1000.0 if unit == "ms" else v)
+            tot[k][0] += 1
+            tot[k][1] += us
+        elif name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot[k][2] += v * scale.get(unit, 1.0)
     total = sum(v[1] for v in tot.values()) or 1.0
-    out = ["| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
-    for k, (n, us) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
-        out.append(f"| `{k}` | {n} | {us:.1f} | {100 * us / total:.1f}% | {us / n:.2f} |")
-    out.append(f"\n{len(rows)} launches, {total:.1f} us of kernel time in the window.")
+    have_dram = any(v[2] for v in tot.values())
+    out = ["| kernel | launches | total us | share | avg us |" + (" DRAM MB / launch |" if have_dram else ""),
+           "|---|---|---|---|---|" + ("---|" if have_dram else "")]
+    for k, (n, us, by) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"| `{k}` | {n} | {us:.1f} | {100 * us / total:.1f}% | {us / n:.2f} |" +
+                   (f" {by / n / 1e6:.1f} |" if have_dram else ""))
+    nl = sum(v[0] for v in tot.values())
+    out.append(f"\n{nl} launches, {total:.1f} us of kernel time in the window.")
+    if have_dram:
+        g = [v for k, v in tot.items() if "gemm_tc_kernel" in k]
+        n, by = sum(v[0] for v in g), sum(v[2] for v in g)
+        if n:
+            out.append(f"gemm_tc_kernel: {n} launches, mean DRAM read + write {by / n:.0f} bytes per launch.")
     return "\n".join(out)
 
 
