@@ -1,7 +1,7 @@
 // Softmax attention backward on tcgen05 tensor cores (head dim 64 or 128, seq % 128 == 0).
 // Persistent and key-outer: one CTA per SM walks work items
-// (128-key tile j, sequence, head) -- j-major, so causal items with the most query
-// tiles go first -- and for each item the query tiles i that can see it:
+// (128-key tile j, sequence, head) -- (sequence, head)-major, see item_of -- and for each
+// item the query tiles i that can see it:
 //
 //   UMMA  S^T  = K_j Q_i^T          128 x 128 fp32, TMEM [0, 128)
 //   UMMA  dP^T = V_j dO_i^T         TMEM [128, 256)
@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "launch.h"
@@ -98,10 +99,19 @@ struct Item {
     int bh, j, i0, iters;
 };
 
+// Item order: (sequence, head)-major -- the nq key tiles of one (sequence, head) are
+// consecutive items, so the CTAs running them at the same time share its Q / dO / lse /
+// delta tiles and its dQ accumulator rows in L2 (the former key-tile-major order re-read
+// them from DRAM for every key tile; in the GPT-2.2B step +0.4%, paired runs).  Causal
+// items differ in length (nq - j query tiles); j is rotated by the (sequence, head) index
+// so that the static round-robin hands every CTA a mix of lengths (with nq | #CTAs an
+// unrotated order would give CTA b only j = b % nq).
 __device__ __forceinline__ Item item_of(int n, int bhn, int nq, bool causal) {
+    (void)bhn;
     Item it;
-    it.j = n / bhn;
-    it.bh = n % bhn;
+    it.bh = n / nq;
+    const int r = n % nq;
+    it.j = causal ? (r + it.bh) % nq : r;
     it.i0 = causal ? it.j : 0;
     it.iters = nq - it.i0;
     return it;
