@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "profiler.h"
 #include "ptx.cuh"
@@ -450,26 +451,37 @@ __global__ void __launch_bounds__(256) k_ln_fwd_wide(const bf16* __restrict__ x,
 // group's warps through SMEM (named barrier per group, fixed order: every warp of the
 // group sees identical sums; deterministic).  dx may alias dy: a row is read (into
 // the ring) before it is written, and the ring only fetches rows not yet written.
-constexpr int kLnBwdThreads = 768;  // 85 registers per thread; G = 24 / wpr row groups
+// Wide rows (h >= 1024) run with TWO vectors per lane (NVL = 2) in CTAs of 512 threads:
+// a group of ceil(h / 512) warps per row, so the per-row shuffle / named-barrier / SMEM
+// exchange work is spread over twice the elements (the kernel is issue-bound: ~300 SASS
+// per warp-row at NVL = 1, h 1920).  P2BW_LN_BWD_NVL = 1 / 2 forces one layout.
+template <int NVL>
+constexpr int ln_bwd_threads() { return NVL == 1 ? 768 : 512; }  // 85 / 128 registers per thread
 
 struct LnBwdShape {
+    int nvl;  // 16-byte vectors per lane
     int wpr;  // warps per row
     int G;    // row groups per CTA
 };
 
-inline LnBwdShape ln_bwd_shape(int h) {
+inline int ln_bwd_nvl(int h) {
+    const char* env = std::getenv("P2BW_LN_BWD_NVL");  // read per call: tests switch it
+    if (env && (env[0] == '1' || env[0] == '2')) return env[0] - '0';
+    return h >= 1024 ? 2 : 1;
+}
+
+inline LnBwdShape ln_bwd_shape(int h, int nvl) {
     const int hv = h / 8;
-    int wpr = (hv + 31) / 32;
+    int wpr = (hv + 32 * nvl - 1) / (32 * nvl);
     if (wpr > 4) wpr = 8;  // instantiated group widths: 1, 2, 3, 4, 8
-    int G = (kLnBwdThreads / 32) / wpr;
+    int G = ((nvl == 1 ? ln_bwd_threads<1>() : ln_bwd_threads<2>()) / 32) / wpr;
     if (wpr > 1) G = std::min(G, 15);  // named barriers 1..15
-    return {wpr, G};
+    return {nvl, wpr, G};
 }
 
 // SMEM: red [G][h] fp32 | row-sum exchange [G][2][wpr][2] fp32 | row ring [G][NS] x
 // {x, dy, dres} bf16 rows | ring barriers [G][NS].
-inline size_t ln_bwd_fixed_bytes(int h) {
-    const LnBwdShape sh = ln_bwd_shape(h);
+inline size_t ln_bwd_fixed_bytes(int h, const LnBwdShape& sh) {
     const size_t f = (static_cast<size_t>(sh.G) * h + static_cast<size_t>(sh.G) * 2 * sh.wpr * 2) * sizeof(float);
     return (f + 127) & ~static_cast<size_t>(127);
 }
@@ -480,17 +492,16 @@ inline size_t ln_bwd_fixed_bytes(int h) {
 // BERT-base (h 768, G 8 groups): 1 / 2 / 3 / 4 slots measured 16.1 / 16.0 / 16.2 / 16.5 us.
 // Wide rows leave few groups per CTA (h 1920: G 3), so the ring deepens until ~16 rows
 // per SM are in flight (Little's law at ~6.5 TB/s and ~1 us of latency: ~45 KB per SM).
-inline int ln_bwd_ring_depth(int h) {
-    const int G = ln_bwd_shape(h).G;
+inline int ln_bwd_ring_depth(int h, const LnBwdShape& sh) {
+    const int G = sh.G;
     int ns = std::max(2, std::min(8, (16 + G - 1) / G));
     const size_t per_slot = static_cast<size_t>(G) * (3ull * h * 2 + 8);
-    while (ns > 2 && ln_bwd_fixed_bytes(h) + ns * per_slot > 200u * 1024u) --ns;
+    while (ns > 2 && ln_bwd_fixed_bytes(h, sh) + ns * per_slot > 200u * 1024u) --ns;
     return ns;
 }
 
-inline size_t ln_bwd_smem_bytes(int h) {
-    const LnBwdShape sh = ln_bwd_shape(h);
-    return ln_bwd_fixed_bytes(h) + static_cast<size_t>(sh.G) * ln_bwd_ring_depth(h) * (3ull * h * 2 + 8);
+inline size_t ln_bwd_smem_bytes(int h, const LnBwdShape& sh) {
+    return ln_bwd_fixed_bytes(h, sh) + static_cast<size_t>(sh.G) * ln_bwd_ring_depth(h, sh) * (3ull * h * 2 + 8);
 }
 
 __device__ __forceinline__ void group_bar(int id, int threads) {
@@ -498,14 +509,14 @@ __device__ __forceinline__ void group_bar(int id, int threads) {
 }
 
 // LayerNorm backward + residual, persistent: 148 CTAs x G row groups of wpr warps (one
-// row per group at a time, lane = one 8-column vector).  Each group streams its rows
-// (r, r + G * grid, ...) through an NS-deep SMEM ring filled by 1D bulk copies (x, dy,
-// dres rows: NS rows in flight per group without holding them in registers -- the
-// register-prefetch version kept one row in flight and ran at ~2.7 TB/s).
+// row per group at a time, lane = NVL 8-column vectors, wpr * 32 columns apart).  Each
+// group streams its rows (r, r + G * grid, ...) through an NS-deep SMEM ring filled by
+// 1D bulk copies (x, dy, dres rows: NS rows in flight per group without holding them in
+// registers -- the register-prefetch version kept one row in flight and ran at ~2.7 TB/s).
 //   dx = rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)) + dres
 // plus per-CTA partial column sums of dy*xhat (dgamma), dy (dbeta) and, kSum, bf16(dx).
-template <bool kSum, int wpr, bool kRes>
-__global__ void __launch_bounds__(kLnBwdThreads, 1)
+template <bool kSum, int wpr, bool kRes, int NVL>
+__global__ void __launch_bounds__(ln_bwd_threads<NVL>(), 1)
     k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean,
              const float* __restrict__ rstd, const bf16* __restrict__ g, const bf16* __restrict__ dres,
              bf16* dx, int rows, int h, int G, int fixed_bytes, int NS, float* __restrict__ part) {
@@ -516,8 +527,13 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = warp / wpr, wi = warp % wpr;
     const int hv = h / 8;
-    const int vi = wi * 32 + lane;  // my 8-column vector of every row
-    const bool act = grp < G && vi < hv;
+    int vi[NVL];  // my 8-column vectors of every row
+    bool act[NVL];
+#pragma unroll
+    for (int v = 0; v < NVL; ++v) {
+        vi[v] = wi * 32 + lane + v * wpr * 32;
+        act[v] = grp < G && vi[v] < hv;
+    }
     constexpr bool has_res = kRes;  // residual gradient added to dx (compile-time: no per-row branches)
     const float inv_h = 1.0f / static_cast<float>(h);
     float* xs = ln_smem + static_cast<size_t>(G) * h;
@@ -549,14 +565,21 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
         for (int i = 0; i < NS; ++i) issue(r0 + i * stride, i);
     // the row math runs on packed fp32 pairs (FFMA2 / FADD2 / FMUL2): the kernel is issue-
     // bound, so half the FP instructions per element is what moves it
-    unsigned long long g2[4] = {0ull, 0ull, 0ull, 0ull};
-    if (act) {
-        const uint4 gp = *reinterpret_cast<const uint4*>(g + vi * 8);
-        g2[0] = ptx::bf2_to_f2(gp.x), g2[1] = ptx::bf2_to_f2(gp.y), g2[2] = ptx::bf2_to_f2(gp.z),
-        g2[3] = ptx::bf2_to_f2(gp.w);
+    unsigned long long g2[NVL][4];
+#pragma unroll
+    for (int v = 0; v < NVL; ++v) {
+        g2[v][0] = g2[v][1] = g2[v][2] = g2[v][3] = 0ull;
+        if (act[v]) {
+            const uint4 gp = *reinterpret_cast<const uint4*>(g + vi[v] * 8);
+            g2[v][0] = ptx::bf2_to_f2(gp.x), g2[v][1] = ptx::bf2_to_f2(gp.y), g2[v][2] = ptx::bf2_to_f2(gp.z),
+            g2[v][3] = ptx::bf2_to_f2(gp.w);
+        }
     }
-    unsigned long long ag[4] = {0ull, 0ull, 0ull, 0ull}, ab[4] = {0ull, 0ull, 0ull, 0ull},
-                       as[4] = {0ull, 0ull, 0ull, 0ull};  // (0.0f, 0.0f) pairs
+    unsigned long long ag[NVL][4], ab[NVL][4], as[NVL][4];  // (0.0f, 0.0f) pairs
+#pragma unroll
+    for (int v = 0; v < NVL; ++v)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) ag[v][t] = ab[v][t] = as[v][t] = 0ull;
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
     int r = r0;
     float mu = 0.0f, rs = 0.0f;
@@ -573,28 +596,33 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
             nrs = rstd[r + stride];
         }
         ptx::mbar_wait(&my_bars[slot], phase);
-        const uint8_t* src = my_ring + slot * stage_bytes + vi * 16;
-        uint4 xp = z4, dp = z4, rp = z4;
-        if (act) {
-            xp = *reinterpret_cast<const uint4*>(src);
-            dp = *reinterpret_cast<const uint4*>(src + row_bytes);
-            if (has_res) rp = *reinterpret_cast<const uint4*>(src + 2 * row_bytes);
-        }
-        unsigned long long xh[4], dg[4];
+        const uint8_t* src = my_ring + slot * stage_bytes;
+        uint4 rp[NVL];
+        unsigned long long xh[NVL][4], dg[NVL][4];
         float s1, s2;
         {
-            const uint32_t xw[4] = {xp.x, xp.y, xp.z, xp.w}, dw[4] = {dp.x, dp.y, dp.z, dp.w};
             const unsigned long long rs2 = ptx::f2(rs, rs), sh2 = ptx::f2(-mu * rs, -mu * rs);
             unsigned long long a1 = 0ull, a2 = 0ull;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const unsigned long long x2 = ptx::bf2_to_f2(xw[t]), d2 = ptx::bf2_to_f2(dw[t]);
-                xh[t] = ptx::ffma2(x2, rs2, sh2);  // (x - mu) rstd
-                dg[t] = ptx::fmul2(d2, g2[t]);
-                ag[t] = ptx::ffma2(d2, xh[t], ag[t]);  // inactive lanes hold zero data
-                ab[t] = ptx::fadd2(ab[t], d2);
-                a1 = ptx::fadd2(a1, dg[t]);
-                a2 = ptx::ffma2(dg[t], xh[t], a2);
+            for (int v = 0; v < NVL; ++v) {
+                uint4 xp = z4, dp = z4;
+                rp[v] = z4;
+                if (act[v]) {
+                    xp = *reinterpret_cast<const uint4*>(src + vi[v] * 16);
+                    dp = *reinterpret_cast<const uint4*>(src + row_bytes + vi[v] * 16);
+                    if (has_res) rp[v] = *reinterpret_cast<const uint4*>(src + 2 * row_bytes + vi[v] * 16);
+                }
+                const uint32_t xw[4] = {xp.x, xp.y, xp.z, xp.w}, dw[4] = {dp.x, dp.y, dp.z, dp.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const unsigned long long x2 = ptx::bf2_to_f2(xw[t]), d2 = ptx::bf2_to_f2(dw[t]);
+                    xh[v][t] = ptx::ffma2(x2, rs2, sh2);  // (x - mu) rstd
+                    dg[v][t] = ptx::fmul2(d2, g2[v][t]);
+                    ag[v][t] = ptx::ffma2(d2, xh[v][t], ag[v][t]);  // inactive lanes hold zero data
+                    ab[v][t] = ptx::fadd2(ab[v][t], d2);
+                    a1 = ptx::fadd2(a1, dg[v][t]);
+                    a2 = ptx::ffma2(dg[v][t], xh[v][t], a2);
+                }
             }
             const float2 f1 = ptx::f2_split(a1), f2v = ptx::f2_split(a2);
             s1 = f1.x + f1.y;
@@ -604,17 +632,15 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
         s2 = warp_sum(s2);
         if constexpr (wpr > 1) {
             float* sl = xs + (static_cast<size_t>(grp) * 2 + (it & 1)) * wpr * 2;
-            if (lane == 0) {
-                sl[wi * 2] = s1;
-                sl[wi * 2 + 1] = s2;
-            }
+            if (lane == 0) *reinterpret_cast<float2*>(sl + wi * 2) = make_float2(s1, s2);
             group_bar(1 + grp, wpr * 32);  // also: every warp of the group has read the slot
             s1 = 0.0f;
             s2 = 0.0f;
 #pragma unroll
             for (int w = 0; w < wpr; ++w) {
-                s1 += sl[w * 2];
-                s2 += sl[w * 2 + 1];
+                const float2 p = *reinterpret_cast<const float2*>(sl + w * 2);
+                s1 += p.x;
+                s2 += p.y;
             }
         } else {
             __syncwarp();
@@ -624,20 +650,24 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
             slot = 0;
             phase ^= 1;
         }
-        if (act) {
-            // dx = rstd (dg - m1 - xh m2) = dg rstd + xh (-rstd m2) + (-rstd m1)
-            const float c1 = -rs * s1 * inv_h, c2 = -rs * s2 * inv_h;
-            const unsigned long long rs2 = ptx::f2(rs, rs), c12 = ptx::f2(c1, c1), c22 = ptx::f2(c2, c2);
-            const uint32_t rw[4] = {rp.x, rp.y, rp.z, rp.w};
-            uint32_t ow[4];
+        // dx = rstd (dg - m1 - xh m2) = dg rstd + xh (-rstd m2) + (-rstd m1)
+        const float c1 = -rs * s1 * inv_h, c2 = -rs * s2 * inv_h;
+        const unsigned long long rs2 = ptx::f2(rs, rs), c12 = ptx::f2(c1, c1), c22 = ptx::f2(c2, c2);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                unsigned long long o = ptx::ffma2(xh[t], c22, ptx::ffma2(dg[t], rs2, c12));
-                if (has_res) o = ptx::fadd2(o, ptx::bf2_to_f2(rw[t]));
-                ow[t] = ptx::f2_to_bf2(o);
-                if constexpr (kSum) as[t] = ptx::fadd2(as[t], ptx::bf2_to_f2(ow[t]));  // what the next GEMM reads
+        for (int v = 0; v < NVL; ++v) {
+            if (act[v]) {
+                const uint32_t rw[4] = {rp[v].x, rp[v].y, rp[v].z, rp[v].w};
+                uint32_t ow[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    unsigned long long o = ptx::ffma2(xh[v][t], c22, ptx::ffma2(dg[v][t], rs2, c12));
+                    if (has_res) o = ptx::fadd2(o, ptx::bf2_to_f2(rw[t]));
+                    ow[t] = ptx::f2_to_bf2(o);
+                    if constexpr (kSum) as[v][t] = ptx::fadd2(as[v][t], ptx::bf2_to_f2(ow[t]));  // what the next GEMM reads
+                }
+                *reinterpret_cast<uint4*>(dx + static_cast<size_t>(r) * h + vi[v] * 8) =
+                    make_uint4(ow[0], ow[1], ow[2], ow[3]);
             }
-            *reinterpret_cast<uint4*>(dx + static_cast<size_t>(r) * h + vi * 8) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
         mu = nmu;
         rs = nrs;
@@ -645,12 +675,14 @@ __global__ void __launch_bounds__(kLnBwdThreads, 1)
     // CTA reduction over the row groups, one statistic at a time, fixed order
     for (int st = 0; st < (kSum ? 3 : 2); ++st) {
         __syncthreads();
-        if (act) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const float2 v = ptx::f2_split(st == 0 ? ag[t] : (st == 1 ? ab[t] : as[t]));
-                ln_smem[static_cast<size_t>(grp) * h + vi * 8 + 2 * t] = v.x;
-                ln_smem[static_cast<size_t>(grp) * h + vi * 8 + 2 * t + 1] = v.y;
+        for (int v = 0; v < NVL; ++v) {
+            if (act[v]) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float2 q = ptx::f2_split(st == 0 ? ag[v][t] : (st == 1 ? ab[v][t] : as[v][t]));
+                    *reinterpret_cast<float2*>(ln_smem + static_cast<size_t>(grp) * h + vi[v] * 8 + 2 * t) = q;
+                }
             }
         }
         __syncthreads();
@@ -1051,25 +1083,35 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 
 size_t layernorm_bwd_scratch_floats(int rows, int h) { return static_cast<size_t>(ln_bwd_blocks(rows)) * h * 3; }
 
-template <bool kSum>
-void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
-                   const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
-    const LnBwdShape sh = ln_bwd_shape(h);
-    const size_t smem = ln_bwd_smem_bytes(h);
+template <bool kSum, int NVL>
+void launch_ln_bwd_nvl(int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
+                       const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
+    const LnBwdShape sh = ln_bwd_shape(h, NVL);
+    const size_t smem = ln_bwd_smem_bytes(h, sh);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024)
             check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(ln bwd smem)");
-        launch_pdl(kern, dim3(grid), dim3(kLnBwdThreads), smem, s, "k_ln_bwd", dy, x, mean, rstd, g, dres, dx, rows, h,
-                   sh.G, static_cast<int>(ln_bwd_fixed_bytes(h)), ln_bwd_ring_depth(h), part);
+        launch_pdl(kern, dim3(grid), dim3(ln_bwd_threads<NVL>()), smem, s, "k_ln_bwd", dy, x, mean, rstd, g, dres, dx,
+                   rows, h, sh.G, static_cast<int>(ln_bwd_fixed_bytes(h, sh)), ln_bwd_ring_depth(h, sh), part);
     };
     switch (sh.wpr) {
-        case 1: dres ? go(k_ln_bwd<kSum, 1, true>) : go(k_ln_bwd<kSum, 1, false>); break;
-        case 2: dres ? go(k_ln_bwd<kSum, 2, true>) : go(k_ln_bwd<kSum, 2, false>); break;
-        case 3: dres ? go(k_ln_bwd<kSum, 3, true>) : go(k_ln_bwd<kSum, 3, false>); break;
-        case 4: dres ? go(k_ln_bwd<kSum, 4, true>) : go(k_ln_bwd<kSum, 4, false>); break;
-        default: dres ? go(k_ln_bwd<kSum, 8, true>) : go(k_ln_bwd<kSum, 8, false>); break;
+        case 1: dres ? go(k_ln_bwd<kSum, 1, true, NVL>) : go(k_ln_bwd<kSum, 1, false, NVL>); break;
+        case 2: dres ? go(k_ln_bwd<kSum, 2, true, NVL>) : go(k_ln_bwd<kSum, 2, false, NVL>); break;
+        case 3: dres ? go(k_ln_bwd<kSum, 3, true, NVL>) : go(k_ln_bwd<kSum, 3, false, NVL>); break;
+        case 4: dres ? go(k_ln_bwd<kSum, 4, true, NVL>) : go(k_ln_bwd<kSum, 4, false, NVL>); break;
+        default:
+            if constexpr (NVL == 1) dres ? go(k_ln_bwd<kSum, 8, true, 1>) : go(k_ln_bwd<kSum, 8, false, 1>);
+            else throw Error("layernorm_bwd: no 8-warp group at two vectors per lane");
+            break;
     }
+}
+
+template <bool kSum>
+void launch_ln_bwd(int grid, const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
+                   const bf16* dres, bf16* dx, int rows, int h, float* part, cudaStream_t s) {
+    if (ln_bwd_nvl(h) == 2) launch_ln_bwd_nvl<kSum, 2>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s);
+    else launch_ln_bwd_nvl<kSum, 1>(grid, dy, x, mean, rstd, g, dres, dx, rows, h, part, s);
 }
 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,

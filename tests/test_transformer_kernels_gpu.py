@@ -190,6 +190,16 @@ def test_colsum_bias_grad_vs_torch(rows, n, ld, overwrite):
     assert (out - ref).abs().max().item() < 1e-3 * max(1.0, ref.abs().max().item())
 
 
+@pytest.mark.parametrize("nvl", ["1", "2"])
+@pytest.mark.parametrize("rows,h", [(4099, 1920), (700, 1024), (2500, 1280), (5000, 2048), (300, 512), (1000, 768)])
+def test_layernorm_bwd_vectors_per_lane(rows, h, nvl, monkeypatch):
+    """Both LayerNorm-backward layouts (one or two 16-byte vectors per lane; P2BW_LN_BWD_NVL
+    forces one, the default picks two for h >= 1024) against torch."""
+    monkeypatch.setenv("P2BW_LN_BWD_NVL", nvl)
+    test_layernorm_fwd_bwd_vs_torch(rows, h, True)
+    test_layernorm_fwd_bwd_vs_torch(rows, h, False)
+
+
 @pytest.mark.parametrize("rows,h", [(128, 128), (4096, 768)])
 def test_layernorm_bwd_small_hidden(rows, h):
     test_layernorm_fwd_bwd_vs_torch(rows, h, True)
