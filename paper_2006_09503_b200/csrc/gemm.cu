@@ -946,6 +946,16 @@ bool tail_enabled() {
     return on;
 }
 
+// Upper bound on split-K slices of the fp32 (weight-gradient) GEMMs; P2BW_GEMM_MAX_SPLIT
+// overrides it (diagnostic A/B knob).
+int max_split_cap() {
+    static const int cap = [] {
+        const char* e = std::getenv("P2BW_GEMM_MAX_SPLIT");
+        return e ? std::max(1, std::atoi(e)) : 1 << 20;
+    }();
+    return cap;
+}
+
 bool tile_ok(int bn, int cl, bool bmn) { return !(bmn && cl >= 2 && (bn / 2) % 64 != 0); }
 
 // Steady-state speed of a tile shape relative to the 256 x 256 CTA-pair tile, from the
@@ -990,7 +1000,7 @@ TileChoice choose_tile(int m, int n, int k, bool f32_out, bool bmn, bool allow_s
             if (!tile_ok(bn, cl, bmn) || (cl == 2 && m <= kBM) || (cl == 2 && single_cta)) continue;
             const int tiles_m = (m + kBM - 1) / kBM;
             const int tiles = (cl == 2 ? (tiles_m + 1) / 2 : tiles_m) * ((n + bn - 1) / bn);
-            const int max_split = allow_split ? std::max(1, kblocks / 8) : 1;  // >= 8 k-blocks (512) per slice
+            const int max_split = allow_split ? std::min(max_split_cap(), std::max(1, kblocks / 8)) : 1;  // >= 8 k-blocks (512) per slice
             const double per_kb = (bn / 256.0) / tile_speed(bn, cl);
             for (int sp = 1; sp <= max_split; ++sp) {
                 const int kb_per = (kblocks + sp - 1) / sp;

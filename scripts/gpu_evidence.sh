@@ -18,3 +18,7 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_a
 for c in bert-base bert-large gpt-24 small gpt-2.2b-h128; do
   timeout 600 python bench.py --config $c > gpurun_out/ev/bench_$c.json 2> gpurun_out/ev/bench_$c.err; tail -c 200 gpurun_out/ev/bench_$c.json
 done
+# the reference arm and the multi-rank plumbing (4 ranks sharing the one GPU: not a scaling number)
+timeout 600 python bench.py --impl reference > gpurun_out/ev/bench_reference.json 2> gpurun_out/ev/bench_reference.err; tail -c 300 gpurun_out/ev/bench_reference.json
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 4 --config bert-base --steps 5 --warmup 3 > gpurun_out/ev/bench_bert-base_4ranks_shared.json 2> gpurun_out/ev/bench_4ranks.err; tail -c 300 gpurun_out/ev/bench_bert-base_4ranks_shared.json
