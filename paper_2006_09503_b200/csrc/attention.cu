@@ -35,11 +35,13 @@ size_t attention_bwd_scratch_floats(int batch, int seq, int heads, int head_dim)
 }
 
 void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
-                   float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s, int head_dim) {
+                   float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s, int head_dim,
+                   float* dq_alt, int phase, bool last) {
     check_shape(seq, heads, head_dim);
     const double flops = 8.0 * batch * heads * head_dim * seq * seq * (causal ? 0.5 : 1.0);
     prof::Scope scope("attention_bwd", flops, 2.0 * batch * seq * heads * head_dim * 8.0, 3, s);
-    attention_bwd_tc(qkv, o, dout, lse, dqkv, delta, scratch, batch, seq, heads, causal, s, head_dim);
+    attention_bwd_tc(qkv, o, dout, lse, dqkv, delta, scratch, batch, seq, heads, causal, s, head_dim, dq_alt, phase,
+                     last);
 }
 
 }  // namespace p2bw

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                   const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ nl2,
                   const float* __restrict__ delta, bf16* __restrict__ dqkv, float* __restrict__ dq_acc, int seq,
-                  int heads, int bhn) {
+                  int heads, int bhn, float4* __restrict__ zero_next, long long zero_n4) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -247,6 +247,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (have) issue_mm2(prev);
+        }
+    } else if (warp == 3) {
+        // idle role warp: zero the NEXT call's dQ accumulator (double-buffered per stage,
+        // attention_bwd_tc), which takes the zero-fill off the delta kernel on the stage
+        // stream's critical path; plain 512 B-per-instruction stores, drained at exit
+        if (zero_next != nullptr) {
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (long long i = static_cast<long long>(blockIdx.x) * 32 + lane; i < zero_n4;
+                 i += static_cast<long long>(gridDim.x) * 32)
+                zero_next[i] = z;
         }
     } else if (warp >= 4 && warp < 4 + kElemWarps) {
         // ---------------- elementwise: P^T, dS^T ----------------
@@ -450,7 +460,8 @@ template <bool kCausal>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_bwd_tc128(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                      const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ nl2,
-                     const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int heads, int bhn) {
+                     const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int heads, int bhn,
+                     float4* __restrict__ zero_next, long long zero_n4) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -566,6 +577,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (t == it.iters - 1) ptx::umma_commit(&bar[d128::bKvEmpty]);
                 }
             }
+        }
+    } else if (warp == 3) {
+        // idle role warp: zero the NEXT call's dQ accumulator (double-buffered per stage,
+        // attention_bwd_tc), which takes the zero-fill off the delta kernel on the stage
+        // stream's critical path; plain 512 B-per-instruction stores, drained at exit
+        if (zero_next != nullptr) {
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (long long i = static_cast<long long>(blockIdx.x) * 32 + lane; i < zero_n4;
+                 i += static_cast<long long>(gridDim.x) * 32)
+                zero_next[i] = z;
         }
     } else if (warp >= 4 && warp < 4 + kElemWarps) {
         // ---------------- elementwise: P^T, dS^T -> SMEM ----------------
@@ -742,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D>
 __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
                              float* __restrict__ delta, float* __restrict__ nl2, float* __restrict__ dq_acc, int tokens,
-                             int seq, int heads) {
+                             int seq, int heads, int zero) {
     constexpr int kD = D, kSub = D / 8;  // threads per (token, head), 8 elements each
     ptx::pdl_trigger();
     ptx::pdl_wait();
@@ -765,9 +786,11 @@ __global__ void k_attn_delta(const bf16* __restrict__ o, const bf16* __restrict_
 #pragma unroll
     for (int w = 1; w < kSub; w *= 2) acc += __shfl_xor_sync(0xffffffffu, acc, w);
     if (!ok) return;
-    float4* z = reinterpret_cast<float4*>(dq_acc + off);
-    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (zero) {  // else the previous call's backward kernel zeroed this accumulator
+        float4* z = reinterpret_cast<float4*>(dq_acc + off);
+        z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     if (sub == 0) {
         const int b = t / seq, i = t % seq;
         const size_t si = (static_cast<size_t>(b) * heads + hd) * seq + i;
@@ -820,19 +843,28 @@ size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads, int head_d
 }
 
 void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv, float* delta,
-                      float* dq_acc, int batch, int seq, int heads, bool causal, cudaStream_t s, int head_dim) {
+                      float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s, int head_dim,
+                      float* dq_alt, int phase, bool last) {
     const bool d128 = head_dim == 128;
     const int h = heads * head_dim;
     const int tokens = batch * seq;
     const int pairs = tokens * heads;
-    float* nl2 = dq_acc + static_cast<size_t>(tokens) * h;
+    float* nl2 = scratch + static_cast<size_t>(tokens) * h;
+    // dQ accumulator of this call: with dq_alt (the model's consecutive calls, phase = 0, 1,
+    // ...) the two buffers alternate; the delta kernel zeroes only the first call's, and
+    // each call's backward kernel zeroes the next call's (read by its dq convert already).
+    const bool dbuf = dq_alt != nullptr;
+    float* dq_acc = dbuf && (phase & 1) ? dq_alt : scratch;
+    float4* zero_next = dbuf && !last ? reinterpret_cast<float4*>((phase & 1) ? scratch : dq_alt) : nullptr;
+    const long long zero_n4 = static_cast<long long>(tokens) * h / 4;
+    const int zero_own = !dbuf || phase == 0;
     const int sub = head_dim / 8;
     if (d128)
         launch_pdl(k_attn_delta<128>, dim3((pairs * sub + 255) / 256), dim3(256), 0, s, "k_attn_delta", o, dout, lse,
-                   delta, nl2, dq_acc, tokens, seq, heads);
+                   delta, nl2, dq_acc, tokens, seq, heads, zero_own);
     else
         launch_pdl(k_attn_delta<64>, dim3((pairs * sub + 255) / 256), dim3(256), 0, s, "k_attn_delta", o, dout, lse,
-                   delta, nl2, dq_acc, tokens, seq, heads);
+                   delta, nl2, dq_acc, tokens, seq, heads, zero_own);
     const CUtensorMap tq = make_tmap_bf16_2d(qkv, 3ull * h, static_cast<uint64_t>(tokens), 3ll * h, 64, kT);
     const CUtensorMap tdo = make_tmap_bf16_2d(dout, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 64, kT);
     const CUtensorMap tdq = make_tmap_f32_2d(dq_acc, static_cast<uint64_t>(h), static_cast<uint64_t>(tokens), h, 32, 32);
@@ -845,20 +877,20 @@ void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const fl
         if (causal) {
             set_smem_once<0>(k_attn_bwd_tc128<true>, d128::kSmem);
             launch_pdl(k_attn_bwd_tc128<true>, dim3(grid), dim3(kThreads), d128::kSmem, s, "k_attn_bwd_tc", tq, tdo,
-                       tdq, cnl2, cdelta, dqkv, seq, heads, bhn);
+                       tdq, cnl2, cdelta, dqkv, seq, heads, bhn, zero_next, zero_n4);
         } else {
             set_smem_once<1>(k_attn_bwd_tc128<false>, d128::kSmem);
             launch_pdl(k_attn_bwd_tc128<false>, dim3(grid), dim3(kThreads), d128::kSmem, s, "k_attn_bwd_tc", tq, tdo,
-                       tdq, cnl2, cdelta, dqkv, seq, heads, bhn);
+                       tdq, cnl2, cdelta, dqkv, seq, heads, bhn, zero_next, zero_n4);
         }
     } else if (causal) {
         set_smem_once<2>(k_attn_bwd_tc<true>, kSmem);
         launch_pdl(k_attn_bwd_tc<true>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq, cnl2,
-                   cdelta, dqkv, dq_acc, seq, heads, bhn);
+                   cdelta, dqkv, dq_acc, seq, heads, bhn, zero_next, zero_n4);
     } else {
         set_smem_once<3>(k_attn_bwd_tc<false>, kSmem);
         launch_pdl(k_attn_bwd_tc<false>, dim3(grid), dim3(kThreads), kSmem, s, "k_attn_bwd_tc", tq, tdo, tdq, cnl2,
-                   cdelta, dqkv, dq_acc, seq, heads, bhn);
+                   cdelta, dqkv, dq_acc, seq, heads, bhn, zero_next, zero_n4);
     }
     const size_t vecs = static_cast<size_t>(tokens) * h / 8;
     const dim3 cgrid(static_cast<int>(std::min<size_t>((vecs + 255) / 256, 148u * 16u)));

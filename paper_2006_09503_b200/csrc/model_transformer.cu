@@ -41,6 +41,16 @@ int debug_dup(int bit) {
     }();
     return (mask & bit) ? 2 : 1;
 }
+
+// Two alternating attention dQ accumulators per stage (zero-fill inside the previous
+// layer's backward kernel instead of the delta kernel); P2BW_ATTN_DQ_DBUF=0 turns it off.
+bool dq_double_buffer() {
+    static const bool on = [] {
+        const char* e = std::getenv("P2BW_ATTN_DQ_DBUF");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+}
 }  // namespace
 
 namespace {
@@ -342,8 +352,12 @@ public:
             done(kEvDoneC);
             // attention
             wait_side(kEvDoneD, s);  // g3_ free (previous layer's Wqkv / bqkv gradients)
-            for (int dup_ = 0; dup_ < debug_dup(16); ++dup_) attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
-                          cfg_.causal != 0, s, hd_);
+            // the layers' calls alternate two dQ accumulators (each call's kernel zeroes the
+            // next one's, attention_bwd_tc); debug duplicates keep the single-buffer path
+            for (int dup_ = 0; dup_ < debug_dup(16); ++dup_)
+                attention_bwd(st.qkv[l], st.o[l], gX_, st.lse[l], g3_, delta_, attn_scratch_, b_, seq_, heads_,
+                              cfg_.causal != 0, s, hd_, debug_dup(16) > 1 ? nullptr : attn_dq_alt_,
+                              layers_ - 1 - l, l == 0);
             fork(kEvG3, s);
             // QKV: dxn1 = dqkv Wqkv
             gemm_store_mn_b(g3_, 3 * h_, W + o.wqkv, h_, T_, h_, 3 * h_, gX_, s);
@@ -521,6 +535,7 @@ private:
         g4_ = dalloc<bf16>(T * 4 * h);
         delta_ = dalloc<float>(stat);
         attn_scratch_ = dalloc<float>(attention_bwd_scratch_floats(b_, seq_, heads_, hd_));
+        if (dq_double_buffer()) attn_dq_alt_ = dalloc<float>(static_cast<size_t>(T_) * h_);
         if (last_) {
             row_loss_ = dalloc<float>(static_cast<size_t>(R_));
             head_ws_ = dalloc<float>(static_cast<size_t>(R_) * h);
@@ -636,6 +651,7 @@ private:
     bf16 *gA_ = nullptr, *gB_ = nullptr, *gX_ = nullptr, *g3_ = nullptr, *g4_ = nullptr, *gH_ = nullptr;
     float* delta_ = nullptr;
     float* attn_scratch_ = nullptr;
+    float* attn_dq_alt_ = nullptr;    // second dQ accumulator [T x h] (dq_double_buffer)
     float* red_scratch_ = nullptr;
     float* side_red_ = nullptr;       // colsum / wgrad-bias partials of the side stream
     int64_t side_red_floats_ = 0;

@@ -59,12 +59,15 @@ void attention_fwd_tc(const bf16* qkv, bf16* o, float* lse, int batch, int seq, 
 size_t attention_bwd_tc_scratch_floats(int batch, int seq, int heads, int head_dim);
 void attention_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv,
                       float* delta, float* dq_part, int batch, int seq, int heads, bool causal, cudaStream_t s,
-                      int head_dim);
+                      int head_dim, float* dq_alt = nullptr, int phase = 0, bool last = true);
 // dqkv [T x 3h] from do [T x h]; delta: [b*nh*seq] floats; scratch: attention_bwd_scratch_floats.
+// A run of consecutive calls on one stream (a stage's layers in one Backward) may pass a
+// second dQ accumulator dq_alt ([T x h] floats) with phase = 0, 1, ... and last on the
+// final call: the accumulators alternate and each call's kernel zeroes the next one's.
 size_t attention_bwd_scratch_floats(int batch, int seq, int heads, int head_dim = 64);
 void attention_bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, bf16* dqkv,
                    float* delta, float* scratch, int batch, int seq, int heads, bool causal, cudaStream_t s,
-                   int head_dim = 64);
+                   int head_dim = 64, float* dq_alt = nullptr, int phase = 0, bool last = true);
 
 // Momentum SGD with dampening (semantics.cpp:153-165) on the flat fp32 master:
 //   g = grad / count; v = beta v + (1-beta) g; w -= lr v; out_bf16 = bf16(w)

@@ -105,6 +105,7 @@ def test_bench_width_layers_match_delayed_oracle(depth, layers, batch, hidden, c
 
 @pytest.mark.parametrize("depth,layers,batch,hidden,heads,causal,vocab",
                          [(2, 2, 2, 256, 2, True, 500),
+                          (1, 3, 2, 256, 2, False, 500),      # odd layer count: dQ accumulators alternate
                           (1, 2, 1, 1920, 15, True, 51200)])  # GPT-2.2B at SURVEY a14's 15 x 128 heads
 def test_head_dim_128_matches_delayed_oracle(depth, layers, batch, hidden, heads, causal, vocab):
     """Heads of 128 columns through the whole engine (the D = 128 tcgen05 attention
