@@ -102,6 +102,11 @@ struct KParams {
     // Grouped raster: tiles walk N inside groups of `group_m` M tiles (0: M-fastest over
     // the whole output), so the operand L2 can hold is the one re-read.
     int group_m;
+    // Ragged last N tile with <= BN / 2 valid columns (e.g. N = 1920 on 256-wide tiles):
+    // issue its MMAs at N = BN / 2 (pair: BN / 4 columns of B per CTA) instead of spending
+    // half the tensor work on zero-filled columns.  The accumulator's upper half then
+    // holds stale values, which only ever reach columns >= n (clipped by the TMA stores).
+    int half_n;
 };
 
 // Output tile (M-group index, N-group index) of tile number t.
@@ -228,6 +233,8 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
     const int w0 = blockIdx.x / kCl, wstep = gridDim.x / kCl;
     const uint16_t pair_mask = static_cast<uint16_t>(kPair ? (0x3 << (2 * pair)) : 0x1);  // my pair's CTAs
     constexpr uint16_t kAllMask = kCl == 4 ? 0xF : (kCl == 2 ? 0x3 : 0x1);
+    // half-width last tile: MN-major B halves must stay whole 64-column atoms
+    constexpr bool kHalfOk = kCl <= 2 && (!kBMN || (BN / (kPair ? 4 : 2)) % 64 == 0);
     if (threadIdx.x == 0) gmark(0);
 
     if (warp == 0 && lane == 0) {
@@ -305,7 +312,8 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
                         } else {
                             ptx::tma_load_2d_2sm(da, &tmap_a, &full_bar[stage], k0, m0);
                         }
-                        const int nb = n0 + rank * (BN / 2);  // my half of the B tile
+                        const bool half = kHalfOk && p.half_n && p.n - n0 <= BN / 2;
+                        const int nb = n0 + rank * (half ? BN / 4 : BN / 2);  // my half of the B tile
                         if constexpr (kBMN) {
 #pragma unroll
                             for (int j = 0; j < BN / 128; ++j)
@@ -341,7 +349,8 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
         }
     } else if (warp == 1) {
         if (lane == 0 && prank == 0) {  // pair mode: the even CTA issues for both
-            constexpr uint32_t idesc = ptx::idesc_bf16(kBM * (kPair ? 2 : 1), BN, kAMN, kBMN);
+            constexpr uint32_t idesc_full = ptx::idesc_bf16(kBM * (kPair ? 2 : 1), BN, kAMN, kBMN);
+            constexpr uint32_t idesc_half = ptx::idesc_bf16(kBM * (kPair ? 2 : 1), BN / 2, kAMN, kBMN);
             // K-major SW128: rows of 128 B, 8-row groups 1024 B apart; a K step of 16
             // elements is +32 B inside the swizzle atom.  MN-major SW128: 64-element MN
             // groups one TMA box (kBK rows x 128 B) apart, 8-row K groups 1024 B apart;
@@ -357,6 +366,8 @@ __global__ void __launch_bounds__(gemm_threads(kEW), 1)
             for (int w = w0; w < num_work; w += wstep) {
                 const Unit u = unit_of(w, num_tiles, kblocks, kb_per, p);
                 const int kb0 = u.kb0, kb1 = u.kb1;
+                const int n0 = tile_mn(u.tile, tiles_mg, tiles_ng, p.group_m).y * kNP * BN;
+                const uint32_t idesc = kHalfOk && p.half_n && p.n - n0 <= BN / 2 ? idesc_half : idesc_full;
                 ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -946,6 +957,15 @@ bool tail_enabled() {
     return on;
 }
 
+// Half-width ragged last N tile (KParams::half_n); P2BW_GEMM_HALF_N=0 turns it off.
+bool half_n_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("P2BW_GEMM_HALF_N");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // Upper bound on split-K slices of the fp32 (weight-gradient) GEMMs; P2BW_GEMM_MAX_SPLIT
 // overrides it (diagnostic A/B knob).
 int max_split_cap() {
@@ -1169,7 +1189,7 @@ void gemm_bf16(const GemmOperand& a, const GemmOperand& b, int m, int n, int k,
         const double a_bytes = 2.0 * m * k, b_bytes = 2.0 * n * k, resident = 48e6;
         if (a_bytes > resident) group_m = b_bytes <= resident ? 1 : 8;
     }
-    KParams p{m, n, k, splits, epi, rsum, tail_tiles, tail_f, tp.ws, tp.flags, group_m};
+    KParams p{m, n, k, splits, epi, rsum, tail_tiles, tail_f, tp.ws, tp.flags, group_m, half_n_enabled() ? 1 : 0};
     const double out_bytes = epi.kind == EpiKind::StoreF32 ? (epi.beta != 0.0f ? 8.0 : 4.0) : 2.0;
     // profiler class by pass: forward (K-major x K-major), dgrad (B MN-major), wgrad (both MN-major)
     const char* cls = amn ? "gemm_wgrad" : (bmn ? "gemm_dgrad" : "gemm_fwd");

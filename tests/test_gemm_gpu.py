@@ -115,15 +115,17 @@ def test_gemm_wgrad_split_k(m, n, k, beta):
 
 @pytest.mark.parametrize("tile", ["128,1", "128,2", "192,1", "192,2", "256,1", "256,2", "128,4", "192,4", "256,4"])
 @pytest.mark.parametrize("am,bm,kind", [(0, 0, 0), (0, 1, 0), (1, 1, 1), (0, 1, 2)])
-def test_gemm_every_tile(monkeypatch, tile, am, bm, kind):
+@pytest.mark.parametrize("n", [768, 640, 608])  # 640 / 608: a last N tile of <= BN / 2 columns
+def test_gemm_every_tile(monkeypatch, tile, am, bm, kind, n):
     """Every (BN, cluster) tile the shape-based chooser may pick, on a ragged shape,
     for the forward (bf16 + bias), dgrad (bf16 / dGELU) and wgrad (fp32) layouts.
     Pair tiles whose B half is not whole 64-column atoms fall back to one CTA.  The
     4-CTA clusters (two pairs sharing A through TMA multicast) leave the second pair
-    of the last N group past N when the tile count along N is odd."""
+    of the last N group past N when the tile count along N is odd.  A last N tile with
+    at most BN / 2 valid columns runs its MMAs at N = BN / 2 (KParams::half_n)."""
     monkeypatch.setenv("P2BW_GEMM_TILE", tile)
-    m, n, k = 1000, 768, 704
-    gen = torch.Generator(device="cuda").manual_seed(17 + am + 2 * bm + 4 * kind)
+    m, k = 1000, 704
+    gen = torch.Generator(device="cuda").manual_seed(17 + am + 2 * bm + 4 * kind + n)
     A, a, lda = _operand(m, k, am, gen)
     B, b, ldb = _operand(n, k, bm, gen)
     ref = A.float() @ B.float().t()
