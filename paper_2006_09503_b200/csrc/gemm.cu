@@ -836,6 +836,8 @@ CUtensorMap make_map(const bf16* ptr, uint64_t inner, uint64_t outer, int64_t ld
     return make_map_t(ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, inner, outer, ld_elems, 64, box_outer);
 }
 
+int wgrad_sms();
+
 template <int BN, bool kAMN, bool kBMN, EpiKind kKind, int kCl, int kEW>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const KParams& p, cudaStream_t s) {
     using Cfg = GemmCfg<BN, kCl, kEW>;
@@ -854,7 +856,9 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, con
     const int tiles_ng = kCl == 4 ? (tiles_n + 1) / 2 : tiles_n;
     const int work = p.tail_tiles > 0 ? tiles_mg * tiles_ng + p.tail_tiles * (p.tail_f - 1)
                                       : tiles_mg * tiles_ng * p.splits;
-    const int slots = num_sms() / kCl;
+    // fp32 (weight-gradient) GEMMs may be held to fewer SMs (P2BW_GEMM_WGRAD_SMS, diagnostic:
+    // the side stream's share of the GPU while the stage stream's chain runs beside it)
+    const int slots = (kKind == EpiKind::StoreF32 && p.splits == 1 ? wgrad_sms() : num_sms()) / kCl;
     const int grid = kCl * (work < slots ? work : slots);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -957,6 +961,14 @@ bool tail_enabled() {
     return on;
 }
 
+int wgrad_sms() {
+    static const int n = [] {
+        const char* e = std::getenv("P2BW_GEMM_WGRAD_SMS");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 2 && v < num_sms() ? v : num_sms();
+    }();
+    return n;
+}
 // Half-width ragged last N tile (KParams::half_n); P2BW_GEMM_HALF_N=0 turns it off.
 bool half_n_enabled() {
     static const bool on = [] {
