@@ -777,7 +777,7 @@ __device__ __forceinline__ float2 unpack_bf16x2_opaque(uint32_t w) {
 }
 
 template <int NVT>
-__global__ void __launch_bounds__(256) k_softmax_xent_reg(bf16* __restrict__ logits, const int* __restrict__ targets,
+__global__ void __launch_bounds__(256, NVT <= 25 ? 2 : 1) k_softmax_xent_reg(bf16* __restrict__ logits, const int* __restrict__ targets,
                                                           int vocab, int vp, float grad_scale,
                                                           float* __restrict__ row_loss) {
     __shared__ float red[8];
@@ -1148,12 +1148,24 @@ void colsum_bf16(const bf16* x, int rows, int n, int ld, float* out, bool overwr
     check_cuda(cudaGetLastError(), "colsum");
 }
 
+bool xent_two_per_sm() {  // P2BW_XENT_2CTA=0: the one-CTA-per-SM <32> instantiation (A/B knob)
+    static const bool on = [] {
+        const char* e = std::getenv("P2BW_XENT_2CTA");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 void softmax_xent(bf16* logits, const int* targets, int rows, int vocab, int vp, float grad_scale,
                   float* row_loss, cudaStream_t s) {
     if (vp % 8 != 0) throw Error("softmax_xent: padded vocab must be a multiple of 8");
     prof::Scope scope("softmax_xent", 0.0, 4.0 * rows * static_cast<double>(vp) + 8.0 * rows, 1, s);
     const int nvt = (vp / 8 + 255) / 256;  // 16-byte vectors per thread for a register-resident row
     if (nvt <= 16) k_softmax_xent_reg<16><<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
+    // <= 25 vectors per thread (V <= 51200): <= 128 registers, so two rows share an SM and
+    // one row's exponentials overlap the other's loads (one CTA per SM left the memory pipe
+    // idle during the exp passes: 548 us per 8192-row GPT-2.2B head at 3.1 TB/s)
+    else if (nvt <= 25 && xent_two_per_sm()) k_softmax_xent_reg<25><<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
     else if (nvt <= 32) k_softmax_xent_reg<32><<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
     else k_softmax_xent<<<rows, 256, 0, s>>>(logits, targets, vocab, vp, grad_scale, row_loss);
     check_cuda(cudaGetLastError(), "softmax_xent");
